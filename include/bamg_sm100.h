@@ -1,0 +1,227 @@
+/*
+ * bamg_sm100.h -- C ABI of libbamg_sm100.so, the B200 (sm_100a) engine behind
+ * the BAMG setup + AMG-preconditioned GMRES path of arxiv/paper_1402_4005.
+ *
+ * The reference (`markovmg`, pure Python) has no FFI of its own: its
+ * "operator API" is a set of module-level Python functions.  Every entry point
+ * below replaces the arithmetic of one of those functions (cited per
+ * declaration as reference file:line, relative to
+ * /root/reference/pkg/src/markovmg/).  The Python package
+ * `paper_1402_4005_b200` binds these through ctypes (INTEGRATION.md shows the
+ * stub) and re-exports the reference's names and signatures.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the name ends in `_host`.
+ *     Buffers passed in are caller-owned; library workspaces and hierarchy /
+ *     basis storage are owned by the handle and released by *_destroy.
+ *   - Values are fp64, CSR indices int32 (every nnz in scope is < 2^31),
+ *     vector blocks of k test vectors are n x k row-major ("interleaved":
+ *     the k values of one state are contiguous).
+ *   - Calls are stream-ordered on the stream given to bamg_ctx_create and are
+ *     not re-entrant per context.  One context per (device, stream).
+ *   - Return codes: 0 ok; < 0 CUDA / argument error (text via
+ *     bamg_last_error); > 0 numerical status (1 = not converged,
+ *     2 = singular pivot / not positive definite).
+ *   - Kernels tagged BIT-EXACT reproduce the reference's scipy arithmetic bit
+ *     for bit (sequential ascending-column sums, no FMA contraction).
+ */
+#ifndef BAMG_SM100_H
+#define BAMG_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bamg_ctx bamg_ctx;
+typedef struct bamg_hier bamg_hier;
+
+/* A CSR matrix in device memory (canonical form: sorted, no duplicates). */
+typedef struct bamg_csr {
+  int32_t nrows;
+  int32_t ncols;
+  int64_t nnz;
+  const int32_t* rowptr; /* nrows + 1 */
+  const int32_t* col;    /* nnz */
+  const double* val;     /* nnz */
+} bamg_csr;
+
+/* ---------------------------------------------------------------- context */
+int bamg_ctx_create(int device, void* cuda_stream, bamg_ctx** out);
+int bamg_ctx_destroy(bamg_ctx* ctx);
+const char* bamg_last_error(bamg_ctx* ctx);
+int bamg_version(void);
+/* Number of kernels this context has launched (evidence for bench.py). */
+int64_t bamg_launch_count(bamg_ctx* ctx);
+int bamg_sync(bamg_ctx* ctx);
+
+/* ------------------------------------------------------- sparse (sparse.py) */
+/* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;
+ * with A = explicit transpose it replaces spmv_transpose, sparse.py:89-94. */
+int bamg_spmv(bamg_ctx* ctx, const bamg_csr* A, const double* x, double* y);
+/* Y = A X for k interleaved vectors (n x k).  BIT-EXACT per column vs
+ * csr_matvecs (interp.py:95, bootstrap.py:384-385). */
+int bamg_spmm(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k);
+/* Explicit transpose with sorted columns: out arrays sized ncols+1 / nnz.
+ * Replaces transpose, sparse.py:97-99. */
+int bamg_csr_transpose(bamg_ctx* ctx, const bamg_csr* A, int32_t* rowptr_t,
+                       int32_t* col_t, double* val_t);
+/* Pattern of A + A^T without the diagonal (unit weights implicit).
+ * Two calls: rowptr (n+1) first, then columns.  A_t is the explicit
+ * transpose of A.  Replaces adjacency_structure, sparse.py:120-128. */
+int bamg_sym_pattern_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                           int32_t* rowptr_s, int64_t* nnz_host);
+int bamg_sym_pattern_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                          const int32_t* rowptr_s, int32_t* col_s);
+/* d_i = A_ii (0 when not stored).  B.diagonal(). */
+int bamg_diag(bamg_ctx* ctx, const bamg_csr* A, double* d);
+/* Count of d_i <= 0 (bootstrap.py:332-334, _operator_degenerate). */
+int bamg_count_nonpositive(bamg_ctx* ctx, const double* d, int64_t n, int64_t* count_host);
+
+/* Two-pass SpGEMM C = A B with scipy csr_matmat semantics: sums accumulated in
+ * A-row order then B-row order, exact-zero results dropped.  `order`:
+ *   0 = canonical (sorted columns, |v| < 1e-300 also dropped: make_csr),
+ *   1 = scipy storage order (reverse first touch), exact zeros dropped only.
+ * Count pass fills rowptr_c (nrows+1) and returns nnz; fill pass writes.
+ * Replaces triple_product, sparse.py:102-117 and bootstrap.py:372-373. */
+int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                      int32_t* rowptr_c, int64_t* nnz_host);
+int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                     const int32_t* rowptr_c, int32_t* col_c, double* val_c);
+
+/* ------------------------------------------------------ relax (relax.py) */
+/* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit
+ * transpose for the column variant.  Replaces degenerate_rows, relax.py:47-63. */
+int bamg_degenerate_rows(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip);
+/* One weighted-Jacobi sweep on k interleaved vectors, BIT-EXACT vs
+ * _apply_sweep (relax.py:66-83):  x' = x + (omega (b - A x)) / d on unskipped
+ * rows.  b may be NULL (homogeneous).  When b_scale is non-NULL the
+ * right-hand side is b_scale[c] * b (the sigma * M u of bootstrap.py:296).
+ * peak (k doubles, may be NULL) receives max |x'| per vector. */
+int bamg_jacobi(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip,
+                const double* b, const double* b_scale, const double* x, double* x_out,
+                int k, double omega, double* peak);
+
+/* --------------------------------------------------- dense block reductions */
+/* out[c] = ||X[:, c]||_2 for n x k interleaved X (deterministic tree). */
+int bamg_col_norms(bamg_ctx* ctx, const double* X, int64_t n, int k, double* out);
+/* out[c] = sum_i X[i,c] * Y[i,c]. */
+int bamg_col_dots(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
+                  double* out);
+/* X[:, c] /= s[c] where s[c] != 0 (zero norms left as 1: bootstrap.py:160-163). */
+int bamg_col_scale_div(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s);
+/* X[i, c] = value for all i (pinning the constant left vector). */
+int bamg_col_fill(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);
+/* Y[i, :] = X[idx[i], :] (triplet injection, bootstrap.py:375-377). */
+int bamg_gather_rows(bamg_ctx* ctx, const double* X, const int32_t* idx, int64_t m, int k,
+                     double* Y);
+
+/* -------------------------------------------------- bootstrap (bootstrap.py) */
+/* One _smooth_block (bootstrap.py:284-314) on device: nsweeps coupled sweeps
+ * of the k right vectors V (with A) and the k left vectors U (with A^T),
+ * optional inhomogeneous rhs sigma*M u / sigma*N v with per-sweep Rayleigh
+ * updates, runaway rescaling, row normalisation, the pinned constant left
+ * slot and the sigma refresh (bootstrap.py:166-177).  M / N NULL = identity.
+ * U, V are updated in place; sigma (k doubles, device) in place. */
+int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                      const bamg_csr* M, const bamg_csr* N, const double* d,
+                      const uint8_t* skip, const uint8_t* skip_t, double* U, double* V,
+                      double* sigma, int k, int nsweeps, double omega, int inhomogeneous,
+                      int smooth, int refresh);
+/* Rayleigh refresh only (bootstrap.py:166-177). */
+int bamg_refresh_sigmas(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M,
+                        const bamg_csr* N, const double* U, const double* V, double* U_flip,
+                        double* sigma, int k);
+
+/* ------------------------------------------------------ interp (interp.py) */
+/* Normalised test vectors and weights 1/||A v||^2 with the caps of
+ * singular_test_weights (interp.py:82-102).  Pass A^T for the left side.
+ * inf_slot < 0 for none.  Xn (n x k) receives the unit vectors. */
+int bamg_test_weights(bamg_ctx* ctx, const bamg_csr* A, const double* X, int64_t n, int k,
+                      int inf_slot, double* Xn, double* w);
+/* Greedy caliber-bounded weighted ridge LS per fine point, one warp per point
+ * (interp.py:129-289).  adj: pattern(A+A^T) without diagonal; coarse_rank[i]
+ * >= 0 marks a C point.  Writes, per state i, up to `caliber` (column, value)
+ * pairs into out_col/out_val (n x caliber) and out_cnt[i] (C points: their
+ * identity entry; no-candidate F points: 0).  status_host[0] counts fits that
+ * needed the rank-deficient pseudo-inverse branch. */
+int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
+                  const double* X, const double* w, int64_t n, int k, int caliber,
+                  int radius, double improvement_tol, int constrain, int nonnegative,
+                  int32_t* out_cnt, int32_t* out_col, double* out_val, int64_t* status_host);
+/* Compact the fixed-stride rows into canonical CSR (sorted columns, |v| <
+ * 1e-300 dropped: csr_from_coo, sparse.py:42-46).  Two calls. */
+int bamg_rows_count(bamg_ctx* ctx, const int32_t* cnt, const double* val, int64_t n,
+                    int stride, int32_t* rowptr, int64_t* nnz_host);
+int bamg_rows_fill(bamg_ctx* ctx, const int32_t* cnt, const int32_t* col, const double* val,
+                   int64_t n, int stride, const int32_t* rowptr, int32_t* col_out,
+                   double* val_out);
+
+/* ---------------------------------------------------- coarsen (coarsen.py) */
+/* Rank of every coordinate among the distinct values of its axis
+ * (np.unique(..., return_inverse=True), coarsen.py:84-87). */
+int bamg_axis_ranks(bamg_ctx* ctx, const double* coord, int64_t n, int32_t* rank);
+/* Ranks on the coarse level from the parent ranks of the kept points. */
+int bamg_rerank(bamg_ctx* ctx, const int32_t* parent_rank, const int32_t* coarse_idx,
+                int64_t nc, int64_t nvalues_parent, int32_t* rank_out);
+/* mask from per-axis ranks: every rank even (geometric_coarsen, coarsen.py:90-109). */
+int bamg_even_mask(bamg_ctx* ctx, const int32_t* const* ranks_host, int ndim, int64_t n,
+                   uint8_t* mask);
+/* coarse list / fine list / coarse_rank from a mask (CfSplitting, coarsen.py:23-52). */
+int bamg_split_from_mask(bamg_ctx* ctx, const uint8_t* mask, int64_t n, int32_t* coarse,
+                         int32_t* fine, int32_t* coarse_rank, int64_t* nc_host);
+/* One compatible-relaxation pass (coarsen.py:129-166): x_F from the host draw,
+ * unit-RMS scaling, `sweeps` F-relaxation sweeps, mu, and the greedy MIS in
+ * (-mu, index) order computed as a parallel lexicographically-first MIS.
+ * `normals` holds the n_fine draws in ascending fine-index order.  Sets new
+ * coarse points in cmask; returns the number of candidates in *ncand_host
+ * and, when the pass found none on an empty coarse set, the fallback index. */
+int bamg_cr_pass(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* adj, const double* d,
+                 uint8_t* cmask, const double* normals, int64_t n_fine, int sweeps,
+                 double omega, double threshold, int64_t* ncand_host);
+
+/* ------------------------------------------------------------ dense (dense.py) */
+/* Scatter a CSR into a dense column-major n x n matrix. */
+int bamg_csr_to_dense(bamg_ctx* ctx, const bamg_csr* A, double* D, int ld, int transpose);
+/* Explicit pseudo-inverse Z = A^+ (column-major n x n) by one-sided Jacobi SVD
+ * with rank_tol * sigma_max (PinvOperator, dense.py:118-131). */
+int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* Z);
+/* Coarsest generalized singular triplets (coarsest_triplets, bootstrap.py:205-281):
+ * M = L_M L_M^T, N = L_N L_N^T, SVD of L_M^-1 B L_N^-T, r smallest triplets,
+ * halves normalised, sign so u^T B v >= 0, null-slot cleanup.  Inputs dense
+ * column-major; outputs U, V as n x r interleaved and sigma (r). */
+int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const double* Md,
+                           const double* Nd, int n, int r, double* U, double* V,
+                           double* sigma);
+
+/* ----------------------------------------------------------- solver (solver.py) */
+/* Hierarchy for the V-cycle (VCycleOperator, solver.py:79-124).  Level
+ * matrices are borrowed (caller keeps them alive); the library owns the
+ * per-level work vectors.  The coarsest level is applied as Z b with the
+ * explicit pseudo-inverse Z (n_L x n_L, column-major, borrowed). */
+int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out);
+int bamg_hier_destroy(bamg_hier* h);
+int bamg_hier_set_level(bamg_hier* h, int level, const bamg_csr* B, const double* d,
+                        const uint8_t* skip, const bamg_csr* P, const bamg_csr* Q);
+int bamg_hier_set_coarsest(bamg_hier* h, const double* Z, int n);
+int bamg_hier_set_smoother(bamg_hier* h, double omega, int nu_pre, int nu_post);
+/* x = C b, one V-cycle from a zero guess. */
+int bamg_vcycle(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x);
+/* Left-preconditioned GMRES (solver.py:136-226): Arnoldi with two-pass
+ * classical Gram-Schmidt (CGS2) as fused multi-vector reductions, Givens
+ * rotations on device, per-iteration true residual ||Bx||/||x||.
+ * h may be NULL (unpreconditioned).  restart <= 0 = unrestarted.
+ * history_host receives max_iters + 1 doubles; returns 0 converged, 1 not. */
+int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* b,
+               const double* x0, double* x, int restart, int max_iters, double rtol,
+               int* iters_host, double* history_host, int* nhistory_host);
+/* x0 finalisation (bootstrap.py:420-428 and solver.py:229-235): non-finite or
+ * all-zero -> uniform 1/n, sign so the max-|.| entry is positive, l1 = 1. */
+int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int stride, double* out,
+                     int uniform_fallback);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAMG_SM100_H */

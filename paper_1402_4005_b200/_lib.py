@@ -1,0 +1,168 @@
+"""ctypes binding of libbamg_sm100.so (the C ABI declared in include/bamg_sm100.h).
+
+There is deliberately no fallback: if the library is missing, or no CUDA
+device is visible, every entry point raises `BamgUnavailable`.  The product
+path never computes on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libbamg_sm100.so"
+
+
+class BamgUnavailable(RuntimeError):
+    """The sm_100a engine cannot run here (library not built or no GPU)."""
+
+
+class BamgError(RuntimeError):
+    """A CUDA or argument error reported by the engine."""
+
+
+class CSR(C.Structure):
+    _fields_ = [("nrows", C.c_int32), ("ncols", C.c_int32), ("nnz", C.c_int64),
+                ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
+P = C.c_void_p
+PCSR = C.POINTER(CSR)
+I32, I64, F64 = C.c_int32, C.c_int64, C.c_double
+PI64 = C.POINTER(C.c_int64)
+PINT = C.POINTER(C.c_int)
+PF64 = C.POINTER(C.c_double)
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+_SIGS = {
+    "bamg_ctx_create": [C.c_int, P, C.POINTER(P)],
+    "bamg_ctx_destroy": [P],
+    "bamg_last_error": [P],
+    "bamg_version": [],
+    "bamg_launch_count": [P],
+    "bamg_sync": [P],
+    "bamg_spmv": [P, PCSR, P, P],
+    "bamg_spmm": [P, PCSR, P, P, C.c_int],
+    "bamg_csr_transpose": [P, PCSR, P, P, P],
+    "bamg_sym_pattern_count": [P, PCSR, PCSR, P, PI64],
+    "bamg_sym_pattern_fill": [P, PCSR, PCSR, P, P],
+    "bamg_diag": [P, PCSR, P],
+    "bamg_count_nonpositive": [P, P, I64, PI64],
+    "bamg_spgemm_count": [P, PCSR, PCSR, C.c_int, P, PI64],
+    "bamg_spgemm_fill": [P, PCSR, PCSR, C.c_int, P, P, P],
+    "bamg_degenerate_rows": [P, PCSR, P, P],
+    "bamg_jacobi": [P, PCSR, P, P, P, P, P, P, C.c_int, F64, P],
+    "bamg_col_norms": [P, P, I64, C.c_int, P],
+    "bamg_col_dots": [P, P, P, I64, C.c_int, P],
+    "bamg_col_scale_div": [P, P, I64, C.c_int, P],
+    "bamg_col_fill": [P, P, I64, C.c_int, C.c_int, F64],
+    "bamg_gather_rows": [P, P, P, I64, C.c_int, P],
+    "bamg_smooth_block": [P, PCSR, PCSR, PCSR, PCSR, P, P, P, P, P, P, C.c_int, C.c_int, F64,
+                          C.c_int, C.c_int, C.c_int],
+    "bamg_refresh_sigmas": [P, PCSR, PCSR, PCSR, P, P, P, P, C.c_int],
+    "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
+    "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
+                      P, P, P, PI64],
+    "bamg_rows_count": [P, P, P, I64, C.c_int, P, PI64],
+    "bamg_rows_fill": [P, P, P, P, I64, C.c_int, P, P, P],
+    "bamg_axis_ranks": [P, P, I64, P],
+    "bamg_rerank": [P, P, P, I64, I64, P],
+    "bamg_even_mask": [P, C.POINTER(P), C.c_int, I64, P],
+    "bamg_split_from_mask": [P, P, I64, P, P, P, PI64],
+    "bamg_cr_pass": [P, PCSR, PCSR, P, P, P, I64, C.c_int, F64, F64, PI64],
+    "bamg_csr_to_dense": [P, PCSR, P, C.c_int, C.c_int],
+    "bamg_dense_pinv": [P, P, C.c_int, F64, P],
+    "bamg_coarsest_triplets": [P, P, P, P, C.c_int, C.c_int, P, P, P],
+    "bamg_hier_create": [P, C.c_int, C.POINTER(P)],
+    "bamg_hier_destroy": [P],
+    "bamg_hier_set_level": [P, C.c_int, PCSR, P, P, PCSR, PCSR],
+    "bamg_hier_set_coarsest": [P, P, C.c_int],
+    "bamg_hier_set_smoother": [P, F64, C.c_int, C.c_int],
+    "bamg_vcycle": [P, P, P, P],
+    "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, PINT, PF64, PINT],
+    "bamg_sign_fix_l1": [P, P, I64, C.c_int, P, C.c_int],
+}
+_RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64}
+
+_lock = threading.Lock()
+_lib = None
+_ctx = {}
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def load_library(require_gpu: bool = False):
+    """dlopen the engine.  `require_gpu` additionally demands a CUDA device."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise BamgUnavailable(
+                    f"{LIB_PATH} is not built; run `python -m paper_1402_4005_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+            missing = []
+            for name, args in _SIGS.items():
+                try:
+                    fn = getattr(lib, name)
+                except AttributeError:
+                    missing.append(name)
+                    continue
+                fn.argtypes = args
+                fn.restype = _RESTYPES.get(name, C.c_int)
+            lib.missing_symbols = missing
+            _lib = lib
+    if require_gpu and not torch.cuda.is_available():
+        raise BamgUnavailable("no CUDA device visible: the sm_100a engine has no CPU fallback")
+    return _lib
+
+
+def lib():
+    return load_library(require_gpu=True)
+
+
+def ctx(device: int | None = None):
+    """Per-device engine context bound to torch's current stream at first use."""
+    L = lib()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    key = dev
+    if key not in _ctx:
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            out = P()
+            rc = L.bamg_ctx_create(dev, P(stream), C.byref(out))
+            if rc != 0:
+                raise BamgError(f"bamg_ctx_create failed ({rc})")
+            _ctx[key] = out
+    return _ctx[key]
+
+
+def check(rc: int, what: str, c=None):
+    """Raise on negative codes; return the (non-negative) status otherwise."""
+    if rc < 0:
+        msg = lib().bamg_last_error(c if c is not None else ctx())
+        raise BamgError(f"{what}: {msg.decode() if msg else rc}")
+    return rc
+
+
+def call(name: str, *args):
+    c = ctx()
+    rc = getattr(lib(), name)(c, *args)
+    return check(rc, name, c)
+
+
+def launches() -> int:
+    return int(lib().bamg_launch_count(ctx()))
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return P(t.data_ptr())

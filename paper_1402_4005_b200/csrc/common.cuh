@@ -1,0 +1,155 @@
+// common.cuh -- shared plumbing for libbamg_sm100.so (context, arena, launch
+// accounting, deterministic block reductions, device scan).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/bamg_sm100.h"
+
+#define BAMG_VERSION 1
+
+struct Arena {
+  struct Chunk {
+    char* ptr;
+    size_t size;
+    size_t used;
+  };
+  std::vector<Chunk> chunks;
+  // Reset is only legal at API entry: every previous user has been enqueued on
+  // the same stream, so reuse is stream-ordered.
+  void reset() {
+    for (auto& c : chunks) c.used = 0;
+  }
+  cudaError_t get(size_t bytes, void** out) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    for (auto& c : chunks) {
+      if (c.size - c.used >= bytes) {
+        *out = c.ptr + c.used;
+        c.used += bytes;
+        return cudaSuccess;
+      }
+    }
+    size_t sz = bytes > (size_t(64) << 20) ? bytes : (size_t(64) << 20);
+    char* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) return e;
+    chunks.push_back({p, sz, bytes});
+    *out = p;
+    return cudaSuccess;
+  }
+  void release() {
+    for (auto& c : chunks) cudaFree(c.ptr);
+    chunks.clear();
+  }
+};
+
+struct bamg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  std::string err;
+  Arena arena;
+  double* pinned = nullptr;  // small pinned host staging buffer
+  size_t pinned_doubles = 0;
+};
+
+// ---------------------------------------------------------------- error glue
+#define BAMG_CHECK_CUDA(ctx, expr)                                              \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e) +         \
+                   " at " + __FILE__ + ":" + std::to_string(__LINE__);          \
+      return -1;                                                                \
+    }                                                                           \
+  } while (0)
+
+#define BAMG_REQUIRE(ctx, cond, msg)                                            \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      (ctx)->err = std::string("argument error: ") + (msg);                     \
+      return -2;                                                                \
+    }                                                                           \
+  } while (0)
+
+// Launch + accounting + immediate launch-error check.
+#define BAMG_LAUNCH(ctx, kernel, grid, block, smem, ...)                        \
+  do {                                                                          \
+    if ((grid) > 0) {                                                           \
+      kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);          \
+      (ctx)->launches++;                                                        \
+      BAMG_CHECK_CUDA(ctx, cudaGetLastError());                                 \
+    }                                                                           \
+  } while (0)
+
+#define BAMG_TRY(expr)                                                          \
+  do {                                                                          \
+    int _rc = (expr);                                                           \
+    if (_rc != 0) return _rc;                                                   \
+  } while (0)
+
+template <typename T>
+static inline int arena_get(bamg_ctx* ctx, size_t count, T** out) {
+  void* p = nullptr;
+  cudaError_t e = ctx->arena.get(count * sizeof(T), &p);
+  if (e != cudaSuccess) {
+    ctx->err = std::string("workspace allocation failed: ") + cudaGetErrorString(e);
+    return -1;
+  }
+  *out = static_cast<T*>(p);
+  return 0;
+}
+
+// Pinned staging for small device->host reads (synchronises the stream).
+int ctx_read_doubles(bamg_ctx* ctx, const double* dev, size_t n, double* host);
+int ctx_read_i64(bamg_ctx* ctx, const int64_t* dev, size_t n, int64_t* host);
+int ctx_read_i32(bamg_ctx* ctx, const int32_t* dev, size_t n, int32_t* host);
+
+static inline int grid_for(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// ------------------------------------------------------- device-wide scans
+// out[0..n] exclusive prefix sums of in[0..n-1] (out[n] = total).  Optional
+// total read back to the host.
+int scan_i32(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_host);
+// Same for uint8 flags -> int32 offsets.
+int scan_u8(bamg_ctx* ctx, const uint8_t* in, int32_t* out, int64_t n, int64_t* total_host);
+
+// --------------------------------------------------- block reduce helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// max of non-negative doubles through their bit patterns (order-preserving,
+// NaN propagates as the largest pattern).
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            (unsigned long long)__double_as_longlong(v));
+}
+
+// Deterministic column reductions over n x k interleaved blocks: a fixed grid
+// of partial sums (rows chunked contiguously), then a fixed tree.
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs; constant => bit-reproducible
+constexpr int RED_THREADS = 256;
+
+// compute partial[b * k + c] for op(x, y) summed over the rows of block b.
+// kinds: 0 = x*x, 1 = x*y
+int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k, int kind,
+              double* out_dev /* k */, int take_sqrt);

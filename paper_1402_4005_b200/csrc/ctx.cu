@@ -1,0 +1,296 @@
+// ctx.cu -- context lifetime, pinned staging, device scans and deterministic
+// column reductions shared by every other translation unit.
+#include "common.cuh"
+
+extern "C" int bamg_version(void) { return BAMG_VERSION; }
+
+extern "C" int bamg_ctx_create(int device, void* cuda_stream, bamg_ctx** out) {
+  if (!out) return -2;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return -1;
+  bamg_ctx* ctx = new bamg_ctx();
+  ctx->device = device;
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
+  ctx->pinned_doubles = 1 << 16;
+  if (cudaMallocHost(&ctx->pinned, ctx->pinned_doubles * sizeof(double)) != cudaSuccess) {
+    delete ctx;
+    return -1;
+  }
+  *out = ctx;
+  return 0;
+}
+
+extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaStreamSynchronize(ctx->stream);
+  ctx->arena.release();
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  return 0;
+}
+
+extern "C" const char* bamg_last_error(bamg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" int64_t bamg_launch_count(bamg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int bamg_sync(bamg_ctx* ctx) {
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+static int ctx_read_bytes(bamg_ctx* ctx, const void* dev, size_t bytes, void* host) {
+  if (bytes == 0) return 0;
+  if (bytes > ctx->pinned_doubles * sizeof(double)) {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(host, ctx->pinned, bytes);
+  return 0;
+}
+
+int ctx_read_doubles(bamg_ctx* ctx, const double* dev, size_t n, double* host) {
+  return ctx_read_bytes(ctx, dev, n * sizeof(double), host);
+}
+int ctx_read_i64(bamg_ctx* ctx, const int64_t* dev, size_t n, int64_t* host) {
+  return ctx_read_bytes(ctx, dev, n * sizeof(int64_t), host);
+}
+int ctx_read_i32(bamg_ctx* ctx, const int32_t* dev, size_t n, int32_t* host) {
+  return ctx_read_bytes(ctx, dev, n * sizeof(int32_t), host);
+}
+
+// ------------------------------------------------------------------ scans
+// Three-phase exclusive scan: per-tile sums, a single-block scan of the tile
+// sums, then per-tile scan with the tile offset.  Tiles of 4096 elements.
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+template <typename T>
+__global__ void scan_tile_sums(const T* __restrict__ in, int64_t n, int64_t* __restrict__ sums) {
+  __shared__ int64_t warp_tot[32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int64_t local = 0;
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+    if (idx < n) local += (int64_t)in[idx];
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t v = warp_tot[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) sums[blockIdx.x] = v;
+  }
+}
+
+// exclusive scan of `sums` in place (single block, any length), total at sums[m]
+__global__ void scan_sums_single(int64_t* sums, int64_t m) {
+  __shared__ int64_t buf[SCAN_THREADS];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += SCAN_THREADS) {
+    int64_t idx = base + threadIdx.x;
+    int64_t v = idx < m ? sums[idx] : 0;
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < SCAN_THREADS; off <<= 1) {
+      int64_t t = threadIdx.x >= off ? buf[threadIdx.x - off] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += t;
+      __syncthreads();
+    }
+    int64_t incl = buf[threadIdx.x];
+    if (idx < m) sums[idx] = carry + incl - v;
+    __syncthreads();
+    if (threadIdx.x == SCAN_THREADS - 1) carry += incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[m] = carry;
+}
+
+template <typename T>
+__global__ void scan_tile_apply(const T* __restrict__ in, int64_t n, const int64_t* __restrict__ sums,
+                                int32_t* __restrict__ out, int64_t m) {
+  __shared__ int64_t warp_tot[32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int64_t v[SCAN_ITEMS];
+  int64_t local = 0;
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+    v[i] = idx < n ? (int64_t)in[idx] : 0;
+    local += v[i];
+  }
+  // inclusive warp scan of per-thread totals
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t inc = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t w = lane < (SCAN_THREADS / 32) ? warp_tot[lane] : 0;
+    int64_t wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < (SCAN_THREADS / 32)) warp_tot[lane] = wi - w;
+  }
+  __syncthreads();
+  int64_t run = sums[blockIdx.x] + warp_tot[wid] + inc - local;
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+    if (idx < n) out[idx] = (int32_t)run;
+    run += v[i];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (int32_t)sums[m];
+}
+
+template <typename T>
+static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_t* total_host) {
+  int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (tiles < 1) tiles = 1;
+  int64_t* sums = nullptr;
+  BAMG_TRY(arena_get(ctx, (size_t)tiles + 1, &sums));
+  BAMG_LAUNCH(ctx, scan_tile_sums<T>, (int)tiles, SCAN_THREADS, 0, in, n, sums);
+  BAMG_LAUNCH(ctx, scan_sums_single, 1, SCAN_THREADS, 0, sums, tiles);
+  BAMG_LAUNCH(ctx, scan_tile_apply<T>, (int)tiles, SCAN_THREADS, 0, in, n, sums, out, tiles);
+  if (total_host) BAMG_TRY(ctx_read_i64(ctx, sums + tiles, 1, total_host));
+  return 0;
+}
+
+int scan_i32(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_host) {
+  return scan_impl<int32_t>(ctx, in, out, n, total_host);
+}
+int scan_u8(bamg_ctx* ctx, const uint8_t* in, int32_t* out, int64_t n, int64_t* total_host) {
+  return scan_impl<uint8_t>(ctx, in, out, n, total_host);
+}
+
+// ------------------------------------------------- deterministic colreduce
+constexpr int KMAX = 32;
+
+__global__ void colreduce_partial(const double* __restrict__ X, const double* __restrict__ Y,
+                                  int64_t n, int k, int kind, double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS / 32][KMAX];
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = r0 + per < n ? r0 + per : n;
+  double acc[KMAX];
+#pragma unroll
+  for (int c = 0; c < KMAX; ++c) acc[c] = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double* xr = X + r * k;
+    if (kind == 0) {
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < k) acc[c] += xr[c] * xr[c];
+    } else {
+      const double* yr = Y + r * k;
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < k) acc[c] += xr[c] * yr[c];
+    }
+  }
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < KMAX; ++c) {
+    if (c < k) {
+      double v = warp_sum(acc[c]);
+      if (lane == 0) sh[wid][c] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double v = 0.0;
+    for (int w = 0; w < RED_THREADS / 32; ++w) v += sh[w][threadIdx.x];
+    partial[(int64_t)blockIdx.x * k + threadIdx.x] = v;
+  }
+}
+
+__global__ void colreduce_final(const double* __restrict__ partial, int nb, int k, double* out,
+                                int take_sqrt) {
+  int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (c >= k) return;
+  double v = 0.0;
+  for (int b = lane; b < nb; b += 32) v += partial[(int64_t)b * k + c];
+  v = warp_sum(v);
+  if (lane == 0) out[c] = take_sqrt ? sqrt(v) : v;
+}
+
+int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k, int kind,
+              double* out_dev, int take_sqrt) {
+  BAMG_REQUIRE(ctx, k >= 1 && k <= KMAX, "k must lie in [1, 32]");
+  double* partial = nullptr;
+  BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * k, &partial));
+  BAMG_LAUNCH(ctx, colreduce_partial, RED_BLOCKS, RED_THREADS, 0, X, Y, n, k, kind, partial);
+  BAMG_LAUNCH(ctx, colreduce_final, 1, 32 * k, 0, partial, RED_BLOCKS, k, out_dev, take_sqrt);
+  return 0;
+}
+
+extern "C" int bamg_col_norms(bamg_ctx* ctx, const double* X, int64_t n, int k, double* out) {
+  ctx->arena.reset();
+  return colreduce(ctx, X, nullptr, n, k, 0, out, 1);
+}
+
+extern "C" int bamg_col_dots(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
+                             double* out) {
+  ctx->arena.reset();
+  return colreduce(ctx, X, Y, n, k, 1, out, 0);
+}
+
+__global__ void col_scale_div_kernel(double* X, int64_t total, int k, const double* s) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  double d = s[i % k];
+  if (d == 0.0) d = 1.0;
+  X[i] = X[i] / d;
+}
+
+int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
+  int64_t total = n * k;
+  BAMG_LAUNCH(ctx, col_scale_div_kernel, grid_for(total, 256), 256, 0, X, total, k, s);
+  return 0;
+}
+
+extern "C" int bamg_col_scale_div(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
+  return col_scale_div_dev(ctx, X, n, k, s);
+}
+
+__global__ void col_fill_kernel(double* X, int64_t n, int k, int c, double value) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) X[i * k + c] = value;
+}
+
+int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value) {
+  BAMG_LAUNCH(ctx, col_fill_kernel, grid_for(n, 256), 256, 0, X, n, k, c, value);
+  return 0;
+}
+
+extern "C" int bamg_col_fill(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value) {
+  return col_fill_dev(ctx, X, n, k, c, value);
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ X, const int32_t* __restrict__ idx,
+                                   int64_t m, int k, double* __restrict__ Y) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * k) return;
+  int64_t r = t / k;
+  int c = (int)(t - r * k);
+  Y[t] = X[(int64_t)idx[r] * k + c];
+}
+
+extern "C" int bamg_gather_rows(bamg_ctx* ctx, const double* X, const int32_t* idx, int64_t m,
+                                int k, double* Y) {
+  BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m * k, 256), 256, 0, X, idx, m, k, Y);
+  return 0;
+}

@@ -1,0 +1,22 @@
+// internal.cuh -- cross-translation-unit entry points (no arena reset inside;
+// the exported extern "C" wrapper owns the reset).
+#pragma once
+#include "common.cuh"
+
+int spmm_dev(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k);
+int resid_dev(bamg_ctx* ctx, const bamg_csr* A, const double* b, const double* X, double* R);
+int addmv_dev(bamg_ctx* ctx, const bamg_csr* A, const double* Xc, const double* Xold, double* Y, int k);
+int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip,
+               const double* b, const double* b_scale, const double* x, double* x_out, int k,
+               double omega, double* peak);
+int diag_dev(bamg_ctx* ctx, const bamg_csr* A, double* d);
+int degenerate_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip);
+int transpose_dev(bamg_ctx* ctx, const bamg_csr* A, int32_t* rowptr_t, int32_t* col_t, double* val_t);
+
+// per-vector helpers on n x k interleaved blocks (reduce.cu)
+int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg_csr* N,
+                 const double* U, const double* V, int64_t n, int k, double* sigma,
+                 double* U_flip_or_null, int mode, double* work3);
+int normalize_cols_dev(bamg_ctx* ctx, double* X, int64_t n, int k);
+int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s);
+int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);

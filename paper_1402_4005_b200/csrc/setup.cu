@@ -1,0 +1,267 @@
+// setup.cu -- bootstrap relaxation of the k left / k right test vectors and
+// the singular-test weights, all on device.
+//
+// _smooth_block (bootstrap.py:284-314): per sweep one fused k-wide Jacobi
+// launch per side (right vectors with B, left vectors with the explicit B^T,
+// both through the bit-exact CSR-stream kernel of sparse.cu), the optional
+// inhomogeneous right-hand sides sigma*M u / sigma*N v folded into the
+// Jacobi epilogue, runaway rescaling driven by the per-vector peak the
+// Jacobi epilogue already reduces, and the per-sweep Rayleigh quotient
+// (bootstrap.py:144-153) from three k-wide SpMMs and one fused column-dot
+// pass.  Row normalisation, the pinned constant left slot and the sigma
+// refresh (bootstrap.py:160-177) close the block.  No host synchronisation.
+//
+// singular_test_weights (interp.py:82-102): unit-normalise, ||A v||, then the
+// caps 1e16 / 1e4 x median and the infinite constraint slot, in one tiny
+// single-CTA kernel over the k residual norms.
+#include <cmath>
+
+#include "internal.cuh"
+
+// X[:, c] /= peak[c] when peak[c] > 1e100 (bootstrap.py:302-306)
+__global__ void rescale_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ peak) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  double p = peak[i % k];
+  if (p > 1e100) X[i] = X[i] / p;
+}
+
+// rayleigh quotient finish.  dots = [uMu(k) | vNv(k) | uBv(k)].
+// mode 0: sigma = s (or prev when a normaliser collapses)
+// mode 1: refresh: s < -1e-13 -> flip[c] = 1, s = -s; sigma = |s|
+__global__ void rayleigh_finish_kernel(const double* __restrict__ dots, int k, double* __restrict__ sigma,
+                                       double* __restrict__ flip, int mode) {
+  int c = threadIdx.x;
+  if (c >= k) return;
+  double du = sqrt(fmax(dots[c], 0.0));
+  double dv = sqrt(fmax(dots[k + c], 0.0));
+  double prev = sigma[c];
+  double s = (du < 1e-15 || dv < 1e-15) ? prev : dots[2 * k + c] / (du * dv);
+  if (mode == 0) {
+    sigma[c] = s;
+  } else {
+    double f = 0.0;
+    if (s < -1e-13) {
+      f = 1.0;
+      s = -s;
+    }
+    flip[c] = f;
+    sigma[c] = fabs(s);
+  }
+}
+
+// u_c <- -u_c for flagged columns
+__global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ flip) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  if (flip[i % k] != 0.0) X[i] = -X[i];
+}
+
+// three column-dot sums in one pass: a.b, c.d, e.f per column
+__global__ void tri_colreduce_partial(const double* __restrict__ A, const double* __restrict__ Bm,
+                                      const double* __restrict__ Cm, const double* __restrict__ Dm,
+                                      const double* __restrict__ Em, const double* __restrict__ Fm,
+                                      int64_t n, int k, double* __restrict__ partial) {
+  constexpr int KM = 32;
+  __shared__ double sh[RED_THREADS / 32][3 * KM];
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = min(r0 + per, n);
+  double a0[KM], a1[KM], a2[KM];
+#pragma unroll
+  for (int c = 0; c < KM; ++c) a0[c] = a1[c] = a2[c] = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    int64_t o = r * k;
+#pragma unroll
+    for (int c = 0; c < KM; ++c) {
+      if (c < k) {
+        a0[c] += A[o + c] * Bm[o + c];
+        a1[c] += Cm[o + c] * Dm[o + c];
+        a2[c] += Em[o + c] * Fm[o + c];
+      }
+    }
+  }
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < KM; ++c) {
+    if (c < k) {
+      double v0 = warp_sum(a0[c]), v1 = warp_sum(a1[c]), v2 = warp_sum(a2[c]);
+      if (lane == 0) {
+        sh[wid][c] = v0;
+        sh[wid][k + c] = v1;
+        sh[wid][2 * k + c] = v2;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 * k) {
+    double v = 0.0;
+    for (int w = 0; w < RED_THREADS / 32; ++w) v += sh[w][threadIdx.x];
+    partial[(int64_t)blockIdx.x * 3 * k + threadIdx.x] = v;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int nb, int m, double* __restrict__ out) {
+  int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (; i < m; i += blockDim.x >> 5) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += partial[(int64_t)b * m + i];
+    v = warp_sum(v);
+    if (lane == 0) out[i] = v;
+  }
+}
+
+// sigma update from (U, V): mode 0 smoothing, mode 1 refresh (+ flips of U).
+int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg_csr* N,
+                 const double* U, const double* V, int64_t n, int k, double* sigma,
+                 double* U_flip_or_null, int mode, double* work3) {
+  double *MU, *NV, *AV, *dots, *partial, *flip;
+  const double* mu = U;
+  const double* nv = V;
+  if (!work3) BAMG_TRY(arena_get(ctx, (size_t)3 * n * k, &work3));
+  MU = work3;
+  NV = work3 + (size_t)n * k;
+  AV = work3 + (size_t)2 * n * k;
+  if (M) {
+    BAMG_TRY(spmm_dev(ctx, M, U, MU, k));
+    mu = MU;
+  }
+  if (N) {
+    BAMG_TRY(spmm_dev(ctx, N, V, NV, k));
+    nv = NV;
+  }
+  BAMG_TRY(spmm_dev(ctx, A, V, AV, k));
+  BAMG_TRY(arena_get(ctx, (size_t)3 * k, &dots));
+  BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * 3 * k, &partial));
+  BAMG_TRY(arena_get(ctx, (size_t)k, &flip));
+  BAMG_LAUNCH(ctx, tri_colreduce_partial, RED_BLOCKS, RED_THREADS, 0, U, mu, V, nv, U, AV, n, k, partial);
+  BAMG_LAUNCH(ctx, sum_partials_kernel, 1, 32 * 3 * k > 1024 ? 1024 : 32 * 3 * k, 0, partial, RED_BLOCKS, 3 * k, dots);
+  BAMG_LAUNCH(ctx, rayleigh_finish_kernel, 1, 32, 0, dots, k, sigma, flip, mode);
+  if (mode == 1 && U_flip_or_null) {
+    int64_t total = n * k;
+    BAMG_LAUNCH(ctx, flip_kernel, grid_for(total, 256), 256, 0, U_flip_or_null, total, k, flip);
+  }
+  return 0;
+}
+
+int normalize_cols_dev(bamg_ctx* ctx, double* X, int64_t n, int k) {
+  double* nrm;
+  BAMG_TRY(arena_get(ctx, (size_t)k, &nrm));
+  BAMG_TRY(colreduce(ctx, X, nullptr, n, k, 0, nrm, 1));
+  int64_t total = n * k;
+  (void)total;
+  return col_scale_div_dev(ctx, X, n, k, nrm);
+}
+
+extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                                 const bamg_csr* M, const bamg_csr* N, const double* d,
+                                 const uint8_t* skip, const uint8_t* skip_t, double* U, double* V,
+                                 double* sigma, int k, int nsweeps, double omega, int inhomogeneous,
+                                 int smooth, int refresh) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, A && A_t && A->nrows == A->ncols, "square operator and its transpose expected");
+  BAMG_REQUIRE(ctx, k >= 1 && k <= 32, "k must lie in [1, 32]");
+  const int64_t n = A->nrows;
+  const int64_t total = n * k;
+  if (smooth && nsweeps > 0) {
+    double *U2, *V2, *MU = nullptr, *NV = nullptr, *peak, *work3 = nullptr;
+    if (inhomogeneous) BAMG_TRY(arena_get(ctx, (size_t)3 * total, &work3));
+    BAMG_TRY(arena_get(ctx, (size_t)total, &U2));
+    BAMG_TRY(arena_get(ctx, (size_t)total, &V2));
+    BAMG_TRY(arena_get(ctx, (size_t)2 * k, &peak));
+    if (inhomogeneous) {
+      if (M) BAMG_TRY(arena_get(ctx, (size_t)total, &MU));
+      if (N) BAMG_TRY(arena_get(ctx, (size_t)total, &NV));
+    }
+    double *u = U, *v = V, *uo = U2, *vo = V2;
+    for (int s = 0; s < nsweeps; ++s) {
+      const double* bv = nullptr;  // rhs for the right vectors: sigma * M u
+      const double* bu = nullptr;  // rhs for the left vectors:  sigma * N v
+      if (inhomogeneous) {
+        if (M) {
+          BAMG_TRY(spmm_dev(ctx, M, u, MU, k));
+          bv = MU;
+        } else {
+          bv = u;
+        }
+        if (N) {
+          BAMG_TRY(spmm_dev(ctx, N, v, NV, k));
+          bu = NV;
+        } else {
+          bu = v;
+        }
+      }
+      BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * 2 * k, ctx->stream));
+      BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak));
+      BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k));
+      BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, vo, total, k, peak);
+      BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, uo, total, k, peak + k);
+      std::swap(u, uo);
+      std::swap(v, vo);
+      if (inhomogeneous) BAMG_TRY(rayleigh_dev(ctx, A, M, N, u, v, n, k, sigma, nullptr, 0, work3));
+    }
+    if (u != U) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(U, u, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (v != V) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(V, v, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (refresh) {
+    BAMG_TRY(normalize_cols_dev(ctx, U, n, k));
+    BAMG_TRY(normalize_cols_dev(ctx, V, n, k));
+    BAMG_TRY(col_fill_dev(ctx, U, n, k, 0, 1.0 / std::sqrt((double)n)));
+    BAMG_TRY(rayleigh_dev(ctx, A, M, N, U, V, n, k, sigma, U, 1, nullptr));
+  }
+  return 0;
+}
+
+extern "C" int bamg_refresh_sigmas(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg_csr* N,
+                                   const double* U, const double* V, double* U_flip, double* sigma, int k) {
+  ctx->arena.reset();
+  return rayleigh_dev(ctx, A, M, N, U, V, A->nrows, k, sigma, U_flip, 1, nullptr);
+}
+
+// --------------------------------------------------- singular test weights
+// w = 1/res^2; nan/inf -> 1e16; min(w, 1e16); min(w, 1e4 * max(median, 1e-16));
+// w[inf_slot] = inf   (interp.py:96-101)
+__global__ void weights_finish_kernel(const double* __restrict__ res, int k, int inf_slot, double* __restrict__ w) {
+  if (threadIdx.x != 0) return;
+  const double CAP = 1e16, SPREAD = 1e4;
+  double t[32], s[32];
+  for (int c = 0; c < k; ++c) {
+    double r2 = res[c] * res[c];
+    double v = 1.0 / r2;
+    if (isnan(v)) v = CAP;
+    if (isinf(v) && v > 0) v = CAP;
+    v = fmin(v, CAP);
+    t[c] = v;
+    s[c] = v;
+  }
+  for (int i = 1; i < k; ++i) {  // insertion sort for the median
+    double x = s[i];
+    int j = i - 1;
+    while (j >= 0 && s[j] > x) {
+      s[j + 1] = s[j];
+      --j;
+    }
+    s[j + 1] = x;
+  }
+  double med = (k & 1) ? s[k / 2] : (s[k / 2 - 1] + s[k / 2]) / 2.0;
+  double lim = SPREAD * fmax(med, 1.0 / CAP);
+  for (int c = 0; c < k; ++c) w[c] = fmin(t[c], lim);
+  if (inf_slot >= 0 && inf_slot < k) w[inf_slot] = INFINITY;
+}
+
+extern "C" int bamg_test_weights(bamg_ctx* ctx, const bamg_csr* A, const double* X, int64_t n, int k,
+                                 int inf_slot, double* Xn, double* w) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, k >= 1 && k <= 32, "k must lie in [1, 32]");
+  const int64_t total = n * k;
+  if (Xn != X)
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Xn, X, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(normalize_cols_dev(ctx, Xn, n, k));
+  double *R, *res;
+  BAMG_TRY(arena_get(ctx, (size_t)total, &R));
+  BAMG_TRY(arena_get(ctx, (size_t)k, &res));
+  BAMG_TRY(spmm_dev(ctx, A, Xn, R, k));
+  BAMG_TRY(colreduce(ctx, R, nullptr, n, k, 0, res, 1));
+  BAMG_LAUNCH(ctx, weights_finish_kernel, 1, 32, 0, res, k, inf_slot, w);
+  return 0;
+}

@@ -1,0 +1,675 @@
+// solver.cu -- V-cycle preconditioner and left-preconditioned GMRES.
+//
+// VCycleOperator (solver.py:79-124): per level nu1 weighted-Jacobi sweeps
+// from a zero guess, residual, restriction by Q, recursion, prolongation +
+// correction by P, nu2 sweeps; the coarsest level applies the explicit
+// pseudo-inverse Z = B_L^+ (built once in setup by dense.cu) as one GEMV.
+// All level kernels are the bit-exact CSR-stream kernels of sparse.cu, so a
+// V-cycle on identical operators reproduces the reference bit for bit apart
+// from the coarsest GEMV.
+//
+// GMRES (solver.py:136-226): left preconditioning op(v) = C(Bv), Arnoldi
+// orthogonalisation by two-pass classical Gram-Schmidt (CGS2: three fused
+// passes over the basis -- dot, update+dot, update+norm -- instead of the
+// reference's 2(j+1) serial MGS dot/axpy pairs), Givens rotations and the
+// triangular solve in a one-CTA kernel, x = x0 + e + V y fused, and the true
+// residual ||Bx||/||x|| every iteration (one 3-double device->host read per
+// iteration, the only host synchronisation of the solve).
+#include <cmath>
+#include <vector>
+
+#include "internal.cuh"
+
+struct HLevel {
+  bamg_csr B{}, P{}, Q{};
+  const double* d = nullptr;
+  const uint8_t* skip = nullptr;
+  int n = 0;
+  double* x = nullptr;   // iterate
+  double* x2 = nullptr;  // ping-pong partner
+  double* b = nullptr;   // rhs (levels >= 1)
+  double* r = nullptr;   // residual
+};
+
+struct bamg_hier {
+  bamg_ctx* ctx = nullptr;
+  std::vector<HLevel> lv;
+  const double* Z = nullptr;
+  int nz = 0;
+  double omega = 0.7;
+  int nu1 = 3, nu2 = 3;
+  std::vector<void*> owned;
+  bool ready = false;
+};
+
+extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
+  BAMG_REQUIRE(ctx, nlevels >= 1 && out, "hierarchy needs at least one level");
+  bamg_hier* h = new bamg_hier();
+  h->ctx = ctx;
+  h->lv.resize(nlevels);
+  *out = h;
+  return 0;
+}
+
+extern "C" int bamg_hier_destroy(bamg_hier* h) {
+  if (!h) return 0;
+  cudaStreamSynchronize(h->ctx->stream);
+  for (void* p : h->owned) cudaFree(p);
+  delete h;
+  return 0;
+}
+
+extern "C" int bamg_hier_set_level(bamg_hier* h, int level, const bamg_csr* B, const double* d,
+                                   const uint8_t* skip, const bamg_csr* P, const bamg_csr* Q) {
+  bamg_ctx* ctx = h->ctx;
+  BAMG_REQUIRE(ctx, level >= 0 && level < (int)h->lv.size(), "level out of range");
+  HLevel& L = h->lv[level];
+  L.B = *B;
+  L.d = d;
+  L.skip = skip;
+  L.n = B->nrows;
+  if (P) L.P = *P;
+  if (Q) L.Q = *Q;
+  h->ready = false;
+  return 0;
+}
+
+extern "C" int bamg_hier_set_coarsest(bamg_hier* h, const double* Z, int n) {
+  h->Z = Z;
+  h->nz = n;
+  return 0;
+}
+
+extern "C" int bamg_hier_set_smoother(bamg_hier* h, double omega, int nu_pre, int nu_post) {
+  h->omega = omega;
+  h->nu1 = nu_pre;
+  h->nu2 = nu_post;
+  return 0;
+}
+
+static int hier_prepare(bamg_hier* h) {
+  if (h->ready) return 0;
+  bamg_ctx* ctx = h->ctx;
+  int L = (int)h->lv.size();
+  BAMG_REQUIRE(ctx, h->Z && h->nz == h->lv[L - 1].n, "coarsest pseudo-inverse missing or wrong size");
+  for (int l = 0; l < L; ++l) {
+    HLevel& v = h->lv[l];
+    BAMG_REQUIRE(ctx, v.B.rowptr != nullptr, "level operator missing");
+    if (l + 1 < L) BAMG_REQUIRE(ctx, v.P.rowptr && v.Q.rowptr, "transfer operators missing");
+    size_t n = (size_t)v.n;
+    double* buf = nullptr;
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&buf, sizeof(double) * 4 * (n > 0 ? n : 1)));
+    h->owned.push_back(buf);
+    v.x = buf;
+    v.x2 = buf + n;
+    v.b = buf + 2 * n;
+    v.r = buf + 3 * n;
+  }
+  h->ready = true;
+  return 0;
+}
+
+// x = 0 + (omega * (b - 0)) / d  on unskipped rows (the first sweep from the
+// zero guess, bit-identical to relax.py:78-83 with x = 0).
+__global__ void jacobi_from_zero_kernel(int n, const double* __restrict__ b, const double* __restrict__ d,
+                                        const uint8_t* __restrict__ skip, double omega,
+                                        double* __restrict__ x) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double upd = skip[i] ? 0.0 : __ddiv_rn(__dmul_rn(omega, b[i]), d[i]);
+  x[i] = __dadd_rn(0.0, upd);
+}
+
+// y = Z b, Z row-major n x n (warp per row, coalesced).
+__global__ void gemv_rowmajor_kernel(int n, const double* __restrict__ Z, const double* __restrict__ b,
+                                     double* __restrict__ y) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const double* zr = Z + (int64_t)warp * n;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s += zr[j] * b[j];
+  s = warp_sum(s);
+  if (lane == 0) y[warp] = s;
+}
+
+static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* x_out) {
+  BAMG_TRY(hier_prepare(h));
+  int L = (int)h->lv.size();
+  const double om = h->omega;
+  // downward
+  const double* bl = b_in;
+  std::vector<double*> xs(L);
+  for (int l = 0; l < L - 1; ++l) {
+    HLevel& v = h->lv[l];
+    double* cur = v.x;
+    double* oth = v.x2;
+    if (h->nu1 > 0) {
+      BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(v.n, 256), 256, 0, v.n, bl, v.d, v.skip, om, cur);
+      for (int s = 1; s < h->nu1; ++s) {
+        BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, bl, nullptr, cur, oth, 1, om, nullptr));
+        std::swap(cur, oth);
+      }
+    } else {
+      BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(cur, 0, sizeof(double) * v.n, ctx->stream));
+    }
+    xs[l] = cur;
+    v.x2 = oth;
+    v.x = cur;
+    BAMG_TRY(resid_dev(ctx, &v.B, bl, cur, v.r));
+    HLevel& c = h->lv[l + 1];
+    BAMG_TRY(spmm_dev(ctx, &v.Q, v.r, c.b, 1));
+    bl = c.b;
+  }
+  // coarsest: x_L = Z b_L
+  HLevel& cl = h->lv[L - 1];
+  double* xc = (L == 1) ? x_out : cl.x;
+  BAMG_LAUNCH(ctx, gemv_rowmajor_kernel, grid_for((int64_t)h->nz * 32, 256), 256, 0, h->nz, h->Z, bl, xc);
+  // upward
+  for (int l = L - 2; l >= 0; --l) {
+    HLevel& v = h->lv[l];
+    const double* blv = (l == 0) ? b_in : v.b;
+    double* cur = v.x;
+    double* oth = v.x2;
+    // x <- x + P xc  (written to the partner buffer, then ping-pong)
+    BAMG_TRY(addmv_dev(ctx, &v.P, xc, cur, oth, 1));
+    std::swap(cur, oth);
+    for (int s = 0; s < h->nu2; ++s) {
+      double* dst = (l == 0 && s == h->nu2 - 1) ? x_out : oth;
+      BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, blv, nullptr, cur, dst, 1, om, nullptr));
+      if (dst == x_out) {
+        cur = x_out;
+      } else {
+        std::swap(cur, oth);
+      }
+    }
+    if (l == 0 && h->nu2 == 0)
+      BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(x_out, cur, sizeof(double) * v.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    v.x = cur == x_out ? v.x : cur;
+    xc = cur;
+  }
+  return 0;
+}
+
+extern "C" int bamg_vcycle(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
+  ctx->arena.reset();
+  return vcycle_impl(ctx, h, b, x);
+}
+
+// ===================================================================== GMRES
+constexpr int GM_BLOCKS = RED_BLOCKS;
+constexpr int GM_THREADS = 256;
+constexpr int GM_GROUP = 16;  // basis vectors per register group
+
+// partial[b * m + i] = sum over block b's chunk of V_i . w   (i < m)
+__global__ void __launch_bounds__(GM_THREADS)
+mdot_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ w, int64_t n,
+            double* __restrict__ partial) {
+  __shared__ double sh[GM_THREADS / 32][GM_GROUP];
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = min(r0 + per, n);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g0 = 0; g0 < m; g0 += GM_GROUP) {
+    double acc[GM_GROUP];
+#pragma unroll
+    for (int g = 0; g < GM_GROUP; ++g) acc[g] = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += GM_THREADS) {
+      double wi = w[i];
+#pragma unroll
+      for (int g = 0; g < GM_GROUP; ++g)
+        if (g0 + g < m) acc[g] += Vp[g0 + g][i] * wi;
+    }
+#pragma unroll
+    for (int g = 0; g < GM_GROUP; ++g) {
+      double v = warp_sum(acc[g]);
+      if (lane == 0) sh[wid][g] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < GM_GROUP && g0 + threadIdx.x < m) {
+      double v = 0.0;
+      for (int q = 0; q < GM_THREADS / 32; ++q) v += sh[q][threadIdx.x];
+      partial[(int64_t)blockIdx.x * m + g0 + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// w -= sum_i c_i V_i ; then optionally partial dots V_i . w_new (mode 1) or
+// the partial |w_new|^2 (mode 2).  c read from device.
+template <int MODE>
+__global__ void __launch_bounds__(GM_THREADS)
+mupdate_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
+               double* __restrict__ w, int64_t n, double* __restrict__ partial) {
+  __shared__ double sh[GM_THREADS / 32][GM_GROUP];
+  __shared__ double sc[1024];
+  for (int i = threadIdx.x; i < m && i < 1024; i += GM_THREADS) sc[i] = c[i];
+  __syncthreads();
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = min(r0 + per, n);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += GM_THREADS) {
+    double t = 0.0;
+    for (int g = 0; g < m; ++g) t += (g < 1024 ? sc[g] : c[g]) * Vp[g][i];
+    double wn = w[i] - t;
+    w[i] = wn;
+    if (MODE == 2) nrm += wn * wn;
+  }
+  if (MODE == 2) {
+    double v = warp_sum(nrm);
+    if (lane == 0) sh[wid][0] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int q = 0; q < GM_THREADS / 32; ++q) s += sh[q][0];
+      partial[blockIdx.x] = s;
+    }
+  }
+}
+
+// out[i] = sum_b partial[b * m + i]  (fixed order -> deterministic)
+__global__ void mreduce_kernel(const double* __restrict__ partial, int nb, int m, double* __restrict__ out,
+                               int accumulate) {
+  int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if (i >= m) return;
+  double v = 0.0;
+  for (int b = lane; b < nb; b += 32) v += partial[(int64_t)b * m + i];
+  v = warp_sum(v);
+  if (lane == 0) out[i] = accumulate ? out[i] + v : v;
+}
+
+// Arnoldi bookkeeping for column j (solver.py:189-209), one thread:
+//   h[j+1] = sqrt(nrm2); happy test; previous rotations; new rotation;
+//   R[:, j]; g; y = R^-1 g (back substitution).  state[0] = happy flag,
+//   state[1] = h[j+1].
+__global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const double* __restrict__ nrm2,
+                              double beta, double* __restrict__ R, double* __restrict__ g,
+                              double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ y,
+                              double* __restrict__ state) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double hj1 = sqrt(nrm2[0]);
+  h[j + 1] = hj1;
+  double happy = (hj1 <= 1e-14 * beta) ? 1.0 : 0.0;
+  for (int i = 0; i < j; ++i) {
+    double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  double rad = hypot(h[j], h[j + 1]);
+  if (rad == 0.0) {
+    cs[j] = 1.0;
+    sn[j] = 0.0;
+  } else {
+    cs[j] = h[j] / rad;
+    sn[j] = h[j + 1] / rad;
+  }
+  for (int i = 0; i <= j; ++i) R[(int64_t)j * ldr + i] = h[i];  // column j (column-major)
+  R[(int64_t)j * ldr + j] = rad;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  // back substitution R[:j+1,:j+1] y = g[:j+1]
+  for (int i = j; i >= 0; --i) {
+    double s = g[i];
+    for (int q = i + 1; q <= j; ++q) s -= R[(int64_t)q * ldr + i] * y[q];
+    y[i] = s / R[(int64_t)i * ldr + i];
+  }
+  state[0] = happy;
+  state[1] = hj1;
+}
+
+// dst = w / h  unless the happy-breakdown flag is set
+__global__ void scale_new_basis_kernel(const double* __restrict__ w, const double* __restrict__ state,
+                                       int64_t n, double* __restrict__ dst) {
+  if (state[0] != 0.0) return;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double h = state[1];
+  if (i < n) dst[i] = w[i] / h;
+}
+
+// out = base + add + sum_g y_g V_g   (add may be null)
+__global__ void combine_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ y,
+                               const double* __restrict__ base, const double* __restrict__ e_add,
+                               const double* __restrict__ e_add2, int64_t n, double* __restrict__ out) {
+  __shared__ double sy[1024];
+  for (int i = threadIdx.x; i < m && i < 1024; i += blockDim.x) sy[i] = y[i];
+  __syncthreads();
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t = 0.0;
+  for (int g = 0; g < m; ++g) t += (g < 1024 ? sy[g] : y[g]) * Vp[g][i];
+  double e = e_add ? e_add[i] + t : t;   // e_try = e + V y
+  out[i] = base ? base[i] + e : e;        // x = x0 + e_try
+  (void)e_add2;
+}
+
+__global__ void axpby_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                             double* __restrict__ out) {  // out = a - b
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] - b[i];
+}
+
+__global__ void scale_div_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ s,
+                                 double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] / s[0];
+}
+
+struct GmresWork {
+  std::vector<double*> basis;     // device vectors (owned)
+  double** dVp = nullptr;         // device pointer table
+  size_t cap = 0;
+  size_t uploaded = 0;
+  int64_t n = 0;
+};
+
+static int basis_reserve(bamg_ctx* ctx, GmresWork& W, int64_t n, int count) {
+  if (W.n != n) {
+    for (double* p : W.basis) cudaFree(p);
+    W.basis.clear();
+    W.n = n;
+    W.uploaded = 0;
+  }
+  if ((int)W.basis.size() >= count && W.uploaded >= W.basis.size()) return 0;
+  // grow in chunks of 8 vectors so allocation stays off the per-iteration path
+  int target = ((count + 7) / 8) * 8;
+  while ((int)W.basis.size() < target) {
+    double* p = nullptr;
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&p, sizeof(double) * (n > 0 ? n : 1)));
+    W.basis.push_back(p);
+  }
+  if (W.cap < W.basis.size()) {
+    if (W.dVp) {
+      BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFree(W.dVp);
+    }
+    W.cap = W.basis.size() + 32;
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&W.dVp, sizeof(double*) * W.cap));
+  }
+  // the host table must stay alive until the copy lands: synchronous copy
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpy(W.dVp, W.basis.data(), sizeof(double*) * W.basis.size(),
+                                  cudaMemcpyHostToDevice));
+  W.uploaded = W.basis.size();
+  return 0;
+}
+
+static GmresWork& gmres_work(bamg_ctx* ctx) {
+  static thread_local std::vector<std::pair<bamg_ctx*, GmresWork*>> table;
+  for (auto& e : table)
+    if (e.first == ctx) return *e.second;
+  table.push_back({ctx, new GmresWork()});
+  return *table.back().second;
+}
+
+static int apply_op(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* v, double* tmp,
+                    double* out) {
+  if (h) {
+    BAMG_TRY(spmm_dev(ctx, B, v, tmp, 1));
+    return vcycle_impl(ctx, h, tmp, out);
+  }
+  return spmm_dev(ctx, B, v, out, 1);
+}
+
+extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* b,
+                          const double* x0, double* x, int restart, int max_iters, double rtol,
+                          int* iters_host, double* history_host, int* nhistory_host) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, B && B->nrows == B->ncols, "square operator expected");
+  BAMG_REQUIRE(ctx, max_iters >= 0, "max_iters must be nonnegative");
+  const int64_t n = B->nrows;
+  const int nb = GM_BLOCKS;
+  // workspace
+  double *tmp, *w, *e, *rhs, *r, *R, *g, *cs, *sn, *y, *hv, *h2, *part, *scal, *state;
+  int m_cap = (restart > 0 ? restart : max_iters);
+  if (m_cap > max_iters) m_cap = max_iters;
+  if (m_cap < 1) m_cap = 1;
+  BAMG_TRY(arena_get(ctx, n, &tmp));
+  BAMG_TRY(arena_get(ctx, n, &w));
+  BAMG_TRY(arena_get(ctx, n, &e));
+  BAMG_TRY(arena_get(ctx, n, &rhs));
+  BAMG_TRY(arena_get(ctx, n, &r));
+  BAMG_TRY(arena_get(ctx, (size_t)m_cap * m_cap, &R));
+  BAMG_TRY(arena_get(ctx, m_cap + 1, &g));
+  BAMG_TRY(arena_get(ctx, m_cap, &cs));
+  BAMG_TRY(arena_get(ctx, m_cap, &sn));
+  BAMG_TRY(arena_get(ctx, m_cap, &y));
+  BAMG_TRY(arena_get(ctx, m_cap + 2, &hv));
+  BAMG_TRY(arena_get(ctx, m_cap + 2, &h2));
+  BAMG_TRY(arena_get(ctx, (size_t)nb * (m_cap + 2), &part));
+  BAMG_TRY(arena_get(ctx, 8, &scal));
+  BAMG_TRY(arena_get(ctx, 4, &state));
+  GmresWork& W = gmres_work(ctx);
+  const int blk = 256;
+  const int grd = grid_for(n, blk);
+
+  auto norm_into = [&](const double* v, double* out) -> int {
+    return colreduce(ctx, v, nullptr, n, 1, 0, out, 1);
+  };
+  auto metric = [&](const double* xv, double* out_host) -> int {
+    BAMG_TRY(spmm_dev(ctx, B, xv, tmp, 1));
+    BAMG_TRY(norm_into(tmp, scal));
+    BAMG_TRY(norm_into(xv, scal + 1));
+    double hv2[2];
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 2, hv2));
+    *out_host = hv2[1] == 0.0 ? INFINITY : hv2[0] / hv2[1];
+    return 0;
+  };
+
+  int nhist = 0;
+  double m0;
+  BAMG_TRY(metric(x0, &m0));
+  history_host[nhist++] = m0;
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  *iters_host = 0;
+  if (m0 <= rtol) {
+    *nhistory_host = nhist;
+    return 0;
+  }
+  // rhs = C(b - B x0)
+  BAMG_TRY(spmm_dev(ctx, B, x0, tmp, 1));
+  BAMG_LAUNCH(ctx, axpby_kernel, grd, blk, 0, n, b, tmp, w);
+  if (h) {
+    BAMG_TRY(vcycle_impl(ctx, h, w, rhs));
+  } else {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(rhs, w, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(e, 0, sizeof(double) * n, ctx->stream));
+
+  int iters = 0;
+  bool converged = false;
+  bool first_cycle = true;
+  while (iters < max_iters && !converged) {
+    // r = rhs - op(e)
+    if (first_cycle) {
+      BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(r, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      BAMG_TRY(apply_op(ctx, B, h, e, w, tmp));
+      BAMG_LAUNCH(ctx, axpby_kernel, grd, blk, 0, n, rhs, tmp, r);
+    }
+    first_cycle = false;
+    double beta;
+    BAMG_TRY(norm_into(r, scal + 2));
+    BAMG_TRY(ctx_read_doubles(ctx, scal + 2, 1, &beta));
+    if (beta == 0.0) break;
+    int m = (restart > 0 ? restart : max_iters);
+    if (m > max_iters - iters) m = max_iters - iters;
+    BAMG_TRY(basis_reserve(ctx, W, n, 1));
+    BAMG_LAUNCH(ctx, scale_div_kernel, grd, blk, 0, n, r, scal + 2, W.basis[0]);
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(R, 0, sizeof(double) * (size_t)m_cap * m_cap, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(g, 0, sizeof(double) * (m_cap + 1), ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(g, scal + 2, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    int used = 0;
+    bool broke = false;
+    for (int j = 0; j < m; ++j) {
+      BAMG_TRY(basis_reserve(ctx, W, n, j + 2));
+      // w = op(V_j)
+      BAMG_TRY(apply_op(ctx, B, h, W.basis[j], tmp, w));
+      // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; |w|^2
+      BAMG_LAUNCH(ctx, mdot_kernel, nb, GM_THREADS, 0, W.dVp, j + 1, w, n, part);
+      BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, part, nb, j + 1, hv, 0);
+      BAMG_LAUNCH(ctx, mupdate_kernel<0>, nb, GM_THREADS, 0, W.dVp, j + 1, hv, w, n, part);
+      BAMG_LAUNCH(ctx, mdot_kernel, nb, GM_THREADS, 0, W.dVp, j + 1, w, n, part);
+      BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, part, nb, j + 1, h2, 0);
+      BAMG_LAUNCH(ctx, mupdate_kernel<2>, nb, GM_THREADS, 0, W.dVp, j + 1, h2, w, n, part);
+      BAMG_LAUNCH(ctx, mreduce_kernel, 1, 32, 0, part, nb, 1, scal + 3, 0);
+      // h += h2 (length j+1) via the reduce kernel's accumulate path
+      BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, h2, 1, j + 1, hv, 1);
+      BAMG_LAUNCH(ctx, givens_kernel, 1, 32, 0, j, m_cap, hv, scal + 3, beta, R, g, cs, sn, y, state);
+      BAMG_LAUNCH(ctx, scale_new_basis_kernel, grd, blk, 0, w, state, n, W.basis[j + 1]);
+      ++iters;
+      used = j + 1;
+      // x = x0 + (e + V y)
+      BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, x0, e, nullptr, n, x);
+      double mval;
+      BAMG_TRY(metric(x, &mval));
+      history_host[nhist++] = mval;
+      double st[1];
+      BAMG_TRY(ctx_read_doubles(ctx, state, 1, st));
+      bool happy = st[0] != 0.0;
+      if (mval <= rtol) converged = true;
+      if (converged || happy || iters >= max_iters) {
+        if (happy) converged = true;
+        BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, nullptr, e, nullptr, n, tmp);
+        BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        broke = true;
+        break;
+      }
+    }
+    if (!broke) {
+      // restart: e += V y (y of the last column is still current)
+      BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, nullptr, e, nullptr, n, tmp);
+      BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, 0, y, x0, e, nullptr, n, x);
+    }
+  }
+  *iters_host = iters;
+  *nhistory_host = nhist;
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return converged ? 0 : 1;
+}
+
+// ===================================================== sign fix + l1 norm
+// stats: [0] max|x| (bits), [1] first index of the max, [2] sum|x|,
+// [3] non-finite flag
+__global__ void signfix_extract_kernel(const double* __restrict__ x, int64_t n, int stride,
+                                       double* __restrict__ out, unsigned long long* __restrict__ flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = x[i * stride];
+  out[i] = v;
+  if (!isfinite(v)) atomicOr(flags, 1ull);
+}
+
+__global__ void absstats_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ psum,
+                                        double* __restrict__ pmax, long long* __restrict__ pidx) {
+  __shared__ double ss[256], sm[256];
+  __shared__ long long si[256];
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double s = 0.0, mx = -1.0;
+  long long mi = -1;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    double a = fabs(x[i]);
+    s += a;
+    if (a > mx) {
+      mx = a;
+      mi = i;
+    }
+  }
+  ss[threadIdx.x] = s;
+  sm[threadIdx.x] = mx;
+  si[threadIdx.x] = mi;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      ss[threadIdx.x] += ss[threadIdx.x + off];
+      double m2 = sm[threadIdx.x + off];
+      long long i2 = si[threadIdx.x + off];
+      if (m2 > sm[threadIdx.x] || (m2 == sm[threadIdx.x] && i2 >= 0 && (si[threadIdx.x] < 0 || i2 < si[threadIdx.x]))) {
+        sm[threadIdx.x] = m2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    psum[blockIdx.x] = ss[0];
+    pmax[blockIdx.x] = sm[0];
+    pidx[blockIdx.x] = si[0];
+  }
+}
+
+__global__ void absstats_final_kernel(int nb, const double* psum, const double* pmax, const long long* pidx,
+                                      double* stats) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0, mx = -1.0;
+  long long mi = -1;
+  for (int b = 0; b < nb; ++b) {
+    s += psum[b];
+    if (pmax[b] > mx) {
+      mx = pmax[b];
+      mi = pidx[b];
+    }
+  }
+  stats[0] = mx;
+  stats[1] = (double)mi;
+  stats[2] = s;
+}
+
+__global__ void uniform_fill_kernel(double* out, int64_t n, const unsigned long long* flags,
+                                    const double* stats) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (flags[0] != 0ull || stats[2] == 0.0) out[i] = 1.0 / (double)n;
+}
+
+__global__ void signfix_apply_kernel(double* out, int64_t n, const double* stats) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long pk = (long long)stats[1];
+  double v = out[i];
+  // stats computed on the current contents; peak value sign decides
+  double sgn_src = stats[3];
+  if (sgn_src < 0.0) v = -v;
+  double tot = stats[2];
+  out[i] = tot > 0.0 ? v / tot : v;
+  (void)pk;
+}
+
+__global__ void peak_sign_kernel(const double* out, double* stats) {
+  long long pk = (long long)stats[1];
+  stats[3] = pk >= 0 ? out[pk] : 1.0;
+}
+
+static int absstats(bamg_ctx* ctx, const double* x, int64_t n, double* stats) {
+  double *psum, *pmax;
+  long long* pidx;
+  BAMG_TRY(arena_get(ctx, RED_BLOCKS, &psum));
+  BAMG_TRY(arena_get(ctx, RED_BLOCKS, &pmax));
+  BAMG_TRY(arena_get(ctx, RED_BLOCKS, &pidx));
+  BAMG_LAUNCH(ctx, absstats_partial_kernel, RED_BLOCKS, 256, 0, x, n, psum, pmax, pidx);
+  BAMG_LAUNCH(ctx, absstats_final_kernel, 1, 32, 0, RED_BLOCKS, psum, pmax, pidx, stats);
+  return 0;
+}
+
+extern "C" int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int stride, double* out,
+                                int uniform_fallback) {
+  ctx->arena.reset();
+  unsigned long long* flags;
+  double* stats;
+  BAMG_TRY(arena_get(ctx, 1, &flags));
+  BAMG_TRY(arena_get(ctx, 4, &stats));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(flags, 0, sizeof(*flags), ctx->stream));
+  BAMG_LAUNCH(ctx, signfix_extract_kernel, grid_for(n, 256), 256, 0, x, n, stride, out, flags);
+  BAMG_TRY(absstats(ctx, out, n, stats));
+  if (uniform_fallback) {
+    BAMG_LAUNCH(ctx, uniform_fill_kernel, grid_for(n, 256), 256, 0, out, n, flags, stats);
+    BAMG_TRY(absstats(ctx, out, n, stats));
+  }
+  BAMG_LAUNCH(ctx, peak_sign_kernel, 1, 1, 0, out, stats);
+  BAMG_LAUNCH(ctx, signfix_apply_kernel, grid_for(n, 256), 256, 0, out, n, stats);
+  return 0;
+}

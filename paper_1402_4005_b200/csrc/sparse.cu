@@ -1,0 +1,366 @@
+// sparse.cu -- bit-exact CSR SpMV / k-wide SpMM / fused weighted Jacobi,
+// diagonal, degenerate-row mask, explicit transpose, symmetric pattern.
+//
+// Layout: CSR (int32 rowptr/col, fp64 val); k vectors interleaved n x k.
+// Kernel shape ("CSR-stream"): one CTA owns a tile of TILE_ROWS consecutive
+// rows, stages the tile's contiguous [rowptr[r0], rowptr[r0+R]) slice of
+// col/val into shared memory with coalesced loads, then each thread walks
+// one (row, vector) pair SEQUENTIALLY in ascending column order with
+// __dmul_rn/__dadd_rn -- exactly scipy's csr_matvec(s) arithmetic
+// (sparse.py:81-86 -> scipy _sparsetools csr_matvec: sum = 0; sum += a*x).
+// The Jacobi epilogue reproduces relax.py:78-83 bit for bit:
+//   r = b - Ax;  upd = (omega * r) / d;  upd = 0 on skipped rows;  x + upd.
+#include "common.cuh"
+
+constexpr int TILE_ROWS = 256;
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_NNZ = 2048;  // 24 KB of staged col/val per CTA
+
+enum { EPI_PLAIN = 0, EPI_JACOBI = 1, EPI_RESID = 2, EPI_ADD = 3 };
+
+struct EpiArgs {
+  const double* d;        // diagonal
+  const uint8_t* skip;    // rows left alone
+  const double* b;        // rhs (may be null)
+  const double* b_scale;  // per-vector scale of b (may be null)
+  const double* xold;     // iterate being relaxed (EPI_JACOBI)
+  double omega;
+  double* peak;           // per-vector max |x'| (may be null)
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(TILE_THREADS)
+csr_tile_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ X, int k,
+                double* __restrict__ Y, EpiArgs ea) {
+  __shared__ int32_t s_rp[TILE_ROWS + 1];
+  __shared__ int32_t s_col[TILE_NNZ];
+  __shared__ double s_val[TILE_NNZ];
+  __shared__ unsigned long long s_peak[32];
+
+  const int r0 = blockIdx.x * TILE_ROWS;
+  const int rows = min(TILE_ROWS, nrows - r0);
+  for (int i = threadIdx.x; i <= rows; i += TILE_THREADS) s_rp[i] = rowptr[r0 + i];
+  if (EPI == EPI_JACOBI && ea.peak && threadIdx.x < 32) s_peak[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int nz0 = s_rp[0];
+  const int tile_nnz = s_rp[rows] - nz0;
+  const bool staged = tile_nnz <= TILE_NNZ;
+  if (staged) {
+    for (int j = threadIdx.x; j < tile_nnz; j += TILE_THREADS) {
+      s_col[j] = col[nz0 + j];
+      s_val[j] = val[nz0 + j];
+    }
+  }
+  __syncthreads();
+
+  const int pairs = rows * k;
+  for (int p = threadIdx.x; p < pairs; p += TILE_THREADS) {
+    const int lr = p / k;
+    const int c = p - lr * k;
+    const int row = r0 + lr;
+    const int jb = s_rp[lr], je = s_rp[lr + 1];
+    double sum = 0.0;
+    if (staged) {
+      for (int j = jb - nz0; j < je - nz0; ++j)
+        sum = __dadd_rn(sum, __dmul_rn(s_val[j], X[(int64_t)s_col[j] * k + c]));
+    } else {
+      for (int j = jb; j < je; ++j)
+        sum = __dadd_rn(sum, __dmul_rn(val[j], X[(int64_t)col[j] * k + c]));
+    }
+    const int64_t idx = (int64_t)row * k + c;
+    if (EPI == EPI_PLAIN) {
+      Y[idx] = sum;
+    } else if (EPI == EPI_RESID) {
+      Y[idx] = __dsub_rn(ea.b[idx], sum);
+    } else if (EPI == EPI_ADD) {
+      Y[idx] = __dadd_rn(ea.xold[idx], sum);
+    } else {
+      double bb = 0.0;
+      if (ea.b) bb = ea.b_scale ? __dmul_rn(ea.b_scale[c], ea.b[idx]) : ea.b[idx];
+      const double r = __dsub_rn(bb, sum);
+      double upd = 0.0;
+      if (!ea.skip[row]) upd = __ddiv_rn(__dmul_rn(ea.omega, r), ea.d[row]);
+      const double xn = __dadd_rn(ea.xold[idx], upd);
+      Y[idx] = xn;
+      if (ea.peak) atomicMax(&s_peak[c], (unsigned long long)__double_as_longlong(fabs(xn)));
+    }
+  }
+  if (EPI == EPI_JACOBI && ea.peak) {
+    __syncthreads();
+    if (threadIdx.x < k) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
+  }
+}
+
+static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
+  BAMG_REQUIRE(ctx, A && A->rowptr && (A->nnz == 0 || (A->col && A->val)), "null CSR");
+  BAMG_REQUIRE(ctx, A->nrows >= 0 && A->ncols >= 0, "negative CSR shape");
+  return 0;
+}
+
+static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, int k,
+                       double* Y, const EpiArgs& ea) {
+  BAMG_TRY(check_csr(ctx, A));
+  BAMG_REQUIRE(ctx, k >= 1 && k <= 32, "k must lie in [1, 32]");
+  int grid = (A->nrows + TILE_ROWS - 1) / TILE_ROWS;
+  if (grid == 0) return 0;
+  switch (epi) {
+    case EPI_PLAIN:
+      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
+                  A->col, A->val, X, k, Y, ea);
+      break;
+    case EPI_RESID:
+      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_RESID>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
+                  A->col, A->val, X, k, Y, ea);
+      break;
+    case EPI_ADD:
+      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_ADD>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
+                  A->col, A->val, X, k, Y, ea);
+      break;
+    default:
+      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
+                  A->col, A->val, X, k, Y, ea);
+  }
+  return 0;
+}
+
+// Internal entry points (used by the setup / solver translation units).
+int spmm_dev(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k) {
+  EpiArgs ea{};
+  return launch_tile(ctx, EPI_PLAIN, A, X, k, Y, ea);
+}
+
+int resid_dev(bamg_ctx* ctx, const bamg_csr* A, const double* b, const double* X, double* R) {
+  EpiArgs ea{};
+  ea.b = b;
+  return launch_tile(ctx, EPI_RESID, A, X, 1, R, ea);
+}
+
+// Y = Xold + A Xc (prolongation + correction, solver.py:116: x + P @ xc)
+int addmv_dev(bamg_ctx* ctx, const bamg_csr* A, const double* Xc, const double* Xold, double* Y, int k) {
+  EpiArgs ea{};
+  ea.xold = Xold;
+  return launch_tile(ctx, EPI_ADD, A, Xc, k, Y, ea);
+}
+
+int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip,
+               const double* b, const double* b_scale, const double* x, double* x_out, int k,
+               double omega, double* peak) {
+  EpiArgs ea{};
+  ea.d = d;
+  ea.skip = skip;
+  ea.b = b;
+  ea.b_scale = b_scale;
+  ea.xold = x;
+  ea.omega = omega;
+  ea.peak = peak;
+  return launch_tile(ctx, EPI_JACOBI, A, x, k, x_out, ea);
+}
+
+extern "C" int bamg_spmv(bamg_ctx* ctx, const bamg_csr* A, const double* x, double* y) {
+  return spmm_dev(ctx, A, x, y, 1);
+}
+
+extern "C" int bamg_spmm(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k) {
+  return spmm_dev(ctx, A, X, Y, k);
+}
+
+extern "C" int bamg_jacobi(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip,
+                           const double* b, const double* b_scale, const double* x,
+                           double* x_out, int k, double omega, double* peak) {
+  BAMG_REQUIRE(ctx, x != x_out, "Jacobi needs distinct input and output iterates");
+  if (peak) BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * k, ctx->stream));
+  return jacobi_dev(ctx, A, d, skip, b, b_scale, x, x_out, k, omega, peak);
+}
+
+// ------------------------------------------------------------ diagonal
+__global__ void diag_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, double* __restrict__ d) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lo = rp[i], hi = rp[i + 1] - 1;
+  double v = 0.0;
+  while (lo <= hi) {  // columns are sorted
+    int mid = (lo + hi) >> 1;
+    int c = col[mid];
+    if (c == i) {
+      v = val[mid];
+      break;
+    }
+    if (c < i) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  d[i] = v;
+}
+
+int diag_dev(bamg_ctx* ctx, const bamg_csr* A, double* d) {
+  int n = A->nrows < A->ncols ? A->nrows : A->ncols;
+  BAMG_LAUNCH(ctx, diag_kernel, grid_for(n, 256), 256, 0, n, A->rowptr, A->col, A->val, d);
+  return 0;
+}
+
+extern "C" int bamg_diag(bamg_ctx* ctx, const bamg_csr* A, double* d) {
+  BAMG_TRY(check_csr(ctx, A));
+  return diag_dev(ctx, A, d);
+}
+
+__global__ void count_nonpos_kernel(const double* __restrict__ d, int64_t n, unsigned long long* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int flag = (i < n) && (d[i] <= 0.0);
+  int cnt = __syncthreads_count(flag);
+  if (threadIdx.x == 0 && cnt) atomicAdd(out, (unsigned long long)cnt);
+}
+
+extern "C" int bamg_count_nonpositive(bamg_ctx* ctx, const double* d, int64_t n, int64_t* count_host) {
+  ctx->arena.reset();
+  unsigned long long* cnt = nullptr;
+  BAMG_TRY(arena_get(ctx, 1, &cnt));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(*cnt), ctx->stream));
+  BAMG_LAUNCH(ctx, count_nonpos_kernel, grid_for(n, 256), 256, 0, d, n, cnt);
+  return ctx_read_i64(ctx, reinterpret_cast<int64_t*>(cnt), 1, count_host);
+}
+
+// ------------------------------------------------------ degenerate rows
+// relax.py:47-63: off = (sum_j |a_ij|) - |d_i| (sequential row sum, as
+// np.add.reduceat / the ones-vector product); skip = d <= 0 | off > 4 d.
+__global__ void degenerate_kernel(int n, const int32_t* __restrict__ rp, const double* __restrict__ val,
+                                  const double* __restrict__ d, uint8_t* __restrict__ skip) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double mass = 0.0;
+  for (int j = rp[i]; j < rp[i + 1]; ++j) mass = __dadd_rn(mass, fabs(val[j]));
+  double di = d[i];
+  double off = __dsub_rn(mass, fabs(di));
+  skip[i] = (di <= 0.0) || (off > __dmul_rn(4.0, di));
+}
+
+int degenerate_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip) {
+  BAMG_LAUNCH(ctx, degenerate_kernel, grid_for(A->nrows, 256), 256, 0, A->nrows, A->rowptr, A->val, d, skip);
+  return 0;
+}
+
+extern "C" int bamg_degenerate_rows(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip) {
+  BAMG_TRY(check_csr(ctx, A));
+  return degenerate_dev(ctx, A, d, skip);
+}
+
+// ------------------------------------------------------------ transpose
+// count per column -> exclusive scan -> scatter by (row-major) order using a
+// per-column cursor, then sort each output row by source row (stable result
+// independent of atomic order).  Output rows are short for every operator in
+// scope; long rows fall back to a shell sort in the same thread.
+__global__ void col_count_kernel(int64_t nnz, const int32_t* __restrict__ col, int32_t* __restrict__ cnt) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nnz) atomicAdd(&cnt[col[j]], 1);
+}
+
+__global__ void transpose_scatter_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                         const double* __restrict__ val, int32_t* __restrict__ cursor,
+                                         int32_t* __restrict__ col_t, double* __restrict__ val_t) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = rp[i]; j < rp[i + 1]; ++j) {
+    int pos = atomicAdd(&cursor[col[j]], 1);
+    col_t[pos] = i;
+    val_t[pos] = val[j];
+  }
+}
+
+__device__ void sort_segment(int32_t* key, double* val, int len) {
+  // insertion sort (segments are short); shell gaps for long ones
+  int gaps[] = {701, 301, 132, 57, 23, 10, 4, 1};
+  for (int g = 0; g < 8; ++g) {
+    int gap = gaps[g];
+    if (gap >= len) continue;
+    for (int i = gap; i < len; ++i) {
+      int32_t kk = key[i];
+      double vv = val ? val[i] : 0.0;
+      int j = i;
+      while (j >= gap && key[j - gap] > kk) {
+        key[j] = key[j - gap];
+        if (val) val[j] = val[j - gap];
+        j -= gap;
+      }
+      key[j] = kk;
+      if (val) val[j] = vv;
+    }
+  }
+}
+
+__global__ void sort_rows_kernel(int n, const int32_t* __restrict__ rp, int32_t* col, double* val) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int b = rp[i], e = rp[i + 1];
+  sort_segment(col + b, val ? val + b : nullptr, e - b);
+}
+
+int transpose_dev(bamg_ctx* ctx, const bamg_csr* A, int32_t* rowptr_t, int32_t* col_t, double* val_t) {
+  int32_t* cnt = nullptr;
+  int32_t* cursor = nullptr;
+  BAMG_TRY(arena_get(ctx, (size_t)A->ncols + 1, &cnt));
+  BAMG_TRY(arena_get(ctx, (size_t)A->ncols + 1, &cursor));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (A->ncols + 1), ctx->stream));
+  BAMG_LAUNCH(ctx, col_count_kernel, grid_for(A->nnz, 256), 256, 0, A->nnz, A->col, cnt);
+  BAMG_TRY(scan_i32(ctx, cnt, rowptr_t, A->ncols, nullptr));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(cursor, rowptr_t, sizeof(int32_t) * (A->ncols + 1),
+                                       cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_LAUNCH(ctx, transpose_scatter_kernel, grid_for(A->nrows, 256), 256, 0, A->nrows, A->rowptr,
+              A->col, A->val, cursor, col_t, val_t);
+  BAMG_LAUNCH(ctx, sort_rows_kernel, grid_for(A->ncols, 256), 256, 0, A->ncols, rowptr_t, col_t, val_t);
+  return 0;
+}
+
+extern "C" int bamg_csr_transpose(bamg_ctx* ctx, const bamg_csr* A, int32_t* rowptr_t, int32_t* col_t,
+                                  double* val_t) {
+  BAMG_TRY(check_csr(ctx, A));
+  ctx->arena.reset();
+  return transpose_dev(ctx, A, rowptr_t, col_t, val_t);
+}
+
+// ------------------------------------------------------ symmetric pattern
+// pattern(A + A^T) minus the diagonal = sorted union of row i of A and row i
+// of A^T (both sorted), without i.  (sparse.py:120-128)
+template <bool FILL>
+__global__ void sym_union_kernel(int n, const int32_t* __restrict__ ra, const int32_t* __restrict__ ca,
+                                 const int32_t* __restrict__ rt, const int32_t* __restrict__ ct,
+                                 int32_t* __restrict__ cnt_or_rp, int32_t* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int a = ra[i], ae = ra[i + 1], t = rt[i], te = rt[i + 1];
+  int w = FILL ? cnt_or_rp[i] : 0;
+  int count = 0;
+  while (a < ae || t < te) {
+    int x;
+    if (t >= te || (a < ae && ca[a] < ct[t])) x = ca[a++];
+    else if (a >= ae || ct[t] < ca[a]) x = ct[t++];
+    else {
+      x = ca[a];
+      ++a;
+      ++t;
+    }
+    if (x == i) continue;
+    if (FILL) out[w + count] = x;
+    ++count;
+  }
+  if (!FILL) cnt_or_rp[i] = count;
+}
+
+extern "C" int bamg_sym_pattern_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                                      int32_t* rowptr_s, int64_t* nnz_host) {
+  BAMG_TRY(check_csr(ctx, A));
+  BAMG_TRY(check_csr(ctx, A_t));
+  BAMG_REQUIRE(ctx, A->nrows == A->ncols && A_t->nrows == A->nrows, "square matrix expected");
+  ctx->arena.reset();
+  int32_t* cnt = nullptr;
+  BAMG_TRY(arena_get(ctx, (size_t)A->nrows + 1, &cnt));
+  BAMG_LAUNCH(ctx, sym_union_kernel<false>, grid_for(A->nrows, 256), 256, 0, A->nrows, A->rowptr, A->col,
+              A_t->rowptr, A_t->col, cnt, (int32_t*)nullptr);
+  return scan_i32(ctx, cnt, rowptr_s, A->nrows, nnz_host);
+}
+
+extern "C" int bamg_sym_pattern_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* A_t,
+                                     const int32_t* rowptr_s, int32_t* col_s) {
+  BAMG_LAUNCH(ctx, sym_union_kernel<true>, grid_for(A->nrows, 256), 256, 0, A->nrows, A->rowptr, A->col,
+              A_t->rowptr, A_t->col, const_cast<int32_t*>(rowptr_s), col_s);
+  return 0;
+}

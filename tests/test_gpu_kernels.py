@@ -1,0 +1,155 @@
+"""GPU parity of the sparse kernels, the V-cycle and GMRES against the oracle.
+
+Inputs are the reference's own golden fixtures; every comparison here is
+bit-exact (SpMV / SpMM / Jacobi / transpose / residual) or within the stated
+tolerance (coarsest GEMV inside the V-cycle, GMRES reductions).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import csr_from, gmres_args, oracle_cfg
+from oracle import bamg_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1402_4005_b200 import _lib, device
+    _lib.lib()
+    return _lib, device
+
+
+def up(eng, M):
+    return eng[1].DeviceCSR.from_host(M)
+
+
+def dvec(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def test_spmv_bitexact(eng, golden):
+    g = golden("kernels")
+    A = csr_from(g, "A")
+    dA = up(eng, A)
+    y = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    dx = dvec(g["x"])
+    eng[0].call("bamg_spmv", dA.ref(), eng[0].ptr(dx), eng[0].ptr(y))
+    assert np.array_equal(y.cpu().numpy(), g["Ax"])
+
+
+def test_transpose_and_spmv_transpose_bitexact(eng, golden):
+    g = golden("kernels")
+    A = csr_from(g, "A")
+    dA = up(eng, A)
+    rp = torch.empty(A.shape[1] + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(A.nnz, dtype=torch.int32, device="cuda")
+    va = torch.empty(A.nnz, dtype=torch.float64, device="cuda")
+    eng[0].call("bamg_csr_transpose", dA.ref(), eng[0].ptr(rp), eng[0].ptr(ci), eng[0].ptr(va))
+    ref = csr_from(g, "AT")
+    assert np.array_equal(rp.cpu().numpy(), ref.indptr)
+    assert np.array_equal(ci.cpu().numpy(), ref.indices)
+    assert np.array_equal(va.cpu().numpy(), ref.data)
+    dT = eng[1].DeviceCSR(rp, ci, va, (A.shape[1], A.shape[0]))
+    y = torch.empty(A.shape[1], dtype=torch.float64, device="cuda")
+    dx = dvec(g["x"])
+    eng[0].call("bamg_spmv", dT.ref(), eng[0].ptr(dx), eng[0].ptr(y))
+    assert np.array_equal(y.cpu().numpy(), g["ATx"])
+
+
+@pytest.mark.parametrize("k", [1, 8, 12, 16])
+def test_spmm_bitexact(eng, k):
+    rng = np.random.default_rng(k)
+    from scipy import sparse as sp
+    A = orc.canon(sp.random_array((3000, 2500), density=0.003, random_state=rng))
+    X = rng.standard_normal((2500, k))
+    dA = up(eng, A)
+    Y = torch.empty((3000, k), dtype=torch.float64, device="cuda")
+    dX = dvec(X)
+    eng[0].call("bamg_spmm", dA.ref(), eng[0].ptr(dX), eng[0].ptr(Y), k)
+    ref = np.stack([A @ X[:, c] for c in range(k)], axis=1)
+    assert np.array_equal(Y.cpu().numpy(), ref)
+
+
+def test_jacobi_bitexact_with_degenerate_rows(eng, golden):
+    g = golden("kernels")
+    B = csr_from(g, "jacB")
+    d = B.diagonal()
+    dB = up(eng, B)
+    dd = dvec(d)
+    skip = torch.empty(B.shape[0], dtype=torch.uint8, device="cuda")
+    eng[0].call("bamg_degenerate_rows", dB.ref(), eng[0].ptr(dd), eng[0].ptr(skip))
+    assert np.array_equal(skip.cpu().numpy().astype(bool), g["jac_skip"])
+    out = torch.empty(B.shape[0], dtype=torch.float64, device="cuda")
+    bb, xx = dvec(g["jac_b"]), dvec(g["jac_x"])  # keep the inputs alive across the call
+    eng[0].call("bamg_jacobi", dB.ref(), eng[0].ptr(dd), eng[0].ptr(skip), eng[0].ptr(bb),
+                None, eng[0].ptr(xx), eng[0].ptr(out), 1, 0.7, None)
+    assert np.array_equal(out.cpu().numpy(), g["jac_out"])
+
+
+def _device_hierarchy(eng, levels, omega, nu1, nu2):
+    """Upload an oracle-built hierarchy (test input) into an engine hierarchy."""
+    import ctypes as C
+    L = eng[0]
+    keep = []
+    h = C.c_void_p()
+    L.check(L.lib().bamg_hier_create(L.ctx(), len(levels), C.byref(h)), "hier_create")
+    for i, lv in enumerate(levels):
+        dB = up(eng, lv.B)
+        d = dvec(lv.d)
+        sk = torch.from_numpy(orc.skip_rows(lv.B, lv.d).astype(np.uint8)).cuda()
+        dP = up(eng, lv.P) if lv.P is not None else None
+        dQ = up(eng, lv.Q) if lv.Q is not None else None
+        keep += [dB, d, sk, dP, dQ]
+        L.check(L.lib().bamg_hier_set_level(h, i, dB.ref(), L.ptr(d), L.ptr(sk),
+                                            dP.ref() if dP else None, dQ.ref() if dQ else None), "set_level")
+    A = levels[-1].B.toarray()
+    U, s, Vt = np.linalg.svd(A)
+    keep_s = s > 1e-12 * s[0]
+    Z = (Vt[keep_s].T / s[keep_s]) @ U[:, keep_s].T
+    dZ = dvec(np.ascontiguousarray(Z))
+    keep.append(dZ)
+    L.check(L.lib().bamg_hier_set_coarsest(h, L.ptr(dZ), A.shape[0]), "set_coarsest")
+    L.check(L.lib().bamg_hier_set_smoother(h, omega, nu1, nu2), "set_smoother")
+    return h, keep
+
+
+@pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_planar1024_k12", "pipe_uniform63"])
+def test_vcycle_and_gmres_match_oracle(eng, golden, name):
+    import ctypes as C
+    g = golden(name)
+    B = csr_from(g, "B")
+    cfg = oracle_cfg(g)
+    restart, max_iters, rtol = gmres_args(g)
+    levels, T, x0 = orc.setup(B, cfg, g.get("geometry"), g["init_right_draw"], g["init_left_draw"])
+    Cv = orc.VCycle(levels, cfg["omega"], cfg["nu_pre"], cfg["nu_post"])
+    h, keep = _device_hierarchy(eng, levels, cfg["omega"], cfg["nu_pre"], cfg["nu_post"])
+    L = eng[0]
+    b = g["vcycle_in"]
+    out = torch.empty(B.shape[0], dtype=torch.float64, device="cuda")
+    db = dvec(b)
+    L.call("bamg_vcycle", h, L.ptr(db), L.ptr(out))
+    ref = Cv(b)
+    got = out.cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.abs(got - g["vcycle_out"]).max() <= 1e-12 * np.abs(ref).max()
+    # GMRES
+    dB = up(eng, B)
+    x = torch.empty(B.shape[0], dtype=torch.float64, device="cuda")
+    its = C.c_int(0)
+    nh = C.c_int(0)
+    hist = (C.c_double * (max_iters + 1))()
+    zero, dx0 = torch.zeros_like(x), dvec(x0)
+    rc = L.lib().bamg_gmres(L.ctx(), dB.ref(), h, L.ptr(zero), L.ptr(dx0), L.ptr(x),
+                            -1 if restart is None else restart, max_iters, rtol,
+                            C.byref(its), hist, C.byref(nh))
+    L.check(rc, "gmres")
+    assert rc == 0
+    assert its.value == int(g["iterations"])
+    xs = orc.l1_sign_fix(x.cpu().numpy())
+    assert np.abs(xs - g["x"]).sum() <= 1e-10
+    L.lib().bamg_hier_destroy(h)
