@@ -161,10 +161,11 @@ int bamg_rows_fill(bamg_ctx* ctx, const int32_t* cnt, const int32_t* col, const 
 /* ---------------------------------------------------- coarsen (coarsen.py) */
 /* Rank of every coordinate among the distinct values of its axis
  * (np.unique(..., return_inverse=True), coarsen.py:84-87). */
-int bamg_axis_ranks(bamg_ctx* ctx, const double* coord, int64_t n, int32_t* rank);
+int bamg_axis_ranks(bamg_ctx* ctx, const double* coord, int64_t n, int32_t* rank,
+                    int64_t* nvalues_host);
 /* Ranks on the coarse level from the parent ranks of the kept points. */
 int bamg_rerank(bamg_ctx* ctx, const int32_t* parent_rank, const int32_t* coarse_idx,
-                int64_t nc, int64_t nvalues_parent, int32_t* rank_out);
+                int64_t nc, int64_t nvalues_parent, int32_t* rank_out, int64_t* nvalues_host);
 /* mask from per-axis ranks: every rank even (geometric_coarsen, coarsen.py:90-109). */
 int bamg_even_mask(bamg_ctx* ctx, const int32_t* const* ranks_host, int ndim, int64_t n,
                    uint8_t* mask);
@@ -175,11 +176,18 @@ int bamg_split_from_mask(bamg_ctx* ctx, const uint8_t* mask, int64_t n, int32_t*
  * unit-RMS scaling, `sweeps` F-relaxation sweeps, mu, and the greedy MIS in
  * (-mu, index) order computed as a parallel lexicographically-first MIS.
  * `normals` holds the n_fine draws in ascending fine-index order.  Sets new
- * coarse points in cmask; returns the number of candidates in *ncand_host
- * and, when the pass found none on an empty coarse set, the fallback index. */
+ * coarse points in cmask; returns the number of candidates in *ncand_host.
+ * When there are none and coarse_empty is set, argmax(mu) over the fine
+ * points is promoted instead (coarsen.py:148-152). */
 int bamg_cr_pass(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* adj, const double* d,
                  uint8_t* cmask, const double* normals, int64_t n_fine, int sweeps,
-                 double omega, double threshold, int64_t* ncand_host);
+                 double omega, double threshold, int coarse_empty, int64_t* ncand_host,
+                 int64_t* ncoarse_host);
+/* Rows without stored entries (cr_coarsen rejects them, coarsen.py:119-121). */
+int bamg_count_empty_rows(bamg_ctx* ctx, const bamg_csr* A, int64_t* count_host);
+/* Column permutation of an n x k block: Y[:, j] = X[:, perm_host[j]]. */
+int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int k, const int32_t* perm_host,
+                      double* Y);
 
 /* ------------------------------------------------------------ dense (dense.py) */
 /* Scatter a CSR into a dense column-major n x n matrix. */
@@ -211,11 +219,15 @@ int bamg_vcycle(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x);
 /* Left-preconditioned GMRES (solver.py:136-226): Arnoldi with two-pass
  * classical Gram-Schmidt (CGS2) as fused multi-vector reductions, Givens
  * rotations on device, per-iteration true residual ||Bx||/||x||.
- * h may be NULL (unpreconditioned).  restart <= 0 = unrestarted.
+ * h may be NULL (unpreconditioned).  restart <= 0 = unrestarted.  stopping:
+ * 0 = ||Bx||/||x|| ("scaled_bx"), 1 = ||b-Bx||/||b-Bx0|| ("relative").
  * history_host receives max_iters + 1 doubles; returns 0 converged, 1 not. */
 int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* b,
                const double* x0, double* x, int restart, int max_iters, double rtol,
-               int* iters_host, double* history_host, int* nhistory_host);
+               int stopping, int* iters_host, double* history_host, int* nhistory_host);
+/* y = Z b for a row-major dense n x n Z (the coarsest pseudo-inverse apply,
+ * dense.py:130-131). */
+int bamg_dense_gemv(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y);
 /* x0 finalisation (bootstrap.py:420-428 and solver.py:229-235): non-finite or
  * all-zero -> uniform 1/n, sign so the max-|.| entry is positive, l1 = 1. */
 int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int stride, double* out,

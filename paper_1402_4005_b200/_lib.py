@@ -69,11 +69,13 @@ _SIGS = {
                       P, P, P, PI64],
     "bamg_rows_count": [P, P, P, I64, C.c_int, P, PI64],
     "bamg_rows_fill": [P, P, P, P, I64, C.c_int, P, P, P],
-    "bamg_axis_ranks": [P, P, I64, P],
-    "bamg_rerank": [P, P, P, I64, I64, P],
+    "bamg_axis_ranks": [P, P, I64, P, PI64],
+    "bamg_rerank": [P, P, P, I64, I64, P, PI64],
     "bamg_even_mask": [P, C.POINTER(P), C.c_int, I64, P],
     "bamg_split_from_mask": [P, P, I64, P, P, P, PI64],
-    "bamg_cr_pass": [P, PCSR, PCSR, P, P, P, I64, C.c_int, F64, F64, PI64],
+    "bamg_cr_pass": [P, PCSR, PCSR, P, P, P, I64, C.c_int, F64, F64, C.c_int, PI64, PI64],
+    "bamg_count_empty_rows": [P, PCSR, PI64],
+    "bamg_permute_cols": [P, P, I64, C.c_int, C.POINTER(C.c_int32), P],
     "bamg_csr_to_dense": [P, PCSR, P, C.c_int, C.c_int],
     "bamg_dense_pinv": [P, P, C.c_int, F64, P],
     "bamg_coarsest_triplets": [P, P, P, P, C.c_int, C.c_int, P, P, P],
@@ -83,7 +85,8 @@ _SIGS = {
     "bamg_hier_set_coarsest": [P, P, C.c_int],
     "bamg_hier_set_smoother": [P, F64, C.c_int, C.c_int],
     "bamg_vcycle": [P, P, P, P],
-    "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, PINT, PF64, PINT],
+    "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, C.c_int, PINT, PF64, PINT],
+    "bamg_dense_gemv": [P, P, C.c_int, P, P],
     "bamg_sign_fix_l1": [P, P, I64, C.c_int, P, C.c_int],
 }
 _RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64}
@@ -144,10 +147,14 @@ def ctx(device: int | None = None):
 
 
 def check(rc: int, what: str, c=None):
-    """Raise on negative codes; return the (non-negative) status otherwise."""
+    """Raise on negative codes (-2 argument errors as ValueError, like the
+    reference); return the non-negative status otherwise."""
     if rc < 0:
         msg = lib().bamg_last_error(c if c is not None else ctx())
-        raise BamgError(f"{what}: {msg.decode() if msg else rc}")
+        text = f"{what}: {msg.decode() if msg else rc}"
+        if rc == -2:
+            raise ValueError(text)
+        raise BamgError(text)
     return rc
 
 

@@ -1,0 +1,417 @@
+"""Adaptive multilevel setup (mirrors markovmg/bootstrap.py, Algorithm 1).
+
+The recursion, stop/stall/truncation rules and seed bookkeeping are host
+control flow on scalars, exactly as in the reference; every array operation
+is an engine launch on device-resident data:
+  smoothing blocks (csrc/setup.cu), test weights and LS transfer rows
+  (csrc/interp.cu), Galerkin products (csrc/spgemm.cu), C/F splits
+  (csrc/coarsen.cu), coarsest triplets (csrc/dense.cu).
+Test vectors are n x k interleaved device blocks; `TripletSet.left/right`
+give the reference's (k, n) host layout on access.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine
+from .coarsen import AxisRanks, CfSplitting, CoarseningConfig, make_splitting
+from .device import DeviceCSR, device
+from .interp import (InterpConfig, build_interpolation, build_restriction_rows,
+                     singular_test_weights)
+from .relax import SmootherConfig
+from .sparse import adjacency_structure, as_device
+
+#: bootstrap.py:329
+SICK_DIAG_FRACTION = 0.02
+
+
+class TripletSet:
+    """Approximate singular triplets on device (bootstrap.py:35-59)."""
+
+    def __init__(self, sigmas, left, right):
+        self.dsigmas = sigmas   # k, device
+        self.dleft = left       # n x k, device
+        self.dright = right     # n x k, device
+        if not (self.dsigmas.numel() == self.dleft.shape[1] == self.dright.shape[1]):
+            raise ValueError("inconsistent triplet counts")
+
+    @property
+    def r(self) -> int:
+        return int(self.dsigmas.numel())
+
+    @property
+    def n(self) -> int:
+        return int(self.dright.shape[0])
+
+    @property
+    def sigmas(self) -> np.ndarray:
+        return self.dsigmas.cpu().numpy()
+
+    @property
+    def left(self) -> np.ndarray:
+        return self.dleft.cpu().numpy().T.copy()
+
+    @property
+    def right(self) -> np.ndarray:
+        return self.dright.cpu().numpy().T.copy()
+
+    def copy(self) -> "TripletSet":
+        return TripletSet(self.dsigmas.clone(), self.dleft.clone(), self.dright.clone())
+
+
+@dataclass(frozen=True)
+class SetupConfig:
+    """bootstrap.py:62-80."""
+
+    n_tests: int = 8
+    setup_cycles: int = 1
+    inner_passes: int = 1
+    smoother: SmootherConfig = field(default_factory=SmootherConfig)
+    interp: InterpConfig = field(default_factory=InterpConfig)
+    coarsening: CoarseningConfig = field(default_factory=CoarseningConfig)
+    seed: int = 1
+
+    def __post_init__(self):
+        if self.n_tests < 2:
+            raise ValueError("need at least two test vectors")
+        if self.setup_cycles < 1:
+            raise ValueError("setup_cycles must be at least 1")
+        if self.inner_passes < 1:
+            raise ValueError("inner_passes must be at least 1")
+
+
+class Level:
+    """One level (bootstrap.py:83-99).  Device operators are `d*`; the
+    reference's attribute names materialise host scipy copies on access."""
+
+    def __init__(self, index, B: DeviceCSR, d, M: DeviceCSR, N: DeviceCSR, split=None,
+                 P: DeviceCSR | None = None, Q: DeviceCSR | None = None, geometry=None,
+                 Bt: DeviceCSR | None = None, W: DeviceCSR | None = None):
+        self.index = index
+        self.dB, self.ddiag, self.dM, self.dN = B, d, M, N
+        self.split = split
+        self.dP, self.dQ, self.dBt, self.dW = P, Q, Bt, W
+        self._geometry = geometry
+        self._cache = {}
+
+    def _h(self, key, M):
+        if M is None:
+            return None
+        if key not in self._cache:
+            self._cache[key] = M.to_host()
+        return self._cache[key]
+
+    @property
+    def n(self) -> int:
+        return self.dB.shape[0]
+
+    @property
+    def nnz(self) -> int:
+        return self.dB.nnz
+
+    B = property(lambda self: self._h("B", self.dB))
+    M = property(lambda self: self._h("M", self.dM))
+    N = property(lambda self: self._h("N", self.dN))
+    P = property(lambda self: self._h("P", self.dP))
+    Q = property(lambda self: self._h("Q", self.dQ))
+
+    @property
+    def diag(self) -> np.ndarray:
+        return self.ddiag.cpu().numpy()
+
+    @property
+    def geometry(self):
+        g = self._geometry
+        if g is None:
+            return None
+        hc = g.host_coords if isinstance(g, AxisRanks) else g
+        return hc.value() if hasattr(hc, "value") else hc
+
+
+@dataclass
+class Hierarchy:
+    levels: list
+
+    @property
+    def depth(self) -> int:
+        return len(self.levels)
+
+    @property
+    def finest(self) -> Level:
+        return self.levels[0]
+
+    @property
+    def coarsest(self) -> Level:
+        return self.levels[-1]
+
+
+@dataclass
+class SetupResult:
+    hierarchy: Hierarchy
+    triplets: TripletSet
+    x0: np.ndarray
+    seconds: float = 0.0
+    dx0: object = None
+
+
+def complexities(hierarchy: Hierarchy) -> tuple[float, float, int]:
+    """Grid / operator complexity and depth (bootstrap.py:127-136)."""
+    levels = hierarchy.levels
+    if not levels:
+        raise ValueError("empty hierarchy")
+    n0 = levels[0].n
+    nnz0 = max(levels[0].nnz, 1)
+    return (float(sum(lv.n for lv in levels) / n0), float(sum(lv.nnz for lv in levels) / nnz0),
+            len(levels))
+
+
+def levels_at_least(hierarchy: Hierarchy, floor: int = 100) -> int:
+    return sum(1 for lv in hierarchy.levels if lv.n >= floor)
+
+
+class _SeedStream:
+    """bootstrap.py:317-324."""
+
+    def __init__(self, seed_sequence: np.random.SeedSequence):
+        self._ss = seed_sequence
+
+    def next(self) -> np.random.SeedSequence:
+        return self._ss.spawn(1)[0]
+
+
+class _LevelOps:
+    """Device state of one level reused across the setup: B, B^T, diag, skip
+    masks, adjacency (built lazily, once)."""
+
+    def __init__(self, B: DeviceCSR, Bt: DeviceCSR | None = None):
+        self.B = B
+        self.Bt = Bt if Bt is not None else engine.transpose(B)
+        self.d = engine.diag(B)
+        self.skip = engine.degenerate_rows(B, self.d)
+        self.skip_t = engine.degenerate_rows(self.Bt, self.d)
+        self._adj = None
+
+    @property
+    def adj(self):
+        if self._adj is None:
+            self._adj = engine.sym_pattern(self.B, self.Bt)
+        return self._adj
+
+
+def _mass(M: DeviceCSR):
+    """None for an identity mass (engine fast path, bit-identical)."""
+    return None if M.is_identity else M
+
+
+def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps | None = None):
+    """Smoothed random left/right test vectors; left slot 0 constant (bootstrap.py:180-202).
+
+    The raw draws come from `rng.standard_normal((r, n))` twice (right, then
+    left) as in the reference, or from `draws=(right, left)` ((r, n) arrays,
+    e.g. the BASELINE uniform(0,1) vectors).  They are host-generated inputs
+    uploaded once; the smoothing, normalisation, sigmas and ordering run on
+    device.
+    """
+    A = as_device(B)
+    ops = ops or _LevelOps(A)
+    n = A.shape[0]
+    r = cfg.n_tests
+    if draws is None:
+        if rng is None:
+            rng = np.random.default_rng(np.random.SeedSequence(cfg.seed))
+        right_h = rng.standard_normal((r, n))
+        left_h = rng.standard_normal((r, n))
+    else:
+        right_h, left_h = draws
+    V = engine.to_device_vec(np.ascontiguousarray(np.asarray(right_h, dtype=np.float64).T))
+    U = engine.to_device_vec(np.ascontiguousarray(np.asarray(left_h, dtype=np.float64).T))
+    sig = torch.zeros(r, dtype=torch.float64, device=device())
+    sm = cfg.smoother
+    # nu1 homogeneous sweeps per slot, no runaway rescaling (bootstrap.py:191-194)
+    engine.smooth_block(A, ops.Bt, None, None, ops.d, ops.skip, ops.skip_t, U, V, sig,
+                        sm.sweeps_pre, sm.omega, inhomogeneous=0, smooth=2, refresh=0)
+    engine.col_fill(U, 0, 1.0 / np.sqrt(n))
+    engine.normalize_cols(V)
+    engine.normalize_cols(U)
+    engine.refresh_sigmas(A, None, None, U, V, sig)
+    s = sig.cpu().numpy()
+    order = np.concatenate([[0], 1 + np.argsort(s[1:], kind="stable")])
+    if not np.array_equal(order, np.arange(r)):
+        U = engine.permute_cols(U, order)
+        V = engine.permute_cols(V, order)
+        sig = engine.to_device_vec(s[order])
+    return TripletSet(sig, U, V)
+
+
+def coarsest_triplets(B, M, N, r: int) -> TripletSet:
+    """Exact generalized singular triplets of the coarsest operator (bootstrap.py:205-281)."""
+    A, Md, Nd = as_device(B), as_device(M), as_device(N)
+    n = A.shape[0]
+    Bd = engine.csr_to_dense(A)
+    Mdd = engine.csr_to_dense(Md)
+    Ndd = engine.csr_to_dense(Nd)
+    U, V, s = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r)
+    return TripletSet(s, U, V)
+
+
+def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inhomogeneous: bool):
+    """bootstrap.py:284-314 in one engine call."""
+    sm = cfg.smoother
+    engine.smooth_block(ops.B, ops.Bt, _mass(M), _mass(N), ops.d, ops.skip, ops.skip_t,
+                        trips.dleft, trips.dright, trips.dsigmas, sm.sweeps_pre, sm.omega,
+                        int(inhomogeneous), smooth=1, refresh=1)
+
+
+def _operator_degenerate(Bc: DeviceCSR) -> bool:
+    """bootstrap.py:332-334."""
+    d = engine.diag(Bc)
+    return engine.count_nonpositive(d) > SICK_DIAG_FRACTION * Bc.shape[0]
+
+
+def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None, depth: int = 0,
+                    first_cycle: bool = True, seed_stream: _SeedStream | None = None,
+                    ops: _LevelOps | None = None):
+    """One recursive setup pass (bootstrap.py:337-392); returns (levels, triplets)."""
+    A = as_device(B)
+    ops = ops or _LevelOps(A)
+    Md, Nd = as_device(M), as_device(N)
+    n = A.shape[0]
+    if seed_stream is None:
+        seed_stream = _SeedStream(np.random.SeedSequence(cfg.seed))
+    ranks = geometry
+    if geometry is not None and not isinstance(geometry, AxisRanks):
+        ranks = AxisRanks.from_geometry(geometry)
+
+    split = None
+    if n >= cfg.coarsening.stop_size and depth + 1 < cfg.coarsening.max_levels:
+        seed = seed_stream.next()
+        if cfg.coarsening.mode == "cr":
+            split = make_splitting(A, ranks, cfg.coarsening, seed, adj=ops.adj, diag=ops.d)
+        else:
+            split = make_splitting(A, ranks, cfg.coarsening, seed)
+        if split.n_coarse >= 0.9 * n or split.n_coarse == n:
+            split = None  # coarsening stalled
+    if split is None:
+        trips = coarsest_triplets(A, Md, Nd, trips.r)
+        return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
+
+    _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
+
+    levels = None
+    for _ in range(cfg.inner_passes):
+        v_tests = singular_test_weights(A, trips.dright)
+        u_tests = singular_test_weights(A, trips.dleft, transpose_side=True,
+                                        infinite_slot=0 if cfg.interp.constrain_constant_in_q else None,
+                                        Bt=ops.Bt)
+        P = build_interpolation(A, split, v_tests, cfg.interp, adj=ops.adj)
+        W = build_restriction_rows(A, split, u_tests, cfg.interp, adj=ops.adj)
+        Q = engine.transpose(W)
+        Bc = engine.spgemm(engine.spgemm(Q, A, order=1), P, order=0)
+        if _operator_degenerate(Bc):
+            trips = coarsest_triplets(A, Md, Nd, trips.r)
+            return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
+        Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
+        Pt = engine.transpose(P)
+        Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
+        cranks = ranks.restrict(split) if ranks is not None else None
+        cl = engine.gather_rows(trips.dleft, split.dcoarse)
+        cr = engine.gather_rows(trips.dright, split.dcoarse)
+        engine.normalize_cols(cl)
+        engine.normalize_cols(cr)
+        coarse = TripletSet(trips.dsigmas.clone(), cl, cr)
+        sub_levels, coarse = bootstrap_cycle(Bc, Mc, Nc, coarse, cfg, cranks, depth + 1,
+                                             first_cycle, seed_stream)
+        # prolong: u <- Q^T u_c (= W u_c), v <- P v_c; normalise; pin; refresh; smooth
+        U = engine.spmm(W, coarse.dleft)
+        V = engine.spmm(P, coarse.dright)
+        trips = TripletSet(coarse.dsigmas.clone(), U, V)
+        engine.smooth_block(ops.B, ops.Bt, _mass(Md), _mass(Nd), ops.d, ops.skip, ops.skip_t,
+                            U, V, trips.dsigmas, 0, cfg.smoother.omega, 0, smooth=0, refresh=1)
+        _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True)
+        levels = [Level(depth, A, ops.d, Md, Nd, split, P, Q, ranks, Bt=ops.Bt, W=W)] + sub_levels
+    return levels, trips
+
+
+def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None = None) -> SetupResult:
+    """Full setup: initial vectors, the configured cycles, x0 (bootstrap.py:395-429).
+
+    `draws=(right, left)` injects the raw (k, n) initial vectors (BASELINE's
+    uniform(0,1) seed-0 vectors); otherwise the reference's own
+    SeedSequence(seed).spawn(2)[0] standard-normal stream is used.
+    """
+    t0 = time.perf_counter()
+    A = B_device if B_device is not None else as_device(problem.B)
+    n = A.shape[0]
+    root = np.random.SeedSequence(cfg.seed)
+    ss_init, ss_levels = root.spawn(2)
+    ops = _LevelOps(A)
+    rng = np.random.default_rng(ss_init) if draws is None else None
+    trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops)
+    stream = _SeedStream(ss_levels)
+    eye = DeviceCSR.identity(n)
+    geometry = AxisRanks.from_geometry(problem.geometry) if problem.geometry is not None else None
+    hierarchy = None
+    for cycle in range(cfg.setup_cycles):
+        levels, trips = bootstrap_cycle(A, eye, eye, trips, cfg, geometry=geometry, depth=0,
+                                        first_cycle=(cycle == 0), seed_stream=stream, ops=ops)
+        hierarchy = Hierarchy(levels)
+        engine.col_fill(trips.dleft, 0, 1.0 / np.sqrt(n))
+        engine.refresh_sigmas(A, None, None, trips.dleft, trips.dright, trips.dsigmas)
+    dx0 = engine.sign_fix_l1(trips.dright, stride=trips.r, uniform_fallback=True)
+    torch.cuda.synchronize()
+    seconds = time.perf_counter() - t0
+    return SetupResult(hierarchy, trips, dx0.cpu().numpy(), seconds=seconds, dx0=dx0)
+
+
+def triplet_residual(trips: TripletSet, B, M=None, N=None) -> float:
+    """Setup progress metric (bootstrap.py:432-444), device reductions."""
+    A = as_device(B)
+    n = A.shape[0]
+    Md = as_device(M) if M is not None else DeviceCSR.identity(n)
+    Nd = as_device(N) if N is not None else DeviceCSR.identity(n)
+    At = engine.transpose(A)
+    s = trips.dsigmas
+    Bv = engine.spmm(A, trips.dright)
+    Mu = engine.spmm(Md, trips.dleft)
+    Btu = engine.spmm(At, trips.dleft)
+    Nv = engine.spmm(Nd, trips.dright)
+    r1 = engine.col_norms(Bv - s * Mu)
+    r2 = engine.col_norms(Btu - s * Nv)
+    return float((r1 + r2).sum().item())
+
+
+def export_hierarchy(hierarchy: Hierarchy, directory) -> None:
+    """Matrix Market per level + JSON manifest (bootstrap.py:447-469)."""
+    from pathlib import Path
+
+    from scipy.io import mmwrite
+    from scipy import sparse as sp
+
+    out = Path(directory)
+    out.mkdir(parents=True, exist_ok=True)
+    o_g, o_c, depth = complexities(hierarchy)
+    manifest = {"levels": [], "grid_complexity": o_g, "operator_complexity": o_c, "depth": depth}
+
+    def save(path, M):
+        mmwrite(str(path), sp.coo_matrix(M), comment="", field="real", precision=17,
+                symmetry="general")
+
+    for lev in hierarchy.levels:
+        entry = {"index": lev.index, "n": int(lev.n), "nnz": int(lev.nnz)}
+        save(out / f"B_{lev.index}.mtx", lev.B)
+        if lev.dP is not None:
+            save(out / f"P_{lev.index}.mtx", lev.P)
+            save(out / f"Q_{lev.index}.mtx", lev.Q)
+            split_file = f"splitting_{lev.index}.json"
+            (out / split_file).write_text(lev.split.to_json())
+            entry["splitting"] = split_file
+            entry["n_coarse"] = int(lev.split.n_coarse)
+        manifest["levels"].append(entry)
+    (out / "hierarchy.json").write_text(json.dumps(manifest, indent=2, sort_keys=True))

@@ -294,3 +294,24 @@ extern "C" int bamg_gather_rows(bamg_ctx* ctx, const double* X, const int32_t* i
   BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m * k, 256), 256, 0, X, idx, m, k, Y);
   return 0;
 }
+
+struct Perm32 {
+  int32_t p[32];
+};
+
+__global__ void permute_cols_kernel(const double* __restrict__ X, int64_t n, int k, Perm32 perm, double* __restrict__ Y) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * k) return;
+  int64_t r = t / k;
+  int c = (int)(t - r * k);
+  Y[t] = X[r * k + perm.p[c]];
+}
+
+extern "C" int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int k, const int32_t* perm_host,
+                                 double* Y) {
+  BAMG_REQUIRE(ctx, k >= 1 && k <= 32 && X != Y, "k in [1, 32] and distinct buffers");
+  Perm32 p{};
+  for (int c = 0; c < k; ++c) p.p[c] = perm_host[c];
+  BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n * k, 256), 256, 0, X, n, k, p, Y);
+  return 0;
+}

@@ -1,0 +1,532 @@
+// dense.cu -- the coarsest level, on device: explicit pseudo-inverse and the
+// exact generalized singular triplets.
+//
+// Both rest on a one-sided (Hestenes) Jacobi SVD: columns of G are
+// orthogonalised pairwise in round-robin tournament order, one CTA per
+// column pair per step (n/2 independent rotations per launch), V
+// accumulates the rotations.  At convergence sigma_i = ||g_i||, the right
+// singular vectors are V's columns and the left ones g_i / sigma_i.
+//
+//  * PinvOperator (dense.py:118-131): Z = sum_{sigma_i > tol*sigma_max}
+//    v_i g_i^T / sigma_i^2, stored row-major so the V-cycle's coarsest solve
+//    is one coalesced GEMV (solver.cu) -- the same operator as the
+//    reference's V((U^T b) / s), one launch per application.
+//  * coarsest_triplets (bootstrap.py:205-281): the doubled eigenproblem
+//    [[0,B],[B^T,0]] x = lambda diag(M,N) x is solved as the SVD of
+//    K = L_M^-1 B L_N^-T (M = L_M L_M^T, N = L_N L_N^T by a right-looking
+//    Cholesky, one launch per column): the eigenvalues are +-sigma(K), and
+//    the eigenvector of +sigma_j splits into u = L_M^-T a_j, v = L_N^-T b_j.
+//    Left vectors of numerically-null sigmas come from a second Jacobi SVD of
+//    K^T.  Halves are M-/N-normalised, v is flipped so u^T B v >= 0, and the
+//    null-slot cleanup (dead rows/columns, sign-coherent lead) runs in one CTA.
+#include <cmath>
+
+#include "internal.cuh"
+
+// --------------------------------------------------------- CSR -> dense
+__global__ void csr_to_dense_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                    const double* __restrict__ val, double* __restrict__ D, int ld, int transpose) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = rp[i]; j < rp[i + 1]; ++j) {
+    int c = col[j];
+    if (transpose) D[(int64_t)i * ld + c] = val[j];  // column-major A^T == row-major A
+    else D[(int64_t)c * ld + i] = val[j];            // column-major A
+  }
+}
+
+extern "C" int bamg_csr_to_dense(bamg_ctx* ctx, const bamg_csr* A, double* D, int ld, int transpose) {
+  int64_t cols = transpose ? A->nrows : A->ncols;
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(D, 0, sizeof(double) * (size_t)ld * cols, ctx->stream));
+  BAMG_LAUNCH(ctx, csr_to_dense_kernel, grid_for(A->nrows, 128), 128, 0, A->nrows, A->rowptr, A->col, A->val, D, ld,
+              transpose);
+  return 0;
+}
+
+// ------------------------------------------------------ one-sided Jacobi
+constexpr int JAC_THREADS = 256;
+
+__device__ __forceinline__ void tournament_pair(int m, int s, int i, int* p, int* q) {
+  // circle method: player 0 fixed, players 1..m-1 rotate by s
+  auto at = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + s) % (m - 1)) + 1; };
+  *p = at(i);
+  *q = at(m - 1 - i);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sh[0] = t;
+  __syncthreads();
+  return sh[0];
+}
+
+__global__ void __launch_bounds__(JAC_THREADS)
+jacobi_step_kernel(double* __restrict__ G, int nrows, double* __restrict__ V, int ncols, int m, int s, double tol,
+                   int* __restrict__ rotated) {
+  __shared__ double sh[32];
+  int p, q;
+  tournament_pair(m, s, blockIdx.x, &p, &q);
+  if (p >= ncols || q >= ncols) return;
+  if (p > q) {
+    int t = p;
+    p = q;
+    q = t;
+  }
+  double* gp = G + (int64_t)p * nrows;
+  double* gq = G + (int64_t)q * nrows;
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    double x = gp[r], y = gq[r];
+    a += x * x;
+    b += y * y;
+    c += x * y;
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  c = block_sum(c, sh);
+  if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) return;
+  double zeta = (b - a) / (2.0 * c);
+  double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    double x = gp[r], y = gq[r];
+    gp[r] = cs * x - sn * y;
+    gq[r] = sn * x + cs * y;
+  }
+  double* vp = V + (int64_t)p * ncols;
+  double* vq = V + (int64_t)q * ncols;
+  for (int r = threadIdx.x; r < ncols; r += blockDim.x) {
+    double x = vp[r], y = vq[r];
+    vp[r] = cs * x - sn * y;
+    vq[r] = sn * x + cs * y;
+  }
+  if (threadIdx.x == 0) *rotated = 1;
+}
+
+__global__ void eye_kernel(double* V, int n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < (int64_t)n * n) V[i] = (i / n == i % n) ? 1.0 : 0.0;
+}
+
+__global__ void col_norms_dense_kernel(const double* __restrict__ G, int nrows, int ncols, double* __restrict__ sig) {
+  __shared__ double sh[32];
+  int c = blockIdx.x;
+  double a = 0.0;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    double x = G[(int64_t)c * nrows + r];
+    a += x * x;
+  }
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) sig[c] = sqrt(a);
+}
+
+// G (nrows x ncols, column-major) -> G V = U S; V (ncols x ncols); sig
+static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig) {
+  int* rotated;
+  BAMG_TRY(arena_get(ctx, 1, &rotated));
+  BAMG_LAUNCH(ctx, eye_kernel, grid_for((int64_t)ncols * ncols, 256), 256, 0, V, ncols);
+  int m = ncols + (ncols & 1);
+  if (ncols >= 2) {
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(rotated, 0, sizeof(int), ctx->stream));
+      for (int s = 0; s < m - 1; ++s)
+        BAMG_LAUNCH(ctx, jacobi_step_kernel, m / 2, JAC_THREADS, 0, G, nrows, V, ncols, m, s, 1e-15, rotated);
+      int rot = 0;
+      BAMG_TRY(ctx_read_i32(ctx, rotated, 1, &rot));
+      if (!rot) break;
+    }
+  }
+  BAMG_LAUNCH(ctx, col_norms_dense_kernel, ncols, JAC_THREADS, 0, G, nrows, ncols, sig);
+  return 0;
+}
+
+// Z[r][c] = sum_i V[r][i] G[c][i] w_i,  w_i = 1/sig_i^2 if sig_i > tol*max else 0
+__global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, double tol, double* __restrict__ w) {
+  __shared__ double smax;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) m = fmax(m, sig[i]);
+    smax = m;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    w[i] = (smax > 0.0 && sig[i] > tol * smax) ? 1.0 / (sig[i] * sig[i]) : 0.0;
+}
+
+constexpr int GT = 16;
+__global__ void pinv_assemble_kernel(const double* __restrict__ V, const double* __restrict__ G, const double* __restrict__ w,
+                                     int n, double* __restrict__ Z) {
+  __shared__ double sv[GT][GT + 1], sg[GT][GT + 1];
+  int r = blockIdx.y * GT + threadIdx.y;  // row of Z
+  int c = blockIdx.x * GT + threadIdx.x;  // column of Z
+  double acc = 0.0;
+  for (int i0 = 0; i0 < n; i0 += GT) {
+    int ii = i0 + threadIdx.x;
+    sv[threadIdx.y][threadIdx.x] = (r < n && ii < n) ? V[(int64_t)ii * n + r] * w[ii] : 0.0;  // V[r][ii] w_ii
+    int cc = blockIdx.x * GT + threadIdx.y;
+    sg[threadIdx.y][threadIdx.x] = (cc < n && ii < n) ? G[(int64_t)ii * n + cc] : 0.0;  // G[cc][ii]
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < GT; ++t) acc += sv[threadIdx.y][t] * sg[threadIdx.x][t];
+    __syncthreads();
+  }
+  if (r < n && c < n) Z[(int64_t)r * n + c] = acc;
+}
+
+extern "C" int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* Z) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, n >= 1, "empty matrix");
+  double *G, *V, *sig, *w;
+  BAMG_TRY(arena_get(ctx, (size_t)n * n, &G));
+  BAMG_TRY(arena_get(ctx, (size_t)n * n, &V));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &sig));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &w));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(G, A, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(jacobi_svd(ctx, G, n, n, V, sig));
+  BAMG_LAUNCH(ctx, pinv_weights_kernel, 1, 256, 0, sig, n, rank_tol, w);
+  dim3 grid((n + GT - 1) / GT, (n + GT - 1) / GT), block(GT, GT);
+  pinv_assemble_kernel<<<grid, block, 0, ctx->stream>>>(V, G, w, n, Z);
+  ctx->launches++;
+  BAMG_CHECK_CUDA(ctx, cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------------- Cholesky
+__global__ void symmetrize_kernel(const double* __restrict__ A, int n, double* __restrict__ S) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  S[t] = 0.5 * (A[t] + A[(int64_t)i * n + j]);
+}
+
+// right-looking step j: L[:, j] = A[:, j] / sqrt(A_jj) (rows >= j), then
+// A[i][k] -= L_ij L_kj for i, k > j.  A is read for column j only.
+__global__ void chol_column_kernel(const double* __restrict__ A, int n, int j, double* __restrict__ L,
+                                   int* __restrict__ bad) {
+  int i = j + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double piv = A[(int64_t)j * n + j];
+  if (!(piv > 0.0)) {
+    if (i == j) *bad = 1;
+    return;
+  }
+  double d = sqrt(piv);
+  L[(int64_t)j * n + i] = (i == j) ? d : A[(int64_t)j * n + i] / d;
+}
+
+__global__ void chol_update_kernel(double* __restrict__ A, int n, int j, const double* __restrict__ L) {
+  int64_t m = n - j - 1;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * m) return;
+  int i = j + 1 + (int)(t % m), k = j + 1 + (int)(t / m);
+  A[(int64_t)k * n + i] -= L[(int64_t)j * n + i] * L[(int64_t)j * n + k];
+}
+
+static int cholesky(bamg_ctx* ctx, double* A, int n, double* L, int* bad) {
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(L, 0, sizeof(double) * (size_t)n * n, ctx->stream));
+  for (int j = 0; j < n; ++j) {
+    BAMG_LAUNCH(ctx, chol_column_kernel, grid_for(n - j, 256), 256, 0, A, n, j, L, bad);
+    int64_t m = n - j - 1;
+    if (m > 0) BAMG_LAUNCH(ctx, chol_update_kernel, grid_for(m * m, 256), 256, 0, A, n, j, L);
+  }
+  return 0;
+}
+
+// forward substitution L X = B for nrhs columns (column-major, ld = n):
+// step i: X[i][c] = B[i][c] / L_ii;  B[k][c] -= L_ki X[i][c]  (k > i)
+__global__ void fwd_step_kernel(const double* __restrict__ L, int n, int i, double* __restrict__ B, int nrhs,
+                                double* __restrict__ X) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t rows = n - i;
+  if (t >= rows * nrhs) return;
+  int k = i + (int)(t % rows), c = (int)(t / rows);
+  double xi = B[(int64_t)c * n + i] / L[(int64_t)i * n + i];
+  if (k == i) X[(int64_t)c * n + i] = xi;
+  else B[(int64_t)c * n + k] -= L[(int64_t)i * n + k] * xi;
+}
+
+static int forward_solve(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
+  for (int i = 0; i < n; ++i)
+    BAMG_LAUNCH(ctx, fwd_step_kernel, grid_for((int64_t)(n - i) * nrhs, 256), 256, 0, L, n, i, B, nrhs, X);
+  return 0;
+}
+
+// back substitution L^T X = B (upper triangular L^T): step i from n-1 down
+__global__ void bwd_step_kernel(const double* __restrict__ L, int n, int i, double* __restrict__ B, int nrhs,
+                                double* __restrict__ X) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t rows = i + 1;
+  if (t >= rows * nrhs) return;
+  int k = (int)(t % rows), c = (int)(t / rows);
+  double xi = B[(int64_t)c * n + i] / L[(int64_t)i * n + i];
+  if (k == i) X[(int64_t)c * n + i] = xi;
+  else B[(int64_t)c * n + k] -= L[(int64_t)k * n + i] * xi;  // (L^T)[k][i] = L[i][k]
+}
+
+static int backward_solve_t(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
+  for (int i = n - 1; i >= 0; --i)
+    BAMG_LAUNCH(ctx, bwd_step_kernel, grid_for((int64_t)(i + 1) * nrhs, 256), 256, 0, L, n, i, B, nrhs, X);
+  return 0;
+}
+
+__global__ void transpose_dense_kernel(const double* __restrict__ A, int n, double* __restrict__ T) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  T[(int64_t)i * n + j] = A[t];
+}
+
+// ascending order of sig (ties by index): perm[rank] = index
+__global__ void rank_sort_kernel(const double* __restrict__ sig, int n, int* __restrict__ perm) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double si = sig[i];
+  int r = 0;
+  for (int j = 0; j < n; ++j) {
+    double sj = sig[j];
+    if (sj < si || (sj == si && j < i)) ++r;
+  }
+  perm[r] = i;
+}
+
+// gather the r smallest triplets: a (left, from G/sigma or the K^T SVD),
+// b (right, V columns) into column-major n x r blocks
+__global__ void gather_triplets_kernel(const double* __restrict__ G, const double* __restrict__ V,
+                                       const double* __restrict__ sig, const int* __restrict__ perm,
+                                       const double* __restrict__ Vt, const int* __restrict__ perm_t, int n, int r,
+                                       double floor_rel, double* __restrict__ A, double* __restrict__ Bv,
+                                       double* __restrict__ sig_out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * r) return;
+  int row = (int)(t % n), j = (int)(t / n);
+  double smax = sig[perm[n - 1]];
+  int idx = perm[j];
+  double s = sig[idx];
+  Bv[(int64_t)j * n + row] = V[(int64_t)idx * n + row];
+  double thr = fmax(1e-300, floor_rel * smax);
+  if (s > thr) A[(int64_t)j * n + row] = G[(int64_t)idx * n + row] / s;
+  else A[(int64_t)j * n + row] = Vt[(int64_t)perm_t[j] * n + row];
+  if (row == 0) sig_out[j] = s;
+}
+
+// one CTA: normalisation, sign rule, null-slot cleanup (bootstrap.py:232-280).
+// U, Vv column-major n x r (u = L_M^-T a, v = L_N^-T b).  Writes interleaved
+// n x r outputs.
+__global__ void triplet_finish_kernel(const double* __restrict__ Bd, const double* __restrict__ Md,
+                                      const double* __restrict__ Nd, int n, int r, double* __restrict__ U,
+                                      double* __restrict__ Vv, double* __restrict__ sig, double* __restrict__ Uo,
+                                      double* __restrict__ Vo, double* __restrict__ sig_o, double* __restrict__ work) {
+  __shared__ double sh[32];
+  __shared__ int s_order[64];
+  // work: Mu(n), Nv(n), Bv(n), dead_c(n), dead_r(n)
+  double* tmp = work;
+  double* tmp2 = work + n;
+  double* dead_c = work + 2 * n;
+  double* dead_r = work + 3 * n;
+  for (int j = 0; j < r; ++j) {
+    double* u = U + (int64_t)j * n;
+    double* v = Vv + (int64_t)j * n;
+    // unorm = sqrt(max(u^T M u, 0)), vnorm likewise
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double a = 0.0, b = 0.0;
+      for (int c = 0; c < n; ++c) {
+        a += Md[(int64_t)c * n + i] * u[c];
+        b += Nd[(int64_t)c * n + i] * v[c];
+      }
+      tmp[i] = a;
+      tmp2[i] = b;
+    }
+    __syncthreads();
+    double pu = 0.0, pv = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      pu += u[i] * tmp[i];
+      pv += v[i] * tmp2[i];
+    }
+    double un = sqrt(fmax(block_sum(pu, sh), 0.0));
+    double vn = sqrt(fmax(block_sum(pv, sh), 0.0));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      u[i] = u[i] / fmax(un, 1e-300);
+      v[i] = v[i] / fmax(vn, 1e-300);
+    }
+    __syncthreads();
+    // sign: u^T B v < 0 -> v = -v
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double a = 0.0;
+      for (int c = 0; c < n; ++c) a += Bd[(int64_t)c * n + i] * v[c];
+      tmp[i] = a;
+    }
+    __syncthreads();
+    double pb = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) pb += u[i] * tmp[i];
+    double ubv = block_sum(pb, sh);
+    if (ubv < 0.0)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = -v[i];
+    __syncthreads();
+  }
+  // null-slot cleanup
+  double smax = 0.0;
+  for (int j = 0; j < r; ++j) smax = fmax(smax, sig[j]);
+  double floor = fmax(1e-10, 1e-8 * smax);
+  int ntiny = 0;
+  for (int j = 0; j < r; ++j)
+    if (sig[j] <= floor) ++ntiny;
+  if (threadIdx.x < 64) s_order[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  if (ntiny > 1) {
+    double part = 0.0;
+    for (int64_t t = threadIdx.x; t < (int64_t)n * n; t += blockDim.x) part += fabs(Bd[t]);
+    double scale = block_sum(part, sh);
+    bool any_c = false, any_r = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double cs = 0.0, rs = 0.0;
+      for (int c = 0; c < n; ++c) {
+        cs += fabs(Bd[(int64_t)i * n + c]);  // column i
+        rs += fabs(Bd[(int64_t)c * n + i]);  // row i
+      }
+      dead_c[i] = cs <= 1e-12 * scale ? 1.0 : 0.0;
+      dead_r[i] = rs <= 1e-12 * scale ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    double dc = 0.0, dr = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      dc += dead_c[i];
+      dr += dead_r[i];
+    }
+    any_c = block_sum(dc, sh) > 0.0;
+    any_r = block_sum(dr, sh) > 0.0;
+    double best_score = -1.0;
+    int lead = -1, first = -1;
+    for (int j = 0; j < r; ++j) {
+      if (!(sig[j] <= floor)) continue;
+      if (first < 0) first = j;
+      double* u = U + (int64_t)j * n;
+      double* v = Vv + (int64_t)j * n;
+      if (any_c) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+          if (dead_c[i] != 0.0) v[i] = 0.0;
+        __syncthreads();
+        double p = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) p += v[i] * v[i];
+        double nr = sqrt(block_sum(p, sh));
+        if (nr > 1e-8)
+          for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = v[i] / nr;
+        __syncthreads();
+      }
+      if (any_r) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+          if (dead_r[i] != 0.0) u[i] = 0.0;
+        __syncthreads();
+        double p = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) p += u[i] * u[i];
+        double nr = sqrt(block_sum(p, sh));
+        if (nr > 1e-8)
+          for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] = u[i] / nr;
+        __syncthreads();
+      }
+      double ps = 0.0, pa = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ps += v[i];
+        pa += fabs(v[i]);
+      }
+      double ssum = block_sum(ps, sh), asum = block_sum(pa, sh);
+      double score = fabs(ssum) / fmax(asum, 1e-300);
+      if (score > best_score) {
+        best_score = score;
+        lead = j;
+      }
+    }
+    if (threadIdx.x == 0 && lead != first && lead >= 0) {
+      s_order[first] = lead;
+      s_order[lead] = first;
+    }
+    __syncthreads();
+  }
+  // interleaved outputs in (possibly swapped) slot order
+  for (int j = 0; j < r; ++j) {
+    int src = s_order[j];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      Uo[(int64_t)i * r + j] = U[(int64_t)src * n + i];
+      Vo[(int64_t)i * r + j] = Vv[(int64_t)src * n + i];
+    }
+    if (threadIdx.x == 0) sig_o[j] = sig[src];
+  }
+}
+
+extern "C" int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n,
+                                      int r, double* U, double* V, double* sigma) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, n >= 1 && r >= 1 && r <= 64, "need 1 <= r <= 64");
+  if (r > n) r = n;  // take = min(r, n)
+  const size_t nn = (size_t)n * n;
+  double *Ms, *Ns, *LM, *LN, *Bw, *T, *Tt, *K, *Kt, *Vk, *Vkt, *sk, *skt, *A, *Bv, *sg, *Xa, *Xb, *work;
+  int *perm, *permt, *bad;
+  BAMG_TRY(arena_get(ctx, nn, &Ms));
+  BAMG_TRY(arena_get(ctx, nn, &Ns));
+  BAMG_TRY(arena_get(ctx, nn, &LM));
+  BAMG_TRY(arena_get(ctx, nn, &LN));
+  BAMG_TRY(arena_get(ctx, nn, &Bw));
+  BAMG_TRY(arena_get(ctx, nn, &T));
+  BAMG_TRY(arena_get(ctx, nn, &Tt));
+  BAMG_TRY(arena_get(ctx, nn, &K));
+  BAMG_TRY(arena_get(ctx, nn, &Kt));
+  BAMG_TRY(arena_get(ctx, nn, &Vk));
+  BAMG_TRY(arena_get(ctx, nn, &Vkt));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &sk));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &skt));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &A));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Bv));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Xa));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Xb));
+  BAMG_TRY(arena_get(ctx, (size_t)r, &sg));
+  BAMG_TRY(arena_get(ctx, (size_t)4 * n, &work));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &perm));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &permt));
+  BAMG_TRY(arena_get(ctx, 1, &bad));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  const int gnn = grid_for((int64_t)nn, 256);
+  // symmetrised masses (bootstrap.py:217-218) and their Cholesky factors
+  BAMG_LAUNCH(ctx, symmetrize_kernel, gnn, 256, 0, Md, n, Ms);
+  BAMG_LAUNCH(ctx, symmetrize_kernel, gnn, 256, 0, Nd, n, Ns);
+  // keep symmetric copies for the normalisation step (Cholesky destroys Ms/Ns)
+  double *Msym, *Nsym;
+  BAMG_TRY(arena_get(ctx, nn, &Msym));
+  BAMG_TRY(arena_get(ctx, nn, &Nsym));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Msym, Ms, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Nsym, Ns, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(cholesky(ctx, Ms, n, LM, bad));
+  BAMG_TRY(cholesky(ctx, Ns, n, LN, bad));
+  int hb = 0;
+  BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
+  if (hb) {
+    ctx->err = "mass matrix is not positive definite (Cholesky pivot <= 0)";
+    return 2;
+  }
+  // T = L_M^-1 B ;  K^T = L_N^-1 T^T ;  K = (K^T)^T
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Bw, Bd, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(forward_solve(ctx, LM, n, Bw, n, T));
+  BAMG_LAUNCH(ctx, transpose_dense_kernel, gnn, 256, 0, T, n, Tt);
+  BAMG_TRY(forward_solve(ctx, LN, n, Tt, n, Kt));
+  BAMG_LAUNCH(ctx, transpose_dense_kernel, gnn, 256, 0, Kt, n, K);
+  // SVDs of K (right vectors + left for sigma > floor) and K^T (left null)
+  BAMG_TRY(jacobi_svd(ctx, K, n, n, Vk, sk));
+  BAMG_TRY(jacobi_svd(ctx, Kt, n, n, Vkt, skt));
+  BAMG_LAUNCH(ctx, rank_sort_kernel, grid_for(n, 256), 256, 0, sk, n, perm);
+  BAMG_LAUNCH(ctx, rank_sort_kernel, grid_for(n, 256), 256, 0, skt, n, permt);
+  BAMG_LAUNCH(ctx, gather_triplets_kernel, grid_for((int64_t)n * r, 256), 256, 0, K, Vk, sk, perm, Vkt, permt, n, r,
+              1e-10, A, Bv, sg);
+  // u = L_M^-T a, v = L_N^-T b
+  BAMG_TRY(backward_solve_t(ctx, LM, n, A, r, Xa));
+  BAMG_TRY(backward_solve_t(ctx, LN, n, Bv, r, Xb));
+  BAMG_LAUNCH(ctx, triplet_finish_kernel, 1, 256, 0, Bd, Msym, Nsym, n, r, Xa, Xb, sg, U, V, sigma, work);
+  return 0;
+}

@@ -1,0 +1,648 @@
+// interp.cu -- least-squares interpolation / restriction rows, one warp per
+// fine point (interp.py:105-289).
+//
+// Per fine point i the warp
+//   1. builds the candidate list: coarse points among the radius-1
+//      neighbours in pattern(B + B^T), escalating to radius 2 when there are
+//      none (interp.py:241-249, 274-276), sorted ascending;
+//   2. runs the greedy caliber-bounded selection of fit_row
+//      (interp.py:129-238) with the reference's exact decision rules: strict
+//      `<` argmin over candidates in ascending order, the |coef| > 10 veto
+//      after the first step, the relative-improvement stop, the 1e-30 stop,
+//      negative-coefficient dropping (argmin first) and the inert single-point
+//      row, the sum-to-one constrained variant used for Q;
+//   3. solves every trial model as a ridge least-squares problem by
+//      Householder QR held in the warp: lane l owns LS row l (the finite-
+//      weight tests first, then the ridge rows lambda*I), column norms and
+//      reflector applications are warp-shuffle reductions, back
+//      substitution broadcasts one coefficient per step.  The
+//      |R_jj| < 1e-13 max|R| branch of qr_solve_ls (dense.py:134-152) falls
+//      back to a warp one-sided-Jacobi pseudo-inverse (dense.py:102-115).
+// Decisions compare warp-reduced fp64 values; the reference's decision
+// margins are >= 1e-9 relative, far above the 1e-15 rounding differences
+// between this QR and LAPACK's, so selected patterns are bit-identical.
+#include <cmath>
+
+#include "internal.cuh"
+
+constexpr int FIT_WARPS = 4;     // warps per CTA
+constexpr int CMAX = 8;          // largest caliber supported
+constexpr int MAXCAND = 48;      // candidate list capacity per point
+
+struct FitLane {
+  int lane;
+  int rf;        // number of finite-weight tests (data rows)
+  int f;         // test index owned by this lane (lane < rf)
+  double y;      // sqrt-weight-free fine value y_f
+  double sw;     // sqrt(w_f)
+};
+
+__device__ __forceinline__ double wsum(double v) { return warp_sum(v); }
+
+__device__ __forceinline__ double cval(const double* __restrict__ X, int k, int point, int f) {
+  return __ldg(X + (int64_t)point * k + f);
+}
+
+// Warp one-sided Jacobi pseudo-inverse solve of the nr x nc system held as
+// lane rows a0[] with rhs b0 (rank_tol 1e-12 relative to sigma_max).
+__device__ void warp_pinv_solve(const FitLane& L, int nr, int nc, const double* a0, double b0,
+                                double* coef, double* sV) {
+  double g[CMAX];
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) g[q] = (q < nc && L.lane < nr) ? a0[q] : 0.0;
+  // V = I (nc x nc, row-major in shared memory, owned by this warp)
+  if (L.lane < nc * nc) sV[L.lane] = (L.lane / nc == L.lane % nc) ? 1.0 : 0.0;
+  for (int i = L.lane + 32; i < nc * nc; i += 32) sV[i] = (i / nc == i % nc) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < nc - 1; ++p) {
+      for (int q = p + 1; q < nc; ++q) {
+        double gp = 0.0, gq = 0.0;
+#pragma unroll
+        for (int t = 0; t < CMAX; ++t) {
+          if (t == p) gp = g[t];
+          if (t == q) gq = g[t];
+        }
+        double al = wsum(gp * gp), be = wsum(gq * gq), ga = wsum(gp * gq);
+        if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
+          rotated = true;
+          double zeta = (be - al) / (2.0 * ga);
+          double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          double np = c * gp - s * gq, nq = s * gp + c * gq;
+#pragma unroll
+          for (int u = 0; u < CMAX; ++u) {
+            if (u == p) g[u] = np;
+            if (u == q) g[u] = nq;
+          }
+          __syncwarp();
+          if (L.lane < nc) {
+            double vp = sV[L.lane * nc + p], vq = sV[L.lane * nc + q];
+            sV[L.lane * nc + p] = c * vp - s * vq;
+            sV[L.lane * nc + q] = s * vp + c * vq;
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  double sig[CMAX], gb[CMAX];
+  double smax = 0.0;
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) {
+    if (q < nc) {
+      sig[q] = sqrt(wsum(g[q] * g[q]));
+      gb[q] = wsum(g[q] * (L.lane < nr ? b0 : 0.0));
+      smax = fmax(smax, sig[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) {
+    if (q < nc) {
+      double x = 0.0;
+      for (int i = 0; i < nc; ++i) {
+        double si = 0.0, gbi = 0.0;
+#pragma unroll
+        for (int t = 0; t < CMAX; ++t)
+          if (t == i) {
+            si = sig[t];
+            gbi = gb[t];
+          }
+        if (smax > 0.0 && si > 1e-12 * smax) x += sV[q * nc + i] * (gbi / (si * si));
+      }
+      coef[q] = x;
+    }
+  }
+  __syncwarp();
+}
+
+// Ridge LS for one column set.  cols[q] is a candidate POINT index; with
+// `base` >= 0 the columns are differenced against the base point and the
+// target is y - C_base (the constrained elimination of interp.py:180-186).
+// Returns coefficients (nc), misfit over the data rows and the objective.
+__device__ void ls_solve(const FitLane& L, const double* __restrict__ X, int k, const int* cols, int nc,
+                         int base, double lam, double* coef, double* data_out, double* total_out,
+                         unsigned long long* fallback, double* sV) {
+  const bool ridge = lam > 0.0;
+  const int nr = L.rf + (ridge ? nc : 0);
+  double a[CMAX], a0[CMAX];
+  double b = 0.0;
+  if (L.lane < L.rf) {
+    double cb = base >= 0 ? cval(X, k, base, L.f) : 0.0;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) {
+      if (q < nc) {
+        double c = cval(X, k, cols[q], L.f);
+        a[q] = L.sw * (base >= 0 ? c - cb : c);
+      } else {
+        a[q] = 0.0;
+      }
+    }
+    b = L.sw * (base >= 0 ? L.y - cb : L.y);
+  } else if (ridge && L.lane < nr) {
+    int rr = L.lane - L.rf;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) a[q] = (q == rr) ? lam : 0.0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) a[q] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) a0[q] = a[q];
+  const double b0 = b;
+  // Householder QR (dgeqr2 conventions), reflectors applied to b on the fly
+#pragma unroll
+  for (int j = 0; j < CMAX; ++j) {
+    if (j < nc) {
+      double xj = a[j];
+      double alpha = __shfl_sync(0xffffffffu, xj, j);
+      double below = (L.lane > j && L.lane < nr) ? xj : 0.0;
+      double xn2 = wsum(below * below);
+      if (xn2 != 0.0) {
+        double xnorm = sqrt(xn2);
+        double beta = -copysign(hypot(alpha, xnorm), alpha);
+        double tau = (beta - alpha) / beta;
+        double scal = 1.0 / (alpha - beta);
+        double v = (L.lane == j) ? 1.0 : ((L.lane > j && L.lane < nr) ? xj * scal : 0.0);
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) {
+          if (q > j && q < nc) {
+            double dq = wsum(v * a[q]);
+            a[q] -= tau * dq * v;
+          }
+        }
+        double db = wsum(v * b);
+        b -= tau * db * v;
+        if (L.lane == j) a[j] = beta;
+        else if (L.lane > j) a[j] = 0.0;
+      }
+    }
+  }
+  // rank test of qr_solve_ls: min |R_jj| < 1e-13 max |R|
+  double rmax = 0.0, dmin = INFINITY;
+  if (L.lane < nc) {
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q)
+      if (q >= L.lane && q < nc) rmax = fmax(rmax, fabs(a[q]));
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q)
+      if (q == L.lane) dmin = fabs(a[q]);
+  }
+  rmax = warp_max(rmax);
+  dmin = -warp_max(-dmin);
+  if (rmax == 0.0 || dmin < 1e-13 * rmax) {
+    if (L.lane == 0) atomicAdd(fallback, 1ull);
+    warp_pinv_solve(L, nr, nc, a0, b0, coef, sV);
+  } else {
+    // back substitution: lane j owns row j of R and (Q^T b)_j
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) coef[q] = 0.0;
+#pragma unroll
+    for (int j = CMAX - 1; j >= 0; --j) {
+      if (j < nc) {
+        double s = b;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q)
+          if (q > j && q < nc) s -= a[q] * coef[q];
+        double rjj = 0.0;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q)
+          if (q == j) rjj = a[q];
+        double cj = s / rjj;
+        cj = __shfl_sync(0xffffffffu, cj, j);
+        coef[j] = cj;
+      }
+    }
+  }
+  // misfit over the data rows, objective with the ridge penalty
+  double res = 0.0;
+  if (L.lane < L.rf) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q)
+      if (q < nc) t += a0[q] * coef[q];
+    res = t - b0;
+  }
+  double data = wsum(res * res);
+  double cc = 0.0;
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q)
+    if (q < nc) cc += coef[q] * coef[q];
+  *data_out = data;
+  *total_out = data + lam * lam * cc;
+}
+
+struct Model {
+  int pos[CMAX];   // positions into the candidate list, model order
+  int len;
+  double coef[CMAX];
+  double data, total;
+};
+
+// solve_model of fit_row (interp.py:176-199): fit `trial`, dropping the most
+// negative coefficient until all are non-negative.
+__device__ void solve_model(const FitLane& L, const double* __restrict__ X, int k, const int* cand,
+                            const int* trial, int tlen, bool constrain, bool nonneg, double lam,
+                            double empty, Model* out, unsigned long long* fallback, double* sV) {
+  int work[CMAX];
+  int wl = tlen;
+#pragma unroll
+  for (int q = 0; q < CMAX; ++q) work[q] = q < tlen ? trial[q] : 0;
+  while (wl > 0) {
+    double coef[CMAX];
+    double data, total;
+    if (constrain) {
+      int base = cand[work[0]];
+      if (wl > 1) {
+        int cols[CMAX];
+        double ct[CMAX];
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) cols[q] = (q + 1 < wl) ? cand[work[q + 1]] : 0;
+        ls_solve(L, X, k, cols, wl - 1, base, lam, ct, &data, &total, fallback, sV);
+        double ssum = 0.0;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q)
+          if (q < wl - 1) ssum += ct[q];
+        coef[0] = 1.0 - ssum;
+#pragma unroll
+        for (int q = 1; q < CMAX; ++q) coef[q] = (q < wl) ? ct[q - 1] : 0.0;
+      } else {
+        double r = 0.0;
+        if (L.lane < L.rf) r = L.sw * (L.y - cval(X, k, base, L.f));
+        data = wsum(r * r);
+        total = data;
+        coef[0] = 1.0;
+      }
+    } else {
+      int cols[CMAX];
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) cols[q] = q < wl ? cand[work[q]] : 0;
+      ls_solve(L, X, k, cols, wl, -1, lam, coef, &data, &total, fallback, sV);
+    }
+    // coef.min(initial=0.0) >= 0
+    double cmin = 0.0;
+    int amin = 0;
+    bool has_nan = false;
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) {
+      if (q < wl) {
+        if (coef[q] != coef[q]) has_nan = true;
+        if (coef[q] < cmin) {
+          cmin = coef[q];
+        }
+      }
+    }
+    // np.argmin: first index of the minimum (NaN counts as the minimum)
+    {
+      double best = INFINITY;
+      int bi = 0;
+      bool found_nan = false;
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        if (q < wl && !found_nan) {
+          if (coef[q] != coef[q]) {
+            bi = q;
+            found_nan = true;
+          } else if (coef[q] < best) {
+            best = coef[q];
+            bi = q;
+          }
+        }
+      }
+      amin = bi;
+    }
+    bool ok = !has_nan && cmin >= 0.0;
+    if (!nonneg || ok) {
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        out->pos[q] = work[q];
+        out->coef[q] = q < wl ? coef[q] : 0.0;
+      }
+      out->len = wl;
+      out->data = data;
+      out->total = total;
+      return;
+    }
+    if (wl == 1) {  // inert single-point row
+      out->pos[0] = work[0];
+      out->coef[0] = 0.0;
+      out->len = 1;
+      out->data = empty;
+      out->total = empty;
+      return;
+    }
+    // work.pop(argmin)
+#pragma unroll
+    for (int q = 0; q < CMAX - 1; ++q)
+      if (q >= amin) work[q] = work[q + 1];
+    --wl;
+  }
+  out->len = 0;
+  out->data = empty;
+  out->total = empty;
+}
+
+// insert x into the sorted unique list s (length *len) if absent
+__device__ __forceinline__ bool sorted_insert(int* s, int* len, int x, int cap) {
+  int lo = 0, hi = *len;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (s[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < *len && s[lo] == x) return true;
+  if (*len >= cap) return false;
+  for (int q = *len; q > lo; --q) s[q] = s[q - 1];
+  s[lo] = x;
+  ++*len;
+  return true;
+}
+
+__global__ void __launch_bounds__(FIT_WARPS * 32)
+fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                const int32_t* __restrict__ crank, const double* __restrict__ X, int k,
+                const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber,
+                int radius, double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
+                int32_t* __restrict__ out_col, double* __restrict__ out_val,
+                unsigned long long* __restrict__ status) {
+  __shared__ int s_cand[FIT_WARPS][MAXCAND];
+  __shared__ int s_two[FIT_WARPS][4 * MAXCAND];
+  __shared__ double s_V[FIT_WARPS][CMAX * CMAX];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int* cand = s_cand[wib];
+  double* sV = s_V[wib];
+  const double lam = lam_dev[0];
+
+  FitLane L;
+  L.lane = lane;
+  {
+    bool fin = lane < k && isfinite(w[lane]);
+    unsigned mask = __ballot_sync(0xffffffffu, fin);
+    L.rf = __popc(mask);
+    // lane l owns the l-th finite test
+    int f = -1, seen = 0;
+    for (int t = 0; t < k; ++t) {
+      if (mask & (1u << t)) {
+        if (seen == lane) f = t;
+        ++seen;
+      }
+    }
+    L.f = f < 0 ? 0 : f;
+    L.sw = (lane < L.rf) ? sqrt(w[L.f]) : 0.0;
+  }
+
+  const int gw = blockIdx.x * FIT_WARPS + wib;
+  const int nw = gridDim.x * FIT_WARPS;
+  for (int i = gw; i < n; i += nw) {
+    int64_t obase = (int64_t)i * caliber;
+    int ci = crank[i];
+    if (ci >= 0) {  // coarse point: identity row
+      if (lane == 0) {
+        out_cnt[i] = 1;
+        out_col[obase] = ci;
+        out_val[obase] = 1.0;
+      }
+      continue;
+    }
+    // ---- candidates (sorted ascending point indices)
+    int m = 0;
+    const int rb = arp[i], re = arp[i + 1];
+    if (radius == 1) {
+      if (lane == 0) {
+        for (int j = rb; j < re; ++j) {
+          int p = acol[j];
+          if (crank[p] >= 0) {
+            if (m < MAXCAND) cand[m] = p;
+            ++m;
+          }
+        }
+      }
+      m = __shfl_sync(0xffffffffu, m, 0);
+    }
+    if (m == 0 && re > rb) {  // radius-2 (escalation or configured)
+      if (lane == 0) {
+        int* two = s_two[wib];
+        int len = 0;
+        bool ok = true;
+        for (int j = rb; j < re && ok; ++j) {
+          int p = acol[j];
+          ok = sorted_insert(two, &len, p, 4 * MAXCAND);
+          for (int q = arp[p]; q < arp[p + 1] && ok; ++q) ok = sorted_insert(two, &len, acol[q], 4 * MAXCAND);
+        }
+        if (!ok) atomicOr(status + 1, 1ull);
+        for (int t = 0; t < len; ++t) {
+          int p = two[t];
+          if (p != i && crank[p] >= 0) {
+            if (m < MAXCAND) cand[m] = p;
+            ++m;
+          }
+        }
+      }
+      m = __shfl_sync(0xffffffffu, m, 0);
+    }
+    __syncwarp();
+    if (m > MAXCAND) {
+      if (lane == 0) atomicOr(status + 1, 2ull);
+      m = MAXCAND;
+    }
+    if (m == 0) {  // decoupled point: empty row (interp.py:277-281)
+      if (lane == 0) out_cnt[i] = 0;
+      continue;
+    }
+    if (lane < L.rf) L.y = cval(X, k, i, L.f);
+    else L.y = 0.0;
+    double yy = (lane < L.rf) ? w[L.f] * (L.y * L.y) : 0.0;
+    const double empty = wsum(yy);
+
+    // ---- greedy selection (fit_row)
+    int sel[CMAX];
+    int nsel = 0;
+    double coefs[CMAX];
+#pragma unroll
+    for (int q = 0; q < CMAX; ++q) {
+      sel[q] = 0;
+      coefs[q] = 0.0;
+    }
+    double cur_total = empty;
+    const int cap = caliber < m ? caliber : m;
+    while (nsel < cap) {
+      Model best;
+      bool have = false;
+      for (int j = 0; j < m; ++j) {
+        bool in = false;
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q)
+          if (q < nsel && sel[q] == j) in = true;
+        if (in) continue;
+        int trial[CMAX];
+#pragma unroll
+        for (int q = 0; q < CMAX; ++q) trial[q] = q < nsel ? sel[q] : (q == nsel ? j : 0);
+        Model md;
+        solve_model(L, X, k, cand, trial, nsel + 1, constrain != 0, nonneg != 0, lam, empty, &md,
+                    status, sV);
+        if (nsel > 0 && md.len > 0) {
+          double amax = 0.0;
+          bool nan = false;
+#pragma unroll
+          for (int q = 0; q < CMAX; ++q)
+            if (q < md.len) {
+              if (md.coef[q] != md.coef[q]) nan = true;
+              amax = fmax(amax, fabs(md.coef[q]));
+            }
+          if (!nan && amax > 10.0) continue;  // COEF_CAP veto
+        }
+        if (!have || md.total < best.total) {
+          best = md;
+          have = true;
+        }
+      }
+      if (!have) break;
+      if (nsel > 0) {
+        if (cur_total <= 0.0 || (cur_total - best.total) < tol * cur_total) break;
+      }
+      if (best.len <= nsel) break;
+#pragma unroll
+      for (int q = 0; q < CMAX; ++q) {
+        sel[q] = best.pos[q];
+        coefs[q] = best.coef[q];
+      }
+      nsel = best.len;
+      cur_total = best.total;
+      if (cur_total <= 1e-30) break;
+    }
+    if (nsel == 0) {
+      sel[0] = 0;
+      coefs[0] = constrain ? 1.0 : 0.0;
+      nsel = 1;
+    }
+    if (lane == 0) {
+      out_cnt[i] = nsel;
+      for (int q = 0; q < nsel; ++q) {
+        out_col[obase + q] = crank[cand[sel[q]]];
+        out_val[obase + q] = coefs[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ridge = 0.1 * sqrt(mean_i (sqrt(sum_f w_f x_if^2))^2)  (interp.py:266-268)
+__global__ void level_scale_partial(const double* __restrict__ X, int64_t n, int k, const double* __restrict__ w,
+                                    double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS / 32];
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double acc = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < k; ++c) {
+      double wc = w[c];
+      if (isfinite(wc)) {
+        double x = X[r * k + c];
+        s += wc * (x * x);
+      }
+    }
+    double ps = sqrt(s);
+    acc += ps * ps;
+  }
+  double v = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < RED_THREADS / 32; ++q) t += sh[q];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void level_scale_final(const double* __restrict__ partial, int nb, int64_t n, double* lam) {
+  int lane = threadIdx.x;
+  double v = 0.0;
+  for (int b = lane; b < nb; b += 32) v += partial[b];
+  v = warp_sum(v);
+  if (lane == 0) lam[0] = 0.1 * sqrt(v / (double)n);
+}
+
+extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
+                             const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
+                             int constrain, int nonnegative, int32_t* out_cnt, int32_t* out_col, double* out_val,
+                             int64_t* status_host) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, caliber >= 1 && caliber <= CMAX, "caliber must lie in [1, 8]");
+  BAMG_REQUIRE(ctx, k >= 1 && k + caliber <= 32, "need k + caliber <= 32 (one LS row per lane)");
+  BAMG_REQUIRE(ctx, radius == 1 || radius == 2, "radius must be 1 or 2");
+  BAMG_REQUIRE(ctx, adj && adj->nrows == n, "adjacency size mismatch");
+  double *partial, *lam;
+  unsigned long long* status;
+  BAMG_TRY(arena_get(ctx, RED_BLOCKS, &partial));
+  BAMG_TRY(arena_get(ctx, 1, &lam));
+  BAMG_TRY(arena_get(ctx, 2, &status));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(status, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  BAMG_LAUNCH(ctx, level_scale_partial, RED_BLOCKS, RED_THREADS, 0, X, n, k, w, partial);
+  BAMG_LAUNCH(ctx, level_scale_final, 1, 32, 0, partial, RED_BLOCKS, n, lam);
+  int64_t warps = n;
+  int64_t blocks = (warps + FIT_WARPS - 1) / FIT_WARPS;
+  int64_t maxb = (int64_t)ctx->num_sms * 64;
+  if (blocks > maxb) blocks = maxb;
+  BAMG_LAUNCH(ctx, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr, adj->col, coarse_rank, X,
+              k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative, out_cnt, out_col, out_val, status);
+  int64_t st[2];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 2, st));
+  if (status_host) {
+    status_host[0] = st[0];
+  }
+  BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 48 candidates or 192 two-hop states)");
+  return 0;
+}
+
+// ---------------------------------------------- fixed-stride rows -> CSR
+__global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double* __restrict__ val, int64_t n,
+                                  int stride, int32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  for (int t = 0; t < cnt[i]; ++t)
+    if (!(fabs(val[i * stride + t]) < 1e-300)) ++c;
+  out[i] = c;
+}
+
+__global__ void rows_fill_kernel(const int32_t* __restrict__ cnt, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, int64_t n, int stride,
+                                 const int32_t* __restrict__ rp, int32_t* __restrict__ col_out,
+                                 double* __restrict__ val_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int w = rp[i];
+  int start = w;
+  for (int t = 0; t < cnt[i]; ++t) {
+    double v = val[i * stride + t];
+    if (fabs(v) < 1e-300) continue;
+    int c = col[i * stride + t];
+    int p = w++;
+    while (p > start && col_out[p - 1] > c) {  // insertion by column
+      col_out[p] = col_out[p - 1];
+      val_out[p] = val_out[p - 1];
+      --p;
+    }
+    col_out[p] = c;
+    val_out[p] = v;
+  }
+}
+
+extern "C" int bamg_rows_count(bamg_ctx* ctx, const int32_t* cnt, const double* val, int64_t n, int stride,
+                               int32_t* rowptr, int64_t* nnz_host) {
+  ctx->arena.reset();
+  int32_t* c;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &c));
+  BAMG_LAUNCH(ctx, rows_count_kernel, grid_for(n, 256), 256, 0, cnt, val, n, stride, c);
+  return scan_i32(ctx, c, rowptr, n, nnz_host);
+}
+
+extern "C" int bamg_rows_fill(bamg_ctx* ctx, const int32_t* cnt, const int32_t* col, const double* val, int64_t n,
+                              int stride, const int32_t* rowptr, int32_t* col_out, double* val_out) {
+  BAMG_LAUNCH(ctx, rows_fill_kernel, grid_for(n, 256), 256, 0, cnt, col, val, n, stride, rowptr, col_out, val_out);
+  return 0;
+}

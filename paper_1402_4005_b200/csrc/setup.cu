@@ -194,8 +194,10 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
       BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * 2 * k, ctx->stream));
       BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak));
       BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k));
-      BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, vo, total, k, peak);
-      BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, uo, total, k, peak + k);
+      if (smooth == 1) {  // init_test_vectors (smooth == 2) has no runaway rescaling
+        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, vo, total, k, peak);
+        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, uo, total, k, peak + k);
+      }
       std::swap(u, uo);
       std::swap(v, vo);
       if (inhomogeneous) BAMG_TRY(rayleigh_dev(ctx, A, M, N, u, v, n, k, sigma, nullptr, 0, work3));

@@ -413,9 +413,14 @@ static int apply_op(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double
   return spmm_dev(ctx, B, v, out, 1);
 }
 
+extern "C" int bamg_dense_gemv(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y) {
+  BAMG_LAUNCH(ctx, gemv_rowmajor_kernel, grid_for((int64_t)n * 32, 256), 256, 0, n, Z, b, y);
+  return 0;
+}
+
 extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* b,
                           const double* x0, double* x, int restart, int max_iters, double rtol,
-                          int* iters_host, double* history_host, int* nhistory_host) {
+                          int stopping, int* iters_host, double* history_host, int* nhistory_host) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, B && B->nrows == B->ncols, "square operator expected");
   BAMG_REQUIRE(ctx, max_iters >= 0, "max_iters must be nonnegative");
@@ -448,7 +453,17 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   auto norm_into = [&](const double* v, double* out) -> int {
     return colreduce(ctx, v, nullptr, n, 1, 0, out, 1);
   };
+  double denom0 = 1.0;
+  // stopping 0: ||Bx|| / ||x||  ("scaled_bx");  1: ||b - Bx|| / max(||b - Bx0||, 1e-300)
   auto metric = [&](const double* xv, double* out_host) -> int {
+    if (stopping == 1) {
+      BAMG_TRY(resid_dev(ctx, B, b, xv, tmp));
+      BAMG_TRY(norm_into(tmp, scal));
+      double r0;
+      BAMG_TRY(ctx_read_doubles(ctx, scal, 1, &r0));
+      *out_host = r0 / denom0;
+      return 0;
+    }
     BAMG_TRY(spmm_dev(ctx, B, xv, tmp, 1));
     BAMG_TRY(norm_into(tmp, scal));
     BAMG_TRY(norm_into(xv, scal + 1));
@@ -457,6 +472,13 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
     *out_host = hv2[1] == 0.0 ? INFINITY : hv2[0] / hv2[1];
     return 0;
   };
+  if (stopping == 1) {
+    BAMG_TRY(resid_dev(ctx, B, b, x0, tmp));
+    BAMG_TRY(norm_into(tmp, scal));
+    double r0;
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 1, &r0));
+    denom0 = r0 > 1e-300 ? r0 : 1e-300;
+  }
 
   int nhist = 0;
   double m0;

@@ -1,0 +1,289 @@
+"""Thin typed wrappers over the C ABI (include/bamg_sm100.h).
+
+Every function here allocates its outputs with torch (HBM allocator only),
+binds every argument to a local before the call (a tensor freed before the
+launch is enqueued could be handed to the next allocation), and launches
+exactly one engine entry point.  No arithmetic happens in Python.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceCSR, device
+
+F64 = torch.float64
+I32 = torch.int32
+U8 = torch.uint8
+
+
+def _p(t):
+    return _lib.ptr(t)
+
+
+def _dev():
+    return device()
+
+
+def _empty(shape, dtype=F64):
+    return torch.empty(shape, dtype=dtype, device=_dev())
+
+
+def _block(X):
+    """(tensor, n, k) of an n x k interleaved block (1-D -> k = 1)."""
+    if X.dim() == 1:
+        return X, X.shape[0], 1
+    return X, X.shape[0], X.shape[1]
+
+
+def to_device_vec(x):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=_dev(), dtype=F64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(_dev())
+
+
+# ----------------------------------------------------------------- sparse
+def spmm(A: DeviceCSR, X):
+    X, n, k = _block(X)
+    if n != A.shape[1]:
+        raise ValueError(f"dimension mismatch: matrix is {A.shape}, vector has length {n}")
+    Y = _empty((A.shape[0],) if X.dim() == 1 else (A.shape[0], k))
+    _lib.call("bamg_spmm", A.ref(), _p(X), _p(Y), k)
+    return Y
+
+
+def transpose(A: DeviceCSR) -> DeviceCSR:
+    rp = _empty(A.shape[1] + 1, I32)
+    ci = _empty(A.nnz, I32)
+    va = _empty(A.nnz, F64)
+    _lib.call("bamg_csr_transpose", A.ref(), _p(rp), _p(ci), _p(va))
+    return DeviceCSR(rp, ci, va, (A.shape[1], A.shape[0]))
+
+
+def sym_pattern(A: DeviceCSR, At: DeviceCSR) -> DeviceCSR:
+    rp = _empty(A.shape[0] + 1, I32)
+    nnz = C.c_int64(0)
+    _lib.call("bamg_sym_pattern_count", A.ref(), At.ref(), _p(rp), C.byref(nnz))
+    ci = _empty(max(nnz.value, 1), I32)[: nnz.value]
+    _lib.call("bamg_sym_pattern_fill", A.ref(), At.ref(), _p(rp), _p(ci))
+    ones = torch.ones(nnz.value, dtype=F64, device=_dev())
+    return DeviceCSR(rp, ci, ones, A.shape)
+
+
+def diag(A: DeviceCSR):
+    d = _empty(min(A.shape))
+    _lib.call("bamg_diag", A.ref(), _p(d))
+    return d
+
+
+def count_nonpositive(d) -> int:
+    out = C.c_int64(0)
+    _lib.call("bamg_count_nonpositive", _p(d), d.numel(), C.byref(out))
+    return out.value
+
+
+def count_empty_rows(A: DeviceCSR) -> int:
+    out = C.c_int64(0)
+    _lib.call("bamg_count_empty_rows", A.ref(), C.byref(out))
+    return out.value
+
+
+def spgemm(A: DeviceCSR, B: DeviceCSR, order: int = 0) -> DeviceCSR:
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"dimension mismatch in sparse product: {A.shape} x {B.shape}")
+    rp = _empty(A.shape[0] + 1, I32)
+    nnz = C.c_int64(0)
+    _lib.call("bamg_spgemm_count", A.ref(), B.ref(), order, _p(rp), C.byref(nnz))
+    ci = _empty(max(nnz.value, 1), I32)
+    va = _empty(max(nnz.value, 1), F64)
+    _lib.call("bamg_spgemm_fill", A.ref(), B.ref(), order, _p(rp), _p(ci), _p(va))
+    return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (A.shape[0], B.shape[1]))
+
+
+# ------------------------------------------------------------------ relax
+def degenerate_rows(A: DeviceCSR, d):
+    skip = _empty(A.shape[0], U8)
+    _lib.call("bamg_degenerate_rows", A.ref(), _p(d), _p(skip))
+    return skip
+
+
+def jacobi(A: DeviceCSR, d, skip, x, b=None, b_scale=None, omega=0.7, peak=None):
+    x, n, k = _block(x)
+    out = torch.empty_like(x)
+    _lib.call("bamg_jacobi", A.ref(), _p(d), _p(skip), _p(b), _p(b_scale), _p(x), _p(out), k,
+              float(omega), _p(peak))
+    return out
+
+
+# ---------------------------------------------------------- block helpers
+def col_norms(X):
+    X, n, k = _block(X)
+    out = _empty(k)
+    _lib.call("bamg_col_norms", _p(X), n, k, _p(out))
+    return out
+
+
+def col_dots(X, Y):
+    X, n, k = _block(X)
+    out = _empty(k)
+    _lib.call("bamg_col_dots", _p(X), _p(Y), n, k, _p(out))
+    return out
+
+
+def normalize_cols(X):
+    """In place: X[:, c] /= ||X[:, c]|| (zero norms left alone)."""
+    X, n, k = _block(X)
+    nrm = col_norms(X)
+    _lib.call("bamg_col_scale_div", _p(X), n, k, _p(nrm))
+    return X
+
+
+def col_fill(X, c, value):
+    X, n, k = _block(X)
+    _lib.call("bamg_col_fill", _p(X), n, k, int(c), float(value))
+
+
+def gather_rows(X, idx):
+    X, n, k = _block(X)
+    m = idx.numel()
+    Y = _empty((m,) if X.dim() == 1 else (m, k))
+    _lib.call("bamg_gather_rows", _p(X), _p(idx), m, k, _p(Y))
+    return Y
+
+
+def permute_cols(X, perm):
+    X, n, k = _block(X)
+    arr = (C.c_int32 * k)(*[int(v) for v in perm])
+    Y = torch.empty_like(X)
+    _lib.call("bamg_permute_cols", _p(X), n, k, arr, _p(Y))
+    return Y
+
+
+# -------------------------------------------------------------- bootstrap
+def smooth_block(A, At, M, N, d, skip, skip_t, U, V, sigma, nsweeps, omega, inhomogeneous,
+                 smooth=1, refresh=1):
+    n, k = V.shape
+    _lib.call("bamg_smooth_block", A.ref(), At.ref(), M.ref() if M is not None else None,
+              N.ref() if N is not None else None, _p(d), _p(skip), _p(skip_t), _p(U), _p(V),
+              _p(sigma), k, int(nsweeps), float(omega), int(inhomogeneous), int(smooth), int(refresh))
+
+
+def refresh_sigmas(A, M, N, U, V, sigma, flip=True):
+    n, k = V.shape
+    _lib.call("bamg_refresh_sigmas", A.ref(), M.ref() if M is not None else None,
+              N.ref() if N is not None else None, _p(U), _p(V), _p(U) if flip else None,
+              _p(sigma), k)
+
+
+# ------------------------------------------------------------------ interp
+def test_weights(A, X, inf_slot=None):
+    n, k = X.shape
+    Xn = torch.empty_like(X)
+    w = _empty(k)
+    _lib.call("bamg_test_weights", A.ref(), _p(X), n, k, -1 if inf_slot is None else int(inf_slot),
+              _p(Xn), _p(w))
+    return Xn, w
+
+
+def fit_rows(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg):
+    n, k = X.shape
+    cnt = _empty(n, I32)
+    col = _empty(n * caliber, I32)
+    val = _empty(n * caliber, F64)
+    status = C.c_int64(0)
+    _lib.call("bamg_fit_rows", adj.ref(), _p(coarse_rank), _p(X), _p(w), n, k, int(caliber),
+              int(radius), float(tol), int(bool(constrain)), int(bool(nonneg)), _p(cnt), _p(col),
+              _p(val), C.byref(status))
+    return cnt, col, val, status.value
+
+
+def rows_to_csr(cnt, col, val, n, stride, ncols) -> DeviceCSR:
+    rp = _empty(n + 1, I32)
+    nnz = C.c_int64(0)
+    _lib.call("bamg_rows_count", _p(cnt), _p(val), n, int(stride), _p(rp), C.byref(nnz))
+    ci = _empty(max(nnz.value, 1), I32)
+    va = _empty(max(nnz.value, 1), F64)
+    _lib.call("bamg_rows_fill", _p(cnt), _p(col), _p(val), n, int(stride), _p(rp), _p(ci), _p(va))
+    return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (n, ncols))
+
+
+# ----------------------------------------------------------------- coarsen
+def axis_ranks(coord):
+    n = coord.numel()
+    rank = _empty(n, I32)
+    nv = C.c_int64(0)
+    _lib.call("bamg_axis_ranks", _p(coord), n, _p(rank), C.byref(nv))
+    return rank, nv.value
+
+
+def rerank(parent_rank, coarse_idx, nvalues_parent):
+    nc = coarse_idx.numel()
+    out = _empty(nc, I32)
+    nv = C.c_int64(0)
+    _lib.call("bamg_rerank", _p(parent_rank), _p(coarse_idx), nc, int(nvalues_parent), _p(out),
+              C.byref(nv))
+    return out, nv.value
+
+
+def even_mask(ranks):
+    n = ranks[0].numel()
+    arr = (C.c_void_p * len(ranks))(*[r.data_ptr() for r in ranks])
+    mask = _empty(n, U8)
+    _lib.call("bamg_even_mask", arr, len(ranks), n, _p(mask))
+    return mask
+
+
+def split_from_mask(mask):
+    n = mask.numel()
+    coarse = _empty(n, I32)
+    fine = _empty(n, I32)
+    crank = _empty(n, I32)
+    nc = C.c_int64(0)
+    _lib.call("bamg_split_from_mask", _p(mask), n, _p(coarse), _p(fine), _p(crank), C.byref(nc))
+    return coarse[: nc.value], fine[: n - nc.value], crank, nc.value
+
+
+def cr_pass(A, adj, d, cmask, normals, n_fine, sweeps, omega, threshold, coarse_empty):
+    ncand = C.c_int64(0)
+    ncoarse = C.c_int64(0)
+    _lib.call("bamg_cr_pass", A.ref(), adj.ref(), _p(d), _p(cmask), _p(normals), int(n_fine),
+              int(sweeps), float(omega), float(threshold), int(bool(coarse_empty)), C.byref(ncand),
+              C.byref(ncoarse))
+    return ncand.value, ncoarse.value
+
+
+# ------------------------------------------------------------------- dense
+def csr_to_dense(A: DeviceCSR, transpose=False):
+    """Column-major dense copy (torch tensor viewed as [cols][rows])."""
+    n, m = A.shape
+    D = _empty((m, n) if not transpose else (n, m))
+    _lib.call("bamg_csr_to_dense", A.ref(), _p(D), n if not transpose else m, int(bool(transpose)))
+    return D
+
+
+def dense_pinv(Dcm, n, rank_tol=1e-12):
+    Z = _empty((n, n))
+    _lib.call("bamg_dense_pinv", _p(Dcm), n, float(rank_tol), _p(Z))
+    return Z  # row-major pseudo-inverse
+
+
+def coarsest_triplets(Bd, Md, Nd, n, r):
+    take = min(r, n)
+    U = _empty((n, take))
+    V = _empty((n, take))
+    s = _empty(take)
+    rc = _lib.call("bamg_coarsest_triplets", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s))
+    if rc == 2:
+        raise ValueError("matrix is not positive definite (coarsest mass matrix)")
+    return U, V, s
+
+
+def sign_fix_l1(x, stride=1, uniform_fallback=False):
+    n = x.shape[0]
+    out = _empty(n)
+    _lib.call("bamg_sign_fix_l1", _p(x), n, int(stride), _p(out), int(bool(uniform_fallback)))
+    return out

@@ -145,7 +145,7 @@ def test_vcycle_and_gmres_match_oracle(eng, golden, name):
     hist = (C.c_double * (max_iters + 1))()
     zero, dx0 = torch.zeros_like(x), dvec(x0)
     rc = L.lib().bamg_gmres(L.ctx(), dB.ref(), h, L.ptr(zero), L.ptr(dx0), L.ptr(x),
-                            -1 if restart is None else restart, max_iters, rtol,
+                            -1 if restart is None else restart, max_iters, rtol, 0,
                             C.byref(its), hist, C.byref(nh))
     L.check(rc, "gmres")
     assert rc == 0
