@@ -1,0 +1,389 @@
+"""Benchmark: BAMG setup + AMG-preconditioned GMRES to ||Bx||/||x|| < 1e-8 on B200.
+
+Contract (see the task statement): `python bench.py --gpus N --steps K
+--warmup W [--impl reference] [--config cfgX]` prints ONE JSON line on rank 0.
+
+A step is one full pass of the hot path over the workload: run_setup
+(bootstrap AMG: smoothing, LS transfer operators, Galerkin products, coarsest
+triplets) + VCycleOperator (coarsest pseudo-inverse) + preconditioned GMRES
+to rtol 1e-8.  The default workload is BASELINE.json configs[1] (uniform 2-D
+random walk, 1023 x 1023 = 1,046,529 states, k = 8, seed-0 uniform(0,1)
+test vectors).  The metric is a time: `value` = device seconds per step with
+the operator, geometry and initial vectors resident in HBM;
+`e2e` = the same through `solve_steady_state` with host inputs (pinned
+H2D of B / draws / geometry and the D2H of x inside the timed region).
+
+Multi-GPU: the path is replicated, one independent solve per rank ("replicas
+only", weak scaling); every rank times its own steps and rank 0 reports the
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (family, side / n, k, stop_size override, gmres restart, description)
+    "cfg0": ("tandem", 64, 8, 65, None, "tandem queue 64x64 (4,096 states), k=8, coarsest<=64"),
+    "cfg1": ("uniform2d", 1023, 8, None, None, "uniform 2-D walk 1023x1023 (1,046,529 states), k=8"),
+    "cfg2": ("tandem", 1024, 16, None, 30, "tandem queue 1024x1024 (1,048,576 states), k=16, GMRES(30)"),
+    "cfg3": ("planar", 2 ** 21, 12, None, None, "random planar Delaunay chain, 2^21 states, k=12"),
+    "cfg4": ("tandem", 4095, 16, None, None, "tandem queue 4095x4095 (16,769,025 states), k=16"),
+}
+RTOL = 1e-8
+METRIC = "AMG-GMRES setup+solve time to ||Bx||/||x||<1e-8 (s); V-cycle HBM GB/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def build_problem(name, validate=False):
+    from paper_1402_4005_b200 import chains
+    fam, size, k, stop, restart, _ = CONFIGS[name]
+    if fam == "tandem":
+        prob = chains.tandem_queue(size, validate=validate)
+    elif fam == "uniform2d":
+        prob = chains.uniform_2d(size, validate=validate)
+    else:
+        prob = chains.random_planar(size, seed=1, validate=validate)
+    return prob
+
+
+def setup_config(name):
+    from dataclasses import replace
+
+    from paper_1402_4005_b200 import default_setup_config
+    fam, size, k, stop, restart, _ = CONFIGS[name]
+    cfg = default_setup_config(fam, seed=0, n_tests=k)
+    if stop is not None:
+        cfg = replace(cfg, coarsening=replace(cfg.coarsening, stop_size=stop))
+    return cfg
+
+
+def draws_for(k, n):
+    g = np.random.default_rng(0)  # BASELINE: k uniform(0,1) vectors, seed 0 (right, then left)
+    return g.random((k, n)), g.random((k, n))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() in ("active", "1")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def vcycle_bytes(levels, nu1, nu2):
+    """Algorithmic HBM bytes of one V-cycle (SURVEY.md section 8(d) model)."""
+    total = 0.0
+    for li, lv in enumerate(levels[:-1]):
+        n, nnz = lv.n, lv.nnz
+        sweep = 12 * nnz + 4 * (n + 1) + 32 * n
+        first = 24 * n
+        resid = 12 * nnz + 4 * (n + 1) + 24 * n
+        nc = levels[li + 1].n
+        restrict = 12 * lv.dQ.nnz + 4 * (nc + 1) + 8 * n + 8 * nc
+        prolong = 12 * lv.dP.nnz + 4 * (n + 1) + 8 * nc + 16 * n
+        total += first + (nu1 - 1 + nu2) * sweep + resid + restrict + prolong
+    nl = levels[-1].n
+    total += 8 * (nl + 1) ** 2 + 16 * (nl + 1)
+    return total
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_1402_4005_b200 as pb
+    from paper_1402_4005_b200 import _lib
+    from paper_1402_4005_b200.chains import ChainProblem
+    from paper_1402_4005_b200.device import DeviceCSR
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    name = args.config
+    fam, size, k, stop, restart, desc = CONFIGS[name]
+    prob = build_problem(name)
+    n = prob.n
+    cfg = setup_config(name)
+    gcfg = pb.GmresConfig(restart=restart, rtol=RTOL)
+    right_h, left_h = draws_for(k, n)
+
+    # ---- inputs resident in HBM for the device-timed `value`
+    dB = DeviceCSR.from_host(prob.B)
+    dV = torch.from_numpy(np.ascontiguousarray(right_h.T)).cuda()
+    dU = torch.from_numpy(np.ascontiguousarray(left_h.T)).cuda()
+    dgeo = torch.from_numpy(np.ascontiguousarray(prob.geometry.T)).cuda() if prob.geometry is not None else None
+    dprob = ChainProblem(A=None, B=dB, n=n, family=fam, params={}, geometry=dgeo)
+    zero = torch.zeros(n, dtype=torch.float64, device="cuda")
+    L = _lib.lib()
+    c = _lib.ctx()
+
+    def step():
+        setup = pb.run_setup(dprob, cfg, draws=(dV, dU), B_device=dB)
+        vop = pb.VCycleOperator(setup.hierarchy, cfg.smoother)
+        rep = pb.gmres(dB, zero, setup.dx0, gcfg, vop, to_host=False)
+        return setup, vop, rep
+
+    for _ in range(args.warmup):
+        setup, vop, rep = step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-timed region: K steps, barrier + sync both sides
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = int(L.bamg_launch_count(c))
+    L.bamg_prof_enable(c, 0b11)  # CSR-stream family + LS-fit family, CUDA events on our stream
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        iters = []
+        for _ in range(args.steps):
+            setup, vop, rep = step()
+            iters.append(rep.iterations)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = int(L.bamg_launch_count(c)) - launches0
+    import ctypes as C
+    fam_stats = {}
+    for fid, fname in ((0, "csr_stream_spmv_spmm_jacobi"), (1, "ls_fit_warp_per_point")):
+        ms, cnt, by = C.c_double(), C.c_int64(), C.c_double()
+        L.bamg_prof_read(c, fid, C.byref(ms), C.byref(cnt), C.byref(by))
+        fam_stats[fname] = (ms.value, cnt.value, by.value)
+    L.bamg_prof_enable(c, 0)
+    dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    if dist is not None:
+        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    converged = bool(rep.converged) and rep.residual_history[-1] < RTOL
+
+    # ---- V-cycle throughput (secondary metric of BASELINE.json)
+    levels = setup.hierarchy.levels
+    vb = vcycle_bytes(levels, cfg.smoother.sweeps_pre, cfg.smoother.sweeps_post)
+    b = torch.randn(n, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        vop.apply(b)
+    nv = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(nv):
+        vop.apply(b)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    vms = e0.elapsed_time(e1) / nv
+    peak, peak_kind = peaks()
+
+    # ---- e2e through the public API with host inputs
+    Bh = prob.B
+    pins = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in
+            (Bh.indptr.astype(np.int32), Bh.indices.astype(np.int32), Bh.data,
+             np.ascontiguousarray(right_h.T), np.ascontiguousarray(left_h.T),
+             np.ascontiguousarray(prob.geometry.T))]
+    h2d = sum(t.numel() * t.element_size() for t in pins)
+    xout = torch.empty(n, dtype=torch.float64).pin_memory()
+    d2h = xout.numel() * 8
+
+    def e2e_step():
+        rp, ci, va, rv, lv, ge = [t.to("cuda", non_blocking=True) for t in pins]
+        B = DeviceCSR(rp, ci, va, Bh.shape)
+        p = ChainProblem(A=None, B=B, n=n, family=fam, params={}, geometry=ge)
+        rep2 = pb.solve_steady_state(p, cfg, gcfg, draws=(rv, lv), to_host=False)
+        xout.copy_(rep2.x_device, non_blocking=True)
+        torch.cuda.synchronize()
+        return rep2
+
+    e2e_step()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        rep2 = e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0) / args.steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # ---- dominant kernel family -> roofline
+    dom = max(fam_stats, key=lambda f: fam_stats[f][0])
+    ms, cnt, by = fam_stats[dom]
+    per_launch_s = ms / 1e3 / max(cnt, 1)
+    achieved = (by / max(cnt, 1)) / per_launch_s / 1e9 if cnt else 0.0
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "launches_in_timed_region": cnt, "share_of_step": round(ms / 1e3 / (dev_s * args.steps), 4),
+            "families": {f: {"ms_total": round(v[0], 3), "launches": v[1],
+                             "alg_GBps": round((v[2] / max(v[1], 1)) / (v[0] / 1e3 / max(v[1], 1)) / 1e9, 1) if v[1] else 0}
+                         for f, v in fam_stats.items()}}
+    line = {
+        "metric": METRIC, "value": round(dev_s, 6), "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
+        "config": {"workload": f"{name}: {desc}", "n": n, "nnz": int(dB.nnz), "k": k,
+                   "gmres_restart": restart, "rtol": RTOL, "setup_cycles": cfg.setup_cycles,
+                   "levels": [lv.n for lv in levels], "gmres_iterations": iters[-1],
+                   "converged": converged, "parallelism": f"replicas x{world}",
+                   "l2": "working set (operators + k-vector blocks) > 126 MB L2; no flush"},
+        "vcycle": {"ms": round(vms, 4), "alg_bytes": int(vb), "GBps": round(vb / (vms / 1e3) / 1e9, 1),
+                   "frac_of_hbm_peak": round(vb / (vms / 1e3) / 1e9 / peak, 4)},
+        "roofline": roof,
+        "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, args.cpu_sample)
+    if dist is not None:
+        dist.destroy_process_group()
+    return line
+
+
+def cpu_baseline(name, sample=None, repeat=1):
+    """The oracle (numpy restatement of the reference) on a bounded sample of the
+    same family, extrapolated linearly in the state count to the full workload."""
+    sys.path.insert(0, str(ROOT))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import bamg_oracle as orc
+    fam, size, k, stop, restart, desc = CONFIGS[name]
+    from paper_1402_4005_b200 import chains
+    if fam == "planar":
+        n_s = sample or 4096
+        prob = chains.random_planar(n_s, seed=1, validate=False)
+        n_full = size
+    else:
+        side = sample or (127 if fam == "uniform2d" else 128)
+        prob = chains.tandem_queue(side, validate=False) if fam == "tandem" else chains.uniform_2d(side, validate=False)
+        n_s = prob.n
+        n_full = size * size
+    cfg = orc.default_cfg(fam, k=k, stop=stop, seed=0)
+    right, left = draws_for(k, prob.n)
+    best = None
+    for _ in range(repeat):
+        t0 = time.perf_counter()
+        levels, T, x0, its, hist, conv, x = orc.solve(prob.B, cfg, prob.geometry, right, left, restart, RTOL)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": round(best * n_full / n_s, 2), "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"oracle (numpy/scipy restatement, 1 thread) setup+solve on {fam} n={n_s} "
+                      f"({best:.2f} s, {its} GMRES its), scaled x{n_full / n_s:.1f} linearly in n to "
+                      f"n={n_full}"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port; /root/reference is not on the GPU box), rank 0 only."""
+    if rank != 0:
+        return None
+    name = args.config
+    for _ in range(args.warmup):
+        pass
+    vals = []
+    for _ in range(args.steps):
+        cb = cpu_baseline(name, args.cpu_sample)
+        vals.append(cb["value"])
+    v = float(np.mean(vals))
+    fam, size, k, stop, restart, desc = CONFIGS[name]
+    return {"metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
+            "config": {"workload": f"{name}: {desc}", "k": k, "gmres_restart": restart, "rtol": RTOL},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

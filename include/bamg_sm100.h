@@ -55,6 +55,12 @@ int bamg_version(void);
 /* Number of kernels this context has launched (evidence for bench.py). */
 int64_t bamg_launch_count(bamg_ctx* ctx);
 int bamg_sync(bamg_ctx* ctx);
+/* Live per-kernel-family timing with CUDA events on the context's stream.
+ * Families: 0 CSR-stream SpMV/SpMM/Jacobi, 1 LS fit, 2 SpGEMM, 3 GMRES
+ * orthogonalisation, 4 dense coarsest, 5 other.  enable() resets counters. */
+int bamg_prof_enable(bamg_ctx* ctx, unsigned family_mask);
+int bamg_prof_read(bamg_ctx* ctx, int family, double* ms_host, int64_t* launches_host,
+                   double* bytes_host);
 
 /* ------------------------------------------------------- sparse (sparse.py) */
 /* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;

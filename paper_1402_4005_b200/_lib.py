@@ -45,6 +45,8 @@ _SIGS = {
     "bamg_version": [],
     "bamg_launch_count": [P],
     "bamg_sync": [P],
+    "bamg_prof_enable": [P, C.c_uint],
+    "bamg_prof_read": [P, C.c_int, PF64, PI64, PF64],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
     "bamg_csr_transpose": [P, PCSR, P, P, P],

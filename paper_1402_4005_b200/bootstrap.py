@@ -31,6 +31,25 @@ from .sparse import adjacency_structure, as_device
 #: bootstrap.py:329
 SICK_DIAG_FRACTION = 0.02
 
+#: optional phase profiler (bench.py --breakdown): name -> seconds.  Each
+#: phase boundary synchronises the device, so it is off on the timed path.
+PHASES: dict | None = None
+
+
+class _phase:
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if PHASES is not None:
+            torch.cuda.synchronize()
+            self.t = time.perf_counter()
+
+    def __exit__(self, *exc):
+        if PHASES is not None:
+            torch.cuda.synchronize()
+            PHASES[self.name] = PHASES.get(self.name, 0.0) + time.perf_counter() - self.t
+
 
 class TripletSet:
     """Approximate singular triplets on device (bootstrap.py:35-59)."""
@@ -152,13 +171,21 @@ class Hierarchy:
         return self.levels[-1]
 
 
-@dataclass
 class SetupResult:
-    hierarchy: Hierarchy
-    triplets: TripletSet
-    x0: np.ndarray
-    seconds: float = 0.0
-    dx0: object = None
+    """bootstrap.py:119-124; `x0` is materialised on the host on first access."""
+
+    def __init__(self, hierarchy, triplets, dx0, seconds=0.0):
+        self.hierarchy = hierarchy
+        self.triplets = triplets
+        self.dx0 = dx0
+        self.seconds = seconds
+        self._x0 = None
+
+    @property
+    def x0(self) -> np.ndarray:
+        if self._x0 is None:
+            self._x0 = self.dx0.cpu().numpy()
+        return self._x0
 
 
 def complexities(hierarchy: Hierarchy) -> tuple[float, float, int]:
@@ -230,8 +257,13 @@ def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps 
         left_h = rng.standard_normal((r, n))
     else:
         right_h, left_h = draws
-    V = engine.to_device_vec(np.ascontiguousarray(np.asarray(right_h, dtype=np.float64).T))
-    U = engine.to_device_vec(np.ascontiguousarray(np.asarray(left_h, dtype=np.float64).T))
+    if isinstance(right_h, torch.Tensor):
+        # device-resident draws, already n x k interleaved; the smoothing works in place
+        V = right_h.clone()
+        U = left_h.clone()
+    else:
+        V = engine.to_device_vec(np.ascontiguousarray(np.asarray(right_h, dtype=np.float64).T))
+        U = engine.to_device_vec(np.ascontiguousarray(np.asarray(left_h, dtype=np.float64).T))
     sig = torch.zeros(r, dtype=torch.float64, device=device())
     sm = cfg.smoother
     # nu1 homogeneous sweeps per slot, no runaway rescaling (bootstrap.py:191-194)
@@ -280,7 +312,9 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
                     ops: _LevelOps | None = None):
     """One recursive setup pass (bootstrap.py:337-392); returns (levels, triplets)."""
     A = as_device(B)
-    ops = ops or _LevelOps(A)
+    if ops is None:
+        with _phase("level_ops"):
+            ops = _LevelOps(A)
     Md, Nd = as_device(M), as_device(N)
     n = A.shape[0]
     if seed_stream is None:
@@ -292,49 +326,63 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
     split = None
     if n >= cfg.coarsening.stop_size and depth + 1 < cfg.coarsening.max_levels:
         seed = seed_stream.next()
-        if cfg.coarsening.mode == "cr":
-            split = make_splitting(A, ranks, cfg.coarsening, seed, adj=ops.adj, diag=ops.d)
-        else:
-            split = make_splitting(A, ranks, cfg.coarsening, seed)
+        with _phase("split"):
+            if cfg.coarsening.mode == "cr":
+                split = make_splitting(A, ranks, cfg.coarsening, seed, adj=ops.adj, diag=ops.d)
+            else:
+                split = make_splitting(A, ranks, cfg.coarsening, seed)
         if split.n_coarse >= 0.9 * n or split.n_coarse == n:
             split = None  # coarsening stalled
     if split is None:
-        trips = coarsest_triplets(A, Md, Nd, trips.r)
+        with _phase("coarsest"):
+            trips = coarsest_triplets(A, Md, Nd, trips.r)
         return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
 
-    _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
+    with _phase("smooth"):
+        _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
 
     levels = None
     for _ in range(cfg.inner_passes):
-        v_tests = singular_test_weights(A, trips.dright)
-        u_tests = singular_test_weights(A, trips.dleft, transpose_side=True,
-                                        infinite_slot=0 if cfg.interp.constrain_constant_in_q else None,
-                                        Bt=ops.Bt)
-        P = build_interpolation(A, split, v_tests, cfg.interp, adj=ops.adj)
-        W = build_restriction_rows(A, split, u_tests, cfg.interp, adj=ops.adj)
-        Q = engine.transpose(W)
-        Bc = engine.spgemm(engine.spgemm(Q, A, order=1), P, order=0)
-        if _operator_degenerate(Bc):
-            trips = coarsest_triplets(A, Md, Nd, trips.r)
+        with _phase("weights"):
+            v_tests = singular_test_weights(A, trips.dright)
+            u_tests = singular_test_weights(A, trips.dleft, transpose_side=True,
+                                            infinite_slot=0 if cfg.interp.constrain_constant_in_q else None,
+                                            Bt=ops.Bt)
+        with _phase("adjacency"):
+            adj = ops.adj
+        with _phase("ls_fit"):
+            P = build_interpolation(A, split, v_tests, cfg.interp, adj=adj)
+            W = build_restriction_rows(A, split, u_tests, cfg.interp, adj=adj)
+        with _phase("galerkin"):
+            Q = engine.transpose(W)
+            Bc = engine.spgemm(engine.spgemm(Q, A, order=1), P, order=0)
+            sick = _operator_degenerate(Bc)
+        if sick:
+            with _phase("coarsest"):
+                trips = coarsest_triplets(A, Md, Nd, trips.r)
             return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
-        Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
-        Pt = engine.transpose(P)
-        Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
-        cranks = ranks.restrict(split) if ranks is not None else None
-        cl = engine.gather_rows(trips.dleft, split.dcoarse)
-        cr = engine.gather_rows(trips.dright, split.dcoarse)
-        engine.normalize_cols(cl)
-        engine.normalize_cols(cr)
+        with _phase("galerkin"):
+            Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
+            Pt = engine.transpose(P)
+            Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
+        with _phase("inject"):
+            cranks = ranks.restrict(split) if ranks is not None else None
+            cl = engine.gather_rows(trips.dleft, split.dcoarse)
+            cr = engine.gather_rows(trips.dright, split.dcoarse)
+            engine.normalize_cols(cl)
+            engine.normalize_cols(cr)
         coarse = TripletSet(trips.dsigmas.clone(), cl, cr)
         sub_levels, coarse = bootstrap_cycle(Bc, Mc, Nc, coarse, cfg, cranks, depth + 1,
                                              first_cycle, seed_stream)
         # prolong: u <- Q^T u_c (= W u_c), v <- P v_c; normalise; pin; refresh; smooth
-        U = engine.spmm(W, coarse.dleft)
-        V = engine.spmm(P, coarse.dright)
-        trips = TripletSet(coarse.dsigmas.clone(), U, V)
-        engine.smooth_block(ops.B, ops.Bt, _mass(Md), _mass(Nd), ops.d, ops.skip, ops.skip_t,
-                            U, V, trips.dsigmas, 0, cfg.smoother.omega, 0, smooth=0, refresh=1)
-        _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True)
+        with _phase("prolong"):
+            U = engine.spmm(W, coarse.dleft)
+            V = engine.spmm(P, coarse.dright)
+            trips = TripletSet(coarse.dsigmas.clone(), U, V)
+            engine.smooth_block(ops.B, ops.Bt, _mass(Md), _mass(Nd), ops.d, ops.skip, ops.skip_t,
+                                U, V, trips.dsigmas, 0, cfg.smoother.omega, 0, smooth=0, refresh=1)
+        with _phase("smooth"):
+            _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True)
         levels = [Level(depth, A, ops.d, Md, Nd, split, P, Q, ranks, Bt=ops.Bt, W=W)] + sub_levels
     return levels, trips
 
@@ -351,12 +399,17 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     n = A.shape[0]
     root = np.random.SeedSequence(cfg.seed)
     ss_init, ss_levels = root.spawn(2)
-    ops = _LevelOps(A)
+    with _phase("level_ops"):
+        ops = _LevelOps(A)
     rng = np.random.default_rng(ss_init) if draws is None else None
-    trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops)
+    with _phase("init"):
+        trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops)
     stream = _SeedStream(ss_levels)
     eye = DeviceCSR.identity(n)
-    geometry = AxisRanks.from_geometry(problem.geometry) if problem.geometry is not None else None
+    geometry = problem.geometry
+    if geometry is not None and not isinstance(geometry, AxisRanks):
+        with _phase("axis_ranks"):
+            geometry = AxisRanks.from_geometry(geometry)
     hierarchy = None
     for cycle in range(cfg.setup_cycles):
         levels, trips = bootstrap_cycle(A, eye, eye, trips, cfg, geometry=geometry, depth=0,
@@ -367,7 +420,7 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     dx0 = engine.sign_fix_l1(trips.dright, stride=trips.r, uniform_fallback=True)
     torch.cuda.synchronize()
     seconds = time.perf_counter() - t0
-    return SetupResult(hierarchy, trips, dx0.cpu().numpy(), seconds=seconds, dx0=dx0)
+    return SetupResult(hierarchy, trips, dx0, seconds=seconds)
 
 
 def triplet_residual(trips: TripletSet, B, M=None, N=None) -> float:

@@ -109,16 +109,23 @@ class AxisRanks:
 
     @classmethod
     def from_geometry(cls, geometry):
-        g = np.asarray(geometry, dtype=np.float64)
-        if g.ndim != 2:
-            raise ValueError("geometry must be an (n, d) array")
+        """`geometry`: host (n, d) array, or device per-axis coordinate columns
+        (a d x n tensor) already resident in HBM."""
+        if isinstance(geometry, torch.Tensor):
+            cols = [geometry[a].contiguous() for a in range(geometry.shape[0])]
+            host = None
+        else:
+            g = np.asarray(geometry, dtype=np.float64)
+            if g.ndim != 2:
+                raise ValueError("geometry must be an (n, d) array")
+            cols = [torch.from_numpy(np.ascontiguousarray(g[:, a])).to(device()) for a in range(g.shape[1])]
+            host = g
         ranks, nvals = [], []
-        for a in range(g.shape[1]):
-            col = torch.from_numpy(np.ascontiguousarray(g[:, a])).to(device())
+        for col in cols:
             r, nv = engine.axis_ranks(col)
             ranks.append(r)
             nvals.append(nv)
-        return cls(ranks, nvals, g)
+        return cls(ranks, nvals, host)
 
     @property
     def ndim(self):

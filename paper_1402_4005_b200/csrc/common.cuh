@@ -49,6 +49,18 @@ struct Arena {
   }
 };
 
+// Per-family kernel timing with CUDA events on the launching stream
+// (bench.py's live roofline).  Off unless bamg_prof_enable() set the family.
+enum { FAM_TILE = 0, FAM_FIT = 1, FAM_SPGEMM = 2, FAM_ORTHO = 3, FAM_DENSE = 4, FAM_OTHER = 5, NFAM = 6 };
+
+struct KProf {
+  unsigned mask = 0;
+  std::vector<cudaEvent_t> ev[NFAM];  // start/stop pairs
+  size_t used[NFAM] = {0, 0, 0, 0, 0, 0};
+  double bytes[NFAM] = {0, 0, 0, 0, 0, 0};
+  double flops[NFAM] = {0, 0, 0, 0, 0, 0};
+};
+
 struct bamg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -58,7 +70,30 @@ struct bamg_ctx {
   Arena arena;
   double* pinned = nullptr;  // small pinned host staging buffer
   size_t pinned_doubles = 0;
+  KProf prof;
 };
+
+// event pair around one launch of family `fam` (no-op unless profiled)
+static inline cudaEvent_t prof_event(bamg_ctx* ctx, int fam) {
+  KProf& P = ctx->prof;
+  if (P.used[fam] >= P.ev[fam].size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    P.ev[fam].push_back(e);
+  }
+  return P.ev[fam][P.used[fam]++];
+}
+
+#define BAMG_LAUNCH_FAM(ctx, fam, nbytes, kernel, grid, block, smem, ...)       \
+  do {                                                                          \
+    bool _prof = ((ctx)->prof.mask >> (fam)) & 1u;                              \
+    if (_prof && (grid) > 0) {                                                  \
+      cudaEventRecord(prof_event(ctx, fam), (ctx)->stream);                     \
+      (ctx)->prof.bytes[fam] += (double)(nbytes);                               \
+    }                                                                           \
+    BAMG_LAUNCH(ctx, kernel, grid, block, smem, __VA_ARGS__);                   \
+    if (_prof && (grid) > 0) cudaEventRecord(prof_event(ctx, fam), (ctx)->stream); \
+  } while (0)
 
 // ---------------------------------------------------------------- error glue
 #define BAMG_CHECK_CUDA(ctx, expr)                                              \

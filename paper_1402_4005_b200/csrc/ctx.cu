@@ -315,3 +315,32 @@ extern "C" int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int 
   BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n * k, 256), 256, 0, X, n, k, p, Y);
   return 0;
 }
+
+extern "C" int bamg_prof_enable(bamg_ctx* ctx, unsigned mask) {
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->prof.mask = mask;
+  for (int f = 0; f < NFAM; ++f) {
+    ctx->prof.used[f] = 0;
+    ctx->prof.bytes[f] = 0.0;
+    ctx->prof.flops[f] = 0.0;
+  }
+  return 0;
+}
+
+// total device milliseconds, launch count and algorithmic bytes of family fam
+extern "C" int bamg_prof_read(bamg_ctx* ctx, int fam, double* ms_host, int64_t* launches_host,
+                              double* bytes_host) {
+  BAMG_REQUIRE(ctx, fam >= 0 && fam < NFAM, "family out of range");
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  KProf& P = ctx->prof;
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < P.used[fam]; i += 2) {
+    float ms = 0.f;
+    BAMG_CHECK_CUDA(ctx, cudaEventElapsedTime(&ms, P.ev[fam][i], P.ev[fam][i + 1]));
+    tot += ms;
+  }
+  *ms_host = tot;
+  *launches_host = (int64_t)(P.used[fam] / 2);
+  *bytes_host = P.bytes[fam];
+  return 0;
+}

@@ -587,7 +587,9 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
   int64_t blocks = (warps + FIT_WARPS - 1) / FIT_WARPS;
   int64_t maxb = (int64_t)ctx->num_sms * 64;
   if (blocks > maxb) blocks = maxb;
-  BAMG_LAUNCH(ctx, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr, adj->col, coarse_rank, X,
+  // algorithmic bytes: test vectors of every point + adjacency + rank map + the row output
+  double fbytes = 8.0 * n * k + 4.0 * (n + 1) + 4.0 * adj->nnz + 4.0 * n + 16.0 * n * caliber;
+  BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr, adj->col, coarse_rank, X,
               k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative, out_cnt, out_col, out_val, status);
   int64_t st[2];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 2, st));

@@ -104,22 +104,28 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   BAMG_REQUIRE(ctx, k >= 1 && k <= 32, "k must lie in [1, 32]");
   int grid = (A->nrows + TILE_ROWS - 1) / TILE_ROWS;
   if (grid == 0) return 0;
+  // algorithmic bytes: rowptr + col/val + each x once + y written (+ epilogue inputs)
+  const double n = A->nrows, kk = k;
+  double bytes = 4.0 * (n + 1) + 12.0 * (double)A->nnz + 8.0 * kk * A->ncols + 8.0 * kk * n;
+  if (epi == EPI_RESID) bytes += 8.0 * n;                         // b
+  if (epi == EPI_ADD) bytes += 8.0 * kk * n;                      // x_old
+  if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * kk * n : 0.0) + 9.0 * n;  // b, d, skip (x_old == X)
   switch (epi) {
     case EPI_PLAIN:
-      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
-                  A->col, A->val, X, k, Y, ea);
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     case EPI_RESID:
-      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_RESID>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
-                  A->col, A->val, X, k, Y, ea);
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_RESID>, grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     case EPI_ADD:
-      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_ADD>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
-                  A->col, A->val, X, k, Y, ea);
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_ADD>, grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     default:
-      BAMG_LAUNCH(ctx, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows, A->rowptr,
-                  A->col, A->val, X, k, Y, ea);
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->col, A->val, X, k, Y, ea);
   }
   return 0;
 }

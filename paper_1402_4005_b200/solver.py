@@ -143,8 +143,11 @@ class VCycleOperator:
             pass
 
 
-def gmres(B, b, x_init, cfg: GmresConfig, precond: VCycleOperator | None = None) -> SolveReport:
-    """Restarted, left-preconditioned GMRES with the true-residual stop (solver.py:136-226)."""
+def gmres(B, b, x_init, cfg: GmresConfig, precond: VCycleOperator | None = None,
+          to_host: bool = True) -> SolveReport:
+    """Restarted, left-preconditioned GMRES with the true-residual stop (solver.py:136-226).
+
+    `to_host=False` leaves the iterate on the device only (report.x_device)."""
     A = as_device(B)
     n = A.shape[0]
     bv = _vec(b, n)
@@ -160,9 +163,8 @@ def gmres(B, b, x_init, cfg: GmresConfig, precond: VCycleOperator | None = None)
                                C.byref(nh))
     _lib.check(rc, "bamg_gmres")
     history = [float(hist[i]) for i in range(nh.value)]
-    converged = rc == 0 and (history[-1] <= cfg.rtol or its.value < cfg.max_iters) if history else False
     converged = rc == 0
-    return SolveReport(its.value, history, converged, x.cpu().numpy(), x_device=x)
+    return SolveReport(its.value, history, converged, x.cpu().numpy() if to_host else None, x_device=x)
 
 
 def _sign_fix_l1(x):
@@ -173,7 +175,7 @@ def _sign_fix_l1(x):
 
 
 def solve_steady_state(problem, setup_cfg: SetupConfig | None, gmres_cfg: GmresConfig,
-                       draws=None) -> SolveReport:
+                       draws=None, to_host: bool = True) -> SolveReport:
     """Two-phase solve: adaptive setup, then preconditioned GMRES (solver.py:238-268).
 
     `draws=(right, left)` injects the raw initial test vectors (see run_setup).
@@ -194,10 +196,11 @@ def solve_steady_state(problem, setup_cfg: SetupConfig | None, gmres_cfg: GmresC
     t0 = time.perf_counter()
     vop = VCycleOperator(setup.hierarchy, setup_cfg.smoother)
     zero = torch.zeros(n, dtype=torch.float64, device=A.rowptr.device)
-    report = gmres(A, zero, setup.dx0, gmres_cfg, precond=vop)
+    report = gmres(A, zero, setup.dx0, gmres_cfg, precond=vop, to_host=False)
     xs = engine.sign_fix_l1(report.x_device)
     report.x_device = xs
-    report.x = xs.cpu().numpy()
+    report.x = xs.cpu().numpy() if to_host else None
+    torch.cuda.synchronize()
     report.solve_seconds = time.perf_counter() - t0
     report.setup_seconds = setup.seconds
     o_g, o_c, depth = complexities(setup.hierarchy)

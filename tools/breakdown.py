@@ -1,0 +1,53 @@
+"""Phase breakdown of setup + solve on one config (development tool, syncs per phase)."""
+import argparse, json, sys, time
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+
+import paper_1402_4005_b200 as pb
+from paper_1402_4005_b200 import bootstrap as bs, chains
+from paper_1402_4005_b200.device import DeviceCSR
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg1")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+C = {"cfg0": ("tandem", 64, 8, 65, None), "cfg1": ("uniform2d", 1023, 8, None, None),
+     "cfg2": ("tandem", 1024, 16, None, 30), "cfg4": ("tandem", 4095, 16, None, None)}[a.config]
+fam, side, k, stop, restart = C
+t = time.time()
+prob = chains.tandem_queue(side, validate=False) if fam == "tandem" else chains.uniform_2d(side, validate=False)
+print("gen", time.time() - t, flush=True)
+over = {"n_tests": k}
+cfg = pb.default_setup_config(fam, seed=0, **over)
+if stop:
+    from dataclasses import replace
+    cfg = replace(cfg, coarsening=replace(cfg.coarsening, stop_size=stop))
+g = np.random.default_rng(0)
+draws = (g.random((k, prob.n)), g.random((k, prob.n)))
+dB = DeviceCSR.from_host(prob.B)
+dV = torch.from_numpy(np.ascontiguousarray(draws[0].T)).cuda()
+dU = torch.from_numpy(np.ascontiguousarray(draws[1].T)).cuda()
+geo = torch.from_numpy(np.ascontiguousarray(prob.geometry.T)).cuda()
+P = chains.ChainProblem(A=None, B=dB, n=prob.n, family=fam, params={}, geometry=geo)
+gcfg = pb.GmresConfig(restart=restart, rtol=1e-8)
+for rep in range(a.reps):
+    bs.PHASES = {}
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    setup = pb.run_setup(P, cfg, draws=(dV, dU), B_device=dB)
+    torch.cuda.synchronize(); t1 = time.perf_counter()
+    vop = pb.VCycleOperator(setup.hierarchy, cfg.smoother)
+    torch.cuda.synchronize(); t2 = time.perf_counter()
+    zero = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+    r = pb.gmres(dB, zero, setup.dx0, gcfg, vop, to_host=False)
+    torch.cuda.synchronize(); t3 = time.perf_counter()
+    # V-cycle timing
+    b = torch.randn(prob.n, dtype=torch.float64, device="cuda")
+    vop.apply(b); torch.cuda.synchronize()
+    tv = time.perf_counter()
+    for _ in range(10): vop.apply(b)
+    torch.cuda.synchronize(); tv = (time.perf_counter() - tv) / 10
+    levels = [(l.n, l.nnz) for l in setup.hierarchy.levels]
+    print(json.dumps({"rep": rep, "setup": t1 - t0, "pinv": t2 - t1, "gmres": t3 - t2, "its": r.iterations,
+                      "hist": r.residual_history[-1], "vcycle_ms": tv * 1e3, "levels": levels,
+                      "phases": {k2: round(v, 4) for k2, v in bs.PHASES.items()}}), flush=True)
