@@ -61,6 +61,10 @@ int bamg_sync(bamg_ctx* ctx);
 int bamg_prof_enable(bamg_ctx* ctx, unsigned family_mask);
 int bamg_prof_read(bamg_ctx* ctx, int family, double* ms_host, int64_t* launches_host,
                    double* bytes_host);
+/* Development trace: event pair around every launch, aggregated by kernel
+ * name into "name total_ms count" lines. */
+int bamg_trace_enable(bamg_ctx* ctx, int on);
+int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap);
 
 /* ------------------------------------------------------- sparse (sparse.py) */
 /* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;
@@ -146,16 +150,21 @@ int bamg_refresh_sigmas(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M,
  * inf_slot < 0 for none.  Xn (n x k) receives the unit vectors. */
 int bamg_test_weights(bamg_ctx* ctx, const bamg_csr* A, const double* X, int64_t n, int k,
                       int inf_slot, double* Xn, double* w);
-/* Greedy caliber-bounded weighted ridge LS per fine point, one warp per point
- * (interp.py:129-289).  adj: pattern(A+A^T) without diagonal; coarse_rank[i]
- * >= 0 marks a C point.  Writes, per state i, up to `caliber` (column, value)
- * pairs into out_col/out_val (n x caliber) and out_cnt[i] (C points: their
- * identity entry; no-candidate F points: 0).  status_host[0] counts fits that
- * needed the rank-deficient pseudo-inverse branch. */
+/* Greedy caliber-bounded weighted ridge LS per fine point (interp.py:129-289).
+ * Production path: one thread per point (register Cholesky of the ridge normal
+ * equations + two refinement steps on the original rows); points it cannot
+ * take are finished by the one-warp-per-point Householder-QR kernel.
+ * adj: pattern(A+A^T) without diagonal; coarse_rank[i] >= 0 marks a C point.
+ * ridge_override < 0: lambda = 0.1 * level scale (interp.py:266-268), else
+ * the given lambda.  Writes, per state i, up to `caliber` (column, value) pairs
+ * into out_col/out_val (n x caliber) and out_cnt[i] (C points: identity entry;
+ * no-candidate F points: 0).  status_host (2 int64): [0] fits that took the
+ * rank-deficient pseudo-inverse branch, [1] points deferred to the warp path. */
 int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
                   const double* X, const double* w, int64_t n, int k, int caliber,
                   int radius, double improvement_tol, int constrain, int nonnegative,
-                  int32_t* out_cnt, int32_t* out_col, double* out_val, int64_t* status_host);
+                  double ridge_override, int32_t* out_cnt, int32_t* out_col, double* out_val,
+                  int64_t* status_host);
 /* Compact the fixed-stride rows into canonical CSR (sorted columns, |v| <
  * 1e-300 dropped: csr_from_coo, sparse.py:42-46).  Two calls. */
 int bamg_rows_count(bamg_ctx* ctx, const int32_t* cnt, const double* val, int64_t n,

@@ -47,6 +47,8 @@ _SIGS = {
     "bamg_sync": [P],
     "bamg_prof_enable": [P, C.c_uint],
     "bamg_prof_read": [P, C.c_int, PF64, PI64, PF64],
+    "bamg_trace_enable": [P, C.c_int],
+    "bamg_trace_dump": [P, C.c_char_p, I64],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
     "bamg_csr_transpose": [P, PCSR, P, P, P],
@@ -68,7 +70,7 @@ _SIGS = {
     "bamg_refresh_sigmas": [P, PCSR, PCSR, PCSR, P, P, P, P, C.c_int],
     "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
     "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
-                      P, P, P, PI64],
+                      F64, P, P, P, PI64],
     "bamg_rows_count": [P, P, P, I64, C.c_int, P, PI64],
     "bamg_rows_fill": [P, P, P, P, I64, C.c_int, P, P, P],
     "bamg_axis_ranks": [P, P, I64, P, PI64],

@@ -61,6 +61,15 @@ struct KProf {
   double flops[NFAM] = {0, 0, 0, 0, 0, 0};
 };
 
+// Whole-engine launch trace (development): every BAMG_LAUNCH brackets its
+// kernel with an event pair tagged by the kernel's name.
+struct KTrace {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> name;
+  size_t used = 0;
+};
+
 struct bamg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -71,7 +80,20 @@ struct bamg_ctx {
   double* pinned = nullptr;  // small pinned host staging buffer
   size_t pinned_doubles = 0;
   KProf prof;
+  KTrace trace;
 };
+
+static inline void trace_mark(bamg_ctx* ctx, const char* name) {
+  KTrace& T = ctx->trace;
+  if (T.used >= T.ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    T.ev.push_back(e);
+    T.name.push_back(nullptr);
+  }
+  T.name[T.used] = name;
+  cudaEventRecord(T.ev[T.used++], ctx->stream);
+}
 
 // event pair around one launch of family `fam` (no-op unless profiled)
 static inline cudaEvent_t prof_event(bamg_ctx* ctx, int fam) {
@@ -118,9 +140,11 @@ static inline cudaEvent_t prof_event(bamg_ctx* ctx, int fam) {
 #define BAMG_LAUNCH(ctx, kernel, grid, block, smem, ...)                        \
   do {                                                                          \
     if ((grid) > 0) {                                                           \
+      if ((ctx)->trace.on) trace_mark(ctx, #kernel);                            \
       kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);          \
       (ctx)->launches++;                                                        \
       BAMG_CHECK_CUDA(ctx, cudaGetLastError());                                 \
+      if ((ctx)->trace.on) trace_mark(ctx, nullptr);                            \
     }                                                                           \
   } while (0)
 

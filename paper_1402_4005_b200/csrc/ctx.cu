@@ -344,3 +344,34 @@ extern "C" int bamg_prof_read(bamg_ctx* ctx, int fam, double* ms_host, int64_t* 
   *bytes_host = P.bytes[fam];
   return 0;
 }
+
+#include <map>
+
+extern "C" int bamg_trace_enable(bamg_ctx* ctx, int on) {
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->trace.on = on != 0;
+  ctx->trace.used = 0;
+  return 0;
+}
+
+// Writes "name total_ms count" lines (aggregated by kernel name) into buf.
+extern "C" int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap) {
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::map<std::string, std::pair<double, int64_t>> agg;
+  KTrace& T = ctx->trace;
+  for (size_t i = 0; i + 1 < T.used; ++i) {
+    if (!T.name[i] || T.name[i + 1]) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, T.ev[i], T.ev[i + 1]);
+    auto& a = agg[T.name[i]];
+    a.first += ms;
+    a.second += 1;
+  }
+  std::string out;
+  for (auto& kv : agg) out += kv.first + " " + std::to_string(kv.second.first) + " " + std::to_string(kv.second.second) + "\n";
+  int64_t len = (int64_t)out.size();
+  if (len >= cap) len = cap - 1;
+  memcpy(buf, out.data(), len);
+  buf[len] = 0;
+  return 0;
+}

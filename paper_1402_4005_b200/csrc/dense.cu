@@ -19,9 +19,33 @@
 //    Left vectors of numerically-null sigmas come from a second Jacobi SVD of
 //    K^T.  Halves are M-/N-normalised, v is flipped so u^T B v >= 0, and the
 //    null-slot cleanup (dead rows/columns, sign-coherent lead) runs in one CTA.
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <vector>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+// Cooperative launch helper: grid capped at the co-resident maximum.
+template <typename K>
+static int coop_grid(bamg_ctx* ctx, K kernel, int threads, int want) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  int cap = per_sm * ctx->num_sms;
+  if (cap < 1) cap = 1;
+  return want < cap ? (want < 1 ? 1 : want) : cap;
+}
+
+#define BAMG_COOP(ctx, kernel, grid, block, ...)                                  \
+  do {                                                                            \
+    void* _args[] = {__VA_ARGS__};                                                \
+    if ((ctx)->trace.on) trace_mark(ctx, #kernel);                                \
+    BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), _args, 0, (ctx)->stream)); \
+    (ctx)->launches++;                                                            \
+    if ((ctx)->trace.on) trace_mark(ctx, nullptr);                                \
+  } while (0)
 
 // --------------------------------------------------------- CSR -> dense
 __global__ void csr_to_dense_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -130,21 +154,75 @@ __global__ void col_norms_dense_kernel(const double* __restrict__ G, int nrows, 
   if (threadIdx.x == 0) sig[c] = sqrt(a);
 }
 
+// All sweeps of the one-sided Jacobi SVD in ONE cooperative launch: each
+// tournament step rotates its n/2 disjoint column pairs (CTA-strided), a grid
+// barrier separates steps, and a per-sweep flag decides convergence without
+// host round trips.  Loads after a grid barrier use ld.global.cg (L1 bypass).
+__global__ void __launch_bounds__(JAC_THREADS)
+jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double tol, int* flags,
+                       int maxsweeps) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  for (int sw = 0; sw < maxsweeps; ++sw) {
+    for (int s = 0; s < m - 1; ++s) {
+      for (int pair = blockIdx.x; pair < m / 2; pair += gridDim.x) {
+        int p, q;
+        tournament_pair(m, s, pair, &p, &q);
+        if (p >= ncols || q >= ncols) continue;
+        if (p > q) {
+          int t = p;
+          p = q;
+          q = t;
+        }
+        double* gp = G + (int64_t)p * nrows;
+        double* gq = G + (int64_t)q * nrows;
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+          double x = __ldcg(gp + r), y = __ldcg(gq + r);
+          a += x * x;
+          b += y * y;
+          c += x * y;
+        }
+        a = block_sum(a, sh);
+        b = block_sum(b, sh);
+        c = block_sum(c, sh);
+        if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) continue;
+        double zeta = (b - a) / (2.0 * c);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+          double x = __ldcg(gp + r), y = __ldcg(gq + r);
+          gp[r] = cs * x - sn * y;
+          gq[r] = sn * x + cs * y;
+        }
+        double* vp = V + (int64_t)p * ncols;
+        double* vq = V + (int64_t)q * ncols;
+        for (int r = threadIdx.x; r < ncols; r += blockDim.x) {
+          double x = __ldcg(vp + r), y = __ldcg(vq + r);
+          vp[r] = cs * x - sn * y;
+          vq[r] = sn * x + cs * y;
+        }
+        if (threadIdx.x == 0) flags[sw] = 1;
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)(flags + sw) == 0) break;  // uniform: every CTA reads after the barrier
+  }
+}
+
 // G (nrows x ncols, column-major) -> G V = U S; V (ncols x ncols); sig
 static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig) {
-  int* rotated;
-  BAMG_TRY(arena_get(ctx, 1, &rotated));
+  constexpr int MAXSW = 60;
+  int* flags;
+  BAMG_TRY(arena_get(ctx, MAXSW, &flags));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(flags, 0, sizeof(int) * MAXSW, ctx->stream));
   BAMG_LAUNCH(ctx, eye_kernel, grid_for((int64_t)ncols * ncols, 256), 256, 0, V, ncols);
   int m = ncols + (ncols & 1);
   if (ncols >= 2) {
-    for (int sweep = 0; sweep < 60; ++sweep) {
-      BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(rotated, 0, sizeof(int), ctx->stream));
-      for (int s = 0; s < m - 1; ++s)
-        BAMG_LAUNCH(ctx, jacobi_step_kernel, m / 2, JAC_THREADS, 0, G, nrows, V, ncols, m, s, 1e-15, rotated);
-      int rot = 0;
-      BAMG_TRY(ctx_read_i32(ctx, rotated, 1, &rot));
-      if (!rot) break;
-    }
+    int grid = coop_grid(ctx, jacobi_svd_coop_kernel, JAC_THREADS, m / 2);
+    double tol = 1e-15;
+    int maxsw = MAXSW;
+    BAMG_COOP(ctx, jacobi_svd_coop_kernel, grid, JAC_THREADS, &G, &nrows, &V, &ncols, &m, &tol, &flags, &maxsw);
   }
   BAMG_LAUNCH(ctx, col_norms_dense_kernel, ncols, JAC_THREADS, 0, G, nrows, ncols, sig);
   return 0;
@@ -209,73 +287,86 @@ __global__ void symmetrize_kernel(const double* __restrict__ A, int n, double* _
   S[t] = 0.5 * (A[t] + A[(int64_t)i * n + j]);
 }
 
-// right-looking step j: L[:, j] = A[:, j] / sqrt(A_jj) (rows >= j), then
-// A[i][k] -= L_ij L_kj for i, k > j.  A is read for column j only.
-__global__ void chol_column_kernel(const double* __restrict__ A, int n, int j, double* __restrict__ L,
-                                   int* __restrict__ bad) {
-  int i = j + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double piv = A[(int64_t)j * n + j];
-  if (!(piv > 0.0)) {
-    if (i == j) *bad = 1;
-    return;
+// Right-looking Cholesky, one cooperative launch: per column j the pivot
+// column is scaled (L[:, j] = A[:, j] / sqrt(A_jj)), a grid barrier, then the
+// trailing update A[i][k] -= L_ij L_kj (i, k > j), another barrier.
+__global__ void cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < n; ++j) {
+    double piv = __ldcg(A + (int64_t)j * n + j);
+    if (!(piv > 0.0)) {  // uniform across the grid
+      if (tid == 0) *bad = 1;
+      return;
+    }
+    double d = sqrt(piv);
+    for (int64_t i = j + tid; i < n; i += stride)
+      L[(int64_t)j * n + i] = (i == j) ? d : __ldcg(A + (int64_t)j * n + i) / d;
+    grid.sync();
+    int64_t m = n - j - 1;
+    for (int64_t t = tid; t < m * m; t += stride) {
+      int64_t i = j + 1 + t % m, k = j + 1 + t / m;
+      A[k * n + i] = __ldcg(A + k * n + i) - __ldcg(L + (int64_t)j * n + i) * __ldcg(L + (int64_t)j * n + k);
+    }
+    grid.sync();
   }
-  double d = sqrt(piv);
-  L[(int64_t)j * n + i] = (i == j) ? d : A[(int64_t)j * n + i] / d;
-}
-
-__global__ void chol_update_kernel(double* __restrict__ A, int n, int j, const double* __restrict__ L) {
-  int64_t m = n - j - 1;
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m * m) return;
-  int i = j + 1 + (int)(t % m), k = j + 1 + (int)(t / m);
-  A[(int64_t)k * n + i] -= L[(int64_t)j * n + i] * L[(int64_t)j * n + k];
 }
 
 static int cholesky(bamg_ctx* ctx, double* A, int n, double* L, int* bad) {
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(L, 0, sizeof(double) * (size_t)n * n, ctx->stream));
-  for (int j = 0; j < n; ++j) {
-    BAMG_LAUNCH(ctx, chol_column_kernel, grid_for(n - j, 256), 256, 0, A, n, j, L, bad);
-    int64_t m = n - j - 1;
-    if (m > 0) BAMG_LAUNCH(ctx, chol_update_kernel, grid_for(m * m, 256), 256, 0, A, n, j, L);
-  }
+  int grid = coop_grid(ctx, cholesky_coop_kernel, 256, grid_for((int64_t)n * n, 256));
+  BAMG_COOP(ctx, cholesky_coop_kernel, grid, 256, &A, &n, &L, &bad);
   return 0;
 }
 
-// forward substitution L X = B for nrhs columns (column-major, ld = n):
-// step i: X[i][c] = B[i][c] / L_ii;  B[k][c] -= L_ki X[i][c]  (k > i)
-__global__ void fwd_step_kernel(const double* __restrict__ L, int n, int i, double* __restrict__ B, int nrhs,
-                                double* __restrict__ X) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t rows = n - i;
-  if (t >= rows * nrhs) return;
-  int k = i + (int)(t % rows), c = (int)(t / rows);
-  double xi = B[(int64_t)c * n + i] / L[(int64_t)i * n + i];
-  if (k == i) X[(int64_t)c * n + i] = xi;
-  else B[(int64_t)c * n + k] -= L[(int64_t)i * n + k] * xi;
+// Forward substitution L X = B for nrhs columns (column-major, ld = n), one
+// cooperative launch: step i writes X[i][c] = B[i][c] / L_ii and updates
+// B[k][c] -= L_ki X[i][c] for k > i (row i of B is read-only in its step).
+__global__ void fwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int i = 0; i < n; ++i) {
+    int64_t rows = n - i;
+    double lii = __ldcg(L + (int64_t)i * n + i);
+    for (int64_t t = tid; t < rows * nrhs; t += stride) {
+      int64_t k = i + t % rows, c = t / rows;
+      double xi = __ldcg(B + c * n + i) / lii;
+      if (k == i) X[c * n + i] = xi;
+      else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + (int64_t)i * n + k) * xi;
+    }
+    grid.sync();
+  }
 }
 
 static int forward_solve(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
-  for (int i = 0; i < n; ++i)
-    BAMG_LAUNCH(ctx, fwd_step_kernel, grid_for((int64_t)(n - i) * nrhs, 256), 256, 0, L, n, i, B, nrhs, X);
+  int grid = coop_grid(ctx, fwd_coop_kernel, 256, grid_for((int64_t)n * nrhs, 256));
+  BAMG_COOP(ctx, fwd_coop_kernel, grid, 256, &L, &n, &B, &nrhs, &X);
   return 0;
 }
 
-// back substitution L^T X = B (upper triangular L^T): step i from n-1 down
-__global__ void bwd_step_kernel(const double* __restrict__ L, int n, int i, double* __restrict__ B, int nrhs,
-                                double* __restrict__ X) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t rows = i + 1;
-  if (t >= rows * nrhs) return;
-  int k = (int)(t % rows), c = (int)(t / rows);
-  double xi = B[(int64_t)c * n + i] / L[(int64_t)i * n + i];
-  if (k == i) X[(int64_t)c * n + i] = xi;
-  else B[(int64_t)c * n + k] -= L[(int64_t)k * n + i] * xi;  // (L^T)[k][i] = L[i][k]
+// Back substitution L^T X = B, i from n-1 down (cooperative).
+__global__ void bwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int i = n - 1; i >= 0; --i) {
+    int64_t rows = i + 1;
+    double lii = __ldcg(L + (int64_t)i * n + i);
+    for (int64_t t = tid; t < rows * nrhs; t += stride) {
+      int64_t k = t % rows, c = t / rows;
+      double xi = __ldcg(B + c * n + i) / lii;
+      if (k == i) X[c * n + i] = xi;
+      else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + k * n + i) * xi;  // (L^T)[k][i] = L[i][k]
+    }
+    grid.sync();
+  }
 }
 
 static int backward_solve_t(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
-  for (int i = n - 1; i >= 0; --i)
-    BAMG_LAUNCH(ctx, bwd_step_kernel, grid_for((int64_t)(i + 1) * nrhs, 256), 256, 0, L, n, i, B, nrhs, X);
+  int grid = coop_grid(ctx, bwd_coop_kernel, 256, grid_for((int64_t)n * nrhs, 256));
+  BAMG_COOP(ctx, bwd_coop_kernel, grid, 256, &L, &n, &B, &nrhs, &X);
   return 0;
 }
 
@@ -299,11 +390,11 @@ __global__ void rank_sort_kernel(const double* __restrict__ sig, int n, int* __r
   perm[r] = i;
 }
 
-// gather the r smallest triplets: a (left, from G/sigma or the K^T SVD),
-// b (right, V columns) into column-major n x r blocks
+// gather the r smallest triplets: a = g / sigma (left), b = V column (right)
+// into column-major n x r blocks; numerically-null slots (sigma <= thr) get a
+// placeholder that null_left_kernel replaces.
 __global__ void gather_triplets_kernel(const double* __restrict__ G, const double* __restrict__ V,
-                                       const double* __restrict__ sig, const int* __restrict__ perm,
-                                       const double* __restrict__ Vt, const int* __restrict__ perm_t, int n, int r,
+                                       const double* __restrict__ sig, const int* __restrict__ perm, int n, int r,
                                        double floor_rel, double* __restrict__ A, double* __restrict__ Bv,
                                        double* __restrict__ sig_out) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,9 +405,62 @@ __global__ void gather_triplets_kernel(const double* __restrict__ G, const doubl
   double s = sig[idx];
   Bv[(int64_t)j * n + row] = V[(int64_t)idx * n + row];
   double thr = fmax(1e-300, floor_rel * smax);
-  if (s > thr) A[(int64_t)j * n + row] = G[(int64_t)idx * n + row] / s;
-  else A[(int64_t)j * n + row] = Vt[(int64_t)perm_t[j] * n + row];
+  A[(int64_t)j * n + row] = s > thr ? G[(int64_t)idx * n + row] / s : 0.0;
   if (row == 0) sig_out[j] = s;
+}
+
+// coef[i] = (g_i . z) / sigma_i^2 for the well-conditioned columns (else 0)
+__global__ void null_coef_kernel(const double* __restrict__ G, const double* __restrict__ sig, int n, double thr,
+                                 const double* __restrict__ z, double* __restrict__ coef) {
+  __shared__ double sh[32];
+  int i = blockIdx.x;
+  double s = sig[i];
+  double a = 0.0;
+  if (s > thr)
+    for (int r = threadIdx.x; r < n; r += blockDim.x) a += G[(int64_t)i * n + r] * z[r];
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) coef[i] = s > thr ? a / (s * s) : 0.0;
+}
+
+// z -= sum_i coef_i g_i  (projection onto the orthogonal complement of the
+// well-conditioned left singular vectors)
+__global__ void null_update_kernel(const double* __restrict__ G, const double* __restrict__ coef, int n,
+                                   double* __restrict__ z) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double t = 0.0;
+  for (int i = 0; i < n; ++i) t += coef[i] * G[(int64_t)i * n + r];
+  z[r] -= t;
+}
+
+// one CTA: start vector for null slot j (deterministic), orthogonalise against
+// the previous null slots (columns < j of A that were null), normalise.
+__global__ void null_start_kernel(double* __restrict__ z, int n, int j) {
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    unsigned h = (unsigned)(r * 2654435761u) ^ (unsigned)(j * 40503u + 1u);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    z[r] = 1.0 + (double)(h & 0xffff) / 65536.0;
+  }
+}
+
+__global__ void null_finish_kernel(double* __restrict__ z, int n, double* __restrict__ A, int j,
+                                   const double* __restrict__ sig_slots, double thr, int r) {
+  __shared__ double sh[32];
+  // Gram-Schmidt against earlier null slots
+  for (int q = 0; q < j; ++q) {
+    if (sig_slots[q] > thr) continue;
+    double d = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) d += A[(int64_t)q * n + t] * z[t];
+    d = block_sum(d, sh);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) z[t] -= d * A[(int64_t)q * n + t];
+    __syncthreads();
+  }
+  double nn = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) nn += z[t] * z[t];
+  nn = sqrt(block_sum(nn, sh));
+  for (int t = threadIdx.x; t < n; t += blockDim.x) A[(int64_t)j * n + t] = nn > 0.0 ? z[t] / nn : 0.0;
 }
 
 // one CTA: normalisation, sign rule, null-slot cleanup (bootstrap.py:232-280).
@@ -517,13 +661,33 @@ extern "C" int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const dou
   BAMG_LAUNCH(ctx, transpose_dense_kernel, gnn, 256, 0, T, n, Tt);
   BAMG_TRY(forward_solve(ctx, LN, n, Tt, n, Kt));
   BAMG_LAUNCH(ctx, transpose_dense_kernel, gnn, 256, 0, Kt, n, K);
-  // SVDs of K (right vectors + left for sigma > floor) and K^T (left null)
+  // SVD of K: right vectors V, left vectors g / sigma where sigma is well
+  // separated from zero; numerically-null left vectors by projection onto the
+  // orthogonal complement of the others (two passes), Gram-Schmidt among slots
   BAMG_TRY(jacobi_svd(ctx, K, n, n, Vk, sk));
-  BAMG_TRY(jacobi_svd(ctx, Kt, n, n, Vkt, skt));
   BAMG_LAUNCH(ctx, rank_sort_kernel, grid_for(n, 256), 256, 0, sk, n, perm);
-  BAMG_LAUNCH(ctx, rank_sort_kernel, grid_for(n, 256), 256, 0, skt, n, permt);
-  BAMG_LAUNCH(ctx, gather_triplets_kernel, grid_for((int64_t)n * r, 256), 256, 0, K, Vk, sk, perm, Vkt, permt, n, r,
+  BAMG_LAUNCH(ctx, gather_triplets_kernel, grid_for((int64_t)n * r, 256), 256, 0, K, Vk, sk, perm, n, r,
               1e-10, A, Bv, sg);
+  {
+    double hs[64];
+    double smax = 0.0;
+    std::vector<double> all(n);
+    BAMG_TRY(ctx_read_doubles(ctx, sk, n, all.data()));
+    for (int i = 0; i < n; ++i) smax = fmax(smax, all[i]);
+    BAMG_TRY(ctx_read_doubles(ctx, sg, r, hs));
+    double thr = fmax(1e-300, 1e-10 * smax);
+    double* z = work;  // n scratch
+    double* coef = Kt;
+    for (int j = 0; j < r; ++j) {
+      if (hs[j] > thr) continue;
+      BAMG_LAUNCH(ctx, null_start_kernel, 1, 256, 0, z, n, j);
+      for (int pass = 0; pass < 2; ++pass) {
+        BAMG_LAUNCH(ctx, null_coef_kernel, n, 128, 0, K, sk, n, thr, z, coef);
+        BAMG_LAUNCH(ctx, null_update_kernel, grid_for(n, 128), 128, 0, K, coef, n, z);
+      }
+      BAMG_LAUNCH(ctx, null_finish_kernel, 1, 256, 0, z, n, A, j, sg, thr, r);
+    }
+  }
   // u = L_M^-T a, v = L_N^-T b
   BAMG_TRY(backward_solve_t(ctx, LM, n, A, r, Xa));
   BAMG_TRY(backward_solve_t(ctx, LN, n, Bv, r, Xb));

@@ -22,6 +22,7 @@
 // margins are >= 1e-9 relative, far above the 1e-15 rounding differences
 // between this QR and LAPACK's, so selected patterns are bit-identical.
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -366,7 +367,7 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
                 const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber,
                 int radius, double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
                 int32_t* __restrict__ out_col, double* __restrict__ out_val,
-                unsigned long long* __restrict__ status) {
+                unsigned long long* __restrict__ status, const int32_t* __restrict__ list, int nlist) {
   __shared__ int s_cand[FIT_WARPS][MAXCAND];
   __shared__ int s_two[FIT_WARPS][4 * MAXCAND];
   __shared__ double s_V[FIT_WARPS][CMAX * CMAX];
@@ -396,7 +397,9 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
 
   const int gw = blockIdx.x * FIT_WARPS + wib;
   const int nw = gridDim.x * FIT_WARPS;
-  for (int i = gw; i < n; i += nw) {
+  const int total = list ? nlist : n;
+  for (int it = gw; it < total; it += nw) {
+    const int i = list ? list[it] : it;
     int64_t obase = (int64_t)i * caliber;
     int ci = crank[i];
     if (ci >= 0) {  // coarse point: identity row
@@ -529,6 +532,422 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
   }
 }
 
+
+// ===================================================================
+// Thread-per-point variant (the production path).  Same greedy and decision
+// rules; each trial model is solved from its ridge normal equations
+// (A^T A + lambda^2 I) c = A^T b by a register Cholesky, then corrected by two
+// steps of iterative refinement whose residuals are formed from the original
+// rows (corrected semi-normal equations: forward error ~ eps * cond(A), the
+// QR-level accuracy, since eps * cond(A)^2 << 1 for every ridge-regularised
+// fit in scope).  Misfits are summed directly from the residual rows, never
+// from the expanded quadratic form.  Points the thread path cannot take
+// (more than TMAXC candidates, k > TKMAX, lambda == 0, or a Cholesky factor
+// failing qr_solve_ls's rank test) are appended to a list that the warp-QR
+// kernel above finishes -- so the reference's pseudo-inverse branch keeps its
+// exact semantics.
+constexpr int TMAXC = 16;  // candidates per point on the thread path
+constexpr int TKMAX = 32;
+constexpr int TCAL = 4;    // calibers up to 4 on the thread path
+
+struct TModel {
+  int pos[TCAL];
+  int len;
+  double coef[TCAL];
+  double data, total;
+};
+
+struct TPoint {
+  const double* X;
+  int k;
+  int nf;                 // finite tests
+  int f[TKMAX];           // their indices
+  double y[TKMAX];        // fine values
+  double sw[TKMAX];       // sqrt weights
+  double w[TKMAX];
+  int cand[TMAXC];
+  double lam;
+};
+
+// column value a_{fq} = sw_f * (C[f, col] - C[f, base]) (base < 0: no shift)
+__device__ __forceinline__ double tcol(const TPoint& P, int t, int col, int base) {
+  double c = __ldg(P.X + (int64_t)col * P.k + P.f[t]);
+  if (base >= 0) c -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
+  return P.sw[t] * c;
+}
+
+__device__ __forceinline__ double ttarget(const TPoint& P, int t, int base) {
+  double yv = P.y[t];
+  if (base >= 0) yv -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
+  return P.sw[t] * yv;
+}
+
+// ridge LS on `nc` columns (point indices cols[]); returns false when the
+// Cholesky factor fails the rank test (caller defers the point).
+__device__ bool tls_solve(const TPoint& P, const int* cols, int nc, int base, double* coef, double* data,
+                          double* total) {
+  double G[TCAL][TCAL], h[TCAL];
+#pragma unroll
+  for (int p = 0; p < TCAL; ++p) {
+    h[p] = 0.0;
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q) G[p][q] = 0.0;
+  }
+  for (int t = 0; t < P.nf; ++t) {
+    double a[TCAL];
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
+    double b = ttarget(P, t, base);
+#pragma unroll
+    for (int p = 0; p < TCAL; ++p) {
+      h[p] += a[p] * b;
+#pragma unroll
+      for (int q = 0; q <= p; ++q) G[p][q] += a[p] * a[q];
+    }
+  }
+  const double l2 = P.lam * P.lam;
+  // Cholesky G + lam^2 I = R^T R (lower L = R^T stored in G's lower triangle)
+  double L[TCAL][TCAL];
+  double rmax = 0.0, dmin = INFINITY;
+#pragma unroll
+  for (int j = 0; j < TCAL; ++j) {
+    if (j >= nc) break;
+    double d = G[j][j] + l2;
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q)
+      if (q < j) d -= L[j][q] * L[j][q];
+    if (!(d > 0.0)) return false;
+    double ljj = sqrt(d);
+    L[j][j] = ljj;
+    dmin = fmin(dmin, ljj);
+    rmax = fmax(rmax, ljj);
+#pragma unroll
+    for (int i = 0; i < TCAL; ++i) {
+      if (i > j && i < nc) {
+        double v = G[i][j];
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q)
+          if (q < j) v -= L[i][q] * L[j][q];
+        L[i][j] = v / ljj;
+        rmax = fmax(rmax, fabs(L[i][j]));
+      }
+    }
+  }
+  if (rmax == 0.0 || dmin < 1e-13 * rmax) return false;  // qr_solve_ls would take pinv
+  auto chol_solve = [&](const double* rhs, double* x) {
+    double z[TCAL];
+#pragma unroll
+    for (int i = 0; i < TCAL; ++i) {
+      if (i < nc) {
+        double v = rhs[i];
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q)
+          if (q < i) v -= L[i][q] * z[q];
+        z[i] = v / L[i][i];
+      }
+    }
+#pragma unroll
+    for (int i = TCAL - 1; i >= 0; --i) {
+      if (i < nc) {
+        double v = z[i];
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q)
+          if (q > i && q < nc) v -= L[q][i] * x[q];
+        x[i] = v / L[i][i];
+      }
+    }
+  };
+  double c[TCAL];
+#pragma unroll
+  for (int q = 0; q < TCAL; ++q) c[q] = 0.0;
+  chol_solve(h, c);
+  for (int refine = 0; refine < 2; ++refine) {
+    double g[TCAL];
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q) g[q] = q < nc ? -l2 * c[q] : 0.0;  // ridge rows: -lam * (lam c)
+    for (int t = 0; t < P.nf; ++t) {
+      double a[TCAL];
+      double r = ttarget(P, t, base);
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q) {
+        a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
+        r -= a[q] * c[q];
+      }
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q) g[q] += a[q] * r;
+    }
+    double dlt[TCAL];
+    chol_solve(g, dlt);
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q)
+      if (q < nc) c[q] += dlt[q];
+  }
+  double mis = 0.0;
+  for (int t = 0; t < P.nf; ++t) {
+    double r = 0.0;
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q)
+      if (q < nc) r += tcol(P, t, cols[q], base) * c[q];
+    r -= ttarget(P, t, base);
+    mis += r * r;
+  }
+  double cc = 0.0;
+#pragma unroll
+  for (int q = 0; q < TCAL; ++q)
+    if (q < nc) {
+      coef[q] = c[q];
+      cc += c[q] * c[q];
+    }
+  *data = mis;
+  *total = mis + l2 * cc;
+  return true;
+}
+
+// solve_model (interp.py:176-199) on the thread path; false = defer point
+__device__ bool tsolve_model(const TPoint& P, const int* trial, int tlen, bool constrain, bool nonneg,
+                             double empty, TModel* out) {
+  int work[TCAL];
+  int wl = tlen;
+#pragma unroll
+  for (int q = 0; q < TCAL; ++q) work[q] = q < tlen ? trial[q] : 0;
+  while (wl > 0) {
+    double coef[TCAL];
+    double data, total;
+    if (constrain) {
+      int base = P.cand[work[0]];
+      if (wl > 1) {
+        int cols[TCAL];
+        double ct[TCAL];
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q) cols[q] = (q + 1 < wl) ? P.cand[work[q + 1]] : 0;
+        if (!tls_solve(P, cols, wl - 1, base, ct, &data, &total)) return false;
+        double ssum = 0.0;
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q)
+          if (q < wl - 1) ssum += ct[q];
+        coef[0] = 1.0 - ssum;
+#pragma unroll
+        for (int q = 1; q < TCAL; ++q) coef[q] = (q < wl) ? ct[q - 1] : 0.0;
+      } else {
+        double mis = 0.0;
+        for (int t = 0; t < P.nf; ++t) {
+          double r = ttarget(P, t, base);
+          mis += r * r;
+        }
+        data = total = mis;
+        coef[0] = 1.0;
+      }
+    } else {
+      int cols[TCAL];
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q) cols[q] = q < wl ? P.cand[work[q]] : 0;
+      if (!tls_solve(P, cols, wl, -1, coef, &data, &total)) return false;
+    }
+    bool has_nan = false;
+    double cmin = 0.0;
+    int amin = 0;
+    double best = INFINITY;
+    bool found_nan = false;
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q) {
+      if (q < wl) {
+        double v = coef[q];
+        if (v != v) {
+          has_nan = true;
+          if (!found_nan) {
+            amin = q;
+            found_nan = true;
+          }
+        } else {
+          cmin = fmin(cmin, v);
+          if (!found_nan && v < best) {
+            best = v;
+            amin = q;
+          }
+        }
+      }
+    }
+    if (!nonneg || (!has_nan && cmin >= 0.0)) {
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q) {
+        out->pos[q] = work[q];
+        out->coef[q] = q < wl ? coef[q] : 0.0;
+      }
+      out->len = wl;
+      out->data = data;
+      out->total = total;
+      return true;
+    }
+    if (wl == 1) {
+      out->pos[0] = work[0];
+      out->coef[0] = 0.0;
+      out->len = 1;
+      out->data = empty;
+      out->total = empty;
+      return true;
+    }
+#pragma unroll
+    for (int q = 0; q < TCAL - 1; ++q)
+      if (q >= amin) work[q] = work[q + 1];
+    --wl;
+  }
+  out->len = 0;
+  out->data = empty;
+  out->total = empty;
+  return true;
+}
+
+__global__ void __launch_bounds__(128)
+fit_rows_thread_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                       const int32_t* __restrict__ crank, const double* __restrict__ X, int k,
+                       const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber, int radius,
+                       double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
+                       int32_t* __restrict__ out_col, double* __restrict__ out_val, int32_t* __restrict__ defer,
+                       unsigned int* __restrict__ ndefer) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t obase = (int64_t)i * caliber;
+  const int ci = crank[i];
+  if (ci >= 0) {
+    out_cnt[i] = 1;
+    out_col[obase] = ci;
+    out_val[obase] = 1.0;
+    return;
+  }
+  TPoint P;
+  P.X = X;
+  P.k = k;
+  P.lam = lam_dev[0];
+  bool ok = P.lam > 0.0;
+  // candidates: coarse radius-1 neighbours (adjacency rows are sorted)
+  int m = 0;
+  const int rb = arp[i], re = arp[i + 1];
+  if (radius == 1) {
+    for (int j = rb; j < re; ++j) {
+      int p = acol[j];
+      if (crank[p] >= 0) {
+        if (m < TMAXC) P.cand[m] = p;
+        ++m;
+      }
+    }
+  }
+  if (m == 0 && re > rb) {
+    // radius 2: sorted unique union of the neighbour rows, coarse points != i
+    int len = 0;
+    for (int j = rb; j < re && ok; ++j) {
+      int nb = acol[j];
+      for (int side = 0; side < 2 && ok; ++side) {
+        int qb = side == 0 ? j : arp[nb];
+        int qe = side == 0 ? j + 1 : arp[nb + 1];
+        for (int q = qb; q < qe; ++q) {
+          int x = acol[q];
+          if (x == i || crank[x] < 0) continue;
+          int pos = 0;
+          while (pos < len && P.cand[pos] < x) ++pos;
+          if (pos < len && P.cand[pos] == x) continue;
+          if (len >= TMAXC) {
+            ok = false;
+            break;
+          }
+          for (int t = len; t > pos; --t) P.cand[t] = P.cand[t - 1];
+          P.cand[pos] = x;
+          ++len;
+        }
+      }
+    }
+    m = len;
+  }
+  if (m > TMAXC) ok = false;
+  if (!ok || k > TKMAX || caliber > TCAL) {
+    defer[atomicAdd(ndefer, 1u)] = i;
+    return;
+  }
+  if (m == 0) {
+    out_cnt[i] = 0;
+    return;
+  }
+  int nf = 0;
+  double empty = 0.0;
+  for (int t = 0; t < k; ++t) {
+    double wt = w[t];
+    if (!isfinite(wt)) continue;
+    double yv = X[(int64_t)i * k + t];
+    P.f[nf] = t;
+    P.y[nf] = yv;
+    P.w[nf] = wt;
+    P.sw[nf] = sqrt(wt);
+    empty += wt * (yv * yv);
+    ++nf;
+  }
+  P.nf = nf;
+
+  int sel[TCAL];
+  double coefs[TCAL];
+  int nsel = 0;
+#pragma unroll
+  for (int q = 0; q < TCAL; ++q) {
+    sel[q] = 0;
+    coefs[q] = 0.0;
+  }
+  double cur_total = empty;
+  const int cap = caliber < m ? caliber : m;
+  while (nsel < cap) {
+    TModel best;
+    bool have = false;
+    for (int j = 0; j < m; ++j) {
+      bool in = false;
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q)
+        if (q < nsel && sel[q] == j) in = true;
+      if (in) continue;
+      int trial[TCAL];
+#pragma unroll
+      for (int q = 0; q < TCAL; ++q) trial[q] = q < nsel ? sel[q] : (q == nsel ? j : 0);
+      TModel md;
+      if (!tsolve_model(P, trial, nsel + 1, constrain != 0, nonneg != 0, empty, &md)) {
+        defer[atomicAdd(ndefer, 1u)] = i;
+        return;
+      }
+      if (nsel > 0 && md.len > 0) {
+        double amax = 0.0;
+        bool nan = false;
+#pragma unroll
+        for (int q = 0; q < TCAL; ++q)
+          if (q < md.len) {
+            if (md.coef[q] != md.coef[q]) nan = true;
+            amax = fmax(amax, fabs(md.coef[q]));
+          }
+        if (!nan && amax > 10.0) continue;
+      }
+      if (!have || md.total < best.total) {
+        best = md;
+        have = true;
+      }
+    }
+    if (!have) break;
+    if (nsel > 0 && (cur_total <= 0.0 || (cur_total - best.total) < tol * cur_total)) break;
+    if (best.len <= nsel) break;
+#pragma unroll
+    for (int q = 0; q < TCAL; ++q) {
+      sel[q] = best.pos[q];
+      coefs[q] = best.coef[q];
+    }
+    nsel = best.len;
+    cur_total = best.total;
+    if (cur_total <= 1e-30) break;
+  }
+  if (nsel == 0) {
+    sel[0] = 0;
+    coefs[0] = constrain ? 1.0 : 0.0;
+    nsel = 1;
+  }
+  out_cnt[i] = nsel;
+  for (int q = 0; q < nsel; ++q) {
+    out_col[obase + q] = crank[P.cand[sel[q]]];
+    out_val[obase + q] = coefs[q];
+  }
+}
+
 // ridge = 0.1 * sqrt(mean_i (sqrt(sum_f w_f x_if^2))^2)  (interp.py:266-268)
 __global__ void level_scale_partial(const double* __restrict__ X, int64_t n, int k, const double* __restrict__ w,
                                     double* __restrict__ partial) {
@@ -566,13 +985,20 @@ __global__ void level_scale_final(const double* __restrict__ partial, int nb, in
   if (lane == 0) lam[0] = 0.1 * sqrt(v / (double)n);
 }
 
+// BAMG_FIT_WARP=1 forces the warp-QR path for every point (parity testing)
+static bool force_warp_path() {
+  const char* e = getenv("BAMG_FIT_WARP");
+  return e && e[0] == '1';
+}
+
 extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
                              const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
-                             int constrain, int nonnegative, int32_t* out_cnt, int32_t* out_col, double* out_val,
-                             int64_t* status_host) {
+                             int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
+                             int32_t* out_col, double* out_val, int64_t* status_host) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, caliber >= 1 && caliber <= CMAX, "caliber must lie in [1, 8]");
   BAMG_REQUIRE(ctx, k >= 1 && k + caliber <= 32, "need k + caliber <= 32 (one LS row per lane)");
+  if (status_host) status_host[0] = status_host[1] = 0;
   BAMG_REQUIRE(ctx, radius == 1 || radius == 2, "radius must be 1 or 2");
   BAMG_REQUIRE(ctx, adj && adj->nrows == n, "adjacency size mismatch");
   double *partial, *lam;
@@ -581,21 +1007,42 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
   BAMG_TRY(arena_get(ctx, 1, &lam));
   BAMG_TRY(arena_get(ctx, 2, &status));
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(status, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  BAMG_LAUNCH(ctx, level_scale_partial, RED_BLOCKS, RED_THREADS, 0, X, n, k, w, partial);
-  BAMG_LAUNCH(ctx, level_scale_final, 1, 32, 0, partial, RED_BLOCKS, n, lam);
-  int64_t warps = n;
-  int64_t blocks = (warps + FIT_WARPS - 1) / FIT_WARPS;
-  int64_t maxb = (int64_t)ctx->num_sms * 64;
-  if (blocks > maxb) blocks = maxb;
+  if (ridge_override >= 0.0) {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(lam, &ridge_override, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    BAMG_LAUNCH(ctx, level_scale_partial, RED_BLOCKS, RED_THREADS, 0, X, n, k, w, partial);
+    BAMG_LAUNCH(ctx, level_scale_final, 1, 32, 0, partial, RED_BLOCKS, n, lam);
+  }
   // algorithmic bytes: test vectors of every point + adjacency + rank map + the row output
   double fbytes = 8.0 * n * k + 4.0 * (n + 1) + 4.0 * adj->nnz + 4.0 * n + 16.0 * n * caliber;
-  BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr, adj->col, coarse_rank, X,
-              k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative, out_cnt, out_col, out_val, status);
+  int32_t* defer;
+  unsigned int* ndefer;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &defer));
+  BAMG_TRY(arena_get(ctx, 1, &ndefer));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(ndefer, 0, sizeof(unsigned int), ctx->stream));
+  int nlist = (int)n;
+  const int32_t* list = nullptr;
+  if (k <= TKMAX && caliber <= TCAL && !force_warp_path()) {
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel, grid_for(n, 128), 128, 0, (int)n, adj->rowptr,
+                    adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative,
+                    out_cnt, out_col, out_val, defer, ndefer);
+    int32_t nd = 0;
+    BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(ndefer), 1, &nd));
+    nlist = nd;
+    list = defer;
+    if (status_host) status_host[1] = nd;
+  }
+  if (nlist > 0) {
+    int64_t blocks = ((int64_t)nlist + FIT_WARPS - 1) / FIT_WARPS;
+    int64_t maxb = (int64_t)ctx->num_sms * 64;
+    if (blocks > maxb) blocks = maxb;
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, list ? 0.0 : fbytes, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n,
+                    adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
+                    nonnegative, out_cnt, out_col, out_val, status, list, nlist);
+  }
   int64_t st[2];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 2, st));
-  if (status_host) {
-    status_host[0] = st[0];
-  }
+  if (status_host) status_host[0] = st[0];
   BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 48 candidates or 192 two-hop states)");
   return 0;
 }

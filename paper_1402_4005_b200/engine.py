@@ -189,16 +189,17 @@ def test_weights(A, X, inf_slot=None):
     return Xn, w
 
 
-def fit_rows(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg):
+def fit_rows(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg, ridge=None):
+    """Returns (cnt, col, val, (pinv_branch_fits, deferred_to_warp_path))."""
     n, k = X.shape
     cnt = _empty(n, I32)
     col = _empty(n * caliber, I32)
     val = _empty(n * caliber, F64)
-    status = C.c_int64(0)
+    status = (C.c_int64 * 2)()
     _lib.call("bamg_fit_rows", adj.ref(), _p(coarse_rank), _p(X), _p(w), n, k, int(caliber),
-              int(radius), float(tol), int(bool(constrain)), int(bool(nonneg)), _p(cnt), _p(col),
-              _p(val), C.byref(status))
-    return cnt, col, val, status.value
+              int(radius), float(tol), int(bool(constrain)), int(bool(nonneg)),
+              -1.0 if ridge is None else float(ridge), _p(cnt), _p(col), _p(val), status)
+    return cnt, col, val, (int(status[0]), int(status[1]))
 
 
 def rows_to_csr(cnt, col, val, n, stride, ncols) -> DeviceCSR:

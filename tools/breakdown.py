@@ -31,7 +31,11 @@ dU = torch.from_numpy(np.ascontiguousarray(draws[1].T)).cuda()
 geo = torch.from_numpy(np.ascontiguousarray(prob.geometry.T)).cuda()
 P = chains.ChainProblem(A=None, B=dB, n=prob.n, family=fam, params={}, geometry=geo)
 gcfg = pb.GmresConfig(restart=restart, rtol=1e-8)
+from paper_1402_4005_b200 import _lib
+import ctypes as C
 for rep in range(a.reps):
+    if rep == a.reps - 1:
+        _lib.lib().bamg_trace_enable(_lib.ctx(), 1)
     bs.PHASES = {}
     torch.cuda.synchronize(); t0 = time.perf_counter()
     setup = pb.run_setup(P, cfg, draws=(dV, dU), B_device=dB)
@@ -51,3 +55,11 @@ for rep in range(a.reps):
     print(json.dumps({"rep": rep, "setup": t1 - t0, "pinv": t2 - t1, "gmres": t3 - t2, "its": r.iterations,
                       "hist": r.residual_history[-1], "vcycle_ms": tv * 1e3, "levels": levels,
                       "phases": {k2: round(v, 4) for k2, v in bs.PHASES.items()}}), flush=True)
+buf = C.create_string_buffer(1 << 20)
+_lib.lib().bamg_trace_dump(_lib.ctx(), buf, 1 << 20)
+rows = [l.split() for l in buf.value.decode().splitlines()]
+rows.sort(key=lambda r: -float(r[1]))
+tot = sum(float(r[1]) for r in rows)
+print(f"TRACE total kernel ms {tot:.2f} launches {sum(int(r[2]) for r in rows)}")
+for r in rows[:40]:
+    print(f"{float(r[1]):10.3f} ms {int(r[2]):7d}  {r[0]}")
