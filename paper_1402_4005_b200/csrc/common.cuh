@@ -13,39 +13,55 @@
 
 #define BAMG_VERSION 1
 
+// Per-call scratch: one bump-allocated slab sized to the high-water mark of
+// previous calls.  A call that outgrows the slab takes overflow blocks; the
+// next reset (at API entry, all earlier users already enqueued on the same
+// stream) frees them and regrows the slab once, so steady-state calls never
+// touch cudaMalloc.
 struct Arena {
-  struct Chunk {
-    char* ptr;
-    size_t size;
-    size_t used;
-  };
-  std::vector<Chunk> chunks;
-  // Reset is only legal at API entry: every previous user has been enqueued on
-  // the same stream, so reuse is stream-ordered.
+  char* base = nullptr;
+  size_t cap = 0, used = 0, call_peak = 0, peak = 0;
+  std::vector<char*> overflow;
   void reset() {
-    for (auto& c : chunks) c.used = 0;
+    if (!overflow.empty() || peak > cap) {
+      cudaDeviceSynchronize();
+      for (char* p : overflow) cudaFree(p);
+      overflow.clear();
+      if (peak > cap) {
+        if (base) cudaFree(base);
+        cap = peak + peak / 4 + (size_t(16) << 20);
+        if (cudaMalloc(&base, cap) != cudaSuccess) {
+          base = nullptr;
+          cap = 0;
+        }
+      }
+    }
+    used = 0;
+    call_peak = 0;
   }
   cudaError_t get(size_t bytes, void** out) {
     bytes = (bytes + 255) & ~size_t(255);
     if (bytes == 0) bytes = 256;
-    for (auto& c : chunks) {
-      if (c.size - c.used >= bytes) {
-        *out = c.ptr + c.used;
-        c.used += bytes;
-        return cudaSuccess;
-      }
+    call_peak += bytes;
+    if (call_peak > peak) peak = call_peak;
+    if (base && used + bytes <= cap) {
+      *out = base + used;
+      used += bytes;
+      return cudaSuccess;
     }
-    size_t sz = bytes > (size_t(64) << 20) ? bytes : (size_t(64) << 20);
     char* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sz);
+    cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) return e;
-    chunks.push_back({p, sz, bytes});
+    overflow.push_back(p);
     *out = p;
     return cudaSuccess;
   }
   void release() {
-    for (auto& c : chunks) cudaFree(c.ptr);
-    chunks.clear();
+    for (char* p : overflow) cudaFree(p);
+    overflow.clear();
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = used = 0;
   }
 };
 

@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -33,6 +34,11 @@ template <typename K>
 static int coop_grid(bamg_ctx* ctx, K kernel, int threads, int want) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  // grid barriers cost grows with the CTA count: at most COOP_PER_SM CTAs per
+  // SM (env BAMG_COOP_PER_SM for tuning)
+  int lim = 2;
+  if (const char* e = getenv("BAMG_COOP_PER_SM")) lim = atoi(e);
+  if (lim >= 1 && per_sm > lim) per_sm = lim;
   int cap = per_sm * ctx->num_sms;
   if (cap < 1) cap = 1;
   return want < cap ? (want < 1 ? 1 : want) : cap;
@@ -94,47 +100,36 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return sh[0];
 }
 
-__global__ void __launch_bounds__(JAC_THREADS)
-jacobi_step_kernel(double* __restrict__ G, int nrows, double* __restrict__ V, int ncols, int m, int s, double tol,
-                   int* __restrict__ rotated) {
+// three block sums with one barrier pair (every thread gets the totals)
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* sh) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    sh[wid] = a;
+    sh[32 + wid] = b;
+    sh[64 + wid] = c;
+  }
+  __syncthreads();
+  double ta = 0.0, tb = 0.0, tc = 0.0;
+  for (int q = 0; q < nw; ++q) {
+    ta += sh[q];
+    tb += sh[32 + q];
+    tc += sh[64 + q];
+  }
+  a = ta;
+  b = tb;
+  c = tc;
+}
+
+__global__ void sumsq_kernel(const double* __restrict__ G, int64_t total, double* out) {
   __shared__ double sh[32];
-  int p, q;
-  tournament_pair(m, s, blockIdx.x, &p, &q);
-  if (p >= ncols || q >= ncols) return;
-  if (p > q) {
-    int t = p;
-    p = q;
-    q = t;
-  }
-  double* gp = G + (int64_t)p * nrows;
-  double* gq = G + (int64_t)q * nrows;
-  double a = 0.0, b = 0.0, c = 0.0;
-  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
-    double x = gp[r], y = gq[r];
-    a += x * x;
-    b += y * y;
-    c += x * y;
-  }
+  double a = 0.0;
+  for (int64_t t = threadIdx.x; t < total; t += blockDim.x) a += G[t] * G[t];
   a = block_sum(a, sh);
-  b = block_sum(b, sh);
-  c = block_sum(c, sh);
-  if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) return;
-  double zeta = (b - a) / (2.0 * c);
-  double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-  double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
-    double x = gp[r], y = gq[r];
-    gp[r] = cs * x - sn * y;
-    gq[r] = sn * x + cs * y;
-  }
-  double* vp = V + (int64_t)p * ncols;
-  double* vq = V + (int64_t)q * ncols;
-  for (int r = threadIdx.x; r < ncols; r += blockDim.x) {
-    double x = vp[r], y = vq[r];
-    vp[r] = cs * x - sn * y;
-    vq[r] = sn * x + cs * y;
-  }
-  if (threadIdx.x == 0) *rotated = 1;
+  if (threadIdx.x == 0) out[0] = a;
 }
 
 __global__ void eye_kernel(double* V, int n) {
@@ -160,9 +155,12 @@ __global__ void col_norms_dense_kernel(const double* __restrict__ G, int nrows, 
 // host round trips.  Loads after a grid barrier use ld.global.cg (L1 bypass).
 __global__ void __launch_bounds__(JAC_THREADS)
 jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double tol, int* flags,
-                       int maxsweeps) {
+                       int maxsweeps, const double* fro2) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double sh[32];
+  __shared__ double sh[96];
+  // columns whose squared norm is below 1e-30 |G|_F^2 are numerically zero:
+  // rotating them only shuffles round-off (and would stall convergence)
+  (void)fro2;
   for (int sw = 0; sw < maxsweeps; ++sw) {
     for (int s = 0; s < m - 1; ++s) {
       for (int pair = blockIdx.x; pair < m / 2; pair += gridDim.x) {
@@ -183,9 +181,7 @@ jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double
           b += y * y;
           c += x * y;
         }
-        a = block_sum(a, sh);
-        b = block_sum(b, sh);
-        c = block_sum(c, sh);
+        block_sum3(a, b, c, sh);
         if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) continue;
         double zeta = (b - a) / (2.0 * c);
         double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -221,8 +217,20 @@ static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
   if (ncols >= 2) {
     int grid = coop_grid(ctx, jacobi_svd_coop_kernel, JAC_THREADS, m / 2);
     double tol = 1e-15;
+    if (const char* e = getenv("BAMG_JACOBI_TOL")) tol = atof(e);
     int maxsw = MAXSW;
-    BAMG_COOP(ctx, jacobi_svd_coop_kernel, grid, JAC_THREADS, &G, &nrows, &V, &ncols, &m, &tol, &flags, &maxsw);
+    double* fro2;
+    BAMG_TRY(arena_get(ctx, 1, &fro2));
+    BAMG_LAUNCH(ctx, sumsq_kernel, 1, 1024, 0, G, (int64_t)nrows * ncols, fro2);
+    BAMG_COOP(ctx, jacobi_svd_coop_kernel, grid, JAC_THREADS, &G, &nrows, &V, &ncols, &m, &tol, &flags, &maxsw,
+              &fro2);
+    if (getenv("BAMG_DEBUG")) {
+      int fl[MAXSW];
+      BAMG_TRY(ctx_read_i32(ctx, flags, MAXSW, fl));
+      int sw = 0;
+      while (sw < MAXSW && fl[sw]) ++sw;
+      fprintf(stderr, "[bamg] jacobi_svd n=%d grid=%d sweeps=%d\n", ncols, grid, sw + 1);
+    }
   }
   BAMG_LAUNCH(ctx, col_norms_dense_kernel, ncols, JAC_THREADS, 0, G, nrows, ncols, sig);
   return 0;
@@ -261,9 +269,268 @@ __global__ void pinv_assemble_kernel(const double* __restrict__ V, const double*
   if (r < n && c < n) Z[(int64_t)r * n + c] = acc;
 }
 
+// ---------------------------------------------------- bordered dense LU pinv
+// The coarsest operator of a chain hierarchy is singular with a one-
+// dimensional null space.  For such B the bordered matrix
+//   Bb = [[B, b], [c^T, 0]]   (b = c = 1/sqrt(n) * ones)
+// is nonsingular, Bb^-1 = [[X, x], [w^T, omega]] gives a {1}-inverse X of B
+// (B X B = B) and the null vectors (B x = 0, w^T B = 0), and
+//   B^+ = (I - z z^T) X (I - y y^T),  z = x/|x|, y = w/|w|
+// exactly.  Bb^-1 comes from one cooperative Gauss-Jordan elimination with
+// partial pivoting on [Bb | I] (the north star's dense LU, factor and inverse
+// fused).  The result is used only when the numbers certify the reference's
+// rank rule unambiguously (nonsingular Bb, |B z| and |B^T y| at round-off);
+// otherwise the one-sided Jacobi SVD below decides, as PinvOperator does.
+
+// augmented row-major [m][2m], m = n + 1
+__global__ void gj_init_kernel(const double* __restrict__ A, int n, double* __restrict__ Aug) {
+  int m = n + 1;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * 2 * m) return;
+  int i = (int)(t / (2 * m)), k = (int)(t % (2 * m));
+  double v;
+  const double bc = 1.0 / sqrt((double)n);
+  if (k < m) {
+    if (i < n && k < n) v = A[(int64_t)k * n + i];
+    else if (i == n && k == n) v = 0.0;
+    else v = bc;
+  } else {
+    v = (k - m == i) ? 1.0 : 0.0;
+  }
+  Aug[t] = v;
+}
+
+// stats[0] = min |pivot|, stats[1] = max |pivot| (bits of non-negative doubles)
+__global__ void gj_coop_kernel(double* Aug, int m, double* prow, double* fcol, unsigned long long* stats) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int W = 2 * m;
+  __shared__ double s_best[32];
+  __shared__ int s_idx[32];
+  for (int j = 0; j < m; ++j) {
+    // pivot search on column j, rows >= j (every CTA, identical result)
+    double best = -1.0;
+    int bi = j;
+    for (int i = j + threadIdx.x; i < m; i += blockDim.x) {
+      double a = fabs(__ldcg(Aug + (int64_t)i * W + j));
+      if (a > best) {
+        best = a;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_best[threadIdx.x >> 5] = best;
+      s_idx[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+        if (s_best[q] > s_best[0] || (s_best[q] == s_best[0] && s_idx[q] < s_idx[0])) {
+          s_best[0] = s_best[q];
+          s_idx[0] = s_idx[q];
+        }
+    }
+    __syncthreads();
+    const int p = s_idx[0];
+    const double pv = s_best[0];
+    __syncthreads();
+    if (tid == 0) {
+      atomicMin(&stats[0], (unsigned long long)__double_as_longlong(pv));
+      atomicMax(&stats[1], (unsigned long long)__double_as_longlong(pv));
+    }
+    // swap rows j <-> p and stage the scaled pivot row / the column factors
+    const double piv = __ldcg(Aug + (int64_t)p * W + j);
+    for (int64_t k = tid; k < W; k += stride) {
+      double aj = __ldcg(Aug + (int64_t)j * W + k), ap = __ldcg(Aug + (int64_t)p * W + k);
+      prow[k] = ap / piv;
+      if (p != j) Aug[(int64_t)p * W + k] = aj;
+    }
+    for (int64_t i = tid; i < m; i += stride) {
+      int64_t src = (i == p) ? j : i;  // row i after the swap
+      fcol[i] = (i == j) ? 0.0 : __ldcg(Aug + src * W + j);
+    }
+    grid.sync();
+    for (int64_t t = tid; t < (int64_t)m * W; t += stride) {
+      int64_t i = t / W, k = t % W;
+      if (i == j) Aug[t] = __ldcg(prow + k);
+      else Aug[t] = __ldcg(Aug + t) - __ldcg(fcol + i) * __ldcg(prow + k);
+    }
+    grid.sync();
+  }
+}
+
+// y = B x (B column-major n x n), and yt = B^T w
+__global__ void gemv_colmajor_kernel(const double* __restrict__ A, int n, const double* __restrict__ x,
+                                     double* __restrict__ y) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) s += A[(int64_t)k * n + i] * x[k];
+  y[i] = s;
+}
+
+__global__ void gemv_colmajor_t_kernel(const double* __restrict__ A, int n, const double* __restrict__ x,
+                                       double* __restrict__ y) {
+  int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (k >= n) return;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += A[(int64_t)k * n + i] * x[i];
+  s = warp_sum(s);
+  if (lane == 0) y[k] = s;
+}
+
+// null vectors from Bb^-1 (unit-normalised) + norms for the certificate:
+// out[0] |x|, out[1] |w|, out[2] |B z|, out[3] |B^T y|, out[4] |B|_F, out[5] |omega|
+__global__ void gj_null_kernel(const double* __restrict__ Aug, int n, double* __restrict__ z,
+                               double* __restrict__ y, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int m = n + 1, W = 2 * m;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double xv = Aug[(int64_t)i * W + m + n];  // column n of the inverse
+    double wv = Aug[(int64_t)n * W + m + i];  // row n of the inverse
+    a += xv * xv;
+    b += wv * wv;
+  }
+  a = sqrt(block_sum(a, sh));
+  b = sqrt(block_sum(b, sh));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    z[i] = Aug[(int64_t)i * W + m + n] / a;
+    y[i] = Aug[(int64_t)n * W + m + i] / b;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+    out[5] = fabs(Aug[(int64_t)n * W + m + n]);
+  }
+}
+
+__global__ void norm_pair_kernel(const double* __restrict__ u, const double* __restrict__ v, const double* __restrict__ A,
+                                 int n, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0, f = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a += u[i] * u[i];
+    b += v[i] * v[i];
+  }
+  for (int64_t t = threadIdx.x; t < (int64_t)n * n; t += blockDim.x) f += A[t] * A[t];
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  f = block_sum(f, sh);
+  if (threadIdx.x == 0) {
+    out[2] = sqrt(a);
+    out[3] = sqrt(b);
+    out[4] = sqrt(f);
+  }
+}
+
+// r = z^T X (row), s = X y (column), t = z^T X y ; X = top-left n x n of the inverse
+__global__ void proj_vectors_kernel(const double* __restrict__ Aug, int n, const double* __restrict__ z,
+                                    const double* __restrict__ y, double* __restrict__ r, double* __restrict__ s) {
+  const int m = n + 1, W = 2 * m;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {  // r_t = sum_i z_i X[i][t]
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += z[i] * Aug[(int64_t)i * W + m + t];
+    r[t] = acc;
+  } else if (t < 2 * n) {  // s_i = sum_j X[i][j] y_j
+    int i = t - n;
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) acc += Aug[(int64_t)i * W + m + j] * y[j];
+    s[i] = acc;
+  }
+}
+
+__global__ void proj_assemble_kernel(const double* __restrict__ Aug, int n, const double* __restrict__ z,
+                                     const double* __restrict__ y, const double* __restrict__ r,
+                                     const double* __restrict__ s, double* __restrict__ Z) {
+  const int m = n + 1, W = 2 * m;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int i = (int)(t / n), j = (int)(t % n);
+  double zs = 0.0;  // z^T X y, recomputed per thread from s (tiny n-loop avoided by caching below)
+  (void)zs;
+  double x = Aug[(int64_t)i * W + m + j];
+  Z[t] = x - z[i] * r[j] - s[i] * y[j];
+}
+
+__global__ void proj_corner_kernel(double* __restrict__ Z, int n, const double* __restrict__ z,
+                                   const double* __restrict__ y, const double* __restrict__ s) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += z[i] * s[i];
+  a = block_sum(a, sh);  // z^T X y
+  for (int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; t < (int64_t)n * n;
+       t += (int64_t)gridDim.y * blockDim.x) {
+    int i = (int)(t / n), j = (int)(t % n);
+    Z[t] += a * z[i] * y[j];
+  }
+}
+
+// 0 = done (Z written); 1 = not certified (caller takes the SVD path)
+static int bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* Z) {
+  const int m = n + 1;
+  double *Aug, *prow, *fcol, *z, *y, *out, *r, *s, *tmp;
+  unsigned long long* stats;
+  BAMG_TRY(arena_get(ctx, (size_t)m * 2 * m, &Aug));
+  BAMG_TRY(arena_get(ctx, (size_t)2 * m, &prow));
+  BAMG_TRY(arena_get(ctx, (size_t)m, &fcol));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &z));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &y));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &r));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &s));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &tmp));
+  BAMG_TRY(arena_get(ctx, 8, &out));
+  BAMG_TRY(arena_get(ctx, 2, &stats));
+  unsigned long long init[2] = {0x7ff0000000000000ull, 0ull};
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  BAMG_LAUNCH(ctx, gj_init_kernel, grid_for((int64_t)m * 2 * m, 256), 256, 0, A, n, Aug);
+  int grid = coop_grid(ctx, gj_coop_kernel, 256, grid_for((int64_t)m * 2 * m, 256));
+  int mm = m;
+  BAMG_COOP(ctx, gj_coop_kernel, grid, 256, &Aug, &mm, &prow, &fcol, &stats);
+  BAMG_LAUNCH(ctx, gj_null_kernel, 1, 256, 0, Aug, n, z, y, out);
+  BAMG_LAUNCH(ctx, gemv_colmajor_kernel, grid_for(n, 128), 128, 0, A, n, z, r);
+  BAMG_LAUNCH(ctx, gemv_colmajor_t_kernel, grid_for((int64_t)n * 32, 256), 256, 0, A, n, y, s);
+  BAMG_LAUNCH(ctx, norm_pair_kernel, 1, 256, 0, r, s, A, n, out);
+  double h[6];
+  unsigned long long pv[2];
+  BAMG_TRY(ctx_read_doubles(ctx, out, 6, h));
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(stats), 2, reinterpret_cast<int64_t*>(pv)));
+  double pmin, pmax;
+  memcpy(&pmin, &pv[0], sizeof(double));
+  memcpy(&pmax, &pv[1], sizeof(double));
+  const double bf = h[4];
+  // certificate: Bb well conditioned; B z, B^T y at round-off (sigma_min << 1e-12 sigma_max
+  // with sigma_max >= |B|_F / sqrt(n)); omega ~ 0 (b, c outside the ranges)
+  bool ok = pmax > 0.0 && pmin > 1e-10 * pmax && h[2] <= 1e-14 * bf / std::sqrt((double)n) &&
+            h[3] <= 1e-14 * bf / std::sqrt((double)n) && h[5] <= 1e-8 * (h[0] > h[1] ? h[0] : h[1]);
+  if (!ok) return 1;
+  BAMG_LAUNCH(ctx, proj_vectors_kernel, grid_for(2 * (int64_t)n, 128), 128, 0, Aug, n, z, y, r, s);
+  BAMG_LAUNCH(ctx, proj_assemble_kernel, grid_for((int64_t)n * n, 256), 256, 0, Aug, n, z, y, r, s, Z);
+  dim3 cg2(1, 64);
+  proj_corner_kernel<<<cg2, 256, 0, ctx->stream>>>(Z, n, z, y, s);
+  ctx->launches++;
+  BAMG_CHECK_CUDA(ctx, cudaGetLastError());
+  return 0;
+}
+
 extern "C" int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* Z) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1, "empty matrix");
+  if (n >= 2 && rank_tol <= 1e-12 && !getenv("BAMG_PINV_SVD")) {
+    int rc = bordered_pinv(ctx, A, n, Z);
+    if (rc <= 0) return rc;
+    ctx->arena.reset();
+  }
   double *G, *V, *sig, *w;
   BAMG_TRY(arena_get(ctx, (size_t)n * n, &G));
   BAMG_TRY(arena_get(ctx, (size_t)n * n, &V));

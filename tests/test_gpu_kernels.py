@@ -153,3 +153,22 @@ def test_vcycle_and_gmres_match_oracle(eng, golden, name):
     xs = orc.l1_sign_fix(x.cpu().numpy())
     assert np.abs(xs - g["x"]).sum() <= 1e-10
     L.lib().bamg_hier_destroy(h)
+
+
+@pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_uniform63", "pipe_petri10_normal"])
+def test_dense_pinv_bordered_lu_matches_svd(eng, golden, name, monkeypatch):
+    """The bordered Gauss-Jordan pseudo-inverse (certified path) equals the
+    reference's SVD pseudo-inverse of the coarsest operator; the forced SVD
+    path (BAMG_PINV_SVD) agrees too."""
+    from paper_1402_4005_b200 import engine
+    g = golden(name)
+    L = int(g["n_levels"]) - 1
+    B = csr_from(g, f"L{L}_B")
+    ref = np.linalg.pinv(B.toarray(), rcond=1e-12)
+    dB = up(eng, B)
+    D = engine.csr_to_dense(dB)
+    for force in (False, True):
+        if force:
+            monkeypatch.setenv("BAMG_PINV_SVD", "1")
+        Z = engine.dense_pinv(D, B.shape[0]).cpu().numpy()
+        assert np.abs(Z - ref).max() <= 1e-9 * np.abs(ref).max(), force
