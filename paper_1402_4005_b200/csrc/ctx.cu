@@ -368,7 +368,7 @@ extern "C" int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap) {
     a.second += 1;
   }
   std::string out;
-  for (auto& kv : agg) out += kv.first + " " + std::to_string(kv.second.first) + " " + std::to_string(kv.second.second) + "\n";
+  for (auto& kv : agg) out += kv.first + "\t" + std::to_string(kv.second.first) + "\t" + std::to_string(kv.second.second) + "\n";
   int64_t len = (int64_t)out.size();
   if (len >= cap) len = cap - 1;
   memcpy(buf, out.data(), len);

@@ -557,26 +557,28 @@ struct TModel {
   double data, total;
 };
 
+template <int KM>
 struct TPoint {
   const double* X;
   int k;
-  int nf;                 // finite tests
-  int f[TKMAX];           // their indices
-  double y[TKMAX];        // fine values
-  double sw[TKMAX];       // sqrt weights
-  double w[TKMAX];
+  int nf;               // finite tests
+  int f[KM];            // their indices
+  double y[KM];         // fine values
+  double sw[KM];        // sqrt weights
   int cand[TMAXC];
   double lam;
 };
 
 // column value a_{fq} = sw_f * (C[f, col] - C[f, base]) (base < 0: no shift)
-__device__ __forceinline__ double tcol(const TPoint& P, int t, int col, int base) {
+template <int KM>
+__device__ __forceinline__ double tcol(const TPoint<KM>& P, int t, int col, int base) {
   double c = __ldg(P.X + (int64_t)col * P.k + P.f[t]);
   if (base >= 0) c -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
   return P.sw[t] * c;
 }
 
-__device__ __forceinline__ double ttarget(const TPoint& P, int t, int base) {
+template <int KM>
+__device__ __forceinline__ double ttarget(const TPoint<KM>& P, int t, int base) {
   double yv = P.y[t];
   if (base >= 0) yv -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
   return P.sw[t] * yv;
@@ -584,7 +586,8 @@ __device__ __forceinline__ double ttarget(const TPoint& P, int t, int base) {
 
 // ridge LS on `nc` columns (point indices cols[]); returns false when the
 // Cholesky factor fails the rank test (caller defers the point).
-__device__ bool tls_solve(const TPoint& P, const int* cols, int nc, int base, double* coef, double* data,
+template <int KM>
+__device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base, double* coef, double* data,
                           double* total) {
   double G[TCAL][TCAL], h[TCAL];
 #pragma unroll
@@ -704,7 +707,8 @@ __device__ bool tls_solve(const TPoint& P, const int* cols, int nc, int base, do
 }
 
 // solve_model (interp.py:176-199) on the thread path; false = defer point
-__device__ bool tsolve_model(const TPoint& P, const int* trial, int tlen, bool constrain, bool nonneg,
+template <int KM>
+__device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bool constrain, bool nonneg,
                              double empty, TModel* out) {
   int work[TCAL];
   int wl = tlen;
@@ -797,24 +801,40 @@ __device__ bool tsolve_model(const TPoint& P, const int* trial, int tlen, bool c
   return true;
 }
 
-__global__ void __launch_bounds__(128)
-fit_rows_thread_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+// coarse points: identity rows; fine points: appended to the work list
+__global__ void fit_prepare_kernel(int n, const int32_t* __restrict__ crank, int caliber, int32_t* __restrict__ out_cnt,
+                                   int32_t* __restrict__ out_col, double* __restrict__ out_val,
+                                   int32_t* __restrict__ list, unsigned int* __restrict__ nlist) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int ci = crank[i];
+  if (ci >= 0) {
+    int64_t o = (int64_t)i * caliber;
+    out_cnt[i] = 1;
+    out_col[o] = ci;
+    out_val[o] = 1.0;
+  } else {
+    list[atomicAdd(nlist, 1u)] = i;
+  }
+}
+
+#ifndef BAMG_FIT_MINBLOCKS
+#define BAMG_FIT_MINBLOCKS 3
+#endif
+template <int KM>
+__global__ void __launch_bounds__(128, BAMG_FIT_MINBLOCKS)
+fit_rows_thread_kernel(const int32_t* __restrict__ list, const unsigned int* __restrict__ nlist,
+                       const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
                        const int32_t* __restrict__ crank, const double* __restrict__ X, int k,
                        const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber, int radius,
                        double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
                        int32_t* __restrict__ out_col, double* __restrict__ out_val, int32_t* __restrict__ defer,
                        unsigned int* __restrict__ ndefer) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int)*nlist) return;
+  const int i = list[t];
   const int64_t obase = (int64_t)i * caliber;
-  const int ci = crank[i];
-  if (ci >= 0) {
-    out_cnt[i] = 1;
-    out_col[obase] = ci;
-    out_val[obase] = 1.0;
-    return;
-  }
-  TPoint P;
+  TPoint<KM> P;
   P.X = X;
   P.k = k;
   P.lam = lam_dev[0];
@@ -858,7 +878,7 @@ fit_rows_thread_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __
     m = len;
   }
   if (m > TMAXC) ok = false;
-  if (!ok || k > TKMAX || caliber > TCAL) {
+  if (!ok || k > KM || caliber > TCAL) {
     defer[atomicAdd(ndefer, 1u)] = i;
     return;
   }
@@ -868,13 +888,12 @@ fit_rows_thread_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __
   }
   int nf = 0;
   double empty = 0.0;
-  for (int t = 0; t < k; ++t) {
-    double wt = w[t];
+  for (int tt = 0; tt < k; ++tt) {
+    double wt = w[tt];
     if (!isfinite(wt)) continue;
-    double yv = X[(int64_t)i * k + t];
-    P.f[nf] = t;
+    double yv = X[(int64_t)i * k + tt];
+    P.f[nf] = tt;
     P.y[nf] = yv;
-    P.w[nf] = wt;
     P.sw[nf] = sqrt(wt);
     empty += wt * (yv * yv);
     ++nf;
@@ -1023,9 +1042,22 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
   int nlist = (int)n;
   const int32_t* list = nullptr;
   if (k <= TKMAX && caliber <= TCAL && !force_warp_path()) {
-    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel, grid_for(n, 128), 128, 0, (int)n, adj->rowptr,
-                    adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative,
-                    out_cnt, out_col, out_val, defer, ndefer);
+    int32_t* flist;
+    unsigned int* nfl;
+    BAMG_TRY(arena_get(ctx, (size_t)n + 1, &flist));
+    BAMG_TRY(arena_get(ctx, 1, &nfl));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nfl, 0, sizeof(unsigned int), ctx->stream));
+    BAMG_LAUNCH(ctx, fit_prepare_kernel, grid_for(n, 256), 256, 0, (int)n, coarse_rank, caliber, out_cnt, out_col,
+                out_val, flist, nfl);
+    if (k <= 16) {
+      BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<16>, grid_for(n, 128), 128, 0, flist, nfl,
+                      adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
+                      nonnegative, out_cnt, out_col, out_val, defer, ndefer);
+    } else {
+      BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<TKMAX>, grid_for(n, 128), 128, 0, flist, nfl,
+                      adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
+                      nonnegative, out_cnt, out_col, out_val, defer, ndefer);
+    }
     int32_t nd = 0;
     BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(ndefer), 1, &nd));
     nlist = nd;

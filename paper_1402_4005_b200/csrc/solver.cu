@@ -16,6 +16,7 @@
 // residual ||Bx||/||x|| every iteration (one 3-double device->host read per
 // iteration, the only host synchronisation of the solve).
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -31,6 +32,16 @@ struct HLevel {
   double* r = nullptr;   // residual
 };
 
+// A captured V-cycle for one (b, x) pointer pair: the ~10 launches per level
+// of the V-cycle replay as one cudaGraphLaunch (no per-kernel CPU launch cost,
+// device-side back-to-back scheduling of the dependent level kernels).
+struct VGraph {
+  const double* b;
+  double* x;
+  cudaGraphExec_t exec;
+  int nkernels;
+};
+
 struct bamg_hier {
   bamg_ctx* ctx = nullptr;
   std::vector<HLevel> lv;
@@ -40,7 +51,14 @@ struct bamg_hier {
   int nu1 = 3, nu2 = 3;
   std::vector<void*> owned;
   bool ready = false;
+  std::vector<VGraph> graphs;
+  cudaStream_t cap_stream = nullptr;
 };
+
+static void hier_drop_graphs(bamg_hier* h) {
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
+}
 
 extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
   BAMG_REQUIRE(ctx, nlevels >= 1 && out, "hierarchy needs at least one level");
@@ -54,6 +72,8 @@ extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
 extern "C" int bamg_hier_destroy(bamg_hier* h) {
   if (!h) return 0;
   cudaStreamSynchronize(h->ctx->stream);
+  hier_drop_graphs(h);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   for (void* p : h->owned) cudaFree(p);
   delete h;
   return 0;
@@ -71,12 +91,14 @@ extern "C" int bamg_hier_set_level(bamg_hier* h, int level, const bamg_csr* B, c
   if (P) L.P = *P;
   if (Q) L.Q = *Q;
   h->ready = false;
+  hier_drop_graphs(h);
   return 0;
 }
 
 extern "C" int bamg_hier_set_coarsest(bamg_hier* h, const double* Z, int n) {
   h->Z = Z;
   h->nz = n;
+  hier_drop_graphs(h);
   return 0;
 }
 
@@ -84,6 +106,7 @@ extern "C" int bamg_hier_set_smoother(bamg_hier* h, double omega, int nu_pre, in
   h->omega = omega;
   h->nu1 = nu_pre;
   h->nu2 = nu_post;
+  hier_drop_graphs(h);
   return 0;
 }
 
@@ -191,9 +214,55 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
   return 0;
 }
 
+static bool graphs_enabled(bamg_ctx* ctx) {
+  if (ctx->trace.on) return false;  // the development trace wants every launch
+  const char* e = getenv("BAMG_NO_GRAPHS");
+  return !(e && e[0] == '1');
+}
+
+// V-cycle through a cached CUDA graph keyed by (b, x); captured on a private
+// non-blocking stream (the context stream may be the legacy default stream,
+// which cannot capture) and replayed on the context stream.
+static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
+  if (!graphs_enabled(ctx)) return vcycle_impl(ctx, h, b, x);
+  BAMG_TRY(hier_prepare(h));
+  VGraph* g = nullptr;
+  for (auto& e : h->graphs)
+    if (e.b == b && e.x == x) g = &e;
+  if (!g) {
+    if (h->graphs.size() >= 8) hier_drop_graphs(h);
+    if (!h->cap_stream) BAMG_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t saved = ctx->stream;
+    int64_t l0 = ctx->launches;
+    unsigned saved_mask = ctx->prof.mask;  // no profiler events inside the graph
+    ctx->prof.mask = 0;
+    ctx->stream = h->cap_stream;
+    cudaGraph_t graph;
+    cudaError_t e1 = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+    int rc = e1 == cudaSuccess ? vcycle_impl(ctx, h, b, x) : -1;
+    cudaError_t e2 = cudaStreamEndCapture(h->cap_stream, &graph);
+    ctx->stream = saved;
+    ctx->prof.mask = saved_mask;
+    int nk = (int)(ctx->launches - l0);
+    ctx->launches = l0;
+    if (e1 != cudaSuccess || e2 != cudaSuccess || rc != 0) {
+      ctx->err = std::string("V-cycle graph capture failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
+      return rc != 0 ? rc : -1;
+    }
+    cudaGraphExec_t exec;
+    BAMG_CHECK_CUDA(ctx, cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    h->graphs.push_back({b, x, exec, nk});
+    g = &h->graphs.back();
+  }
+  BAMG_CHECK_CUDA(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+  ctx->launches += g->nkernels;
+  return 0;
+}
+
 extern "C" int bamg_vcycle(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
   ctx->arena.reset();
-  return vcycle_impl(ctx, h, b, x);
+  return vcycle_run(ctx, h, b, x);
 }
 
 // ===================================================================== GMRES
@@ -408,7 +477,7 @@ static int apply_op(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double
                     double* out) {
   if (h) {
     BAMG_TRY(spmm_dev(ctx, B, v, tmp, 1));
-    return vcycle_impl(ctx, h, tmp, out);
+    return vcycle_run(ctx, h, tmp, out);
   }
   return spmm_dev(ctx, B, v, out, 1);
 }
@@ -494,7 +563,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   BAMG_TRY(spmm_dev(ctx, B, x0, tmp, 1));
   BAMG_LAUNCH(ctx, axpby_kernel, grd, blk, 0, n, b, tmp, w);
   if (h) {
-    BAMG_TRY(vcycle_impl(ctx, h, w, rhs));
+    BAMG_TRY(vcycle_run(ctx, h, w, rhs));
   } else {
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(rhs, w, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }

@@ -10,6 +10,8 @@
 // (sparse.py:81-86 -> scipy _sparsetools csr_matvec: sum = 0; sum += a*x).
 // The Jacobi epilogue reproduces relax.py:78-83 bit for bit:
 //   r = b - Ax;  upd = (omega * r) / d;  upd = 0 on skipped rows;  x + upd.
+#include <cstdlib>
+
 #include "common.cuh"
 
 constexpr int TILE_ROWS = 256;
@@ -92,6 +94,161 @@ csr_tile_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
   }
 }
 
+
+// Row-per-thread variant for compile-time K (1, 2, 4, 8, 12, 16): a thread owns
+// one row and all K vectors, so col/val/d/skip are read once per row, the K
+// partial sums live in registers and each neighbour's K-value segment is read
+// with 16-byte vector loads.  Per-vector sums stay sequential in ascending
+// column order (bit-identical to the pair kernel and to scipy).
+template <int K>
+struct VecIO {
+  static __device__ __forceinline__ void load(const double* __restrict__ p, double* v) {
+    if constexpr (K % 2 == 0) {
+      const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+      for (int i = 0; i < K / 2; ++i) {
+        double2 t = __ldg(q + i);
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) v[i] = __ldg(p + i);
+    }
+  }
+  static __device__ __forceinline__ void store(double* __restrict__ p, const double* v) {
+    if constexpr (K % 2 == 0) {
+      double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+      for (int i = 0; i < K / 2; ++i) q[i] = make_double2(v[2 * i], v[2 * i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) p[i] = v[i];
+    }
+  }
+};
+
+template <int EPI, int K>
+__global__ void __launch_bounds__(TILE_THREADS)
+csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y, EpiArgs ea) {
+  __shared__ int32_t s_rp[TILE_ROWS + 1];
+  __shared__ int32_t s_col[TILE_NNZ];
+  __shared__ double s_val[TILE_NNZ];
+  __shared__ unsigned long long s_peak[K];
+  const int r0 = blockIdx.x * TILE_ROWS;
+  const int rows = min(TILE_ROWS, nrows - r0);
+  for (int i = threadIdx.x; i <= rows; i += TILE_THREADS) s_rp[i] = rowptr[r0 + i];
+  if (EPI == EPI_JACOBI && ea.peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int nz0 = s_rp[0];
+  const int tile_nnz = s_rp[rows] - nz0;
+  const bool staged = tile_nnz <= TILE_NNZ;
+  if (staged) {
+    for (int j = threadIdx.x; j < tile_nnz; j += TILE_THREADS) {
+      s_col[j] = col[nz0 + j];
+      s_val[j] = val[nz0 + j];
+    }
+  }
+  __syncthreads();
+  const int lr = threadIdx.x;
+  if (lr < rows) {
+    const int row = r0 + lr;
+    double acc[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    const int jb = s_rp[lr], je = s_rp[lr + 1];
+    for (int j = jb; j < je; ++j) {
+      int c;
+      double a;
+      if (staged) {
+        c = s_col[j - nz0];
+        a = s_val[j - nz0];
+      } else {
+        c = col[j];
+        a = val[j];
+      }
+      double xv[K];
+      VecIO<K>::load(X + (int64_t)c * K, xv);
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(a, xv[q]));
+    }
+    const int64_t base = (int64_t)row * K;
+    double out[K];
+    if (EPI == EPI_PLAIN) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) out[q] = acc[q];
+    } else if (EPI == EPI_RESID) {
+      double bv[K];
+      VecIO<K>::load(ea.b + base, bv);
+#pragma unroll
+      for (int q = 0; q < K; ++q) out[q] = __dsub_rn(bv[q], acc[q]);
+    } else if (EPI == EPI_ADD) {
+      double xo[K];
+      VecIO<K>::load(ea.xold + base, xo);
+#pragma unroll
+      for (int q = 0; q < K; ++q) out[q] = __dadd_rn(xo[q], acc[q]);
+    } else {
+      double bv[K];
+      if (ea.b) {
+        VecIO<K>::load(ea.b + base, bv);
+        if (ea.b_scale) {
+#pragma unroll
+          for (int q = 0; q < K; ++q) bv[q] = __dmul_rn(ea.b_scale[q], bv[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) bv[q] = 0.0;
+      }
+      double xo[K];
+      VecIO<K>::load(ea.xold + base, xo);
+      const bool sk = ea.skip[row] != 0;
+      const double dd = ea.d[row];
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        double upd = sk ? 0.0 : __ddiv_rn(__dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q])), dd);
+        out[q] = __dadd_rn(xo[q], upd);
+      }
+      if (ea.peak) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          atomicMax(&s_peak[q], (unsigned long long)__double_as_longlong(fabs(out[q])));
+      }
+    }
+    VecIO<K>::store(Y + base, out);
+  }
+  if (EPI == EPI_JACOBI && ea.peak) {
+    __syncthreads();
+    if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
+  }
+}
+
+template <int EPI>
+static int launch_rows(bamg_ctx* ctx, int k, int grid, double bytes, const bamg_csr* A, const double* X, double* Y,
+                       const EpiArgs& ea) {
+  switch (k) {
+#define BAMG_ROWS_CASE(KK)                                                                                     \
+  case KK:                                                                                                     \
+    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK>), grid, TILE_THREADS, 0, A->nrows, A->rowptr, \
+                    A->col, A->val, X, Y, ea);                                                                 \
+    return 0;
+    BAMG_ROWS_CASE(1)
+    BAMG_ROWS_CASE(2)
+    BAMG_ROWS_CASE(4)
+    BAMG_ROWS_CASE(8)
+    BAMG_ROWS_CASE(12)
+    BAMG_ROWS_CASE(16)
+#undef BAMG_ROWS_CASE
+    default:
+      return 1;  // not specialised
+  }
+}
+
+static bool rows_kernel_enabled() {
+  const char* e = getenv("BAMG_PAIR_KERNEL");
+  return !(e && e[0] == '1');
+}
+
 static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
   BAMG_REQUIRE(ctx, A && A->rowptr && (A->nnz == 0 || (A->col && A->val)), "null CSR");
   BAMG_REQUIRE(ctx, A->nrows >= 0 && A->ncols >= 0, "negative CSR shape");
@@ -110,6 +267,19 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   if (epi == EPI_RESID) bytes += 8.0 * n;                         // b
   if (epi == EPI_ADD) bytes += 8.0 * kk * n;                      // x_old
   if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * kk * n : 0.0) + 9.0 * n;  // b, d, skip (x_old == X)
+  // 16-byte vector loads need aligned blocks when K is even (K = 1 has none)
+  bool aligned = (k & 1) || ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
+                              reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold)) & 15) == 0;
+  if (rows_kernel_enabled() && aligned) {
+    int rc = 1;
+    switch (epi) {
+      case EPI_PLAIN: rc = launch_rows<EPI_PLAIN>(ctx, k, grid, bytes, A, X, Y, ea); break;
+      case EPI_RESID: rc = launch_rows<EPI_RESID>(ctx, k, grid, bytes, A, X, Y, ea); break;
+      case EPI_ADD: rc = launch_rows<EPI_ADD>(ctx, k, grid, bytes, A, X, Y, ea); break;
+      default: rc = launch_rows<EPI_JACOBI>(ctx, k, grid, bytes, A, X, Y, ea);
+    }
+    if (rc <= 0) return rc;
+  }
   switch (epi) {
     case EPI_PLAIN:
       BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows,

@@ -13,15 +13,113 @@
 //             intermediate Q*B that feeds the second product (its storage
 //             order fixes the accumulation order of (QB)P);
 //   order 0 = canonical (sorted columns), the make_csr'd result.
-// The per-row lists live in a global scratch slice sized by the structural
-// upper bound sum_j nnz(B_j) (row-chunked so the slice stays bounded).
+//
+// Fast path: the list (<= LCAP distinct columns) and a 128-slot open-
+// addressing index live in thread-local memory (L1-resident), so each product
+// costs ~1 probe.  Rows with more distinct columns are flagged during the
+// count and finished by the slow path, whose lists live in a global scratch
+// slice sized by the structural upper bound sum_j nnz(B_j).  The flagged rows
+// and their scratch offsets are memoised in the context between the count and
+// fill calls, so a product costs two host synchronisations (row count, total).
 #include "internal.cuh"
 
-__global__ void spgemm_ub_kernel(int r0, int nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                                 const int32_t* __restrict__ brp, int32_t* __restrict__ ub) {
+constexpr int LCAP = 64;   // distinct columns per row on the fast path
+constexpr int HSLOTS = 128;
+
+__device__ __forceinline__ bool keep_value(int order, double x) {
+  return order == 0 ? !(fabs(x) < 1e-300) : (x != 0.0);
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(128)
+spgemm_local_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                    const double* __restrict__ aval, const int32_t* __restrict__ brp,
+                    const int32_t* __restrict__ bcol, const double* __restrict__ bval, int order,
+                    int32_t* __restrict__ cnt, int32_t* __restrict__ big_list, unsigned int* __restrict__ nbig,
+                    const int32_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int key[LCAP];
+  double val[LCAP];
+  unsigned int slotw[HSLOTS / 4];  // 1-byte list indices, 0xff = empty
+#pragma unroll
+  for (int h = 0; h < HSLOTS / 4; ++h) slotw[h] = 0xffffffffu;
+  int len = 0;
+  bool overflow = false;
+  for (int jj = arp[i]; jj < arp[i + 1] && !overflow; ++jj) {
+    int j = acol[jj];
+    double v = aval[jj];
+    for (int kk = brp[j]; kk < brp[j + 1]; ++kk) {
+      int c = bcol[kk];
+      double p = __dmul_rn(v, bval[kk]);
+      unsigned h = ((unsigned)c * 2654435761u) >> 25;  // 7 bits
+      while (true) {
+        unsigned int s = (slotw[h >> 2] >> ((h & 3) * 8)) & 0xffu;
+        if (s == 0xffu) {
+          if (len >= LCAP) {
+            overflow = true;
+            break;
+          }
+          slotw[h >> 2] = (slotw[h >> 2] & ~(0xffu << ((h & 3) * 8))) | ((unsigned int)len << ((h & 3) * 8));
+          key[len] = c;
+          val[len] = __dadd_rn(0.0, p);
+          ++len;
+          break;
+        }
+        if (key[s] == c) {
+          val[s] = __dadd_rn(val[s], p);
+          break;
+        }
+        h = (h + 1) & (HSLOTS - 1);
+      }
+      if (overflow) break;
+    }
+  }
+  if (PASS == 0) {
+    if (overflow) {
+      cnt[i] = 0;
+      big_list[atomicAdd(nbig, 1u)] = i;
+      return;
+    }
+    int c = 0;
+    for (int q = 0; q < len; ++q) c += keep_value(order, val[q]) ? 1 : 0;
+    cnt[i] = c;
+    return;
+  }
+  if (overflow) return;  // slow path writes this row
+  int w = crp[i];
+  if (order == 1) {  // reverse first touch
+    for (int q = len - 1; q >= 0; --q)
+      if (keep_value(order, val[q])) {
+        ccol[w] = key[q];
+        cval[w] = val[q];
+        ++w;
+      }
+  } else {  // sorted by column
+    int start = w;
+    for (int q = 0; q < len; ++q) {
+      if (!keep_value(order, val[q])) continue;
+      int c = key[q];
+      double x = val[q];
+      int p = w++;
+      while (p > start && ccol[p - 1] > c) {
+        ccol[p] = ccol[p - 1];
+        cval[p] = cval[p - 1];
+        --p;
+      }
+      ccol[p] = c;
+      cval[p] = x;
+    }
+  }
+}
+
+// slow path over the flagged rows: list in a global scratch slice
+__global__ void spgemm_big_ub_kernel(int nb, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
+                                     const int32_t* __restrict__ acol, const int32_t* __restrict__ brp,
+                                     int32_t* __restrict__ ub) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nr) return;
-  int i = r0 + t;
+  if (t >= nb) return;
+  int i = list[t];
   int s = 0;
   for (int jj = arp[i]; jj < arp[i + 1]; ++jj) {
     int j = acol[jj];
@@ -31,16 +129,16 @@ __global__ void spgemm_ub_kernel(int r0, int nr, const int32_t* __restrict__ arp
 }
 
 template <int PASS>
-__global__ void spgemm_row_kernel(int r0, int nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                                  const double* __restrict__ aval, const int32_t* __restrict__ brp,
-                                  const int32_t* __restrict__ bcol, const double* __restrict__ bval,
-                                  const int32_t* __restrict__ soff, int32_t* __restrict__ skey,
-                                  double* __restrict__ sval, int order, int32_t* __restrict__ cnt,
-                                  const int32_t* __restrict__ crp, int32_t* __restrict__ ccol,
-                                  double* __restrict__ cval) {
+__global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
+                                  const int32_t* __restrict__ acol, const double* __restrict__ aval,
+                                  const int32_t* __restrict__ brp, const int32_t* __restrict__ bcol,
+                                  const double* __restrict__ bval, const int32_t* __restrict__ soff,
+                                  int32_t* __restrict__ skey, double* __restrict__ sval, int order,
+                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ crp,
+                                  int32_t* __restrict__ ccol, double* __restrict__ cval) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nr) return;
-  int i = r0 + t;
+  if (t >= nb) return;
+  int i = list[t];
   int32_t* key = skey + soff[t];
   double* val = sval + soff[t];
   int len = 0;
@@ -61,25 +159,24 @@ __global__ void spgemm_row_kernel(int r0, int nr, const int32_t* __restrict__ ar
       }
     }
   }
-  auto keep = [&](double x) { return order == 0 ? !(fabs(x) < 1e-300) : (x != 0.0); };
   if (PASS == 0) {
     int c = 0;
-    for (int q = 0; q < len; ++q) c += keep(val[q]) ? 1 : 0;
-    cnt[t] = c;
+    for (int q = 0; q < len; ++q) c += keep_value(order, val[q]) ? 1 : 0;
+    cnt[i] = c;
     return;
   }
   int w = crp[i];
-  if (order == 1) {  // reverse first touch
+  if (order == 1) {
     for (int q = len - 1; q >= 0; --q)
-      if (keep(val[q])) {
+      if (keep_value(order, val[q])) {
         ccol[w] = key[q];
         cval[w] = val[q];
         ++w;
       }
-  } else {  // sorted by column
+  } else {
     int start = w;
     for (int q = 0; q < len; ++q) {
-      if (!keep(val[q])) continue;
+      if (!keep_value(order, val[q])) continue;
       int c = key[q];
       double x = val[q];
       int p = w++;
@@ -94,51 +191,34 @@ __global__ void spgemm_row_kernel(int r0, int nr, const int32_t* __restrict__ ar
   }
 }
 
-__global__ void copy_counts_kernel(const int32_t* __restrict__ src, int nr, int32_t* __restrict__ dst) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < nr) dst[t] = src[t];
+// Memo of the flagged rows between the count and the fill call (owned by the
+// context; overwritten by the next count).
+struct SpgemmMemo {
+  const int32_t* arp = nullptr;
+  const int32_t* brp = nullptr;
+  int order = -1;
+  int nbig = 0;
+  int64_t scratch = 0;
+  int32_t* list = nullptr;   // device, capacity cap
+  int32_t* off = nullptr;    // device, capacity cap + 1
+  int64_t cap = 0;
+};
+
+static SpgemmMemo& memo(bamg_ctx* ctx) {
+  static thread_local std::vector<std::pair<bamg_ctx*, SpgemmMemo*>> table;
+  for (auto& e : table)
+    if (e.first == ctx) return *e.second;
+  table.push_back({ctx, new SpgemmMemo()});
+  return *table.back().second;
 }
 
-constexpr int64_t SPGEMM_SCRATCH = int64_t(1) << 28;  // entries per chunk
-
-static int spgemm_pass(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order, int pass,
-                       int32_t* counts_all, const int32_t* crp, int32_t* ccol, double* cval) {
-  const int n = A->nrows;
-  int32_t* ub;
-  int32_t* off;
-  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &ub));
-  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &off));
-  // chunk rows so the scratch slice stays below SPGEMM_SCRATCH entries;
-  // rows per chunk shrink geometrically when a chunk overflows
-  int r0 = 0;
-  int chunk = n > 0 ? n : 1;
-  int32_t* skey = nullptr;
-  double* sval = nullptr;
-  int64_t scap = 0;
-  while (r0 < n) {
-    int nr = chunk < n - r0 ? chunk : n - r0;
-    BAMG_LAUNCH(ctx, spgemm_ub_kernel, grid_for(nr, 256), 256, 0, r0, nr, A->rowptr, A->col, B->rowptr, ub);
-    int64_t total = 0;
-    BAMG_TRY(scan_i32(ctx, ub, off, nr, &total));
-    if (total > SPGEMM_SCRATCH && nr > 1) {
-      chunk = nr / 2;
-      continue;
-    }
-    if (total > scap) {
-      int64_t want = total > 1024 ? total : 1024;
-      BAMG_TRY(arena_get(ctx, (size_t)want, &skey));
-      BAMG_TRY(arena_get(ctx, (size_t)want, &sval));
-      scap = want;
-    }
-    if (pass == 0) {
-      BAMG_LAUNCH(ctx, spgemm_row_kernel<0>, grid_for(nr, 128), 128, 0, r0, nr, A->rowptr, A->col, A->val,
-                  B->rowptr, B->col, B->val, off, skey, sval, order, counts_all + r0, crp, ccol, cval);
-    } else {
-      BAMG_LAUNCH(ctx, spgemm_row_kernel<1>, grid_for(nr, 128), 128, 0, r0, nr, A->rowptr, A->col, A->val,
-                  B->rowptr, B->col, B->val, off, skey, sval, order, nullptr, crp, ccol, cval);
-    }
-    r0 += nr;
-  }
+static int memo_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t n) {
+  if (m.cap >= n + 1) return 0;
+  if (m.list) cudaFree(m.list);
+  if (m.off) cudaFree(m.off);
+  m.cap = n + 1;
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.list, sizeof(int32_t) * m.cap));
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.off, sizeof(int32_t) * (m.cap + 1)));
   return 0;
 }
 
@@ -147,14 +227,57 @@ extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, A && B && A->ncols == B->nrows, "dimension mismatch in sparse product");
   BAMG_REQUIRE(ctx, order == 0 || order == 1, "order must be 0 (canonical) or 1 (scipy storage order)");
-  int32_t* counts;
-  BAMG_TRY(arena_get(ctx, (size_t)A->nrows + 1, &counts));
-  BAMG_TRY(spgemm_pass(ctx, A, B, order, 0, counts, nullptr, nullptr, nullptr));
-  return scan_i32(ctx, counts, rowptr_c, A->nrows, nnz_host);
+  const int n = A->nrows;
+  SpgemmMemo& m = memo(ctx);
+  BAMG_TRY(memo_reserve(ctx, m, n));
+  int32_t* cnt;
+  unsigned int* nbig;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cnt));
+  BAMG_TRY(arena_get(ctx, 1, &nbig));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(unsigned int), ctx->stream));
+  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
+                  A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
+                  (int32_t*)nullptr, (double*)nullptr);
+  int32_t nb = 0;
+  BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(nbig), 1, &nb));
+  m.arp = A->rowptr;
+  m.brp = B->rowptr;
+  m.order = order;
+  m.nbig = nb;
+  m.scratch = 0;
+  if (nb > 0) {
+    int32_t* ub;
+    BAMG_TRY(arena_get(ctx, (size_t)nb + 1, &ub));
+    BAMG_LAUNCH(ctx, spgemm_big_ub_kernel, grid_for(nb, 128), 128, 0, nb, m.list, A->rowptr, A->col, B->rowptr, ub);
+    BAMG_TRY(scan_i32(ctx, ub, m.off, nb, &m.scratch));
+    int32_t *skey;
+    double* sval;
+    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &skey));
+    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &sval));
+    BAMG_LAUNCH(ctx, spgemm_big_kernel<0>, grid_for(nb, 128), 128, 0, nb, m.list, A->rowptr, A->col, A->val,
+                B->rowptr, B->col, B->val, m.off, skey, sval, order, cnt, (const int32_t*)nullptr,
+                (int32_t*)nullptr, (double*)nullptr);
+  }
+  return scan_i32(ctx, cnt, rowptr_c, n, nnz_host);
 }
 
 extern "C" int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
                                 const int32_t* rowptr_c, int32_t* col_c, double* val_c) {
   ctx->arena.reset();
-  return spgemm_pass(ctx, A, B, order, 1, nullptr, rowptr_c, col_c, val_c);
+  const int n = A->nrows;
+  SpgemmMemo& m = memo(ctx);
+  BAMG_REQUIRE(ctx, m.arp == A->rowptr && m.brp == B->rowptr && m.order == order,
+               "bamg_spgemm_fill must follow bamg_spgemm_count on the same operands");
+  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<1>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
+                  A->val, B->rowptr, B->col, B->val, order, (int32_t*)nullptr, (int32_t*)nullptr,
+                  (unsigned int*)nullptr, rowptr_c, col_c, val_c);
+  if (m.nbig > 0) {
+    int32_t* skey;
+    double* sval;
+    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &skey));
+    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &sval));
+    BAMG_LAUNCH(ctx, spgemm_big_kernel<1>, grid_for(m.nbig, 128), 128, 0, m.nbig, m.list, A->rowptr, A->col, A->val,
+                B->rowptr, B->col, B->val, m.off, skey, sval, order, (int32_t*)nullptr, rowptr_c, col_c, val_c);
+  }
+  return 0;
 }

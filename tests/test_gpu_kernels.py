@@ -61,8 +61,11 @@ def test_transpose_and_spmv_transpose_bitexact(eng, golden):
     assert np.array_equal(y.cpu().numpy(), g["ATx"])
 
 
-@pytest.mark.parametrize("k", [1, 8, 12, 16])
-def test_spmm_bitexact(eng, k):
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("k", [1, 3, 8, 12, 16])
+def test_spmm_bitexact(eng, k, pair, monkeypatch):
+    if pair:
+        monkeypatch.setenv("BAMG_PAIR_KERNEL", "1")
     rng = np.random.default_rng(k)
     from scipy import sparse as sp
     A = orc.canon(sp.random_array((3000, 2500), density=0.003, random_state=rng))
@@ -119,8 +122,11 @@ def _device_hierarchy(eng, levels, omega, nu1, nu2):
 
 
 @pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_planar1024_k12", "pipe_uniform63"])
-def test_vcycle_and_gmres_match_oracle(eng, golden, name):
+@pytest.mark.parametrize("graphs", [True, False])
+def test_vcycle_and_gmres_match_oracle(eng, golden, name, graphs, monkeypatch):
     import ctypes as C
+    if not graphs:
+        monkeypatch.setenv("BAMG_NO_GRAPHS", "1")
     g = golden(name)
     B = csr_from(g, "B")
     cfg = oracle_cfg(g)
@@ -172,3 +178,33 @@ def test_dense_pinv_bordered_lu_matches_svd(eng, golden, name, monkeypatch):
             monkeypatch.setenv("BAMG_PINV_SVD", "1")
         Z = engine.dense_pinv(D, B.shape[0]).cpu().numpy()
         assert np.abs(Z - ref).max() <= 1e-9 * np.abs(ref).max(), force
+
+
+@pytest.mark.parametrize("shape", [(300, 400, 500, 0.05, 0.03), (500, 500, 500, 0.004, 0.004)])
+def test_spgemm_matches_scipy_storage_order_and_canonical(eng, shape):
+    """C = A B with scipy csr_matmat semantics: order 1 reproduces scipy's raw
+    product arrays (reverse-first-touch rows) bit for bit, order 0 the
+    canonical make_csr form.  The first shape has rows with > 64 distinct
+    columns (global-scratch slow path), the second only fast-path rows."""
+    from scipy import sparse as sp
+    from paper_1402_4005_b200 import engine
+    m, k, n, da, db = shape
+    rng = np.random.default_rng(m + n)
+    A = sp.random_array((m, k), density=da, format="csr", random_state=rng)
+    B = sp.random_array((k, n), density=db, format="csr", random_state=rng)
+    A = sp.csr_array(A)
+    B = sp.csr_array(B)
+    A.data = rng.standard_normal(A.nnz)
+    B.data = rng.standard_normal(B.nnz)
+    A.sort_indices()
+    B.sort_indices()
+    raw = A @ B  # scipy csr_matmat, unsorted rows
+    dA, dB = up(eng, A), up(eng, B)
+    C1 = engine.spgemm(dA, dB, order=1).to_host()
+    assert np.array_equal(C1.indptr, raw.indptr)
+    assert np.array_equal(C1.indices, raw.indices)
+    assert np.array_equal(C1.data, raw.data)
+    C0 = engine.spgemm(dA, dB, order=0).to_host()
+    ref = orc.canon(raw)
+    assert np.array_equal(C0.indptr, ref.indptr) and np.array_equal(C0.indices, ref.indices)
+    assert np.array_equal(C0.data, ref.data)

@@ -57,7 +57,7 @@ for rep in range(a.reps):
                       "phases": {k2: round(v, 4) for k2, v in bs.PHASES.items()}}), flush=True)
 buf = C.create_string_buffer(1 << 20)
 _lib.lib().bamg_trace_dump(_lib.ctx(), buf, 1 << 20)
-rows = [l.split() for l in buf.value.decode().splitlines()]
+rows = [l.split("\t") for l in buf.value.decode().splitlines()]
 rows.sort(key=lambda r: -float(r[1]))
 tot = sum(float(r[1]) for r in rows)
 print(f"TRACE total kernel ms {tot:.2f} launches {sum(int(r[2]) for r in rows)}")
