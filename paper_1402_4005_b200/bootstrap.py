@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import json
 import math
+import os
+import sys
 import time
 from dataclasses import dataclass, field
 
@@ -30,6 +32,8 @@ from .sparse import adjacency_structure, as_device
 
 #: bootstrap.py:329
 SICK_DIAG_FRACTION = 0.02
+
+_DEBUG = bool(os.environ.get("BAMG_DEBUG"))
 
 #: optional phase profiler (bench.py --breakdown): name -> seconds.  Each
 #: phase boundary synchronises the device, so it is off on the timed path.
@@ -304,7 +308,11 @@ def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inh
 def _operator_degenerate(Bc: DeviceCSR) -> bool:
     """bootstrap.py:332-334."""
     d = engine.diag(Bc)
-    return engine.count_nonpositive(d) > SICK_DIAG_FRACTION * Bc.shape[0]
+    bad = engine.count_nonpositive(d)
+    if _DEBUG:
+        print(f"[bamg] galerkin n_c={Bc.shape[0]} nnz={Bc.nnz} nonpositive_diag={bad} "
+              f"limit={SICK_DIAG_FRACTION * Bc.shape[0]:.1f}", file=sys.stderr, flush=True)
+    return bad > SICK_DIAG_FRACTION * Bc.shape[0]
 
 
 def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None, depth: int = 0,
@@ -331,9 +339,13 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
                 split = make_splitting(A, ranks, cfg.coarsening, seed, adj=ops.adj, diag=ops.d)
             else:
                 split = make_splitting(A, ranks, cfg.coarsening, seed)
+        if _DEBUG:
+            print(f"[bamg] level {depth} n={n} split n_c={split.n_coarse}", file=sys.stderr, flush=True)
         if split.n_coarse >= 0.9 * n or split.n_coarse == n:
             split = None  # coarsening stalled
     if split is None:
+        if _DEBUG:
+            print(f"[bamg] coarsest level {depth} n={n}", file=sys.stderr, flush=True)
         with _phase("coarsest"):
             trips = coarsest_triplets(A, Md, Nd, trips.r)
         return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
@@ -358,6 +370,8 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             Bc = engine.spgemm(engine.spgemm(Q, A, order=1), P, order=0)
             sick = _operator_degenerate(Bc)
         if sick:
+            if _DEBUG:
+                print(f"[bamg] truncated at level {depth} n={n} (sick Galerkin product)", file=sys.stderr, flush=True)
             with _phase("coarsest"):
                 trips = coarsest_triplets(A, Md, Nd, trips.r)
             return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips

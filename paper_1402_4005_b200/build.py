@@ -65,7 +65,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + ["-lcudart_static"]
+    cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
+        "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

@@ -36,12 +36,32 @@ static int coop_grid(bamg_ctx* ctx, K kernel, int threads, int want) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
   // grid barriers cost grows with the CTA count: at most COOP_PER_SM CTAs per
   // SM (env BAMG_COOP_PER_SM for tuning)
-  int lim = 2;
+  int lim = 8;
   if (const char* e = getenv("BAMG_COOP_PER_SM")) lim = atoi(e);
   if (lim >= 1 && per_sm > lim) per_sm = lim;
   int cap = per_sm * ctx->num_sms;
+  if (const char* e = getenv("BAMG_COOP_MAXCTA")) {
+    int m = atoi(e);
+    if (m >= 1 && m < cap) cap = m;
+  }
   if (cap < 1) cap = 1;
   return want < cap ? (want < 1 ? 1 : want) : cap;
+}
+
+// Small dense problems run their n sequential steps inside ONE CTA of 1024
+// threads (the grid barrier degenerates to a CTA barrier); larger ones spread
+// over the GPU.  Threshold overridable with BAMG_DENSE_ONE_CTA.
+template <typename K>
+static void dense_shape(bamg_ctx* ctx, K kernel, int n, int64_t work, int* grid, int* block) {
+  int lim = 0;
+  if (const char* e = getenv("BAMG_DENSE_ONE_CTA")) lim = atoi(e);
+  if (n <= lim) {
+    *grid = 1;
+    *block = 1024;
+  } else {
+    *block = 256;
+    *grid = coop_grid(ctx, kernel, 256, grid_for(work, 256));
+  }
 }
 
 #define BAMG_COOP(ctx, kernel, grid, block, ...)                                  \
@@ -236,6 +256,31 @@ static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
   return 0;
 }
 
+int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig) {
+  return jacobi_svd(ctx, G, nrows, ncols, V, sig);
+}
+
+int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out, double* zout,
+                        double* yout);
+int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double* Nd, int n, int r, double* U,
+                            double* V, double* sigma);
+int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out);
+
+static int large_threshold() {
+  int t = 1536;
+  if (const char* e = getenv("BAMG_DENSE_LARGE_N")) t = atoi(e);
+  return t;
+}
+
+// release a huge per-call slab so the HBM returns to the torch allocator
+static void arena_trim(bamg_ctx* ctx) {
+  if (ctx->arena.cap > (size_t(8) << 30)) {
+    cudaStreamSynchronize(ctx->stream);
+    ctx->arena.release();
+    ctx->arena.peak = 0;
+  }
+}
+
 // Z[r][c] = sum_i V[r][i] G[c][i] w_i,  w_i = 1/sig_i^2 if sig_i > tol*max else 0
 __global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, double tol, double* __restrict__ w) {
   __shared__ double smax;
@@ -301,7 +346,7 @@ __global__ void gj_init_kernel(const double* __restrict__ A, int n, double* __re
 }
 
 // stats[0] = min |pivot|, stats[1] = max |pivot| (bits of non-negative doubles)
-__global__ void gj_coop_kernel(double* Aug, int m, double* prow, double* fcol, unsigned long long* stats) {
+__global__ void __launch_bounds__(1024) gj_coop_kernel(double* Aug, int m, double* prow, double* fcol, unsigned long long* stats) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -359,10 +404,13 @@ __global__ void gj_coop_kernel(double* Aug, int m, double* prow, double* fcol, u
       fcol[i] = (i == j) ? 0.0 : __ldcg(Aug + src * W + j);
     }
     grid.sync();
-    for (int64_t t = tid; t < (int64_t)m * W; t += stride) {
-      int64_t i = t / W, k = t % W;
-      if (i == j) Aug[t] = __ldcg(prow + k);
-      else Aug[t] = __ldcg(Aug + t) - __ldcg(fcol + i) * __ldcg(prow + k);
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+      const double f = __ldcg(fcol + i);
+      double* row = Aug + i * W;
+      for (int64_t k = threadIdx.x; k < W; k += blockDim.x) {
+        if (i == j) row[k] = __ldcg(prow + k);
+        else if (f != 0.0) row[k] = __ldcg(row + k) - f * __ldcg(prow + k);
+      }
     }
     grid.sync();
   }
@@ -494,9 +542,10 @@ static int bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* Z) {
   unsigned long long init[2] = {0x7ff0000000000000ull, 0ull};
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
   BAMG_LAUNCH(ctx, gj_init_kernel, grid_for((int64_t)m * 2 * m, 256), 256, 0, A, n, Aug);
-  int grid = coop_grid(ctx, gj_coop_kernel, 256, grid_for((int64_t)m * 2 * m, 256));
+  int grid, block;
+  dense_shape(ctx, gj_coop_kernel, m, (int64_t)m * 2 * m, &grid, &block);
   int mm = m;
-  BAMG_COOP(ctx, gj_coop_kernel, grid, 256, &Aug, &mm, &prow, &fcol, &stats);
+  BAMG_COOP(ctx, gj_coop_kernel, grid, block, &Aug, &mm, &prow, &fcol, &stats);
   BAMG_LAUNCH(ctx, gj_null_kernel, 1, 256, 0, Aug, n, z, y, out);
   BAMG_LAUNCH(ctx, gemv_colmajor_kernel, grid_for(n, 128), 128, 0, A, n, z, r);
   BAMG_LAUNCH(ctx, gemv_colmajor_t_kernel, grid_for((int64_t)n * 32, 256), 256, 0, A, n, y, s);
@@ -526,6 +575,14 @@ static int bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* Z) {
 extern "C" int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* Z) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1, "empty matrix");
+  if (n > large_threshold() && rank_tol <= 1e-12) {
+    int rc = large_bordered_pinv(ctx, A, n, Z, 1, nullptr, nullptr);
+    if (rc == 1) rc = large_full_rank_inverse(ctx, A, n, Z, 1);
+    arena_trim(ctx);
+    if (rc <= 0) return rc;
+    ctx->err = "large coarsest operator: pseudo-inverse not certified (no dense SVD fallback at this size)";
+    return -2;
+  }
   if (n >= 2 && rank_tol <= 1e-12 && !getenv("BAMG_PINV_SVD")) {
     int rc = bordered_pinv(ctx, A, n, Z);
     if (rc <= 0) return rc;
@@ -557,7 +614,7 @@ __global__ void symmetrize_kernel(const double* __restrict__ A, int n, double* _
 // Right-looking Cholesky, one cooperative launch: per column j the pivot
 // column is scaled (L[:, j] = A[:, j] / sqrt(A_jj)), a grid barrier, then the
 // trailing update A[i][k] -= L_ij L_kj (i, k > j), another barrier.
-__global__ void cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
+__global__ void __launch_bounds__(1024) cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -572,9 +629,11 @@ __global__ void cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
       L[(int64_t)j * n + i] = (i == j) ? d : __ldcg(A + (int64_t)j * n + i) / d;
     grid.sync();
     int64_t m = n - j - 1;
-    for (int64_t t = tid; t < m * m; t += stride) {
-      int64_t i = j + 1 + t % m, k = j + 1 + t / m;
-      A[k * n + i] = __ldcg(A + k * n + i) - __ldcg(L + (int64_t)j * n + i) * __ldcg(L + (int64_t)j * n + k);
+    (void)m;
+    for (int64_t k = j + 1 + blockIdx.x; k < n; k += gridDim.x) {  // column k: CTAs
+      const double lk = __ldcg(L + (int64_t)j * n + k);
+      for (int64_t i = j + 1 + threadIdx.x; i < n; i += blockDim.x)  // rows: threads (contiguous)
+        A[k * n + i] = __ldcg(A + k * n + i) - __ldcg(L + (int64_t)j * n + i) * lk;
     }
     grid.sync();
   }
@@ -582,58 +641,65 @@ __global__ void cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
 
 static int cholesky(bamg_ctx* ctx, double* A, int n, double* L, int* bad) {
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(L, 0, sizeof(double) * (size_t)n * n, ctx->stream));
-  int grid = coop_grid(ctx, cholesky_coop_kernel, 256, grid_for((int64_t)n * n, 256));
-  BAMG_COOP(ctx, cholesky_coop_kernel, grid, 256, &A, &n, &L, &bad);
+  int grid, block;
+  dense_shape(ctx, cholesky_coop_kernel, n, (int64_t)n * n, &grid, &block);
+  BAMG_COOP(ctx, cholesky_coop_kernel, grid, block, &A, &n, &L, &bad);
   return 0;
 }
 
 // Forward substitution L X = B for nrhs columns (column-major, ld = n), one
 // cooperative launch: step i writes X[i][c] = B[i][c] / L_ii and updates
 // B[k][c] -= L_ki X[i][c] for k > i (row i of B is read-only in its step).
-__global__ void fwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+__global__ void __launch_bounds__(1024) fwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int i = 0; i < n; ++i) {
     int64_t rows = n - i;
     double lii = __ldcg(L + (int64_t)i * n + i);
-    for (int64_t t = tid; t < rows * nrhs; t += stride) {
-      int64_t k = i + t % rows, c = t / rows;
-      double xi = __ldcg(B + c * n + i) / lii;
-      if (k == i) X[c * n + i] = xi;
-      else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + (int64_t)i * n + k) * xi;
+    (void)rows;
+    for (int64_t c = blockIdx.x; c < nrhs; c += gridDim.x) {
+      const double xi = __ldcg(B + c * n + i) / lii;
+      for (int64_t k = i + threadIdx.x; k < n; k += blockDim.x) {
+        if (k == i) X[c * n + i] = xi;
+        else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + (int64_t)i * n + k) * xi;
+      }
     }
     grid.sync();
   }
 }
 
 static int forward_solve(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
-  int grid = coop_grid(ctx, fwd_coop_kernel, 256, grid_for((int64_t)n * nrhs, 256));
-  BAMG_COOP(ctx, fwd_coop_kernel, grid, 256, &L, &n, &B, &nrhs, &X);
+  int grid, block;
+  dense_shape(ctx, fwd_coop_kernel, n, (int64_t)n * nrhs, &grid, &block);
+  BAMG_COOP(ctx, fwd_coop_kernel, grid, block, &L, &n, &B, &nrhs, &X);
   return 0;
 }
 
 // Back substitution L^T X = B, i from n-1 down (cooperative).
-__global__ void bwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+__global__ void __launch_bounds__(1024) bwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int i = n - 1; i >= 0; --i) {
     int64_t rows = i + 1;
     double lii = __ldcg(L + (int64_t)i * n + i);
-    for (int64_t t = tid; t < rows * nrhs; t += stride) {
-      int64_t k = t % rows, c = t / rows;
-      double xi = __ldcg(B + c * n + i) / lii;
-      if (k == i) X[c * n + i] = xi;
-      else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + k * n + i) * xi;  // (L^T)[k][i] = L[i][k]
+    (void)rows;
+    for (int64_t c = blockIdx.x; c < nrhs; c += gridDim.x) {
+      const double xi = __ldcg(B + c * n + i) / lii;
+      for (int64_t k = threadIdx.x; k <= i; k += blockDim.x) {
+        if (k == i) X[c * n + i] = xi;
+        else B[c * n + k] = __ldcg(B + c * n + k) - __ldcg(L + k * n + i) * xi;  // (L^T)[k][i] = L[i][k]
+      }
     }
     grid.sync();
   }
 }
 
 static int backward_solve_t(bamg_ctx* ctx, const double* L, int n, double* B, int nrhs, double* X) {
-  int grid = coop_grid(ctx, bwd_coop_kernel, 256, grid_for((int64_t)n * nrhs, 256));
-  BAMG_COOP(ctx, bwd_coop_kernel, grid, 256, &L, &n, &B, &nrhs, &X);
+  int grid, block;
+  dense_shape(ctx, bwd_coop_kernel, n, (int64_t)n * nrhs, &grid, &block);
+  BAMG_COOP(ctx, bwd_coop_kernel, grid, block, &L, &n, &B, &nrhs, &X);
   return 0;
 }
 
@@ -878,6 +944,11 @@ extern "C" int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const dou
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1 && r >= 1 && r <= 64, "need 1 <= r <= 64");
   if (r > n) r = n;  // take = min(r, n)
+  if (n > large_threshold()) {
+    int rc = large_coarsest_triplets(ctx, Bd, const_cast<double*>(Md), const_cast<double*>(Nd), n, r, U, V, sigma);
+    arena_trim(ctx);
+    return rc;
+  }
   const size_t nn = (size_t)n * n;
   double *Ms, *Ns, *LM, *LN, *Bw, *T, *Tt, *K, *Kt, *Vk, *Vkt, *sk, *skt, *A, *Bv, *sg, *Xa, *Xb, *work;
   int *perm, *permt, *bad;

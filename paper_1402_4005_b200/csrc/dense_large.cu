@@ -1,0 +1,791 @@
+// dense_large.cu -- the coarsest level when it is large (n > ~1.5k).
+//
+// The reference's hierarchy-shape rules can stop early: the Galerkin product
+// of the 16,769,025-state tandem chain (cfg4) is truncated at n_L = 16,384 and
+// the 2^21-point planar chain (cfg3) at n_L = 47,824 (bootstrap.py:366-371,
+// `_operator_degenerate`).  The reference then densifies the coarsest operator
+// (PinvOperator's SVD, coarsest_triplets' 2n-sized generalized eigenproblem),
+// O(n^3) work.  Here the same quantities come from blocked, GEMM-rich
+// algorithms (trailing updates and triangular solves as fp64 cuBLAS GEMMs, the
+// panels as cooperative kernels):
+//   * pseudo-inverse: blocked LU with partial pivoting of the bordered matrix
+//     [[B, b], [c^T, 0]], explicit inverse by blocked triangular solves, then
+//     B^+ = (I - z z^T) X (I - y y^T) (same certificate as the small path);
+//   * coarsest triplets: blocked Cholesky of M and N, K = L_M^-1 B L_N^-T by
+//     blocked triangular solves, K^+ by the bordered inverse of K, and the r
+//     smallest singular triplets of K as the largest of K^+ by block subspace
+//     iteration with Rayleigh-Ritz (one-sided Jacobi on the n x p projection);
+//     slot 0 is the exact null triplet from the bordered inverse.
+// Column-major storage throughout (ld = rows).
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+constexpr int NB = 128;  // block size of the blocked algorithms
+
+static cublasHandle_t cublas(bamg_ctx* ctx) {
+  static thread_local std::vector<std::pair<bamg_ctx*, cublasHandle_t>> table;
+  for (auto& e : table)
+    if (e.first == ctx) {
+      cublasSetStream(e.second, ctx->stream);
+      return e.second;
+    }
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  cublasSetStream(h, ctx->stream);
+  table.push_back({ctx, h});
+  return h;
+}
+
+// C = alpha op(A) op(B) + beta C  (column-major, fp64)
+static int gemm(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+                const double* B, int ldb, double beta, double* C, int ldc) {
+  if (m <= 0 || n <= 0) return 0;
+  cublasHandle_t h = cublas(ctx);
+  BAMG_REQUIRE(ctx, h != nullptr, "cuBLAS handle creation failed");
+  cublasStatus_t st = cublasDgemm(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha,
+                                  A, lda, B, ldb, &beta, C, ldc);
+  ctx->launches++;
+  if (st != CUBLAS_STATUS_SUCCESS) {
+    ctx->err = "cublasDgemm failed (" + std::to_string((int)st) + ")";
+    return -1;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ double bsum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sh[q];
+  __syncthreads();
+  return t;
+}
+
+// ----------------------------------------------------------- small helpers
+__global__ void copy_block_kernel(const double* __restrict__ S, int lds, double* __restrict__ D, int ldd, int rows,
+                                  int cols) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)rows * cols) return;
+  int r = (int)(t % rows), c = (int)(t / rows);
+  D[(int64_t)c * ldd + r] = S[(int64_t)c * lds + r];
+}
+
+static int copy_block(bamg_ctx* ctx, const double* S, int lds, double* D, int ldd, int rows, int cols) {
+  if (rows <= 0 || cols <= 0) return 0;
+  BAMG_LAUNCH(ctx, copy_block_kernel, grid_for((int64_t)rows * cols, 256), 256, 0, S, lds, D, ldd, rows, cols);
+  return 0;
+}
+
+__global__ void transpose_big_kernel(const double* __restrict__ A, int n, double* __restrict__ T) {
+  __shared__ double tile[32][33];
+  int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    int r = bx + threadIdx.x, c = by + j;
+    if (r < n && c < n) tile[j][threadIdx.x] = A[(int64_t)c * n + r];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    int r = by + threadIdx.x, c = bx + j;
+    if (r < n && c < n) T[(int64_t)c * n + r] = tile[threadIdx.x][j];
+  }
+}
+
+static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
+  transpose_big_kernel<<<grid, block, 0, ctx->stream>>>(A, n, T);
+  ctx->launches++;
+  BAMG_CHECK_CUDA(ctx, cudaGetLastError());
+  return 0;
+}
+
+// Inverse of a triangular nb x nb block (ld) into Ti (nb x nb, ld nb), one
+// CTA, one thread per column of the identity.  kind 0: unit lower, 1: lower,
+// 2: upper.
+__global__ void tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind, double* __restrict__ Ti) {
+  int c = threadIdx.x;
+  if (c >= nb) return;
+  double* x = Ti + (int64_t)c * nb;
+  if (kind == 2) {
+    for (int i = nb - 1; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int j = i + 1; j < nb; ++j) s -= T[(int64_t)j * ld + i] * x[j];
+      x[i] = s / T[(int64_t)i * ld + i];
+    }
+  } else {
+    for (int i = 0; i < nb; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int j = 0; j < i; ++j) s -= T[(int64_t)j * ld + i] * x[j];
+      x[i] = kind == 0 ? s : s / T[(int64_t)i * ld + i];
+    }
+  }
+}
+
+static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
+  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, NB, 0, T, ld, nb, kind, Ti);
+  return 0;
+}
+
+// Blocked triangular solve op(T) X = B in place on B (n x m, ldb).  T is the
+// n x n column-major factor: lower (unit or not) or, with `upper`, the upper
+// triangle; `trans` solves with T^T (a lower T^T is upper).
+static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, bool unit, bool trans, double* B,
+                     int ldb, int m, double* work /* NB*NB + NB*m */) {
+  double* Ti = work;
+  double* tmp = work + NB * NB;
+  // effective shape of op(T): lower if (lower_stored xor trans)
+  const bool eff_lower = lower_stored != trans;
+  const int nblk = (n + NB - 1) / NB;
+  for (int s = 0; s < nblk; ++s) {
+    int bi = eff_lower ? s : nblk - 1 - s;
+    int i0 = bi * NB, ib = (i0 + NB <= n) ? NB : n - i0;
+    // inverse of the diagonal block of op(T)
+    const double* Tii = T + (int64_t)i0 * n + i0;
+    int kind = lower_stored ? (unit ? 0 : 1) : 2;
+    BAMG_TRY(tri_inv(ctx, Tii, n, ib, kind, Ti));  // inverse of the stored block
+    // X_i = op(Tii)^-1 B_i   (op(inv) = inv(op))
+    BAMG_TRY(gemm(ctx, trans, false, ib, m, ib, 1.0, Ti, ib, B + i0, ldb, 0.0, tmp, ib));
+    BAMG_TRY(copy_block(ctx, tmp, ib, B + i0, ldb, ib, m));
+    // update the remaining block rows: B_rest -= op(T)_{rest,i} X_i
+    if (eff_lower) {
+      int r0 = i0 + ib, rn = n - r0;
+      if (rn > 0) {
+        // op(T)[r0:, i0:i0+ib] = trans ? T[i0:i0+ib, r0:]^T : T[r0:, i0:i0+ib]
+        const double* Tb = trans ? T + (int64_t)r0 * n + i0 : T + (int64_t)i0 * n + r0;
+        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, n, B + i0, ldb, 1.0, B + r0, ldb));
+      }
+    } else {
+      int rn = i0;
+      if (rn > 0) {
+        // op(T)[0:i0, i0:i0+ib] = trans ? T[i0:i0+ib, 0:i0]^T : T[0:i0, i0:i0+ib]
+        const double* Tb = trans ? T + i0 : T + (int64_t)i0 * n;
+        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, n, B + i0, ldb, 1.0, B, ldb));
+      }
+    }
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------- Cholesky
+// unblocked in-place lower Cholesky of a jb x jb diagonal block (one CTA)
+__global__ void chol_block_kernel(double* A, int ld, int jb, int* bad) {
+  __shared__ double d;
+  for (int j = 0; j < jb; ++j) {
+    if (threadIdx.x == 0) {
+      double p = A[(int64_t)j * ld + j];
+      if (!(p > 0.0)) *bad = 1;
+      d = sqrt(fmax(p, 1e-300));
+      A[(int64_t)j * ld + j] = d;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < jb; i += blockDim.x) A[(int64_t)j * ld + i] /= d;
+    __syncthreads();
+    for (int k = j + 1; k < jb; ++k) {
+      double lk = A[(int64_t)j * ld + k];
+      for (int i = k + threadIdx.x; i < jb; i += blockDim.x) A[(int64_t)k * ld + i] -= A[(int64_t)j * ld + i] * lk;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void zero_upper_kernel(double* A, int n) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int r = (int)(t % n), c = (int)(t / n);
+  if (r < c) A[t] = 0.0;
+}
+
+static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* work) {
+  double* Li = work;            // NB x NB
+  double* tmp = work + NB * NB;  // n x NB
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    int jb = (j0 + NB <= n) ? NB : n - j0;
+    double* Ajj = A + (int64_t)j0 * n + j0;
+    BAMG_LAUNCH(ctx, chol_block_kernel, 1, 256, 0, Ajj, n, jb, bad);
+    int r0 = j0 + jb, rn = n - r0;
+    if (rn <= 0) break;
+    BAMG_TRY(tri_inv(ctx, Ajj, n, jb, 1, Li));
+    // L21 = A21 L11^-T
+    double* A21 = A + (int64_t)j0 * n + r0;
+    BAMG_TRY(gemm(ctx, false, true, rn, jb, jb, 1.0, A21, n, Li, jb, 0.0, tmp, rn));
+    BAMG_TRY(copy_block(ctx, tmp, rn, A21, n, rn, jb));
+    // A22 -= L21 L21^T
+    BAMG_TRY(gemm(ctx, false, true, rn, rn, jb, -1.0, A21, n, A21, n, 1.0, A + (int64_t)r0 * n + r0, n));
+  }
+  BAMG_LAUNCH(ctx, zero_upper_kernel, grid_for((int64_t)n * n, 256), 256, 0, A, n);
+  return 0;
+}
+
+// -------------------------------------------------------- LU, partial pivoting
+// Panel factorisation of A[j0:n, j0:j0+jb] (cooperative; pivot rows recorded
+// in piv[j0..j0+jb), swaps applied inside the panel only).
+__global__ void __launch_bounds__(256) panel_lu_kernel(double* A, int n, int j0, int jb, int* piv, double* pmax,
+                                                       int* pidx, int* bad) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sb[8];
+  __shared__ int si[8];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = j0; j < j0 + jb; ++j) {
+    // per-CTA argmax |A[i][j]|, i >= j (first index on ties)
+    double best = -1.0;
+    int bi = j;
+    for (int64_t i = j + tid; i < n; i += stride) {
+      double a = fabs(__ldcg(A + (int64_t)j * n + i));
+      if (a > best) {
+        best = a;
+        bi = (int)i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sb[threadIdx.x >> 5] = best;
+      si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < 8; ++q)
+        if (sb[q] > sb[0] || (sb[q] == sb[0] && si[q] < si[0])) {
+          sb[0] = sb[q];
+          si[0] = si[q];
+        }
+      pmax[blockIdx.x] = sb[0];
+      pidx[blockIdx.x] = si[0];
+    }
+    __syncthreads();
+    grid.sync();
+    // every CTA reduces the per-CTA candidates identically
+    double pb = -1.0;
+    int p = j;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      double v = __ldcg(pmax + b);
+      int ix = __ldcg(pidx + b);
+      if (v > pb || (v == pb && ix < p)) {
+        pb = v;
+        p = ix;
+      }
+    }
+    if (tid == 0) {
+      piv[j] = p;
+      if (!(pb > 0.0)) *bad = 1;
+    }
+    // swap rows j and p inside the panel
+    if (p != j)
+      for (int64_t c = j0 + tid; c < j0 + jb; c += stride) {
+        double a = __ldcg(A + c * n + j), b = __ldcg(A + c * n + p);
+        A[c * n + j] = b;
+        A[c * n + p] = a;
+      }
+    grid.sync();
+    const double d = __ldcg(A + (int64_t)j * n + j);
+    // scale the column below the pivot and update the rest of the panel
+    for (int64_t i = j + 1 + tid; i < n; i += stride) {
+      double l = __ldcg(A + (int64_t)j * n + i) / (d != 0.0 ? d : 1.0);
+      A[(int64_t)j * n + i] = l;
+      for (int c = j + 1; c < j0 + jb; ++c) A[(int64_t)c * n + i] = __ldcg(A + (int64_t)c * n + i) - l * __ldcg(A + (int64_t)c * n + j);
+    }
+    grid.sync();
+  }
+}
+
+// apply the panel's row interchanges to columns outside [j0, j0+jb)
+__global__ void apply_swaps_kernel(double* A, int n, int j0, int jb, const int* piv) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n || (c >= j0 && c < j0 + jb)) return;
+  double* col = A + (int64_t)c * n;
+  for (int j = j0; j < j0 + jb; ++j) {
+    int p = piv[j];
+    if (p != j) {
+      double t = col[j];
+      col[j] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, double* work) {
+  double* Li = work;             // NB x NB
+  double* tmp = work + NB * NB;  // NB x n
+  double* pmax;
+  int* pidx;
+  BAMG_TRY(arena_get(ctx, 2048, &pmax));
+  BAMG_TRY(arena_get(ctx, 2048, &pidx));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_lu_kernel, 256, 0);
+  int pgrid = per_sm * ctx->num_sms;
+  if (pgrid > 2048) pgrid = 2048;
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    int jb = (j0 + NB <= n) ? NB : n - j0;
+    int want = (n - j0 + 255) / 256;
+    int g = want < pgrid ? (want < 1 ? 1 : want) : pgrid;
+    void* args[] = {&A, &n, &j0, &jb, &piv, &pmax, &pidx, &bad};
+    BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(g), dim3(256), args, 0,
+                                                     ctx->stream));
+    ctx->launches++;
+    BAMG_LAUNCH(ctx, apply_swaps_kernel, grid_for(n, 256), 256, 0, A, n, j0, jb, piv);
+    int r0 = j0 + jb, rn = n - r0;
+    if (rn <= 0) break;
+    // U12 = L11^-1 A12
+    double* Ajj = A + (int64_t)j0 * n + j0;
+    double* A12 = A + (int64_t)r0 * n + j0;
+    BAMG_TRY(tri_inv(ctx, Ajj, n, jb, 0, Li));
+    BAMG_TRY(gemm(ctx, false, false, jb, rn, jb, 1.0, Li, jb, A12, n, 0.0, tmp, jb));
+    BAMG_TRY(copy_block(ctx, tmp, jb, A12, n, jb, rn));
+    // A22 -= L21 U12
+    BAMG_TRY(gemm(ctx, false, false, rn, rn, jb, -1.0, A + (int64_t)j0 * n + r0, n, A12, n, 1.0,
+                  A + (int64_t)r0 * n + r0, n));
+  }
+  return 0;
+}
+
+// X = P^T-permuted identity: row swaps of piv applied to I (column-major n x n)
+__global__ void perm_identity_kernel(double* X, int n, const int* piv) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double* col = X + (int64_t)c * n;
+  for (int r = 0; r < n; ++r) col[r] = (r == c) ? 1.0 : 0.0;
+  for (int j = 0; j < n; ++j) {
+    int p = piv[j];
+    if (p != j) {
+      double t = col[j];
+      col[j] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+// inverse from the LU factors (A = P^T L U): X = U^-1 L^-1 P I
+static int lu_inverse(bamg_ctx* ctx, const double* LU, int n, const int* piv, double* X, double* work) {
+  BAMG_LAUNCH(ctx, perm_identity_kernel, grid_for(n, 128), 128, 0, X, n, piv);
+  BAMG_TRY(tri_solve(ctx, LU, n, true, true, false, X, n, n, work));    // L (unit lower)
+  BAMG_TRY(tri_solve(ctx, LU, n, false, false, false, X, n, n, work));  // U (upper)
+  return 0;
+}
+
+// ------------------------------------------------- bordered inverse -> pinv
+__global__ void border_fill_kernel(const double* __restrict__ A, int n, double* __restrict__ Bb) {
+  const int m = n + 1;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * m) return;
+  int r = (int)(t % m), c = (int)(t / m);
+  const double bc = 1.0 / sqrt((double)n);
+  double v;
+  if (r < n && c < n) v = A[(int64_t)c * n + r];
+  else if (r == n && c == n) v = 0.0;
+  else v = bc;
+  Bb[t] = v;
+}
+
+// null vectors (unit) + certificate inputs from the bordered inverse Xb (m x m):
+// x = Xb[0:n, n], w = Xb[n, 0:n];  out: |x|, |w|, |omega|
+__global__ void border_null_kernel(const double* __restrict__ Xb, int n, double* __restrict__ z, double* __restrict__ y,
+                                   double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int m = n + 1;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double xv = Xb[(int64_t)n * m + i];
+    double wv = Xb[(int64_t)i * m + n];
+    a += xv * xv;
+    b += wv * wv;
+  }
+  a = sqrt(bsum(a, sh));
+  b = sqrt(bsum(b, sh));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    z[i] = Xb[(int64_t)n * m + i] / a;
+    y[i] = Xb[(int64_t)i * m + n] / b;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+    out[5] = fabs(Xb[(int64_t)n * m + n]);
+  }
+}
+
+// |B z|, |B^T y|, |B|_F
+__global__ void border_cert_kernel(const double* __restrict__ Bz, const double* __restrict__ Bty,
+                                   const double* __restrict__ A, int n, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0, f = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a += Bz[i] * Bz[i];
+    b += Bty[i] * Bty[i];
+  }
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n; t += blockDim.x) f += A[t] * A[t];
+  a = bsum(a, sh);
+  b = bsum(b, sh);
+  f = bsum(f, sh);
+  if (threadIdx.x == 0) {
+    out[2] = sqrt(a);
+    out[3] = sqrt(b);
+    out[4] = sqrt(f);
+  }
+}
+
+// P = (I - z z^T) X (I - y y^T) with X = Xb[0:n, 0:n]; r = z^T X, s = X y,
+// t = z^T X y.  Output column-major (rowmajor_out: transposed write).
+__global__ void border_project_kernel(const double* __restrict__ Xb, int n, const double* __restrict__ z,
+                                      const double* __restrict__ y, const double* __restrict__ r,
+                                      const double* __restrict__ s, const double* __restrict__ t, double* __restrict__ P,
+                                      int rowmajor_out) {
+  const int m = n + 1;
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int i = (int)(idx % n), j = (int)(idx / n);  // (row i, column j)
+  double v = Xb[(int64_t)j * m + i] - z[i] * r[j] - s[i] * y[j] + t[0] * z[i] * y[j];
+  if (rowmajor_out) P[(int64_t)i * n + j] = v;
+  else P[idx] = v;
+}
+
+__global__ void dot1_kernel(const double* __restrict__ a, const double* __restrict__ b, int n, double* out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
+  s = bsum(s, sh);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// Bordered pseudo-inverse of a large singular A (column-major n x n).
+// 0: written to P (row-major if rowmajor_out); 1: certificate failed.
+// zout / yout (optional) receive the unit right / left null vectors.
+int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out, double* zout,
+                        double* yout) {
+  const int m = n + 1;
+  double *Bb, *Xb, *work, *z, *y, *r, *s, *t, *out;
+  int *piv, *bad;
+  BAMG_TRY(arena_get(ctx, (size_t)m * m, &Bb));
+  BAMG_TRY(arena_get(ctx, (size_t)m * m, &Xb));
+  BAMG_TRY(arena_get(ctx, (size_t)NB * NB + (size_t)NB * m + 64, &work));
+  BAMG_TRY(arena_get(ctx, (size_t)m, &piv));
+  BAMG_TRY(arena_get(ctx, 1, &bad));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &z));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &y));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &r));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &s));
+  BAMG_TRY(arena_get(ctx, 1, &t));
+  BAMG_TRY(arena_get(ctx, 8, &out));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  BAMG_LAUNCH(ctx, border_fill_kernel, grid_for((int64_t)m * m, 256), 256, 0, A, n, Bb);
+  BAMG_TRY(lu_blocked(ctx, Bb, m, piv, bad, work));
+  BAMG_TRY(lu_inverse(ctx, Bb, m, piv, Xb, work));
+  BAMG_LAUNCH(ctx, border_null_kernel, 1, 1024, 0, Xb, n, z, y, out);
+  // certificate: |B z|, |B^T y| at round-off, omega ~ 0, LU pivots nonzero
+  BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, A, n, z, n, 0.0, r, n));
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, A, n, y, n, 0.0, s, n));
+  BAMG_LAUNCH(ctx, border_cert_kernel, 1, 1024, 0, r, s, A, n, out);
+  double h[6];
+  int hb = 0;
+  BAMG_TRY(ctx_read_doubles(ctx, out, 6, h));
+  BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
+  const double bf = h[4];
+  bool ok = !hb && h[2] <= 1e-14 * bf / std::sqrt((double)n) && h[3] <= 1e-14 * bf / std::sqrt((double)n) &&
+            h[5] <= 1e-8 * (h[0] > h[1] ? h[0] : h[1]);
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] large pinv n=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e omega=%.3e bad=%d -> %s\n", n, h[2], h[3],
+            bf, h[5], hb, ok ? "certified" : "not certified");
+  if (!ok) return 1;
+  // r = z^T X = X^T z ; s = X y ; t = z^T s
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, Xb, m, z, n, 0.0, r, n));
+  BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Xb, m, y, n, 0.0, s, n));
+  BAMG_LAUNCH(ctx, dot1_kernel, 1, 1024, 0, z, s, n, t);
+  BAMG_LAUNCH(ctx, border_project_kernel, grid_for((int64_t)n * n, 256), 256, 0, Xb, n, z, y, r, s, t, P, rowmajor_out);
+  if (zout) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(zout, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (yout) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(yout, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  return 0;
+}
+
+__global__ void frob2_kernel(const double* __restrict__ A, int64_t total, double* out) {
+  __shared__ double sh[32];
+  double f = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
+    f += A[t] * A[t];
+  f = bsum(f, sh);
+  if (threadIdx.x == 0) atomicAdd(out, f);
+}
+
+__global__ void transpose_copy_kernel(const double* __restrict__ X, int n, double* __restrict__ P) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int i = (int)(t % n), j = (int)(t / n);
+  P[(int64_t)i * n + j] = X[t];
+}
+
+// Full-rank case: A^+ = A^-1 when sigma_min > 1e-12 sigma_max, certified by
+// |A|_F |A^-1|_F < 1e12.  0: written; 1: not certified.
+int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out) {
+  double *LU, *X, *work, *f;
+  int *piv, *bad;
+  BAMG_TRY(arena_get(ctx, (size_t)n * n, &LU));
+  BAMG_TRY(arena_get(ctx, (size_t)n * n, &X));
+  BAMG_TRY(arena_get(ctx, (size_t)NB * NB + (size_t)NB * (n + 1) + 64, &work));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &piv));
+  BAMG_TRY(arena_get(ctx, 1, &bad));
+  BAMG_TRY(arena_get(ctx, 2, &f));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(f, 0, 2 * sizeof(double), ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(LU, A, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(lu_blocked(ctx, LU, n, piv, bad, work));
+  BAMG_TRY(lu_inverse(ctx, LU, n, piv, X, work));
+  BAMG_LAUNCH(ctx, frob2_kernel, 256, 256, 0, A, (int64_t)n * n, f);
+  BAMG_LAUNCH(ctx, frob2_kernel, 256, 256, 0, X, (int64_t)n * n, f + 1);
+  double h[2];
+  int hb = 0;
+  BAMG_TRY(ctx_read_doubles(ctx, f, 2, h));
+  BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
+  double cond = std::sqrt(h[0]) * std::sqrt(h[1]);
+  bool ok = !hb && std::isfinite(cond) && cond < 1e12;
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] large inverse n=%d |A|F|A^-1|F=%.3e bad=%d -> %s\n", n, cond, hb,
+            ok ? "certified full rank" : "not certified");
+  if (!ok) return 1;
+  if (rowmajor_out) BAMG_LAUNCH(ctx, transpose_copy_kernel, grid_for((int64_t)n * n, 256), 256, 0, X, n, P);
+  else BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(P, X, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  return 0;
+}
+
+// ------------------------------------------------- coarsest triplets (large)
+__global__ void symmetrize_inplace_kernel(double* A, int n) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int r = (int)(t % n), c = (int)(t / n);
+  if (r < c) {
+    double a = A[t], b = A[(int64_t)r * n + c];
+    double v = 0.5 * (a + b);
+    A[t] = v;
+    A[(int64_t)r * n + c] = v;
+  } else if (r == c) {
+    A[t] = 0.5 * (A[t] + A[t]);
+  }
+}
+
+__global__ void pseudo_random_kernel(double* X, int64_t total, unsigned seed) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  unsigned h = (unsigned)(t * 2654435761ull) ^ (seed * 0x9e3779b9u);
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  X[t] = (double)(h & 0xffffff) / 16777216.0 - 0.5;
+}
+
+// CholQR2-free orthonormalisation of n x p Y by two passes of Gram-Schmidt on
+// the Gram matrix: G = Y^T Y, R = chol(G), Y <- Y R^-1 (twice).
+__global__ void small_chol_inv_kernel(double* G, int p, double* Rinv) {
+  // one CTA: G (p x p, col-major) -> upper R with R^T R = G, then R^-1 (upper)
+  __shared__ double R[64 * 64];
+  int tid = threadIdx.x;
+  for (int t = tid; t < p * p; t += blockDim.x) R[t] = G[t];
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < p; ++j) {
+      double d = R[j * p + j];
+      for (int k = 0; k < j; ++k) d -= R[j * p + k] * R[j * p + k];  // R[k][j] stored at (col j, row k)
+      d = sqrt(fmax(d, 1e-300));
+      R[j * p + j] = d;
+      for (int i = j + 1; i < p; ++i) {
+        double v = R[i * p + j];
+        for (int k = 0; k < j; ++k) v -= R[j * p + k] * R[i * p + k];
+        R[i * p + j] = v / d;
+      }
+      for (int i = j + 1; i < p; ++i) R[j * p + i] = 0.0;  // lower part cleared
+    }
+  }
+  __syncthreads();
+  // R is upper (entries R[k][j], k <= j at index j*p + k); invert column by column
+  for (int c = tid; c < p; c += blockDim.x) {
+    for (int i = p - 1; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int j = i + 1; j < p; ++j) s -= R[j * p + i] * Rinv[c * p + j];
+      Rinv[c * p + i] = s / R[i * p + i];
+    }
+  }
+}
+
+static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp) {
+  for (int pass = 0; pass < 2; ++pass) {
+    BAMG_TRY(gemm(ctx, true, false, p, p, n, 1.0, Y, n, Y, n, 0.0, G, p));
+    BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 64, 0, G, p, Rinv);
+    BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Rinv, p, 0.0, tmp, n));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Y, tmp, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return 0;
+}
+
+int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig);
+
+// column-major n x r block helpers for the large finish
+__global__ void cm_colnorm_scale_kernel(double* X, int n) {
+  __shared__ double sh[32];
+  double* c = X + (int64_t)blockIdx.x * n;
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += c[i] * c[i];
+  a = sqrt(bsum(a, sh));
+  double d = fmax(a, 1e-300);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) c[i] = c[i] / d;
+}
+
+__global__ void cm_coldot_kernel(const double* X, const double* Y, int n, double* out) {
+  __shared__ double sh[32];
+  const double* a = X + (int64_t)blockIdx.x * n;
+  const double* b = Y + (int64_t)blockIdx.x * n;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
+  s = bsum(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// interleave: Uo[i*r + j] = U[j*n + i]; V flipped where u^T B v < 0
+__global__ void cm_interleave_kernel(const double* U, const double* V, const double* sgn, int n, int r, double* Uo,
+                                     double* Vo) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * r) return;
+  int i = (int)(t / r), j = (int)(t % r);
+  Uo[t] = U[(int64_t)j * n + i];
+  double v = V[(int64_t)j * n + i];
+  Vo[t] = sgn[j] < 0.0 ? -v : v;
+}
+
+// Large-n coarsest triplets.  Md and Nd are overwritten by their Cholesky
+// factors (they are the caller's dense temporaries).
+int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double* Nd, int n, int r, double* U,
+                            double* V, double* sigma) {
+  const size_t nn = (size_t)n * n;
+  const int p = r + 12 < n ? r + 12 : n;
+  double *K, *Kp, *Y, *Z, *Gs, *Ri, *tmp, *Vs, *sv, *work, *a0, *b0, *A, *Bv, *KB, *dots;
+  int* bad;
+  BAMG_TRY(arena_get(ctx, nn, &K));
+  BAMG_TRY(arena_get(ctx, nn, &Kp));
+  BAMG_TRY(arena_get(ctx, (size_t)n * p, &Y));
+  BAMG_TRY(arena_get(ctx, (size_t)n * p, &Z));
+  BAMG_TRY(arena_get(ctx, (size_t)n * p, &tmp));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Gs));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Ri));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Vs));
+  BAMG_TRY(arena_get(ctx, (size_t)p, &sv));
+  BAMG_TRY(arena_get(ctx, (size_t)NB * NB + (size_t)NB * (n + 1) + 64, &work));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &a0));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &b0));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &A));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Bv));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &KB));
+  BAMG_TRY(arena_get(ctx, (size_t)r, &dots));
+  BAMG_TRY(arena_get(ctx, 1, &bad));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  // symmetrised masses (bootstrap.py:217-218), Cholesky in place
+  BAMG_LAUNCH(ctx, symmetrize_inplace_kernel, grid_for((int64_t)nn, 256), 256, 0, Md, n);
+  BAMG_LAUNCH(ctx, symmetrize_inplace_kernel, grid_for((int64_t)nn, 256), 256, 0, Nd, n);
+  BAMG_TRY(cholesky_blocked(ctx, Md, n, bad, work));
+  BAMG_TRY(cholesky_blocked(ctx, Nd, n, bad, work));
+  int hb = 0;
+  BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
+  if (hb) {
+    ctx->err = "mass matrix is not positive definite (Cholesky pivot <= 0)";
+    return 2;
+  }
+  // K = L_M^-1 B L_N^-T :  T = L_M^-1 B ; K^T = L_N^-1 T^T
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(K, Bd, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(tri_solve(ctx, Md, n, true, false, false, K, n, n, work));
+  BAMG_TRY(transpose_sq(ctx, K, n, Kp));
+  BAMG_TRY(tri_solve(ctx, Nd, n, true, false, false, Kp, n, n, work));
+  BAMG_TRY(transpose_sq(ctx, Kp, n, K));
+  // K^+ (column-major into Kp) and the exact null triplet (K b0 = 0, a0^T K = 0);
+  // a nonsingular K (chains whose coarse column sums drifted) takes K^-1 and
+  // all r slots from the subspace iteration
+  int rc = large_bordered_pinv(ctx, K, n, Kp, 0, b0, a0);
+  if (rc < 0) return rc;
+  const bool null_slot = rc == 0;
+  if (rc == 1) {
+    rc = large_full_rank_inverse(ctx, K, n, Kp, 0);
+    if (rc < 0) return rc;
+    if (rc == 1) {
+      ctx->err = "large coarsest operator: neither rank n-1 nor well-conditioned full rank (no dense SVD at this size)";
+      return -2;
+    }
+  }
+  // block subspace iteration on K^+ : Z = orth(K^+^T Y), Y = orth(K^+ Z)
+  BAMG_LAUNCH(ctx, pseudo_random_kernel, grid_for((int64_t)n * p, 256), 256, 0, Y, (int64_t)n * p, 12345u);
+  BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+  std::vector<double> prev(p, 0.0), cur(p, 0.0);
+  int iters = 0;
+  for (int it = 0; it < 500; ++it) {
+    BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+    BAMG_TRY(orthonormalize(ctx, Z, n, p, Gs, Ri, tmp));
+    BAMG_TRY(gemm(ctx, false, false, n, p, n, 1.0, Kp, n, Z, n, 0.0, Y, n));
+    BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+    iters = it + 1;
+    if ((it + 1) % 5 == 0) {
+      BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+      BAMG_TRY(jacobi_svd_public(ctx, Z, n, p, Vs, sv));
+      BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
+      std::vector<double> c2 = cur;
+      std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
+      double change = 0.0;
+      for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
+      prev = c2;
+      if (change < 1e-14) break;
+    }
+  }
+  // Rayleigh-Ritz: G = K^+^T Y, Jacobi: G Vs = W diag(s); K's left vectors
+  // are W's columns, right vectors Y Vs
+  BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+  BAMG_TRY(jacobi_svd_public(ctx, Z, n, p, Vs, sv));
+  std::vector<double> sh(p);
+  BAMG_TRY(ctx_read_doubles(ctx, sv, p, sh.data()));
+  std::vector<int> order(p);
+  for (int q = 0; q < p; ++q) order[q] = q;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return sh[a] > sh[b] || (sh[a] == sh[b] && a < b); });
+  BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Vs, p, 0.0, tmp, n));
+  std::vector<double> sig_host(r);
+  const int first = null_slot ? 1 : 0;
+  if (null_slot) {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(A, a0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Bv, b0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    sig_host[0] = 0.0;
+  }
+  for (int j = first; j < r; ++j) {
+    int q = order[j - first];
+    sig_host[j] = sh[q] > 0.0 ? 1.0 / sh[q] : INFINITY;
+    BAMG_TRY(copy_block(ctx, Z + (int64_t)q * n, n, A + (int64_t)j * n, n, n, 1));
+    BAMG_TRY(copy_block(ctx, tmp + (int64_t)q * n, n, Bv + (int64_t)j * n, n, n, 1));
+  }
+  double smax = 0.0;
+  int ntiny = 0;
+  for (int j = 0; j < r; ++j) smax = fmax(smax, sig_host[j]);
+  for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
+  BAMG_REQUIRE(ctx, ntiny <= 1, "large coarsest operator has more than one numerically-null triplet");
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+  // unit a, b  ->  u = L_M^-T a, v = L_N^-T b are M- / N-normalised
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, A, n);
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, Bv, n);
+  // sign rule u^T B v = a^T K b >= 0
+  BAMG_TRY(gemm(ctx, false, false, n, r, n, 1.0, K, n, Bv, n, 0.0, KB, n));
+  BAMG_LAUNCH(ctx, cm_coldot_kernel, r, 256, 0, A, KB, n, dots);
+  BAMG_TRY(tri_solve(ctx, Md, n, true, false, true, A, n, r, work));
+  BAMG_TRY(tri_solve(ctx, Nd, n, true, false, true, Bv, n, r, work));
+  BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] large triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p, iters,
+            r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);
+  return 0;
+}

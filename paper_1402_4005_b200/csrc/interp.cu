@@ -28,7 +28,7 @@
 
 constexpr int FIT_WARPS = 4;     // warps per CTA
 constexpr int CMAX = 8;          // largest caliber supported
-constexpr int MAXCAND = 48;      // candidate list capacity per point
+constexpr int MAXCAND = 256;     // candidate list capacity per point (warp path)
 
 struct FitLane {
   int lane;
@@ -369,7 +369,6 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
                 int32_t* __restrict__ out_col, double* __restrict__ out_val,
                 unsigned long long* __restrict__ status, const int32_t* __restrict__ list, int nlist) {
   __shared__ int s_cand[FIT_WARPS][MAXCAND];
-  __shared__ int s_two[FIT_WARPS][4 * MAXCAND];
   __shared__ double s_V[FIT_WARPS][CMAX * CMAX];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -427,22 +426,20 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
     }
     if (m == 0 && re > rb) {  // radius-2 (escalation or configured)
       if (lane == 0) {
-        int* two = s_two[wib];
+        // only coarse points (!= i) enter the sorted set: the reference's
+        // unique(one + two-hop) filtered by (two != i) & coarse_mask
         int len = 0;
         bool ok = true;
         for (int j = rb; j < re && ok; ++j) {
           int p = acol[j];
-          ok = sorted_insert(two, &len, p, 4 * MAXCAND);
-          for (int q = arp[p]; q < arp[p + 1] && ok; ++q) ok = sorted_insert(two, &len, acol[q], 4 * MAXCAND);
-        }
-        if (!ok) atomicOr(status + 1, 1ull);
-        for (int t = 0; t < len; ++t) {
-          int p = two[t];
-          if (p != i && crank[p] >= 0) {
-            if (m < MAXCAND) cand[m] = p;
-            ++m;
+          if (p != i && crank[p] >= 0) ok = sorted_insert(cand, &len, p, MAXCAND);
+          for (int q = arp[p]; q < arp[p + 1] && ok; ++q) {
+            int x = acol[q];
+            if (x != i && crank[x] >= 0) ok = sorted_insert(cand, &len, x, MAXCAND);
           }
         }
+        if (!ok) atomicOr(status + 1, 1ull);
+        m = len;
       }
       m = __shfl_sync(0xffffffffu, m, 0);
     }
@@ -557,30 +554,41 @@ struct TModel {
   double data, total;
 };
 
+// KM <= 16: "exact" mode, KM == k at compile time -- every loop over the tests
+// is unrolled, test t lives in registers, and infinite-weight tests are
+// masked by sw = 0 (their rows add exact zeros).  KM == 32: generic mode for
+// any k, finite tests compacted into f[] (local memory).
 template <int KM>
 struct TPoint {
+  static constexpr bool EXACT = KM <= 16;
   const double* X;
   int k;
-  int nf;               // finite tests
-  int f[KM];            // their indices
-  double y[KM];         // fine values
-  double sw[KM];        // sqrt weights
+  int nf;                        // finite tests (generic mode)
+  int f[EXACT ? 1 : KM];         // their indices (generic mode)
+  double y[KM];                  // fine values
+  double sw[KM];                 // sqrt weights (0 for masked tests)
   int cand[TMAXC];
   double lam;
+  __device__ __forceinline__ int ntest() const { return EXACT ? KM : nf; }
+  __device__ __forceinline__ int stride() const { return EXACT ? KM : k; }
+  __device__ __forceinline__ int test(int t) const {
+    if constexpr (EXACT) return t;
+    else return f[t];
+  }
 };
 
 // column value a_{fq} = sw_f * (C[f, col] - C[f, base]) (base < 0: no shift)
 template <int KM>
 __device__ __forceinline__ double tcol(const TPoint<KM>& P, int t, int col, int base) {
-  double c = __ldg(P.X + (int64_t)col * P.k + P.f[t]);
-  if (base >= 0) c -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
+  double c = __ldg(P.X + (int64_t)col * P.stride() + P.test(t));
+  if (base >= 0) c -= __ldg(P.X + (int64_t)base * P.stride() + P.test(t));
   return P.sw[t] * c;
 }
 
 template <int KM>
 __device__ __forceinline__ double ttarget(const TPoint<KM>& P, int t, int base) {
   double yv = P.y[t];
-  if (base >= 0) yv -= __ldg(P.X + (int64_t)base * P.k + P.f[t]);
+  if (base >= 0) yv -= __ldg(P.X + (int64_t)base * P.stride() + P.test(t));
   return P.sw[t] * yv;
 }
 
@@ -596,7 +604,7 @@ __device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base
 #pragma unroll
     for (int q = 0; q < TCAL; ++q) G[p][q] = 0.0;
   }
-  for (int t = 0; t < P.nf; ++t) {
+  _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
     double a[TCAL];
 #pragma unroll
     for (int q = 0; q < TCAL; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
@@ -668,7 +676,7 @@ __device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base
     double g[TCAL];
 #pragma unroll
     for (int q = 0; q < TCAL; ++q) g[q] = q < nc ? -l2 * c[q] : 0.0;  // ridge rows: -lam * (lam c)
-    for (int t = 0; t < P.nf; ++t) {
+    _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
       double a[TCAL];
       double r = ttarget(P, t, base);
 #pragma unroll
@@ -686,7 +694,7 @@ __device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base
       if (q < nc) c[q] += dlt[q];
   }
   double mis = 0.0;
-  for (int t = 0; t < P.nf; ++t) {
+  _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
     double r = 0.0;
 #pragma unroll
     for (int q = 0; q < TCAL; ++q)
@@ -734,7 +742,7 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
         for (int q = 1; q < TCAL; ++q) coef[q] = (q < wl) ? ct[q - 1] : 0.0;
       } else {
         double mis = 0.0;
-        for (int t = 0; t < P.nf; ++t) {
+        _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
           double r = ttarget(P, t, base);
           mis += r * r;
         }
@@ -886,19 +894,32 @@ fit_rows_thread_kernel(const int32_t* __restrict__ list, const unsigned int* __r
     out_cnt[i] = 0;
     return;
   }
-  int nf = 0;
   double empty = 0.0;
-  for (int tt = 0; tt < k; ++tt) {
-    double wt = w[tt];
-    if (!isfinite(wt)) continue;
-    double yv = X[(int64_t)i * k + tt];
-    P.f[nf] = tt;
-    P.y[nf] = yv;
-    P.sw[nf] = sqrt(wt);
-    empty += wt * (yv * yv);
-    ++nf;
+  if constexpr (TPoint<KM>::EXACT) {
+#pragma unroll
+    for (int tt = 0; tt < KM; ++tt) {
+      double wt = w[tt];
+      double yv = X[(int64_t)i * KM + tt];
+      bool fin = isfinite(wt);
+      P.y[tt] = yv;
+      P.sw[tt] = fin ? sqrt(wt) : 0.0;
+      if (fin) empty += wt * (yv * yv);
+    }
+    P.nf = KM;
+  } else {
+    int nf = 0;
+    for (int tt = 0; tt < k; ++tt) {
+      double wt = w[tt];
+      if (!isfinite(wt)) continue;
+      double yv = X[(int64_t)i * k + tt];
+      P.f[nf] = tt;
+      P.y[nf] = yv;
+      P.sw[nf] = sqrt(wt);
+      empty += wt * (yv * yv);
+      ++nf;
+    }
+    P.nf = nf;
   }
-  P.nf = nf;
 
   int sel[TCAL];
   double coefs[TCAL];
@@ -1049,11 +1070,13 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
     BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nfl, 0, sizeof(unsigned int), ctx->stream));
     BAMG_LAUNCH(ctx, fit_prepare_kernel, grid_for(n, 256), 256, 0, (int)n, coarse_rank, caliber, out_cnt, out_col,
                 out_val, flist, nfl);
-    if (k <= 16) {
-      BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<16>, grid_for(n, 128), 128, 0, flist, nfl,
-                      adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
-                      nonnegative, out_cnt, out_col, out_val, defer, ndefer);
-    } else {
+#define BAMG_FIT_EXACT(KK)                                                                                       \
+  if (k == KK) {                                                                                                   \
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<KK>, grid_for(n, 128), 128, 0, flist, nfl,        \
+                    adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, \
+                    nonnegative, out_cnt, out_col, out_val, defer, ndefer);                                        \
+  } else
+    BAMG_FIT_EXACT(8) BAMG_FIT_EXACT(10) BAMG_FIT_EXACT(12) BAMG_FIT_EXACT(16) {
       BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<TKMAX>, grid_for(n, 128), 128, 0, flist, nfl,
                       adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
                       nonnegative, out_cnt, out_col, out_val, defer, ndefer);
@@ -1075,7 +1098,7 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
   int64_t st[2];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 2, st));
   if (status_host) status_host[0] = st[0];
-  BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 48 candidates or 192 two-hop states)");
+  BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 256 coarse candidates for one point)");
   return 0;
 }
 

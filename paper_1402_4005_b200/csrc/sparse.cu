@@ -128,22 +128,30 @@ struct VecIO {
   }
 };
 
-template <int EPI, int K>
+// G threads share a row, each owning V = K / G consecutive vectors (one
+// 16-byte load per neighbour when V = 2), and the row's entries are consumed
+// U at a time: all U neighbour segments are loaded before any is accumulated,
+// so each thread keeps U independent loads in flight.  256 threads per CTA,
+// 256 / G rows per CTA; col/val of the CTA's rows staged in shared memory.
+template <int EPI, int K, int G, int U>
 __global__ void __launch_bounds__(TILE_THREADS)
 csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y, EpiArgs ea) {
-  __shared__ int32_t s_rp[TILE_ROWS + 1];
-  __shared__ int32_t s_col[TILE_NNZ];
-  __shared__ double s_val[TILE_NNZ];
+  constexpr int V = K / G;
+  constexpr int RB = TILE_THREADS / G;  // rows per CTA
+  constexpr int NNZ_CAP = RB * 12;  // staged when the tile averages <= 12 entries per row
+  __shared__ int32_t s_rp[RB + 1];
+  __shared__ int32_t s_col[NNZ_CAP];
+  __shared__ double s_val[NNZ_CAP];
   __shared__ unsigned long long s_peak[K];
-  const int r0 = blockIdx.x * TILE_ROWS;
-  const int rows = min(TILE_ROWS, nrows - r0);
+  const int r0 = blockIdx.x * RB;
+  const int rows = min(RB, nrows - r0);
   for (int i = threadIdx.x; i <= rows; i += TILE_THREADS) s_rp[i] = rowptr[r0 + i];
   if (EPI == EPI_JACOBI && ea.peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
   __syncthreads();
   const int nz0 = s_rp[0];
   const int tile_nnz = s_rp[rows] - nz0;
-  const bool staged = tile_nnz <= TILE_NNZ;
+  const bool staged = tile_nnz <= NNZ_CAP;
   if (staged) {
     for (int j = threadIdx.x; j < tile_nnz; j += TILE_THREADS) {
       s_col[j] = col[nz0 + j];
@@ -151,71 +159,78 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
     }
   }
   __syncthreads();
-  const int lr = threadIdx.x;
+  const int lr = threadIdx.x / G;
+  const int sub = threadIdx.x - lr * G;
   if (lr < rows) {
     const int row = r0 + lr;
-    double acc[K];
+    const int voff = sub * V;
+    double acc[V];
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    for (int q = 0; q < V; ++q) acc[q] = 0.0;
     const int jb = s_rp[lr], je = s_rp[lr + 1];
-    for (int j = jb; j < je; ++j) {
-      int c;
-      double a;
-      if (staged) {
-        c = s_col[j - nz0];
-        a = s_val[j - nz0];
-      } else {
-        c = col[j];
-        a = val[j];
-      }
-      double xv[K];
-      VecIO<K>::load(X + (int64_t)c * K, xv);
+    for (int j = jb; j < je; j += U) {
+      int cc[U];
+      double aa[U];
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(a, xv[q]));
+      for (int u = 0; u < U; ++u) {
+        const int jj = j + u < je ? j + u : je - 1;
+        cc[u] = staged ? s_col[jj - nz0] : col[jj];
+        aa[u] = staged ? s_val[jj - nz0] : val[jj];
+      }
+      double xv[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u) VecIO<V>::load(X + (int64_t)cc[u] * K + voff, xv[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (j + u < je) {
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+        }
+      }
     }
-    const int64_t base = (int64_t)row * K;
-    double out[K];
+    const int64_t base = (int64_t)row * K + voff;
+    double out[V];
     if (EPI == EPI_PLAIN) {
 #pragma unroll
-      for (int q = 0; q < K; ++q) out[q] = acc[q];
+      for (int q = 0; q < V; ++q) out[q] = acc[q];
     } else if (EPI == EPI_RESID) {
-      double bv[K];
-      VecIO<K>::load(ea.b + base, bv);
+      double bv[V];
+      VecIO<V>::load(ea.b + base, bv);
 #pragma unroll
-      for (int q = 0; q < K; ++q) out[q] = __dsub_rn(bv[q], acc[q]);
+      for (int q = 0; q < V; ++q) out[q] = __dsub_rn(bv[q], acc[q]);
     } else if (EPI == EPI_ADD) {
-      double xo[K];
-      VecIO<K>::load(ea.xold + base, xo);
+      double xo[V];
+      VecIO<V>::load(ea.xold + base, xo);
 #pragma unroll
-      for (int q = 0; q < K; ++q) out[q] = __dadd_rn(xo[q], acc[q]);
+      for (int q = 0; q < V; ++q) out[q] = __dadd_rn(xo[q], acc[q]);
     } else {
-      double bv[K];
+      double bv[V];
       if (ea.b) {
-        VecIO<K>::load(ea.b + base, bv);
+        VecIO<V>::load(ea.b + base, bv);
         if (ea.b_scale) {
 #pragma unroll
-          for (int q = 0; q < K; ++q) bv[q] = __dmul_rn(ea.b_scale[q], bv[q]);
+          for (int q = 0; q < V; ++q) bv[q] = __dmul_rn(ea.b_scale[voff + q], bv[q]);
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < K; ++q) bv[q] = 0.0;
+        for (int q = 0; q < V; ++q) bv[q] = 0.0;
       }
-      double xo[K];
-      VecIO<K>::load(ea.xold + base, xo);
+      double xo[V];
+      VecIO<V>::load(ea.xold + base, xo);
       const bool sk = ea.skip[row] != 0;
       const double dd = ea.d[row];
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
+      for (int q = 0; q < V; ++q) {
         double upd = sk ? 0.0 : __ddiv_rn(__dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q])), dd);
         out[q] = __dadd_rn(xo[q], upd);
       }
       if (ea.peak) {
 #pragma unroll
-        for (int q = 0; q < K; ++q)
-          atomicMax(&s_peak[q], (unsigned long long)__double_as_longlong(fabs(out[q])));
+        for (int q = 0; q < V; ++q)
+          atomicMax(&s_peak[voff + q], (unsigned long long)__double_as_longlong(fabs(out[q])));
       }
     }
-    VecIO<K>::store(Y + base, out);
+    VecIO<V>::store(Y + base, out);
   }
   if (EPI == EPI_JACOBI && ea.peak) {
     __syncthreads();
@@ -224,20 +239,22 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 }
 
 template <int EPI>
-static int launch_rows(bamg_ctx* ctx, int k, int grid, double bytes, const bamg_csr* A, const double* X, double* Y,
+static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const bamg_csr* A, const double* X, double* Y,
                        const EpiArgs& ea) {
   switch (k) {
-#define BAMG_ROWS_CASE(KK)                                                                                     \
-  case KK:                                                                                                     \
-    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK>), grid, TILE_THREADS, 0, A->nrows, A->rowptr, \
-                    A->col, A->val, X, Y, ea);                                                                 \
-    return 0;
-    BAMG_ROWS_CASE(1)
-    BAMG_ROWS_CASE(2)
-    BAMG_ROWS_CASE(4)
-    BAMG_ROWS_CASE(8)
-    BAMG_ROWS_CASE(12)
-    BAMG_ROWS_CASE(16)
+#define BAMG_ROWS_CASE(KK, GG, UU)                                                                                  \
+  case KK: {                                                                                                        \
+    int g = (A->nrows + TILE_THREADS / GG - 1) / (TILE_THREADS / GG);                                               \
+    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU>), g, TILE_THREADS, 0, A->nrows, A->rowptr, \
+                    A->col, A->val, X, Y, ea);                                                                      \
+    return 0;                                                                                                       \
+  }
+    BAMG_ROWS_CASE(1, 1, 4)
+    BAMG_ROWS_CASE(2, 1, 4)
+    BAMG_ROWS_CASE(4, 2, 4)
+    BAMG_ROWS_CASE(8, 4, 4)
+    BAMG_ROWS_CASE(12, 6, 4)
+    BAMG_ROWS_CASE(16, 8, 4)
 #undef BAMG_ROWS_CASE
     default:
       return 1;  // not specialised

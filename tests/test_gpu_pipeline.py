@@ -118,3 +118,35 @@ def test_gmres_matches(runs, name):
     assert rep.converged == bool(g["converged"])
     x = _sign_fix_l1(rep.x)
     assert np.abs(x - g["x"]).sum() <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_uniform63", "pipe_tandem32_k16_r30",
+                                  "pipe_petri10_normal"])
+def test_large_coarsest_path_matches(golden, name, monkeypatch):
+    """The blocked-LU / subspace-iteration coarsest path (used for n_L > 1536,
+    e.g. cfg4's n_L = 16,384) forced on small coarsest levels: same x0, x and
+    iteration count as the reference."""
+    from paper_1402_4005_b200 import GmresConfig, VCycleOperator, gmres, run_setup
+    from paper_1402_4005_b200.solver import _sign_fix_l1
+    monkeypatch.setenv("BAMG_DENSE_LARGE_N", "16")
+    g = golden(name)
+    prob = _problem(g)
+    cfg = _setup_cfg(g)
+    injected = int(g["cfg_ints"][13]) >= 0
+    draws = (g["init_right_draw"], g["init_left_draw"]) if injected else None
+    setup = run_setup(prob, cfg, draws=draws)
+    assert np.abs(setup.x0 - g["x0"]).sum() <= 1e-9
+    vop = VCycleOperator(setup.hierarchy, cfg.smoother)
+    got = vop.apply(g["vcycle_in"])
+    assert _close(got, g["vcycle_out"], 1e-9)
+    restart, max_iters, rtol = gmres_args(g)
+    rep = gmres(prob.B, np.zeros(prob.n), setup.x0, GmresConfig(restart=restart, max_iters=max_iters, rtol=rtol),
+                precond=vop)
+    assert abs(rep.iterations - int(g["iterations"])) <= max(1, int(0.1 * int(g["iterations"])))
+    assert np.abs(_sign_fix_l1(rep.x) - g["x"]).sum() <= 1e-8
+    # the smallest singular values of the coarsest problem agree with the small path
+    monkeypatch.setenv("BAMG_DENSE_LARGE_N", "100000")
+    ref = run_setup(prob, cfg, draws=draws)
+    s_large = setup.triplets.sigmas
+    s_small = ref.triplets.sigmas
+    assert np.allclose(s_large, s_small, rtol=1e-6, atol=1e-12)

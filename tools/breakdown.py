@@ -12,17 +12,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg1")
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
-C = {"cfg0": ("tandem", 64, 8, 65, None), "cfg1": ("uniform2d", 1023, 8, None, None),
-     "cfg2": ("tandem", 1024, 16, None, 30), "cfg4": ("tandem", 4095, 16, None, None)}[a.config]
-fam, side, k, stop, restart = C
+import bench
+fam, side, k, stop, restart, _ = bench.CONFIGS[a.config]
 t = time.time()
-prob = chains.tandem_queue(side, validate=False) if fam == "tandem" else chains.uniform_2d(side, validate=False)
+prob = bench.build_problem(a.config)
 print("gen", time.time() - t, flush=True)
-over = {"n_tests": k}
-cfg = pb.default_setup_config(fam, seed=0, **over)
-if stop:
-    from dataclasses import replace
-    cfg = replace(cfg, coarsening=replace(cfg.coarsening, stop_size=stop))
+cfg = bench.setup_config(a.config)
 g = np.random.default_rng(0)
 draws = (g.random((k, prob.n)), g.random((k, prob.n)))
 dB = DeviceCSR.from_host(prob.B)
