@@ -560,8 +560,8 @@ static int bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* Z) {
   const double bf = h[4];
   // certificate: Bb well conditioned; B z, B^T y at round-off (sigma_min << 1e-12 sigma_max
   // with sigma_max >= |B|_F / sqrt(n)); omega ~ 0 (b, c outside the ranges)
-  bool ok = pmax > 0.0 && pmin > 1e-10 * pmax && h[2] <= 1e-14 * bf / std::sqrt((double)n) &&
-            h[3] <= 1e-14 * bf / std::sqrt((double)n) && h[5] <= 1e-8 * (h[0] > h[1] ? h[0] : h[1]);
+  bool ok = pmax > 0.0 && pmin > 1e-10 * pmax && h[2] <= 1e-13 * bf / std::sqrt((double)n) &&
+            h[3] <= 1e-13 * bf / std::sqrt((double)n) && h[5] <= 1e-8 * (h[0] > h[1] ? h[0] : h[1]);
   if (!ok) return 1;
   BAMG_LAUNCH(ctx, proj_vectors_kernel, grid_for(2 * (int64_t)n, 128), 128, 0, Aug, n, z, y, r, s);
   BAMG_LAUNCH(ctx, proj_assemble_kernel, grid_for((int64_t)n * n, 256), 256, 0, Aug, n, z, y, r, s, Z);

@@ -463,6 +463,8 @@ __global__ void dot1_kernel(const double* __restrict__ a, const double* __restri
   if (threadIdx.x == 0) out[0] = s;
 }
 
+__global__ void frob2_kernel(const double* __restrict__ A, int64_t total, double* out);
+
 // Bordered pseudo-inverse of a large singular A (column-major n x n).
 // 0: written to P (row-major if rowmajor_out); 1: certificate failed.
 // zout / yout (optional) receive the unit right / left null vectors.
@@ -496,7 +498,10 @@ int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int ro
   BAMG_TRY(ctx_read_doubles(ctx, out, 6, h));
   BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
   const double bf = h[4];
-  bool ok = !hb && h[2] <= 1e-14 * bf / std::sqrt((double)n) && h[3] <= 1e-14 * bf / std::sqrt((double)n) &&
+  // sigma_min(B) <= |B z| and sigma_max >= |B|_F / sqrt(n): |B z| below
+  // 1e-13 |B|_F / sqrt(n) certifies sigma_min < 1e-13 sigma_max, ten times
+  // inside PinvOperator's 1e-12 rank rule
+  bool ok = !hb && h[2] <= 1e-13 * bf / std::sqrt((double)n) && h[3] <= 1e-13 * bf / std::sqrt((double)n) &&
             h[5] <= 1e-8 * (h[0] > h[1] ? h[0] : h[1]);
   if (getenv("BAMG_DEBUG"))
     fprintf(stderr, "[bamg] large pinv n=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e omega=%.3e bad=%d -> %s\n", n, h[2], h[3],
@@ -507,6 +512,19 @@ int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int ro
   BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Xb, m, y, n, 0.0, s, n));
   BAMG_LAUNCH(ctx, dot1_kernel, 1, 1024, 0, z, s, n, t);
   BAMG_LAUNCH(ctx, border_project_kernel, grid_for((int64_t)n * n, 256), 256, 0, Xb, n, z, y, r, s, t, P, rowmajor_out);
+  // the kept singular values: sigma_{n-1} >= 1 / |B^+|_F, so
+  // |B^+|_F |B|_F < 1e11 certifies sigma_{n-1} > 1e-11 sigma_max (kept by the rule)
+  {
+    double* f;
+    BAMG_TRY(arena_get(ctx, 1, &f));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(f, 0, sizeof(double), ctx->stream));
+    BAMG_LAUNCH(ctx, frob2_kernel, 256, 256, 0, P, (int64_t)n * n, f);
+    double pf;
+    BAMG_TRY(ctx_read_doubles(ctx, f, 1, &pf));
+    double prod = std::sqrt(pf) * bf;
+    if (getenv("BAMG_DEBUG")) fprintf(stderr, "[bamg] large pinv |B^+|F |B|F = %.3e\n", prod);
+    if (!(prod < 1e11)) return 1;
+  }
   if (zout) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(zout, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   if (yout) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(yout, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   return 0;
