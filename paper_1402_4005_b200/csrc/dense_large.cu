@@ -111,29 +111,41 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 }
 
 // Inverse of a triangular nb x nb block (ld) into Ti (nb x nb, ld nb), one
-// CTA, one thread per column of the identity.  kind 0: unit lower, 1: lower,
-// 2: upper.
+// CTA: the block is staged in shared memory (dynamic, up to 128 KB), one thread
+// per column of the identity.  kind 0: unit lower, 1: lower, 2: upper.
 __global__ void tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind, double* __restrict__ Ti) {
+  extern __shared__ double sT[];
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    int r = t % nb, c = t / nb;
+    sT[t] = T[(int64_t)c * ld + r];
+  }
+  __syncthreads();
   int c = threadIdx.x;
   if (c >= nb) return;
   double* x = Ti + (int64_t)c * nb;
   if (kind == 2) {
     for (int i = nb - 1; i >= 0; --i) {
       double s = (i == c) ? 1.0 : 0.0;
-      for (int j = i + 1; j < nb; ++j) s -= T[(int64_t)j * ld + i] * x[j];
-      x[i] = s / T[(int64_t)i * ld + i];
+      for (int j = i + 1; j < nb; ++j) s -= sT[j * nb + i] * x[j];
+      x[i] = s / sT[i * nb + i];
     }
   } else {
     for (int i = 0; i < nb; ++i) {
       double s = (i == c) ? 1.0 : 0.0;
-      for (int j = 0; j < i; ++j) s -= T[(int64_t)j * ld + i] * x[j];
-      x[i] = kind == 0 ? s : s / T[(int64_t)i * ld + i];
+      for (int j = 0; j < i; ++j) s -= sT[j * nb + i] * x[j];
+      x[i] = kind == 0 ? s : s / sT[i * nb + i];
     }
   }
 }
 
 static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
-  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, NB, 0, T, ld, nb, kind, Ti);
+  static bool attr = false;
+  const int smem = NB * NB * (int)sizeof(double);
+  if (!attr) {
+    BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, NB, smem, T, ld, nb, kind, Ti);
   return 0;
 }
 
@@ -178,25 +190,31 @@ static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, b
 }
 
 // ------------------------------------------------------------- Cholesky
-// unblocked in-place lower Cholesky of a jb x jb diagonal block (one CTA)
+// unblocked in-place lower Cholesky of a jb x jb diagonal block (one CTA,
+// block staged in dynamic shared memory)
 __global__ void chol_block_kernel(double* A, int ld, int jb, int* bad) {
-  __shared__ double d;
+  extern __shared__ double sA[];
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) sA[t] = A[(int64_t)(t / jb) * ld + (t % jb)];
+  __syncthreads();
   for (int j = 0; j < jb; ++j) {
+    double p = sA[j * jb + j];
+    double d = sqrt(fmax(p, 1e-300));
+    __syncthreads();
     if (threadIdx.x == 0) {
-      double p = A[(int64_t)j * ld + j];
       if (!(p > 0.0)) *bad = 1;
-      d = sqrt(fmax(p, 1e-300));
-      A[(int64_t)j * ld + j] = d;
+      sA[j * jb + j] = d;
     }
+    for (int i = j + 1 + threadIdx.x; i < jb; i += blockDim.x) sA[j * jb + i] /= d;
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < jb; i += blockDim.x) A[(int64_t)j * ld + i] /= d;
-    __syncthreads();
-    for (int k = j + 1; k < jb; ++k) {
-      double lk = A[(int64_t)j * ld + k];
-      for (int i = k + threadIdx.x; i < jb; i += blockDim.x) A[(int64_t)k * ld + i] -= A[(int64_t)j * ld + i] * lk;
+    // trailing update of the lower triangle: columns k > j
+    int m = jb - j - 1;
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+      int i = j + 1 + t % m, k = j + 1 + t / m;
+      if (i >= k) sA[k * jb + i] -= sA[j * jb + i] * sA[j * jb + k];
     }
     __syncthreads();
   }
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) A[(int64_t)(t / jb) * ld + (t % jb)] = sA[t];
 }
 
 __global__ void zero_upper_kernel(double* A, int n) {
@@ -212,7 +230,15 @@ static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* w
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
     double* Ajj = A + (int64_t)j0 * n + j0;
-    BAMG_LAUNCH(ctx, chol_block_kernel, 1, 256, 0, Ajj, n, jb, bad);
+    {
+      static bool attr = false;
+      const int smem = NB * NB * (int)sizeof(double);
+      if (!attr) {
+        BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+      }
+      BAMG_LAUNCH(ctx, chol_block_kernel, 1, 1024, smem, Ajj, n, jb, bad);
+    }
     int r0 = j0 + jb, rn = n - r0;
     if (rn <= 0) break;
     BAMG_TRY(tri_inv(ctx, Ajj, n, jb, 1, Li));
@@ -356,25 +382,34 @@ static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, doubl
   return 0;
 }
 
-// X = P^T-permuted identity: row swaps of piv applied to I (column-major n x n)
-__global__ void perm_identity_kernel(double* X, int n, const int* piv) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  double* col = X + (int64_t)c * n;
-  for (int r = 0; r < n; ++r) col[r] = (r == c) ? 1.0 : 0.0;
+// row permutation of the identity: perm[r] = source row after the swaps of piv
+__global__ void perm_vector_kernel(int n, const int* piv, int* perm) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int r = 0; r < n; ++r) perm[r] = r;
   for (int j = 0; j < n; ++j) {
     int p = piv[j];
     if (p != j) {
-      double t = col[j];
-      col[j] = col[p];
-      col[p] = t;
+      int t = perm[j];
+      perm[j] = perm[p];
+      perm[p] = t;
     }
   }
 }
 
+// X[r][c] = (perm[r] == c): the row swaps of piv applied to I (coalesced)
+__global__ void perm_identity_kernel(double* X, int n, const int* perm) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n) return;
+  int r = (int)(t % n), c = (int)(t / n);
+  X[t] = perm[r] == c ? 1.0 : 0.0;
+}
+
 // inverse from the LU factors (A = P^T L U): X = U^-1 L^-1 P I
 static int lu_inverse(bamg_ctx* ctx, const double* LU, int n, const int* piv, double* X, double* work) {
-  BAMG_LAUNCH(ctx, perm_identity_kernel, grid_for(n, 128), 128, 0, X, n, piv);
+  int* perm;
+  BAMG_TRY(arena_get(ctx, (size_t)n, &perm));
+  BAMG_LAUNCH(ctx, perm_vector_kernel, 1, 32, 0, n, piv, perm);
+  BAMG_LAUNCH(ctx, perm_identity_kernel, grid_for((int64_t)n * n, 256), 256, 0, X, n, perm);
   BAMG_TRY(tri_solve(ctx, LU, n, true, true, false, X, n, n, work));    // L (unit lower)
   BAMG_TRY(tri_solve(ctx, LU, n, false, false, false, X, n, n, work));  // U (upper)
   return 0;
@@ -424,20 +459,19 @@ __global__ void border_null_kernel(const double* __restrict__ Xb, int n, double*
 __global__ void border_cert_kernel(const double* __restrict__ Bz, const double* __restrict__ Bty,
                                    const double* __restrict__ A, int n, double* __restrict__ out) {
   __shared__ double sh[32];
-  double a = 0.0, b = 0.0, f = 0.0;
+  double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     a += Bz[i] * Bz[i];
     b += Bty[i] * Bty[i];
   }
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n; t += blockDim.x) f += A[t] * A[t];
   a = bsum(a, sh);
   b = bsum(b, sh);
-  f = bsum(f, sh);
   if (threadIdx.x == 0) {
     out[2] = sqrt(a);
     out[3] = sqrt(b);
-    out[4] = sqrt(f);
+    out[4] = sqrt(out[6]);  // |A|_F^2 accumulated by frob2_kernel into out[6]
   }
+  (void)A;
 }
 
 // P = (I - z z^T) X (I - y y^T) with X = Xb[0:n, 0:n]; r = z^T X, s = X y,
@@ -492,6 +526,8 @@ int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int ro
   // certificate: |B z|, |B^T y| at round-off, omega ~ 0, LU pivots nonzero
   BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, A, n, z, n, 0.0, r, n));
   BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, A, n, y, n, 0.0, s, n));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(out + 6, 0, sizeof(double), ctx->stream));
+  BAMG_LAUNCH(ctx, frob2_kernel, 2 * ctx->num_sms, 256, 0, A, (int64_t)n * n, out + 6);
   BAMG_LAUNCH(ctx, border_cert_kernel, 1, 1024, 0, r, s, A, n, out);
   double h[6];
   int hb = 0;

@@ -358,35 +358,42 @@ __global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const doub
                               double beta, double* __restrict__ R, double* __restrict__ g,
                               double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ y,
                               double* __restrict__ state) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double hj1 = sqrt(nrm2[0]);
-  h[j + 1] = hj1;
-  double happy = (hj1 <= 1e-14 * beta) ? 1.0 : 0.0;
-  for (int i = 0; i < j; ++i) {
-    double t = cs[i] * h[i] + sn[i] * h[i + 1];
-    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
-    h[i] = t;
+  extern __shared__ double sg[];  // j+1 working entries of g during the back substitution
+  if (threadIdx.x == 0) {
+    double hj1 = sqrt(nrm2[0]);
+    h[j + 1] = hj1;
+    double happy = (hj1 <= 1e-14 * beta) ? 1.0 : 0.0;
+    for (int i = 0; i < j; ++i) {
+      double t = cs[i] * h[i] + sn[i] * h[i + 1];
+      h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+      h[i] = t;
+    }
+    double rad = hypot(h[j], h[j + 1]);
+    if (rad == 0.0) {
+      cs[j] = 1.0;
+      sn[j] = 0.0;
+    } else {
+      cs[j] = h[j] / rad;
+      sn[j] = h[j + 1] / rad;
+    }
+    for (int i = 0; i < j; ++i) R[(int64_t)j * ldr + i] = h[i];  // column j (column-major)
+    R[(int64_t)j * ldr + j] = rad;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    state[0] = happy;
+    state[1] = hj1;
   }
-  double rad = hypot(h[j], h[j + 1]);
-  if (rad == 0.0) {
-    cs[j] = 1.0;
-    sn[j] = 0.0;
-  } else {
-    cs[j] = h[j] / rad;
-    sn[j] = h[j + 1] / rad;
-  }
-  for (int i = 0; i <= j; ++i) R[(int64_t)j * ldr + i] = h[i];  // column j (column-major)
-  R[(int64_t)j * ldr + j] = rad;
-  g[j + 1] = -sn[j] * g[j];
-  g[j] = cs[j] * g[j];
-  // back substitution R[:j+1,:j+1] y = g[:j+1]
+  __syncthreads();
+  // back substitution R[:j+1, :j+1] y = g[:j+1], column-oriented: y_i, then
+  // the CTA removes column i of R from the remaining right-hand side
+  for (int q = threadIdx.x; q <= j; q += blockDim.x) sg[q] = g[q];
+  __syncthreads();
   for (int i = j; i >= 0; --i) {
-    double s = g[i];
-    for (int q = i + 1; q <= j; ++q) s -= R[(int64_t)q * ldr + i] * y[q];
-    y[i] = s / R[(int64_t)i * ldr + i];
+    const double yi = sg[i] / R[(int64_t)i * ldr + i];
+    if (threadIdx.x == 0) y[i] = yi;
+    for (int q = threadIdx.x; q < i; q += blockDim.x) sg[q] -= R[(int64_t)i * ldr + q] * yi;
+    __syncthreads();
   }
-  state[0] = happy;
-  state[1] = hj1;
 }
 
 // dst = w / h  unless the happy-breakdown flag is set
@@ -608,7 +615,8 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       BAMG_LAUNCH(ctx, mreduce_kernel, 1, 32, 0, part, nb, 1, scal + 3, 0);
       // h += h2 (length j+1) via the reduce kernel's accumulate path
       BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, h2, 1, j + 1, hv, 1);
-      BAMG_LAUNCH(ctx, givens_kernel, 1, 32, 0, j, m_cap, hv, scal + 3, beta, R, g, cs, sn, y, state);
+      BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn, y,
+                  state);
       BAMG_LAUNCH(ctx, scale_new_basis_kernel, grd, blk, 0, w, state, n, W.basis[j + 1]);
       ++iters;
       used = j + 1;
