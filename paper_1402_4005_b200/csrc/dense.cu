@@ -267,7 +267,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
 int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out);
 
 static int large_threshold() {
-  int t = 1536;
+  int t = 512;
   if (const char* e = getenv("BAMG_DENSE_LARGE_N")) t = atoi(e);
   return t;
 }

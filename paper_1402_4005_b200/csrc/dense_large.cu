@@ -29,7 +29,7 @@
 
 namespace cg = cooperative_groups;
 
-constexpr int NB = 128;  // block size of the blocked algorithms
+constexpr int NB = 64;  // block size of the blocked algorithms
 
 static cublasHandle_t cublas(bamg_ctx* ctx) {
   static thread_local std::vector<std::pair<bamg_ctx*, cublasHandle_t>> table;
@@ -114,38 +114,53 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 // CTA: the block is staged in shared memory (dynamic, up to 128 KB), one thread
 // per column of the identity.  kind 0: unit lower, 1: lower, 2: upper.
 __global__ void tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind, double* __restrict__ Ti) {
-  extern __shared__ double sT[];
+  extern __shared__ double sm[];
+  double* sT = sm;            // nb x nb block
+  double* sX = sm + nb * nb;  // nb x nb inverse, built row by row
   for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
     int r = t % nb, c = t / nb;
     sT[t] = T[(int64_t)c * ld + r];
   }
   __syncthreads();
-  int c = threadIdx.x;
-  if (c >= nb) return;
-  double* x = Ti + (int64_t)c * nb;
-  if (kind == 2) {
-    for (int i = nb - 1; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int j = i + 1; j < nb; ++j) s -= sT[j * nb + i] * x[j];
-      x[i] = s / sT[i * nb + i];
+  // row-oriented substitution: step s fixes row i of X for all columns at once
+  const int c = threadIdx.x % nb;
+  const int lane_rows = blockDim.x / nb;  // threads sharing a column split the inner sum
+  const int part = threadIdx.x / nb;
+  for (int s = 0; s < nb; ++s) {
+    const int i = (kind == 2) ? nb - 1 - s : s;
+    double acc = 0.0;
+    if (kind == 2) {
+      for (int j = i + 1 + part; j < nb; j += lane_rows) acc += sT[j * nb + i] * sX[c * nb + j];
+    } else {
+      for (int j = part; j < i; j += lane_rows) acc += sT[j * nb + i] * sX[c * nb + j];
     }
-  } else {
-    for (int i = 0; i < nb; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int j = 0; j < i; ++j) s -= sT[j * nb + i] * x[j];
-      x[i] = kind == 0 ? s : s / sT[i * nb + i];
+    // combine the partial sums of the threads sharing column c (warp shuffles
+    // would cross columns; use shared scratch after the X block)
+    double* red = sm + 2 * nb * nb;
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (part == 0) {
+      double tot = 0.0;
+      for (int q = 0; q < lane_rows; ++q) tot += red[q * nb + c];
+      double rhs = (i == c ? 1.0 : 0.0) - tot;
+      sX[c * nb + i] = (kind == 0) ? rhs : rhs / sT[i * nb + i];
     }
+    __syncthreads();
   }
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) Ti[t] = sX[t];
 }
 
 static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
   static bool attr = false;
-  const int smem = NB * NB * (int)sizeof(double);
+  const int threads = 8 * NB;  // 8 threads per column
+  const int smem = (2 * NB * NB + threads) * (int)sizeof(double);
   if (!attr) {
     BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, NB, smem, T, ld, nb, kind, Ti);
+  // a partial last block (nb < NB) keeps 8 threads per column of ITS width
+  int th = 8 * nb;
+  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, th, smem, T, ld, nb, kind, Ti);
   return 0;
 }
 
