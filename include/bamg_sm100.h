@@ -243,6 +243,21 @@ int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* b,
 /* y = Z b for a row-major dense n x n Z (the coarsest pseudo-inverse apply,
  * dense.py:130-131). */
 int bamg_dense_gemv(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y);
+/* Rank-local building blocks of the row-partitioned solve (distributed.py):
+ * operators use halo-extended column numbering; mdot / mupdate return local
+ * partial sums that the caller all-reduces over NCCL.  Vp is a DEVICE array
+ * of m basis-vector pointers. */
+int bamg_residual(bamg_ctx* ctx, const bamg_csr* A, const double* b, const double* x, double* r);
+int bamg_addmv(bamg_ctx* ctx, const bamg_csr* A, const double* xc, const double* xold, double* y);
+int bamg_jacobi_zero(bamg_ctx* ctx, int64_t n, const double* b, const double* d, const uint8_t* skip,
+                     double omega, double* x);
+int bamg_dense_gemv_rows(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y);
+int bamg_mdot(bamg_ctx* ctx, const double* const* Vp, int m, const double* w, int64_t n, double* out);
+int bamg_mupdate(bamg_ctx* ctx, const double* const* Vp, int m, const double* c, double* w, int64_t n,
+                 double* nrm2);
+int bamg_combine(bamg_ctx* ctx, const double* const* Vp, int m, const double* y, const double* base,
+                 const double* add, int64_t n, double* out);
+
 /* x0 finalisation (bootstrap.py:420-428 and solver.py:229-235): non-finite or
  * all-zero -> uniform 1/n, sign so the max-|.| entry is positive, l1 = 1. */
 int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int stride, double* out,

@@ -92,6 +92,13 @@ _SIGS = {
     "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, C.c_int, PINT, PF64, PINT],
     "bamg_dense_gemv": [P, P, C.c_int, P, P],
     "bamg_sign_fix_l1": [P, P, I64, C.c_int, P, C.c_int],
+    "bamg_residual": [P, PCSR, P, P, P],
+    "bamg_addmv": [P, PCSR, P, P, P],
+    "bamg_jacobi_zero": [P, I64, P, P, P, F64, P],
+    "bamg_dense_gemv_rows": [P, P, C.c_int, P, P],
+    "bamg_mdot": [P, P, C.c_int, P, I64, P],
+    "bamg_mupdate": [P, P, C.c_int, P, P, I64, P],
+    "bamg_combine": [P, P, C.c_int, P, P, P, I64, P],
 }
 _RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64}
 

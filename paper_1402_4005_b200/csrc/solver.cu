@@ -772,3 +772,58 @@ extern "C" int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int s
   BAMG_LAUNCH(ctx, signfix_apply_kernel, grid_for(n, 256), 256, 0, out, n, stats);
   return 0;
 }
+
+// ===================================================== distributed building blocks
+// Rank-local pieces of the V-cycle and of CGS2 for the row-partitioned solve
+// (paper_1402_4005_b200/distributed.py): the operators carry halo-extended
+// column numbering, dot products are local partial sums the caller all-reduces.
+extern "C" int bamg_residual(bamg_ctx* ctx, const bamg_csr* A, const double* b, const double* x, double* r) {
+  return resid_dev(ctx, A, b, x, r);
+}
+
+extern "C" int bamg_addmv(bamg_ctx* ctx, const bamg_csr* A, const double* xc, const double* xold, double* y) {
+  return addmv_dev(ctx, A, xc, xold, y, 1);
+}
+
+extern "C" int bamg_jacobi_zero(bamg_ctx* ctx, int64_t n, const double* b, const double* d, const uint8_t* skip,
+                                double omega, double* x) {
+  BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(n, 256), 256, 0, (int)n, b, d, skip, omega, x);
+  return 0;
+}
+
+extern "C" int bamg_dense_gemv_rows(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y) {
+  BAMG_LAUNCH(ctx, gemv_rowmajor_kernel, grid_for((int64_t)n * 32, 256), 256, 0, n, Z, b, y);
+  return 0;
+}
+
+// out[i] = V_i . w  (local partial sums), i < m
+extern "C" int bamg_mdot(bamg_ctx* ctx, const double* const* Vp, int m, const double* w, int64_t n, double* out) {
+  ctx->arena.reset();
+  double* part;
+  BAMG_TRY(arena_get(ctx, (size_t)GM_BLOCKS * (m > 0 ? m : 1), &part));
+  BAMG_LAUNCH(ctx, mdot_kernel, GM_BLOCKS, GM_THREADS, 0, Vp, m, w, n, part);
+  BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)m * 32, 256), 256, 0, part, GM_BLOCKS, m, out, 0);
+  return 0;
+}
+
+// w -= sum_i c_i V_i ; nrm2 (optional) = |w_new|^2 local partial
+extern "C" int bamg_mupdate(bamg_ctx* ctx, const double* const* Vp, int m, const double* c, double* w, int64_t n,
+                            double* nrm2) {
+  ctx->arena.reset();
+  double* part;
+  BAMG_TRY(arena_get(ctx, (size_t)GM_BLOCKS + 1, &part));
+  if (nrm2) {
+    BAMG_LAUNCH(ctx, mupdate_kernel<2>, GM_BLOCKS, GM_THREADS, 0, Vp, m, c, w, n, part);
+    BAMG_LAUNCH(ctx, mreduce_kernel, 1, 32, 0, part, GM_BLOCKS, 1, nrm2, 0);
+  } else {
+    BAMG_LAUNCH(ctx, mupdate_kernel<0>, GM_BLOCKS, GM_THREADS, 0, Vp, m, c, w, n, part);
+  }
+  return 0;
+}
+
+// out = base + add + sum_i y_i V_i   (base / add may be NULL)
+extern "C" int bamg_combine(bamg_ctx* ctx, const double* const* Vp, int m, const double* y, const double* base,
+                            const double* add, int64_t n, double* out) {
+  BAMG_LAUNCH(ctx, combine_kernel, grid_for(n, 256), 256, 0, Vp, m, y, base, add, nullptr, n, out);
+  return 0;
+}

@@ -1,0 +1,92 @@
+"""Worker functions for the multi-process tests (importable by spawned ranks)."""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+def plan_worker(rank, world, port, out_dir):
+    """CPU: halo plans of every operator of a golden hierarchy + a host SpMV
+    through the plans (gloo p2p) reproduces the global product bit for bit."""
+    import torch
+    from conftest import csr_from, load_golden
+    from paper_1402_4005_b200.distributed import Comm, RowPartition, localize_host
+    dist = _init(rank, world, port)
+    comm = Comm()
+    g = load_golden("pipe_uniform63")
+    res = {}
+    rng = np.random.default_rng(3)
+    for key, rows_lv, cols_lv in (("L0_B", 0, 0), ("L0_Q", 1, 0), ("L0_P", 0, 1), ("L1_B", 1, 1)):
+        A = csr_from(g, key)
+        rp = RowPartition(A.shape[0], world)
+        cp = RowPartition(A.shape[1], world)
+        indptr, cols, vals, n_ext, plan = localize_host(A, rp, cp, rank, comm)
+        x = rng.standard_normal(A.shape[1])  # same on every rank (same seed)
+        c0, c1 = cp.range(rank)
+        x_ext = np.empty(n_ext)
+        x_ext[: c1 - c0] = x[c0:c1]
+        ops, staged = [], {}
+        for peer in sorted(set(plan.send_local) | set(plan.recv_counts)):
+            if peer in plan.send_local:
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(x_ext[plan.send_local[peer]].copy()), peer))
+            if peer in plan.recv_counts:
+                staged[peer] = torch.empty(plan.recv_counts[peer], dtype=torch.float64)
+                ops.append(dist.P2POp(dist.irecv, staged[peer], peer))
+        for r in (dist.batch_isend_irecv(ops) if ops else []):
+            r.wait()
+        for peer, t in staged.items():
+            o = plan.n_own + plan.recv_offset[peer]
+            x_ext[o:o + t.numel()] = t.numpy()
+        from scipy import sparse as sp
+        loc = sp.csr_array((vals, cols, indptr), shape=(indptr.size - 1, n_ext))
+        y_loc = loc @ x_ext
+        r0, r1 = rp.range(rank)
+        res[key] = bool(np.array_equal(y_loc, (A @ x)[r0:r1]))
+    np.save(Path(out_dir) / f"plan_{rank}.npy", np.array([res[k] for k in sorted(res)]))
+    dist.destroy_process_group()
+
+
+def solve_worker(rank, world, port, out_dir, name, agg):
+    """GPU: distributed V-cycle + GMRES on one shared device (host-staged gloo halos)."""
+    import torch
+    from conftest import csr_from, gmres_args, load_golden
+    import paper_1402_4005_b200 as pb
+    from paper_1402_4005_b200.chains import ChainProblem
+    from paper_1402_4005_b200.distributed import Comm, DistSolver
+    from test_gpu_pipeline import _setup_cfg
+    _init(rank, world, port)
+    torch.cuda.set_device(0)
+    g = load_golden(name)
+    B = csr_from(g, "B")
+    prob = ChainProblem(A=None, B=B, n=B.shape[0], family=str(g["family"]), params={},
+                        geometry=g["geometry"] if "geometry" in g else None)
+    cfg = _setup_cfg(g)
+    setup = pb.run_setup(prob, cfg, draws=(g["init_right_draw"], g["init_left_draw"]))
+    ds = DistSolver(setup.hierarchy, cfg.smoother, Comm(), agglomerate_rows=agg)
+    r0, r1 = ds.r0, ds.r1
+    vin = torch.from_numpy(np.ascontiguousarray(g["vcycle_in"][r0:r1])).cuda()
+    vout = ds.comm.all_gather_vec(ds.vc.apply(vin), ds.part).cpu().numpy()
+    restart, max_iters, rtol = gmres_args(g)
+    x0 = setup.dx0[r0:r1].contiguous()
+    its, hist, conv, x = ds.solve(x0, restart, max_iters, rtol)
+    xf = ds.gather(x).cpu().numpy()
+    np.savez(Path(out_dir) / f"solve_{rank}.npz", vout=vout, x=xf, its=its, conv=int(conv),
+             levels_partitioned=len(ds.vc.levels))
+    import torch.distributed as dist
+    dist.destroy_process_group()
