@@ -13,9 +13,11 @@ the operator, geometry and initial vectors resident in HBM;
 `e2e` = the same through `solve_steady_state` with host inputs (pinned
 H2D of B / draws / geometry and the D2H of x inside the timed region).
 
-Multi-GPU: the path is replicated, one independent solve per rank ("replicas
-only", weak scaling); every rank times its own steps and rank 0 reports the
-max over ranks.
+Multi-GPU (torchrun, one rank per GPU, NCCL): the setup runs replicated on
+every rank and the solve phase is row-partitioned (halo-exchanged V-cycle and
+CGS2 GMRES, paper_1402_4005_b200/distributed.py), strong scaling; `--replicas`
+runs independent solves instead (weak scaling).  Every rank times its own
+steps with CUDA events and rank 0 reports the max over ranks.
 """
 
 from __future__ import annotations
@@ -176,8 +178,20 @@ def run_ours(args, rank, world, local_rank):
     L = _lib.lib()
     c = _lib.ctx()
 
+    distributed = world > 1 and not args.replicas
+
+    class _Rep:
+        def __init__(self, its, hist, conv):
+            self.iterations, self.residual_history, self.converged = its, hist, conv
+
     def step():
         setup = pb.run_setup(dprob, cfg, draws=(dV, dU), B_device=dB)
+        if distributed:
+            # row-partitioned V-cycle + GMRES over NCCL (setup replicated per rank)
+            from paper_1402_4005_b200.distributed import Comm, DistSolver
+            ds = DistSolver(setup.hierarchy, cfg.smoother, Comm())
+            its, hist, conv, x = ds.solve(setup.dx0[ds.r0:ds.r1].contiguous(), restart, 1000, RTOL)
+            return setup, ds, _Rep(its, hist, conv)
         vop = pb.VCycleOperator(setup.hierarchy, cfg.smoother)
         rep = pb.gmres(dB, zero, setup.dx0, gcfg, vop, to_host=False)
         return setup, vop, rep
@@ -223,6 +237,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- V-cycle throughput (secondary metric of BASELINE.json)
     levels = setup.hierarchy.levels
+    if distributed:
+        vop = pb.VCycleOperator(setup.hierarchy, cfg.smoother)
     vb = vcycle_bytes(levels, cfg.smoother.sweeps_pre, cfg.smoother.sweeps_post)
     b = torch.randn(n, dtype=torch.float64, device="cuda")
     for _ in range(3):
@@ -287,12 +303,15 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": round(dev_s, 6), "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong" if distributed else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
         "config": {"workload": f"{name}: {desc}", "n": n, "nnz": int(dB.nnz), "k": k,
                    "gmres_restart": restart, "rtol": RTOL, "setup_cycles": cfg.setup_cycles,
                    "levels": [lv.n for lv in levels], "gmres_iterations": iters[-1],
-                   "converged": converged, "parallelism": f"replicas x{world}",
+                   "converged": converged,
+                   "parallelism": (f"row-partitioned V-cycle+GMRES over NCCL x{world}, setup replicated"
+                                   if distributed else f"replicas x{world}"),
                    "l2": "working set (operators + k-vector blocks) > 126 MB L2; no flush"},
         "vcycle": {"ms": round(vms, 4), "alg_bytes": int(vb), "GBps": round(vb / (vms / 1e3) / 1e9, 1),
                    "frac_of_hbm_peak": round(vb / (vms / 1e3) / 1e9 / peak, 4)},
@@ -372,6 +391,7 @@ def main():
     ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of the row-partitioned solve")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", 0))
