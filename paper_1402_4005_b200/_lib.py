@@ -14,7 +14,8 @@ from pathlib import Path
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libbamg_sm100.so"
+import os as _os
+LIB_PATH = Path(_os.environ.get("BAMG_LIB_PATH", str(_PKG / "libbamg_sm100.so")))
 
 
 class BamgUnavailable(RuntimeError):

@@ -133,49 +133,60 @@ struct VecIO {
 // U at a time: all U neighbour segments are loaded before any is accumulated,
 // so each thread keeps U independent loads in flight.  256 threads per CTA,
 // 256 / G rows per CTA; col/val of the CTA's rows staged in shared memory.
-template <int EPI, int K, int G, int U>
+template <int EPI, int K, int G, int U, bool STAGE>
 __global__ void __launch_bounds__(TILE_THREADS)
 csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y, EpiArgs ea) {
   constexpr int V = K / G;
   constexpr int RB = TILE_THREADS / G;  // rows per CTA
-  constexpr int NNZ_CAP = RB * 12;  // staged when the tile averages <= 12 entries per row
-  __shared__ int32_t s_rp[RB + 1];
+  constexpr int NNZ_CAP = STAGE ? RB * 12 : 1;  // staged when the tile averages <= 12 entries per row
   __shared__ int32_t s_col[NNZ_CAP];
   __shared__ double s_val[NNZ_CAP];
   __shared__ unsigned long long s_peak[K];
   const int r0 = blockIdx.x * RB;
   const int rows = min(RB, nrows - r0);
-  for (int i = threadIdx.x; i <= rows; i += TILE_THREADS) s_rp[i] = rowptr[r0 + i];
   if (EPI == EPI_JACOBI && ea.peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
-  __syncthreads();
-  const int nz0 = s_rp[0];
-  const int tile_nnz = s_rp[rows] - nz0;
-  const bool staged = tile_nnz <= NNZ_CAP;
-  if (staged) {
-    for (int j = threadIdx.x; j < tile_nnz; j += TILE_THREADS) {
-      s_col[j] = col[nz0 + j];
-      s_val[j] = val[nz0 + j];
+  int nz0 = 0;
+  bool staged = false;
+  if constexpr (STAGE) {
+    nz0 = rowptr[r0];
+    const int tile_nnz = rowptr[r0 + rows] - nz0;
+    staged = tile_nnz <= NNZ_CAP;
+    if (staged) {
+      for (int j = threadIdx.x; j < tile_nnz; j += TILE_THREADS) {
+        s_col[j] = col[nz0 + j];
+        s_val[j] = val[nz0 + j];
+      }
     }
+    __syncthreads();
+  } else if (EPI == EPI_JACOBI && ea.peak) {
+    __syncthreads();
   }
-  __syncthreads();
   const int lr = threadIdx.x / G;
   const int sub = threadIdx.x - lr * G;
+  double pk[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) pk[q] = 0.0;
   if (lr < rows) {
     const int row = r0 + lr;
     const int voff = sub * V;
     double acc[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) acc[q] = 0.0;
-    const int jb = s_rp[lr], je = s_rp[lr + 1];
+    const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
     for (int j = jb; j < je; j += U) {
       int cc[U];
       double aa[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int jj = j + u < je ? j + u : je - 1;
-        cc[u] = staged ? s_col[jj - nz0] : col[jj];
-        aa[u] = staged ? s_val[jj - nz0] : val[jj];
+        if (STAGE && staged) {
+          cc[u] = s_col[jj - nz0];
+          aa[u] = s_val[jj - nz0];
+        } else {
+          cc[u] = __ldg(col + jj);
+          aa[u] = __ldg(val + jj);
+        }
       }
       double xv[U][V];
 #pragma unroll
@@ -223,36 +234,68 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       for (int q = 0; q < V; ++q) {
         double upd = sk ? 0.0 : __ddiv_rn(__dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q])), dd);
         out[q] = __dadd_rn(xo[q], upd);
-      }
-      if (ea.peak) {
-#pragma unroll
-        for (int q = 0; q < V; ++q)
-          atomicMax(&s_peak[voff + q], (unsigned long long)__double_as_longlong(fabs(out[q])));
+        pk[q] = fabs(out[q]);
       }
     }
     VecIO<V>::store(Y + base, out);
   }
   if (EPI == EPI_JACOBI && ea.peak) {
+    // max over the lanes that own the same vectors (lane % G), then one
+    // shared atomic per (warp, vector) and one global atomic per (CTA, vector)
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      double m = pk[q];
+      for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      pk[q] = m;
+    }
+    if ((threadIdx.x & 31) < G) {
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        atomicMax(&s_peak[sub * V + q], (unsigned long long)__double_as_longlong(pk[q]));
+    }
     __syncthreads();
     if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
   }
+}
+
+#ifndef BAMG_U1
+#define BAMG_U1 4
+#endif
+#ifndef BAMG_G8
+#define BAMG_G8 4
+#endif
+#ifndef BAMG_U8
+#define BAMG_U8 4
+#endif
+
+static int rows_stage_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("BAMG_ROWS_STAGE");
+    mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  return mode;
 }
 
 template <int EPI>
 static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const bamg_csr* A, const double* X, double* Y,
                        const EpiArgs& ea) {
   switch (k) {
-#define BAMG_ROWS_CASE(KK, GG, UU)                                                                                  \
-  case KK: {                                                                                                        \
-    int g = (A->nrows + TILE_THREADS / GG - 1) / (TILE_THREADS / GG);                                               \
-    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU>), g, TILE_THREADS, 0, A->nrows, A->rowptr, \
-                    A->col, A->val, X, Y, ea);                                                                      \
-    return 0;                                                                                                       \
+#define BAMG_ROWS_CASE(KK, GG, UU)                                                                         \
+  case KK: {                                                                                               \
+    int g = (A->nrows + TILE_THREADS / GG - 1) / (TILE_THREADS / GG);                                      \
+    if (rows_stage_mode())                                                                                 \
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, true>), g, TILE_THREADS, 0,  \
+                      A->nrows, A->rowptr, A->col, A->val, X, Y, ea);                                      \
+    else                                                                                                   \
+      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, false>), g, TILE_THREADS, 0, \
+                      A->nrows, A->rowptr, A->col, A->val, X, Y, ea);                                      \
+    return 0;                                                                                              \
   }
-    BAMG_ROWS_CASE(1, 1, 4)
+    BAMG_ROWS_CASE(1, 1, BAMG_U1)
     BAMG_ROWS_CASE(2, 1, 4)
     BAMG_ROWS_CASE(4, 2, 4)
-    BAMG_ROWS_CASE(8, 4, 4)
+    BAMG_ROWS_CASE(8, BAMG_G8, BAMG_U8)
     BAMG_ROWS_CASE(12, 6, 4)
     BAMG_ROWS_CASE(16, 8, 4)
 #undef BAMG_ROWS_CASE

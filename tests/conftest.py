@@ -21,7 +21,7 @@ def pytest_configure(config):
 
 PIPE_CASES = ["pipe_cfg0_tandem64", "pipe_tandem32_k16_r30", "pipe_uniform33",
               "pipe_uniform63", "pipe_planar1024_k12", "pipe_bd257_normal",
-              "pipe_petri10_normal"]
+              "pipe_petri10_normal", "pipe2_tandem33_bamg2", "pipe2_uniform33_bamg2"]
 
 
 def load_golden(name):

@@ -237,6 +237,15 @@ def pipeline_cases():
     cases["pipe_uniform33"] = lambda: uniform(33)
     cases["pipe_uniform63"] = lambda: uniform(63)
 
+    def two_cycles(fam, side, k):
+        prob = chains.tandem_queue(side) if fam == "tandem" else chains.uniform_2d(side)
+        cfg = presets.default_setup_config(fam, cycles=2, seed=0, n_tests=k)
+        return prob, cfg, solver.GmresConfig(rtol=1e-8), 0
+
+    # BAMG^2: a second setup cycle with inhomogeneous smoothing on every level
+    cases["pipe2_tandem33_bamg2"] = lambda: two_cycles("tandem", 33, 8)
+    cases["pipe2_uniform33_bamg2"] = lambda: two_cycles("uniform2d", 33, 8)
+
     def planar(n, k=12):
         prob = chains.random_planar(n, seed=1)
         cfg = presets.default_setup_config("planar", cycles=1, seed=0, n_tests=k)
