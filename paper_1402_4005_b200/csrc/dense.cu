@@ -266,8 +266,12 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
                             double* V, double* sigma);
 int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out);
 
-static int large_threshold() {
-  int t = 512;
+// Size above which the blocked / subspace-iteration path replaces the
+// cooperative Jacobi SVD (triplets) and the one-kernel Gauss-Jordan (pinv):
+// measured crossovers on B200 (tools/dense_tune.py).  BAMG_DENSE_LARGE_N
+// overrides both.
+static int large_threshold(bool pinv) {
+  int t = pinv ? 1536 : 128;
   if (const char* e = getenv("BAMG_DENSE_LARGE_N")) t = atoi(e);
   return t;
 }
@@ -575,7 +579,7 @@ static int bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* Z) {
 extern "C" int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* Z) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1, "empty matrix");
-  if (n > large_threshold() && rank_tol <= 1e-12) {
+  if (n > large_threshold(true) && rank_tol <= 1e-12) {
     int rc = large_bordered_pinv(ctx, A, n, Z, 1, nullptr, nullptr);
     if (rc == 1) rc = large_full_rank_inverse(ctx, A, n, Z, 1);
     arena_trim(ctx);
@@ -944,7 +948,7 @@ extern "C" int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const dou
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1 && r >= 1 && r <= 64, "need 1 <= r <= 64");
   if (r > n) r = n;  // take = min(r, n)
-  if (n > large_threshold()) {
+  if (n > large_threshold(false)) {
     int rc = large_coarsest_triplets(ctx, Bd, const_cast<double*>(Md), const_cast<double*>(Nd), n, r, U, V, sigma);
     arena_trim(ctx);
     return rc;

@@ -113,54 +113,46 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 // Inverse of a triangular nb x nb block (ld) into Ti (nb x nb, ld nb), one
 // CTA: the block is staged in shared memory (dynamic, up to 128 KB), one thread
 // per column of the identity.  kind 0: unit lower, 1: lower, 2: upper.
-__global__ void tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind, double* __restrict__ Ti) {
-  extern __shared__ double sm[];
-  double* sT = sm;            // nb x nb block
-  double* sX = sm + nb * nb;  // nb x nb inverse, built row by row
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    int r = t % nb, c = t / nb;
-    sT[t] = T[(int64_t)c * ld + r];
+// One thread per column of the identity, the column held in registers (the
+// loops are fully unrolled for the block size NB, so every index is static);
+// the block itself is staged once in shared memory (broadcast reads).
+template <int NBT>
+__global__ void __launch_bounds__(NBT) tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind,
+                                                      double* __restrict__ Ti) {
+  __shared__ double sT[NBT * NBT];
+  for (int t = threadIdx.x; t < NBT * NBT; t += blockDim.x) {
+    int r = t % NBT, c = t / NBT;
+    sT[t] = (r < nb && c < nb) ? T[(int64_t)c * ld + r] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  // row-oriented substitution: step s fixes row i of X for all columns at once
-  const int c = threadIdx.x % nb;
-  const int lane_rows = blockDim.x / nb;  // threads sharing a column split the inner sum
-  const int part = threadIdx.x / nb;
-  for (int s = 0; s < nb; ++s) {
-    const int i = (kind == 2) ? nb - 1 - s : s;
-    double acc = 0.0;
-    if (kind == 2) {
-      for (int j = i + 1 + part; j < nb; j += lane_rows) acc += sT[j * nb + i] * sX[c * nb + j];
-    } else {
-      for (int j = part; j < i; j += lane_rows) acc += sT[j * nb + i] * sX[c * nb + j];
+  const int c = threadIdx.x;
+  double x[NBT];
+  if (kind == 2) {
+#pragma unroll
+    for (int i = NBT - 1; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = i + 1; j < NBT; ++j) s -= sT[j * NBT + i] * x[j];
+      x[i] = s / sT[i * NBT + i];
     }
-    // combine the partial sums of the threads sharing column c (warp shuffles
-    // would cross columns; use shared scratch after the X block)
-    double* red = sm + 2 * nb * nb;
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    if (part == 0) {
-      double tot = 0.0;
-      for (int q = 0; q < lane_rows; ++q) tot += red[q * nb + c];
-      double rhs = (i == c ? 1.0 : 0.0) - tot;
-      sX[c * nb + i] = (kind == 0) ? rhs : rhs / sT[i * nb + i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < NBT; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < i; ++j) s -= sT[j * NBT + i] * x[j];
+      x[i] = kind == 0 ? s : s / sT[i * NBT + i];
     }
-    __syncthreads();
   }
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) Ti[t] = sX[t];
+  if (c < nb) {
+#pragma unroll
+    for (int i = 0; i < NBT; ++i)
+      if (i < nb) Ti[(int64_t)c * nb + i] = x[i];
+  }
 }
 
 static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
-  static bool attr = false;
-  const int threads = 8 * NB;  // 8 threads per column
-  const int smem = (2 * NB * NB + threads) * (int)sizeof(double);
-  if (!attr) {
-    BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  // a partial last block (nb < NB) keeps 8 threads per column of ITS width
-  int th = 8 * nb;
-  BAMG_LAUNCH(ctx, tri_inv_kernel, 1, th, smem, T, ld, nb, kind, Ti);
+  BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 1, NB, 0, T, ld, nb, kind, Ti);
   return 0;
 }
 
@@ -660,32 +652,32 @@ __global__ void pseudo_random_kernel(double* X, int64_t total, unsigned seed) {
 // CholQR2-free orthonormalisation of n x p Y by two passes of Gram-Schmidt on
 // the Gram matrix: G = Y^T Y, R = chol(G), Y <- Y R^-1 (twice).
 __global__ void small_chol_inv_kernel(double* G, int p, double* Rinv) {
-  // one CTA: G (p x p, col-major) -> upper R with R^T R = G, then R^-1 (upper)
+  // one CTA: G (p x p, col-major, SPD) -> upper R with R^T R = G (right-looking,
+  // parallel trailing updates), then R^-1 one column per thread
   __shared__ double R[64 * 64];
-  int tid = threadIdx.x;
-  for (int t = tid; t < p * p; t += blockDim.x) R[t] = G[t];
+  const int tid = threadIdx.x;
+  for (int t = tid; t < p * p; t += blockDim.x) R[t] = G[t];  // R[col * p + row]
   __syncthreads();
-  if (tid == 0) {
-    for (int j = 0; j < p; ++j) {
-      double d = R[j * p + j];
-      for (int k = 0; k < j; ++k) d -= R[j * p + k] * R[j * p + k];  // R[k][j] stored at (col j, row k)
-      d = sqrt(fmax(d, 1e-300));
-      R[j * p + j] = d;
-      for (int i = j + 1; i < p; ++i) {
-        double v = R[i * p + j];
-        for (int k = 0; k < j; ++k) v -= R[j * p + k] * R[i * p + k];
-        R[i * p + j] = v / d;
-      }
-      for (int i = j + 1; i < p; ++i) R[j * p + i] = 0.0;  // lower part cleared
+  for (int j = 0; j < p; ++j) {
+    const double d = sqrt(fmax(R[j * p + j], 1e-300));
+    __syncthreads();
+    // row j of R (entries (j, t), t > j): R[t*p + j] /= d ; diagonal
+    for (int t = j + 1 + tid; t < p; t += blockDim.x) R[t * p + j] /= d;
+    if (tid == 0) R[j * p + j] = d;
+    __syncthreads();
+    // trailing update of the upper triangle: (i, t) with j < i <= t
+    const int m = p - j - 1;
+    for (int q = tid; q < m * m; q += blockDim.x) {
+      int i = j + 1 + q % m, t = j + 1 + q / m;
+      if (i <= t) R[t * p + i] -= R[i * p + j] * R[t * p + j];
     }
+    __syncthreads();
   }
-  __syncthreads();
-  // R is upper (entries R[k][j], k <= j at index j*p + k); invert column by column
   for (int c = tid; c < p; c += blockDim.x) {
     for (int i = p - 1; i >= 0; --i) {
       double s = (i == c) ? 1.0 : 0.0;
       for (int j = i + 1; j < p; ++j) s -= R[j * p + i] * Rinv[c * p + j];
-      Rinv[c * p + i] = s / R[i * p + i];
+      Rinv[c * p + i] = (i > c) ? 0.0 : s / R[i * p + i];
     }
   }
 }
@@ -693,7 +685,7 @@ __global__ void small_chol_inv_kernel(double* G, int p, double* Rinv) {
 static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp) {
   for (int pass = 0; pass < 2; ++pass) {
     BAMG_TRY(gemm(ctx, true, false, p, p, n, 1.0, Y, n, Y, n, 0.0, G, p));
-    BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 64, 0, G, p, Rinv);
+    BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 256, 0, G, p, Rinv);
     BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Rinv, p, 0.0, tmp, n));
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Y, tmp, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToDevice, ctx->stream));
   }
