@@ -85,29 +85,59 @@ def draws_for(k, n):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
+
+    Polls NVML in-process (pynvml; ctypes calls release the GIL) every 50 ms
+    -- forking nvidia-smi from a CUDA process stalls the host thread that
+    issues the step's launches.  Falls back to nvidia-smi when pynvml is
+    missing."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    BITS = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
 
     def __init__(self, index):
         self.index = index
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            try:
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS]
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        return [v.strip() for v in out.split(",")] if out else None
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
+                row = self._sample()
+                if row:
+                    self.rows.append(row)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -214,9 +244,12 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ev0.record(stream)
         iters = []
+        marks = []
         for _ in range(args.steps):
             setup, vop, rep = step()
             iters.append(rep.iterations)
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -229,6 +262,7 @@ def run_ours(args, rank, world, local_rank):
         fam_stats[fname] = (ms.value, cnt.value, by.value)
     L.bamg_prof_enable(c, 0)
     dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    step_ms = [ev0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
     if dist is not None:
         t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -305,6 +339,8 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3, 3),
         "higher_is_better": False, "scaling": "strong" if distributed else "weak", "vs_baseline": None,
         "dtype": "f64",
+        "step_ms": {"min": round(min(step_ms), 3), "median": round(float(np.median(step_ms)), 3),
+                    "max": round(max(step_ms), 3)},
         "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
         "config": {"workload": f"{name}: {desc}", "n": n, "nnz": int(dB.nnz), "k": k,
                    "gmres_restart": restart, "rtol": RTOL, "setup_cycles": cfg.setup_cycles,

@@ -170,8 +170,21 @@ def check(rc: int, what: str, c=None):
     return rc
 
 
+# BAMG_SLOWCALL_MS=<ms>: report engine calls whose host wall time exceeds
+# the threshold (development aid for host-side stalls)
+_SLOW_MS = float(_os.environ.get("BAMG_SLOWCALL_MS", "0") or 0)
+
+
 def call(name: str, *args):
     c = ctx()
+    if _SLOW_MS > 0:
+        import time
+        t0 = time.perf_counter()
+        rc = getattr(lib(), name)(c, *args)
+        dt = (time.perf_counter() - t0) * 1e3
+        if dt > _SLOW_MS:
+            print(f"[bamg slow call] {name} {dt:.1f} ms", flush=True)
+        return check(rc, name, c)
     rc = getattr(lib(), name)(c, *args)
     return check(rc, name, c)
 

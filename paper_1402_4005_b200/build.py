@@ -40,11 +40,11 @@ def _headers_mtime() -> float:
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = BUILD / (src.stem + ".o")
+def _compile(src: Path, verbose: bool, bdir: Path = BUILD, extra=()) -> Path:
+    obj = bdir / (src.stem + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, _headers_mtime()):
         return obj
-    cmd = [nvcc(), "-c", str(src), "-o", str(obj), "-I", str(INCLUDE)] + NVCC_FLAGS
+    cmd = [nvcc(), "-c", str(src), "-o", str(obj), "-I", str(INCLUDE)] + NVCC_FLAGS + list(extra)
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -53,28 +53,37 @@ def _compile(src: Path, verbose: bool) -> Path:
     return obj
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, force: bool = False, variant: str = "", defines=()) -> Path:
+    """Build the library; `variant`/`defines` build a tuning variant
+    (`_build_<variant>/`, `libbamg_sm100_<variant>.so`, extra -D flags) that
+    BAMG_LIB_PATH can select."""
+    bdir = BUILD if not variant else PKG / f"_build_{variant}"
+    lib = LIB if not variant else PKG / f"libbamg_sm100_{variant}.so"
+    extra = [f"-D{d}" for d in defines]
+    bdir.mkdir(exist_ok=True)
     if force:
-        for o in BUILD.glob("*.o"):
+        for o in bdir.glob("*.o"):
             o.unlink()
     sources = sorted(CSRC.glob("*.cu"))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources))
+        objs = list(ex.map(lambda s: _compile(s, verbose, bdir, extra), sources))
     newest = max(o.stat().st_mtime for o in objs)
-    if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+    if lib.exists() and lib.stat().st_mtime >= newest and not force:
+        return lib
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
         "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}", flush=True)
-    return LIB
+        print(f"built {lib}", flush=True)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    args = sys.argv[1:]
+    var = next((a.split("=", 1)[1] for a in args if a.startswith("--variant=")), "")
+    defs = [a.split("=", 1)[1] for a in args if a.startswith("-D=")]
+    build(verbose=True, force="--force" in args, variant=var, defines=defs)

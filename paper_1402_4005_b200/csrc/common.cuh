@@ -97,6 +97,13 @@ struct bamg_ctx {
   size_t pinned_doubles = 0;
   KProf prof;
   KTrace trace;
+  // V-cycle graph plumbing recycled across hierarchies (one hierarchy per
+  // setup; a solve loop builds one per step): the capture stream, the level
+  // buffers and the instantiated graphs (re-pointed by cudaGraphExecUpdate),
+  // so steady-state steps make no cudaMalloc/cudaFree/instantiate calls.
+  cudaStream_t cap_stream = nullptr;
+  std::vector<std::pair<char*, size_t>> buf_pool;
+  std::vector<cudaGraphExec_t> exec_pool;
 };
 
 static inline void trace_mark(bamg_ctx* ctx, const char* name) {

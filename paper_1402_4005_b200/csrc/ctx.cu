@@ -28,6 +28,9 @@ extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->arena.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto& b : ctx->buf_pool) cudaFree(b.first);
+  for (auto e : ctx->exec_pool) cudaGraphExecDestroy(e);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return 0;
 }

@@ -546,6 +546,9 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
 constexpr int TMAXC = 16;  // candidates per point on the thread path
 constexpr int TKMAX = 32;
 constexpr int TCAL = 4;    // calibers up to 4 on the thread path
+#ifndef BAMG_FIT_RECIP
+#define BAMG_FIT_RECIP 1
+#endif
 
 struct TModel {
   int pos[TCAL];
@@ -567,8 +570,9 @@ struct TPoint {
   int f[EXACT ? 1 : KM];         // their indices (generic mode)
   double y[KM];                  // fine values
   double sw[KM];                 // sqrt weights (0 for masked tests)
-  int cand[TMAXC];
   double lam;
+  __device__ __forceinline__ double yv(int t) const { return y[t]; }
+  __device__ __forceinline__ double swv(int t) const { return sw[t]; }
   __device__ __forceinline__ int ntest() const { return EXACT ? KM : nf; }
   __device__ __forceinline__ int stride() const { return EXACT ? KM : k; }
   __device__ __forceinline__ int test(int t) const {
@@ -582,35 +586,38 @@ template <int KM>
 __device__ __forceinline__ double tcol(const TPoint<KM>& P, int t, int col, int base) {
   double c = __ldg(P.X + (int64_t)col * P.stride() + P.test(t));
   if (base >= 0) c -= __ldg(P.X + (int64_t)base * P.stride() + P.test(t));
-  return P.sw[t] * c;
+  return P.swv(t) * c;
 }
 
 template <int KM>
 __device__ __forceinline__ double ttarget(const TPoint<KM>& P, int t, int base) {
-  double yv = P.y[t];
+  double yv = P.yv(t);
   if (base >= 0) yv -= __ldg(P.X + (int64_t)base * P.stride() + P.test(t));
-  return P.sw[t] * yv;
+  return P.swv(t) * yv;
 }
 
-// ridge LS on `nc` columns (point indices cols[]); returns false when the
-// Cholesky factor fails the rank test (caller defers the point).
-template <int KM>
-__device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base, double* coef, double* data,
-                          double* total) {
-  double G[TCAL][TCAL], h[TCAL];
+// ridge LS on NC columns (point indices cols[]); returns false when the
+// Cholesky factor fails the rank test (caller defers the point).  NC is a
+// compile-time constant so no guarded (issued but idle) lanes of the 4x4
+// Gram / Cholesky / triangular loops execute for small trial models.
+template <int KM, int NC>
+__device__ __forceinline__ bool tls_solve_n(const TPoint<KM>& P, const int* cols, int base, double* coef,
+                                            double* data, double* total) {
+  constexpr int nc = NC;
+  double G[NC][NC], h[NC];
 #pragma unroll
-  for (int p = 0; p < TCAL; ++p) {
+  for (int p = 0; p < NC; ++p) {
     h[p] = 0.0;
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q) G[p][q] = 0.0;
+    for (int q = 0; q < NC; ++q) G[p][q] = 0.0;
   }
   _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-    double a[TCAL];
+    double a[NC];
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
+    for (int q = 0; q < NC; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
     double b = ttarget(P, t, base);
 #pragma unroll
-    for (int p = 0; p < TCAL; ++p) {
+    for (int p = 0; p < NC; ++p) {
       h[p] += a[p] * b;
 #pragma unroll
       for (int q = 0; q <= p; ++q) G[p][q] += a[p] * a[q];
@@ -618,93 +625,102 @@ __device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base
   }
   const double l2 = P.lam * P.lam;
   // Cholesky G + lam^2 I = R^T R (lower L = R^T stored in G's lower triangle)
-  double L[TCAL][TCAL];
+  double L[NC][NC];
+#if BAMG_FIT_RECIP
+  double rinv[NC];  // reciprocal pivots: one division per column
+#define BAMG_PIVDIV(v, j) ((v) * rinv[j])
+#else
+#define BAMG_PIVDIV(v, j) ((v) / L[j][j])
+#endif
   double rmax = 0.0, dmin = INFINITY;
 #pragma unroll
-  for (int j = 0; j < TCAL; ++j) {
+  for (int j = 0; j < NC; ++j) {
     if (j >= nc) break;
     double d = G[j][j] + l2;
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q)
+    for (int q = 0; q < NC; ++q)
       if (q < j) d -= L[j][q] * L[j][q];
     if (!(d > 0.0)) return false;
     double ljj = sqrt(d);
     L[j][j] = ljj;
+#if BAMG_FIT_RECIP
+    rinv[j] = 1.0 / ljj;
+#endif
     dmin = fmin(dmin, ljj);
     rmax = fmax(rmax, ljj);
 #pragma unroll
-    for (int i = 0; i < TCAL; ++i) {
+    for (int i = 0; i < NC; ++i) {
       if (i > j && i < nc) {
         double v = G[i][j];
 #pragma unroll
-        for (int q = 0; q < TCAL; ++q)
+        for (int q = 0; q < NC; ++q)
           if (q < j) v -= L[i][q] * L[j][q];
-        L[i][j] = v / ljj;
+        L[i][j] = BAMG_PIVDIV(v, j);
         rmax = fmax(rmax, fabs(L[i][j]));
       }
     }
   }
   if (rmax == 0.0 || dmin < 1e-13 * rmax) return false;  // qr_solve_ls would take pinv
   auto chol_solve = [&](const double* rhs, double* x) {
-    double z[TCAL];
+    double z[NC];
 #pragma unroll
-    for (int i = 0; i < TCAL; ++i) {
+    for (int i = 0; i < NC; ++i) {
       if (i < nc) {
         double v = rhs[i];
 #pragma unroll
-        for (int q = 0; q < TCAL; ++q)
+        for (int q = 0; q < NC; ++q)
           if (q < i) v -= L[i][q] * z[q];
-        z[i] = v / L[i][i];
+        z[i] = BAMG_PIVDIV(v, i);
       }
     }
 #pragma unroll
-    for (int i = TCAL - 1; i >= 0; --i) {
+    for (int i = NC - 1; i >= 0; --i) {
       if (i < nc) {
         double v = z[i];
 #pragma unroll
-        for (int q = 0; q < TCAL; ++q)
+        for (int q = 0; q < NC; ++q)
           if (q > i && q < nc) v -= L[q][i] * x[q];
-        x[i] = v / L[i][i];
+        x[i] = BAMG_PIVDIV(v, i);
       }
     }
   };
-  double c[TCAL];
+  double c[NC];
 #pragma unroll
-  for (int q = 0; q < TCAL; ++q) c[q] = 0.0;
+  for (int q = 0; q < NC; ++q) c[q] = 0.0;
   chol_solve(h, c);
   for (int refine = 0; refine < 2; ++refine) {
-    double g[TCAL];
+    double g[NC];
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q) g[q] = q < nc ? -l2 * c[q] : 0.0;  // ridge rows: -lam * (lam c)
+    for (int q = 0; q < NC; ++q) g[q] = q < nc ? -l2 * c[q] : 0.0;  // ridge rows: -lam * (lam c)
     _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-      double a[TCAL];
+      double a[NC];
       double r = ttarget(P, t, base);
 #pragma unroll
-      for (int q = 0; q < TCAL; ++q) {
+      for (int q = 0; q < NC; ++q) {
         a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
         r -= a[q] * c[q];
       }
 #pragma unroll
-      for (int q = 0; q < TCAL; ++q) g[q] += a[q] * r;
+      for (int q = 0; q < NC; ++q) g[q] += a[q] * r;
     }
-    double dlt[TCAL];
+    double dlt[NC];
     chol_solve(g, dlt);
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q)
+    for (int q = 0; q < NC; ++q)
       if (q < nc) c[q] += dlt[q];
   }
   double mis = 0.0;
   _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
     double r = 0.0;
 #pragma unroll
-    for (int q = 0; q < TCAL; ++q)
+    for (int q = 0; q < NC; ++q)
       if (q < nc) r += tcol(P, t, cols[q], base) * c[q];
     r -= ttarget(P, t, base);
     mis += r * r;
   }
   double cc = 0.0;
 #pragma unroll
-  for (int q = 0; q < TCAL; ++q)
+  for (int q = 0; q < NC; ++q)
     if (q < nc) {
       coef[q] = c[q];
       cc += c[q] * c[q];
@@ -712,6 +728,19 @@ __device__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base
   *data = mis;
   *total = mis + l2 * cc;
   return true;
+}
+#undef BAMG_PIVDIV
+
+template <int KM>
+__device__ __forceinline__ bool tls_solve(const TPoint<KM>& P, const int* cols, int nc, int base, double* coef,
+                                          double* data, double* total) {
+  static_assert(TCAL == 4, "tls_solve dispatch covers calibers 1..4");
+  switch (nc) {
+    case 1: return tls_solve_n<KM, 1>(P, cols, base, coef, data, total);
+    case 2: return tls_solve_n<KM, 2>(P, cols, base, coef, data, total);
+    case 3: return tls_solve_n<KM, 3>(P, cols, base, coef, data, total);
+    default: return tls_solve_n<KM, 4>(P, cols, base, coef, data, total);
+  }
 }
 
 // solve_model (interp.py:176-199) on the thread path; false = defer point
@@ -726,12 +755,12 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
     double coef[TCAL];
     double data, total;
     if (constrain) {
-      int base = P.cand[work[0]];
+      int base = work[0];
       if (wl > 1) {
         int cols[TCAL];
         double ct[TCAL];
 #pragma unroll
-        for (int q = 0; q < TCAL; ++q) cols[q] = (q + 1 < wl) ? P.cand[work[q + 1]] : 0;
+        for (int q = 0; q < TCAL; ++q) cols[q] = (q + 1 < wl) ? work[q + 1] : 0;
         if (!tls_solve(P, cols, wl - 1, base, ct, &data, &total)) return false;
         double ssum = 0.0;
 #pragma unroll
@@ -752,7 +781,7 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
     } else {
       int cols[TCAL];
 #pragma unroll
-      for (int q = 0; q < TCAL; ++q) cols[q] = q < wl ? P.cand[work[q]] : 0;
+      for (int q = 0; q < TCAL; ++q) cols[q] = q < wl ? work[q] : 0;
       if (!tls_solve(P, cols, wl, -1, coef, &data, &total)) return false;
     }
     bool has_nan = false;
@@ -826,72 +855,152 @@ __global__ void fit_prepare_kernel(int n, const int32_t* __restrict__ crank, int
   }
 }
 
-#ifndef BAMG_FIT_MINBLOCKS
-#define BAMG_FIT_MINBLOCKS 3
-#endif
-template <int KM>
-__global__ void __launch_bounds__(128, BAMG_FIT_MINBLOCKS)
-fit_rows_thread_kernel(const int32_t* __restrict__ list, const unsigned int* __restrict__ nlist,
-                       const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                       const int32_t* __restrict__ crank, const double* __restrict__ X, int k,
-                       const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber, int radius,
-                       double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
-                       int32_t* __restrict__ out_col, double* __restrict__ out_val, int32_t* __restrict__ defer,
-                       unsigned int* __restrict__ ndefer) {
+// Candidate pass of the thread path: coarse radius-1 neighbours (adjacency
+// rows are sorted), escalating to the sorted unique radius-2 union when there
+// are none (interp.py:241-249, 274-276).  Writes the list to cbuf[t][TMAXC]
+// and counts the points per candidate count, so the fit kernel can run warps
+// of equal-sized problems (the greedy loop's trip counts follow m).  Points
+// with no candidates get an empty row here; overflowing ones go to the warp
+// path.
+__global__ void __launch_bounds__(256)
+fit_cands_kernel(const int32_t* __restrict__ list, const unsigned int* __restrict__ nlist,
+                 const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                 const int32_t* __restrict__ crank, int radius, int32_t* __restrict__ mcnt,
+                 int32_t* __restrict__ cbuf, unsigned int* __restrict__ hist, int32_t* __restrict__ out_cnt,
+                 int32_t* __restrict__ defer, unsigned int* __restrict__ ndefer) {
+  __shared__ unsigned int sh[TMAXC + 1];
+  if (threadIdx.x <= TMAXC) sh[threadIdx.x] = 0;
+  __syncthreads();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int)*nlist) return;
-  const int i = list[t];
+  if (t < (int)*nlist) {
+    const int i = list[t];
+    int32_t* cand = cbuf + (int64_t)t * TMAXC;
+    int m = 0;
+    bool ok = true;
+    const int rb = arp[i], re = arp[i + 1];
+    if (radius == 1) {
+      for (int j = rb; j < re; ++j) {
+        int p = acol[j];
+        if (crank[p] >= 0) {
+          if (m < TMAXC) cand[m] = p;
+          ++m;
+        }
+      }
+      if (m > TMAXC) ok = false;
+    }
+    if (ok && m == 0 && re > rb) {
+      int len = 0;
+      for (int j = rb; j < re && ok; ++j) {
+        int nb = acol[j];
+        for (int side = 0; side < 2 && ok; ++side) {
+          int qb = side == 0 ? j : arp[nb];
+          int qe = side == 0 ? j + 1 : arp[nb + 1];
+          for (int q = qb; q < qe; ++q) {
+            int x = acol[q];
+            if (x == i || crank[x] < 0) continue;
+            int pos = 0;
+            while (pos < len && cand[pos] < x) ++pos;
+            if (pos < len && cand[pos] == x) continue;
+            if (len >= TMAXC) {
+              ok = false;
+              break;
+            }
+            for (int u = len; u > pos; --u) cand[u] = cand[u - 1];
+            cand[pos] = x;
+            ++len;
+          }
+        }
+      }
+      m = len;
+    }
+    if (!ok) {
+      defer[atomicAdd(ndefer, 1u)] = i;
+      mcnt[t] = -1;
+    } else if (m == 0) {
+      out_cnt[i] = 0;
+      mcnt[t] = -1;
+    } else {
+      mcnt[t] = m;
+      atomicAdd(&sh[m], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x <= TMAXC && sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+// exclusive scan of the candidate-count histogram -> bucket cursors
+__global__ void fit_bucket_scan_kernel(unsigned int* __restrict__ hist, unsigned int* __restrict__ nsorted) {
+  if (threadIdx.x != 0) return;
+  unsigned int acc = 0;
+  for (int b = 0; b <= TMAXC; ++b) {
+    unsigned int c = hist[b];
+    hist[b] = acc;
+    acc += c;
+  }
+  *nsorted = acc;
+}
+
+// bucket the points by candidate count (order inside a bucket is immaterial:
+// every point's row is computed independently)
+__global__ void __launch_bounds__(256)
+fit_bucket_scatter_kernel(const int32_t* __restrict__ mcnt, const unsigned int* __restrict__ nlist,
+                          unsigned int* __restrict__ cursor, int32_t* __restrict__ order) {
+  __shared__ unsigned int sh[TMAXC + 1], base[TMAXC + 1];
+  if (threadIdx.x <= TMAXC) sh[threadIdx.x] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = t < (int)*nlist ? mcnt[t] : -1;
+  unsigned int r = m > 0 ? atomicAdd(&sh[m], 1u) : 0u;
+  __syncthreads();
+  if (threadIdx.x <= TMAXC) base[threadIdx.x] = sh[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], sh[threadIdx.x]) : 0u;
+  __syncthreads();
+  if (m > 0) order[base[m] + r] = t;
+}
+
+#ifndef BAMG_FIT_MINBLOCKS
+#define BAMG_FIT_MINBLOCKS 2
+#endif
+constexpr int TFIT_THREADS = 128;
+
+// Greedy selection of one fine point per thread over its m candidates.  The
+// candidate list sits in shared memory (one column per thread); the selection
+// and the trial models carry candidate point ids, so no per-thread array is
+// indexed dynamically.
+template <int KM>
+__global__ void __launch_bounds__(TFIT_THREADS, BAMG_FIT_MINBLOCKS)
+fit_rows_thread_kernel(const int32_t* __restrict__ order, const unsigned int* __restrict__ nsorted,
+                       const int32_t* __restrict__ list, const int32_t* __restrict__ mcnt,
+                       const int32_t* __restrict__ cbuf, const int32_t* __restrict__ crank,
+                       const double* __restrict__ X, int k, const double* __restrict__ w,
+                       const double* __restrict__ lam_dev, int caliber, double tol, int constrain, int nonneg,
+                       int32_t* __restrict__ out_cnt, int32_t* __restrict__ out_col, double* __restrict__ out_val,
+                       int32_t* __restrict__ defer, unsigned int* __restrict__ ndefer) {
+  __shared__ int s_cand[TMAXC][TFIT_THREADS];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int)*nsorted) return;
+  const int s = order[t];
+  const int i = list[s];
+  const int m = mcnt[s];
   const int64_t obase = (int64_t)i * caliber;
+  {
+    const int4* src = reinterpret_cast<const int4*>(cbuf + (int64_t)s * TMAXC);
+#pragma unroll
+    for (int v = 0; v < TMAXC / 4; ++v) {
+      if (4 * v < m) {
+        int4 c4 = src[v];
+        s_cand[4 * v][threadIdx.x] = c4.x;
+        s_cand[4 * v + 1][threadIdx.x] = c4.y;
+        s_cand[4 * v + 2][threadIdx.x] = c4.z;
+        s_cand[4 * v + 3][threadIdx.x] = c4.w;
+      }
+    }
+  }
   TPoint<KM> P;
   P.X = X;
   P.k = k;
   P.lam = lam_dev[0];
-  bool ok = P.lam > 0.0;
-  // candidates: coarse radius-1 neighbours (adjacency rows are sorted)
-  int m = 0;
-  const int rb = arp[i], re = arp[i + 1];
-  if (radius == 1) {
-    for (int j = rb; j < re; ++j) {
-      int p = acol[j];
-      if (crank[p] >= 0) {
-        if (m < TMAXC) P.cand[m] = p;
-        ++m;
-      }
-    }
-  }
-  if (m == 0 && re > rb) {
-    // radius 2: sorted unique union of the neighbour rows, coarse points != i
-    int len = 0;
-    for (int j = rb; j < re && ok; ++j) {
-      int nb = acol[j];
-      for (int side = 0; side < 2 && ok; ++side) {
-        int qb = side == 0 ? j : arp[nb];
-        int qe = side == 0 ? j + 1 : arp[nb + 1];
-        for (int q = qb; q < qe; ++q) {
-          int x = acol[q];
-          if (x == i || crank[x] < 0) continue;
-          int pos = 0;
-          while (pos < len && P.cand[pos] < x) ++pos;
-          if (pos < len && P.cand[pos] == x) continue;
-          if (len >= TMAXC) {
-            ok = false;
-            break;
-          }
-          for (int t = len; t > pos; --t) P.cand[t] = P.cand[t - 1];
-          P.cand[pos] = x;
-          ++len;
-        }
-      }
-    }
-    m = len;
-  }
-  if (m > TMAXC) ok = false;
-  if (!ok || k > KM || caliber > TCAL) {
+  if (!(P.lam > 0.0)) {
     defer[atomicAdd(ndefer, 1u)] = i;
-    return;
-  }
-  if (m == 0) {
-    out_cnt[i] = 0;
     return;
   }
   double empty = 0.0;
@@ -935,14 +1044,15 @@ fit_rows_thread_kernel(const int32_t* __restrict__ list, const unsigned int* __r
     TModel best;
     bool have = false;
     for (int j = 0; j < m; ++j) {
+      const int cj = s_cand[j][threadIdx.x];
       bool in = false;
 #pragma unroll
       for (int q = 0; q < TCAL; ++q)
-        if (q < nsel && sel[q] == j) in = true;
+        if (q < nsel && sel[q] == cj) in = true;
       if (in) continue;
       int trial[TCAL];
 #pragma unroll
-      for (int q = 0; q < TCAL; ++q) trial[q] = q < nsel ? sel[q] : (q == nsel ? j : 0);
+      for (int q = 0; q < TCAL; ++q) trial[q] = q < nsel ? sel[q] : (q == nsel ? cj : 0);
       TModel md;
       if (!tsolve_model(P, trial, nsel + 1, constrain != 0, nonneg != 0, empty, &md)) {
         defer[atomicAdd(ndefer, 1u)] = i;
@@ -977,15 +1087,17 @@ fit_rows_thread_kernel(const int32_t* __restrict__ list, const unsigned int* __r
     if (cur_total <= 1e-30) break;
   }
   if (nsel == 0) {
-    sel[0] = 0;
+    sel[0] = s_cand[0][threadIdx.x];
     coefs[0] = constrain ? 1.0 : 0.0;
     nsel = 1;
   }
   out_cnt[i] = nsel;
-  for (int q = 0; q < nsel; ++q) {
-    out_col[obase + q] = crank[P.cand[sel[q]]];
-    out_val[obase + q] = coefs[q];
-  }
+#pragma unroll
+  for (int q = 0; q < TCAL; ++q)
+    if (q < nsel) {
+      out_col[obase + q] = crank[sel[q]];
+      out_val[obase + q] = coefs[q];
+    }
 }
 
 // ridge = 0.1 * sqrt(mean_i (sqrt(sum_f w_f x_if^2))^2)  (interp.py:266-268)
@@ -1070,17 +1182,30 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
     BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nfl, 0, sizeof(unsigned int), ctx->stream));
     BAMG_LAUNCH(ctx, fit_prepare_kernel, grid_for(n, 256), 256, 0, (int)n, coarse_rank, caliber, out_cnt, out_col,
                 out_val, flist, nfl);
+    int32_t *mcnt, *cbuf, *order;
+    unsigned int *hist, *nsorted;
+    BAMG_TRY(arena_get(ctx, (size_t)n + 1, &mcnt));
+    BAMG_TRY(arena_get(ctx, (size_t)n * TMAXC + 4, &cbuf));
+    BAMG_TRY(arena_get(ctx, (size_t)n + 1, &order));
+    BAMG_TRY(arena_get(ctx, TMAXC + 2, &hist));
+    nsorted = hist + TMAXC + 1;
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(hist, 0, (TMAXC + 2) * sizeof(unsigned int), ctx->stream));
+    BAMG_LAUNCH(ctx, fit_cands_kernel, grid_for(n, 256), 256, 0, flist, nfl, adj->rowptr, adj->col, coarse_rank,
+                radius, mcnt, cbuf, hist, out_cnt, defer, ndefer);
+    BAMG_LAUNCH(ctx, fit_bucket_scan_kernel, 1, 32, 0, hist, nsorted);
+    BAMG_LAUNCH(ctx, fit_bucket_scatter_kernel, grid_for(n, 256), 256, 0, mcnt, nfl, hist, order);
 #define BAMG_FIT_EXACT(KK)                                                                                       \
   if (k == KK) {                                                                                                   \
-    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<KK>, grid_for(n, 128), 128, 0, flist, nfl,        \
-                    adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, \
-                    nonnegative, out_cnt, out_col, out_val, defer, ndefer);                                        \
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<KK>, grid_for(n, TFIT_THREADS), TFIT_THREADS, 0,  \
+                    order, nsorted, flist, mcnt, cbuf, coarse_rank, X, k, w, lam, caliber, improvement_tol,        \
+                    constrain, nonnegative, out_cnt, out_col, out_val, defer, ndefer);                             \
   } else
     BAMG_FIT_EXACT(8) BAMG_FIT_EXACT(10) BAMG_FIT_EXACT(12) BAMG_FIT_EXACT(16) {
-      BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<TKMAX>, grid_for(n, 128), 128, 0, flist, nfl,
-                      adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
-                      nonnegative, out_cnt, out_col, out_val, defer, ndefer);
+      BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<TKMAX>, grid_for(n, TFIT_THREADS), TFIT_THREADS,
+                      0, order, nsorted, flist, mcnt, cbuf, coarse_rank, X, k, w, lam, caliber, improvement_tol,
+                      constrain, nonnegative, out_cnt, out_col, out_val, defer, ndefer);
     }
+#undef BAMG_FIT_EXACT
     int32_t nd = 0;
     BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(ndefer), 1, &nd));
     nlist = nd;

@@ -49,15 +49,48 @@ struct bamg_hier {
   int nz = 0;
   double omega = 0.7;
   int nu1 = 3, nu2 = 3;
-  std::vector<void*> owned;
+  std::vector<std::pair<char*, size_t>> owned;  // level buffers (from / back to ctx->buf_pool)
   bool ready = false;
   std::vector<VGraph> graphs;
-  cudaStream_t cap_stream = nullptr;
 };
 
+constexpr size_t EXEC_POOL_MAX = 16;
+constexpr size_t BUF_POOL_MAX = 8;
+
+// graphs go back to the context pool (a later hierarchy re-points them)
 static void hier_drop_graphs(bamg_hier* h) {
-  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+  bamg_ctx* ctx = h->ctx;
+  for (auto& g : h->graphs) {
+    if (ctx->exec_pool.size() < EXEC_POOL_MAX) ctx->exec_pool.push_back(g.exec);
+    else cudaGraphExecDestroy(g.exec);
+  }
   h->graphs.clear();
+}
+
+// smallest pooled buffer of at least `bytes`, else a fresh allocation
+static int pool_take(bamg_ctx* ctx, size_t bytes, char** out) {
+  int best = -1;
+  for (int i = 0; i < (int)ctx->buf_pool.size(); ++i)
+    if (ctx->buf_pool[i].second >= bytes && (best < 0 || ctx->buf_pool[i].second < ctx->buf_pool[best].second))
+      best = i;
+  if (best >= 0) {
+    *out = ctx->buf_pool[best].first;
+    ctx->buf_pool.erase(ctx->buf_pool.begin() + best);
+    return 0;
+  }
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(out, bytes));
+  return 0;
+}
+
+static void pool_give(bamg_ctx* ctx, char* p, size_t bytes) {
+  ctx->buf_pool.push_back({p, bytes});
+  while (ctx->buf_pool.size() > BUF_POOL_MAX) {  // drop the smallest
+    int s = 0;
+    for (int i = 1; i < (int)ctx->buf_pool.size(); ++i)
+      if (ctx->buf_pool[i].second < ctx->buf_pool[s].second) s = i;
+    cudaFree(ctx->buf_pool[s].first);
+    ctx->buf_pool.erase(ctx->buf_pool.begin() + s);
+  }
 }
 
 extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
@@ -71,10 +104,11 @@ extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
 
 extern "C" int bamg_hier_destroy(bamg_hier* h) {
   if (!h) return 0;
+  // in-flight replays of this hierarchy's graphs must finish before their
+  // executables and buffers are handed to the next hierarchy
   cudaStreamSynchronize(h->ctx->stream);
   hier_drop_graphs(h);
-  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
-  for (void* p : h->owned) cudaFree(p);
+  for (auto& b : h->owned) pool_give(h->ctx, b.first, b.second);
   delete h;
   return 0;
 }
@@ -115,18 +149,29 @@ static int hier_prepare(bamg_hier* h) {
   bamg_ctx* ctx = h->ctx;
   int L = (int)h->lv.size();
   BAMG_REQUIRE(ctx, h->Z && h->nz == h->lv[L - 1].n, "coarsest pseudo-inverse missing or wrong size");
+  size_t total = 0;
   for (int l = 0; l < L; ++l) {
     HLevel& v = h->lv[l];
     BAMG_REQUIRE(ctx, v.B.rowptr != nullptr, "level operator missing");
     if (l + 1 < L) BAMG_REQUIRE(ctx, v.P.rowptr && v.Q.rowptr, "transfer operators missing");
-    size_t n = (size_t)v.n;
-    double* buf = nullptr;
-    BAMG_CHECK_CUDA(ctx, cudaMalloc(&buf, sizeof(double) * 4 * (n > 0 ? n : 1)));
-    h->owned.push_back(buf);
+    total += (size_t)4 * (v.n > 0 ? v.n : 1) + 32;  // 256-byte aligned level slices
+  }
+  if (h->owned.empty() || h->owned[0].second < total * sizeof(double)) {
+    for (auto& b : h->owned) pool_give(ctx, b.first, b.second);
+    h->owned.clear();
+    char* p = nullptr;
+    BAMG_TRY(pool_take(ctx, total * sizeof(double), &p));
+    h->owned.push_back({p, total * sizeof(double)});
+  }
+  double* buf = reinterpret_cast<double*>(h->owned[0].first);
+  for (int l = 0; l < L; ++l) {
+    HLevel& v = h->lv[l];
+    size_t n = (size_t)(v.n > 0 ? v.n : 1);
     v.x = buf;
     v.x2 = buf + n;
     v.b = buf + 2 * n;
     v.r = buf + 3 * n;
+    buf += ((4 * n + 31) / 32) * 32;
   }
   h->ready = true;
   return 0;
@@ -231,16 +276,17 @@ static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
     if (e.b == b && e.x == x) g = &e;
   if (!g) {
     if (h->graphs.size() >= 8) hier_drop_graphs(h);
-    if (!h->cap_stream) BAMG_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    if (!ctx->cap_stream) BAMG_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t cap = ctx->cap_stream;
     cudaStream_t saved = ctx->stream;
     int64_t l0 = ctx->launches;
     unsigned saved_mask = ctx->prof.mask;  // no profiler events inside the graph
     ctx->prof.mask = 0;
-    ctx->stream = h->cap_stream;
+    ctx->stream = cap;
     cudaGraph_t graph;
-    cudaError_t e1 = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+    cudaError_t e1 = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     int rc = e1 == cudaSuccess ? vcycle_impl(ctx, h, b, x) : -1;
-    cudaError_t e2 = cudaStreamEndCapture(h->cap_stream, &graph);
+    cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     ctx->stream = saved;
     ctx->prof.mask = saved_mask;
     int nk = (int)(ctx->launches - l0);
@@ -249,8 +295,21 @@ static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
       ctx->err = std::string("V-cycle graph capture failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
       return rc != 0 ? rc : -1;
     }
-    cudaGraphExec_t exec;
-    BAMG_CHECK_CUDA(ctx, cudaGraphInstantiate(&exec, graph, 0));
+    // re-point a pooled executable of the same topology (a V-cycle of another
+    // hierarchy with the same level count); instantiate only when none fits
+    cudaGraphExec_t exec = nullptr;
+    while (!exec && !ctx->exec_pool.empty()) {
+      cudaGraphExec_t cand = ctx->exec_pool.back();
+      ctx->exec_pool.pop_back();
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(cand, graph, &info) == cudaSuccess) {
+        exec = cand;
+      } else {
+        (void)cudaGetLastError();  // clear the non-sticky update failure
+        cudaGraphExecDestroy(cand);
+      }
+    }
+    if (!exec) BAMG_CHECK_CUDA(ctx, cudaGraphInstantiate(&exec, graph, 0));
     cudaGraphDestroy(graph);
     h->graphs.push_back({b, x, exec, nk});
     g = &h->graphs.back();
