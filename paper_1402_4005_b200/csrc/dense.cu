@@ -226,6 +226,73 @@ jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double
   }
 }
 
+// Single-CTA one-sided Jacobi for matrices that fit in shared memory (G and
+// V staged together): one warp per column pair of a tournament round, warp
+// shuffles for the three dot products, __syncthreads between rounds -- no grid
+// barriers.  Same rotation formula and threshold as the cooperative kernel.
+constexpr int JAC_SMEM_MAX = 200 * 1024;
+__global__ void __launch_bounds__(1024)
+jacobi_svd_smem_kernel(double* G, int nrows, double* V, int ncols, int m, double tol, int maxsweeps) {
+  extern __shared__ double sm[];
+  double* sG = sm;
+  double* sV = sm + (size_t)nrows * ncols;
+  __shared__ int rotated;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = threadIdx.x; t < nrows * ncols; t += blockDim.x) sG[t] = G[t];
+  for (int t = threadIdx.x; t < ncols * ncols; t += blockDim.x) sV[t] = (t / ncols == t % ncols) ? 1.0 : 0.0;
+  for (int sw = 0; sw < maxsweeps; ++sw) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int s = 0; s < m - 1; ++s) {
+      for (int pair = wid; pair < m / 2; pair += nw) {
+        int p, q;
+        tournament_pair(m, s, pair, &p, &q);
+        if (p >= ncols || q >= ncols) continue;
+        if (p > q) {
+          int t = p;
+          p = q;
+          q = t;
+        }
+        double* gp = sG + (size_t)p * nrows;
+        double* gq = sG + (size_t)q * nrows;
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int r = lane; r < nrows; r += 32) {
+          double x = gp[r], y = gq[r];
+          a += x * x;
+          b += y * y;
+          c += x * y;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        c = warp_sum(c);
+        if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) continue;
+        double zeta = (b - a) / (2.0 * c);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int r = lane; r < nrows; r += 32) {
+          double x = gp[r], y = gq[r];
+          gp[r] = cs * x - sn * y;
+          gq[r] = sn * x + cs * y;
+        }
+        double* vp = sV + (size_t)p * ncols;
+        double* vq = sV + (size_t)q * ncols;
+        for (int r = lane; r < ncols; r += 32) {
+          double x = vp[r], y = vq[r];
+          vp[r] = cs * x - sn * y;
+          vq[r] = sn * x + cs * y;
+        }
+        if (lane == 0) rotated = 1;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nrows * ncols; t += blockDim.x) G[t] = sG[t];
+  for (int t = threadIdx.x; t < ncols * ncols; t += blockDim.x) V[t] = sV[t];
+}
+
 // G (nrows x ncols, column-major) -> G V = U S; V (ncols x ncols); sig
 static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig) {
   constexpr int MAXSW = 60;
@@ -234,7 +301,18 @@ static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(flags, 0, sizeof(int) * MAXSW, ctx->stream));
   BAMG_LAUNCH(ctx, eye_kernel, grid_for((int64_t)ncols * ncols, 256), 256, 0, V, ncols);
   int m = ncols + (ncols & 1);
-  if (ncols >= 2) {
+  const size_t smem = sizeof(double) * ((size_t)nrows * ncols + (size_t)ncols * ncols);
+  if (ncols >= 2 && smem <= (size_t)JAC_SMEM_MAX && !getenv("BAMG_JACOBI_COOP")) {
+    static bool attr = false;
+    if (!attr) {
+      BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(jacobi_svd_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                JAC_SMEM_MAX));
+      attr = true;
+    }
+    double tol = 1e-15;
+    if (const char* e = getenv("BAMG_JACOBI_TOL")) tol = atof(e);
+    BAMG_LAUNCH(ctx, jacobi_svd_smem_kernel, 1, 1024, smem, G, nrows, V, ncols, m, tol, MAXSW);
+  } else if (ncols >= 2) {
     int grid = coop_grid(ctx, jacobi_svd_coop_kernel, JAC_THREADS, m / 2);
     double tol = 1e-15;
     if (const char* e = getenv("BAMG_JACOBI_TOL")) tol = atof(e);
@@ -271,7 +349,7 @@ int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, in
 // measured crossovers on B200 (tools/dense_tune.py).  BAMG_DENSE_LARGE_N
 // overrides both.
 static int large_threshold(bool pinv) {
-  int t = pinv ? 1536 : 128;
+  int t = pinv ? 200 : 128;
   if (const char* e = getenv("BAMG_DENSE_LARGE_N")) t = atoi(e);
   return t;
 }

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -111,48 +112,73 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 }
 
 // Inverse of a triangular nb x nb block (ld) into Ti (nb x nb, ld nb), one
-// CTA: the block is staged in shared memory (dynamic, up to 128 KB), one thread
-// per column of the identity.  kind 0: unit lower, 1: lower, 2: upper.
-// One thread per column of the identity, the column held in registers (the
-// loops are fully unrolled for the block size NB, so every index is static);
-// the block itself is staged once in shared memory (broadcast reads).
+// CTA.  kind 0: unit lower, 1: lower, 2: upper.  The block is staged once in
+// shared memory (broadcast reads) with its reciprocal diagonal; four threads
+// share one column of the identity: thread q of the group owns the solution
+// entries j = q (mod 4) in registers (static indices: the loops are unrolled
+// for the block size NBT), forms the partial sums over its entries, and the
+// group combines them with two shuffles per row.
 template <int NBT>
-__global__ void __launch_bounds__(NBT) tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind,
-                                                      double* __restrict__ Ti) {
+__global__ void __launch_bounds__(4 * NBT) tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind,
+                                                          double* __restrict__ Ti) {
   __shared__ double sT[NBT * NBT];
+  __shared__ double rdg[NBT];
   for (int t = threadIdx.x; t < NBT * NBT; t += blockDim.x) {
     int r = t % NBT, c = t / NBT;
     sT[t] = (r < nb && c < nb) ? T[(int64_t)c * ld + r] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  const int c = threadIdx.x;
-  double x[NBT];
+  for (int i = threadIdx.x; i < NBT; i += blockDim.x) rdg[i] = kind == 0 ? 1.0 : 1.0 / sT[i * NBT + i];
+  __syncthreads();
+  const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+  constexpr int NQ = NBT / 4;
+  double xs[NQ];
+#pragma unroll
+  for (int u = 0; u < NQ; ++u) xs[u] = 0.0;
   if (kind == 2) {
 #pragma unroll
     for (int i = NBT - 1; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
+      double part = 0.0;
 #pragma unroll
-      for (int j = i + 1; j < NBT; ++j) s -= sT[j * NBT + i] * x[j];
-      x[i] = s / sT[i * NBT + i];
+      for (int u = 0; u < NQ; ++u) {
+        if (4 * u + 3 > i) {  // some j = 4u + q may exceed i
+          int j = 4 * u + q;
+          if (j > i) part += sT[j * NBT + i] * xs[u];
+        }
+      }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      double xi = ((i == c) ? 1.0 - part : -part) * rdg[i];
+      if ((i & 3) == q) xs[i >> 2] = xi;
     }
   } else {
 #pragma unroll
     for (int i = 0; i < NBT; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
+      double part = 0.0;
 #pragma unroll
-      for (int j = 0; j < i; ++j) s -= sT[j * NBT + i] * x[j];
-      x[i] = kind == 0 ? s : s / sT[i * NBT + i];
+      for (int u = 0; u < NQ; ++u) {
+        if (4 * u < i) {
+          int j = 4 * u + q;
+          if (j < i) part += sT[j * NBT + i] * xs[u];
+        }
+      }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      double xi = ((i == c) ? 1.0 - part : -part) * rdg[i];
+      if ((i & 3) == q) xs[i >> 2] = xi;
     }
   }
   if (c < nb) {
 #pragma unroll
-    for (int i = 0; i < NBT; ++i)
-      if (i < nb) Ti[(int64_t)c * nb + i] = x[i];
+    for (int u = 0; u < NQ; ++u) {
+      int i = 4 * u + q;
+      if (i < nb) Ti[(int64_t)c * nb + i] = xs[u];
+    }
   }
 }
 
 static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
-  BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 1, NB, 0, T, ld, nb, kind, Ti);
+  BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 1, 4 * NB, 0, T, ld, nb, kind, Ti);
   return 0;
 }
 
@@ -339,6 +365,90 @@ __global__ void __launch_bounds__(256) panel_lu_kernel(double* A, int n, int j0,
   }
 }
 
+// Single-CTA panel factorisation with the whole panel A[j0:n, j0:j0+jb]
+// staged in shared memory (column-major, ld = n - j0): the per-column pivot
+// search, swap, scaling and rank-1 update cost __syncthreads instead of grid
+// barriers.  Same pivot rule as panel_lu_kernel (max |a|, first index on ties).
+constexpr int PANEL_SMEM_MAX = 200 * 1024;
+__global__ void __launch_bounds__(1024) panel_lu_smem_kernel(double* A, int n, int j0, int jb, int* piv, int* bad) {
+  extern __shared__ double sP[];
+  __shared__ double wb[32];
+  __shared__ int wi[32];
+  __shared__ int s_p;
+  const int rows = n - j0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int t = tid; t < rows * jb; t += blockDim.x) {
+    int c = t / rows, r = t - c * rows;
+    sP[t] = A[(int64_t)(j0 + c) * n + j0 + r];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < jb; ++jj) {
+    double* col = sP + (int64_t)jj * rows;
+    double best = -1.0;
+    int bi = jj;
+    for (int r = jj + tid; r < rows; r += blockDim.x) {
+      double a = fabs(col[r]);
+      if (a > best) {
+        best = a;
+        bi = r;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      wb[wid] = best;
+      wi[wid] = bi;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      best = lane < nw ? wb[lane] : -1.0;
+      bi = lane < nw ? wi[lane] : rows;
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        piv[j0 + jj] = j0 + bi;
+        if (!(best > 0.0)) *bad = 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != jj)
+      for (int c = tid; c < jb; c += blockDim.x) {
+        double a = sP[(int64_t)c * rows + jj];
+        sP[(int64_t)c * rows + jj] = sP[(int64_t)c * rows + p];
+        sP[(int64_t)c * rows + p] = a;
+      }
+    __syncthreads();
+    const double d = col[jj];
+    const double dd = d != 0.0 ? d : 1.0;
+    for (int r = jj + 1 + tid; r < rows; r += blockDim.x) col[r] = col[r] / dd;
+    __syncthreads();
+    const int mr = rows - jj - 1, mc = jb - jj - 1;
+    for (int t = tid; t < mr * mc; t += blockDim.x) {
+      int c = jj + 1 + t / mr, r = jj + 1 + t % mr;
+      sP[(int64_t)c * rows + r] -= col[r] * sP[(int64_t)c * rows + jj];
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < rows * jb; t += blockDim.x) {
+    int c = t / rows, r = t - c * rows;
+    A[(int64_t)(j0 + c) * n + j0 + r] = sP[t];
+  }
+}
+
 // apply the panel's row interchanges to columns outside [j0, j0+jb)
 __global__ void apply_swaps_kernel(double* A, int n, int j0, int jb, const int* piv) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,14 +475,25 @@ static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, doubl
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_lu_kernel, 256, 0);
   int pgrid = per_sm * ctx->num_sms;
   if (pgrid > 2048) pgrid = 2048;
+  static bool smem_attr = false;
+  if (!smem_attr) {
+    BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(panel_lu_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              PANEL_SMEM_MAX));
+    smem_attr = true;
+  }
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
-    int want = (n - j0 + 255) / 256;
-    int g = want < pgrid ? (want < 1 ? 1 : want) : pgrid;
-    void* args[] = {&A, &n, &j0, &jb, &piv, &pmax, &pidx, &bad};
-    BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(g), dim3(256), args, 0,
-                                                     ctx->stream));
-    ctx->launches++;
+    const size_t panel_bytes = (size_t)(n - j0) * jb * sizeof(double);
+    if (panel_bytes <= (size_t)PANEL_SMEM_MAX) {
+      BAMG_LAUNCH(ctx, panel_lu_smem_kernel, 1, 1024, panel_bytes, A, n, j0, jb, piv, bad);
+    } else {
+      int want = (n - j0 + 255) / 256;
+      int g = want < pgrid ? (want < 1 ? 1 : want) : pgrid;
+      void* args[] = {&A, &n, &j0, &jb, &piv, &pmax, &pidx, &bad};
+      BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(g), dim3(256), args, 0,
+                                                       ctx->stream));
+      ctx->launches++;
+    }
     BAMG_LAUNCH(ctx, apply_swaps_kernel, grid_for(n, 256), 256, 0, A, n, j0, jb, piv);
     int r0 = j0 + jb, rn = n - r0;
     if (rn <= 0) break;
@@ -649,23 +770,26 @@ __global__ void pseudo_random_kernel(double* X, int64_t total, unsigned seed) {
   X[t] = (double)(h & 0xffffff) / 16777216.0 - 0.5;
 }
 
-// CholQR2-free orthonormalisation of n x p Y by two passes of Gram-Schmidt on
-// the Gram matrix: G = Y^T Y, R = chol(G), Y <- Y R^-1 (twice).
-__global__ void small_chol_inv_kernel(double* G, int p, double* Rinv) {
-  // one CTA: G (p x p, col-major, SPD) -> upper R with R^T R = G (right-looking,
-  // parallel trailing updates), then R^-1 one column per thread
-  __shared__ double R[64 * 64];
+constexpr int SMALLP = 48;  // subspace block size limit (p = r + 12, r <= 31)
+
+// One CTA: G (p x p, col-major, SPD, p <= SMALLP) -> upper R with R^T R = G
+// (right-looking, parallel trailing updates in shared memory), then R^-1 one
+// column per thread, also in shared memory (no global read-after-write), and
+// the diagonal of R into rdiag (the subspace iteration's Ritz estimates).
+__global__ void __launch_bounds__(256) small_chol_inv_kernel(const double* __restrict__ G, int p,
+                                                             double* __restrict__ Rinv, double* __restrict__ rdiag) {
+  __shared__ double R[SMALLP * SMALLP];
+  __shared__ double X[SMALLP * SMALLP];
   const int tid = threadIdx.x;
   for (int t = tid; t < p * p; t += blockDim.x) R[t] = G[t];  // R[col * p + row]
   __syncthreads();
   for (int j = 0; j < p; ++j) {
     const double d = sqrt(fmax(R[j * p + j], 1e-300));
+    const double di = 1.0 / d;
     __syncthreads();
-    // row j of R (entries (j, t), t > j): R[t*p + j] /= d ; diagonal
-    for (int t = j + 1 + tid; t < p; t += blockDim.x) R[t * p + j] /= d;
+    for (int t = j + 1 + tid; t < p; t += blockDim.x) R[t * p + j] *= di;
     if (tid == 0) R[j * p + j] = d;
     __syncthreads();
-    // trailing update of the upper triangle: (i, t) with j < i <= t
     const int m = p - j - 1;
     for (int q = tid; q < m * m; q += blockDim.x) {
       int i = j + 1 + q % m, t = j + 1 + q / m;
@@ -676,16 +800,90 @@ __global__ void small_chol_inv_kernel(double* G, int p, double* Rinv) {
   for (int c = tid; c < p; c += blockDim.x) {
     for (int i = p - 1; i >= 0; --i) {
       double s = (i == c) ? 1.0 : 0.0;
-      for (int j = i + 1; j < p; ++j) s -= R[j * p + i] * Rinv[c * p + j];
-      Rinv[c * p + i] = (i > c) ? 0.0 : s / R[i * p + i];
+      for (int j = i + 1; j <= c; ++j) s -= R[j * p + i] * X[c * p + j];
+      X[c * p + i] = (i > c) ? 0.0 : s / R[i * p + i];
     }
+  }
+  __syncthreads();
+  for (int t = tid; t < p * p; t += blockDim.x) Rinv[t] = X[t];
+  if (rdiag)
+    for (int t = tid; t < p; t += blockDim.x) rdiag[t] = R[t * p + t];
+}
+
+// Fused CholQR step for p in {16, 20, 24, 28, 32}: every CTA factors the p x p Gram matrix
+// G = L L^T in one warp (lane i holds row i in registers, the column of L
+// being eliminated is broadcast by shuffles), publishes L and 1/diag(L) in
+// shared memory, then each thread replaces one row y of Y by x with
+// x L^T = y (forward substitution) -- i.e. Y <- Y R^-1 with R = L^T, in place,
+// without forming R^-1.
+template <int P>
+__global__ void __launch_bounds__(256) cholqr_apply_kernel(const double* __restrict__ G, double* Y, int n) {
+  static_assert(P <= 32, "one Gram row per lane");
+  __shared__ double sA[P * (P + 1)];  // row-major, padded: lane i owns row i
+  __shared__ double sRd[P];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane < P)
+      for (int j = 0; j < P; ++j) sA[lane * (P + 1) + j] = G[(int64_t)j * P + lane];
+    __syncwarp();
+    double* row = sA + lane * (P + 1);
+#pragma unroll 1
+    for (int j = 0; j < P; ++j) {
+      const double djj = fmax(sA[j * (P + 1) + j], 1e-300);  // as small_chol_inv_kernel
+      const double ljj = sqrt(djj), inv = 1.0 / ljj;
+      __syncwarp();
+      double lij = 0.0;
+      if (lane > j && lane < P) {
+        lij = row[j] * inv;
+        row[j] = lij;
+      } else if (lane == j) {
+        row[j] = ljj;
+        sRd[j] = inv;
+      }
+      __syncwarp();
+      if (lane > j && lane < P)
+        for (int t = j + 1; t <= lane; ++t) row[t] -= lij * sA[t * (P + 1) + j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // one row per thread and no row loop: a loop would let the compiler hoist
+  // all P^2/2 shared-memory reads of L into registers (and spill them)
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) {
+    double x[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) x[i] = Y[(int64_t)i * n + r];
+    // column-oriented forward substitution: x_j final, then eliminate below
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      x[j] *= sRd[j];
+#pragma unroll
+      for (int i = j + 1; i < P; ++i) x[i] -= sA[i * (P + 1) + j] * x[j];
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) Y[(int64_t)i * n + r] = x[i];
   }
 }
 
-static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp) {
+// CholQR2 orthonormalisation of n x p Y: G = Y^T Y, R = chol(G), Y <- Y R^-1,
+// twice.  rdiag (optional, 2p) receives both passes' R diagonals (p > 32 path).
+static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp,
+                          double* rdiag = nullptr) {
+  BAMG_REQUIRE(ctx, p <= SMALLP, "subspace block wider than the small Cholesky kernel");
   for (int pass = 0; pass < 2; ++pass) {
     BAMG_TRY(gemm(ctx, true, false, p, p, n, 1.0, Y, n, Y, n, 0.0, G, p));
-    BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 256, 0, G, p, Rinv);
+    if (!rdiag && (p == 20 || p == 24 || p == 28 || p == 32 || p == 16)) {
+      switch (p) {  // p = r + 12 for the usual test-vector counts r = 4, 8, 12, 16, 20
+        case 16: BAMG_LAUNCH(ctx, cholqr_apply_kernel<16>, grid_for(n, 256), 256, 0, G, Y, n); break;
+        case 20: BAMG_LAUNCH(ctx, cholqr_apply_kernel<20>, grid_for(n, 256), 256, 0, G, Y, n); break;
+        case 24: BAMG_LAUNCH(ctx, cholqr_apply_kernel<24>, grid_for(n, 256), 256, 0, G, Y, n); break;
+        case 28: BAMG_LAUNCH(ctx, cholqr_apply_kernel<28>, grid_for(n, 256), 256, 0, G, Y, n); break;
+        default: BAMG_LAUNCH(ctx, cholqr_apply_kernel<32>, grid_for(n, 256), 256, 0, G, Y, n); break;
+      }
+      continue;
+    }
+    BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 256, 0, G, p, Rinv, rdiag ? rdiag + pass * p : nullptr);
     BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Rinv, p, 0.0, tmp, n));
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Y, tmp, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToDevice, ctx->stream));
   }
@@ -755,6 +953,18 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   // symmetrised masses (bootstrap.py:217-218), Cholesky in place
   BAMG_LAUNCH(ctx, symmetrize_inplace_kernel, grid_for((int64_t)nn, 256), 256, 0, Md, n);
   BAMG_LAUNCH(ctx, symmetrize_inplace_kernel, grid_for((int64_t)nn, 256), 256, 0, Nd, n);
+  // BAMG_DENSE_TIMING=1: synchronised wall time per stage (development aid)
+  const bool timing = getenv("BAMG_DENSE_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* name) {
+    if (!timing) return;
+    cudaStreamSynchronize(ctx->stream);
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bamg dense] n=%d %-10s %8.3f ms\n", n, name,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  stage("start");
   BAMG_TRY(cholesky_blocked(ctx, Md, n, bad, work));
   BAMG_TRY(cholesky_blocked(ctx, Nd, n, bad, work));
   int hb = 0;
@@ -763,6 +973,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     ctx->err = "mass matrix is not positive definite (Cholesky pivot <= 0)";
     return 2;
   }
+  stage("cholesky");
   // K = L_M^-1 B L_N^-T :  T = L_M^-1 B ; K^T = L_N^-1 T^T
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(K, Bd, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
   BAMG_TRY(tri_solve(ctx, Md, n, true, false, false, K, n, n, work));
@@ -772,6 +983,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   // K^+ (column-major into Kp) and the exact null triplet (K b0 = 0, a0^T K = 0);
   // a nonsingular K (chains whose coarse column sums drifted) takes K^-1 and
   // all r slots from the subspace iteration
+  stage("K");
   int rc = large_bordered_pinv(ctx, K, n, Kp, 0, b0, a0);
   if (rc < 0) return rc;
   const bool null_slot = rc == 0;
@@ -783,29 +995,74 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
       return -2;
     }
   }
+  stage("pinv");
   // block subspace iteration on K^+ : Z = orth(K^+^T Y), Y = orth(K^+ Z)
   BAMG_LAUNCH(ctx, pseudo_random_kernel, grid_for((int64_t)n * p, 256), 256, 0, Y, (int64_t)n * p, 12345u);
   BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+  // convergence: every 5 iterations, the Ritz values of K^+ on the current
+  // subspace (one-CTA Jacobi SVD of the n x p block when it fits in shared
+  // memory) must agree with the previous check to 1e-14 relative.  The first
+  // 5-iteration block runs eagerly; the block is then captured once as a CUDA
+  // graph (cuBLAS GEMMs included) and replayed, so the host launches one graph
+  // per check instead of ~70 kernels.
+  auto block5 = [&]() -> int {
+    for (int it = 0; it < 5; ++it) {
+      BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+      BAMG_TRY(orthonormalize(ctx, Z, n, p, Gs, Ri, tmp));
+      BAMG_TRY(gemm(ctx, false, false, n, p, n, 1.0, Kp, n, Z, n, 0.0, Y, n));
+      BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+    }
+    BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+    return jacobi_svd_public(ctx, Z, n, p, Vs, sv);
+  };
   std::vector<double> prev(p, 0.0), cur(p, 0.0);
   int iters = 0;
-  for (int it = 0; it < 500; ++it) {
-    BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
-    BAMG_TRY(orthonormalize(ctx, Z, n, p, Gs, Ri, tmp));
-    BAMG_TRY(gemm(ctx, false, false, n, p, n, 1.0, Kp, n, Z, n, 0.0, Y, n));
-    BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
-    iters = it + 1;
-    if ((it + 1) % 5 == 0) {
-      BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
-      BAMG_TRY(jacobi_svd_public(ctx, Z, n, p, Vs, sv));
-      BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
-      std::vector<double> c2 = cur;
-      std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
-      double change = 0.0;
-      for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
-      prev = c2;
-      if (change < 1e-14) break;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t gk = 0;
+  const bool use_graph = !ctx->trace.on && !getenv("BAMG_NO_GRAPHS") && !getenv("BAMG_DEBUG");
+  for (int blk = 0; blk < 100; ++blk) {
+    if (blk == 0 || !use_graph) {
+      BAMG_TRY(block5());
+    } else {
+      if (!gexec) {
+        if (!ctx->cap_stream) BAMG_CHECK_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t saved = ctx->stream;
+        unsigned saved_mask = ctx->prof.mask;
+        int64_t l0 = ctx->launches;
+        ctx->prof.mask = 0;
+        ctx->stream = ctx->cap_stream;
+        cudaGraph_t graph;
+        cudaError_t e1 = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+        int rc = e1 == cudaSuccess ? block5() : -1;
+        cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &graph);
+        ctx->stream = saved;
+        ctx->prof.mask = saved_mask;
+        gk = ctx->launches - l0;
+        ctx->launches = l0;
+        if (e1 != cudaSuccess || e2 != cudaSuccess || rc != 0) {
+          ctx->err = std::string("subspace iteration graph capture failed: ") +
+                     cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
+          return rc != 0 ? rc : -1;
+        }
+        cudaError_t e3 = cudaGraphInstantiate(&gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        BAMG_CHECK_CUDA(ctx, e3);
+      }
+      BAMG_CHECK_CUDA(ctx, cudaGraphLaunch(gexec, ctx->stream));
+      ctx->launches += gk;
     }
+    iters += 5;
+    BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
+    std::vector<double> c2 = cur;
+    std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
+    double change = 0.0;
+    for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
+    prev = c2;
+    if (change < 1e-14) break;
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (timing) fprintf(stderr, "[bamg dense] n=%d p=%d subspace iterations %d\n", n, p, iters);
+  stage("subspace");
   // Rayleigh-Ritz: G = K^+^T Y, Jacobi: G Vs = W diag(s); K's left vectors
   // are W's columns, right vectors Y Vs
   BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
@@ -835,6 +1092,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
   BAMG_REQUIRE(ctx, ntiny <= 1, "large coarsest operator has more than one numerically-null triplet");
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+  stage("ritz");
   // unit a, b  ->  u = L_M^-T a, v = L_N^-T b are M- / N-normalised
   BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, A, n);
   BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, Bv, n);
@@ -845,6 +1103,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   BAMG_TRY(tri_solve(ctx, Nd, n, true, false, true, Bv, n, r, work));
   BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
+  stage("finish");
   if (getenv("BAMG_DEBUG"))
     fprintf(stderr, "[bamg] large triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p, iters,
             r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);

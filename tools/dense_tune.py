@@ -4,7 +4,8 @@ sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_1402_4005_b200 import engine, chains
 from paper_1402_4005_b200.device import DeviceCSR
-for side in (16, 32):
+sides = [int(a) for a in sys.argv[1:]] or [16, 32]
+for side in sides:
     prob = chains.tandem_queue(side, validate=False)
     B = DeviceCSR.from_host(prob.B)
     D = engine.csr_to_dense(B)
