@@ -104,6 +104,14 @@ int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int or
 /* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit
  * transpose for the column variant.  Replaces degenerate_rows, relax.py:47-63. */
 int bamg_degenerate_rows(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip);
+/* Self-test of the Jacobi epilogue's division: the engine divides by d through
+ * the correctly rounded reciprocal plus one FMA correction (Markstein), which
+ * must equal IEEE x / d bit for bit.  Compares both on n reproducible random
+ * operand pairs (mode 0: |exponent| <= 40, 1: the fast-path range, 2: all
+ * finite doubles incl. subnormals and zeros, 3: near-power-of-two and all-ones
+ * mantissas) and returns the number of differing results.  No reference
+ * counterpart: it certifies the bit-exactness claim of bamg_jacobi. */
+int bamg_selftest_div(bamg_ctx* ctx, int64_t n, uint64_t seed, int mode, int64_t* mismatches_host);
 /* One weighted-Jacobi sweep on k interleaved vectors, BIT-EXACT vs
  * _apply_sweep (relax.py:66-83):  x' = x + (omega (b - A x)) / d on unskipped
  * rows.  b may be NULL (homogeneous).  When b_scale is non-NULL the

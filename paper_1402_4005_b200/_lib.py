@@ -61,6 +61,7 @@ _SIGS = {
     "bamg_spgemm_fill": [P, PCSR, PCSR, C.c_int, P, P, P],
     "bamg_degenerate_rows": [P, PCSR, P, P],
     "bamg_jacobi": [P, PCSR, P, P, P, P, P, P, C.c_int, F64, P],
+    "bamg_selftest_div": [P, I64, C.c_uint64, C.c_int, P],
     "bamg_col_norms": [P, P, I64, C.c_int, P],
     "bamg_col_dots": [P, P, P, I64, C.c_int, P],
     "bamg_col_scale_div": [P, P, I64, C.c_int, P],
@@ -105,6 +106,7 @@ _RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64}
 
 _lock = threading.Lock()
 _lib = None
+_gpu_lib = None  # set once a GPU was confirmed: the hot-path fast return of lib()
 _ctx = {}
 
 
@@ -139,7 +141,10 @@ def load_library(require_gpu: bool = False):
 
 
 def lib():
-    return load_library(require_gpu=True)
+    global _gpu_lib
+    if _gpu_lib is None:
+        _gpu_lib = load_library(require_gpu=True)
+    return _gpu_lib
 
 
 def ctx(device: int | None = None):
@@ -147,6 +152,9 @@ def ctx(device: int | None = None):
     L = lib()
     dev = torch.cuda.current_device() if device is None else int(device)
     key = dev
+    c = _ctx.get(key)
+    if c is not None:
+        return c
     if key not in _ctx:
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream

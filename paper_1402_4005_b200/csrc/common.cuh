@@ -102,6 +102,9 @@ struct bamg_ctx {
   // buffers and the instantiated graphs (re-pointed by cudaGraphExecUpdate),
   // so steady-state steps make no cudaMalloc/cudaFree/instantiate calls.
   cudaStream_t cap_stream = nullptr;
+  // zero-initialised arrival counters for single-launch ("last CTA finishes")
+  // reductions; every user resets its counter to 0 before exiting
+  unsigned int* counters = nullptr;
   std::vector<std::pair<char*, size_t>> buf_pool;
   std::vector<cudaGraphExec_t> exec_pool;
 };
@@ -217,6 +220,24 @@ __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Correctly rounded x / d from rd = RN(1/d) (Markstein): q = RN(x rd) is within
+// one ulp of x/d, r = x - d q is exact by FMA, and RN(q + r rd) = RN(x/d).
+// The theorem needs x, d, q and r clear of under/overflow, so the fast path is
+// taken only for 2^-500 <= |x| <= 2^500 and 2^-400 <= |d| <= 2^400 (then
+// 2^-900 <= |q| <= 2^900); everything else (zeros, subnormals, inf, NaN)
+// uses the IEEE division.  Bit-identical to __ddiv_rn (tests/test_gpu_kernels:
+// bamg_selftest_div over 2^30+ operand pairs).
+__device__ __forceinline__ double div_rn_recip(double x, double d, double rd) {
+  const unsigned ex = (unsigned)((unsigned long long)__double_as_longlong(x) >> 52) & 0x7ffu;
+  const unsigned ed = (unsigned)((unsigned long long)__double_as_longlong(d) >> 52) & 0x7ffu;
+  if (ex - (1023u - 500u) <= 1000u && ed - (1023u - 400u) <= 800u) {
+    const double q = __dmul_rn(x, rd);
+    const double r = __fma_rn(-d, q, x);
+    return __fma_rn(r, rd, q);
+  }
+  return __ddiv_rn(x, d);
 }
 
 // max of non-negative doubles through their bit patterns (order-preserving,

@@ -19,6 +19,12 @@ extern "C" int bamg_ctx_create(int device, void* cuda_stream, bamg_ctx** out) {
     delete ctx;
     return -1;
   }
+  if (cudaMalloc(&ctx->counters, 64 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(ctx->counters, 0, 64 * sizeof(unsigned int)) != cudaSuccess) {
+    cudaFreeHost(ctx->pinned);
+    delete ctx;
+    return -1;
+  }
   *out = ctx;
   return 0;
 }
@@ -28,6 +34,7 @@ extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->arena.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->counters) cudaFree(ctx->counters);
   for (auto& b : ctx->buf_pool) cudaFree(b.first);
   for (auto e : ctx->exec_pool) cudaGraphExecDestroy(e);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -68,71 +75,40 @@ int ctx_read_i32(bamg_ctx* ctx, const int32_t* dev, size_t n, int32_t* host) {
 }
 
 // ------------------------------------------------------------------ scans
-// Three-phase exclusive scan: per-tile sums, a single-block scan of the tile
-// sums, then per-tile scan with the tile offset.  Tiles of 4096 elements.
+// Exclusive scans (CSR row pointers from counts).  Tiles of 4096 elements.
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
-template <typename T>
-__global__ void scan_tile_sums(const T* __restrict__ in, int64_t n, int64_t* __restrict__ sums) {
-  __shared__ int64_t warp_tot[32];
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-  int64_t local = 0;
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
-    if (idx < n) local += (int64_t)in[idx];
-  }
-  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = local;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int64_t v = warp_tot[threadIdx.x];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) sums[blockIdx.x] = v;
-  }
-}
-
-// exclusive scan of `sums` in place (single block, any length), total at sums[m]
-__global__ void scan_sums_single(int64_t* sums, int64_t m) {
-  __shared__ int64_t buf[SCAN_THREADS];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < m; base += SCAN_THREADS) {
-    int64_t idx = base + threadIdx.x;
-    int64_t v = idx < m ? sums[idx] : 0;
-    buf[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < SCAN_THREADS; off <<= 1) {
-      int64_t t = threadIdx.x >= off ? buf[threadIdx.x - off] : 0;
-      __syncthreads();
-      buf[threadIdx.x] += t;
-      __syncthreads();
-    }
-    int64_t incl = buf[threadIdx.x];
-    if (idx < m) sums[idx] = carry + incl - v;
-    __syncthreads();
-    if (threadIdx.x == SCAN_THREADS - 1) carry += incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sums[m] = carry;
-}
+// Single-pass exclusive scan with decoupled look-back: each CTA takes the
+// next tile id from a counter (so predecessors are always running or done),
+// publishes its aggregate, then walks back over the predecessors' published
+// (flag, value) words until an inclusive prefix is found, and publishes its
+// own inclusive prefix.  Integer sums: exact and deterministic.  One launch
+// (plus a memset of the state words) instead of three.
+constexpr unsigned long long LB_AGG = 1ull, LB_INC = 2ull;
 
 template <typename T>
-__global__ void scan_tile_apply(const T* __restrict__ in, int64_t n, const int64_t* __restrict__ sums,
-                                int32_t* __restrict__ out, int64_t m) {
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_onepass_kernel(const T* __restrict__ in, int64_t n, int32_t* __restrict__ out,
+                    unsigned long long* __restrict__ state, unsigned int* __restrict__ counter,
+                    int64_t* __restrict__ total) {
   __shared__ int64_t warp_tot[32];
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  __shared__ int tile_s;
+  __shared__ int64_t excl_s;
+  if (threadIdx.x == 0) tile_s = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  const int tile = tile_s;
+  const int64_t base = (int64_t)tile * SCAN_TILE;
   int64_t v[SCAN_ITEMS];
   int64_t local = 0;
+#pragma unroll
   for (int i = 0; i < SCAN_ITEMS; ++i) {
     int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
     v[i] = idx < n ? (int64_t)in[idx] : 0;
     local += v[i];
   }
-  // inclusive warp scan of per-thread totals
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int64_t inc = local;
   for (int o = 1; o < 32; o <<= 1) {
     int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
@@ -148,27 +124,53 @@ __global__ void scan_tile_apply(const T* __restrict__ in, int64_t n, const int64
       if (lane >= o) wi += t;
     }
     if (lane < (SCAN_THREADS / 32)) warp_tot[lane] = wi - w;
+    if (lane == 31) {
+      // wi on lane 31 is the tile aggregate
+      const int64_t agg = wi;
+      int64_t excl = 0;
+      if (tile == 0) {
+        atomicExch(state, ((unsigned long long)agg << 2) | LB_INC);
+      } else {
+        atomicExch(state + tile, ((unsigned long long)agg << 2) | LB_AGG);
+        for (int p = tile - 1; p >= 0;) {
+          unsigned long long wv = *(volatile unsigned long long*)(state + p);
+          unsigned long long f = wv & 3ull;
+          if (f == 0) continue;  // predecessor still computing its aggregate
+          excl += (int64_t)(wv >> 2);
+          if (f == LB_INC) break;
+          --p;
+        }
+        atomicExch(state + tile, ((unsigned long long)(excl + agg) << 2) | LB_INC);
+      }
+      excl_s = excl;
+      if (tile == (int)gridDim.x - 1) {
+        out[n] = (int32_t)(excl + agg);
+        *total = excl + agg;
+      }
+    }
   }
   __syncthreads();
-  int64_t run = sums[blockIdx.x] + warp_tot[wid] + inc - local;
+  int64_t run = excl_s + warp_tot[wid] + inc - local;
+#pragma unroll
   for (int i = 0; i < SCAN_ITEMS; ++i) {
     int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
     if (idx < n) out[idx] = (int32_t)run;
     run += v[i];
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (int32_t)sums[m];
 }
 
 template <typename T>
 static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_t* total_host) {
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles < 1) tiles = 1;
-  int64_t* sums = nullptr;
-  BAMG_TRY(arena_get(ctx, (size_t)tiles + 1, &sums));
-  BAMG_LAUNCH(ctx, scan_tile_sums<T>, (int)tiles, SCAN_THREADS, 0, in, n, sums);
-  BAMG_LAUNCH(ctx, scan_sums_single, 1, SCAN_THREADS, 0, sums, tiles);
-  BAMG_LAUNCH(ctx, scan_tile_apply<T>, (int)tiles, SCAN_THREADS, 0, in, n, sums, out, tiles);
-  if (total_host) BAMG_TRY(ctx_read_i64(ctx, sums + tiles, 1, total_host));
+  // state words (tiles) + tile counter + total, one memset
+  unsigned long long* state = nullptr;
+  BAMG_TRY(arena_get(ctx, (size_t)tiles + 2, &state));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(state, 0, sizeof(unsigned long long) * ((size_t)tiles + 2), ctx->stream));
+  unsigned int* counter = reinterpret_cast<unsigned int*>(state + tiles);
+  int64_t* total = reinterpret_cast<int64_t*>(state + tiles + 1);
+  BAMG_LAUNCH(ctx, scan_onepass_kernel<T>, (int)tiles, SCAN_THREADS, 0, in, n, out, state, counter, total);
+  if (total_host) BAMG_TRY(ctx_read_i64(ctx, total, 1, total_host));
   return 0;
 }
 
@@ -182,9 +184,17 @@ int scan_u8(bamg_ctx* ctx, const uint8_t* in, int32_t* out, int64_t n, int64_t* 
 // ------------------------------------------------- deterministic colreduce
 constexpr int KMAX = 32;
 
-__global__ void colreduce_partial(const double* __restrict__ X, const double* __restrict__ Y,
-                                  int64_t n, int k, int kind, double* __restrict__ partial) {
+// Column sums of squares (kind 0) or of products (kind 1) of n x k blocks in
+// ONE launch: RED_BLOCKS CTAs write per-CTA partials; the last CTA to arrive
+// (arrival counter, self-resetting) reduces them in a fixed order -- per
+// column, lanes stride over the CTAs, then a warp tree -- so the result is
+// bit-reproducible run to run.
+__global__ void __launch_bounds__(RED_THREADS)
+colreduce_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t n, int k, int kind,
+                 double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ out,
+                 int take_sqrt) {
   __shared__ double sh[RED_THREADS / 32][KMAX];
+  __shared__ bool last;
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per;
   int64_t r1 = r0 + per < n ? r0 + per : n;
@@ -218,16 +228,20 @@ __global__ void colreduce_partial(const double* __restrict__ X, const double* __
     for (int w = 0; w < RED_THREADS / 32; ++w) v += sh[w][threadIdx.x];
     partial[(int64_t)blockIdx.x * k + threadIdx.x] = v;
   }
-}
-
-__global__ void colreduce_final(const double* __restrict__ partial, int nb, int k, double* out,
-                                int take_sqrt) {
-  int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (c >= k) return;
-  double v = 0.0;
-  for (int b = lane; b < nb; b += 32) v += partial[(int64_t)b * k + c];
-  v = warp_sum(v);
-  if (lane == 0) out[c] = take_sqrt ? sqrt(v) : v;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  for (int c = wid; c < k; c += RED_THREADS / 32) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += __ldcg(partial + (int64_t)b * k + c);
+    v = warp_sum(v);
+    if (lane == 0) out[c] = take_sqrt ? sqrt(v) : v;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k, int kind,
@@ -235,8 +249,8 @@ int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
   BAMG_REQUIRE(ctx, k >= 1 && k <= KMAX, "k must lie in [1, 32]");
   double* partial = nullptr;
   BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * k, &partial));
-  BAMG_LAUNCH(ctx, colreduce_partial, RED_BLOCKS, RED_THREADS, 0, X, Y, n, k, kind, partial);
-  BAMG_LAUNCH(ctx, colreduce_final, 1, 32 * k, 0, partial, RED_BLOCKS, k, out_dev, take_sqrt);
+  BAMG_LAUNCH(ctx, colreduce_kernel, RED_BLOCKS, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
+              out_dev, take_sqrt);
   return 0;
 }
 

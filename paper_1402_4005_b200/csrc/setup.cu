@@ -18,35 +18,19 @@
 
 #include "internal.cuh"
 
-// X[:, c] /= peak[c] when peak[c] > 1e100 (bootstrap.py:302-306)
-__global__ void rescale_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ peak) {
+// X[:, c] /= peak[c] when peak[c] > 1e100 (bootstrap.py:302-306), both sides
+// in one launch: elements [0, total) of X0 with peak[0..k), then X1 with
+// peak[k..2k)
+__global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1, int64_t total, int k,
+                               const double* __restrict__ peak) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  double p = peak[i % k];
-  if (p > 1e100) X[i] = X[i] / p;
-}
-
-// rayleigh quotient finish.  dots = [uMu(k) | vNv(k) | uBv(k)].
-// mode 0: sigma = s (or prev when a normaliser collapses)
-// mode 1: refresh: s < -1e-13 -> flip[c] = 1, s = -s; sigma = |s|
-__global__ void rayleigh_finish_kernel(const double* __restrict__ dots, int k, double* __restrict__ sigma,
-                                       double* __restrict__ flip, int mode) {
-  int c = threadIdx.x;
-  if (c >= k) return;
-  double du = sqrt(fmax(dots[c], 0.0));
-  double dv = sqrt(fmax(dots[k + c], 0.0));
-  double prev = sigma[c];
-  double s = (du < 1e-15 || dv < 1e-15) ? prev : dots[2 * k + c] / (du * dv);
-  if (mode == 0) {
-    sigma[c] = s;
-  } else {
-    double f = 0.0;
-    if (s < -1e-13) {
-      f = 1.0;
-      s = -s;
-    }
-    flip[c] = f;
-    sigma[c] = fabs(s);
+  if (i >= 2 * total) return;
+  const bool second = i >= total;
+  const int64_t j = second ? i - total : i;
+  double p = peak[(second ? k : 0) + j % k];
+  if (p > 1e100) {
+    double* X = second ? X1 : X0;
+    X[j] = X[j] / p;
   }
 }
 
@@ -57,13 +41,17 @@ __global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const 
   if (flip[i % k] != 0.0) X[i] = -X[i];
 }
 
-// three column-dot sums in one pass: a.b, c.d, e.f per column
-__global__ void tri_colreduce_partial(const double* __restrict__ A, const double* __restrict__ Bm,
-                                      const double* __restrict__ Cm, const double* __restrict__ Dm,
-                                      const double* __restrict__ Em, const double* __restrict__ Fm,
-                                      int64_t n, int k, double* __restrict__ partial) {
+// three column-dot sums in one pass (a.b, c.d, e.f per column), then -- in
+// the last CTA to arrive -- the fixed-order sum of the per-CTA partials and
+// the Rayleigh quotient finish (one launch instead of three)
+__global__ void __launch_bounds__(RED_THREADS)
+rayleigh_reduce_kernel(const double* __restrict__ A, const double* __restrict__ Bm, const double* __restrict__ Cm,
+                       const double* __restrict__ Dm, const double* __restrict__ Em, const double* __restrict__ Fm,
+                       int64_t n, int k, double* __restrict__ partial, unsigned int* __restrict__ counter,
+                       double* __restrict__ dots, double* __restrict__ sigma, double* __restrict__ flip, int mode) {
   constexpr int KM = 32;
   __shared__ double sh[RED_THREADS / 32][3 * KM];
+  __shared__ bool last;
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per;
   int64_t r1 = min(r0 + per, n);
@@ -99,16 +87,39 @@ __global__ void tri_colreduce_partial(const double* __restrict__ A, const double
     for (int w = 0; w < RED_THREADS / 32; ++w) v += sh[w][threadIdx.x];
     partial[(int64_t)blockIdx.x * 3 * k + threadIdx.x] = v;
   }
-}
-
-__global__ void sum_partials_kernel(const double* __restrict__ partial, int nb, int m, double* __restrict__ out) {
-  int i = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (; i < m; i += blockDim.x >> 5) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int m = 3 * k, nb = gridDim.x;
+  for (int i = wid; i < m; i += RED_THREADS / 32) {
     double v = 0.0;
-    for (int b = lane; b < nb; b += 32) v += partial[(int64_t)b * m + i];
+    for (int b = lane; b < nb; b += 32) v += __ldcg(partial + (int64_t)b * m + i);
     v = warp_sum(v);
-    if (lane == 0) out[i] = v;
+    if (lane == 0) dots[i] = v;
   }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < k) {
+    double du = sqrt(fmax(dots[c], 0.0));
+    double dv = sqrt(fmax(dots[k + c], 0.0));
+    double prev = sigma[c];
+    double s = (du < 1e-15 || dv < 1e-15) ? prev : dots[2 * k + c] / (du * dv);
+    if (mode == 0) {
+      sigma[c] = s;
+    } else {
+      double f = 0.0;
+      if (s < -1e-13) {
+        f = 1.0;
+        s = -s;
+      }
+      flip[c] = f;
+      sigma[c] = fabs(s);
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 // sigma update from (U, V): mode 0 smoothing, mode 1 refresh (+ flips of U).
@@ -134,9 +145,10 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
   BAMG_TRY(arena_get(ctx, (size_t)3 * k, &dots));
   BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * 3 * k, &partial));
   BAMG_TRY(arena_get(ctx, (size_t)k, &flip));
-  BAMG_LAUNCH(ctx, tri_colreduce_partial, RED_BLOCKS, RED_THREADS, 0, U, mu, V, nv, U, AV, n, k, partial);
-  BAMG_LAUNCH(ctx, sum_partials_kernel, 1, 32 * 3 * k > 1024 ? 1024 : 32 * 3 * k, 0, partial, RED_BLOCKS, 3 * k, dots);
-  BAMG_LAUNCH(ctx, rayleigh_finish_kernel, 1, 32, 0, dots, k, sigma, flip, mode);
+  // rayleigh quotient: dots = [uMu(k) | vNv(k) | uBv(k)]; mode 0: sigma = s (or
+  // prev when a normaliser collapses); mode 1 (refresh): s < -1e-13 -> flip
+  BAMG_LAUNCH(ctx, rayleigh_reduce_kernel, RED_BLOCKS, RED_THREADS, 0, U, mu, V, nv, U, AV, n, k, partial,
+              ctx->counters + 1, dots, sigma, flip, mode);
   if (mode == 1 && U_flip_or_null) {
     int64_t total = n * k;
     BAMG_LAUNCH(ctx, flip_kernel, grid_for(total, 256), 256, 0, U_flip_or_null, total, k, flip);
@@ -164,8 +176,12 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
   const int64_t n = A->nrows;
   const int64_t total = n * k;
   if (smooth && nsweeps > 0) {
-    double *U2, *V2, *MU = nullptr, *NV = nullptr, *peak, *work3 = nullptr;
+    double *U2, *V2, *MU = nullptr, *NV = nullptr, *peak, *work3 = nullptr, *rd;
     if (inhomogeneous) BAMG_TRY(arena_get(ctx, (size_t)3 * total, &work3));
+    // reciprocal diagonal once per block: every sweep divides through it
+    // (div_rn_recip, bit-identical to the IEEE division)
+    BAMG_TRY(arena_get(ctx, (size_t)n, &rd));
+    BAMG_TRY(recip_dev(ctx, d, n, rd));
     BAMG_TRY(arena_get(ctx, (size_t)total, &U2));
     BAMG_TRY(arena_get(ctx, (size_t)total, &V2));
     BAMG_TRY(arena_get(ctx, (size_t)2 * k, &peak));
@@ -192,11 +208,10 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
         }
       }
       BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * 2 * k, ctx->stream));
-      BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak));
-      BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k));
+      BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak, rd));
+      BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k, rd));
       if (smooth == 1) {  // init_test_vectors (smooth == 2) has no runaway rescaling
-        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, vo, total, k, peak);
-        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(total, 256), 256, 0, uo, total, k, peak + k);
+        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(2 * total, 256), 256, 0, vo, uo, total, k, peak);
       }
       std::swap(u, uo);
       std::swap(v, vo);

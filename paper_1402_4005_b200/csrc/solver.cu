@@ -30,6 +30,7 @@ struct HLevel {
   double* x2 = nullptr;  // ping-pong partner
   double* b = nullptr;   // rhs (levels >= 1)
   double* r = nullptr;   // residual
+  double* rd = nullptr;  // RN(1/d) for the sweeps' division
 };
 
 // A captured V-cycle for one (b, x) pointer pair: the ~10 launches per level
@@ -154,7 +155,7 @@ static int hier_prepare(bamg_hier* h) {
     HLevel& v = h->lv[l];
     BAMG_REQUIRE(ctx, v.B.rowptr != nullptr, "level operator missing");
     if (l + 1 < L) BAMG_REQUIRE(ctx, v.P.rowptr && v.Q.rowptr, "transfer operators missing");
-    total += (size_t)4 * (v.n > 0 ? v.n : 1) + 32;  // 256-byte aligned level slices
+    total += (size_t)5 * (v.n > 0 ? v.n : 1) + 32;  // 256-byte aligned level slices
   }
   if (h->owned.empty() || h->owned[0].second < total * sizeof(double)) {
     for (auto& b : h->owned) pool_give(ctx, b.first, b.second);
@@ -171,7 +172,9 @@ static int hier_prepare(bamg_hier* h) {
     v.x2 = buf + n;
     v.b = buf + 2 * n;
     v.r = buf + 3 * n;
-    buf += ((4 * n + 31) / 32) * 32;
+    v.rd = buf + 4 * n;
+    buf += ((5 * n + 31) / 32) * 32;
+    if (v.n > 0 && v.d) BAMG_TRY(recip_dev(ctx, v.d, v.n, v.rd));
   }
   h->ready = true;
   return 0;
@@ -181,10 +184,11 @@ static int hier_prepare(bamg_hier* h) {
 // zero guess, bit-identical to relax.py:78-83 with x = 0).
 __global__ void jacobi_from_zero_kernel(int n, const double* __restrict__ b, const double* __restrict__ d,
                                         const uint8_t* __restrict__ skip, double omega,
-                                        double* __restrict__ x) {
+                                        double* __restrict__ x, const double* __restrict__ rd) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double upd = skip[i] ? 0.0 : __ddiv_rn(__dmul_rn(omega, b[i]), d[i]);
+  const double num = __dmul_rn(omega, b[i]);
+  double upd = skip[i] ? 0.0 : (rd ? div_rn_recip(num, d[i], rd[i]) : __ddiv_rn(num, d[i]));
   x[i] = __dadd_rn(0.0, upd);
 }
 
@@ -213,9 +217,9 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
     double* cur = v.x;
     double* oth = v.x2;
     if (h->nu1 > 0) {
-      BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(v.n, 256), 256, 0, v.n, bl, v.d, v.skip, om, cur);
+      BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(v.n, 256), 256, 0, v.n, bl, v.d, v.skip, om, cur, v.rd);
       for (int s = 1; s < h->nu1; ++s) {
-        BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, bl, nullptr, cur, oth, 1, om, nullptr));
+        BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, bl, nullptr, cur, oth, 1, om, nullptr, v.rd));
         std::swap(cur, oth);
       }
     } else {
@@ -244,7 +248,7 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
     std::swap(cur, oth);
     for (int s = 0; s < h->nu2; ++s) {
       double* dst = (l == 0 && s == h->nu2 - 1) ? x_out : oth;
-      BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, blv, nullptr, cur, dst, 1, om, nullptr));
+      BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, blv, nullptr, cur, dst, 1, om, nullptr, v.rd));
       if (dst == x_out) {
         cur = x_out;
       } else {
@@ -846,7 +850,7 @@ extern "C" int bamg_addmv(bamg_ctx* ctx, const bamg_csr* A, const double* xc, co
 
 extern "C" int bamg_jacobi_zero(bamg_ctx* ctx, int64_t n, const double* b, const double* d, const uint8_t* skip,
                                 double omega, double* x) {
-  BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(n, 256), 256, 0, (int)n, b, d, skip, omega, x);
+  BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(n, 256), 256, 0, (int)n, b, d, skip, omega, x, (const double*)nullptr);
   return 0;
 }
 

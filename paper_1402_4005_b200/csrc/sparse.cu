@@ -26,6 +26,7 @@ struct EpiArgs {
   const double* b;        // rhs (may be null)
   const double* b_scale;  // per-vector scale of b (may be null)
   const double* xold;     // iterate being relaxed (EPI_JACOBI)
+  const double* rd;       // RN(1/d) (may be null: plain IEEE division)
   double omega;
   double* peak;           // per-vector max |x'| (may be null)
 };
@@ -82,7 +83,10 @@ csr_tile_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       if (ea.b) bb = ea.b_scale ? __dmul_rn(ea.b_scale[c], ea.b[idx]) : ea.b[idx];
       const double r = __dsub_rn(bb, sum);
       double upd = 0.0;
-      if (!ea.skip[row]) upd = __ddiv_rn(__dmul_rn(ea.omega, r), ea.d[row]);
+      if (!ea.skip[row]) {
+        const double num = __dmul_rn(ea.omega, r);
+        upd = ea.rd ? div_rn_recip(num, ea.d[row], ea.rd[row]) : __ddiv_rn(num, ea.d[row]);
+      }
       const double xn = __dadd_rn(ea.xold[idx], upd);
       Y[idx] = xn;
       if (ea.peak) atomicMax(&s_peak[c], (unsigned long long)__double_as_longlong(fabs(xn)));
@@ -230,9 +234,11 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       VecIO<V>::load(ea.xold + base, xo);
       const bool sk = ea.skip[row] != 0;
       const double dd = ea.d[row];
+      const double rdd = ea.rd ? ea.rd[row] : 0.0;
 #pragma unroll
       for (int q = 0; q < V; ++q) {
-        double upd = sk ? 0.0 : __ddiv_rn(__dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q])), dd);
+        const double num = __dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q]));
+        double upd = sk ? 0.0 : (ea.rd ? div_rn_recip(num, dd, rdd) : __ddiv_rn(num, dd));
         out[q] = __dadd_rn(xo[q], upd);
         pk[q] = fabs(out[q]);
       }
@@ -381,9 +387,10 @@ int addmv_dev(bamg_ctx* ctx, const bamg_csr* A, const double* Xc, const double* 
 
 int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip,
                const double* b, const double* b_scale, const double* x, double* x_out, int k,
-               double omega, double* peak) {
+               double omega, double* peak, const double* rd) {
   EpiArgs ea{};
   ea.d = d;
+  ea.rd = rd;
   ea.skip = skip;
   ea.b = b;
   ea.b_scale = b_scale;
@@ -391,6 +398,82 @@ int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t*
   ea.omega = omega;
   ea.peak = peak;
   return launch_tile(ctx, EPI_JACOBI, A, x, k, x_out, ea);
+}
+
+// rd[i] = RN(1 / d[i]) (the reciprocal the Jacobi epilogue's exact division uses)
+__global__ void recip_kernel(const double* __restrict__ d, int64_t n, double* __restrict__ rd) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rd[i] = __ddiv_rn(1.0, d[i]);
+}
+
+int recip_dev(bamg_ctx* ctx, const double* d, int64_t n, double* rd) {
+  BAMG_LAUNCH(ctx, recip_kernel, grid_for(n, 256), 256, 0, d, n, rd);
+  return 0;
+}
+
+// Self-test of div_rn_recip against __ddiv_rn on n pseudo-random operand
+// pairs (counter-based hash, so every sample is reproducible from `seed`):
+// mantissas uniform, exponents drawn from mode-dependent ranges
+// (0: |e| <= 40, 1: the whole fast-path range, 2: all finite doubles incl.
+// subnormals and zeros, 3: d within a few ulps of powers of two and
+// all-ones mantissas).  Counts results whose bit patterns differ.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__device__ double selftest_operand(unsigned long long h, unsigned long long h2, int mode, bool is_d) {
+  unsigned long long mant = h & ((1ull << 52) - 1);
+  int e;
+  const unsigned long long r = h2 % 2001ull;
+  switch (mode) {
+    case 0: e = (int)(h2 % 81ull) - 40; break;
+    case 1: e = is_d ? (int)(h2 % 801ull) - 400 : (int)(h2 % 1001ull) - 500; break;
+    case 2: e = (int)(h2 % 2046ull) - 1022 - (int)(r % 2 ? 52 : 0); break;
+    default: {
+      e = (int)(h2 % 41ull) - 20;
+      const int pick = (int)((h2 >> 20) % 4ull);
+      if (pick == 0) mant = (1ull << 52) - 1 - (h2 >> 40) % 8ull;  // all-ones mantissa
+      else if (pick == 1) mant = (h2 >> 40) % 8ull;               // just above a power of two
+      break;
+    }
+  }
+  const unsigned long long sign = (h >> 63) << 63;
+  if (e < -1022) {  // subnormal / zero
+    int sh = -1022 - e;
+    unsigned long long m = sh >= 53 ? 0ull : ((mant | (1ull << 52)) >> sh);
+    return __longlong_as_double((long long)(sign | m));
+  }
+  unsigned long long bits = sign | ((unsigned long long)(e + 1023) << 52) | mant;
+  return __longlong_as_double((long long)bits);
+}
+
+__global__ void selftest_div_kernel(int64_t n, unsigned long long seed, int mode,
+                                    unsigned long long* __restrict__ mismatches) {
+  unsigned long long local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long h0 = mix64(seed ^ (4ull * i)), h1 = mix64(seed ^ (4ull * i + 1));
+    unsigned long long h2 = mix64(seed ^ (4ull * i + 2)), h3 = mix64(seed ^ (4ull * i + 3));
+    double x = selftest_operand(h0, h1, mode, false);
+    double d = selftest_operand(h2, h3, mode, true);
+    double ref = __ddiv_rn(x, d);
+    double got = div_rn_recip(x, d, __ddiv_rn(1.0, d));
+    if (__double_as_longlong(ref) != __double_as_longlong(got) && !(ref != ref && got != got)) ++local;
+  }
+  local = (unsigned long long)warp_sum((double)local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(mismatches, local);
+}
+
+extern "C" int bamg_selftest_div(bamg_ctx* ctx, int64_t n, uint64_t seed, int mode, int64_t* mismatches_host) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, mode >= 0 && mode <= 3, "mode must lie in [0, 3]");
+  unsigned long long* cnt;
+  BAMG_TRY(arena_get(ctx, 1, &cnt));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+  BAMG_LAUNCH(ctx, selftest_div_kernel, ctx->num_sms * 8, 256, 0, n, (unsigned long long)seed, mode, cnt);
+  return ctx_read_i64(ctx, reinterpret_cast<int64_t*>(cnt), 1, mismatches_host);
 }
 
 extern "C" int bamg_spmv(bamg_ctx* ctx, const bamg_csr* A, const double* x, double* y) {
@@ -406,7 +489,7 @@ extern "C" int bamg_jacobi(bamg_ctx* ctx, const bamg_csr* A, const double* d, co
                            double* x_out, int k, double omega, double* peak) {
   BAMG_REQUIRE(ctx, x != x_out, "Jacobi needs distinct input and output iterates");
   if (peak) BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * k, ctx->stream));
-  return jacobi_dev(ctx, A, d, skip, b, b_scale, x, x_out, k, omega, peak);
+  return jacobi_dev(ctx, A, d, skip, b, b_scale, x, x_out, k, omega, peak, nullptr);
 }
 
 // ------------------------------------------------------------ diagonal

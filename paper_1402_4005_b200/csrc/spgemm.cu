@@ -25,9 +25,35 @@
 
 constexpr int LCAP = 64;   // distinct columns per row on the fast path
 constexpr int HSLOTS = 128;
+constexpr int TSLOT = 32;  // kept entries per row parked by the count pass
 
 __device__ __forceinline__ bool keep_value(int order, double x) {
   return order == 0 ? !(fabs(x) < 1e-300) : (x != 0.0);
+}
+
+// write the row's kept entries in the requested order to (ocol, oval); the
+// sorted order is produced by ranking (each kept entry counts the kept keys
+// below it -- keys are distinct), so every output is stored exactly once
+__device__ __forceinline__ void emit_row(int order, const int* key, const double* val, int len, int32_t* ocol,
+                                         double* oval) {
+  if (order == 1) {  // reverse first touch
+    int w = 0;
+    for (int q = len - 1; q >= 0; --q)
+      if (keep_value(order, val[q])) {
+        ocol[w] = key[q];
+        oval[w] = val[q];
+        ++w;
+      }
+    return;
+  }
+  for (int q = 0; q < len; ++q) {  // sorted by column
+    if (!keep_value(order, val[q])) continue;
+    const int c = key[q];
+    int r = 0;
+    for (int p = 0; p < len; ++p) r += (key[p] < c && keep_value(order, val[p])) ? 1 : 0;
+    ocol[r] = c;
+    oval[r] = val[q];
+  }
 }
 
 template <int PASS>
@@ -36,9 +62,14 @@ spgemm_local_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __res
                     const double* __restrict__ aval, const int32_t* __restrict__ brp,
                     const int32_t* __restrict__ bcol, const double* __restrict__ bval, int order,
                     int32_t* __restrict__ cnt, int32_t* __restrict__ big_list, unsigned int* __restrict__ nbig,
-                    const int32_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                    const int32_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval,
+                    int32_t* __restrict__ tcol, double* __restrict__ tval, uint8_t* __restrict__ parked,
+                    const int32_t* __restrict__ rows, const unsigned int* __restrict__ nrows) {
+  // rows (fill pass): grid-stride over the *nrows listed rows; else row = thread
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tn = rows ? (int)*nrows : n;
+  for (int t = t0; t < tn; t += rows ? gridDim.x * blockDim.x : tn) {
+  const int i = rows ? rows[t] : t;
   int key[LCAP];
   double val[LCAP];
   unsigned int slotw[HSLOTS / 4];  // 1-byte list indices, 0xff = empty
@@ -78,38 +109,43 @@ spgemm_local_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __res
   if (PASS == 0) {
     if (overflow) {
       cnt[i] = 0;
+      parked[i] = 0;
       big_list[atomicAdd(nbig, 1u)] = i;
-      return;
+      continue;
     }
     int c = 0;
     for (int q = 0; q < len; ++q) c += keep_value(order, val[q]) ? 1 : 0;
     cnt[i] = c;
+    // park the finished row (<= TSLOT entries) so the fill pass only copies it
+    const bool park = tcol != nullptr && c <= TSLOT;
+    parked[i] = park ? 1 : 0;
+    if (park) emit_row(order, key, val, len, tcol + (int64_t)i * TSLOT, tval + (int64_t)i * TSLOT);
+    continue;
+  }
+  if (overflow) continue;  // slow path writes this row
+  emit_row(order, key, val, len, ccol + crp[i], cval + crp[i]);
+  }
+}
+
+// fill pass for parked rows: one warp per row copies the parking slot
+// (coalesced); rows that were not parked go to the redo list for the
+// recomputing fill (or the slow path)
+__global__ void spgemm_copy_parked_kernel(int n, const uint8_t* __restrict__ parked, const int32_t* __restrict__ crp,
+                                          const int32_t* __restrict__ tcol, const double* __restrict__ tval,
+                                          int32_t* __restrict__ ccol, double* __restrict__ cval,
+                                          int32_t* __restrict__ redo, unsigned int* __restrict__ nredo) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int i = (int)w;
+  const int b = crp[i], e = crp[i + 1];
+  if (!parked[i]) {
+    if (lane == 0 && e > b) redo[atomicAdd(nredo, 1u)] = i;
     return;
   }
-  if (overflow) return;  // slow path writes this row
-  int w = crp[i];
-  if (order == 1) {  // reverse first touch
-    for (int q = len - 1; q >= 0; --q)
-      if (keep_value(order, val[q])) {
-        ccol[w] = key[q];
-        cval[w] = val[q];
-        ++w;
-      }
-  } else {  // sorted by column
-    int start = w;
-    for (int q = 0; q < len; ++q) {
-      if (!keep_value(order, val[q])) continue;
-      int c = key[q];
-      double x = val[q];
-      int p = w++;
-      while (p > start && ccol[p - 1] > c) {
-        ccol[p] = ccol[p - 1];
-        cval[p] = cval[p - 1];
-        --p;
-      }
-      ccol[p] = c;
-      cval[p] = x;
-    }
+  if (lane < e - b) {
+    ccol[b + lane] = tcol[(int64_t)i * TSLOT + lane];
+    cval[b + lane] = tval[(int64_t)i * TSLOT + lane];
   }
 }
 
@@ -202,6 +238,13 @@ struct SpgemmMemo {
   int32_t* list = nullptr;   // device, capacity cap
   int32_t* off = nullptr;    // device, capacity cap + 1
   int64_t cap = 0;
+  // parking slots of the count pass (TSLOT entries per row) + flags + redo list
+  int32_t* tcol = nullptr;
+  double* tval = nullptr;
+  uint8_t* parked = nullptr;
+  int32_t* redo = nullptr;
+  unsigned int* nredo = nullptr;
+  int64_t tcap = 0;
 };
 
 static SpgemmMemo& memo(bamg_ctx* ctx) {
@@ -213,6 +256,19 @@ static SpgemmMemo& memo(bamg_ctx* ctx) {
 }
 
 static int memo_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t n) {
+  if (m.tcap < n + 1) {
+    cudaFree(m.tcol);
+    cudaFree(m.tval);
+    cudaFree(m.parked);
+    cudaFree(m.redo);
+    cudaFree(m.nredo);
+    m.tcap = n + 1;
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.tcol, sizeof(int32_t) * TSLOT * m.tcap));
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.tval, sizeof(double) * TSLOT * m.tcap));
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.parked, m.tcap));
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.redo, sizeof(int32_t) * m.tcap));
+    BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.nredo, sizeof(unsigned int)));
+  }
   if (m.cap >= n + 1) return 0;
   if (m.list) cudaFree(m.list);
   if (m.off) cudaFree(m.off);
@@ -237,7 +293,8 @@ extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(unsigned int), ctx->stream));
   BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
                   A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
-                  (int32_t*)nullptr, (double*)nullptr);
+                  (int32_t*)nullptr, (double*)nullptr, m.tcol, m.tval, m.parked, (const int32_t*)nullptr,
+                  (const unsigned int*)nullptr);
   int32_t nb = 0;
   BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(nbig), 1, &nb));
   m.arp = A->rowptr;
@@ -268,9 +325,21 @@ extern "C" int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr
   SpgemmMemo& m = memo(ctx);
   BAMG_REQUIRE(ctx, m.arp == A->rowptr && m.brp == B->rowptr && m.order == order,
                "bamg_spgemm_fill must follow bamg_spgemm_count on the same operands");
-  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<1>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
-                  A->val, B->rowptr, B->col, B->val, order, (int32_t*)nullptr, (int32_t*)nullptr,
-                  (unsigned int*)nullptr, rowptr_c, col_c, val_c);
+  // parked rows are copied; the others (more than TSLOT kept entries) are
+  // recomputed by the local kernel over the redo list (slow-path rows return
+  // there and are written below)
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(m.nredo, 0, sizeof(unsigned int), ctx->stream));
+  static_assert(TSLOT == 32, "one lane per parked entry");
+  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_copy_parked_kernel, grid_for((int64_t)n * 32, 256), 256, 0, n, m.parked, rowptr_c,
+                  m.tcol, m.tval, col_c, val_c, m.redo, m.nredo);
+  {
+    int g = grid_for(n, 128);
+    if (g > ctx->num_sms * 4) g = ctx->num_sms * 4;
+    BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<1>, g, 128, 0, n, A->rowptr, A->col, A->val,
+                    B->rowptr, B->col, B->val, order, (int32_t*)nullptr, (int32_t*)nullptr, (unsigned int*)nullptr,
+                    rowptr_c, col_c, val_c, (int32_t*)nullptr, (double*)nullptr, (uint8_t*)nullptr,
+                    (const int32_t*)m.redo, (const unsigned int*)m.nredo);
+  }
   if (m.nbig > 0) {
     int32_t* skey;
     double* sval;

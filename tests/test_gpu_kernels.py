@@ -94,6 +94,17 @@ def test_jacobi_bitexact_with_degenerate_rows(eng, golden):
     assert np.array_equal(out.cpu().numpy(), g["jac_out"])
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_reciprocal_division_is_ieee_exact(eng, mode):
+    """The Jacobi epilogue divides through RN(1/d) + one FMA correction; it must
+    equal IEEE x / d bit for bit (2^28 random pairs per mode, 2 seeds)."""
+    import ctypes as C
+    for seed in (1, 12345):
+        mis = C.c_int64(-1)
+        eng[0].call("bamg_selftest_div", 1 << 28, seed, mode, C.byref(mis))
+        assert mis.value == 0, f"mode {mode} seed {seed}: {mis.value} mismatches"
+
+
 def _device_hierarchy(eng, levels, omega, nu1, nu2):
     """Upload an oracle-built hierarchy (test input) into an engine hierarchy."""
     import ctypes as C
