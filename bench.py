@@ -327,9 +327,11 @@ def run_ours(args, rank, world, local_rank):
     ms, cnt, by = fam_stats[dom]
     per_launch_s = ms / 1e3 / max(cnt, 1)
     achieved = (by / max(cnt, 1)) / per_launch_s / 1e9 if cnt else 0.0
+    traffic, traffic_src = family_traffic(dom, by / max(cnt, 1))
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+            "alg_bytes_per_launch": round(by / max(cnt, 1)),
             "launches_in_timed_region": cnt, "share_of_step": round(ms / 1e3 / (dev_s * args.steps), 4),
             "families": {f: {"ms_total": round(v[0], 3), "launches": v[1],
                              "alg_GBps": round((v[2] / max(v[1], 1)) / (v[0] / 1e3 / max(v[1], 1)) / 1e9, 1) if v[1] else 0}
@@ -362,6 +364,27 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.destroy_process_group()
     return line
+
+
+def family_traffic(family, alg_per_launch):
+    """roofline.traffic: DRAM bytes per launch of the roofline's kernel family.
+
+    From the committed ncu capture (profiles/rNN_csr_family_traffic.json, made by
+    tools/family_traffic.py): ncu's dram__bytes_read.sum + dram__bytes_write.sum
+    over every CSR row-kernel launch of one cfg1 step, divided by the engine's
+    algorithmic bytes for the same launches (graph-free run, so every launch is
+    profiled).  The timed region's launches (V-cycle graph nodes are not event-
+    timed) get that measured traffic/algorithmic ratio applied to their own
+    algorithmic bytes per launch."""
+    files = sorted(ROOT.glob("profiles/r*_csr_family_traffic.json"))
+    if family != "csr_stream_spmv_spmm_jacobi" or not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    ratio = d.get("traffic_over_alg")
+    if not ratio:
+        return None, None
+    return round(alg_per_launch * ratio), (f"{files[-1].name}: ncu DRAM bytes / algorithmic bytes = {ratio:.3f} "
+                                           f"over {d['launches']} launches of one step, applied per launch")
 
 
 def cpu_baseline(name, sample=None, repeat=1):

@@ -10,6 +10,7 @@ import torch
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg1")
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--prof", action="store_true", help="engine family profiler over the steps (alg bytes per family)")
 a = ap.parse_args()
 
 _gc_t = [0.0]
@@ -42,6 +43,10 @@ dU = torch.from_numpy(np.ascontiguousarray(lh.T)).cuda()
 geo = torch.from_numpy(np.ascontiguousarray(prob.geometry.T)).cuda()
 P = ChainProblem(A=None, B=dB, n=prob.n, family=fam, params={}, geometry=geo)
 zero = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+from paper_1402_4005_b200 import _lib
+import ctypes as C
+if a.prof:
+    _lib.lib().bamg_prof_enable(_lib.ctx(), 0b11)
 for i in range(a.steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -56,3 +61,8 @@ for i in range(a.steps):
     print(json.dumps({"step": i, "total_ms": round((t4 - t0) * 1e3, 2), "setup_ms": round((t1 - t0) * 1e3, 2),
                       "vop_ms": round((t2 - t1) * 1e3, 2), "gmres_ms": round((t3 - t2) * 1e3, 2),
                       "tail_ms": round((t4 - t3) * 1e3, 2)}), flush=True)
+if a.prof:
+    for fid, fname in ((0, "csr_stream_spmv_spmm_jacobi"), (1, "ls_fit")):
+        ms, cnt, by = C.c_double(), C.c_int64(), C.c_double()
+        _lib.lib().bamg_prof_read(_lib.ctx(), fid, C.byref(ms), C.byref(cnt), C.byref(by))
+        print(json.dumps({"family": fname, "ms": ms.value, "launches": cnt.value, "alg_bytes": by.value}), flush=True)
