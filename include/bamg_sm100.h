@@ -93,6 +93,11 @@ int bamg_count_nonpositive(bamg_ctx* ctx, const double* d, int64_t n, int64_t* c
  * A-row order then B-row order, exact-zero results dropped.  `order`:
  *   0 = canonical (sorted columns, |v| < 1e-300 also dropped: make_csr),
  *   1 = scipy storage order (reverse first touch), exact zeros dropped only.
+ * Flags or'ed into `order`: 2 = walk each row of A in reverse storage order,
+ * 4 = walk each row of B in reverse.  They give (A I) B and A (I B) with an
+ * identity mass I bit-identically without forming the identity product
+ * (scipy stores A I / I B with every row reversed: bootstrap.py:372-373 at the
+ * finest level, where M = N = I).
  * Count pass fills rowptr_c (nrows+1) and returns nnz; fill pass writes.
  * Replaces triple_product, sparse.py:102-117 and bootstrap.py:372-373. */
 int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,

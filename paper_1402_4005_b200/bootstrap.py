@@ -376,9 +376,18 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
                 trips = coarsest_triplets(A, Md, Nd, trips.r)
             return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
         with _phase("galerkin"):
-            Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
+            # identity masses (the finest level): scipy's Q@I / I@P store every
+            # row reversed, so (Q I) W and P^T (I P) are the products with Q's /
+            # P's rows walked in reverse -- bit-identical, no identity product
+            if Md.is_identity:
+                Mc = engine.spgemm(Q, W, order=engine.SPGEMM_REV_A)
+            else:
+                Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
             Pt = engine.transpose(P)
-            Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
+            if Nd.is_identity:
+                Nc = engine.spgemm(Pt, P, order=engine.SPGEMM_REV_B)
+            else:
+                Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
         with _phase("inject"):
             cranks = ranks.restrict(split) if ranks is not None else None
             cl = engine.gather_rows(trips.dleft, split.dcoarse)

@@ -27,8 +27,10 @@ constexpr int LCAP = 64;   // distinct columns per row on the fast path
 constexpr int HSLOTS = 128;
 constexpr int TSLOT = 32;  // kept entries per row parked by the count pass
 
+constexpr int SPG_STORAGE = 1, SPG_REV_A = 2, SPG_REV_B = 4;
+
 __device__ __forceinline__ bool keep_value(int order, double x) {
-  return order == 0 ? !(fabs(x) < 1e-300) : (x != 0.0);
+  return (order & SPG_STORAGE) == 0 ? !(fabs(x) < 1e-300) : (x != 0.0);
 }
 
 // write the row's kept entries in the requested order to (ocol, oval); the
@@ -36,7 +38,7 @@ __device__ __forceinline__ bool keep_value(int order, double x) {
 // below it -- keys are distinct), so every output is stored exactly once
 __device__ __forceinline__ void emit_row(int order, const int* key, const double* val, int len, int32_t* ocol,
                                          double* oval) {
-  if (order == 1) {  // reverse first touch
+  if (order & SPG_STORAGE) {  // reverse first touch
     int w = 0;
     for (int q = len - 1; q >= 0; --q)
       if (keep_value(order, val[q])) {
@@ -77,10 +79,15 @@ spgemm_local_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __res
   for (int h = 0; h < HSLOTS / 4; ++h) slotw[h] = 0xffffffffu;
   int len = 0;
   bool overflow = false;
-  for (int jj = arp[i]; jj < arp[i + 1] && !overflow; ++jj) {
+  const bool rev_a = (order & SPG_REV_A) != 0, rev_b = (order & SPG_REV_B) != 0;
+  const int a0 = arp[i], a1 = arp[i + 1];
+  for (int ja = 0; ja < a1 - a0 && !overflow; ++ja) {
+    const int jj = rev_a ? a1 - 1 - ja : a0 + ja;
     int j = acol[jj];
     double v = aval[jj];
-    for (int kk = brp[j]; kk < brp[j + 1]; ++kk) {
+    const int b0 = brp[j], b1 = brp[j + 1];
+    for (int kb = 0; kb < b1 - b0; ++kb) {
+      const int kk = rev_b ? b1 - 1 - kb : b0 + kb;
       int c = bcol[kk];
       double p = __dmul_rn(v, bval[kk]);
       unsigned h = ((unsigned)c * 2654435761u) >> 25;  // 7 bits
@@ -178,10 +185,15 @@ __global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, cons
   int32_t* key = skey + soff[t];
   double* val = sval + soff[t];
   int len = 0;
-  for (int jj = arp[i]; jj < arp[i + 1]; ++jj) {
+  const bool rev_a = (order & SPG_REV_A) != 0, rev_b = (order & SPG_REV_B) != 0;
+  const int a0 = arp[i], a1 = arp[i + 1];
+  for (int ja = 0; ja < a1 - a0; ++ja) {
+    const int jj = rev_a ? a1 - 1 - ja : a0 + ja;
     int j = acol[jj];
     double v = aval[jj];
-    for (int kk = brp[j]; kk < brp[j + 1]; ++kk) {
+    const int b0 = brp[j], b1 = brp[j + 1];
+    for (int kb = 0; kb < b1 - b0; ++kb) {
+      const int kk = rev_b ? b1 - 1 - kb : b0 + kb;
       int c = bcol[kk];
       double p = __dmul_rn(v, bval[kk]);
       int q = 0;
@@ -202,7 +214,7 @@ __global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, cons
     return;
   }
   int w = crp[i];
-  if (order == 1) {
+  if (order & SPG_STORAGE) {
     for (int q = len - 1; q >= 0; --q)
       if (keep_value(order, val[q])) {
         ccol[w] = key[q];
@@ -282,7 +294,8 @@ extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
                                  int64_t* nnz_host) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, A && B && A->ncols == B->nrows, "dimension mismatch in sparse product");
-  BAMG_REQUIRE(ctx, order == 0 || order == 1, "order must be 0 (canonical) or 1 (scipy storage order)");
+  BAMG_REQUIRE(ctx, order >= 0 && order <= 7,
+               "order must be 0 (canonical) or 1 (scipy storage order), optionally | 2 (reverse A rows) | 4 (reverse B rows)");
   const int n = A->nrows;
   SpgemmMemo& m = memo(ctx);
   BAMG_TRY(memo_reserve(ctx, m, n));

@@ -92,7 +92,13 @@ def count_empty_rows(A: DeviceCSR) -> int:
     return out.value
 
 
+SPGEMM_STORAGE, SPGEMM_REV_A, SPGEMM_REV_B = 1, 2, 4  # bamg_spgemm_count `order` bits
+
+
 def spgemm(A: DeviceCSR, B: DeviceCSR, order: int = 0) -> DeviceCSR:
+    """C = A B with scipy csr_matmat semantics; `order` 0 canonical, 1 scipy
+    storage order, optionally | SPGEMM_REV_A / SPGEMM_REV_B (rows walked in
+    reverse: the products with an identity mass folded in)."""
     if A.shape[1] != B.shape[0]:
         raise ValueError(f"dimension mismatch in sparse product: {A.shape} x {B.shape}")
     rp = _empty(A.shape[0] + 1, I32)

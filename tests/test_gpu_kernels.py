@@ -94,6 +94,32 @@ def test_jacobi_bitexact_with_degenerate_rows(eng, golden):
     assert np.array_equal(out.cpu().numpy(), g["jac_out"])
 
 
+def test_spgemm_identity_mass_flags_bitexact(eng):
+    """(Q I) W == spgemm(Q, W, REV_A) and P^T (I P) == spgemm(P^T, P, REV_B), bit for bit."""
+    import scipy.sparse as sp
+    from paper_1402_4005_b200 import engine
+    from paper_1402_4005_b200.device import DeviceCSR
+    rng = np.random.default_rng(7)
+    n, nc = 900, 240
+    Q = sp.random(nc, n, density=0.02, random_state=rng, format="csr")
+    Q.data = rng.standard_normal(Q.nnz)
+    P = sp.random(n, nc, density=0.02, random_state=rng, format="csr")
+    P.data = rng.standard_normal(P.nnz)
+    Q.sort_indices()
+    P.sort_indices()
+    dQ, dW, dP = DeviceCSR.from_host(Q), DeviceCSR.from_host(Q.T.tocsr()), DeviceCSR.from_host(P)
+    dPt = engine.transpose(dP)
+    I = DeviceCSR.identity(n)
+    a = engine.spgemm(engine.spgemm(dQ, I, order=1), dW, order=0).to_host()
+    b = engine.spgemm(dQ, dW, order=engine.SPGEMM_REV_A).to_host()
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.data.view(np.int64), b.data.view(np.int64))
+    c = engine.spgemm(dPt, engine.spgemm(I, dP, order=1), order=0).to_host()
+    d = engine.spgemm(dPt, dP, order=engine.SPGEMM_REV_B).to_host()
+    assert np.array_equal(c.indptr, d.indptr) and np.array_equal(c.indices, d.indices)
+    assert np.array_equal(c.data.view(np.int64), d.data.view(np.int64))
+
+
 @pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_reciprocal_division_is_ieee_exact(eng, mode):
     """The Jacobi epilogue divides through RN(1/d) + one FMA correction; it must
