@@ -248,13 +248,16 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
   if (EPI == EPI_JACOBI && ea.peak) {
     // max over the lanes that own the same vectors (lane % G), then one
     // shared atomic per (warp, vector) and one global atomic per (CTA, vector)
+    constexpr bool POW2 = (G & (G - 1)) == 0;  // lane % G groups survive xor shuffles
+    if constexpr (POW2) {
 #pragma unroll
-    for (int q = 0; q < V; ++q) {
-      double m = pk[q];
-      for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      pk[q] = m;
+      for (int q = 0; q < V; ++q) {
+        double m = pk[q];
+        for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        pk[q] = m;
+      }
     }
-    if ((threadIdx.x & 31) < G) {
+    if (!POW2 || (threadIdx.x & 31) < G) {
 #pragma unroll
       for (int q = 0; q < V; ++q)
         atomicMax(&s_peak[sub * V + q], (unsigned long long)__double_as_longlong(pk[q]));
@@ -307,6 +310,153 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
 #undef BAMG_ROWS_CASE
     default:
       return 1;  // not specialised
+  }
+}
+
+static int check_csr(bamg_ctx* ctx, const bamg_csr* A);
+
+// Fused Rayleigh quotient for identity masses (bootstrap.py:144-153 with
+// M = N = I): one pass over A computes (A V)[row] per vector with the SpMM's
+// sequential sums and folds it straight into u.(Av); the same pass sums u.u
+// and v.v.  A fixed grid of RED_BLOCKS CTAs strides over row tiles, so the
+// per-CTA partials -- and the last CTA's fixed-order final sum and sigma
+// finish -- are bit-reproducible.  Saves the A V write + re-read and two
+// launches per quotient.
+template <int K, int G, int U>
+__global__ void __launch_bounds__(TILE_THREADS)
+rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                      const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
+                      double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
+                      double* __restrict__ sigma, double* __restrict__ flip, int mode) {
+  constexpr int VV = K / G;
+  constexpr int RB = TILE_THREADS / G;
+  __shared__ double sv[3][TILE_THREADS][VV];
+  __shared__ bool last;
+  const int lr = threadIdx.x / G;
+  const int sub = threadIdx.x - lr * G;
+  const int voff = sub * VV;
+  double s0[VV], s1[VV], s2[VV];
+#pragma unroll
+  for (int q = 0; q < VV; ++q) s0[q] = s1[q] = s2[q] = 0.0;
+  for (int tile = blockIdx.x; tile * RB < nrows; tile += gridDim.x) {
+    const int row = tile * RB + lr;
+    if (row < nrows) {
+      double acc[VV];
+#pragma unroll
+      for (int q = 0; q < VV; ++q) acc[q] = 0.0;
+      const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+      for (int j = jb; j < je; j += U) {
+        int cc[U];
+        double aa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int jj = j + u < je ? j + u : je - 1;
+          cc[u] = __ldg(col + jj);
+          aa[u] = __ldg(val + jj);
+        }
+        double xv[U][VV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) VecIO<VV>::load(Vv + (int64_t)cc[u] * K + voff, xv[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j + u < je) {
+#pragma unroll
+            for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+          }
+        }
+      }
+      double uu[VV], vv[VV];
+      VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
+      VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
+#pragma unroll
+      for (int q = 0; q < VV; ++q) {
+        s0[q] += uu[q] * acc[q];
+        s1[q] += uu[q] * uu[q];
+        s2[q] += vv[q] * vv[q];
+      }
+    }
+  }
+  // CTA sum per (quantity, vector): every thread parks its VV partials, then
+  // thread t < 3K adds the RB threads that own vector (t % K) in row order
+  // (G need not divide the warp: K = 12 runs G = 6)
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < VV; ++q) {
+    sv[0][threadIdx.x][q] = s1[q];  // uMu
+    sv[1][threadIdx.x][q] = s2[q];  // vNv
+    sv[2][threadIdx.x][q] = s0[q];  // uBv
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x < 3 * K) {
+    const int qi = threadIdx.x / K, c = threadIdx.x % K, sb = c / VV, q = c % VV;
+    double v = 0.0;
+    for (int r = 0; r < RB; ++r) v += sv[qi][r * G + sb][q];
+    partial[(int64_t)blockIdx.x * 3 * K + threadIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int m = 3 * K, nb = gridDim.x;
+  for (int i = wid; i < m; i += TILE_THREADS / 32) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += __ldcg(partial + (int64_t)b * m + i);
+    v = warp_sum(v);
+    if (lane == 0) dots[i] = v;
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < K) {
+    double du = sqrt(fmax(dots[c], 0.0));
+    double dv = sqrt(fmax(dots[K + c], 0.0));
+    double prev = sigma[c];
+    double sg = (du < 1e-15 || dv < 1e-15) ? prev : dots[2 * K + c] / (du * dv);
+    if (mode == 0) {
+      sigma[c] = sg;
+    } else {
+      double f = 0.0;
+      if (sg < -1e-13) {
+        f = 1.0;
+        sg = -sg;
+      }
+      flip[c] = f;
+      sigma[c] = fabs(sg);
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// returns 1 when k has no specialisation (caller takes the general path)
+int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const double* V, int k, double* sigma,
+                       double* flip, int mode, double* dots) {
+  BAMG_TRY(check_csr(ctx, A));
+  if (((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(V)) & 15) != 0 && !(k & 1)) return 1;
+  // fixed grid (a constant, so the partial-sum tree is reproducible), up to
+  // 8 CTAs per SM of row tiles in flight
+  constexpr int RQ_BLOCKS = 8 * 148;
+  double* partial;
+  BAMG_TRY(arena_get(ctx, (size_t)RQ_BLOCKS * 3 * k, &partial));
+  const double n = A->nrows;
+  const double bytes = 4.0 * (n + 1) + 12.0 * (double)A->nnz + 8.0 * k * A->ncols + 8.0 * k * n;
+  switch (k) {
+#define BAMG_RQ_CASE(KK, GG, UU)                                                                              \
+  case KK:                                                                                                   \
+    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), RQ_BLOCKS, TILE_THREADS, 0,  \
+                    A->nrows, A->rowptr, A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, \
+                    mode);                                                                                   \
+    return 0;
+    BAMG_RQ_CASE(1, 1, BAMG_U1)
+    BAMG_RQ_CASE(2, 1, 4)
+    BAMG_RQ_CASE(4, 2, 4)
+    BAMG_RQ_CASE(8, BAMG_G8, BAMG_U8)
+    BAMG_RQ_CASE(12, 6, 4)
+    BAMG_RQ_CASE(16, 8, 4)
+#undef BAMG_RQ_CASE
+    default:
+      return 1;
   }
 }
 
