@@ -54,6 +54,8 @@ const char* bamg_last_error(bamg_ctx* ctx);
 int bamg_version(void);
 /* Number of kernels this context has launched (evidence for bench.py). */
 int64_t bamg_launch_count(bamg_ctx* ctx);
+/* Number of times the engine made the host wait on its stream. */
+int64_t bamg_sync_count(bamg_ctx* ctx);
 int bamg_sync(bamg_ctx* ctx);
 /* Live per-kernel-family timing with CUDA events on the context's stream.
  * Families: 0 CSR-stream SpMV/SpMM/Jacobi, 1 LS fit, 2 SpGEMM, 3 GMRES
@@ -65,6 +67,8 @@ int bamg_prof_read(bamg_ctx* ctx, int family, double* ms_host, int64_t* launches
  * name into "name total_ms count" lines. */
 int bamg_trace_enable(bamg_ctx* ctx, int on);
 int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap);
+/* Same trace as a per-launch timeline: "name start_us end_us" lines. */
+int bamg_trace_timeline(bamg_ctx* ctx, char* buf, int64_t cap);
 
 /* ------------------------------------------------------- sparse (sparse.py) */
 /* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;
@@ -230,6 +234,14 @@ int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double rank_tol, doub
 int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const double* Md,
                            const double* Nd, int n, int r, double* U, double* V,
                            double* sigma);
+/* Same, and for the large (blocked) path also the V-cycle's pseudo-inverse of
+ * B (row-major n x n into Z, as bamg_dense_pinv) derived from the same
+ * factors: B^+ = (I - z z^T) L_N^-T K^+ L_M^-1 (I - y y^T).  *z_valid = 1 when
+ * it was computed and certified (else the caller builds it with
+ * bamg_dense_pinv).  Replaces the second factorisation behind PinvOperator
+ * (dense.py:118-131, built solver.py:93-94) for the coarsest level. */
+int bamg_coarsest_triplets_pinv(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n, int r,
+                                double* U, double* V, double* sigma, double* Z, int* z_valid);
 
 /* ----------------------------------------------------------- solver (solver.py) */
 /* Hierarchy for the V-cycle (VCycleOperator, solver.py:79-124).  Level

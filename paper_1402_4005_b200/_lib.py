@@ -45,11 +45,13 @@ _SIGS = {
     "bamg_last_error": [P],
     "bamg_version": [],
     "bamg_launch_count": [P],
+    "bamg_sync_count": [P],
     "bamg_sync": [P],
     "bamg_prof_enable": [P, C.c_uint],
     "bamg_prof_read": [P, C.c_int, PF64, PI64, PF64],
     "bamg_trace_enable": [P, C.c_int],
     "bamg_trace_dump": [P, C.c_char_p, I64],
+    "bamg_trace_timeline": [P, C.c_char_p, I64],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
     "bamg_csr_transpose": [P, PCSR, P, P, P],
@@ -85,6 +87,7 @@ _SIGS = {
     "bamg_csr_to_dense": [P, PCSR, P, C.c_int, C.c_int],
     "bamg_dense_pinv": [P, P, C.c_int, F64, P],
     "bamg_coarsest_triplets": [P, P, P, P, C.c_int, C.c_int, P, P, P],
+    "bamg_coarsest_triplets_pinv": [P, P, P, P, C.c_int, C.c_int, P, P, P, P, P],
     "bamg_hier_create": [P, C.c_int, C.POINTER(P)],
     "bamg_hier_destroy": [P],
     "bamg_hier_set_level": [P, C.c_int, PCSR, P, P, PCSR, PCSR],
@@ -102,7 +105,7 @@ _SIGS = {
     "bamg_mupdate": [P, P, C.c_int, P, P, I64, P],
     "bamg_combine": [P, P, C.c_int, P, P, P, I64, P],
 }
-_RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64}
+_RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64, "bamg_sync_count": C.c_int64}
 
 _lock = threading.Lock()
 _lib = None

@@ -38,6 +38,9 @@ _DEBUG = bool(os.environ.get("BAMG_DEBUG"))
 #: optional phase profiler (bench.py --breakdown): name -> seconds.  Each
 #: phase boundary synchronises the device, so it is off on the timed path.
 PHASES: dict | None = None
+#: optional sync-free phase recorder (tools/timeline.py): called with
+#: (name, entering) at every phase boundary.
+RECORDER = None
 
 
 class _phase:
@@ -45,11 +48,15 @@ class _phase:
         self.name = name
 
     def __enter__(self):
+        if RECORDER is not None:
+            RECORDER(self.name, True)
         if PHASES is not None:
             torch.cuda.synchronize()
             self.t = time.perf_counter()
 
     def __exit__(self, *exc):
+        if RECORDER is not None:
+            RECORDER(self.name, False)
         if PHASES is not None:
             torch.cuda.synchronize()
             PHASES[self.name] = PHASES.get(self.name, 0.0) + time.perf_counter() - self.t
@@ -293,8 +300,12 @@ def coarsest_triplets(B, M, N, r: int) -> TripletSet:
     Bd = engine.csr_to_dense(A)
     Mdd = engine.csr_to_dense(Md)
     Ndd = engine.csr_to_dense(Nd)
-    U, V, s = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r)
-    return TripletSet(s, U, V)
+    U, V, s, Z = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r, with_pinv=True)
+    trips = TripletSet(s, U, V)
+    # B's pseudo-inverse from the same factors (large path): the V-cycle takes
+    # it instead of factorising B again (solver.VCycleOperator)
+    trips.coarse_pinv = Z
+    return trips
 
 
 def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inhomogeneous: bool):
@@ -313,6 +324,12 @@ def _operator_degenerate(Bc: DeviceCSR) -> bool:
         print(f"[bamg] galerkin n_c={Bc.shape[0]} nnz={Bc.nnz} nonpositive_diag={bad} "
               f"limit={SICK_DIAG_FRACTION * Bc.shape[0]:.1f}", file=sys.stderr, flush=True)
     return bad > SICK_DIAG_FRACTION * Bc.shape[0]
+
+
+def _coarsest_level(depth, A, ops, Md, Nd, ranks, trips: TripletSet) -> Level:
+    lev = Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)
+    lev.coarse_pinv = getattr(trips, "coarse_pinv", None)
+    return lev
 
 
 def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None, depth: int = 0,
@@ -348,7 +365,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             print(f"[bamg] coarsest level {depth} n={n}", file=sys.stderr, flush=True)
         with _phase("coarsest"):
             trips = coarsest_triplets(A, Md, Nd, trips.r)
-        return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
+        return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
 
     with _phase("smooth"):
         _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
@@ -374,7 +391,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
                 print(f"[bamg] truncated at level {depth} n={n} (sick Galerkin product)", file=sys.stderr, flush=True)
             with _phase("coarsest"):
                 trips = coarsest_triplets(A, Md, Nd, trips.r)
-            return [Level(depth, A, ops.d, Md, Nd, geometry=ranks, Bt=ops.Bt)], trips
+            return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
         with _phase("galerkin"):
             # identity masses (the finest level): scipy's Q@I / I@P store every
             # row reversed, so (Q I) W and P^T (I P) are the products with Q's /

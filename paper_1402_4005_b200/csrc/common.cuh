@@ -91,6 +91,7 @@ struct bamg_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int64_t launches = 0;
+  int64_t syncs = 0;  // host waits on the stream (small D2H reads, bamg_sync)
   std::string err;
   Arena arena;
   double* pinned = nullptr;  // small pinned host staging buffer

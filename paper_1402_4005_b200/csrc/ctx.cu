@@ -46,13 +46,21 @@ extern "C" const char* bamg_last_error(bamg_ctx* ctx) { return ctx ? ctx->err.c_
 
 extern "C" int64_t bamg_launch_count(bamg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+extern "C" int64_t bamg_sync_count(bamg_ctx* ctx) { return ctx ? ctx->syncs : 0; }
+
 extern "C" int bamg_sync(bamg_ctx* ctx) {
+  ctx->syncs++;
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 
 static int ctx_read_bytes(bamg_ctx* ctx, const void* dev, size_t bytes, void* host) {
   if (bytes == 0) return 0;
+  ctx->syncs++;
+  if (ctx->trace.on) {  // zero-length marker: the host waits here
+    trace_mark(ctx, "<host sync>");
+    trace_mark(ctx, nullptr);
+  }
   if (bytes > ctx->pinned_doubles * sizeof(double)) {
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -372,6 +380,27 @@ extern "C" int bamg_trace_enable(bamg_ctx* ctx, int on) {
 }
 
 // Writes "name total_ms count" lines (aggregated by kernel name) into buf.
+// Per-launch timeline "name<TAB>start_us<TAB>end_us" (relative to the first
+// traced event), in launch order: gaps between consecutive launches are
+// pipeline bubbles (host syncs, host-side work, launch latency).
+extern "C" int bamg_trace_timeline(bamg_ctx* ctx, char* buf, int64_t cap) {
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  KTrace& T = ctx->trace;
+  std::string out;
+  for (size_t i = 0; i + 1 < T.used; ++i) {
+    if (!T.name[i] || T.name[i + 1]) continue;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, T.ev[0], T.ev[i]);
+    cudaEventElapsedTime(&b, T.ev[0], T.ev[i + 1]);
+    out += std::string(T.name[i]) + "\t" + std::to_string(a * 1e3) + "\t" + std::to_string(b * 1e3) + "\n";
+  }
+  int64_t len = (int64_t)out.size();
+  if (len >= cap) len = cap - 1;
+  memcpy(buf, out.data(), len);
+  buf[len] = 0;
+  return 0;
+}
+
 extern "C" int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap) {
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   std::map<std::string, std::pair<double, int64_t>> agg;

@@ -924,10 +924,107 @@ __global__ void cm_interleave_kernel(const double* U, const double* V, const dou
   Vo[t] = sgn[j] < 0.0 ? -v : v;
 }
 
+// Row-major projection in place: Z[i][j] -= z_i gz_j + gy_i y_j - t z_i y_j
+__global__ void rm_project_kernel(double* __restrict__ Z, int n, const double* __restrict__ z,
+                                  const double* __restrict__ y, const double* __restrict__ gz,
+                                  const double* __restrict__ gy, const double* __restrict__ t) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  const int i = (int)(idx / n), j = (int)(idx % n);
+  Z[idx] = Z[idx] - z[i] * gz[j] - gy[i] * y[j] + t[0] * z[i] * y[j];
+}
+
+__global__ void sub_sq_kernel(const double* __restrict__ a, const double* __restrict__ b, int n, double* out) {
+  __shared__ double sh[32];
+  double s = 0.0, w = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = a[i] - b[i];
+    s += d * d;
+    w += b[i] * b[i];
+  }
+  s = bsum(s, sh);
+  w = bsum(w, sh);
+  if (threadIdx.x == 0) {
+    out[0] = sqrt(s);
+    out[1] = sqrt(w);
+  }
+}
+
+// The V-cycle's coarsest pseudo-inverse from the triplet solve's factors
+// (instead of a second bordered LU + inverse of B_L).  With B = L_M K L_N^T,
+// G = L_N^-T K^+ L_M^-1 satisfies B G B = B, and for any such {1}-inverse
+// B^+ = (B^+ B) G (B B^+) = (I - z z^T) G (I - y y^T), where z, y are the
+// unit right / left null vectors of B (z ~ L_N^-T b0, y ~ L_M^-T a0 from K's
+// null vectors b0, a0).  A full-rank K gives B^-1 = G directly.  Written
+// row-major into Z; certified like the bordered pseudo-inverse (|B z|,
+// |B^T y| at round-off, |B^+|_F |B|_F < 1e11) plus |B B^+ B x - B x| <=
+// 1e-10 |B x| for a pseudo-random x.  Returns 0 (Z valid) or 1.
+static int derived_pinv(bamg_ctx* ctx, const double* Bd, const double* LM, const double* LN, const double* Kp,
+                        double* T, int n, bool null_slot, const double* b0, const double* a0, double* Z,
+                        double* work) {
+  double *zz, *yy, *gz, *gy, *t, *out, *x, *w, *tt, *s2;
+  BAMG_TRY(arena_get(ctx, (size_t)n, &zz));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &yy));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &gz));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &gy));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &x));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &w));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &tt));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &s2));
+  BAMG_TRY(arena_get(ctx, 1, &t));
+  BAMG_TRY(arena_get(ctx, 8, &out));
+  const size_t nn = (size_t)n * n;
+  // T = L_N^-T K^+ ; Z = T^T ; Z = L_M^-T Z = (L_N^-T K^+ L_M^-1)^T column-major = G row-major
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(T, Kp, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_TRY(tri_solve(ctx, LN, n, true, false, true, T, n, n, work));
+  BAMG_TRY(transpose_sq(ctx, T, n, Z));
+  BAMG_TRY(tri_solve(ctx, LM, n, true, false, true, Z, n, n, work));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * 8, ctx->stream));
+  if (null_slot) {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(zz, b0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(yy, a0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_TRY(tri_solve(ctx, LN, n, true, false, true, zz, n, 1, work));
+    BAMG_TRY(tri_solve(ctx, LM, n, true, false, true, yy, n, 1, work));
+    BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, zz, n);
+    BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, yy, n);
+    // Z's memory is G^T column-major: gz = G^T z = Zcm z ; gy = G y = Zcm^T y
+    BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Z, n, zz, n, 0.0, gz, n));
+    BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, Z, n, yy, n, 0.0, gy, n));
+    BAMG_LAUNCH(ctx, dot1_kernel, 1, 1024, 0, zz, gy, n, t);
+    BAMG_LAUNCH(ctx, rm_project_kernel, grid_for((int64_t)nn, 256), 256, 0, Z, n, zz, yy, gz, gy, t);
+    // |B z|, |B^T y|
+    BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Bd, n, zz, n, 0.0, gz, n));
+    BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, Bd, n, yy, n, 0.0, gy, n));
+    BAMG_LAUNCH(ctx, frob2_kernel, 1, 256, 0, gz, (int64_t)n, out + 0);
+    BAMG_LAUNCH(ctx, frob2_kernel, 1, 256, 0, gy, (int64_t)n, out + 1);
+  }
+  BAMG_LAUNCH(ctx, frob2_kernel, 2 * ctx->num_sms, 256, 0, Bd, (int64_t)nn, out + 2);
+  BAMG_LAUNCH(ctx, frob2_kernel, 2 * ctx->num_sms, 256, 0, Z, (int64_t)nn, out + 3);
+  // consistency: B (B^+ (B x)) = B x
+  BAMG_LAUNCH(ctx, pseudo_random_kernel, grid_for(n, 256), 256, 0, x, (int64_t)n, 777u);
+  BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Bd, n, x, n, 0.0, w, n));
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, Z, n, w, n, 0.0, tt, n));  // row-major Z: B^+ w
+  BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Bd, n, tt, n, 0.0, s2, n));
+  BAMG_LAUNCH(ctx, sub_sq_kernel, 1, 1024, 0, s2, w, n, out + 4);
+  double h[6];
+  BAMG_TRY(ctx_read_doubles(ctx, out, 6, h));
+  const double bf = std::sqrt(h[2]), zf = std::sqrt(h[3]);
+  const double tol = 1e-13 * bf / std::sqrt((double)n);
+  const bool ok = (!null_slot || (std::sqrt(h[0]) <= tol && std::sqrt(h[1]) <= tol)) && zf * bf < 1e11 &&
+                  h[4] <= 1e-10 * h[5] && std::isfinite(zf);
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] derived pinv n=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e |B+|F|B|F=%.3e consistency=%.3e -> %s\n",
+            n, std::sqrt(h[0]), std::sqrt(h[1]), bf, zf * bf, h[4] / fmax(h[5], 1e-300), ok ? "certified" : "rejected");
+  return ok ? 0 : 1;
+}
+
 // Large-n coarsest triplets.  Md and Nd are overwritten by their Cholesky
-// factors (they are the caller's dense temporaries).
+// factors (they are the caller's dense temporaries).  With Zpinv non-null,
+// the V-cycle's pseudo-inverse of B is derived from the same factors
+// (derived_pinv) and *zvalid says whether it was certified.
 int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double* Nd, int n, int r, double* U,
-                            double* V, double* sigma) {
+                            double* V, double* sigma, double* Zpinv, int* zvalid) {
+  if (zvalid) *zvalid = 0;
   const size_t nn = (size_t)n * n;
   const int p = r + 12 < n ? r + 12 : n;
   double *K, *Kp, *Y, *Z, *Gs, *Ri, *tmp, *Vs, *sv, *work, *a0, *b0, *A, *Bv, *KB, *dots;
@@ -1104,6 +1201,12 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
   stage("finish");
+  if (Zpinv && zvalid) {
+    int zr = derived_pinv(ctx, Bd, Md, Nd, Kp, K, n, null_slot, b0, a0, Zpinv, work);
+    if (zr < 0) return zr;
+    *zvalid = zr == 0;
+    stage("derived_pinv");
+  }
   if (getenv("BAMG_DEBUG"))
     fprintf(stderr, "[bamg] large triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p, iters,
             r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);

@@ -278,14 +278,25 @@ def dense_pinv(Dcm, n, rank_tol=1e-12):
     return Z  # row-major pseudo-inverse
 
 
-def coarsest_triplets(Bd, Md, Nd, n, r):
+def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
+    """(U, V, sigma[, Z]): with `with_pinv`, Z is B's row-major pseudo-inverse
+    derived from the triplet solve's factors, or None when that path did not
+    run or was not certified (the caller then builds it with dense_pinv)."""
     take = min(r, n)
     U = _empty((n, take))
     V = _empty((n, take))
     s = _empty(take)
-    rc = _lib.call("bamg_coarsest_triplets", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s))
+    if with_pinv:
+        Z = _empty((n, n))
+        ok = C.c_int(0)
+        rc = _lib.call("bamg_coarsest_triplets_pinv", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s),
+                       _p(Z), C.byref(ok))
+    else:
+        rc = _lib.call("bamg_coarsest_triplets", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s))
     if rc == 2:
         raise ValueError("matrix is not positive definite (coarsest mass matrix)")
+    if with_pinv:
+        return U, V, s, (Z if ok.value else None)
     return U, V, s
 
 

@@ -88,6 +88,19 @@ def _gemv_rowmajor(Z, b):
     return y if isinstance(b, torch.Tensor) else y.cpu().numpy()
 
 
+class _DerivedPinv:
+    """Row-major coarsest pseudo-inverse handed over by the setup
+    (bamg_coarsest_triplets_pinv); the PinvOperator interface the V-cycle uses."""
+
+    def __init__(self, Z):
+        self.Z = Z
+        self.n = int(Z.shape[0])
+        self.shape = (self.n, self.n)
+
+    def apply(self, b):
+        return _gemv_rowmajor(self.Z, b)
+
+
 class VCycleOperator:
     """One V-cycle from a zero guess, pseudo-inverse on the coarsest level (solver.py:79-124)."""
 
@@ -111,7 +124,12 @@ class VCycleOperator:
                                              lev.dP.ref() if lev.dP is not None else None,
                                              lev.dQ.ref() if lev.dQ is not None else None),
                        "bamg_hier_set_level")
-        self._coarse = PinvOperator(hierarchy.coarsest.dB, rank_tol=coarsest_rank_tol)
+        Zc = getattr(hierarchy.coarsest, "coarse_pinv", None)
+        if Zc is not None and coarsest_rank_tol == 1e-12:
+            # certified B_L^+ derived from the setup's triplet factors (same operator)
+            self._coarse = _DerivedPinv(Zc)
+        else:
+            self._coarse = PinvOperator(hierarchy.coarsest.dB, rank_tol=coarsest_rank_tol)
         _lib.check(L.bamg_hier_set_coarsest(h, _lib.ptr(self._coarse.Z), self._coarse.n),
                    "bamg_hier_set_coarsest")
         sm = self.smoother
