@@ -69,6 +69,8 @@ int bamg_trace_enable(bamg_ctx* ctx, int on);
 int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap);
 /* Same trace as a per-launch timeline: "name start_us end_us" lines. */
 int bamg_trace_timeline(bamg_ctx* ctx, char* buf, int64_t cap);
+/* Number of trace events recorded so far (timeline phase markers). */
+int64_t bamg_trace_position(bamg_ctx* ctx);
 
 /* ------------------------------------------------------- sparse (sparse.py) */
 /* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;

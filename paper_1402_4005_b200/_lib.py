@@ -52,6 +52,7 @@ _SIGS = {
     "bamg_trace_enable": [P, C.c_int],
     "bamg_trace_dump": [P, C.c_char_p, I64],
     "bamg_trace_timeline": [P, C.c_char_p, I64],
+    "bamg_trace_position": [P],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
     "bamg_csr_transpose": [P, PCSR, P, P, P],
@@ -105,7 +106,8 @@ _SIGS = {
     "bamg_mupdate": [P, P, C.c_int, P, P, I64, P],
     "bamg_combine": [P, P, C.c_int, P, P, P, I64, P],
 }
-_RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64, "bamg_sync_count": C.c_int64}
+_RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64, "bamg_sync_count": C.c_int64,
+             "bamg_trace_position": C.c_int64}
 
 _lock = threading.Lock()
 _lib = None

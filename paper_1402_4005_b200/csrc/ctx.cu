@@ -392,7 +392,8 @@ extern "C" int bamg_trace_timeline(bamg_ctx* ctx, char* buf, int64_t cap) {
     float a = 0.f, b = 0.f;
     cudaEventElapsedTime(&a, T.ev[0], T.ev[i]);
     cudaEventElapsedTime(&b, T.ev[0], T.ev[i + 1]);
-    out += std::string(T.name[i]) + "\t" + std::to_string(a * 1e3) + "\t" + std::to_string(b * 1e3) + "\n";
+    out += std::string(T.name[i]) + "\t" + std::to_string(a * 1e3) + "\t" + std::to_string(b * 1e3) + "\t" +
+           std::to_string(i) + "\n";
   }
   int64_t len = (int64_t)out.size();
   if (len >= cap) len = cap - 1;
@@ -400,6 +401,9 @@ extern "C" int bamg_trace_timeline(bamg_ctx* ctx, char* buf, int64_t cap) {
   buf[len] = 0;
   return 0;
 }
+
+// Current trace position (events recorded so far): phase markers for the timeline.
+extern "C" int64_t bamg_trace_position(bamg_ctx* ctx) { return ctx ? (int64_t)ctx->trace.used : 0; }
 
 extern "C" int bamg_trace_dump(bamg_ctx* ctx, char* buf, int64_t cap) {
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

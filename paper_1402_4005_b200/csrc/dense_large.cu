@@ -52,8 +52,10 @@ static int gemm(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alp
   if (m <= 0 || n <= 0) return 0;
   cublasHandle_t h = cublas(ctx);
   BAMG_REQUIRE(ctx, h != nullptr, "cuBLAS handle creation failed");
+  if (ctx->trace.on) trace_mark(ctx, "cublasDgemm");
   cublasStatus_t st = cublasDgemm(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha,
                                   A, lda, B, ldb, &beta, C, ldc);
+  if (ctx->trace.on) trace_mark(ctx, nullptr);
   ctx->launches++;
   if (st != CUBLAS_STATUS_SUCCESS) {
     ctx->err = "cublasDgemm failed (" + std::to_string((int)st) + ")";
@@ -182,11 +184,114 @@ static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, dou
   return 0;
 }
 
+// One-launch triangular solve op(T) X = B for n <= TRSM_MAX_N: CTA b owns the
+// right-hand sides [TRSM_RB*b, TRSM_RB*b + TRSM_RB) staged in shared memory and
+// walks op(T) in 32-row diagonal blocks (forward for a lower op(T), backward
+// for an upper one).  Warp c solves its column's 32 x 32 diagonal block with
+// the block's entries preloaded in registers (lane i owns row i; the solved
+// entry is broadcast by a shuffle), then all 256 threads apply the block's
+// contribution to the remaining rows (32-term dot products, op(T) read from
+// L2, the solved entries broadcast from shared memory).  Replaces the blocked
+// path's ~4 launches per 64 rows (tri_inv + 2 GEMMs + copy) with one launch.
+constexpr int TRSM_MAX_N = 2048;
+constexpr int TRSM_RB = 8;
+__global__ void __launch_bounds__(256) trsm_small_kernel(const double* __restrict__ T, int n, int lower_stored,
+                                                         int unit, int trans, double* __restrict__ B, int ldb, int m) {
+  extern __shared__ double sX[];  // [TRSM_RB][n]
+  const int c0 = blockIdx.x * TRSM_RB;
+  const int mc = min(TRSM_RB, m - c0);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int t = tid; t < mc * n; t += blockDim.x) {
+    const int c = t / n, i = t - c * n;
+    sX[t] = B[(int64_t)(c0 + c) * ldb + i];
+  }
+  __syncthreads();
+  // op(T)(i, j): T(i, j) = T[j*n + i] (column-major), or T(j, i) when trans
+  auto opT = [&](int i, int j) -> double {
+    return trans ? __ldg(T + (int64_t)i * n + j) : __ldg(T + (int64_t)j * n + i);
+  };
+  const bool eff_lower = (lower_stored != 0) != (trans != 0);
+  const int nblk = (n + 31) / 32;
+  for (int s = 0; s < nblk; ++s) {
+    const int bk = eff_lower ? s : nblk - 1 - s;
+    const int k0 = bk * 32, kb = min(32, n - k0);
+    // ---- diagonal block, one warp per right-hand side
+    if (wid < mc) {
+      double* x = sX + (int64_t)wid * n + k0;
+      double row[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) row[j] = (lane < kb && j < kb) ? opT(k0 + lane, k0 + j) : 0.0;
+      double xi = lane < kb ? x[lane] : 0.0;
+      if (eff_lower) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < kb) {
+            if (lane == j && !unit) xi = xi / row[j];
+            const double xj = __shfl_sync(0xffffffffu, xi, j);
+            if (lane > j) xi -= row[j] * xj;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (j < kb) {
+            if (lane == j && !unit) xi = xi / row[j];
+            const double xj = __shfl_sync(0xffffffffu, xi, j);
+            if (lane < j) xi -= row[j] * xj;
+          }
+        }
+      }
+      if (lane < kb) x[lane] = xi;
+    }
+    __syncthreads();
+    // ---- remaining rows: below the block (lower) or above it (upper)
+    const int r0 = eff_lower ? k0 + kb : 0;
+    const int rn = eff_lower ? n - r0 : k0;
+    for (int t = tid; t < rn * mc; t += blockDim.x) {
+      const int c = t / rn, i = r0 + (t - c * rn);
+      const double* xb = sX + (int64_t)c * n + k0;
+      double acc = 0.0;
+      if (trans) {
+        const double* tr = T + (int64_t)i * n + k0;  // op(T)(i, k0 + j) = T[i*n + k0 + j]
+        for (int j = 0; j < kb; ++j) acc += __ldg(tr + j) * xb[j];
+      } else {
+        for (int j = 0; j < kb; ++j) acc += __ldg(T + (int64_t)(k0 + j) * n + i) * xb[j];
+      }
+      sX[(int64_t)c * n + i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < mc * n; t += blockDim.x) {
+    const int c = t / n, i = t - c * n;
+    B[(int64_t)(c0 + c) * ldb + i] = sX[t];
+  }
+}
+
+static bool trsm_small_enabled() {
+  const char* e = getenv("BAMG_TRSM_BLOCKED");  // development: force the blocked path
+  return !(e && e[0] == '1');
+}
+
 // Blocked triangular solve op(T) X = B in place on B (n x m, ldb).  T is the
 // n x n column-major factor: lower (unit or not) or, with `upper`, the upper
 // triangle; `trans` solves with T^T (a lower T^T is upper).
 static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, bool unit, bool trans, double* B,
                      int ldb, int m, double* work /* NB*NB + NB*m */) {
+  // one launch wins when there are enough right-hand sides to fill the GPU
+  // and the 32-row sweep is short (measured: n = 256, m = 256; the blocked
+  // GEMM path wins at n = 1024 or for a handful of columns)
+  if (n <= 512 && m >= 32 && trsm_small_enabled()) {
+    static bool attr = false;
+    if (!attr) {
+      BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(trsm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TRSM_RB * TRSM_MAX_N * (int)sizeof(double)));
+      attr = true;
+    }
+    const size_t smem = (size_t)TRSM_RB * n * sizeof(double);
+    BAMG_LAUNCH(ctx, trsm_small_kernel, (m + TRSM_RB - 1) / TRSM_RB, 256, smem, T, n, (int)lower_stored, (int)unit,
+                (int)trans, B, ldb, m);
+    return 0;
+  }
   double* Ti = work;
   double* tmp = work + NB * NB;
   // effective shape of op(T): lower if (lower_stored xor trans)
@@ -449,6 +554,143 @@ __global__ void __launch_bounds__(1024) panel_lu_smem_kernel(double* A, int n, i
   }
 }
 
+// Panel factorisation for panels larger than one CTA's shared memory: a
+// thread-block cluster of CS CTAs holds the panel A[j0:n, j0:j0+jb] in its
+// distributed shared memory, CTA c owning the contiguous rows
+// [c*R, c*R + R) (column-major, ld R).  Per column: local argmax, one cluster
+// barrier, every CTA picks the same pivot from the CS candidates (read over
+// DSMEM), the two owners exchange the swapped rows through DSMEM, and every
+// CTA copies the pivot row once and updates its own rows.  Three cluster
+// barriers per column instead of three grid barriers; same pivot rule as the
+// other panel kernels (max |a|, first index on ties).
+constexpr int CL_PANEL_NB = 64;
+__global__ void __launch_bounds__(1024) panel_lu_cluster_kernel(double* A, int n, int j0, int jb, int R, int* piv,
+                                                                int* bad) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sP[];
+  __shared__ double wb[32];
+  __shared__ int wi[32];
+  __shared__ double s_best[2];
+  __shared__ int s_bidx[2];
+  __shared__ int s_p;
+  __shared__ double s_prow[CL_PANEL_NB];
+  __shared__ double s_in[CL_PANEL_NB];
+  __shared__ double s_l[1];
+  const int CS = (int)cl.num_blocks(), c = (int)cl.block_rank();
+  const int rows = n - j0;
+  const int r0 = c * R;
+  const int rn = max(0, min(R, rows - r0));
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int t = tid; t < R * jb; t += blockDim.x) {
+    const int col = t / R, r = t - col * R;
+    sP[t] = r < rn ? A[(int64_t)(j0 + col) * n + j0 + r0 + r] : 0.0;
+  }
+  __syncthreads();
+  for (int jj = 0; jj < jb; ++jj) {
+    const int par = jj & 1;
+    double* colp = sP + (int64_t)jj * R;
+    double best = -1.0;
+    int bi = rows;  // panel-relative row index
+    for (int r = max(0, jj - r0) + tid; r < rn; r += blockDim.x) {
+      const double a = fabs(colp[r]);
+      if (a > best) {
+        best = a;
+        bi = r0 + r;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      wb[wid] = best;
+      wi[wid] = bi;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      best = lane < nw ? wb[lane] : -1.0;
+      bi = lane < nw ? wi[lane] : rows;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_best[par] = best;
+        s_bidx[par] = bi;
+      }
+    }
+    cl.sync();  // (A) every CTA's candidate is published
+    if (wid == 0) {
+      best = -1.0;
+      bi = rows;
+      if (lane < CS) {
+        best = *cl.map_shared_rank(&s_best[par], lane);
+        bi = *cl.map_shared_rank(&s_bidx[par], lane);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        if (c == 0) {
+          piv[j0 + jj] = j0 + bi;
+          if (!(best > 0.0)) *bad = 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const int oj = jj / R, op = p / R;
+    if (p != jj) {  // uniform across the cluster
+      if (c == oj && tid < jb) s_in[tid] = *cl.map_shared_rank(sP + (int64_t)tid * R + (p - op * R), op);
+      if (c == op && oj != op && tid < jb) s_prow[tid] = *cl.map_shared_rank(sP + (int64_t)tid * R + (jj - oj * R), oj);
+      if (c == op && oj == op && tid < jb) s_prow[tid] = sP[(int64_t)tid * R + (jj - oj * R)];
+      cl.sync();  // (B) both rows read before either is overwritten
+      if (c == oj && tid < jb) sP[(int64_t)tid * R + (jj - oj * R)] = s_in[tid];
+      if (c == op && tid < jb) sP[(int64_t)tid * R + (p - op * R)] = s_prow[tid];
+    }
+    cl.sync();  // (C) the swapped rows are visible cluster-wide
+    if (tid < jb && tid >= jj) s_prow[tid] = *cl.map_shared_rank(sP + (int64_t)tid * R + (jj - oj * R), oj);
+    __syncthreads();
+    const double d = s_prow[jj];
+    const double dd = d != 0.0 ? d : 1.0;
+    const int rs = max(0, jj + 1 - r0);  // first local row below the pivot
+    for (int r = rs + tid; r < rn; r += blockDim.x) colp[r] = colp[r] / dd;
+    __syncthreads();
+    const int mr = rn - rs, mc = jb - jj - 1;
+    for (int t = tid; t < mr * mc; t += blockDim.x) {
+      const int cc = jj + 1 + t / mr, r = rs + t % mr;
+      sP[(int64_t)cc * R + r] -= colp[r] * s_prow[cc];
+    }
+    __syncthreads();
+  }
+  (void)s_l;
+  for (int t = tid; t < R * jb; t += blockDim.x) {
+    const int col = t / R, r = t - col * R;
+    if (r < rn) A[(int64_t)(j0 + col) * n + j0 + r0 + r] = sP[t];
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+static size_t panel_smem_max() {
+  const char* e = getenv("BAMG_PANEL_SMEM");  // tests: force the cluster path on small panels
+  size_t v = e ? (size_t)atol(e) : (size_t)PANEL_SMEM_MAX;
+  return v < 1024 ? 1024 : (v > (size_t)PANEL_SMEM_MAX ? (size_t)PANEL_SMEM_MAX : v);
+}
+
 // apply the panel's row interchanges to columns outside [j0, j0+jb)
 __global__ void apply_swaps_kernel(double* A, int n, int j0, int jb, const int* piv) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -481,11 +723,40 @@ static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, doubl
                                               PANEL_SMEM_MAX));
     smem_attr = true;
   }
+  static bool cl_attr = false;
+  if (!cl_attr) {
+    BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(panel_lu_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              PANEL_SMEM_MAX));
+    cl_attr = true;
+  }
+  const size_t smax = panel_smem_max();
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
-    const size_t panel_bytes = (size_t)(n - j0) * jb * sizeof(double);
-    if (panel_bytes <= (size_t)PANEL_SMEM_MAX) {
+    const int rows = n - j0;
+    const size_t panel_bytes = (size_t)rows * jb * sizeof(double);
+    const int cs = (int)((panel_bytes + smax - 1) / smax);
+    if (panel_bytes <= smax) {
       BAMG_LAUNCH(ctx, panel_lu_smem_kernel, 1, 1024, panel_bytes, A, n, j0, jb, piv, bad);
+    } else if (cs <= 8) {
+      // thread-block cluster of cs CTAs, the panel spread over their shared memory
+      int R = (rows + cs - 1) / cs;
+      const size_t smem = (size_t)R * jb * sizeof(double);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (ctx->trace.on) trace_mark(ctx, "panel_lu_cluster_kernel");
+      BAMG_CHECK_CUDA(ctx, cudaLaunchKernelEx(&cfg, panel_lu_cluster_kernel, A, n, j0, jb, R, piv, bad));
+      ctx->launches++;
+      if (ctx->trace.on) trace_mark(ctx, nullptr);
     } else {
       int want = (n - j0 + 255) / 256;
       int g = want < pgrid ? (want < 1 ? 1 : want) : pgrid;
@@ -810,6 +1081,40 @@ __global__ void __launch_bounds__(256) small_chol_inv_kernel(const double* __res
     for (int t = tid; t < p; t += blockDim.x) rdiag[t] = R[t * p + t];
 }
 
+// In-place Cholesky G = L L^T of a P x P block held row-major in shared
+// memory (row stride P + 1, lane i owns row i), by one warp, left-looking:
+// at step j lane i >= j forms its dot product of row i with row j over the
+// finished columns k < j (independent shared-memory loads, two accumulators),
+// lane j takes the square root, the others divide.  The dependent chain per
+// step is one dot product + sqrt/divide (a right-looking sweep serialises
+// P^2 / 2 read-modify-writes).  sRd[j] = 1 / L_jj.
+template <int P>
+__device__ __forceinline__ void warp_chol_smem(double* sL, double* sRd, int lane) {
+  constexpr int LD = P + 1;
+  for (int j = 0; j < P; ++j) {
+    double s0 = 0.0, s1 = 0.0;
+    if (lane >= j && lane < P) {
+      const double* ri = sL + lane * LD;
+      const double* rj = sL + j * LD;
+      int k = 0;
+      for (; k + 1 < j; k += 2) {
+        s0 += ri[k] * rj[k];
+        s1 += ri[k + 1] * rj[k + 1];
+      }
+      if (k < j) s0 += ri[k] * rj[k];
+    }
+    const double v = (lane >= j && lane < P) ? sL[lane * LD + j] - (s0 + s1) : 0.0;
+    const double djj = fmax(__shfl_sync(0xffffffffu, v, j), 1e-300);
+    const double ljj = sqrt(djj), inv = 1.0 / ljj;
+    if (lane > j && lane < P) sL[lane * LD + j] = v * inv;
+    if (lane == j) {
+      sL[j * LD + j] = ljj;
+      sRd[j] = inv;
+    }
+    __syncwarp();
+  }
+}
+
 // Fused CholQR step for p in {16, 20, 24, 28, 32}: every CTA factors the p x p Gram matrix
 // G = L L^T in one warp (lane i holds row i in registers, the column of L
 // being eliminated is broadcast by shuffles), publishes L and 1/diag(L) in
@@ -826,25 +1131,7 @@ __global__ void __launch_bounds__(256) cholqr_apply_kernel(const double* __restr
     if (lane < P)
       for (int j = 0; j < P; ++j) sA[lane * (P + 1) + j] = G[(int64_t)j * P + lane];
     __syncwarp();
-    double* row = sA + lane * (P + 1);
-#pragma unroll 1
-    for (int j = 0; j < P; ++j) {
-      const double djj = fmax(sA[j * (P + 1) + j], 1e-300);  // as small_chol_inv_kernel
-      const double ljj = sqrt(djj), inv = 1.0 / ljj;
-      __syncwarp();
-      double lij = 0.0;
-      if (lane > j && lane < P) {
-        lij = row[j] * inv;
-        row[j] = lij;
-      } else if (lane == j) {
-        row[j] = ljj;
-        sRd[j] = inv;
-      }
-      __syncwarp();
-      if (lane > j && lane < P)
-        for (int t = j + 1; t <= lane; ++t) row[t] -= lij * sA[t * (P + 1) + j];
-      __syncwarp();
-    }
+    warp_chol_smem<P>(sA, sRd, lane);
   }
   __syncthreads();
   // one row per thread and no row loop: a loop would let the compiler hoist
@@ -891,6 +1178,133 @@ static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, dou
 }
 
 int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig);
+
+// ---------------------------------------------- fused subspace iteration
+// `iters` steps of the block subspace iteration  Z = orth(K^+T Y),
+// Y = orth(K^+ Z)  in ONE cooperative launch (n <= SUB_MAX_N, p <= 32):
+//  * products: warp per output row; with Kt = (K^+)^T stored column-major,
+//    row j of K^+T is column j of K^+ and row i of K^+ is column i of Kt, so
+//    both products read contiguous columns; lane l accumulates the p dot
+//    products over i = l (mod 32), then a warp tree;
+//  * CholQR2 (twice per orthonormalisation, as orthonormalize()): per-CTA
+//    partial Gram matrices over contiguous row chunks, a fixed-order reduction
+//    (CTA b sums entries b, b + grid, ... over the partials), every CTA then
+//    factors G = L L^T in one warp (as cholqr_apply_kernel) and applies
+//    Y <- Y L^-T to its rows.
+// Three grid barriers per CholQR pass, one per product: ~13 per step instead
+// of ~10 launches (6 cuBLAS GEMMs) per step.
+constexpr int SUB_MAX_N = 512;
+constexpr int SUB_THREADS = 256;
+
+template <int P>
+__device__ void sub_product(const double* __restrict__ Mcols, int n, const double* __restrict__ X,
+                            double* __restrict__ Out) {
+  // Out[j][c] = sum_i Mcols[j*n + i] X[c*n + i]
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int j = gw; j < n; j += nwarp) {
+    double acc[P];
+#pragma unroll
+    for (int c = 0; c < P; ++c) acc[c] = 0.0;
+    const double* col = Mcols + (int64_t)j * n;
+    for (int i = lane; i < n; i += 32) {
+      const double m = __ldg(col + i);
+#pragma unroll
+      for (int c = 0; c < P; ++c) acc[c] += m * __ldcg(X + (int64_t)c * n + i);
+    }
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      double v = acc[c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == c) Out[(int64_t)c * n + j] = v;
+    }
+  }
+}
+
+template <int P>
+__device__ void sub_cholqr_pass(cg::grid_group& grid, double* Y, int n, double* partial, double* G, double* sL,
+                                double* sRd) {
+  const int tid = threadIdx.x;
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+  constexpr int PP = P * P;
+  // partial Gram of this CTA's rows (fixed order within the CTA)
+  for (int e = tid; e < PP; e += blockDim.x) {
+    const int a = e % P, b = e / P;
+    double v = 0.0;
+    if (a <= b)
+      for (int r = r0; r < r1; ++r) v += __ldcg(Y + (int64_t)a * n + r) * __ldcg(Y + (int64_t)b * n + r);
+    partial[(int64_t)blockIdx.x * PP + e] = v;
+  }
+  grid.sync();
+  // fixed-order reduction of the partials: one warp per entry, lanes stride
+  // over the CTAs' partials (independent loads), then a warp tree
+  {
+    const int lane = tid & 31;
+    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+    for (int e = gw; e < PP; e += nwarp) {
+      const int a = e % P, b = e / P;
+      double v = 0.0;
+      if (a <= b)
+        for (int q = lane; q < (int)gridDim.x; q += 32) v += __ldcg(partial + (int64_t)q * PP + e);
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) G[e] = v;
+    }
+  }
+  grid.sync();
+  // every CTA: G = L L^T in one warp with the rows in registers (lane i owns
+  // row i; column j's multipliers are broadcast by shuffles), then Y <- Y L^-T
+  if (tid < 32) {
+    const int lane = tid;
+    if (lane < P)
+      for (int j = 0; j < P; ++j) {
+        const int lo = lane < j ? lane : j, hi = lane < j ? j : lane;  // G is upper-stored
+        sL[lane * (P + 1) + j] = __ldcg(G + (int64_t)hi * P + lo);
+      }
+    __syncwarp();
+    warp_chol_smem<P>(sL, sRd, lane);
+  }
+  __syncthreads();
+  for (int r = r0 + tid; r < r1; r += blockDim.x) {
+    double x[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) x[i] = __ldcg(Y + (int64_t)i * n + r);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      x[j] *= sRd[j];
+#pragma unroll
+      for (int i = j + 1; i < P; ++i) x[i] -= sL[i * (P + 1) + j] * x[j];
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) Y[(int64_t)i * n + r] = x[i];
+  }
+  grid.sync();
+}
+
+template <int P>
+__global__ void __launch_bounds__(SUB_THREADS) subspace_coop_kernel(const double* __restrict__ Kp,
+                                                                    const double* __restrict__ Kt, int n, double* Y,
+                                                                    double* Z, int iters, double* partial,
+                                                                    double* G) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sL[P * (P + 1)];
+  __shared__ double sRd[P];
+  for (int it = 0; it < iters; ++it) {
+    sub_product<P>(Kp, n, Y, Z);  // Z = K^+T Y (row j of K^+T = column j of K^+)
+    grid.sync();
+    sub_cholqr_pass<P>(grid, Z, n, partial, G, sL, sRd);
+    sub_cholqr_pass<P>(grid, Z, n, partial, G, sL, sRd);
+    sub_product<P>(Kt, n, Z, Y);  // Y = K^+ Z (row i of K^+ = column i of Kt)
+    grid.sync();
+    sub_cholqr_pass<P>(grid, Y, n, partial, G, sL, sRd);
+    sub_cholqr_pass<P>(grid, Y, n, partial, G, sL, sRd);
+  }
+}
+
+static bool subspace_fused_enabled() {
+  const char* e = getenv("BAMG_SUBSPACE_GEMM");  // development: force the cuBLAS path
+  return !(e && e[0] == '1');
+}
 
 // column-major n x r block helpers for the large finish
 __global__ void cm_colnorm_scale_kernel(double* X, int n) {
@@ -1054,14 +1468,18 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   const bool timing = getenv("BAMG_DENSE_TIMING") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
   auto stage = [&](const char* name) {
+    if (ctx->trace.on) {  // zero-length timeline marker at the end of the stage
+      trace_mark(ctx, name);
+      trace_mark(ctx, nullptr);
+    }
     if (!timing) return;
     cudaStreamSynchronize(ctx->stream);
     auto t = std::chrono::steady_clock::now();
-    fprintf(stderr, "[bamg dense] n=%d %-10s %8.3f ms\n", n, name,
+    fprintf(stderr, "[bamg dense] n=%d %-10s %8.3f ms\n", n, name + 1,
             std::chrono::duration<double, std::milli>(t - t_last).count());
     t_last = t;
   };
-  stage("start");
+  stage("@start");
   BAMG_TRY(cholesky_blocked(ctx, Md, n, bad, work));
   BAMG_TRY(cholesky_blocked(ctx, Nd, n, bad, work));
   int hb = 0;
@@ -1070,7 +1488,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     ctx->err = "mass matrix is not positive definite (Cholesky pivot <= 0)";
     return 2;
   }
-  stage("cholesky");
+  stage("@cholesky");
   // K = L_M^-1 B L_N^-T :  T = L_M^-1 B ; K^T = L_N^-1 T^T
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(K, Bd, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
   BAMG_TRY(tri_solve(ctx, Md, n, true, false, false, K, n, n, work));
@@ -1080,7 +1498,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   // K^+ (column-major into Kp) and the exact null triplet (K b0 = 0, a0^T K = 0);
   // a nonsingular K (chains whose coarse column sums drifted) takes K^-1 and
   // all r slots from the subspace iteration
-  stage("K");
+  stage("@K");
   int rc = large_bordered_pinv(ctx, K, n, Kp, 0, b0, a0);
   if (rc < 0) return rc;
   const bool null_slot = rc == 0;
@@ -1092,16 +1510,18 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
       return -2;
     }
   }
-  stage("pinv");
+  stage("@pinv");
   // block subspace iteration on K^+ : Z = orth(K^+^T Y), Y = orth(K^+ Z)
   BAMG_LAUNCH(ctx, pseudo_random_kernel, grid_for((int64_t)n * p, 256), 256, 0, Y, (int64_t)n * p, 12345u);
   BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
   // convergence: every 5 iterations, the Ritz values of K^+ on the current
   // subspace (one-CTA Jacobi SVD of the n x p block when it fits in shared
-  // memory) must agree with the previous check to 1e-14 relative.  The first
-  // 5-iteration block runs eagerly; the block is then captured once as a CUDA
-  // graph (cuBLAS GEMMs included) and replayed, so the host launches one graph
-  // per check instead of ~70 kernels.
+  // memory; one-sided Jacobi keeps the small ones relatively accurate) must
+  // agree with the previous check to 1e-14 relative.  (The singular values of
+  // the p x p projection Z^T K^+ Y are only accurate to eps |K^+| and never
+  // settle at this tolerance.)  The first 5-iteration block runs eagerly; the
+  // block is then captured once as a CUDA graph (cuBLAS GEMMs included) and
+  // replayed, so the host launches one graph per check instead of ~50 kernels.
   auto block5 = [&]() -> int {
     for (int it = 0; it < 5; ++it) {
       BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
@@ -1112,13 +1532,53 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
     return jacobi_svd_public(ctx, Z, n, p, Vs, sv);
   };
+  // fused path: one cooperative launch per 5 steps, then the same check
+  const void* sub_kern = nullptr;
+  switch (p) {  // p = r + 12 for the usual test-vector counts r = 4, 8, 12, 16, 20
+    case 16: sub_kern = (const void*)subspace_coop_kernel<16>; break;
+    case 20: sub_kern = (const void*)subspace_coop_kernel<20>; break;
+    case 24: sub_kern = (const void*)subspace_coop_kernel<24>; break;
+    case 28: sub_kern = (const void*)subspace_coop_kernel<28>; break;
+    case 32: sub_kern = (const void*)subspace_coop_kernel<32>; break;
+    default: break;
+  }
+  // measured: ~3% faster than the graph-replayed cuBLAS path at n = 256,
+  // ~3% slower at n = 1024 (both latency-bound: ~13 grid barriers per step)
+  const bool fused = n <= SUB_MAX_N && sub_kern && subspace_fused_enabled();
+  double *Kt = nullptr, *partial = nullptr, *Gsum = nullptr;
+  int sub_grid = 0;
+  if (fused) {
+    int per_sm = 0;
+    BAMG_CHECK_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sub_kern, SUB_THREADS, 0));
+    sub_grid = ctx->num_sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
+    BAMG_TRY(arena_get(ctx, nn, &Kt));
+    BAMG_TRY(arena_get(ctx, (size_t)sub_grid * p * p, &partial));
+    BAMG_TRY(arena_get(ctx, (size_t)p * p, &Gsum));
+    BAMG_TRY(transpose_sq(ctx, Kp, n, Kt));
+  }
+  auto block5_fused = [&]() -> int {
+    int five = 5;
+    void* args[] = {&Kp, &Kt, (void*)&n, &Y, &Z, &five, &partial, &Gsum};
+    if (ctx->trace.on) trace_mark(ctx, "subspace_coop_kernel");
+    BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel(sub_kern, dim3(sub_grid), dim3(SUB_THREADS), args, 0,
+                                                     ctx->stream));
+    ctx->launches++;
+    if (ctx->trace.on) trace_mark(ctx, nullptr);
+    stage("@sub_kernel");
+    BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+    int rc = jacobi_svd_public(ctx, Z, n, p, Vs, sv);
+    stage("@sub_check");
+    return rc;
+  };
   std::vector<double> prev(p, 0.0), cur(p, 0.0);
   int iters = 0;
   cudaGraphExec_t gexec = nullptr;
   int64_t gk = 0;
   const bool use_graph = !ctx->trace.on && !getenv("BAMG_NO_GRAPHS") && !getenv("BAMG_DEBUG");
   for (int blk = 0; blk < 100; ++blk) {
-    if (blk == 0 || !use_graph) {
+    if (fused) {
+      BAMG_TRY(block5_fused());
+    } else if (blk == 0 || !use_graph) {
       BAMG_TRY(block5());
     } else {
       if (!gexec) {
@@ -1159,7 +1619,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   }
   if (gexec) cudaGraphExecDestroy(gexec);
   if (timing) fprintf(stderr, "[bamg dense] n=%d p=%d subspace iterations %d\n", n, p, iters);
-  stage("subspace");
+  stage("@subspace");
   // Rayleigh-Ritz: G = K^+^T Y, Jacobi: G Vs = W diag(s); K's left vectors
   // are W's columns, right vectors Y Vs
   BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
@@ -1189,7 +1649,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
   BAMG_REQUIRE(ctx, ntiny <= 1, "large coarsest operator has more than one numerically-null triplet");
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
-  stage("ritz");
+  stage("@ritz");
   // unit a, b  ->  u = L_M^-T a, v = L_N^-T b are M- / N-normalised
   BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, A, n);
   BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, Bv, n);
@@ -1200,12 +1660,12 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   BAMG_TRY(tri_solve(ctx, Nd, n, true, false, true, Bv, n, r, work));
   BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
-  stage("finish");
+  stage("@finish");
   if (Zpinv && zvalid) {
     int zr = derived_pinv(ctx, Bd, Md, Nd, Kp, K, n, null_slot, b0, a0, Zpinv, work);
     if (zr < 0) return zr;
     *zvalid = zr == 0;
-    stage("derived_pinv");
+    stage("@derived_pinv");
   }
   if (getenv("BAMG_DEBUG"))
     fprintf(stderr, "[bamg] large triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p, iters,

@@ -120,15 +120,20 @@ def test_gmres_matches(runs, name):
     assert np.abs(x - g["x"]).sum() <= 1e-8
 
 
+@pytest.mark.parametrize("panel_smem", [None, "8192"])
 @pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_uniform63", "pipe_tandem32_k16_r30",
                                   "pipe_petri10_normal"])
-def test_large_coarsest_path_matches(golden, name, monkeypatch):
-    """The blocked-LU / subspace-iteration coarsest path (used for n_L > 1536,
-    e.g. cfg4's n_L = 16,384) forced on small coarsest levels: same x0, x and
-    iteration count as the reference."""
+def test_large_coarsest_path_matches(golden, name, panel_smem, monkeypatch):
+    """The blocked-LU / subspace-iteration coarsest path (used for n_L >= 128,
+    e.g. cfg1's 256 and cfg4's 16,384) forced on small coarsest levels: same
+    x0, x and iteration count as the reference.  panel_smem = 8192 forces the
+    thread-block-cluster panel LU (panel spread over 5 CTAs' shared memory);
+    the V-cycle takes the pseudo-inverse derived from the triplet factors."""
     from paper_1402_4005_b200 import GmresConfig, VCycleOperator, gmres, run_setup
-    from paper_1402_4005_b200.solver import _sign_fix_l1
+    from paper_1402_4005_b200.solver import _DerivedPinv, _sign_fix_l1
     monkeypatch.setenv("BAMG_DENSE_LARGE_N", "16")
+    if panel_smem:
+        monkeypatch.setenv("BAMG_PANEL_SMEM", panel_smem)
     g = golden(name)
     prob = _problem(g)
     cfg = _setup_cfg(g)
@@ -137,6 +142,7 @@ def test_large_coarsest_path_matches(golden, name, monkeypatch):
     setup = run_setup(prob, cfg, draws=draws)
     assert np.abs(setup.x0 - g["x0"]).sum() <= 1e-9
     vop = VCycleOperator(setup.hierarchy, cfg.smoother)
+    assert isinstance(vop._coarse, _DerivedPinv)
     got = vop.apply(g["vcycle_in"])
     assert _close(got, g["vcycle_out"], 1e-9)
     restart, max_iters, rtol = gmres_args(g)
@@ -144,6 +150,12 @@ def test_large_coarsest_path_matches(golden, name, monkeypatch):
                 precond=vop)
     assert abs(rep.iterations - int(g["iterations"])) <= max(1, int(0.1 * int(g["iterations"])))
     assert np.abs(_sign_fix_l1(rep.x) - g["x"]).sum() <= 1e-8
+    # the derived coarsest pseudo-inverse equals the directly factorised one
+    from paper_1402_4005_b200 import PinvOperator
+    direct = PinvOperator(setup.hierarchy.coarsest.dB)
+    zd = vop._coarse.Z.cpu().numpy()
+    zr = direct.Z.cpu().numpy()
+    assert np.abs(zd - zr).max() <= 1e-9 * np.abs(zr).max()
     # the smallest singular values of the coarsest problem agree with the small path
     monkeypatch.setenv("BAMG_DENSE_LARGE_N", "100000")
     ref = run_setup(prob, cfg, draws=draws)

@@ -53,7 +53,7 @@ marks = []  # (phase, entering, engine launch count)
 
 
 def rec(name, entering):
-    marks.append((name, entering, int(L.bamg_launch_count(c))))
+    marks.append((name, entering, int(L.bamg_trace_position(c))))
 
 
 def step():
@@ -82,7 +82,6 @@ L.bamg_trace_enable(c, 1)
 torch.cuda.synchronize()
 marks.clear()
 bs.RECORDER = rec
-lc0 = int(L.bamg_launch_count(c))
 t0 = time.perf_counter()
 step()
 torch.cuda.synchronize()
@@ -93,7 +92,13 @@ L.bamg_trace_timeline(c, buf, 16 << 20)
 L.bamg_trace_enable(c, 0)
 rows = [r.split("\t") for r in buf.value.decode().splitlines()]
 ev = [(r[0], float(r[1]), float(r[2])) for r in rows]
-busy = sum(e - s for n, s, e in ev if n != "<host sync>")
+evpos = [int(r[3]) for r in rows]  # trace event index of each entry
+
+
+def marker(name):
+    return name.startswith("<") or name.startswith("@")
+
+busy = sum(e - s for n, s, e in ev if not marker(n))
 span = ev[-1][2] - ev[0][1]
 gaps = []
 idle_after = defaultdict(float)
@@ -114,32 +119,27 @@ for n, v in sorted(idle_after.items(), key=lambda kv: -kv[1])[:a.top]:
 
 # per phase: launches, kernel-busy, span (from the first launch to the first
 # launch after the phase), host syncs
-kern = [e for e in ev if e[0] != "<host sync>"]
-idx_of = []  # trace position of the i-th launch
-for i, e in enumerate(ev):
-    if e[0] != "<host sync>":
-        idx_of.append(i)
+import bisect
 stack, spans = [], defaultdict(lambda: [0, 0.0, 0.0, 0])
 per_kern = defaultdict(lambda: defaultdict(lambda: [0, 0.0]))
-for name, entering, lc in marks:
-    li = lc - lc0
+for name, entering, pos in marks:
     if entering:
-        stack.append((name, li))
+        stack.append((name, pos))
         continue
-    nm, l0 = stack.pop()
-    if l0 >= len(idx_of):
+    nm, p0 = stack.pop()
+    t0 = bisect.bisect_left(evpos, p0)
+    t1 = bisect.bisect_left(evpos, pos)
+    if t0 >= len(ev) or t1 <= t0:
         continue
-    t0 = idx_of[l0]
-    t1 = idx_of[li] if li < len(idx_of) else len(ev)
     seg = ev[t0:t1]
     sp = spans[nm]
-    sp[0] += sum(1 for e in seg if e[0] != "<host sync>")
-    sp[1] += sum(e[2] - e[1] for e in seg if e[0] != "<host sync>")
+    sp[0] += sum(1 for e in seg if not marker(e[0]))
+    sp[1] += sum(e[2] - e[1] for e in seg if not marker(e[0]))
     end = ev[t1][1] if t1 < len(ev) else ev[-1][2]
     sp[2] += end - ev[t0][1]
     sp[3] += sum(1 for e in seg if e[0] == "<host sync>")
     for e in seg:
-        if e[0] != "<host sync>":
+        if not marker(e[0]):
             pk = per_kern[nm][e[0]]
             pk[0] += 1
             pk[1] += e[2] - e[1]
@@ -150,3 +150,10 @@ for nm, (nl, busy_us, span_us, ns) in sorted(spans.items(), key=lambda kv: -kv[1
     print(f"\n[{nm}] top kernels")
     for kn, (cnt, us) in sorted(per_kern[nm].items(), key=lambda kv: -kv[1][1])[:8]:
         print(f"    {us / 1e3:8.3f} ms {cnt:5d}  {kn[:70]}")
+
+# dense coarsest stages (zero-length "@stage" markers at the end of each stage)
+st = [(e[0], e[1]) for e in ev if e[0].startswith("@")]
+if st:
+    print("\ncoarsest stages (ms since previous marker):")
+    for (a0, t0), (a1, t1) in zip(st, st[1:]):
+        print(f"  {a1[1:]:14s} {(t1 - t0) / 1e3:8.3f}")
