@@ -27,6 +27,7 @@ __device__ __forceinline__ unsigned long long order_key(double v) {
 
 __global__ void keys_init_kernel(const double* __restrict__ coord, int64_t n, unsigned long long* __restrict__ key,
                                  int32_t* __restrict__ idx, unsigned long long* orand) {
+  BAMG_PDL_PROLOGUE();
   __shared__ unsigned long long so[256], sa[256];
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long k = 0ull, a = ~0ull;
@@ -54,6 +55,7 @@ __global__ void keys_init_kernel(const double* __restrict__ coord, int64_t n, un
 
 __global__ void bit_flags_kernel(const unsigned long long* __restrict__ key, int64_t n, int bit,
                                  uint8_t* __restrict__ zero) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) zero[i] = ((key[i] >> bit) & 1ull) ? 0 : 1;
 }
@@ -61,6 +63,7 @@ __global__ void bit_flags_kernel(const unsigned long long* __restrict__ key, int
 __global__ void bit_scatter_kernel(const unsigned long long* __restrict__ key, const int32_t* __restrict__ idx,
                                    int64_t n, int bit, const int32_t* __restrict__ zpos,
                                    unsigned long long* __restrict__ key2, int32_t* __restrict__ idx2) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t nz = zpos[n];
@@ -71,12 +74,14 @@ __global__ void bit_scatter_kernel(const unsigned long long* __restrict__ key, c
 }
 
 __global__ void distinct_flags_kernel(const unsigned long long* __restrict__ key, int64_t n, uint8_t* __restrict__ f) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) f[i] = (i > 0 && key[i] != key[i - 1]) ? 1 : 0;
 }
 
 __global__ void rank_scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ pos, const uint8_t* __restrict__ f,
                                     int64_t n, int32_t* __restrict__ rank) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) rank[idx[i]] = pos[i] + f[i];  // inclusive count of "new value" flags
 }
@@ -119,12 +124,14 @@ extern "C" int bamg_axis_ranks(bamg_ctx* ctx, const double* coord, int64_t n, in
 
 __global__ void presence_kernel(const int32_t* __restrict__ prank, const int32_t* __restrict__ cidx, int64_t nc,
                                 uint8_t* __restrict__ present) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nc) present[prank[cidx[i]]] = 1;
 }
 
 __global__ void rerank_kernel(const int32_t* __restrict__ prank, const int32_t* __restrict__ cidx, int64_t nc,
                               const int32_t* __restrict__ pos, int32_t* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nc) out[i] = pos[prank[cidx[i]]];
 }
@@ -148,6 +155,7 @@ struct RankPtrs {
 };
 
 __global__ void even_mask_kernel(RankPtrs rp, int ndim, int64_t n, uint8_t* __restrict__ mask) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   bool ok = true;
@@ -165,6 +173,7 @@ extern "C" int bamg_even_mask(bamg_ctx* ctx, const int32_t* const* ranks_host, i
 
 __global__ void split_scatter_kernel(const uint8_t* __restrict__ mask, const int32_t* __restrict__ pos, int64_t n,
                                      int32_t* __restrict__ coarse, int32_t* __restrict__ fine, int32_t* __restrict__ crank) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t p = pos[i];
@@ -191,6 +200,7 @@ extern "C" int bamg_split_from_mask(bamg_ctx* ctx, const uint8_t* mask, int64_t 
 
 // ------------------------------------------------------ compatible relaxation
 __global__ void count_mask_kernel(const uint8_t* __restrict__ m, int64_t n, unsigned long long* cnt) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int e = (i < n) && m[i];
   int t = __syncthreads_count(e);
@@ -208,6 +218,7 @@ static int count_mask(bamg_ctx* ctx, const uint8_t* m, int64_t n, int64_t* out) 
 
 __global__ void cr_start_kernel(const uint8_t* __restrict__ cmask, const int32_t* __restrict__ fpos,
                                 const double* __restrict__ normals, int64_t n, double* __restrict__ x) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   x[i] = cmask[i] ? 0.0 : normals[i - fpos[i]];
@@ -216,6 +227,7 @@ __global__ void cr_start_kernel(const uint8_t* __restrict__ cmask, const int32_t
 // sum of x_f^2 over fine points (partials, fixed grid)
 __global__ void cr_rms_partial(const double* __restrict__ x, const uint8_t* __restrict__ cmask, int64_t n,
                                double* __restrict__ partial) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[RED_THREADS / 32];
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
@@ -233,6 +245,7 @@ __global__ void cr_rms_partial(const double* __restrict__ x, const uint8_t* __re
 }
 
 __global__ void cr_rms_final(const double* __restrict__ partial, int nb, int64_t nf, double* scale) {
+  BAMG_PDL_PROLOGUE();
   double v = 0.0;
   for (int b = threadIdx.x; b < nb; b += 32) v += partial[b];
   v = warp_sum(v);
@@ -240,16 +253,19 @@ __global__ void cr_rms_final(const double* __restrict__ partial, int nb, int64_t
 }
 
 __global__ void cr_scale_kernel(double* __restrict__ x, int64_t n, const double* __restrict__ scale) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = x[i] / scale[0];
 }
 
 __global__ void zero_where_kernel(double* __restrict__ x, const uint8_t* __restrict__ m, int64_t n) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && m[i]) x[i] = 0.0;
 }
 
 __global__ void dead_mask_kernel(const double* __restrict__ d, int64_t n, uint8_t* __restrict__ dead) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dead[i] = d[i] == 0.0;
 }
@@ -258,6 +274,7 @@ __global__ void dead_mask_kernel(const double* __restrict__ d, int64_t n, uint8_
 __global__ void cr_mu_kernel(const double* __restrict__ x, const uint8_t* __restrict__ cmask, int64_t n, double expo,
                              double thr, double* __restrict__ mu, uint8_t* __restrict__ state,
                              unsigned long long* __restrict__ ncand) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int c = 0;
   if (i < n) {
@@ -275,6 +292,7 @@ __global__ void cr_mu_kernel(const double* __restrict__ x, const uint8_t* __rest
 __global__ void mis_round_kernel(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
                                  const double* __restrict__ mu, volatile uint8_t* state, int* __restrict__ changed,
                                  int* __restrict__ undecided) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (state[i] != 0) return;
@@ -306,6 +324,7 @@ __global__ void mis_round_kernel(int64_t n, const int32_t* __restrict__ arp, con
 }
 
 __global__ void mis_commit_kernel(const uint8_t* __restrict__ state, int64_t n, uint8_t* __restrict__ cmask) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && state[i] == 1) cmask[i] = 1;
 }
@@ -313,6 +332,7 @@ __global__ void mis_commit_kernel(const uint8_t* __restrict__ state, int64_t n, 
 // fallback: coarse[argmax(where(fine, mu, -1))] = True
 __global__ void cr_fallback_kernel(const double* __restrict__ mu, const uint8_t* __restrict__ cmask, int64_t n,
                                    uint8_t* __restrict__ cmask_out) {
+  BAMG_PDL_PROLOGUE();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double best = -INFINITY;
   int64_t bi = 0;
@@ -384,6 +404,7 @@ extern "C" int bamg_cr_pass(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* ad
 }
 
 __global__ void empty_rows_kernel(const int32_t* __restrict__ rp, int64_t n, unsigned long long* cnt) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int e = (i < n) && (rp[i + 1] == rp[i]);
   int t = __syncthreads_count(e);

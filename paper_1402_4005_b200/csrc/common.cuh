@@ -6,7 +6,9 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/bamg_sm100.h"
@@ -163,12 +165,54 @@ static inline cudaEvent_t prof_event(bamg_ctx* ctx, int fam) {
     }                                                                           \
   } while (0)
 
+// Programmatic dependent launch (PDL).  Every engine kernel starts with
+// BAMG_PDL_PROLOGUE: griddepcontrol.wait blocks until the preceding grid in
+// the stream has completed and its writes are visible, so kernel bodies stay
+// strictly stream-ordered; launch_dependents then lets the NEXT launch be
+// scheduled while this grid runs.  With BAMG_LAUNCH's
+// ProgrammaticStreamSerialization attribute the launch latency of kernel i+1
+// (grid setup, CTA rasterisation) overlaps the tail of kernel i instead of
+// sitting in the ~1,700 serial kernel boundaries of a setup + solve.  Both
+// instructions are no-ops for kernels launched without the attribute.
+#define BAMG_PDL_PROLOGUE() \
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
+static inline bool bamg_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BAMG_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t bamg_launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                          cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Launch + accounting + immediate launch-error check.
 #define BAMG_LAUNCH(ctx, kernel, grid, block, smem, ...)                        \
   do {                                                                          \
     if ((grid) > 0) {                                                           \
       if ((ctx)->trace.on) trace_mark(ctx, #kernel);                            \
-      kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);          \
+      if (bamg_pdl_enabled()) {                                                 \
+        BAMG_CHECK_CUDA(ctx, bamg_launch_pdl(kernel, dim3(grid), dim3(block), (size_t)(smem), \
+                                             (ctx)->stream, __VA_ARGS__));     \
+      } else {                                                                  \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);        \
+      }                                                                         \
       (ctx)->launches++;                                                        \
       BAMG_CHECK_CUDA(ctx, cudaGetLastError());                                 \
       if ((ctx)->trace.on) trace_mark(ctx, nullptr);                            \

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(SCAN_THREADS)
 scan_onepass_kernel(const T* __restrict__ in, int64_t n, int32_t* __restrict__ out,
                     unsigned long long* __restrict__ state, unsigned int* __restrict__ counter,
                     int64_t* __restrict__ total) {
+  BAMG_PDL_PROLOGUE();
   __shared__ int64_t warp_tot[32];
   __shared__ int tile_s;
   __shared__ int64_t excl_s;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(RED_THREADS)
 colreduce_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t n, int k, int kind,
                  double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ out,
                  int take_sqrt) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[RED_THREADS / 32][KMAX];
   __shared__ bool last;
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -274,6 +276,7 @@ extern "C" int bamg_col_dots(bamg_ctx* ctx, const double* X, const double* Y, in
 }
 
 __global__ void col_scale_div_kernel(double* X, int64_t total, int k, const double* s) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   double d = s[i % k];
@@ -292,6 +295,7 @@ extern "C" int bamg_col_scale_div(bamg_ctx* ctx, double* X, int64_t n, int k, co
 }
 
 __global__ void col_fill_kernel(double* X, int64_t n, int k, int c, double value) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) X[i * k + c] = value;
 }
@@ -307,6 +311,7 @@ extern "C" int bamg_col_fill(bamg_ctx* ctx, double* X, int64_t n, int k, int c, 
 
 __global__ void gather_rows_kernel(const double* __restrict__ X, const int32_t* __restrict__ idx,
                                    int64_t m, int k, double* __restrict__ Y) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * k) return;
   int64_t r = t / k;
@@ -325,6 +330,7 @@ struct Perm32 {
 };
 
 __global__ void permute_cols_kernel(const double* __restrict__ X, int64_t n, int k, Perm32 perm, double* __restrict__ Y) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * k) return;
   int64_t r = t / k;

@@ -76,6 +76,7 @@ static void dense_shape(bamg_ctx* ctx, K kernel, int n, int64_t work, int* grid,
 // --------------------------------------------------------- CSR -> dense
 __global__ void csr_to_dense_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                     const double* __restrict__ val, double* __restrict__ D, int ld, int transpose) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   for (int j = rp[i]; j < rp[i + 1]; ++j) {
@@ -145,6 +146,7 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
 }
 
 __global__ void sumsq_kernel(const double* __restrict__ G, int64_t total, double* out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double a = 0.0;
   for (int64_t t = threadIdx.x; t < total; t += blockDim.x) a += G[t] * G[t];
@@ -153,11 +155,13 @@ __global__ void sumsq_kernel(const double* __restrict__ G, int64_t total, double
 }
 
 __global__ void eye_kernel(double* V, int n) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < (int64_t)n * n) V[i] = (i / n == i % n) ? 1.0 : 0.0;
 }
 
 __global__ void col_norms_dense_kernel(const double* __restrict__ G, int nrows, int ncols, double* __restrict__ sig) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   int c = blockIdx.x;
   double a = 0.0;
@@ -176,6 +180,7 @@ __global__ void col_norms_dense_kernel(const double* __restrict__ G, int nrows, 
 __global__ void __launch_bounds__(JAC_THREADS)
 jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double tol, int* flags,
                        int maxsweeps, const double* fro2) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[96];
   // columns whose squared norm is below 1e-30 |G|_F^2 are numerically zero:
@@ -233,6 +238,7 @@ jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double
 constexpr int JAC_SMEM_MAX = 200 * 1024;
 __global__ void __launch_bounds__(1024)
 jacobi_svd_smem_kernel(double* G, int nrows, double* V, int ncols, int m, double tol, int maxsweeps) {
+  BAMG_PDL_PROLOGUE();
   extern __shared__ double sm[];
   double* sG = sm;
   double* sV = sm + (size_t)nrows * ncols;
@@ -365,6 +371,7 @@ static void arena_trim(bamg_ctx* ctx) {
 
 // Z[r][c] = sum_i V[r][i] G[c][i] w_i,  w_i = 1/sig_i^2 if sig_i > tol*max else 0
 __global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, double tol, double* __restrict__ w) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double smax;
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -379,6 +386,7 @@ __global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, doubl
 constexpr int GT = 16;
 __global__ void pinv_assemble_kernel(const double* __restrict__ V, const double* __restrict__ G, const double* __restrict__ w,
                                      int n, double* __restrict__ Z) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sv[GT][GT + 1], sg[GT][GT + 1];
   int r = blockIdx.y * GT + threadIdx.y;  // row of Z
   int c = blockIdx.x * GT + threadIdx.x;  // column of Z
@@ -411,6 +419,7 @@ __global__ void pinv_assemble_kernel(const double* __restrict__ V, const double*
 
 // augmented row-major [m][2m], m = n + 1
 __global__ void gj_init_kernel(const double* __restrict__ A, int n, double* __restrict__ Aug) {
+  BAMG_PDL_PROLOGUE();
   int m = n + 1;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)m * 2 * m) return;
@@ -429,6 +438,7 @@ __global__ void gj_init_kernel(const double* __restrict__ A, int n, double* __re
 
 // stats[0] = min |pivot|, stats[1] = max |pivot| (bits of non-negative doubles)
 __global__ void __launch_bounds__(1024) gj_coop_kernel(double* Aug, int m, double* prow, double* fcol, unsigned long long* stats) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -501,6 +511,7 @@ __global__ void __launch_bounds__(1024) gj_coop_kernel(double* Aug, int m, doubl
 // y = B x (B column-major n x n), and yt = B^T w
 __global__ void gemv_colmajor_kernel(const double* __restrict__ A, int n, const double* __restrict__ x,
                                      double* __restrict__ y) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -510,6 +521,7 @@ __global__ void gemv_colmajor_kernel(const double* __restrict__ A, int n, const 
 
 __global__ void gemv_colmajor_t_kernel(const double* __restrict__ A, int n, const double* __restrict__ x,
                                        double* __restrict__ y) {
+  BAMG_PDL_PROLOGUE();
   int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (k >= n) return;
   double s = 0.0;
@@ -522,6 +534,7 @@ __global__ void gemv_colmajor_t_kernel(const double* __restrict__ A, int n, cons
 // out[0] |x|, out[1] |w|, out[2] |B z|, out[3] |B^T y|, out[4] |B|_F, out[5] |omega|
 __global__ void gj_null_kernel(const double* __restrict__ Aug, int n, double* __restrict__ z,
                                double* __restrict__ y, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   const int m = n + 1, W = 2 * m;
   double a = 0.0, b = 0.0;
@@ -546,6 +559,7 @@ __global__ void gj_null_kernel(const double* __restrict__ Aug, int n, double* __
 
 __global__ void norm_pair_kernel(const double* __restrict__ u, const double* __restrict__ v, const double* __restrict__ A,
                                  int n, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double a = 0.0, b = 0.0, f = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -566,6 +580,7 @@ __global__ void norm_pair_kernel(const double* __restrict__ u, const double* __r
 // r = z^T X (row), s = X y (column), t = z^T X y ; X = top-left n x n of the inverse
 __global__ void proj_vectors_kernel(const double* __restrict__ Aug, int n, const double* __restrict__ z,
                                     const double* __restrict__ y, double* __restrict__ r, double* __restrict__ s) {
+  BAMG_PDL_PROLOGUE();
   const int m = n + 1, W = 2 * m;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) {  // r_t = sum_i z_i X[i][t]
@@ -583,6 +598,7 @@ __global__ void proj_vectors_kernel(const double* __restrict__ Aug, int n, const
 __global__ void proj_assemble_kernel(const double* __restrict__ Aug, int n, const double* __restrict__ z,
                                      const double* __restrict__ y, const double* __restrict__ r,
                                      const double* __restrict__ s, double* __restrict__ Z) {
+  BAMG_PDL_PROLOGUE();
   const int m = n + 1, W = 2 * m;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
@@ -595,6 +611,7 @@ __global__ void proj_assemble_kernel(const double* __restrict__ Aug, int n, cons
 
 __global__ void proj_corner_kernel(double* __restrict__ Z, int n, const double* __restrict__ z,
                                    const double* __restrict__ y, const double* __restrict__ s) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double a = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) a += z[i] * s[i];
@@ -687,6 +704,7 @@ extern "C" int bamg_dense_pinv(bamg_ctx* ctx, const double* A, int n, double ran
 
 // ------------------------------------------------------------- Cholesky
 __global__ void symmetrize_kernel(const double* __restrict__ A, int n, double* __restrict__ S) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int i = (int)(t % n), j = (int)(t / n);
@@ -697,6 +715,7 @@ __global__ void symmetrize_kernel(const double* __restrict__ A, int n, double* _
 // column is scaled (L[:, j] = A[:, j] / sqrt(A_jj)), a grid barrier, then the
 // trailing update A[i][k] -= L_ij L_kj (i, k > j), another barrier.
 __global__ void __launch_bounds__(1024) cholesky_coop_kernel(double* A, int n, double* L, int* bad) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -733,6 +752,7 @@ static int cholesky(bamg_ctx* ctx, double* A, int n, double* L, int* bad) {
 // cooperative launch: step i writes X[i][c] = B[i][c] / L_ii and updates
 // B[k][c] -= L_ki X[i][c] for k > i (row i of B is read-only in its step).
 __global__ void __launch_bounds__(1024) fwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -760,6 +780,7 @@ static int forward_solve(bamg_ctx* ctx, const double* L, int n, double* B, int n
 
 // Back substitution L^T X = B, i from n-1 down (cooperative).
 __global__ void __launch_bounds__(1024) bwd_coop_kernel(const double* L, int n, double* B, int nrhs, double* X) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -786,6 +807,7 @@ static int backward_solve_t(bamg_ctx* ctx, const double* L, int n, double* B, in
 }
 
 __global__ void transpose_dense_kernel(const double* __restrict__ A, int n, double* __restrict__ T) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int i = (int)(t % n), j = (int)(t / n);
@@ -794,6 +816,7 @@ __global__ void transpose_dense_kernel(const double* __restrict__ A, int n, doub
 
 // ascending order of sig (ties by index): perm[rank] = index
 __global__ void rank_sort_kernel(const double* __restrict__ sig, int n, int* __restrict__ perm) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double si = sig[i];
@@ -812,6 +835,7 @@ __global__ void gather_triplets_kernel(const double* __restrict__ G, const doubl
                                        const double* __restrict__ sig, const int* __restrict__ perm, int n, int r,
                                        double floor_rel, double* __restrict__ A, double* __restrict__ Bv,
                                        double* __restrict__ sig_out) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * r) return;
   int row = (int)(t % n), j = (int)(t / n);
@@ -827,6 +851,7 @@ __global__ void gather_triplets_kernel(const double* __restrict__ G, const doubl
 // coef[i] = (g_i . z) / sigma_i^2 for the well-conditioned columns (else 0)
 __global__ void null_coef_kernel(const double* __restrict__ G, const double* __restrict__ sig, int n, double thr,
                                  const double* __restrict__ z, double* __restrict__ coef) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   int i = blockIdx.x;
   double s = sig[i];
@@ -841,6 +866,7 @@ __global__ void null_coef_kernel(const double* __restrict__ G, const double* __r
 // well-conditioned left singular vectors)
 __global__ void null_update_kernel(const double* __restrict__ G, const double* __restrict__ coef, int n,
                                    double* __restrict__ z) {
+  BAMG_PDL_PROLOGUE();
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   double t = 0.0;
@@ -851,6 +877,7 @@ __global__ void null_update_kernel(const double* __restrict__ G, const double* _
 // one CTA: start vector for null slot j (deterministic), orthogonalise against
 // the previous null slots (columns < j of A that were null), normalise.
 __global__ void null_start_kernel(double* __restrict__ z, int n, int j) {
+  BAMG_PDL_PROLOGUE();
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     unsigned h = (unsigned)(r * 2654435761u) ^ (unsigned)(j * 40503u + 1u);
     h ^= h >> 13;
@@ -862,6 +889,7 @@ __global__ void null_start_kernel(double* __restrict__ z, int n, int j) {
 
 __global__ void null_finish_kernel(double* __restrict__ z, int n, double* __restrict__ A, int j,
                                    const double* __restrict__ sig_slots, double thr, int r) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   // Gram-Schmidt against earlier null slots
   for (int q = 0; q < j; ++q) {
@@ -885,6 +913,7 @@ __global__ void triplet_finish_kernel(const double* __restrict__ Bd, const doubl
                                       const double* __restrict__ Nd, int n, int r, double* __restrict__ U,
                                       double* __restrict__ Vv, double* __restrict__ sig, double* __restrict__ Uo,
                                       double* __restrict__ Vo, double* __restrict__ sig_o, double* __restrict__ work) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   __shared__ int s_order[64];
   // work: Mu(n), Nv(n), Bv(n), dead_c(n), dead_r(n)

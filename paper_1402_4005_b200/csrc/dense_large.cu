@@ -79,6 +79,7 @@ __device__ __forceinline__ double bsum(double v, double* sh) {
 // ----------------------------------------------------------- small helpers
 __global__ void copy_block_kernel(const double* __restrict__ S, int lds, double* __restrict__ D, int ldd, int rows,
                                   int cols) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)rows * cols) return;
   int r = (int)(t % rows), c = (int)(t / rows);
@@ -92,6 +93,7 @@ static int copy_block(bamg_ctx* ctx, const double* S, int lds, double* D, int ld
 }
 
 __global__ void transpose_big_kernel(const double* __restrict__ A, int n, double* __restrict__ T) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double tile[32][33];
   int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -123,6 +125,7 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 template <int NBT>
 __global__ void __launch_bounds__(4 * NBT) tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind,
                                                           double* __restrict__ Ti) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sT[NBT * NBT];
   __shared__ double rdg[NBT];
   for (int t = threadIdx.x; t < NBT * NBT; t += blockDim.x) {
@@ -197,6 +200,7 @@ constexpr int TRSM_MAX_N = 2048;
 constexpr int TRSM_RB = 8;
 __global__ void __launch_bounds__(256) trsm_small_kernel(const double* __restrict__ T, int n, int lower_stored,
                                                          int unit, int trans, double* __restrict__ B, int ldb, int m) {
+  BAMG_PDL_PROLOGUE();
   extern __shared__ double sX[];  // [TRSM_RB][n]
   const int c0 = blockIdx.x * TRSM_RB;
   const int mc = min(TRSM_RB, m - c0);
@@ -331,6 +335,7 @@ static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, b
 // unblocked in-place lower Cholesky of a jb x jb diagonal block (one CTA,
 // block staged in dynamic shared memory)
 __global__ void chol_block_kernel(double* A, int ld, int jb, int* bad) {
+  BAMG_PDL_PROLOGUE();
   extern __shared__ double sA[];
   for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) sA[t] = A[(int64_t)(t / jb) * ld + (t % jb)];
   __syncthreads();
@@ -356,6 +361,7 @@ __global__ void chol_block_kernel(double* A, int ld, int jb, int* bad) {
 }
 
 __global__ void zero_upper_kernel(double* A, int n) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int r = (int)(t % n), c = (int)(t / n);
@@ -396,6 +402,7 @@ static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* w
 // in piv[j0..j0+jb), swaps applied inside the panel only).
 __global__ void __launch_bounds__(256) panel_lu_kernel(double* A, int n, int j0, int jb, int* piv, double* pmax,
                                                        int* pidx, int* bad) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sb[8];
   __shared__ int si[8];
@@ -476,6 +483,7 @@ __global__ void __launch_bounds__(256) panel_lu_kernel(double* A, int n, int j0,
 // barriers.  Same pivot rule as panel_lu_kernel (max |a|, first index on ties).
 constexpr int PANEL_SMEM_MAX = 200 * 1024;
 __global__ void __launch_bounds__(1024) panel_lu_smem_kernel(double* A, int n, int j0, int jb, int* piv, int* bad) {
+  BAMG_PDL_PROLOGUE();
   extern __shared__ double sP[];
   __shared__ double wb[32];
   __shared__ int wi[32];
@@ -566,6 +574,7 @@ __global__ void __launch_bounds__(1024) panel_lu_smem_kernel(double* A, int n, i
 constexpr int CL_PANEL_NB = 64;
 __global__ void __launch_bounds__(1024) panel_lu_cluster_kernel(double* A, int n, int j0, int jb, int R, int* piv,
                                                                 int* bad) {
+  BAMG_PDL_PROLOGUE();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double sP[];
   __shared__ double wb[32];
@@ -693,6 +702,7 @@ static size_t panel_smem_max() {
 
 // apply the panel's row interchanges to columns outside [j0, j0+jb)
 __global__ void apply_swaps_kernel(double* A, int n, int j0, int jb, const int* piv) {
+  BAMG_PDL_PROLOGUE();
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n || (c >= j0 && c < j0 + jb)) return;
   double* col = A + (int64_t)c * n;
@@ -783,6 +793,7 @@ static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, doubl
 
 // row permutation of the identity: perm[r] = source row after the swaps of piv
 __global__ void perm_vector_kernel(int n, const int* piv, int* perm) {
+  BAMG_PDL_PROLOGUE();
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   for (int r = 0; r < n; ++r) perm[r] = r;
   for (int j = 0; j < n; ++j) {
@@ -797,6 +808,7 @@ __global__ void perm_vector_kernel(int n, const int* piv, int* perm) {
 
 // X[r][c] = (perm[r] == c): the row swaps of piv applied to I (coalesced)
 __global__ void perm_identity_kernel(double* X, int n, const int* perm) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int r = (int)(t % n), c = (int)(t / n);
@@ -816,6 +828,7 @@ static int lu_inverse(bamg_ctx* ctx, const double* LU, int n, const int* piv, do
 
 // ------------------------------------------------- bordered inverse -> pinv
 __global__ void border_fill_kernel(const double* __restrict__ A, int n, double* __restrict__ Bb) {
+  BAMG_PDL_PROLOGUE();
   const int m = n + 1;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)m * m) return;
@@ -832,6 +845,7 @@ __global__ void border_fill_kernel(const double* __restrict__ A, int n, double* 
 // x = Xb[0:n, n], w = Xb[n, 0:n];  out: |x|, |w|, |omega|
 __global__ void border_null_kernel(const double* __restrict__ Xb, int n, double* __restrict__ z, double* __restrict__ y,
                                    double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   const int m = n + 1;
   double a = 0.0, b = 0.0;
@@ -857,6 +871,7 @@ __global__ void border_null_kernel(const double* __restrict__ Xb, int n, double*
 // |B z|, |B^T y|, |B|_F
 __global__ void border_cert_kernel(const double* __restrict__ Bz, const double* __restrict__ Bty,
                                    const double* __restrict__ A, int n, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -879,6 +894,7 @@ __global__ void border_project_kernel(const double* __restrict__ Xb, int n, cons
                                       const double* __restrict__ y, const double* __restrict__ r,
                                       const double* __restrict__ s, const double* __restrict__ t, double* __restrict__ P,
                                       int rowmajor_out) {
+  BAMG_PDL_PROLOGUE();
   const int m = n + 1;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -889,6 +905,7 @@ __global__ void border_project_kernel(const double* __restrict__ Xb, int n, cons
 }
 
 __global__ void dot1_kernel(const double* __restrict__ a, const double* __restrict__ b, int n, double* out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[i] * b[i];
@@ -966,6 +983,7 @@ int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int ro
 }
 
 __global__ void frob2_kernel(const double* __restrict__ A, int64_t total, double* out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double f = 0.0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
@@ -975,6 +993,7 @@ __global__ void frob2_kernel(const double* __restrict__ A, int64_t total, double
 }
 
 __global__ void transpose_copy_kernel(const double* __restrict__ X, int n, double* __restrict__ P) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int i = (int)(t % n), j = (int)(t / n);
@@ -1016,6 +1035,7 @@ int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, in
 
 // ------------------------------------------------- coarsest triplets (large)
 __global__ void symmetrize_inplace_kernel(double* A, int n) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n) return;
   int r = (int)(t % n), c = (int)(t / n);
@@ -1030,6 +1050,7 @@ __global__ void symmetrize_inplace_kernel(double* A, int n) {
 }
 
 __global__ void pseudo_random_kernel(double* X, int64_t total, unsigned seed) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   unsigned h = (unsigned)(t * 2654435761ull) ^ (seed * 0x9e3779b9u);
@@ -1049,6 +1070,7 @@ constexpr int SMALLP = 48;  // subspace block size limit (p = r + 12, r <= 31)
 // the diagonal of R into rdiag (the subspace iteration's Ritz estimates).
 __global__ void __launch_bounds__(256) small_chol_inv_kernel(const double* __restrict__ G, int p,
                                                              double* __restrict__ Rinv, double* __restrict__ rdiag) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double R[SMALLP * SMALLP];
   __shared__ double X[SMALLP * SMALLP];
   const int tid = threadIdx.x;
@@ -1123,6 +1145,7 @@ __device__ __forceinline__ void warp_chol_smem(double* sL, double* sRd, int lane
 // without forming R^-1.
 template <int P>
 __global__ void __launch_bounds__(256) cholqr_apply_kernel(const double* __restrict__ G, double* Y, int n) {
+  BAMG_PDL_PROLOGUE();
   static_assert(P <= 32, "one Gram row per lane");
   __shared__ double sA[P * (P + 1)];  // row-major, padded: lane i owns row i
   __shared__ double sRd[P];
@@ -1286,6 +1309,7 @@ __global__ void __launch_bounds__(SUB_THREADS) subspace_coop_kernel(const double
                                                                     const double* __restrict__ Kt, int n, double* Y,
                                                                     double* Z, int iters, double* partial,
                                                                     double* G) {
+  BAMG_PDL_PROLOGUE();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sL[P * (P + 1)];
   __shared__ double sRd[P];
@@ -1308,6 +1332,7 @@ static bool subspace_fused_enabled() {
 
 // column-major n x r block helpers for the large finish
 __global__ void cm_colnorm_scale_kernel(double* X, int n) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double* c = X + (int64_t)blockIdx.x * n;
   double a = 0.0;
@@ -1318,6 +1343,7 @@ __global__ void cm_colnorm_scale_kernel(double* X, int n) {
 }
 
 __global__ void cm_coldot_kernel(const double* X, const double* Y, int n, double* out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   const double* a = X + (int64_t)blockIdx.x * n;
   const double* b = Y + (int64_t)blockIdx.x * n;
@@ -1330,6 +1356,7 @@ __global__ void cm_coldot_kernel(const double* X, const double* Y, int n, double
 // interleave: Uo[i*r + j] = U[j*n + i]; V flipped where u^T B v < 0
 __global__ void cm_interleave_kernel(const double* U, const double* V, const double* sgn, int n, int r, double* Uo,
                                      double* Vo) {
+  BAMG_PDL_PROLOGUE();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * r) return;
   int i = (int)(t / r), j = (int)(t % r);
@@ -1342,6 +1369,7 @@ __global__ void cm_interleave_kernel(const double* U, const double* V, const dou
 __global__ void rm_project_kernel(double* __restrict__ Z, int n, const double* __restrict__ z,
                                   const double* __restrict__ y, const double* __restrict__ gz,
                                   const double* __restrict__ gy, const double* __restrict__ t) {
+  BAMG_PDL_PROLOGUE();
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
   const int i = (int)(idx / n), j = (int)(idx % n);
@@ -1349,6 +1377,7 @@ __global__ void rm_project_kernel(double* __restrict__ Z, int n, const double* _
 }
 
 __global__ void sub_sq_kernel(const double* __restrict__ a, const double* __restrict__ b, int n, double* out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[32];
   double s = 0.0, w = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {

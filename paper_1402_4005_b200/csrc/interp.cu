@@ -368,6 +368,7 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
                 int radius, double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
                 int32_t* __restrict__ out_col, double* __restrict__ out_val,
                 unsigned long long* __restrict__ status, const int32_t* __restrict__ list, int nlist) {
+  BAMG_PDL_PROLOGUE();
   __shared__ int s_cand[FIT_WARPS][MAXCAND];
   __shared__ double s_V[FIT_WARPS][CMAX * CMAX];
   const int lane = threadIdx.x & 31;
@@ -842,6 +843,7 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
 __global__ void fit_prepare_kernel(int n, const int32_t* __restrict__ crank, int caliber, int32_t* __restrict__ out_cnt,
                                    int32_t* __restrict__ out_col, double* __restrict__ out_val,
                                    int32_t* __restrict__ list, unsigned int* __restrict__ nlist) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int ci = crank[i];
@@ -868,6 +870,7 @@ fit_cands_kernel(const int32_t* __restrict__ list, const unsigned int* __restric
                  const int32_t* __restrict__ crank, int radius, int32_t* __restrict__ mcnt,
                  int32_t* __restrict__ cbuf, unsigned int* __restrict__ hist, int32_t* __restrict__ out_cnt,
                  int32_t* __restrict__ defer, unsigned int* __restrict__ ndefer) {
+  BAMG_PDL_PROLOGUE();
   __shared__ unsigned int sh[TMAXC + 1];
   if (threadIdx.x <= TMAXC) sh[threadIdx.x] = 0;
   __syncthreads();
@@ -930,6 +933,7 @@ fit_cands_kernel(const int32_t* __restrict__ list, const unsigned int* __restric
 
 // exclusive scan of the candidate-count histogram -> bucket cursors
 __global__ void fit_bucket_scan_kernel(unsigned int* __restrict__ hist, unsigned int* __restrict__ nsorted) {
+  BAMG_PDL_PROLOGUE();
   if (threadIdx.x != 0) return;
   unsigned int acc = 0;
   for (int b = 0; b <= TMAXC; ++b) {
@@ -945,6 +949,7 @@ __global__ void fit_bucket_scan_kernel(unsigned int* __restrict__ hist, unsigned
 __global__ void __launch_bounds__(256)
 fit_bucket_scatter_kernel(const int32_t* __restrict__ mcnt, const unsigned int* __restrict__ nlist,
                           unsigned int* __restrict__ cursor, int32_t* __restrict__ order) {
+  BAMG_PDL_PROLOGUE();
   __shared__ unsigned int sh[TMAXC + 1], base[TMAXC + 1];
   if (threadIdx.x <= TMAXC) sh[threadIdx.x] = 0;
   __syncthreads();
@@ -975,6 +980,7 @@ fit_rows_thread_kernel(const int32_t* __restrict__ order, const unsigned int* __
                        const double* __restrict__ lam_dev, int caliber, double tol, int constrain, int nonneg,
                        int32_t* __restrict__ out_cnt, int32_t* __restrict__ out_col, double* __restrict__ out_val,
                        int32_t* __restrict__ defer, unsigned int* __restrict__ ndefer) {
+  BAMG_PDL_PROLOGUE();
   __shared__ int s_cand[TMAXC][TFIT_THREADS];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int)*nsorted) return;
@@ -1103,6 +1109,7 @@ fit_rows_thread_kernel(const int32_t* __restrict__ order, const unsigned int* __
 // ridge = 0.1 * sqrt(mean_i (sqrt(sum_f w_f x_if^2))^2)  (interp.py:266-268)
 __global__ void level_scale_partial(const double* __restrict__ X, int64_t n, int k, const double* __restrict__ w,
                                     double* __restrict__ partial) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[RED_THREADS / 32];
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
@@ -1130,6 +1137,7 @@ __global__ void level_scale_partial(const double* __restrict__ X, int64_t n, int
 }
 
 __global__ void level_scale_final(const double* __restrict__ partial, int nb, int64_t n, double* lam) {
+  BAMG_PDL_PROLOGUE();
   int lane = threadIdx.x;
   double v = 0.0;
   for (int b = lane; b < nb; b += 32) v += partial[b];
@@ -1230,6 +1238,7 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
 // ---------------------------------------------- fixed-stride rows -> CSR
 __global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double* __restrict__ val, int64_t n,
                                   int stride, int32_t* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int c = 0;
@@ -1242,6 +1251,7 @@ __global__ void rows_fill_kernel(const int32_t* __restrict__ cnt, const int32_t*
                                  const double* __restrict__ val, int64_t n, int stride,
                                  const int32_t* __restrict__ rp, int32_t* __restrict__ col_out,
                                  double* __restrict__ val_out) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int w = rp[i];

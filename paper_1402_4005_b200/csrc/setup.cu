@@ -23,6 +23,7 @@
 // peak[k..2k)
 __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1, int64_t total, int k,
                                const double* __restrict__ peak) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * total) return;
   const bool second = i >= total;
@@ -36,6 +37,7 @@ __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1,
 
 // u_c <- -u_c for flagged columns
 __global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ flip) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   if (flip[i % k] != 0.0) X[i] = -X[i];
@@ -49,6 +51,7 @@ rayleigh_reduce_kernel(const double* __restrict__ A, const double* __restrict__ 
                        const double* __restrict__ Dm, const double* __restrict__ Em, const double* __restrict__ Fm,
                        int64_t n, int k, double* __restrict__ partial, unsigned int* __restrict__ counter,
                        double* __restrict__ dots, double* __restrict__ sigma, double* __restrict__ flip, int mode) {
+  BAMG_PDL_PROLOGUE();
   constexpr int KM = 32;
   __shared__ double sh[RED_THREADS / 32][3 * KM];
   __shared__ bool last;
@@ -252,6 +255,7 @@ extern "C" int bamg_refresh_sigmas(bamg_ctx* ctx, const bamg_csr* A, const bamg_
 // w = 1/res^2; nan/inf -> 1e16; min(w, 1e16); min(w, 1e4 * max(median, 1e-16));
 // w[inf_slot] = inf   (interp.py:96-101)
 __global__ void weights_finish_kernel(const double* __restrict__ res, int k, int inf_slot, double* __restrict__ w) {
+  BAMG_PDL_PROLOGUE();
   if (threadIdx.x != 0) return;
   const double CAP = 1e16, SPREAD = 1e4;
   double t[32], s[32];

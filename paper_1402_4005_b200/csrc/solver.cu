@@ -185,6 +185,7 @@ static int hier_prepare(bamg_hier* h) {
 __global__ void jacobi_from_zero_kernel(int n, const double* __restrict__ b, const double* __restrict__ d,
                                         const uint8_t* __restrict__ skip, double omega,
                                         double* __restrict__ x, const double* __restrict__ rd) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double num = __dmul_rn(omega, b[i]);
@@ -195,6 +196,7 @@ __global__ void jacobi_from_zero_kernel(int n, const double* __restrict__ b, con
 // y = Z b, Z row-major n x n (warp per row, coalesced).
 __global__ void gemv_rowmajor_kernel(int n, const double* __restrict__ Z, const double* __restrict__ b,
                                      double* __restrict__ y) {
+  BAMG_PDL_PROLOGUE();
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -337,6 +339,7 @@ constexpr int GM_GROUP = 16;  // basis vectors per register group
 __global__ void __launch_bounds__(GM_THREADS)
 mdot_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ w, int64_t n,
             double* __restrict__ partial) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[GM_THREADS / 32][GM_GROUP];
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per;
@@ -373,6 +376,7 @@ template <int MODE>
 __global__ void __launch_bounds__(GM_THREADS)
 mupdate_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
                double* __restrict__ w, int64_t n, double* __restrict__ partial) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sh[GM_THREADS / 32][GM_GROUP];
   __shared__ double sc[1024];
   for (int i = threadIdx.x; i < m && i < 1024; i += GM_THREADS) sc[i] = c[i];
@@ -404,6 +408,7 @@ mupdate_kernel(const double* const* __restrict__ Vp, int m, const double* __rest
 // out[i] = sum_b partial[b * m + i]  (fixed order -> deterministic)
 __global__ void mreduce_kernel(const double* __restrict__ partial, int nb, int m, double* __restrict__ out,
                                int accumulate) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int lane = threadIdx.x & 31;
   if (i >= m) return;
@@ -421,6 +426,7 @@ __global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const doub
                               double beta, double* __restrict__ R, double* __restrict__ g,
                               double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ y,
                               double* __restrict__ state) {
+  BAMG_PDL_PROLOGUE();
   extern __shared__ double sg[];  // j+1 working entries of g during the back substitution
   if (threadIdx.x == 0) {
     double hj1 = sqrt(nrm2[0]);
@@ -462,6 +468,7 @@ __global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const doub
 // dst = w / h  unless the happy-breakdown flag is set
 __global__ void scale_new_basis_kernel(const double* __restrict__ w, const double* __restrict__ state,
                                        int64_t n, double* __restrict__ dst) {
+  BAMG_PDL_PROLOGUE();
   if (state[0] != 0.0) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double h = state[1];
@@ -472,6 +479,7 @@ __global__ void scale_new_basis_kernel(const double* __restrict__ w, const doubl
 __global__ void combine_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ y,
                                const double* __restrict__ base, const double* __restrict__ e_add,
                                const double* __restrict__ e_add2, int64_t n, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double sy[1024];
   for (int i = threadIdx.x; i < m && i < 1024; i += blockDim.x) sy[i] = y[i];
   __syncthreads();
@@ -485,13 +493,15 @@ __global__ void combine_kernel(const double* const* __restrict__ Vp, int m, cons
 }
 
 __global__ void axpby_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
-                             double* __restrict__ out) {  // out = a - b
+                             double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();  // out = a - b
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = a[i] - b[i];
 }
 
 __global__ void scale_div_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ s,
                                  double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = a[i] / s[0];
 }
@@ -718,6 +728,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
 // [3] non-finite flag
 __global__ void signfix_extract_kernel(const double* __restrict__ x, int64_t n, int stride,
                                        double* __restrict__ out, unsigned long long* __restrict__ flags) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = x[i * stride];
@@ -727,6 +738,7 @@ __global__ void signfix_extract_kernel(const double* __restrict__ x, int64_t n, 
 
 __global__ void absstats_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ psum,
                                         double* __restrict__ pmax, long long* __restrict__ pidx) {
+  BAMG_PDL_PROLOGUE();
   __shared__ double ss[256], sm[256];
   __shared__ long long si[256];
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -766,6 +778,7 @@ __global__ void absstats_partial_kernel(const double* __restrict__ x, int64_t n,
 
 __global__ void absstats_final_kernel(int nb, const double* psum, const double* pmax, const long long* pidx,
                                       double* stats) {
+  BAMG_PDL_PROLOGUE();
   if (threadIdx.x != 0) return;
   double s = 0.0, mx = -1.0;
   long long mi = -1;
@@ -783,12 +796,14 @@ __global__ void absstats_final_kernel(int nb, const double* psum, const double* 
 
 __global__ void uniform_fill_kernel(double* out, int64_t n, const unsigned long long* flags,
                                     const double* stats) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (flags[0] != 0ull || stats[2] == 0.0) out[i] = 1.0 / (double)n;
 }
 
 __global__ void signfix_apply_kernel(double* out, int64_t n, const double* stats) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   long long pk = (long long)stats[1];
@@ -802,6 +817,7 @@ __global__ void signfix_apply_kernel(double* out, int64_t n, const double* stats
 }
 
 __global__ void peak_sign_kernel(const double* out, double* stats) {
+  BAMG_PDL_PROLOGUE();
   long long pk = (long long)stats[1];
   stats[3] = pk >= 0 ? out[pk] : 1.0;
 }

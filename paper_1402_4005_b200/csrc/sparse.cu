@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(TILE_THREADS)
 csr_tile_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, int k,
                 double* __restrict__ Y, EpiArgs ea) {
+  BAMG_PDL_PROLOGUE();
   __shared__ int32_t s_rp[TILE_ROWS + 1];
   __shared__ int32_t s_col[TILE_NNZ];
   __shared__ double s_val[TILE_NNZ];
@@ -138,9 +139,16 @@ struct VecIO {
 // so each thread keeps U independent loads in flight.  256 threads per CTA,
 // 256 / G rows per CTA; col/val of the CTA's rows staged in shared memory.
 template <int EPI, int K, int G, int U, bool STAGE>
-__global__ void __launch_bounds__(TILE_THREADS)
+// 8 resident CTAs per SM caps the row kernels at 32 registers (full
+// occupancy): measured ~25% faster for k = 8 / 16 than the 40-72 registers
+// ptxas picks otherwise (tools/csr_bench.py)
+#ifndef BAMG_ROWS_MINB
+#define BAMG_ROWS_MINB 8
+#endif
+__global__ void __launch_bounds__(TILE_THREADS, BAMG_ROWS_MINB)
 csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y, EpiArgs ea) {
+  BAMG_PDL_PROLOGUE();
   constexpr int V = K / G;
   constexpr int RB = TILE_THREADS / G;  // rows per CTA
   constexpr int NNZ_CAP = STAGE ? RB * 12 : 1;  // staged when the tile averages <= 12 entries per row
@@ -274,7 +282,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 #define BAMG_G8 4
 #endif
 #ifndef BAMG_U8
-#define BAMG_U8 4
+#define BAMG_U8 6
 #endif
 
 static int rows_stage_mode() {
@@ -328,6 +336,7 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
                       const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
                       double* __restrict__ sigma, double* __restrict__ flip, int mode) {
+  BAMG_PDL_PROLOGUE();
   constexpr int VV = K / G;
   constexpr int RB = TILE_THREADS / G;
   __shared__ double sv[3][TILE_THREADS][VV];
@@ -552,6 +561,7 @@ int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t*
 
 // rd[i] = RN(1 / d[i]) (the reciprocal the Jacobi epilogue's exact division uses)
 __global__ void recip_kernel(const double* __restrict__ d, int64_t n, double* __restrict__ rd) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) rd[i] = __ddiv_rn(1.0, d[i]);
 }
@@ -602,6 +612,7 @@ __device__ double selftest_operand(unsigned long long h, unsigned long long h2, 
 
 __global__ void selftest_div_kernel(int64_t n, unsigned long long seed, int mode,
                                     unsigned long long* __restrict__ mismatches) {
+  BAMG_PDL_PROLOGUE();
   unsigned long long local = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long h0 = mix64(seed ^ (4ull * i)), h1 = mix64(seed ^ (4ull * i + 1));
@@ -645,6 +656,7 @@ extern "C" int bamg_jacobi(bamg_ctx* ctx, const bamg_csr* A, const double* d, co
 // ------------------------------------------------------------ diagonal
 __global__ void diag_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                             const double* __restrict__ val, double* __restrict__ d) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int lo = rp[i], hi = rp[i + 1] - 1;
@@ -674,6 +686,7 @@ extern "C" int bamg_diag(bamg_ctx* ctx, const bamg_csr* A, double* d) {
 }
 
 __global__ void count_nonpos_kernel(const double* __restrict__ d, int64_t n, unsigned long long* out) {
+  BAMG_PDL_PROLOGUE();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int flag = (i < n) && (d[i] <= 0.0);
   int cnt = __syncthreads_count(flag);
@@ -694,6 +707,7 @@ extern "C" int bamg_count_nonpositive(bamg_ctx* ctx, const double* d, int64_t n,
 // np.add.reduceat / the ones-vector product); skip = d <= 0 | off > 4 d.
 __global__ void degenerate_kernel(int n, const int32_t* __restrict__ rp, const double* __restrict__ val,
                                   const double* __restrict__ d, uint8_t* __restrict__ skip) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double mass = 0.0;
@@ -719,6 +733,7 @@ extern "C" int bamg_degenerate_rows(bamg_ctx* ctx, const bamg_csr* A, const doub
 // independent of atomic order).  Output rows are short for every operator in
 // scope; long rows fall back to a shell sort in the same thread.
 __global__ void col_count_kernel(int64_t nnz, const int32_t* __restrict__ col, int32_t* __restrict__ cnt) {
+  BAMG_PDL_PROLOGUE();
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < nnz) atomicAdd(&cnt[col[j]], 1);
 }
@@ -726,6 +741,7 @@ __global__ void col_count_kernel(int64_t nnz, const int32_t* __restrict__ col, i
 __global__ void transpose_scatter_kernel(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                          const double* __restrict__ val, int32_t* __restrict__ cursor,
                                          int32_t* __restrict__ col_t, double* __restrict__ val_t) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   for (int j = rp[i]; j < rp[i + 1]; ++j) {
@@ -757,6 +773,7 @@ __device__ void sort_segment(int32_t* key, double* val, int len) {
 }
 
 __global__ void sort_rows_kernel(int n, const int32_t* __restrict__ rp, int32_t* col, double* val) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int b = rp[i], e = rp[i + 1];
@@ -793,6 +810,7 @@ template <bool FILL>
 __global__ void sym_union_kernel(int n, const int32_t* __restrict__ ra, const int32_t* __restrict__ ca,
                                  const int32_t* __restrict__ rt, const int32_t* __restrict__ ct,
                                  int32_t* __restrict__ cnt_or_rp, int32_t* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int a = ra[i], ae = ra[i + 1], t = rt[i], te = rt[i + 1];

@@ -67,6 +67,7 @@ spgemm_local_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __res
                     const int32_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval,
                     int32_t* __restrict__ tcol, double* __restrict__ tval, uint8_t* __restrict__ parked,
                     const int32_t* __restrict__ rows, const unsigned int* __restrict__ nrows) {
+  BAMG_PDL_PROLOGUE();
   // rows (fill pass): grid-stride over the *nrows listed rows; else row = thread
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
   const int tn = rows ? (int)*nrows : n;
@@ -141,6 +142,7 @@ __global__ void spgemm_copy_parked_kernel(int n, const uint8_t* __restrict__ par
                                           const int32_t* __restrict__ tcol, const double* __restrict__ tval,
                                           int32_t* __restrict__ ccol, double* __restrict__ cval,
                                           int32_t* __restrict__ redo, unsigned int* __restrict__ nredo) {
+  BAMG_PDL_PROLOGUE();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= n) return;
@@ -160,6 +162,7 @@ __global__ void spgemm_copy_parked_kernel(int n, const uint8_t* __restrict__ par
 __global__ void spgemm_big_ub_kernel(int nb, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
                                      const int32_t* __restrict__ acol, const int32_t* __restrict__ brp,
                                      int32_t* __restrict__ ub) {
+  BAMG_PDL_PROLOGUE();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nb) return;
   int i = list[t];
@@ -179,6 +182,7 @@ __global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, cons
                                   int32_t* __restrict__ skey, double* __restrict__ sval, int order,
                                   int32_t* __restrict__ cnt, const int32_t* __restrict__ crp,
                                   int32_t* __restrict__ ccol, double* __restrict__ cval) {
+  BAMG_PDL_PROLOGUE();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nb) return;
   int i = list[t];
