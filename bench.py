@@ -238,7 +238,8 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = int(L.bamg_launch_count(c))
-    L.bamg_prof_enable(c, 0b11)  # CSR-stream family + LS-fit family, CUDA events on our stream
+    # CSR-stream family (coarse + finest-level launches) + LS-fit family, CUDA events on our stream
+    L.bamg_prof_enable(c, (1 << 0) | (1 << 1) | (1 << 6))
     with ClockSampler(local_rank) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -256,10 +257,15 @@ def run_ours(args, rank, world, local_rank):
     launches = int(L.bamg_launch_count(c)) - launches0
     import ctypes as C
     fam_stats = {}
-    for fid, fname in ((0, "csr_stream_spmv_spmm_jacobi"), (1, "ls_fit_warp_per_point")):
+    raw = {}
+    for fid in (0, 1, 6):
         ms, cnt, by = C.c_double(), C.c_int64(), C.c_double()
         L.bamg_prof_read(c, fid, C.byref(ms), C.byref(cnt), C.byref(by))
-        fam_stats[fname] = (ms.value, cnt.value, by.value)
+        raw[fid] = (ms.value, cnt.value, by.value)
+    # the CSR family = its launches on every level (engine families 0 + 6)
+    fam_stats["csr_stream_spmv_spmm_jacobi"] = tuple(a + b for a, b in zip(raw[0], raw[6]))
+    fam_stats["ls_fit_warp_per_point"] = raw[1]
+    fine = raw[6]
     L.bamg_prof_enable(c, 0)
     dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
     step_ms = [ev0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
@@ -336,6 +342,13 @@ def run_ours(args, rank, world, local_rank):
             "families": {f: {"ms_total": round(v[0], 3), "launches": v[1],
                              "alg_GBps": round((v[2] / max(v[1], 1)) / (v[0] / 1e3 / max(v[1], 1)) / 1e9, 1) if v[1] else 0}
                          for f, v in fam_stats.items()}}
+    if dom == "csr_stream_spmv_spmm_jacobi" and fine[1]:
+        # the same family restricted to the finest levels (operators >= 2^18 rows):
+        # bandwidth-sized launches, without the latency-bound coarse-level ones
+        fa = (fine[2] / fine[1]) / (fine[0] / 1e3 / fine[1]) / 1e9
+        roof["finest_levels"] = {"rows_min": 1 << 18, "launches": fine[1], "ms_total": round(fine[0], 3),
+                                 "alg_bytes_per_launch": round(fine[2] / fine[1]), "achieved": round(fa, 1),
+                                 "frac": round(fa / peak, 4)}
     line = {
         "metric": METRIC, "value": round(dev_s, 6), "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3, 3),

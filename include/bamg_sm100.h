@@ -184,6 +184,15 @@ int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank
                   int radius, double improvement_tol, int constrain, int nonnegative,
                   double ridge_override, int32_t* out_cnt, int32_t* out_col, double* out_val,
                   int64_t* status_host);
+/* bamg_fit_rows + bamg_rows_count in one call with ONE host read (status as
+ * bamg_fit_rows, nnz of the compacted CSR); rowptr (n + 1) is written, the
+ * caller allocates nnz entries and finishes with bamg_rows_fill.  Replaces
+ * _build_rows, interp.py:252-289. */
+int bamg_fit_rows_csr(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
+                      const double* X, const double* w, int64_t n, int k, int caliber,
+                      int radius, double improvement_tol, int constrain, int nonnegative,
+                      double ridge_override, int32_t* out_cnt, int32_t* out_col, double* out_val,
+                      int32_t* rowptr, int64_t* status_host, int64_t* nnz_host);
 /* Compact the fixed-stride rows into canonical CSR (sorted columns, |v| <
  * 1e-300 dropped: csr_from_coo, sparse.py:42-46).  Two calls. */
 int bamg_rows_count(bamg_ctx* ctx, const int32_t* cnt, const double* val, int64_t n,

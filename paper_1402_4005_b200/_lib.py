@@ -76,6 +76,8 @@ _SIGS = {
     "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
     "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
                       F64, P, P, P, PI64],
+    "bamg_fit_rows_csr": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
+                          F64, P, P, P, P, PI64, PI64],
     "bamg_rows_count": [P, P, P, I64, C.c_int, P, PI64],
     "bamg_rows_fill": [P, P, P, P, I64, C.c_int, P, P, P],
     "bamg_axis_ranks": [P, P, I64, P, PI64],

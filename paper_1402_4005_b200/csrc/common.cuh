@@ -69,14 +69,18 @@ struct Arena {
 
 // Per-family kernel timing with CUDA events on the launching stream
 // (bench.py's live roofline).  Off unless bamg_prof_enable() set the family.
-enum { FAM_TILE = 0, FAM_FIT = 1, FAM_SPGEMM = 2, FAM_ORTHO = 3, FAM_DENSE = 4, FAM_OTHER = 5, NFAM = 6 };
+// FAM_TILE_FINE: the CSR row kernels on operators with >= 2^18 rows (the
+// finest levels), reported beside the whole CSR family (FAM_TILE + FINE)
+enum { FAM_TILE = 0, FAM_FIT = 1, FAM_SPGEMM = 2, FAM_ORTHO = 3, FAM_DENSE = 4, FAM_OTHER = 5, FAM_TILE_FINE = 6,
+       NFAM = 7 };
+constexpr int FINE_ROWS = 1 << 18;
 
 struct KProf {
   unsigned mask = 0;
   std::vector<cudaEvent_t> ev[NFAM];  // start/stop pairs
-  size_t used[NFAM] = {0, 0, 0, 0, 0, 0};
-  double bytes[NFAM] = {0, 0, 0, 0, 0, 0};
-  double flops[NFAM] = {0, 0, 0, 0, 0, 0};
+  size_t used[NFAM] = {};
+  double bytes[NFAM] = {};
+  double flops[NFAM] = {};
 };
 
 // Whole-engine launch trace (development): every BAMG_LAUNCH brackets its
@@ -251,6 +255,8 @@ static inline int grid_for(int64_t work, int block) {
 // out[0..n] exclusive prefix sums of in[0..n-1] (out[n] = total).  Optional
 // total read back to the host.
 int scan_i32(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_host);
+// Same, the total written to a caller-owned device word (no host read).
+int scan_i32_dev(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_dev);
 // Same for uint8 flags -> int32 offsets.
 int scan_u8(bamg_ctx* ctx, const uint8_t* in, int32_t* out, int64_t n, int64_t* total_host);
 

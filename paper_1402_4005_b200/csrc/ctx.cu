@@ -169,7 +169,8 @@ scan_onepass_kernel(const T* __restrict__ in, int64_t n, int32_t* __restrict__ o
 }
 
 template <typename T>
-static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_t* total_host) {
+static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_t* total_host,
+                     int64_t* total_dev = nullptr) {
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles < 1) tiles = 1;
   // state words (tiles) + tile counter + total, one memset
@@ -177,7 +178,7 @@ static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_
   BAMG_TRY(arena_get(ctx, (size_t)tiles + 2, &state));
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(state, 0, sizeof(unsigned long long) * ((size_t)tiles + 2), ctx->stream));
   unsigned int* counter = reinterpret_cast<unsigned int*>(state + tiles);
-  int64_t* total = reinterpret_cast<int64_t*>(state + tiles + 1);
+  int64_t* total = total_dev ? total_dev : reinterpret_cast<int64_t*>(state + tiles + 1);
   BAMG_LAUNCH(ctx, scan_onepass_kernel<T>, (int)tiles, SCAN_THREADS, 0, in, n, out, state, counter, total);
   if (total_host) BAMG_TRY(ctx_read_i64(ctx, total, 1, total_host));
   return 0;
@@ -185,6 +186,9 @@ static int scan_impl(bamg_ctx* ctx, const T* in, int32_t* out, int64_t n, int64_
 
 int scan_i32(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_host) {
   return scan_impl<int32_t>(ctx, in, out, n, total_host);
+}
+int scan_i32_dev(bamg_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int64_t* total_dev) {
+  return scan_impl<int32_t>(ctx, in, out, n, nullptr, total_dev);
 }
 int scan_u8(bamg_ctx* ctx, const uint8_t* in, int32_t* out, int64_t n, int64_t* total_host) {
   return scan_impl<uint8_t>(ctx, in, out, n, total_host);

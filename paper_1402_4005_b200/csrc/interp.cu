@@ -367,8 +367,10 @@ fit_rows_kernel(int n, const int32_t* __restrict__ arp, const int32_t* __restric
                 const double* __restrict__ w, const double* __restrict__ lam_dev, int caliber,
                 int radius, double tol, int constrain, int nonneg, int32_t* __restrict__ out_cnt,
                 int32_t* __restrict__ out_col, double* __restrict__ out_val,
-                unsigned long long* __restrict__ status, const int32_t* __restrict__ list, int nlist) {
+                unsigned long long* __restrict__ status, const int32_t* __restrict__ list, int nlist,
+                const unsigned int* __restrict__ nlist_dev) {
   BAMG_PDL_PROLOGUE();
+  if (nlist_dev) nlist = (int)*nlist_dev;  // deferred points counted on device (no host read)
   __shared__ int s_cand[FIT_WARPS][MAXCAND];
   __shared__ double s_V[FIT_WARPS][CMAX * CMAX];
   const int lane = threadIdx.x & 31;
@@ -1151,22 +1153,23 @@ static bool force_warp_path() {
   return e && e[0] == '1';
 }
 
-extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
-                             const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
-                             int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
-                             int32_t* out_col, double* out_val, int64_t* status_host) {
-  ctx->arena.reset();
+// LS fit of every fine point.  status (device, 4 words): [0] points that took
+// the reference's pseudo-inverse branch, [1] candidate-list overflows,
+// [2] points deferred from the thread path to the warp path.  Nothing is read
+// back here: the deferred points are walked grid-stride over their device
+// count, so the caller reads status once (with its own results).
+static int fit_rows_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
+                           const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
+                           int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
+                           int32_t* out_col, double* out_val, unsigned long long* status) {
   BAMG_REQUIRE(ctx, caliber >= 1 && caliber <= CMAX, "caliber must lie in [1, 8]");
   BAMG_REQUIRE(ctx, k >= 1 && k + caliber <= 32, "need k + caliber <= 32 (one LS row per lane)");
-  if (status_host) status_host[0] = status_host[1] = 0;
   BAMG_REQUIRE(ctx, radius == 1 || radius == 2, "radius must be 1 or 2");
   BAMG_REQUIRE(ctx, adj && adj->nrows == n, "adjacency size mismatch");
   double *partial, *lam;
-  unsigned long long* status;
   BAMG_TRY(arena_get(ctx, RED_BLOCKS, &partial));
   BAMG_TRY(arena_get(ctx, 1, &lam));
-  BAMG_TRY(arena_get(ctx, 2, &status));
-  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(status, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(status, 0, 4 * sizeof(unsigned long long), ctx->stream));
   if (ridge_override >= 0.0) {
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(lam, &ridge_override, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   } else {
@@ -1176,12 +1179,8 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
   // algorithmic bytes: test vectors of every point + adjacency + rank map + the row output
   double fbytes = 8.0 * n * k + 4.0 * (n + 1) + 4.0 * adj->nnz + 4.0 * n + 16.0 * n * caliber;
   int32_t* defer;
-  unsigned int* ndefer;
+  unsigned int* ndefer = reinterpret_cast<unsigned int*>(status + 2);  // low half of status[2]
   BAMG_TRY(arena_get(ctx, (size_t)n + 1, &defer));
-  BAMG_TRY(arena_get(ctx, 1, &ndefer));
-  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(ndefer, 0, sizeof(unsigned int), ctx->stream));
-  int nlist = (int)n;
-  const int32_t* list = nullptr;
   if (k <= TKMAX && caliber <= TCAL && !force_warp_path()) {
     int32_t* flist;
     unsigned int* nfl;
@@ -1214,25 +1213,71 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
                       constrain, nonnegative, out_cnt, out_col, out_val, defer, ndefer);
     }
 #undef BAMG_FIT_EXACT
-    int32_t nd = 0;
-    BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(ndefer), 1, &nd));
-    nlist = nd;
-    list = defer;
-    if (status_host) status_host[1] = nd;
-  }
-  if (nlist > 0) {
-    int64_t blocks = ((int64_t)nlist + FIT_WARPS - 1) / FIT_WARPS;
+    // deferred points (device count): a fixed grid of warps strides over them
+    const int blocks = ctx->num_sms * 4;
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, 0.0, fit_rows_kernel, blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr, adj->col,
+                    coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative, out_cnt,
+                    out_col, out_val, status, (const int32_t*)defer, 0, (const unsigned int*)ndefer);
+  } else if (n > 0) {
+    int64_t blocks = (n + FIT_WARPS - 1) / FIT_WARPS;
     int64_t maxb = (int64_t)ctx->num_sms * 64;
     if (blocks > maxb) blocks = maxb;
-    BAMG_LAUNCH_FAM(ctx, FAM_FIT, list ? 0.0 : fbytes, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n,
-                    adj->rowptr, adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain,
-                    nonnegative, out_cnt, out_col, out_val, status, list, nlist);
+    BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_kernel, (int)blocks, FIT_WARPS * 32, 0, (int)n, adj->rowptr,
+                    adj->col, coarse_rank, X, k, w, lam, caliber, radius, improvement_tol, constrain, nonnegative,
+                    out_cnt, out_col, out_val, status, (const int32_t*)nullptr, (int)n, (const unsigned int*)nullptr);
   }
-  int64_t st[2];
-  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 2, st));
-  if (status_host) status_host[0] = st[0];
+  return 0;
+}
+
+static int fit_status_check(bamg_ctx* ctx, const int64_t* st, int64_t* status_host) {
+  if (status_host) {
+    status_host[0] = st[0];
+    status_host[1] = st[2] & 0xffffffffll;
+  }
   BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 256 coarse candidates for one point)");
   return 0;
+}
+
+extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
+                             const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
+                             int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
+                             int32_t* out_col, double* out_val, int64_t* status_host) {
+  ctx->arena.reset();
+  if (status_host) status_host[0] = status_host[1] = 0;
+  unsigned long long* status;
+  BAMG_TRY(arena_get(ctx, 4, &status));
+  BAMG_TRY(fit_rows_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                           nonnegative, ridge_override, out_cnt, out_col, out_val, status));
+  int64_t st[3];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 3, st));
+  return fit_status_check(ctx, st, status_host);
+}
+
+__global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double* __restrict__ val, int64_t n,
+                                  int stride, int32_t* __restrict__ out);
+
+// The fit, the kept-entry count of its rows and the row-pointer scan in one
+// call with ONE host read: [pinv-branch points, overflows, deferred, nnz].
+// The caller allocates col/val for nnz and finishes with bamg_rows_fill.
+extern "C" int bamg_fit_rows_csr(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
+                                 const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
+                                 int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
+                                 int32_t* out_col, double* out_val, int32_t* rowptr, int64_t* status_host,
+                                 int64_t* nnz_host) {
+  ctx->arena.reset();
+  if (status_host) status_host[0] = status_host[1] = 0;
+  unsigned long long* status;
+  BAMG_TRY(arena_get(ctx, 4, &status));
+  BAMG_TRY(fit_rows_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                           nonnegative, ridge_override, out_cnt, out_col, out_val, status));
+  int32_t* c;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &c));
+  BAMG_LAUNCH(ctx, rows_count_kernel, grid_for(n, 256), 256, 0, out_cnt, out_val, n, caliber, c);
+  BAMG_TRY(scan_i32_dev(ctx, c, rowptr, n, reinterpret_cast<int64_t*>(status + 3)));
+  int64_t st[4];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(status), 4, st));
+  *nnz_host = st[3];
+  return fit_status_check(ctx, st, status_host);
 }
 
 // ---------------------------------------------- fixed-stride rows -> CSR

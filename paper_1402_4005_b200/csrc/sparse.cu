@@ -302,10 +302,10 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
   case KK: {                                                                                               \
     int g = (A->nrows + TILE_THREADS / GG - 1) / (TILE_THREADS / GG);                                      \
     if (rows_stage_mode())                                                                                 \
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, true>), g, TILE_THREADS, 0,  \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, true>), g, TILE_THREADS, 0,  \
                       A->nrows, A->rowptr, A->col, A->val, X, Y, ea);                                      \
     else                                                                                                   \
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, false>), g, TILE_THREADS, 0, \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (csr_rows_kernel<EPI, KK, GG, UU, false>), g, TILE_THREADS, 0, \
                       A->nrows, A->rowptr, A->col, A->val, X, Y, ea);                                      \
     return 0;                                                                                              \
   }
@@ -453,7 +453,7 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   switch (k) {
 #define BAMG_RQ_CASE(KK, GG, UU)                                                                              \
   case KK:                                                                                                   \
-    BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), RQ_BLOCKS, TILE_THREADS, 0,  \
+    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), RQ_BLOCKS, TILE_THREADS, 0,  \
                     A->nrows, A->rowptr, A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, \
                     mode);                                                                                   \
     return 0;
@@ -507,19 +507,19 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   }
   switch (epi) {
     case EPI_PLAIN:
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     case EPI_RESID:
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_RESID>, grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_RESID>, grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     case EPI_ADD:
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_ADD>, grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_ADD>, grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->col, A->val, X, k, Y, ea);
       break;
     default:
-      BAMG_LAUNCH_FAM(ctx, FAM_TILE, bytes, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->col, A->val, X, k, Y, ea);
   }
   return 0;

@@ -21,6 +21,8 @@
 // slice sized by the structural upper bound sum_j nnz(B_j).  The flagged rows
 // and their scratch offsets are memoised in the context between the count and
 // fill calls, so a product costs two host synchronisations (row count, total).
+#include <cstdlib>
+
 #include "internal.cuh"
 
 constexpr int LCAP = 64;   // distinct columns per row on the fast path
@@ -159,33 +161,39 @@ __global__ void spgemm_copy_parked_kernel(int n, const uint8_t* __restrict__ par
 }
 
 // slow path over the flagged rows: list in a global scratch slice
-__global__ void spgemm_big_ub_kernel(int nb, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
-                                     const int32_t* __restrict__ acol, const int32_t* __restrict__ brp,
-                                     int32_t* __restrict__ ub) {
-  BAMG_PDL_PROLOGUE();
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb) return;
-  int i = list[t];
-  int s = 0;
+// Slow-path rows without a host round trip: the count pass's flagged rows are
+// walked grid-stride over the device-resident count; in pass 0 each reserves
+// its structural bound sum_j nnz(B_j) from a bump pointer over the context's
+// scratch pool (soff[t] = start, or -1 when the pool is exhausted: the count
+// call then grows the pool and recounts); pass 1 reuses the reservation.
+__device__ __forceinline__ int32_t big_reserve(int i, const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                                               const int32_t* __restrict__ brp, unsigned long long* pool_used,
+                                               long long pool_cap) {
+  long long s = 0;
   for (int jj = arp[i]; jj < arp[i + 1]; ++jj) {
     int j = acol[jj];
     s += brp[j + 1] - brp[j];
   }
-  ub[t] = s;
+  const unsigned long long at = atomicAdd(pool_used, (unsigned long long)s);
+  return ((long long)at + s <= pool_cap) ? (int32_t)at : -1;
 }
 
 template <int PASS>
-__global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
-                                  const int32_t* __restrict__ acol, const double* __restrict__ aval,
-                                  const int32_t* __restrict__ brp, const int32_t* __restrict__ bcol,
-                                  const double* __restrict__ bval, const int32_t* __restrict__ soff,
-                                  int32_t* __restrict__ skey, double* __restrict__ sval, int order,
-                                  int32_t* __restrict__ cnt, const int32_t* __restrict__ crp,
-                                  int32_t* __restrict__ ccol, double* __restrict__ cval) {
+__global__ void spgemm_big_kernel(const unsigned int* __restrict__ nbig, const int32_t* __restrict__ list,
+                                  const int32_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                                  const double* __restrict__ aval, const int32_t* __restrict__ brp,
+                                  const int32_t* __restrict__ bcol, const double* __restrict__ bval,
+                                  int32_t* __restrict__ soff, int32_t* __restrict__ skey,
+                                  double* __restrict__ sval, int order, int32_t* __restrict__ cnt,
+                                  const int32_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                                  double* __restrict__ cval, unsigned long long* __restrict__ pool_used,
+                                  long long pool_cap) {
   BAMG_PDL_PROLOGUE();
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb) return;
+  const int nb = (int)*nbig;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
   int i = list[t];
+  if (PASS == 0) soff[t] = big_reserve(i, arp, acol, brp, pool_used, pool_cap);
+  if (soff[t] < 0) continue;  // pool exhausted: the count call recounts with a larger pool
   int32_t* key = skey + soff[t];
   double* val = sval + soff[t];
   int len = 0;
@@ -215,7 +223,7 @@ __global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, cons
     int c = 0;
     for (int q = 0; q < len; ++q) c += keep_value(order, val[q]) ? 1 : 0;
     cnt[i] = c;
-    return;
+    continue;
   }
   int w = crp[i];
   if (order & SPG_STORAGE) {
@@ -241,6 +249,7 @@ __global__ void spgemm_big_kernel(int nb, const int32_t* __restrict__ list, cons
       cval[p] = x;
     }
   }
+  }  // grid-stride over the flagged rows
 }
 
 // Memo of the flagged rows between the count and the fill call (owned by the
@@ -250,10 +259,15 @@ struct SpgemmMemo {
   const int32_t* brp = nullptr;
   int order = -1;
   int nbig = 0;
-  int64_t scratch = 0;
+  unsigned int* nbig_dev = nullptr;  // device flagged-row counter (persistent, read by the fill)
   int32_t* list = nullptr;   // device, capacity cap
-  int32_t* off = nullptr;    // device, capacity cap + 1
+  int32_t* off = nullptr;    // device, capacity cap + 1 (per flagged row: scratch start or -1)
   int64_t cap = 0;
+  // slow-path scratch pool (bump-allocated on device by spgemm_big_kernel<0>)
+  int32_t* pkey = nullptr;
+  double* pval = nullptr;
+  int64_t pcap = 0;
+  unsigned long long* stat = nullptr;  // [pool used, flagged rows, nnz(C)] read back in one sync
   // parking slots of the count pass (TSLOT entries per row) + flags + redo list
   int32_t* tcol = nullptr;
   double* tval = nullptr;
@@ -294,6 +308,23 @@ static int memo_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t n) {
   return 0;
 }
 
+static int pool_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t want) {
+  if (!m.stat) BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.stat, sizeof(unsigned long long) * 4));
+  m.nbig_dev = reinterpret_cast<unsigned int*>(m.stat + 1);
+  if (m.pcap >= want) return 0;
+  cudaFree(m.pkey);
+  cudaFree(m.pval);
+  m.pcap = want;
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.pkey, sizeof(int32_t) * m.pcap));
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(&m.pval, sizeof(double) * m.pcap));
+  return 0;
+}
+
+// Count pass in ONE host synchronisation: the flagged (slow-path) rows are
+// handled without reading their number -- grid-stride kernels over the
+// device-resident count, scratch bump-allocated from the memo's pool -- and
+// the pool use, the flagged-row count and nnz(C) come back in one read.  A
+// pool overflow (rows too long for the pool) grows it and recounts.
 extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order, int32_t* rowptr_c,
                                  int64_t* nnz_host) {
   ctx->arena.reset();
@@ -303,36 +334,47 @@ extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
   const int n = A->nrows;
   SpgemmMemo& m = memo(ctx);
   BAMG_TRY(memo_reserve(ctx, m, n));
-  int32_t* cnt;
-  unsigned int* nbig;
-  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cnt));
-  BAMG_TRY(arena_get(ctx, 1, &nbig));
-  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nbig, 0, sizeof(unsigned int), ctx->stream));
-  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
-                  A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
-                  (int32_t*)nullptr, (double*)nullptr, m.tcol, m.tval, m.parked, (const int32_t*)nullptr,
-                  (const unsigned int*)nullptr);
-  int32_t nb = 0;
-  BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<int32_t*>(nbig), 1, &nb));
-  m.arp = A->rowptr;
-  m.brp = B->rowptr;
-  m.order = order;
-  m.nbig = nb;
-  m.scratch = 0;
-  if (nb > 0) {
-    int32_t* ub;
-    BAMG_TRY(arena_get(ctx, (size_t)nb + 1, &ub));
-    BAMG_LAUNCH(ctx, spgemm_big_ub_kernel, grid_for(nb, 128), 128, 0, nb, m.list, A->rowptr, A->col, B->rowptr, ub);
-    BAMG_TRY(scan_i32(ctx, ub, m.off, nb, &m.scratch));
-    int32_t *skey;
-    double* sval;
-    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &skey));
-    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &sval));
-    BAMG_LAUNCH(ctx, spgemm_big_kernel<0>, grid_for(nb, 128), 128, 0, nb, m.list, A->rowptr, A->col, A->val,
-                B->rowptr, B->col, B->val, m.off, skey, sval, order, cnt, (const int32_t*)nullptr,
-                (int32_t*)nullptr, (double*)nullptr);
+  if (const char* e = getenv("BAMG_SPGEMM_POOL")) {  // tests: start from a tiny pool (exercises the regrowth)
+    cudaFree(m.pkey);
+    cudaFree(m.pval);
+    m.pkey = nullptr;
+    m.pval = nullptr;
+    m.pcap = 0;
+    BAMG_TRY(pool_reserve(ctx, m, atoll(e) > 0 ? atoll(e) : 1));
   }
-  return scan_i32(ctx, cnt, rowptr_c, n, nnz_host);
+  BAMG_TRY(pool_reserve(ctx, m, (int64_t)1 << 20));
+  int32_t* cnt;
+  // m.stat: [0] pool words used, [1] flagged rows (32-bit counter in the low
+  // half), [2] nnz(C) from the scan -- one memset, one read
+  unsigned int* nbig = m.nbig_dev;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cnt));
+  const int bgrid = ctx->num_sms * 2;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(m.stat, 0, sizeof(unsigned long long) * 4, ctx->stream));
+    BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
+                    A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
+                    (int32_t*)nullptr, (double*)nullptr, m.tcol, m.tval, m.parked, (const int32_t*)nullptr,
+                    (const unsigned int*)nullptr);
+    BAMG_LAUNCH(ctx, spgemm_big_kernel<0>, bgrid, 128, 0, (const unsigned int*)nbig, m.list, A->rowptr, A->col,
+                A->val, B->rowptr, B->col, B->val, m.off, m.pkey, m.pval, order, cnt, (const int32_t*)nullptr,
+                (int32_t*)nullptr, (double*)nullptr, m.stat, (long long)m.pcap);
+    BAMG_TRY(scan_i32_dev(ctx, cnt, rowptr_c, n, reinterpret_cast<int64_t*>(m.stat + 2)));
+    unsigned long long st[3];
+    BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(m.stat), 3, reinterpret_cast<int64_t*>(st)));
+    st[1] &= 0xffffffffull;
+    if ((int64_t)st[0] > m.pcap) {  // slow-path rows did not fit: grow the pool, recount
+      BAMG_REQUIRE(ctx, attempt == 0, "SpGEMM scratch pool overflow after regrowth");
+      BAMG_TRY(pool_reserve(ctx, m, (int64_t)st[0] + ((int64_t)st[0] >> 2)));
+      continue;
+    }
+    m.arp = A->rowptr;
+    m.brp = B->rowptr;
+    m.order = order;
+    m.nbig = (int)st[1];
+    *nnz_host = (int64_t)st[2];
+    return 0;
+  }
+  return -2;
 }
 
 extern "C" int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
@@ -358,12 +400,9 @@ extern "C" int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr
                     (const int32_t*)m.redo, (const unsigned int*)m.nredo);
   }
   if (m.nbig > 0) {
-    int32_t* skey;
-    double* sval;
-    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &skey));
-    BAMG_TRY(arena_get(ctx, (size_t)m.scratch + 1, &sval));
-    BAMG_LAUNCH(ctx, spgemm_big_kernel<1>, grid_for(m.nbig, 128), 128, 0, m.nbig, m.list, A->rowptr, A->col, A->val,
-                B->rowptr, B->col, B->val, m.off, skey, sval, order, (int32_t*)nullptr, rowptr_c, col_c, val_c);
+    BAMG_LAUNCH(ctx, spgemm_big_kernel<1>, grid_for(m.nbig, 128), 128, 0, (const unsigned int*)m.nbig_dev, m.list,
+                A->rowptr, A->col, A->val, B->rowptr, B->col, B->val, m.off, m.pkey, m.pval, order, (int32_t*)nullptr,
+                rowptr_c, col_c, val_c, (unsigned long long*)nullptr, (long long)0);
   }
   return 0;
 }

@@ -208,6 +208,25 @@ def fit_rows(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg, ri
     return cnt, col, val, (int(status[0]), int(status[1]))
 
 
+def fit_rows_csr(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg, ncols, ridge=None):
+    """fit_rows + rows_to_csr with one host read: (DeviceCSR, (pinv_branch_fits, deferred))."""
+    n, k = X.shape
+    cnt = _empty(n, I32)
+    col = _empty(n * caliber, I32)
+    val = _empty(n * caliber, F64)
+    rp = _empty(n + 1, I32)
+    status = (C.c_int64 * 2)()
+    nnz = C.c_int64(0)
+    _lib.call("bamg_fit_rows_csr", adj.ref(), _p(coarse_rank), _p(X), _p(w), n, k, int(caliber),
+              int(radius), float(tol), int(bool(constrain)), int(bool(nonneg)),
+              -1.0 if ridge is None else float(ridge), _p(cnt), _p(col), _p(val), _p(rp), status,
+              C.byref(nnz))
+    ci = _empty(max(nnz.value, 1), I32)
+    va = _empty(max(nnz.value, 1), F64)
+    _lib.call("bamg_rows_fill", _p(cnt), _p(col), _p(val), n, int(caliber), _p(rp), _p(ci), _p(va))
+    return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (n, ncols)), (int(status[0]), int(status[1]))
+
+
 def rows_to_csr(cnt, col, val, n, stride, ncols) -> DeviceCSR:
     rp = _empty(n + 1, I32)
     nnz = C.c_int64(0)

@@ -81,11 +81,10 @@ def singular_test_weights(B, vectors, transpose_side: bool = False, infinite_slo
 def _build_rows(adj: DeviceCSR, split: CfSplitting, tests: WeightedTestSet, cfg: InterpConfig,
                 constrain: bool) -> DeviceCSR:
     """(n, n_c) operator: identity on C points, greedy LS rows on F points (interp.py:252-289)."""
-    n = split.n
-    cnt, col, val, fallbacks = engine.fit_rows(adj, split.dcrank, tests.dvectors, tests.dweights,
-                                               cfg.caliber, cfg.search_radius, cfg.improvement_tol,
-                                               constrain, cfg.nonnegative)
-    return engine.rows_to_csr(cnt, col, val, n, cfg.caliber, split.n_coarse)
+    R, fallbacks = engine.fit_rows_csr(adj, split.dcrank, tests.dvectors, tests.dweights,
+                                       cfg.caliber, cfg.search_radius, cfg.improvement_tol,
+                                       constrain, cfg.nonnegative, split.n_coarse)
+    return R
 
 
 def build_interpolation(B, split: CfSplitting, tests: WeightedTestSet, cfg: InterpConfig,

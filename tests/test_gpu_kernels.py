@@ -217,14 +217,19 @@ def test_dense_pinv_bordered_lu_matches_svd(eng, golden, name, monkeypatch):
         assert np.abs(Z - ref).max() <= 1e-9 * np.abs(ref).max(), force
 
 
+@pytest.mark.parametrize("pool", [None, "64"])
 @pytest.mark.parametrize("shape", [(300, 400, 500, 0.05, 0.03), (500, 500, 500, 0.004, 0.004)])
-def test_spgemm_matches_scipy_storage_order_and_canonical(eng, shape):
+def test_spgemm_matches_scipy_storage_order_and_canonical(eng, shape, pool, monkeypatch):
     """C = A B with scipy csr_matmat semantics: order 1 reproduces scipy's raw
     product arrays (reverse-first-touch rows) bit for bit, order 0 the
     canonical make_csr form.  The first shape has rows with > 64 distinct
-    columns (global-scratch slow path), the second only fast-path rows."""
+    columns (global-scratch slow path), the second only fast-path rows.
+    pool = 64 starts the slow-path scratch pool at 64 entries, so the count
+    overflows it, grows it and recounts."""
     from scipy import sparse as sp
     from paper_1402_4005_b200 import engine
+    if pool:
+        monkeypatch.setenv("BAMG_SPGEMM_POOL", pool)
     m, k, n, da, db = shape
     rng = np.random.default_rng(m + n)
     A = sp.random_array((m, k), density=da, format="csr", random_state=rng)
