@@ -86,10 +86,64 @@ __global__ void rank_scatter_kernel(const int32_t* __restrict__ idx, const int32
   if (i < n) rank[idx[i]] = pos[i] + f[i];  // inclusive count of "new value" flags
 }
 
+// Integer-coordinate fast path (lattice chains store grid positions): when
+// every value is an integer in [0, 2^24), np.unique's inverse is the prefix
+// count of the present values -- presence flags, one scan, one gather -- in
+// place of the 64-bit LSD radix sort (~3 launches per varying key bit).
+constexpr int64_t INT_RANK_MAX = 1 << 24;
+
+__global__ void int_probe_kernel(const double* __restrict__ coord, int64_t n, unsigned int* __restrict__ probe) {
+  BAMG_PDL_PROLOGUE();
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool ok = true;
+  int v = 0;
+  if (i < n) {
+    const double x = coord[i];
+    ok = x >= 0.0 && x < (double)INT_RANK_MAX && x == floor(x);
+    v = ok ? (int)x : 0;
+  }
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(probe, 1u);
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(probe + 1, (unsigned)v);
+}
+
+__global__ void int_presence_kernel(const double* __restrict__ coord, int64_t n, uint8_t* __restrict__ present) {
+  BAMG_PDL_PROLOGUE();
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) present[(int)coord[i]] = 1;
+}
+
+__global__ void int_rank_kernel(const double* __restrict__ coord, int64_t n, const int32_t* __restrict__ pos,
+                                int32_t* __restrict__ rank) {
+  BAMG_PDL_PROLOGUE();
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rank[i] = pos[(int)coord[i]];
+}
+
 extern "C" int bamg_axis_ranks(bamg_ctx* ctx, const double* coord, int64_t n, int32_t* rank, int64_t* nvalues_host) {
   ctx->arena.reset();
   if (nvalues_host) *nvalues_host = 0;
   if (n == 0) return 0;
+  {
+    unsigned int* probe;
+    BAMG_TRY(arena_get(ctx, 2, &probe));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(probe, 0, 2 * sizeof(unsigned int), ctx->stream));
+    BAMG_LAUNCH(ctx, int_probe_kernel, grid_for(n, 256), 256, 0, coord, n, probe);
+    unsigned int pr[2];
+    BAMG_TRY(ctx_read_i32(ctx, reinterpret_cast<const int32_t*>(probe), 2, reinterpret_cast<int32_t*>(pr)));
+    if (pr[0] == 0u) {
+      const int64_t R = (int64_t)pr[1] + 1;  // values in [0, R)
+      uint8_t* present;
+      int32_t* pos;
+      BAMG_TRY(arena_get(ctx, (size_t)R + 1, &present));
+      BAMG_TRY(arena_get(ctx, (size_t)R + 1, &pos));
+      BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(present, 0, (size_t)R + 1, ctx->stream));
+      BAMG_LAUNCH(ctx, int_presence_kernel, grid_for(n, 256), 256, 0, coord, n, present);
+      BAMG_TRY(scan_u8(ctx, present, pos, R, nvalues_host));
+      BAMG_LAUNCH(ctx, int_rank_kernel, grid_for(n, 256), 256, 0, coord, n, (const int32_t*)pos, rank);
+      return 0;
+    }
+  }
   unsigned long long *k1, *k2, *orand;
   int32_t *i1, *i2, *pos;
   uint8_t* flag;

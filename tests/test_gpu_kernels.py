@@ -250,3 +250,29 @@ def test_spgemm_matches_scipy_storage_order_and_canonical(eng, shape, pool, monk
     ref = orc.canon(raw)
     assert np.array_equal(C0.indptr, ref.indptr) and np.array_equal(C0.indices, ref.indices)
     assert np.array_equal(C0.data, ref.data)
+
+
+@pytest.mark.parametrize("kind", ["lattice", "lattice_sparse", "negative", "fractional", "signed_zero"])
+def test_axis_ranks_match_numpy_unique_inverse(eng, kind):
+    """Per-axis ranks among the distinct coordinate values (np.unique's inverse,
+    coarsen.py:90-109): the integer presence/scan fast path (lattice
+    coordinates) and the 64-bit radix path (everything else) agree with numpy."""
+    from paper_1402_4005_b200 import engine
+    rng = np.random.default_rng(7)
+    n = 50_000
+    if kind == "lattice":
+        x = rng.integers(0, 1024, n).astype(np.float64)
+    elif kind == "lattice_sparse":
+        x = (rng.integers(0, 300, n) * 37).astype(np.float64)
+    elif kind == "negative":
+        x = rng.integers(-500, 500, n).astype(np.float64)
+    elif kind == "fractional":
+        x = np.round(rng.random(n) * 1000, 3)
+    else:
+        x = rng.integers(0, 3, n).astype(np.float64) - 1.0
+        x[x == 0] = -0.0
+        x[::7] = 0.0
+    rank, nv = engine.axis_ranks(dvec(x))
+    vals, inv = np.unique(x, return_inverse=True)
+    assert nv == len(vals)
+    assert np.array_equal(rank.cpu().numpy(), inv.astype(np.int32))
