@@ -197,7 +197,7 @@ static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, dou
 // L2, the solved entries broadcast from shared memory).  Replaces the blocked
 // path's ~4 launches per 64 rows (tri_inv + 2 GEMMs + copy) with one launch.
 constexpr int TRSM_MAX_N = 2048;
-constexpr int TRSM_RB = 8;
+constexpr int TRSM_RB = 2;  // right-hand sides per CTA: n = 256, m = 256 -> 128 CTAs
 __global__ void __launch_bounds__(256) trsm_small_kernel(const double* __restrict__ T, int n, int lower_stored,
                                                          int unit, int trans, double* __restrict__ B, int ldb, int m) {
   BAMG_PDL_PROLOGUE();

@@ -21,17 +21,23 @@
 // X[:, c] /= peak[c] when peak[c] > 1e100 (bootstrap.py:302-306), both sides
 // in one launch: elements [0, total) of X0 with peak[0..k), then X1 with
 // peak[k..2k)
+// Fixed grid, grid-stride; every CTA first checks the 2k peaks and leaves at
+// once when none exceeds the threshold (the common case), so a sweep's
+// rescale costs one short launch instead of a thread per vector entry.
 __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1, int64_t total, int k,
                                const double* __restrict__ peak) {
   BAMG_PDL_PROLOGUE();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 2 * total) return;
-  const bool second = i >= total;
-  const int64_t j = second ? i - total : i;
-  double p = peak[(second ? k : 0) + j % k];
-  if (p > 1e100) {
-    double* X = second ? X1 : X0;
-    X[j] = X[j] / p;
+  const int t = threadIdx.x;
+  const bool big = t < 2 * k && peak[t] > 1e100;
+  if (!__syncthreads_or(big)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < 2 * total; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool second = i >= total;
+    const int64_t j = second ? i - total : i;
+    double p = peak[(second ? k : 0) + j % k];
+    if (p > 1e100) {
+      double* X = second ? X1 : X0;
+      X[j] = X[j] / p;
+    }
   }
 }
 
@@ -227,7 +233,9 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
       BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak, rd));
       BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k, rd));
       if (smooth == 1) {  // init_test_vectors (smooth == 2) has no runaway rescaling
-        BAMG_LAUNCH(ctx, rescale_kernel, grid_for(2 * total, 256), 256, 0, vo, uo, total, k, peak);
+        const int rg = grid_for(2 * total, 256);
+        BAMG_LAUNCH(ctx, rescale_kernel, rg < ctx->num_sms * 8 ? rg : ctx->num_sms * 8, 256, 0, vo, uo, total, k,
+                    peak);
       }
       std::swap(u, uo);
       std::swap(v, vo);
