@@ -1305,7 +1305,7 @@ __device__ void sub_cholqr_pass(cg::grid_group& grid, double* Y, int n, double* 
 }
 
 template <int P>
-__global__ void __launch_bounds__(SUB_THREADS) subspace_coop_kernel(const double* __restrict__ Kp,
+__global__ void __launch_bounds__(SUB_THREADS, 1) subspace_coop_kernel(const double* __restrict__ Kp,
                                                                     const double* __restrict__ Kt, int n, double* Y,
                                                                     double* Z, int iters, double* partial,
                                                                     double* G) {
@@ -1323,6 +1323,151 @@ __global__ void __launch_bounds__(SUB_THREADS) subspace_coop_kernel(const double
     sub_cholqr_pass<P>(grid, Y, n, partial, G, sL, sRd);
     sub_cholqr_pass<P>(grid, Y, n, partial, G, sL, sRd);
   }
+}
+
+// ------------------------------------- subspace iteration on one cluster
+// The same 5-step block for n <= SUBC_MAX_N on ONE thread-block cluster of 8
+// CTAs: CTA c owns rows [c*R, c*R + R) of Y and Z in shared memory; a product
+// first gathers the whole other block over DSMEM into local shared memory,
+// then forms the CTA's rows (columns of K^+ / K^+T read from L2); a CholQR
+// pass sums the 8 per-CTA partial Gram matrices over DSMEM in a fixed order,
+// factors in one warp (warp_chol_smem) and updates the CTA's rows.  Six
+// cluster barriers per step (~0.3 us each) instead of ~13 grid barriers.
+constexpr int SUBC_CS = 8;
+constexpr int SUBC_MAX_N = 512;
+constexpr int SUBC_THREADS = 256;
+
+template <int P>
+__device__ __noinline__ void subc_gather(cg::cluster_group& cl, const double* myblk, double* full, int n, int R) {
+  // full[row * P + c] for every row: rows of CTA q come from q's block
+  const int total = n * P;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int row = e / P, c = e - row * P;
+    const int q = row / R, r = row - q * R;
+    const double* src = cl.map_shared_rank(myblk, q);
+    full[e] = src[r * P + c];
+  }
+}
+
+template <int P>
+__device__ __noinline__ void subc_product(const double* __restrict__ Mcols, int n, int r0, int rn, const double* full,
+                             double* myblk) {
+  // myblk[r][c] = sum_i Mcols[(r0 + r) * n + i] full[i][c]; warp per row
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < rn; r += nw) {
+    double acc[P];
+#pragma unroll
+    for (int c = 0; c < P; ++c) acc[c] = 0.0;
+    const double* col = Mcols + (int64_t)(r0 + r) * n;
+    for (int i = lane; i < n; i += 32) {
+      const double m = __ldg(col + i);
+      const double* fr = full + i * P;
+#pragma unroll
+      for (int c = 0; c < P; ++c) acc[c] += m * fr[c];
+    }
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      double v = acc[c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == c) myblk[r * P + c] = v;
+    }
+  }
+}
+
+template <int P>
+__device__ __noinline__ void subc_cholqr(cg::cluster_group& cl, double* myblk, int rn, double* gpart, double* G, double* sL,
+                            double* sRd) {
+  constexpr int PP = P * P;
+  for (int e = threadIdx.x; e < PP; e += blockDim.x) {
+    const int a = e % P, b = e / P;
+    double v = 0.0;
+    if (a <= b)
+      for (int r = 0; r < rn; ++r) v += myblk[r * P + a] * myblk[r * P + b];
+    gpart[e] = v;
+  }
+  cl.sync();
+  for (int e = threadIdx.x; e < PP; e += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < SUBC_CS; ++q) v += cl.map_shared_rank(gpart, q)[e];  // fixed order
+    G[e] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane < P)
+      for (int j = 0; j < P; ++j) {
+        const int lo = lane < j ? lane : j, hi = lane < j ? j : lane;
+        sL[lane * (P + 1) + j] = G[hi * P + lo];
+      }
+    __syncwarp();
+    warp_chol_smem<P>(sL, sRd, lane);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < rn; r += blockDim.x) {
+    double x[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) x[i] = myblk[r * P + i];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      x[j] *= sRd[j];
+#pragma unroll
+      for (int i = j + 1; i < P; ++i) x[i] -= sL[i * (P + 1) + j] * x[j];
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) myblk[r * P + i] = x[i];
+  }
+  __syncthreads();
+}
+
+template <int P>
+__global__ void __launch_bounds__(SUBC_THREADS, 1) subspace_cluster_kernel(const double* __restrict__ Kp,
+                                                                        const double* __restrict__ Kt, int n,
+                                                                        double* Y, double* Z, int iters) {
+  BAMG_PDL_PROLOGUE();
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double dsm[];
+  const int c = (int)cl.block_rank();
+  const int R = (n + SUBC_CS - 1) / SUBC_CS;
+  const int r0 = c * R, rn = max(0, min(R, n - r0));
+  double* sY = dsm;              // R x P (row-major)
+  double* sZ = sY + R * P;       // R x P
+  double* full = sZ + R * P;     // n x P
+  double* gpart = full + n * P;  // 2 x P x P (pass parity)
+  double* G = gpart + 2 * P * P;
+  __shared__ double sL[P * (P + 1)];
+  __shared__ double sRd[P];
+  for (int e = threadIdx.x; e < R * P; e += blockDim.x) {
+    const int r = e / P, cc = e - r * P;
+    sY[e] = r < rn ? Y[(int64_t)cc * n + r0 + r] : 0.0;
+  }
+  int pass = 0;
+  for (int it = 0; it < iters; ++it) {
+    cl.sync();  // every CTA's Y rows are final
+    subc_gather<P>(cl, sY, full, n, R);
+    __syncthreads();
+    subc_product<P>(Kp, n, r0, rn, full, sZ);  // Z = K^+T Y (row j of K^+T = column j of K^+)
+    __syncthreads();
+    subc_cholqr<P>(cl, sZ, rn, gpart + (pass++ & 1) * P * P, G, sL, sRd);
+    subc_cholqr<P>(cl, sZ, rn, gpart + (pass++ & 1) * P * P, G, sL, sRd);
+    cl.sync();
+    subc_gather<P>(cl, sZ, full, n, R);
+    __syncthreads();
+    subc_product<P>(Kt, n, r0, rn, full, sY);  // Y = K^+ Z (row i of K^+ = column i of Kt)
+    __syncthreads();
+    subc_cholqr<P>(cl, sY, rn, gpart + (pass++ & 1) * P * P, G, sL, sRd);
+    subc_cholqr<P>(cl, sY, rn, gpart + (pass++ & 1) * P * P, G, sL, sRd);
+  }
+  for (int e = threadIdx.x; e < rn * P; e += blockDim.x) {
+    const int r = e / P, cc = e - r * P;
+    Y[(int64_t)cc * n + r0 + r] = sY[e];
+    Z[(int64_t)cc * n + r0 + r] = sZ[e];
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+static bool subspace_cluster_enabled() {
+  const char* e = getenv("BAMG_SUBSPACE_COOP");  // development: force the cooperative-grid kernel
+  return !(e && e[0] == '1');
 }
 
 static bool subspace_fused_enabled() {
@@ -1585,8 +1730,50 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     BAMG_TRY(arena_get(ctx, (size_t)p * p, &Gsum));
     BAMG_TRY(transpose_sq(ctx, Kp, n, Kt));
   }
+  // one cluster of 8 CTAs for n <= 512 (shared-memory blocks + DSMEM)
+  const void* subc_kern = nullptr;
+  switch (p) {
+    case 16: subc_kern = (const void*)subspace_cluster_kernel<16>; break;
+    case 20: subc_kern = (const void*)subspace_cluster_kernel<20>; break;
+    case 24: subc_kern = (const void*)subspace_cluster_kernel<24>; break;
+    case 28: subc_kern = (const void*)subspace_cluster_kernel<28>; break;
+    case 32: subc_kern = (const void*)subspace_cluster_kernel<32>; break;
+    default: break;
+  }
+  const int subc_R = (n + SUBC_CS - 1) / SUBC_CS;
+  const size_t subc_smem = sizeof(double) * ((size_t)2 * subc_R * p + (size_t)n * p + 3 * (size_t)p * p);
+  const bool clustered = fused && subc_kern && n <= SUBC_MAX_N && subc_smem <= 200 * 1024 &&
+                         subspace_cluster_enabled();
+  if (clustered)
+    BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(subc_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)subc_smem));
   auto block5_fused = [&]() -> int {
     int five = 5;
+    if (clustered) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(SUBC_CS);
+      cfg.blockDim = dim3(SUBC_THREADS);
+      cfg.dynamicSmemBytes = subc_smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = SUBC_CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const double* kp = Kp;
+      const double* kt = Kt;
+      void* args[] = {(void*)&kp, (void*)&kt, (void*)&n, &Y, &Z, &five};
+      if (ctx->trace.on) trace_mark(ctx, "subspace_cluster_kernel");
+      BAMG_CHECK_CUDA(ctx, cudaLaunchKernelExC(&cfg, subc_kern, args));
+      ctx->launches++;
+      if (ctx->trace.on) trace_mark(ctx, nullptr);
+      stage("@sub_kernel");
+      BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Kp, n, Y, n, 0.0, Z, n));
+      int rc = jacobi_svd_public(ctx, Z, n, p, Vs, sv);
+      stage("@sub_check");
+      return rc;
+    }
     void* args[] = {&Kp, &Kt, (void*)&n, &Y, &Z, &five, &partial, &Gsum};
     if (ctx->trace.on) trace_mark(ctx, "subspace_coop_kernel");
     BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel(sub_kern, dim3(sub_grid), dim3(SUB_THREADS), args, 0,
