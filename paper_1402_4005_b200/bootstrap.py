@@ -300,7 +300,10 @@ def coarsest_triplets(B, M, N, r: int) -> TripletSet:
     Bd = engine.csr_to_dense(A)
     Mdd = engine.csr_to_dense(Md)
     Ndd = engine.csr_to_dense(Nd)
-    U, V, s, Z = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r, with_pinv=True)
+    # the derived B^+ is one more dense n x n block alive next to B, M, N, K and
+    # K^+ (5 x 18 GB at cfg3's n = 47,824): above 4 GB the V-cycle factorises
+    # B itself after the setup's dense temporaries are gone
+    U, V, s, Z = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r, with_pinv=8 * n * n <= (4 << 30))
     trips = TripletSet(s, U, V)
     # B's pseudo-inverse from the same factors (large path): the V-cycle takes
     # it instead of factorising B again (solver.VCycleOperator)

@@ -298,9 +298,10 @@ def dense_pinv(Dcm, n, rank_tol=1e-12):
 
 
 def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
-    """(U, V, sigma[, Z]): with `with_pinv`, Z is B's row-major pseudo-inverse
-    derived from the triplet solve's factors, or None when that path did not
-    run or was not certified (the caller then builds it with dense_pinv)."""
+    """(U, V, sigma, Z): with `with_pinv`, Z is B's row-major pseudo-inverse
+    derived from the triplet solve's factors; None when not requested, when
+    that path did not run or was not certified (the caller then builds it
+    with dense_pinv)."""
     take = min(r, n)
     U = _empty((n, take))
     V = _empty((n, take))
@@ -316,7 +317,7 @@ def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
         raise ValueError("matrix is not positive definite (coarsest mass matrix)")
     if with_pinv:
         return U, V, s, (Z if ok.value else None)
-    return U, V, s
+    return U, V, s, None
 
 
 def sign_fix_l1(x, stride=1, uniform_fallback=False):

@@ -15,6 +15,6 @@ for side in sides:
         torch.cuda.synchronize(); t = time.perf_counter()
         Z = engine.dense_pinv(D, prob.n)
         torch.cuda.synchronize(); t1 = time.perf_counter()
-        U, V, s = engine.coarsest_triplets(D, M, M, prob.n, 16)
+        U, V, s, _ = engine.coarsest_triplets(D, M, M, prob.n, 16)
         torch.cuda.synchronize(); t2 = time.perf_counter()
     print(f"n={prob.n} pinv {1e3*(t1-t):.2f} ms triplets {1e3*(t2-t1):.2f} ms sig0={s[0].item():.3e} sig1={s[1].item():.3e}", flush=True)

@@ -1,7 +1,7 @@
 """DRAM traffic per launch of the CSR row-kernel family over one bench step.
 
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      -k regex:"csr_rows_kernel|csr_tile_kernel" --csv --log-file t.csv \
+      -k regex:"csr_rows_kernel|csr_tile_kernel|rayleigh_fused_kernel" --csv --log-file t.csv \
       python tools/steptimes.py --steps 1
   python tools/family_traffic.py t.csv profiles/r01_csr_family_traffic.json
 
