@@ -279,18 +279,22 @@ extern "C" int bamg_col_dots(bamg_ctx* ctx, const double* X, const double* Y, in
   return colreduce(ctx, X, Y, n, k, 1, out, 0);
 }
 
-__global__ void col_scale_div_kernel(double* X, int64_t total, int k, const double* s) {
+// n x k block kernels: one thread per row walking its k entries (no 64-bit
+// div/mod per element; a row is one contiguous 8k-byte segment)
+__global__ void col_scale_div_kernel(double* X, int64_t n, int k, const double* s) {
   BAMG_PDL_PROLOGUE();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  double d = s[i % k];
-  if (d == 0.0) d = 1.0;
-  X[i] = X[i] / d;
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double* x = X + r * k;
+  for (int c = 0; c < k; ++c) {
+    double d = s[c];
+    if (d == 0.0) d = 1.0;
+    x[c] = x[c] / d;
+  }
 }
 
 int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
-  int64_t total = n * k;
-  BAMG_LAUNCH(ctx, col_scale_div_kernel, grid_for(total, 256), 256, 0, X, total, k, s);
+  BAMG_LAUNCH(ctx, col_scale_div_kernel, grid_for(n, 256), 256, 0, X, n, k, s);
   return 0;
 }
 
@@ -316,16 +320,16 @@ extern "C" int bamg_col_fill(bamg_ctx* ctx, double* X, int64_t n, int k, int c, 
 __global__ void gather_rows_kernel(const double* __restrict__ X, const int32_t* __restrict__ idx,
                                    int64_t m, int k, double* __restrict__ Y) {
   BAMG_PDL_PROLOGUE();
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m * k) return;
-  int64_t r = t / k;
-  int c = (int)(t - r * k);
-  Y[t] = X[(int64_t)idx[r] * k + c];
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const double* x = X + (int64_t)idx[r] * k;
+  double* y = Y + r * k;
+  for (int c = 0; c < k; ++c) y[c] = x[c];
 }
 
 extern "C" int bamg_gather_rows(bamg_ctx* ctx, const double* X, const int32_t* idx, int64_t m,
                                 int k, double* Y) {
-  BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m * k, 256), 256, 0, X, idx, m, k, Y);
+  BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m, 256), 256, 0, X, idx, m, k, Y);
   return 0;
 }
 
@@ -335,11 +339,14 @@ struct Perm32 {
 
 __global__ void permute_cols_kernel(const double* __restrict__ X, int64_t n, int k, Perm32 perm, double* __restrict__ Y) {
   BAMG_PDL_PROLOGUE();
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * k) return;
-  int64_t r = t / k;
-  int c = (int)(t - r * k);
-  Y[t] = X[r * k + perm.p[c]];
+  __shared__ int sp[32];
+  if (threadIdx.x < 32) sp[threadIdx.x] = perm.p[threadIdx.x];
+  __syncthreads();
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double* x = X + r * k;
+  double* y = Y + r * k;
+  for (int c = 0; c < k; ++c) y[c] = x[sp[c]];
 }
 
 extern "C" int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int k, const int32_t* perm_host,
@@ -347,7 +354,7 @@ extern "C" int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int 
   BAMG_REQUIRE(ctx, k >= 1 && k <= 32 && X != Y, "k in [1, 32] and distinct buffers");
   Perm32 p{};
   for (int c = 0; c < k; ++c) p.p[c] = perm_host[c];
-  BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n * k, 256), 256, 0, X, n, k, p, Y);
+  BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n, 256), 256, 0, X, n, k, p, Y);
   return 0;
 }
 

@@ -30,13 +30,14 @@ __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1,
   const int t = threadIdx.x;
   const bool big = t < 2 * k && peak[t] > 1e100;
   if (!__syncthreads_or(big)) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < 2 * total; i += (int64_t)gridDim.x * blockDim.x) {
-    const bool second = i >= total;
-    const int64_t j = second ? i - total : i;
-    double p = peak[(second ? k : 0) + j % k];
-    if (p > 1e100) {
-      double* X = second ? X1 : X0;
-      X[j] = X[j] / p;
+  const int64_t n = total / k;  // rows per block; thread per row
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool second = i >= n;
+    double* x = (second ? X1 : X0) + (second ? i - n : i) * k;
+    const double* pk = peak + (second ? k : 0);
+    for (int c = 0; c < k; ++c) {
+      const double p = pk[c];
+      if (p > 1e100) x[c] = x[c] / p;
     }
   }
 }
@@ -44,9 +45,11 @@ __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1,
 // u_c <- -u_c for flagged columns
 __global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ flip) {
   BAMG_PDL_PROLOGUE();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  if (flip[i % k] != 0.0) X[i] = -X[i];
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // thread per row
+  if (r >= total / k) return;
+  double* x = X + r * k;
+  for (int c = 0; c < k; ++c)
+    if (flip[c] != 0.0) x[c] = -x[c];
 }
 
 // three column-dot sums in one pass (a.b, c.d, e.f per column), then -- in
@@ -146,7 +149,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
     if (rc == 0) {
       if (mode == 1 && U_flip_or_null) {
         int64_t total = n * k;
-        BAMG_LAUNCH(ctx, flip_kernel, grid_for(total, 256), 256, 0, U_flip_or_null, total, k, flip);
+        BAMG_LAUNCH(ctx, flip_kernel, grid_for(total / k, 256), 256, 0, U_flip_or_null, total, k, flip);
       }
       return 0;
     }
@@ -173,7 +176,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
               ctx->counters + 1, dots, sigma, flip, mode);
   if (mode == 1 && U_flip_or_null) {
     int64_t total = n * k;
-    BAMG_LAUNCH(ctx, flip_kernel, grid_for(total, 256), 256, 0, U_flip_or_null, total, k, flip);
+    BAMG_LAUNCH(ctx, flip_kernel, grid_for(total / k, 256), 256, 0, U_flip_or_null, total, k, flip);
   }
   return 0;
 }
@@ -233,7 +236,7 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
       BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak, rd));
       BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k, rd));
       if (smooth == 1) {  // init_test_vectors (smooth == 2) has no runaway rescaling
-        const int rg = grid_for(2 * total, 256);
+        const int rg = grid_for(2 * n, 256);
         BAMG_LAUNCH(ctx, rescale_kernel, rg < ctx->num_sms * 8 ? rg : ctx->num_sms * 8, 256, 0, vo, uo, total, k,
                     peak);
       }

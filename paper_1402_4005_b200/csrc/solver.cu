@@ -266,7 +266,10 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
 }
 
 static bool graphs_enabled(bamg_ctx* ctx) {
-  if (ctx->trace.on) return false;  // the development trace wants every launch
+  // the development trace wants every launch, unless BAMG_TRACE_GRAPHS=1 (one
+  // timeline entry per V-cycle graph replay)
+  const char* tg = getenv("BAMG_TRACE_GRAPHS");
+  if (ctx->trace.on && !(tg && tg[0] == '1')) return false;
   const char* e = getenv("BAMG_NO_GRAPHS");
   return !(e && e[0] == '1');
 }
@@ -288,6 +291,8 @@ static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
     int64_t l0 = ctx->launches;
     unsigned saved_mask = ctx->prof.mask;  // no profiler events inside the graph
     ctx->prof.mask = 0;
+    const bool saved_trace = ctx->trace.on;  // nor trace events
+    ctx->trace.on = false;
     ctx->stream = cap;
     cudaGraph_t graph;
     cudaError_t e1 = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
@@ -295,6 +300,7 @@ static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     ctx->stream = saved;
     ctx->prof.mask = saved_mask;
+    ctx->trace.on = saved_trace;
     int nk = (int)(ctx->launches - l0);
     ctx->launches = l0;
     if (e1 != cudaSuccess || e2 != cudaSuccess || rc != 0) {
@@ -320,7 +326,9 @@ static int vcycle_run(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x) {
     h->graphs.push_back({b, x, exec, nk});
     g = &h->graphs.back();
   }
+  if (ctx->trace.on) trace_mark(ctx, "vcycle_graph");
   BAMG_CHECK_CUDA(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+  if (ctx->trace.on) trace_mark(ctx, nullptr);
   ctx->launches += g->nkernels;
   return 0;
 }

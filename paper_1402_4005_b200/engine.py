@@ -246,13 +246,16 @@ def axis_ranks(coord):
     return rank, nv.value
 
 
-def rerank(parent_rank, coarse_idx, nvalues_parent):
+def rerank(parent_rank, coarse_idx, nvalues_parent, exact=False):
+    """Dense ranks of the coarse points' values.  The distinct-value count is
+    only ever a buffer bound for the next rerank, so by default it is not read
+    back (the parent's count bounds it; no host synchronisation)."""
     nc = coarse_idx.numel()
     out = _empty(nc, I32)
     nv = C.c_int64(0)
     _lib.call("bamg_rerank", _p(parent_rank), _p(coarse_idx), nc, int(nvalues_parent), _p(out),
-              C.byref(nv))
-    return out, nv.value
+              C.byref(nv) if exact else None)
+    return out, (nv.value if exact else int(nvalues_parent))
 
 
 def even_mask(ranks):
