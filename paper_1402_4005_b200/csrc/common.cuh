@@ -300,8 +300,16 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 // Deterministic column reductions over n x k interleaved blocks: a fixed grid
 // of partial sums (rows chunked contiguously), then a fixed tree.
-constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs; constant => bit-reproducible
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs at most
 constexpr int RED_THREADS = 256;
+// CTAs of a deterministic column reduction over n rows: a fixed function of n
+// (so the partial-sum tree is reproducible run to run), ~2,048 rows per CTA,
+// so a coarse level's reduction is one or a few CTAs instead of 296 near-empty
+// ones and a 296-way finish.
+static inline int red_blocks_for(int64_t n) {
+  const int64_t b = (n + 2047) / 2048;
+  return b < 1 ? 1 : (b > RED_BLOCKS ? RED_BLOCKS : (int)b);
+}
 
 // compute partial[b * k + c] for op(x, y) summed over the rows of block b.
 // kinds: 0 = x*x, 1 = x*y

@@ -263,8 +263,8 @@ int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
   BAMG_REQUIRE(ctx, k >= 1 && k <= KMAX, "k must lie in [1, 32]");
   double* partial = nullptr;
   BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * k, &partial));
-  BAMG_LAUNCH(ctx, colreduce_kernel, RED_BLOCKS, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
-              out_dev, take_sqrt);
+  BAMG_LAUNCH(ctx, colreduce_kernel, red_blocks_for(n), RED_THREADS, 0, X, Y, n, k, kind, partial,
+              ctx->counters + 0, out_dev, take_sqrt);
   return 0;
 }
 

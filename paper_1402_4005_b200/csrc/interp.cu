@@ -1173,8 +1173,9 @@ static int fit_rows_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* co
   if (ridge_override >= 0.0) {
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(lam, &ridge_override, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   } else {
-    BAMG_LAUNCH(ctx, level_scale_partial, RED_BLOCKS, RED_THREADS, 0, X, n, k, w, partial);
-    BAMG_LAUNCH(ctx, level_scale_final, 1, 32, 0, partial, RED_BLOCKS, n, lam);
+    const int nbl = red_blocks_for(n);
+    BAMG_LAUNCH(ctx, level_scale_partial, nbl, RED_THREADS, 0, X, n, k, w, partial);
+    BAMG_LAUNCH(ctx, level_scale_final, 1, 32, 0, partial, nbl, n, lam);
   }
   // algorithmic bytes: test vectors of every point + adjacency + rank map + the row output
   double fbytes = 8.0 * n * k + 4.0 * (n + 1) + 4.0 * adj->nnz + 4.0 * n + 16.0 * n * caliber;

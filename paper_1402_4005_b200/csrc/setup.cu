@@ -172,7 +172,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
   BAMG_TRY(arena_get(ctx, (size_t)k, &flip));
   // rayleigh quotient: dots = [uMu(k) | vNv(k) | uBv(k)]; mode 0: sigma = s (or
   // prev when a normaliser collapses); mode 1 (refresh): s < -1e-13 -> flip
-  BAMG_LAUNCH(ctx, rayleigh_reduce_kernel, RED_BLOCKS, RED_THREADS, 0, U, mu, V, nv, U, AV, n, k, partial,
+  BAMG_LAUNCH(ctx, rayleigh_reduce_kernel, red_blocks_for(n), RED_THREADS, 0, U, mu, V, nv, U, AV, n, k, partial,
               ctx->counters + 1, dots, sigma, flip, mode);
   if (mode == 1 && U_flip_or_null) {
     int64_t total = n * k;
