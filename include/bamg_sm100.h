@@ -110,6 +110,16 @@ int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int o
                       int32_t* rowptr_c, int64_t* nnz_host);
 int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
                      const int32_t* rowptr_c, int32_t* col_c, double* val_c);
+/* Independent products counted together: bamg_spgemm_count_slot launches the
+ * count into one of 4 slots without any host read; bamg_spgemm_count_wait
+ * reads nnz of the listed slots with ONE synchronisation; each product is
+ * then finished with bamg_spgemm_fill_slot on its slot.  (The Galerkin
+ * products of one level -- QB, Q M, N P -- share one wait.) */
+int bamg_spgemm_count_slot(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                           int32_t* rowptr_c, int slot);
+int bamg_spgemm_count_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int64_t* nnz_host);
+int bamg_spgemm_fill_slot(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                          const int32_t* rowptr_c, int32_t* col_c, double* val_c, int slot);
 
 /* ------------------------------------------------------ relax (relax.py) */
 /* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit

@@ -62,6 +62,9 @@ _SIGS = {
     "bamg_count_nonpositive": [P, P, I64, PI64],
     "bamg_spgemm_count": [P, PCSR, PCSR, C.c_int, P, PI64],
     "bamg_spgemm_fill": [P, PCSR, PCSR, C.c_int, P, P, P],
+    "bamg_spgemm_count_slot": [P, PCSR, PCSR, C.c_int, P, C.c_int],
+    "bamg_spgemm_count_wait": [P, C.c_int, P, PI64],
+    "bamg_spgemm_fill_slot": [P, PCSR, PCSR, C.c_int, P, P, P, C.c_int],
     "bamg_degenerate_rows": [P, PCSR, P, P],
     "bamg_jacobi": [P, PCSR, P, P, P, P, P, P, C.c_int, F64, P],
     "bamg_selftest_div": [P, I64, C.c_uint64, C.c_int, P],

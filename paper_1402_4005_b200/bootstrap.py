@@ -386,8 +386,27 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             P = build_interpolation(A, split, v_tests, cfg.interp, adj=adj)
             W = build_restriction_rows(A, split, u_tests, cfg.interp, adj=adj)
         with _phase("galerkin"):
+            # B_c = (Q B) P (sparse.py:102-117), M_c = Q M Q^T, N_c = P^T N P
+            # (bootstrap.py:372-373): the independent products of each stage
+            # are counted together (one host read per stage).  Identity masses
+            # (the finest level): scipy's Q@I / I@P store every row reversed,
+            # so (Q I) W and P^T (I P) are the products with Q's / P's rows
+            # walked in reverse -- bit-identical, no identity product.
             Q = engine.transpose(W)
-            Bc = engine.spgemm(engine.spgemm(Q, A, order=1), P, order=0)
+            Pt = engine.transpose(P)
+            stage1 = [(Q, A, 1)]
+            stage1.append((Q, W, engine.SPGEMM_REV_A) if Md.is_identity else (Q, Md, 1))
+            stage1.append((Pt, P, engine.SPGEMM_REV_B) if Nd.is_identity else (Nd, P, 1))
+            QB, QM, NP = engine.spgemm_many(stage1)
+            stage2 = [(QB, P, 0)]
+            if not Md.is_identity:
+                stage2.append((QM, W, 0))
+            if not Nd.is_identity:
+                stage2.append((Pt, NP, 0))
+            out2 = engine.spgemm_many(stage2)
+            Bc = out2[0]
+            Mc = QM if Md.is_identity else out2[1]
+            Nc = NP if Nd.is_identity else out2[-1]
             sick = _operator_degenerate(Bc)
         if sick:
             if _DEBUG:
@@ -395,19 +414,6 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             with _phase("coarsest"):
                 trips = coarsest_triplets(A, Md, Nd, trips.r)
             return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
-        with _phase("galerkin"):
-            # identity masses (the finest level): scipy's Q@I / I@P store every
-            # row reversed, so (Q I) W and P^T (I P) are the products with Q's /
-            # P's rows walked in reverse -- bit-identical, no identity product
-            if Md.is_identity:
-                Mc = engine.spgemm(Q, W, order=engine.SPGEMM_REV_A)
-            else:
-                Mc = engine.spgemm(engine.spgemm(Q, Md, order=1), W, order=0)
-            Pt = engine.transpose(P)
-            if Nd.is_identity:
-                Nc = engine.spgemm(Pt, P, order=engine.SPGEMM_REV_B)
-            else:
-                Nc = engine.spgemm(Pt, engine.spgemm(Nd, P, order=1), order=0)
         with _phase("inject"):
             cranks = ranks.restrict(split) if ranks is not None else None
             cl = engine.gather_rows(trips.dleft, split.dcoarse)

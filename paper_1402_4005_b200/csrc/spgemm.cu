@@ -22,6 +22,7 @@
 // and their scratch offsets are memoised in the context between the count and
 // fill calls, so a product costs two host synchronisations (row count, total).
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -268,6 +269,8 @@ struct SpgemmMemo {
   double* pval = nullptr;
   int64_t pcap = 0;
   unsigned long long* stat = nullptr;  // [pool used, flagged rows, nnz(C)] read back in one sync
+  bamg_csr a{}, b{};                   // operands of the pending count (async slots)
+  int32_t* rowptr_c = nullptr;
   // parking slots of the count pass (TSLOT entries per row) + flags + redo list
   int32_t* tcol = nullptr;
   double* tval = nullptr;
@@ -277,12 +280,17 @@ struct SpgemmMemo {
   int64_t tcap = 0;
 };
 
-static SpgemmMemo& memo(bamg_ctx* ctx) {
+// SPG_SLOTS independent memos per context: products whose counts are issued
+// together (bamg_spgemm_count_slot) and read back with one synchronisation
+// (bamg_spgemm_count_wait) each keep their own parked rows and scratch.
+constexpr int SPG_SLOTS = 4;
+
+static SpgemmMemo& memo(bamg_ctx* ctx, int slot = 0) {
   static thread_local std::vector<std::pair<bamg_ctx*, SpgemmMemo*>> table;
   for (auto& e : table)
-    if (e.first == ctx) return *e.second;
-  table.push_back({ctx, new SpgemmMemo()});
-  return *table.back().second;
+    if (e.first == ctx) return e.second[slot];
+  table.push_back({ctx, new SpgemmMemo[SPG_SLOTS]()});
+  return table.back().second[slot];
 }
 
 static int memo_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t n) {
@@ -325,63 +333,130 @@ static int pool_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t want) {
 // device-resident count, scratch bump-allocated from the memo's pool -- and
 // the pool use, the flagged-row count and nnz(C) come back in one read.  A
 // pool overflow (rows too long for the pool) grows it and recounts.
-extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order, int32_t* rowptr_c,
-                                 int64_t* nnz_host) {
-  ctx->arena.reset();
+// Count pass of C = A B into memo `m` without reading anything back: the
+// pool use, the flagged-row count and nnz(C) land in m.stat.
+static int spgemm_count_launch(bamg_ctx* ctx, SpgemmMemo& m, const bamg_csr* A, const bamg_csr* B, int order,
+                               int32_t* rowptr_c, bool recount = false) {
   BAMG_REQUIRE(ctx, A && B && A->ncols == B->nrows, "dimension mismatch in sparse product");
   BAMG_REQUIRE(ctx, order >= 0 && order <= 7,
                "order must be 0 (canonical) or 1 (scipy storage order), optionally | 2 (reverse A rows) | 4 (reverse B rows)");
   const int n = A->nrows;
-  SpgemmMemo& m = memo(ctx);
   BAMG_TRY(memo_reserve(ctx, m, n));
-  if (const char* e = getenv("BAMG_SPGEMM_POOL")) {  // tests: start from a tiny pool (exercises the regrowth)
-    cudaFree(m.pkey);
-    cudaFree(m.pval);
-    m.pkey = nullptr;
-    m.pval = nullptr;
-    m.pcap = 0;
+  const char* e = recount ? nullptr : getenv("BAMG_SPGEMM_POOL");
+  if (e) {  // tests: start from a tiny pool (exercises the regrowth)
+    if (m.pcap > atoll(e)) {
+      cudaFree(m.pkey);
+      cudaFree(m.pval);
+      m.pkey = nullptr;
+      m.pval = nullptr;
+      m.pcap = 0;
+    }
     BAMG_TRY(pool_reserve(ctx, m, atoll(e) > 0 ? atoll(e) : 1));
+  } else {
+    BAMG_TRY(pool_reserve(ctx, m, (int64_t)1 << 20));
   }
-  BAMG_TRY(pool_reserve(ctx, m, (int64_t)1 << 20));
   int32_t* cnt;
   // m.stat: [0] pool words used, [1] flagged rows (32-bit counter in the low
   // half), [2] nnz(C) from the scan -- one memset, one read
   unsigned int* nbig = m.nbig_dev;
   BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cnt));
   const int bgrid = ctx->num_sms * 2;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(m.stat, 0, sizeof(unsigned long long) * 4, ctx->stream));
-    BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
-                    A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
-                    (int32_t*)nullptr, (double*)nullptr, m.tcol, m.tval, m.parked, (const int32_t*)nullptr,
-                    (const unsigned int*)nullptr);
-    BAMG_LAUNCH(ctx, spgemm_big_kernel<0>, bgrid, 128, 0, (const unsigned int*)nbig, m.list, A->rowptr, A->col,
-                A->val, B->rowptr, B->col, B->val, m.off, m.pkey, m.pval, order, cnt, (const int32_t*)nullptr,
-                (int32_t*)nullptr, (double*)nullptr, m.stat, (long long)m.pcap);
-    BAMG_TRY(scan_i32_dev(ctx, cnt, rowptr_c, n, reinterpret_cast<int64_t*>(m.stat + 2)));
-    unsigned long long st[3];
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(m.stat, 0, sizeof(unsigned long long) * 4, ctx->stream));
+  BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_local_kernel<0>, grid_for(n, 128), 128, 0, n, A->rowptr, A->col,
+                  A->val, B->rowptr, B->col, B->val, order, cnt, m.list, nbig, (const int32_t*)nullptr,
+                  (int32_t*)nullptr, (double*)nullptr, m.tcol, m.tval, m.parked, (const int32_t*)nullptr,
+                  (const unsigned int*)nullptr);
+  BAMG_LAUNCH(ctx, spgemm_big_kernel<0>, bgrid, 128, 0, (const unsigned int*)nbig, m.list, A->rowptr, A->col,
+              A->val, B->rowptr, B->col, B->val, m.off, m.pkey, m.pval, order, cnt, (const int32_t*)nullptr,
+              (int32_t*)nullptr, (double*)nullptr, m.stat, (long long)m.pcap);
+  BAMG_TRY(scan_i32_dev(ctx, cnt, rowptr_c, n, reinterpret_cast<int64_t*>(m.stat + 2)));
+  m.a = *A;
+  m.b = *B;
+  m.rowptr_c = rowptr_c;
+  m.arp = A->rowptr;
+  m.brp = B->rowptr;
+  m.order = order;
+  return 0;
+}
+
+// Finish counts whose stats were copied to the host: a pool overflow grows
+// the pool and recounts that product synchronously (rare).
+static int spgemm_count_finish(bamg_ctx* ctx, SpgemmMemo& m, unsigned long long* st, int64_t* nnz_host) {
+  st[1] &= 0xffffffffull;
+  if ((int64_t)st[0] > m.pcap) {  // slow-path rows did not fit: grow the pool, recount
+    BAMG_TRY(pool_reserve(ctx, m, (int64_t)st[0] + ((int64_t)st[0] >> 2)));
+    bamg_csr a = m.a, b = m.b;
+    ctx->arena.reset();
+    BAMG_TRY(spgemm_count_launch(ctx, m, &a, &b, m.order, m.rowptr_c, true));
     BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(m.stat), 3, reinterpret_cast<int64_t*>(st)));
     st[1] &= 0xffffffffull;
-    if ((int64_t)st[0] > m.pcap) {  // slow-path rows did not fit: grow the pool, recount
-      BAMG_REQUIRE(ctx, attempt == 0, "SpGEMM scratch pool overflow after regrowth");
-      BAMG_TRY(pool_reserve(ctx, m, (int64_t)st[0] + ((int64_t)st[0] >> 2)));
-      continue;
-    }
-    m.arp = A->rowptr;
-    m.brp = B->rowptr;
-    m.order = order;
-    m.nbig = (int)st[1];
-    *nnz_host = (int64_t)st[2];
-    return 0;
+    BAMG_REQUIRE(ctx, (int64_t)st[0] <= m.pcap, "SpGEMM scratch pool overflow after regrowth");
   }
-  return -2;
+  m.nbig = (int)st[1];
+  *nnz_host = (int64_t)st[2];
+  return 0;
 }
+
+// Count pass in ONE host synchronisation: the flagged (slow-path) rows are
+// handled without reading their number -- grid-stride kernels over the
+// device-resident count, scratch bump-allocated from the memo's pool -- and
+// the pool use, the flagged-row count and nnz(C) come back in one read.  A
+// pool overflow (rows too long for the pool) grows it and recounts.
+extern "C" int bamg_spgemm_count(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order, int32_t* rowptr_c,
+                                 int64_t* nnz_host) {
+  ctx->arena.reset();
+  SpgemmMemo& m = memo(ctx, 0);
+  BAMG_TRY(spgemm_count_launch(ctx, m, A, B, order, rowptr_c));
+  unsigned long long st[3];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(m.stat), 3, reinterpret_cast<int64_t*>(st)));
+  return spgemm_count_finish(ctx, m, st, nnz_host);
+}
+
+// Asynchronous count into slot `slot` (0..3): nothing is read back until
+// bamg_spgemm_count_wait, so independent products share one synchronisation.
+extern "C" int bamg_spgemm_count_slot(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                                      int32_t* rowptr_c, int slot) {
+  BAMG_REQUIRE(ctx, slot >= 0 && slot < SPG_SLOTS, "slot must lie in [0, 4)");
+  ctx->arena.reset();
+  return spgemm_count_launch(ctx, memo(ctx, slot), A, B, order, rowptr_c);
+}
+
+extern "C" int bamg_spgemm_count_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int64_t* nnz_host) {
+  BAMG_REQUIRE(ctx, nslots >= 1 && nslots <= SPG_SLOTS, "1..4 slots");
+  BAMG_REQUIRE(ctx, ctx->pinned_doubles >= (size_t)(3 * SPG_SLOTS), "pinned staging too small");
+  unsigned long long* host = reinterpret_cast<unsigned long long*>(ctx->pinned);
+  for (int i = 0; i < nslots; ++i) {
+    BAMG_REQUIRE(ctx, slots[i] >= 0 && slots[i] < SPG_SLOTS, "slot must lie in [0, 4)");
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(host + 3 * i, memo(ctx, slots[i]).stat, 3 * sizeof(unsigned long long),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  ctx->syncs++;
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long st[3 * SPG_SLOTS];
+  memcpy(st, host, sizeof(unsigned long long) * 3 * nslots);
+  for (int i = 0; i < nslots; ++i) BAMG_TRY(spgemm_count_finish(ctx, memo(ctx, slots[i]), st + 3 * i, nnz_host + i));
+  return 0;
+}
+
+static int spgemm_fill_impl(bamg_ctx* ctx, SpgemmMemo& m, const bamg_csr* A, const bamg_csr* B, int order,
+                            const int32_t* rowptr_c, int32_t* col_c, double* val_c);
 
 extern "C" int bamg_spgemm_fill(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
                                 const int32_t* rowptr_c, int32_t* col_c, double* val_c) {
   ctx->arena.reset();
+  return spgemm_fill_impl(ctx, memo(ctx, 0), A, B, order, rowptr_c, col_c, val_c);
+}
+
+extern "C" int bamg_spgemm_fill_slot(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
+                                     const int32_t* rowptr_c, int32_t* col_c, double* val_c, int slot) {
+  BAMG_REQUIRE(ctx, slot >= 0 && slot < SPG_SLOTS, "slot must lie in [0, 4)");
+  ctx->arena.reset();
+  return spgemm_fill_impl(ctx, memo(ctx, slot), A, B, order, rowptr_c, col_c, val_c);
+}
+
+static int spgemm_fill_impl(bamg_ctx* ctx, SpgemmMemo& m, const bamg_csr* A, const bamg_csr* B, int order,
+                            const int32_t* rowptr_c, int32_t* col_c, double* val_c) {
   const int n = A->nrows;
-  SpgemmMemo& m = memo(ctx);
   BAMG_REQUIRE(ctx, m.arp == A->rowptr && m.brp == B->rowptr && m.order == order,
                "bamg_spgemm_fill must follow bamg_spgemm_count on the same operands");
   // parked rows are copied; the others (more than TSLOT kept entries) are

@@ -110,6 +110,34 @@ def spgemm(A: DeviceCSR, B: DeviceCSR, order: int = 0) -> DeviceCSR:
     return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (A.shape[0], B.shape[1]))
 
 
+def spgemm_many(products):
+    """Independent products [(A, B, order), ...] (at most 4): counts issued
+    together, ONE host read for all their sizes, then the fills.  Same results
+    as spgemm() on each."""
+    if not 1 <= len(products) <= 4:
+        raise ValueError("1..4 products per batch")
+    rps, keep = [], []
+    for slot, (A, B, order) in enumerate(products):
+        if A.shape[1] != B.shape[0]:
+            raise ValueError(f"dimension mismatch in sparse product: {A.shape} x {B.shape}")
+        rp = _empty(A.shape[0] + 1, I32)
+        ra, rb = A.ref(), B.ref()
+        keep += [ra, rb]
+        _lib.call("bamg_spgemm_count_slot", ra, rb, order, _p(rp), slot)
+        rps.append(rp)
+    slots = (C.c_int32 * len(products))(*range(len(products)))
+    nnz = (C.c_int64 * len(products))()
+    _lib.call("bamg_spgemm_count_wait", len(products), slots, nnz)
+    out = []
+    for slot, ((A, B, order), rp) in enumerate(zip(products, rps)):
+        m = int(nnz[slot])
+        ci = _empty(max(m, 1), I32)
+        va = _empty(max(m, 1), F64)
+        _lib.call("bamg_spgemm_fill_slot", A.ref(), B.ref(), order, _p(rp), _p(ci), _p(va), slot)
+        out.append(DeviceCSR(rp, ci[:m], va[:m], (A.shape[0], B.shape[1])))
+    return out
+
+
 # ------------------------------------------------------------------ relax
 def degenerate_rows(A: DeviceCSR, d):
     skip = _empty(A.shape[0], U8)
