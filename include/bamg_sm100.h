@@ -203,6 +203,16 @@ int bamg_fit_rows_csr(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_
                       int radius, double improvement_tol, int constrain, int nonnegative,
                       double ridge_override, int32_t* out_cnt, int32_t* out_col, double* out_val,
                       int32_t* rowptr, int64_t* status_host, int64_t* nnz_host);
+/* Asynchronous bamg_fit_rows_csr into one of 4 slots (no host read), and the
+ * ONE synchronisation that returns status (2 per slot) and nnz of the listed
+ * slots: the P and W fits of a level share it. */
+int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
+                           const double* X, const double* w, int64_t n, int k, int caliber,
+                           int radius, double improvement_tol, int constrain, int nonnegative,
+                           double ridge_override, int32_t* out_cnt, int32_t* out_col, double* out_val,
+                           int32_t* rowptr, int slot);
+int bamg_fit_rows_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int64_t* status_host,
+                       int64_t* nnz_host);
 /* Compact the fixed-stride rows into canonical CSR (sorted columns, |v| <
  * 1e-300 dropped: csr_from_coo, sparse.py:42-46).  Two calls. */
 int bamg_rows_count(bamg_ctx* ctx, const int32_t* cnt, const double* val, int64_t n,

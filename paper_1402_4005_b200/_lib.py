@@ -81,6 +81,9 @@ _SIGS = {
                       F64, P, P, P, PI64],
     "bamg_fit_rows_csr": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
                           F64, P, P, P, P, PI64, PI64],
+    "bamg_fit_rows_csr_slot": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
+                               F64, P, P, P, P, C.c_int],
+    "bamg_fit_rows_wait": [P, C.c_int, P, PI64, PI64],
     "bamg_rows_count": [P, P, P, I64, C.c_int, P, PI64],
     "bamg_rows_fill": [P, P, P, P, I64, C.c_int, P, P, P],
     "bamg_axis_ranks": [P, P, I64, P, PI64],

@@ -25,8 +25,7 @@ import torch
 from . import engine
 from .coarsen import AxisRanks, CfSplitting, CoarseningConfig, make_splitting
 from .device import DeviceCSR, device
-from .interp import (InterpConfig, build_interpolation, build_restriction_rows,
-                     singular_test_weights)
+from .interp import InterpConfig, build_transfer_pair, singular_test_weights
 from .relax import SmootherConfig
 from .sparse import adjacency_structure, as_device
 
@@ -383,8 +382,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         with _phase("adjacency"):
             adj = ops.adj
         with _phase("ls_fit"):
-            P = build_interpolation(A, split, v_tests, cfg.interp, adj=adj)
-            W = build_restriction_rows(A, split, u_tests, cfg.interp, adj=adj)
+            P, W = build_transfer_pair(A, split, v_tests, u_tests, cfg.interp, adj=adj)
         with _phase("galerkin"):
             # B_c = (Q B) P (sparse.py:102-117), M_c = Q M Q^T, N_c = P^T N P
             # (bootstrap.py:372-373): the independent products of each stage

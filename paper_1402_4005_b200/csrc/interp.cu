@@ -1257,6 +1257,63 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
 __global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double* __restrict__ val, int64_t n,
                                   int stride, int32_t* __restrict__ out);
 
+// Per-context status words of asynchronous fits (bamg_fit_rows_csr_slot):
+// 4 slots x 4 words, read back together by bamg_fit_rows_wait.
+constexpr int FIT_SLOTS = 4;
+static unsigned long long* fit_slot_status(bamg_ctx* ctx) {
+  static thread_local std::vector<std::pair<bamg_ctx*, unsigned long long*>> table;
+  for (auto& e : table)
+    if (e.first == ctx) return e.second;
+  unsigned long long* p = nullptr;
+  if (cudaMalloc(&p, sizeof(unsigned long long) * 4 * FIT_SLOTS) != cudaSuccess) return nullptr;
+  table.push_back({ctx, p});
+  return p;
+}
+
+static int fit_rows_csr_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
+                               const double* w, int64_t n, int k, int caliber, int radius, double improvement_tol,
+                               int constrain, int nonnegative, double ridge_override, int32_t* out_cnt,
+                               int32_t* out_col, double* out_val, int32_t* rowptr, unsigned long long* status) {
+  BAMG_TRY(fit_rows_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                           nonnegative, ridge_override, out_cnt, out_col, out_val, status));
+  int32_t* c;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &c));
+  BAMG_LAUNCH(ctx, rows_count_kernel, grid_for(n, 256), 256, 0, out_cnt, out_val, n, caliber, c);
+  return scan_i32_dev(ctx, c, rowptr, n, reinterpret_cast<int64_t*>(status + 3));
+}
+
+// Asynchronous fit + row count + scan into slot `slot` (0..3); the status
+// [pinv-branch points, overflows, deferred, nnz] of every listed slot comes
+// back with ONE synchronisation in bamg_fit_rows_wait (P and W of a level).
+extern "C" int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
+                                      const double* X, const double* w, int64_t n, int k, int caliber, int radius,
+                                      double improvement_tol, int constrain, int nonnegative, double ridge_override,
+                                      int32_t* out_cnt, int32_t* out_col, double* out_val, int32_t* rowptr,
+                                      int slot) {
+  BAMG_REQUIRE(ctx, slot >= 0 && slot < FIT_SLOTS, "slot must lie in [0, 4)");
+  ctx->arena.reset();
+  unsigned long long* st = fit_slot_status(ctx);
+  BAMG_REQUIRE(ctx, st != nullptr, "status allocation failed");
+  return fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                             nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st + 4 * slot);
+}
+
+extern "C" int bamg_fit_rows_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int64_t* status_host,
+                                  int64_t* nnz_host) {
+  BAMG_REQUIRE(ctx, nslots >= 1 && nslots <= FIT_SLOTS, "1..4 slots");
+  unsigned long long* st = fit_slot_status(ctx);
+  BAMG_REQUIRE(ctx, st != nullptr, "status allocation failed");
+  int64_t h[4 * FIT_SLOTS];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(st), 4 * FIT_SLOTS, h));
+  for (int i = 0; i < nslots; ++i) {
+    BAMG_REQUIRE(ctx, slots[i] >= 0 && slots[i] < FIT_SLOTS, "slot must lie in [0, 4)");
+    const int64_t* q = h + 4 * slots[i];
+    nnz_host[i] = q[3];
+    BAMG_TRY(fit_status_check(ctx, q, status_host ? status_host + 2 * i : nullptr));
+  }
+  return 0;
+}
+
 // The fit, the kept-entry count of its rows and the row-pointer scan in one
 // call with ONE host read: [pinv-branch points, overflows, deferred, nnz].
 // The caller allocates col/val for nnz and finishes with bamg_rows_fill.

@@ -255,6 +255,40 @@ def fit_rows_csr(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg
     return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (n, ncols)), (int(status[0]), int(status[1]))
 
 
+def fit_rows_csr_many(fits):
+    """Independent fits [dict(adj, coarse_rank, X, w, caliber, radius, tol,
+    constrain, nonneg, ncols[, ridge])] (at most 4) with ONE host read for all
+    of them: [(DeviceCSR, (pinv_branch_fits, deferred)), ...]."""
+    if not 1 <= len(fits) <= 4:
+        raise ValueError("1..4 fits per batch")
+    bufs = []
+    for slot, f in enumerate(fits):
+        X = f["X"]
+        n, k = X.shape
+        cal = int(f["caliber"])
+        cnt = _empty(n, I32)
+        col = _empty(n * cal, I32)
+        val = _empty(n * cal, F64)
+        rp = _empty(n + 1, I32)
+        ridge = f.get("ridge")
+        _lib.call("bamg_fit_rows_csr_slot", f["adj"].ref(), _p(f["coarse_rank"]), _p(X), _p(f["w"]), n, k, cal,
+                  int(f["radius"]), float(f["tol"]), int(bool(f["constrain"])), int(bool(f["nonneg"])),
+                  -1.0 if ridge is None else float(ridge), _p(cnt), _p(col), _p(val), _p(rp), slot)
+        bufs.append((n, cal, cnt, col, val, rp, int(f["ncols"])))
+    slots = (C.c_int32 * len(fits))(*range(len(fits)))
+    status = (C.c_int64 * (2 * len(fits)))()
+    nnz = (C.c_int64 * len(fits))()
+    _lib.call("bamg_fit_rows_wait", len(fits), slots, status, nnz)
+    out = []
+    for i, (n, cal, cnt, col, val, rp, ncols) in enumerate(bufs):
+        m = int(nnz[i])
+        ci = _empty(max(m, 1), I32)
+        va = _empty(max(m, 1), F64)
+        _lib.call("bamg_rows_fill", _p(cnt), _p(col), _p(val), n, cal, _p(rp), _p(ci), _p(va))
+        out.append((DeviceCSR(rp, ci[:m], va[:m], (n, ncols)), (int(status[2 * i]), int(status[2 * i + 1]))))
+    return out
+
+
 def rows_to_csr(cnt, col, val, n, stride, ncols) -> DeviceCSR:
     rp = _empty(n + 1, I32)
     nnz = C.c_int64(0)

@@ -106,6 +106,20 @@ def build_restriction_rows(B, split: CfSplitting, tests: WeightedTestSet, cfg: I
     return _build_rows(S, split, tests, cfg, constrain=cfg.constrain_constant_in_q)
 
 
+def build_transfer_pair(B, split: CfSplitting, v_tests: WeightedTestSet, u_tests: WeightedTestSet,
+                        cfg: InterpConfig, adj: DeviceCSR | None = None):
+    """(P, W): build_interpolation and build_restriction_rows of one level
+    with one host synchronisation for both fits (they are independent)."""
+    from .sparse import adjacency_structure
+    S = adj if adj is not None else adjacency_structure(B)
+    common = dict(adj=S, coarse_rank=split.dcrank, caliber=cfg.caliber, radius=cfg.search_radius,
+                  tol=cfg.improvement_tol, nonneg=cfg.nonnegative, ncols=split.n_coarse)
+    (P, _), (W, _) = engine.fit_rows_csr_many([
+        dict(common, X=v_tests.dvectors, w=v_tests.dweights, constrain=False),
+        dict(common, X=u_tests.dvectors, w=u_tests.dweights, constrain=cfg.constrain_constant_in_q)])
+    return P, W
+
+
 def build_restriction(B, split: CfSplitting, tests: WeightedTestSet, cfg: InterpConfig,
                       adj: DeviceCSR | None = None) -> DeviceCSR:
     """Q = W^T (interp.py:303-314)."""
