@@ -1,4 +1,5 @@
-"""Run BASELINE configs end to end on the GPU: timings, iterations, invariants.
+"""Run BASELINE configs end to end on the GPU: timings (best of 3 repetitions, host-
+synchronised), iterations, invariants.
 
 python tools/run_configs.py cfg0 cfg1 cfg2 cfg3 cfg4
 """
@@ -48,7 +49,11 @@ def main(names):
         P = ChainProblem(A=None, B=dB, n=prob.n, family=fam, params={}, geometry=geo)
         gcfg = pb.GmresConfig(restart=restart, rtol=1e-8)
         out = {}
-        for rep in range(2):
+        import gc
+        best = None
+        for rep in range(3):
+            gc.collect()  # no collector pause inside the timed repetition (as bench.py)
+            gc.disable()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             setup = pb.run_setup(P, cfg, draws=(dV, dU), B_device=dB)
@@ -59,10 +64,15 @@ def main(names):
             rep_ = pb.gmres(dB, zero, setup.dx0, gcfg, vop, to_host=False)
             torch.cuda.synchronize()
             t2 = time.perf_counter()
+            if best is not None and (t2 - t0) >= best:
+                gc.enable()
+                continue
+            best = t2 - t0
             out = {"config": name, "n": prob.n, "gen_s": round(gen, 2), "setup_s": round(t1 - t0, 4),
                    "solve_s": round(t2 - t1, 4), "its": rep_.iterations, "converged": rep_.converged,
                    "final": rep_.residual_history[-1], "levels": [lv.n for lv in setup.hierarchy.levels],
                    "o_c": round(pb.complexities(setup.hierarchy)[1], 3)}
+            gc.enable()
         x = engine.sign_fix_l1(rep_.x_device)
         out["x_min"] = float(x.min())
         wc, wq = invariants(setup)
