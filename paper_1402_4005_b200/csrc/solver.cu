@@ -629,6 +629,24 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
     *out_host = hv2[1] == 0.0 ? INFINITY : hv2[0] / hv2[1];
     return 0;
   };
+  // the iteration's metric and Givens state (happy flag) in ONE read
+  auto metric_state = [&](const double* xv, double* out_host, bool* happy) -> int {
+    if (stopping == 1) {
+      BAMG_TRY(resid_dev(ctx, B, b, xv, tmp));
+      BAMG_TRY(norm_into(tmp, scal));
+    } else {
+      BAMG_TRY(spmm_dev(ctx, B, xv, tmp, 1));
+      BAMG_TRY(norm_into(tmp, scal));
+      BAMG_TRY(norm_into(xv, scal + 1));
+    }
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(scal + 4, state, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    double hv3[5];
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 5, hv3));
+    if (stopping == 1) *out_host = hv3[0] / denom0;
+    else *out_host = hv3[1] == 0.0 ? INFINITY : hv3[0] / hv3[1];
+    *happy = hv3[4] != 0.0;
+    return 0;
+  };
   if (stopping == 1) {
     BAMG_TRY(resid_dev(ctx, B, b, x0, tmp));
     BAMG_TRY(norm_into(tmp, scal));
@@ -704,11 +722,9 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       // x = x0 + (e + V y)
       BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, x0, e, nullptr, n, x);
       double mval;
-      BAMG_TRY(metric(x, &mval));
+      bool happy = false;
+      BAMG_TRY(metric_state(x, &mval, &happy));
       history_host[nhist++] = mval;
-      double st[1];
-      BAMG_TRY(ctx_read_doubles(ctx, state, 1, st));
-      bool happy = st[0] != 0.0;
       if (mval <= rtol) converged = true;
       if (converged || happy || iters >= max_iters) {
         if (happy) converged = true;
