@@ -121,6 +121,17 @@ int bamg_spgemm_count_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int6
 int bamg_spgemm_fill_slot(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* B, int order,
                           const int32_t* rowptr_c, int32_t* col_c, double* val_c, int slot);
 
+/* ------------------------------------------------ chains (chains.py, inputs) */
+/* On-device assembly of the lattice chains' B = I - A (SURVEY.md section 8(f)
+ * row 1): family 0 = tandem queue (chains.py:134-179, rates lam, mu1, mu2),
+ * 1 = uniform 2-D walk (chains.py:95-131).  Count writes rowptr (side^2 + 1),
+ * the per-axis geometry (2 x side^2, may be null) and returns nnz; fill writes
+ * col/val.  Bit-identical to the host generators (canonical CSR). */
+int bamg_chain_lattice_count(bamg_ctx* ctx, int family, int side, double lam, double mu1, double mu2,
+                             int32_t* rowptr, double* geometry, int64_t* nnz_host);
+int bamg_chain_lattice_fill(bamg_ctx* ctx, int family, int side, double lam, double mu1, double mu2,
+                            const int32_t* rowptr, int32_t* col, double* val);
+
 /* ------------------------------------------------------ relax (relax.py) */
 /* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit
  * transpose for the column variant.  Replaces degenerate_rows, relax.py:47-63. */

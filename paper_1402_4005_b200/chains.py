@@ -134,6 +134,43 @@ def uniform_2d(side: int, validate: bool = True) -> ChainProblem:
     return ChainProblem(A=A, B=B, n=n, family="uniform2d", params=params, geometry=geometry)
 
 
+def lattice_chain_device(family: str, side: int, lam: float = 11.0 / 31.0, mu1: float = 10.0 / 31.0,
+                         mu2: float = 10.0 / 31.0) -> ChainProblem:
+    """The tandem / uniform2d chain's B assembled directly in HBM
+    (csrc/chains.cu): the same canonical CSR as tandem_queue / uniform_2d,
+    bit for bit, without the host matrix or its upload.  A is not formed
+    (`A=None`); geometry is the device (2, n) per-axis block the setup takes."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .device import DeviceCSR, device
+    if family not in ("tandem", "uniform2d"):
+        raise ValueError("device assembly covers the tandem and uniform2d lattices")
+    if side < 2:
+        raise ValueError("side must be at least 2")
+    if family == "tandem" and abs(lam + mu1 + mu2 - 1.0) > 1e-12:
+        raise ValueError("transition probabilities must sum to 1")
+    fid = 0 if family == "tandem" else 1
+    n = side * side
+    dev = device()
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    geo = torch.empty((2, n), dtype=torch.float64, device=dev)
+    nnz = C.c_int64(0)
+    _lib.call("bamg_chain_lattice_count", fid, side, float(lam), float(mu1), float(mu2), _lib.ptr(rp),
+              _lib.ptr(geo), C.byref(nnz))
+    ci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+    va = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+    _lib.call("bamg_chain_lattice_fill", fid, side, float(lam), float(mu1), float(mu2), _lib.ptr(rp),
+              _lib.ptr(ci), _lib.ptr(va))
+    B = DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (n, n))
+    params = {"side": side, "n": n}
+    if family == "tandem":
+        params.update({"lambda": lam, "mu1": mu1, "mu2": mu2})
+    return ChainProblem(A=None, B=B, n=n, family=family, params=params, geometry=geo)
+
+
 def birth_death(n: int, mu: float = 0.96) -> ChainProblem:
     """Biased walk on a path (chains.py:64-92)."""
     if n < 2:

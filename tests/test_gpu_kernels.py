@@ -301,3 +301,18 @@ def test_spgemm_many_matches_single_products(eng):
         got = C.to_host()
         assert np.array_equal(got.indptr, ref.indptr) and np.array_equal(got.indices, ref.indices)
         assert np.array_equal(got.data, ref.data)
+
+
+@pytest.mark.parametrize("family,side", [("tandem", 2), ("tandem", 17), ("tandem", 64), ("uniform2d", 2),
+                                         ("uniform2d", 33), ("uniform2d", 128)])
+def test_device_lattice_chain_matches_host(eng, family, side):
+    """On-device assembly of B: the same canonical CSR
+    arrays and geometry as the host generators, bit for bit."""
+    from paper_1402_4005_b200 import chains
+    host = chains.tandem_queue(side) if family == "tandem" else chains.uniform_2d(side)
+    dev = chains.lattice_chain_device(family, side)
+    H = host.B
+    D = dev.B.to_host()
+    assert np.array_equal(D.indptr, H.indptr) and np.array_equal(D.indices, H.indices)
+    assert np.array_equal(D.data, H.data)
+    assert np.array_equal(dev.geometry.cpu().numpy().T, host.geometry)
