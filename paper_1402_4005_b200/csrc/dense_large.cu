@@ -276,8 +276,81 @@ static bool trsm_small_enabled() {
   return !(e && e[0] == '1');
 }
 
-// Blocked triangular solve op(T) X = B in place on B (n x m, ldb).  T is the
-// n x n column-major factor: lower (unit or not) or, with `upper`, the upper
+// Blocked solve on the ns x ns diagonal block at T (leading dimension lt):
+// tri_inv of each 64-block and two GEMMs per block.
+static int tri_solve_blk(bamg_ctx* ctx, const double* T, int lt, int n, bool lower_stored, bool unit, bool trans,
+                         double* B, int ldb, int m, double* work /* NB*NB + NB*m */) {
+  double* Ti = work;
+  double* tmp = work + NB * NB;
+  // effective shape of op(T): lower if (lower_stored xor trans)
+  const bool eff_lower = lower_stored != trans;
+  const int nblk = (n + NB - 1) / NB;
+  for (int s = 0; s < nblk; ++s) {
+    int bi = eff_lower ? s : nblk - 1 - s;
+    int i0 = bi * NB, ib = (i0 + NB <= n) ? NB : n - i0;
+    // inverse of the diagonal block of op(T)
+    const double* Tii = T + (int64_t)i0 * lt + i0;
+    int kind = lower_stored ? (unit ? 0 : 1) : 2;
+    BAMG_TRY(tri_inv(ctx, Tii, lt, ib, kind, Ti));  // inverse of the stored block
+    // X_i = op(Tii)^-1 B_i   (op(inv) = inv(op))
+    BAMG_TRY(gemm(ctx, trans, false, ib, m, ib, 1.0, Ti, ib, B + i0, ldb, 0.0, tmp, ib));
+    BAMG_TRY(copy_block(ctx, tmp, ib, B + i0, ldb, ib, m));
+    // update the remaining block rows: B_rest -= op(T)_{rest,i} X_i
+    if (eff_lower) {
+      int r0 = i0 + ib, rn = n - r0;
+      if (rn > 0) {
+        // op(T)[r0:, i0:i0+ib] = trans ? T[i0:i0+ib, r0:]^T : T[r0:, i0:i0+ib]
+        const double* Tb = trans ? T + (int64_t)r0 * lt + i0 : T + (int64_t)i0 * lt + r0;
+        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, lt, B + i0, ldb, 1.0, B + r0, ldb));
+      }
+    } else {
+      int rn = i0;
+      if (rn > 0) {
+        // op(T)[0:i0, i0:i0+ib] = trans ? T[i0:i0+ib, 0:i0]^T : T[0:i0, i0:i0+ib]
+        const double* Tb = trans ? T + i0 : T + (int64_t)i0 * lt;
+        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, lt, B + i0, ldb, 1.0, B, ldb));
+      }
+    }
+  }
+  return 0;
+}
+
+// Recursive solve: halve the triangle, solve one half, one large GEMM update
+// of the other, recurse -- the off-diagonal work becomes a few big DGEMMs
+// (k = n/2, n/4, ...) instead of n/64 rank-64 updates.  Leaves of <= 1024
+// rows (BAMG_TRSM_LEAF) take the blocked path.
+static int trsm_leaf() {
+  const char* e = getenv("BAMG_TRSM_LEAF");  // tests: recurse on small coarsest levels
+  return e ? atoi(e) : 1024;
+}
+
+static int tri_solve_rec(bamg_ctx* ctx, const double* T, int lt, int n, bool lower_stored, bool unit, bool trans,
+                         double* B, int ldb, int m, double* work) {
+  const int h = ((n / 2 + NB - 1) / NB) * NB;  // split on a 64-block boundary
+  if (n <= trsm_leaf() || h >= n) return tri_solve_blk(ctx, T, lt, n, lower_stored, unit, trans, B, ldb, m, work);
+  const double* T22 = T + (int64_t)h * lt + h;
+  const bool eff_lower = lower_stored != trans;
+  if (eff_lower) {
+    BAMG_TRY(tri_solve_rec(ctx, T, lt, h, lower_stored, unit, trans, B, ldb, m, work));
+    // B2 -= op(T)[h:n, 0:h] X1
+    const double* Tb = trans ? T + (int64_t)h * lt : T + h;
+    BAMG_TRY(gemm(ctx, trans, false, n - h, m, h, -1.0, Tb, lt, B, ldb, 1.0, B + h, ldb));
+    return tri_solve_rec(ctx, T22, lt, n - h, lower_stored, unit, trans, B + h, ldb, m, work);
+  }
+  BAMG_TRY(tri_solve_rec(ctx, T22, lt, n - h, lower_stored, unit, trans, B + h, ldb, m, work));
+  // B1 -= op(T)[0:h, h:n] X2
+  const double* Tb = trans ? T + h : T + (int64_t)h * lt;
+  BAMG_TRY(gemm(ctx, trans, false, h, m, n - h, -1.0, Tb, lt, B + h, ldb, 1.0, B, ldb));
+  return tri_solve_rec(ctx, T, lt, h, lower_stored, unit, trans, B, ldb, m, work);
+}
+
+static bool trsm_recursive_enabled() {
+  const char* e = getenv("BAMG_TRSM_FLAT");  // development: force the flat blocked path
+  return !(e && e[0] == '1');
+}
+
+// Triangular solve op(T) X = B in place on B (n x m, ldb).  T is the n x n
+// column-major factor: lower (unit or not) or, with `upper`, the upper
 // triangle; `trans` solves with T^T (a lower T^T is upper).
 static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, bool unit, bool trans, double* B,
                      int ldb, int m, double* work /* NB*NB + NB*m */) {
@@ -296,39 +369,8 @@ static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, b
                 (int)trans, B, ldb, m);
     return 0;
   }
-  double* Ti = work;
-  double* tmp = work + NB * NB;
-  // effective shape of op(T): lower if (lower_stored xor trans)
-  const bool eff_lower = lower_stored != trans;
-  const int nblk = (n + NB - 1) / NB;
-  for (int s = 0; s < nblk; ++s) {
-    int bi = eff_lower ? s : nblk - 1 - s;
-    int i0 = bi * NB, ib = (i0 + NB <= n) ? NB : n - i0;
-    // inverse of the diagonal block of op(T)
-    const double* Tii = T + (int64_t)i0 * n + i0;
-    int kind = lower_stored ? (unit ? 0 : 1) : 2;
-    BAMG_TRY(tri_inv(ctx, Tii, n, ib, kind, Ti));  // inverse of the stored block
-    // X_i = op(Tii)^-1 B_i   (op(inv) = inv(op))
-    BAMG_TRY(gemm(ctx, trans, false, ib, m, ib, 1.0, Ti, ib, B + i0, ldb, 0.0, tmp, ib));
-    BAMG_TRY(copy_block(ctx, tmp, ib, B + i0, ldb, ib, m));
-    // update the remaining block rows: B_rest -= op(T)_{rest,i} X_i
-    if (eff_lower) {
-      int r0 = i0 + ib, rn = n - r0;
-      if (rn > 0) {
-        // op(T)[r0:, i0:i0+ib] = trans ? T[i0:i0+ib, r0:]^T : T[r0:, i0:i0+ib]
-        const double* Tb = trans ? T + (int64_t)r0 * n + i0 : T + (int64_t)i0 * n + r0;
-        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, n, B + i0, ldb, 1.0, B + r0, ldb));
-      }
-    } else {
-      int rn = i0;
-      if (rn > 0) {
-        // op(T)[0:i0, i0:i0+ib] = trans ? T[i0:i0+ib, 0:i0]^T : T[0:i0, i0:i0+ib]
-        const double* Tb = trans ? T + i0 : T + (int64_t)i0 * n;
-        BAMG_TRY(gemm(ctx, trans, false, rn, m, ib, -1.0, Tb, n, B + i0, ldb, 1.0, B, ldb));
-      }
-    }
-  }
-  return 0;
+  if (trsm_recursive_enabled()) return tri_solve_rec(ctx, T, n, n, lower_stored, unit, trans, B, ldb, m, work);
+  return tri_solve_blk(ctx, T, n, n, lower_stored, unit, trans, B, ldb, m, work);
 }
 
 // ------------------------------------------------------------- Cholesky
@@ -368,12 +410,14 @@ __global__ void zero_upper_kernel(double* A, int n) {
   if (r < c) A[t] = 0.0;
 }
 
-static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* work) {
+// Blocked right-looking Cholesky of the n x n block at A (leading dimension
+// lt): lower factor in the lower triangle, the upper triangle left stale.
+static int chol_blk(bamg_ctx* ctx, double* A, int lt, int n, int* bad, double* work) {
   double* Li = work;            // NB x NB
   double* tmp = work + NB * NB;  // n x NB
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
-    double* Ajj = A + (int64_t)j0 * n + j0;
+    double* Ajj = A + (int64_t)j0 * lt + j0;
     {
       static bool attr = false;
       const int smem = NB * NB * (int)sizeof(double);
@@ -381,18 +425,63 @@ static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* w
         BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
       }
-      BAMG_LAUNCH(ctx, chol_block_kernel, 1, 1024, smem, Ajj, n, jb, bad);
+      BAMG_LAUNCH(ctx, chol_block_kernel, 1, 1024, smem, Ajj, lt, jb, bad);
     }
     int r0 = j0 + jb, rn = n - r0;
     if (rn <= 0) break;
-    BAMG_TRY(tri_inv(ctx, Ajj, n, jb, 1, Li));
+    BAMG_TRY(tri_inv(ctx, Ajj, lt, jb, 1, Li));
     // L21 = A21 L11^-T
-    double* A21 = A + (int64_t)j0 * n + r0;
-    BAMG_TRY(gemm(ctx, false, true, rn, jb, jb, 1.0, A21, n, Li, jb, 0.0, tmp, rn));
-    BAMG_TRY(copy_block(ctx, tmp, rn, A21, n, rn, jb));
+    double* A21 = A + (int64_t)j0 * lt + r0;
+    BAMG_TRY(gemm(ctx, false, true, rn, jb, jb, 1.0, A21, lt, Li, jb, 0.0, tmp, rn));
+    BAMG_TRY(copy_block(ctx, tmp, rn, A21, lt, rn, jb));
     // A22 -= L21 L21^T
-    BAMG_TRY(gemm(ctx, false, true, rn, rn, jb, -1.0, A21, n, A21, n, 1.0, A + (int64_t)r0 * n + r0, n));
+    BAMG_TRY(gemm(ctx, false, true, rn, rn, jb, -1.0, A21, lt, A21, lt, 1.0, A + (int64_t)r0 * lt + r0, lt));
   }
+  return 0;
+}
+
+// Y (rows x cols, ld ldy) = X^T (X: cols x rows, ld ldx), 32 x 32 tiles
+__global__ void transpose_rect_kernel(const double* __restrict__ X, int ldx, int rows, int cols,
+                                      double* __restrict__ Y, int ldy) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;  // Y rows r0.., Y cols c0..
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int yr = r0 + threadIdx.x, yc = c0 + j;  // X(yc, yr) = X[yr * ldx + yc]
+    if (yr < rows && yc < cols) tile[j][threadIdx.x] = X[(int64_t)yr * ldx + yc];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int yr = r0 + j, yc = c0 + threadIdx.x;
+    if (yr < rows && yc < cols) Y[(int64_t)yc * ldy + yr] = tile[threadIdx.x][j];
+  }
+}
+
+static int trsm_leaf();
+
+// Recursive Cholesky: factor A11, L21^T = L11^-1 A12 (recursive TRSM on the
+// symmetric upper block), write L21, A22 -= L21 L21^T as ONE large DGEMM,
+// recurse on A22.  Leaves take the blocked path.
+static int chol_rec(bamg_ctx* ctx, double* A, int lt, int n, int* bad, double* work) {
+  const int h = ((n / 2 + NB - 1) / NB) * NB;
+  if (n <= trsm_leaf() || h >= n) return chol_blk(ctx, A, lt, n, bad, work);
+  BAMG_TRY(chol_rec(ctx, A, lt, h, bad, work));
+  double* A12 = A + (int64_t)h * lt;  // h x (n - h): becomes X = L21^T
+  BAMG_TRY(tri_solve_rec(ctx, A, lt, h, true, false, false, A12, lt, n - h, work));
+  {
+    dim3 grid((n - h + 31) / 32, (h + 31) / 32), block(32, 8);
+    transpose_rect_kernel<<<grid, block, 0, ctx->stream>>>(A12, lt, n - h, h, A + h, lt);
+    ctx->launches++;
+    BAMG_CHECK_CUDA(ctx, cudaGetLastError());
+  }
+  double* A22 = A + (int64_t)h * lt + h;
+  BAMG_TRY(gemm(ctx, true, false, n - h, n - h, h, -1.0, A12, lt, A12, lt, 1.0, A22, lt));
+  return chol_rec(ctx, A22, lt, n - h, bad, work);
+}
+
+static int cholesky_blocked(bamg_ctx* ctx, double* A, int n, int* bad, double* work) {
+  if (trsm_recursive_enabled()) BAMG_TRY(chol_rec(ctx, A, n, n, bad, work));
+  else BAMG_TRY(chol_blk(ctx, A, n, n, bad, work));
   BAMG_LAUNCH(ctx, zero_upper_kernel, grid_for((int64_t)n * n, 256), 256, 0, A, n);
   return 0;
 }
@@ -716,17 +805,89 @@ __global__ void apply_swaps_kernel(double* A, int n, int j0, int jb, const int* 
   }
 }
 
+struct LuPanelCfg {
+  double* pmax;
+  int* pidx;
+  int pgrid;
+  size_t smax;
+};
+
+// Factor the panel A[j0:n, j0:j0+jb] (shared memory / thread-block cluster /
+// cooperative grid by size) and apply its row interchanges to every other
+// column.
+static int lu_panel(bamg_ctx* ctx, double* A, int n, int j0, int jb, int* piv, int* bad, const LuPanelCfg& pc) {
+  const int rows = n - j0;
+  const size_t panel_bytes = (size_t)rows * jb * sizeof(double);
+  const int cs = (int)((panel_bytes + pc.smax - 1) / pc.smax);
+  if (panel_bytes <= pc.smax) {
+    BAMG_LAUNCH(ctx, panel_lu_smem_kernel, 1, 1024, panel_bytes, A, n, j0, jb, piv, bad);
+  } else if (cs <= 8) {
+    // thread-block cluster of cs CTAs, the panel spread over their shared memory
+    int R = (rows + cs - 1) / cs;
+    const size_t smem = (size_t)R * jb * sizeof(double);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (ctx->trace.on) trace_mark(ctx, "panel_lu_cluster_kernel");
+    BAMG_CHECK_CUDA(ctx, cudaLaunchKernelEx(&cfg, panel_lu_cluster_kernel, A, n, j0, jb, R, piv, bad));
+    ctx->launches++;
+    if (ctx->trace.on) trace_mark(ctx, nullptr);
+  } else {
+    int want = (n - j0 + 255) / 256;
+    int g = want < pc.pgrid ? (want < 1 ? 1 : want) : pc.pgrid;
+    double* pmax = pc.pmax;
+    int* pidx = pc.pidx;
+    void* args[] = {&A, &n, &j0, &jb, &piv, &pmax, &pidx, &bad};
+    BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(g), dim3(256), args, 0,
+                                                     ctx->stream));
+    ctx->launches++;
+  }
+  BAMG_LAUNCH(ctx, apply_swaps_kernel, grid_for(n, 256), 256, 0, A, n, j0, jb, piv);
+  return 0;
+}
+
+// Recursive LU of the columns [j0, j0 + nc) (rows j0..n-1, partial pivoting):
+// left half, U12 = L11^-1 A12 (recursive TRSM), A22 -= L21 U12 as ONE large
+// DGEMM, right half; 64-column panels at the leaves.  Same pivots and the
+// same factor (up to GEMM rounding) as the blocked right-looking loop.
+static int lu_rec(bamg_ctx* ctx, double* A, int n, int j0, int nc, int* piv, int* bad, double* work,
+                  const LuPanelCfg& pc) {
+  // leaves: panels that fit one CTA's or one 8-CTA cluster's shared memory
+  // (tall panels are split down to 8 columns so they do; cooperative-grid
+  // panels only past that)
+  const size_t cl_cap = 8 * pc.smax;
+  const size_t pbytes = (size_t)(n - j0) * nc * sizeof(double);
+  if ((nc <= NB && pbytes <= cl_cap) || nc <= 8) return lu_panel(ctx, A, n, j0, nc, piv, bad, pc);
+  int h = nc > NB ? ((nc / 2 + NB - 1) / NB) * NB : ((nc / 2 + 7) / 8) * 8;
+  if (h >= nc) h = nc - 8;
+  BAMG_TRY(lu_rec(ctx, A, n, j0, h, piv, bad, work, pc));
+  double* L11 = A + (int64_t)j0 * n + j0;
+  double* A12 = A + (int64_t)(j0 + h) * n + j0;
+  BAMG_TRY(tri_solve_rec(ctx, L11, n, h, true, true, false, A12, n, nc - h, work));
+  BAMG_TRY(gemm(ctx, false, false, n - j0 - h, nc - h, h, -1.0, A + (int64_t)j0 * n + j0 + h, n, A12, n, 1.0,
+                A + (int64_t)(j0 + h) * n + j0 + h, n));
+  return lu_rec(ctx, A, n, j0 + h, nc - h, piv, bad, work, pc);
+}
+
 static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, double* work) {
   double* Li = work;             // NB x NB
   double* tmp = work + NB * NB;  // NB x n
-  double* pmax;
-  int* pidx;
-  BAMG_TRY(arena_get(ctx, 2048, &pmax));
-  BAMG_TRY(arena_get(ctx, 2048, &pidx));
+  LuPanelCfg pc{};
+  BAMG_TRY(arena_get(ctx, 2048, &pc.pmax));
+  BAMG_TRY(arena_get(ctx, 2048, &pc.pidx));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_lu_kernel, 256, 0);
-  int pgrid = per_sm * ctx->num_sms;
-  if (pgrid > 2048) pgrid = 2048;
+  pc.pgrid = per_sm * ctx->num_sms;
+  if (pc.pgrid > 2048) pc.pgrid = 2048;
   static bool smem_attr = false;
   if (!smem_attr) {
     BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(panel_lu_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -739,43 +900,11 @@ static int lu_blocked(bamg_ctx* ctx, double* A, int n, int* piv, int* bad, doubl
                                               PANEL_SMEM_MAX));
     cl_attr = true;
   }
-  const size_t smax = panel_smem_max();
+  pc.smax = panel_smem_max();
+  if (n > trsm_leaf() && trsm_recursive_enabled()) return lu_rec(ctx, A, n, 0, n, piv, bad, work, pc);
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
-    const int rows = n - j0;
-    const size_t panel_bytes = (size_t)rows * jb * sizeof(double);
-    const int cs = (int)((panel_bytes + smax - 1) / smax);
-    if (panel_bytes <= smax) {
-      BAMG_LAUNCH(ctx, panel_lu_smem_kernel, 1, 1024, panel_bytes, A, n, j0, jb, piv, bad);
-    } else if (cs <= 8) {
-      // thread-block cluster of cs CTAs, the panel spread over their shared memory
-      int R = (rows + cs - 1) / cs;
-      const size_t smem = (size_t)R * jb * sizeof(double);
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(cs);
-      cfg.blockDim = dim3(1024);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = ctx->stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = cs;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      if (ctx->trace.on) trace_mark(ctx, "panel_lu_cluster_kernel");
-      BAMG_CHECK_CUDA(ctx, cudaLaunchKernelEx(&cfg, panel_lu_cluster_kernel, A, n, j0, jb, R, piv, bad));
-      ctx->launches++;
-      if (ctx->trace.on) trace_mark(ctx, nullptr);
-    } else {
-      int want = (n - j0 + 255) / 256;
-      int g = want < pgrid ? (want < 1 ? 1 : want) : pgrid;
-      void* args[] = {&A, &n, &j0, &jb, &piv, &pmax, &pidx, &bad};
-      BAMG_CHECK_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(g), dim3(256), args, 0,
-                                                       ctx->stream));
-      ctx->launches++;
-    }
-    BAMG_LAUNCH(ctx, apply_swaps_kernel, grid_for(n, 256), 256, 0, A, n, j0, jb, piv);
+    BAMG_TRY(lu_panel(ctx, A, n, j0, jb, piv, bad, pc));
     int r0 = j0 + jb, rn = n - r0;
     if (rn <= 0) break;
     // U12 = L11^-1 A12
