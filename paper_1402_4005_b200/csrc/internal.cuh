@@ -11,7 +11,8 @@ int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t*
                double omega, double* peak, const double* rd = nullptr);
 int recip_dev(bamg_ctx* ctx, const double* d, int64_t n, double* rd);
 int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const double* V, int k, double* sigma,
-                       double* flip, int mode, double* dots);
+                       double* flip, int mode, double* dots, const bamg_csr* M = nullptr,
+                       const bamg_csr* N = nullptr);
 int diag_dev(bamg_ctx* ctx, const bamg_csr* A, double* d);
 int degenerate_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, uint8_t* skip);
 int transpose_dev(bamg_ctx* ctx, const bamg_csr* A, int32_t* rowptr_t, int32_t* col_t, double* val_t);

@@ -141,10 +141,10 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
   double *MU, *NV, *AV, *dots, *partial, *flip;
   const double* mu = U;
   const double* nv = V;
-  if (!M && !N) {  // identity masses: one fused pass (sparse.cu rayleigh_fused_kernel)
+  {  // one fused pass over A (and M, N): sparse.cu rayleigh_fused_kernel
     BAMG_TRY(arena_get(ctx, (size_t)3 * k, &dots));
     BAMG_TRY(arena_get(ctx, (size_t)k, &flip));
-    int rc = rayleigh_fused_dev(ctx, A, U, V, k, sigma, flip, mode, dots);
+    int rc = rayleigh_fused_dev(ctx, A, U, V, k, sigma, flip, mode, dots, M, N);
     if (rc < 0) return rc;
     if (rc == 0) {
       if (mode == 1 && U_flip_or_null) {

@@ -330,12 +330,54 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A);
 // per-CTA partials -- and the last CTA's fixed-order final sum and sigma
 // finish -- are bit-reproducible.  Saves the A V write + re-read and two
 // launches per quotient.
+// slice [voff, voff + VV) of (Op X)[row], sequential ascending-column sums
+template <int K, int VV, int U>
+__device__ __forceinline__ void row_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                          const double* __restrict__ val, const double* __restrict__ X, int row,
+                                          int voff, double* acc) {
+#pragma unroll
+  for (int q = 0; q < VV; ++q) acc[q] = 0.0;
+  const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  for (int j = jb; j < je; j += U) {
+    int cc[U];
+    double aa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = j + u < je ? j + u : je - 1;
+      cc[u] = __ldg(col + jj);
+      aa[u] = __ldg(val + jj);
+    }
+    double xv[U][VV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) VecIO<VV>::load(X + (int64_t)cc[u] * K + voff, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < je) {
+#pragma unroll
+        for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+      }
+    }
+  }
+}
+
+// Masses M, N (nullable = identity): u.(M u) and v.(N v) from their rows in
+// the same pass (the coarse levels' inhomogeneous sweeps), without writing
+// M U, N V, A V.
+struct MassRows {
+  const int32_t* mrp;
+  const int32_t* mcol;
+  const double* mval;
+  const int32_t* nrp;
+  const int32_t* ncol;
+  const double* nval;
+};
+
 template <int K, int G, int U>
 __global__ void __launch_bounds__(TILE_THREADS)
 rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                       const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
-                      double* __restrict__ sigma, double* __restrict__ flip, int mode) {
+                      double* __restrict__ sigma, double* __restrict__ flip, int mode, MassRows ms) {
   BAMG_PDL_PROLOGUE();
   constexpr int VV = K / G;
   constexpr int RB = TILE_THREADS / G;
@@ -377,11 +419,24 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
       double uu[VV], vv[VV];
       VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
       VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
+      double mu[VV], nv[VV];
+      if (ms.mrp) {
+        row_apply<K, VV, U>(ms.mrp, ms.mcol, ms.mval, Uv, row, voff, mu);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VV; ++q) mu[q] = uu[q];
+      }
+      if (ms.nrp) {
+        row_apply<K, VV, U>(ms.nrp, ms.ncol, ms.nval, Vv, row, voff, nv);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VV; ++q) nv[q] = vv[q];
+      }
 #pragma unroll
       for (int q = 0; q < VV; ++q) {
         s0[q] += uu[q] * acc[q];
-        s1[q] += uu[q] * uu[q];
-        s2[q] += vv[q] * vv[q];
+        s1[q] += uu[q] * mu[q];
+        s2[q] += vv[q] * nv[q];
       }
     }
   }
@@ -440,22 +495,34 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
 
 // returns 1 when k has no specialisation (caller takes the general path)
 int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const double* V, int k, double* sigma,
-                       double* flip, int mode, double* dots) {
+                       double* flip, int mode, double* dots, const bamg_csr* M, const bamg_csr* N) {
   BAMG_TRY(check_csr(ctx, A));
   if (((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(V)) & 15) != 0 && !(k & 1)) return 1;
-  // fixed grid (a constant, so the partial-sum tree is reproducible), up to
-  // 8 CTAs per SM of row tiles in flight
+  // grid: a fixed function of the row count (so the partial-sum tree is
+  // reproducible), up to 8 CTAs per SM of row tiles in flight
   constexpr int RQ_BLOCKS = 8 * 148;
+  const int rb_rows = TILE_THREADS / 8;  // rows per tile at the widest G
+  int nblk = (A->nrows + 4 * rb_rows - 1) / (4 * rb_rows);
+  nblk = nblk < 1 ? 1 : (nblk > RQ_BLOCKS ? RQ_BLOCKS : nblk);
   double* partial;
   BAMG_TRY(arena_get(ctx, (size_t)RQ_BLOCKS * 3 * k, &partial));
   const double n = A->nrows;
-  const double bytes = 4.0 * (n + 1) + 12.0 * (double)A->nnz + 8.0 * k * A->ncols + 8.0 * k * n;
+  double bytes = 4.0 * (n + 1) + 12.0 * (double)A->nnz + 8.0 * k * A->ncols + 8.0 * k * n;
+  MassRows ms{};
+  if (M) {
+    ms.mrp = M->rowptr, ms.mcol = M->col, ms.mval = M->val;
+    bytes += 4.0 * (n + 1) + 12.0 * (double)M->nnz;
+  }
+  if (N) {
+    ms.nrp = N->rowptr, ms.ncol = N->col, ms.nval = N->val;
+    bytes += 4.0 * (n + 1) + 12.0 * (double)N->nnz;
+  }
   switch (k) {
 #define BAMG_RQ_CASE(KK, GG, UU)                                                                              \
   case KK:                                                                                                   \
-    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), RQ_BLOCKS, TILE_THREADS, 0,  \
+    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), nblk, TILE_THREADS, 0,  \
                     A->nrows, A->rowptr, A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, \
-                    mode);                                                                                   \
+                    mode, ms);                                                                               \
     return 0;
     BAMG_RQ_CASE(1, 1, BAMG_U1)
     BAMG_RQ_CASE(2, 1, 4)
