@@ -10,6 +10,9 @@ int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t*
                const double* b, const double* b_scale, const double* x, double* x_out, int k,
                double omega, double* peak, const double* rd = nullptr);
 int recip_dev(bamg_ctx* ctx, const double* d, int64_t n, double* rd);
+int jacobi_mass_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip, const bamg_csr* M,
+                    const double* mx, const double* sigma, const double* x, double* x_out, int k, double omega,
+                    double* peak, const double* rd);
 int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const double* V, int k, double* sigma,
                        double* flip, int mode, double* dots, const bamg_csr* M = nullptr,
                        const bamg_csr* N = nullptr);

@@ -216,25 +216,38 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
     }
     double *u = U, *v = V, *uo = U2, *vo = V2;
     for (int s = 0; s < nsweeps; ++s) {
-      const double* bv = nullptr;  // rhs for the right vectors: sigma * M u
-      const double* bu = nullptr;  // rhs for the left vectors:  sigma * N v
-      if (inhomogeneous) {
-        if (M) {
-          BAMG_TRY(spmm_dev(ctx, M, u, MU, k));
-          bv = MU;
-        } else {
-          bv = u;
-        }
-        if (N) {
-          BAMG_TRY(spmm_dev(ctx, N, v, NV, k));
-          bu = NV;
-        } else {
-          bu = v;
-        }
-      }
       BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * 2 * k, ctx->stream));
-      BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak, rd));
-      BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k, rd));
+      // right vectors: rhs sigma * M u (the mass product fused into the sweep
+      // when the rows kernel covers k), left vectors: sigma * N v
+      int rcv = 1, rcu = 1;
+      if (inhomogeneous && M) rcv = jacobi_mass_dev(ctx, A, d, skip, M, u, sigma, v, vo, k, omega, peak, rd);
+      if (rcv < 0) return rcv;
+      if (rcv == 1) {
+        const double* bv = nullptr;
+        if (inhomogeneous) {
+          if (M) {
+            BAMG_TRY(spmm_dev(ctx, M, u, MU, k));
+            bv = MU;
+          } else {
+            bv = u;
+          }
+        }
+        BAMG_TRY(jacobi_dev(ctx, A, d, skip, bv, inhomogeneous ? sigma : nullptr, v, vo, k, omega, peak, rd));
+      }
+      if (inhomogeneous && N) rcu = jacobi_mass_dev(ctx, A_t, d, skip_t, N, v, sigma, u, uo, k, omega, peak + k, rd);
+      if (rcu < 0) return rcu;
+      if (rcu == 1) {
+        const double* bu = nullptr;
+        if (inhomogeneous) {
+          if (N) {
+            BAMG_TRY(spmm_dev(ctx, N, v, NV, k));
+            bu = NV;
+          } else {
+            bu = v;
+          }
+        }
+        BAMG_TRY(jacobi_dev(ctx, A_t, d, skip_t, bu, inhomogeneous ? sigma : nullptr, u, uo, k, omega, peak + k, rd));
+      }
       if (smooth == 1) {  // init_test_vectors (smooth == 2) has no runaway rescaling
         const int rg = grid_for(2 * n, 256);
         BAMG_LAUNCH(ctx, rescale_kernel, rg < ctx->num_sms * 8 ? rg : ctx->num_sms * 8, 256, 0, vo, uo, total, k,

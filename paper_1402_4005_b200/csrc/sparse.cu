@@ -18,7 +18,10 @@ constexpr int TILE_ROWS = 256;
 constexpr int TILE_THREADS = 256;
 constexpr int TILE_NNZ = 2048;  // 24 KB of staged col/val per CTA
 
-enum { EPI_PLAIN = 0, EPI_JACOBI = 1, EPI_RESID = 2, EPI_ADD = 3 };
+// EPI_JACOBI_M: Jacobi whose right-hand side is b_scale * (Mop bx)[row],
+// the mass product formed in the same pass (the inhomogeneous bootstrap
+// sweeps' sigma M u / sigma N v on the coarse levels)
+enum { EPI_PLAIN = 0, EPI_JACOBI = 1, EPI_RESID = 2, EPI_ADD = 3, EPI_JACOBI_M = 4 };
 
 struct EpiArgs {
   const double* d;        // diagonal
@@ -29,6 +32,11 @@ struct EpiArgs {
   const double* rd;       // RN(1/d) (may be null: plain IEEE division)
   double omega;
   double* peak;           // per-vector max |x'| (may be null)
+  const int32_t* mrp;     // EPI_JACOBI_M: the mass operator's CSR ...
+  const int32_t* mcol;
+  const double* mval;
+  const double* mx;       // ... and the block it multiplies
+  int64_t mnnz;
 };
 
 template <int EPI>
@@ -133,6 +141,36 @@ struct VecIO {
   }
 };
 
+// slice [voff, voff + VV) of (Op X)[row], sequential ascending-column sums
+template <int K, int VV, int U>
+__device__ __forceinline__ void row_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                          const double* __restrict__ val, const double* __restrict__ X, int row,
+                                          int voff, double* acc) {
+#pragma unroll
+  for (int q = 0; q < VV; ++q) acc[q] = 0.0;
+  const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  for (int j = jb; j < je; j += U) {
+    int cc[U];
+    double aa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = j + u < je ? j + u : je - 1;
+      cc[u] = __ldg(col + jj);
+      aa[u] = __ldg(val + jj);
+    }
+    double xv[U][VV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) VecIO<VV>::load(X + (int64_t)cc[u] * K + voff, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < je) {
+#pragma unroll
+        for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+      }
+    }
+  }
+}
+
 // G threads share a row, each owning V = K / G consecutive vectors (one
 // 16-byte load per neighbour when V = 2), and the row's entries are consumed
 // U at a time: all U neighbour segments are loaded before any is accumulated,
@@ -157,7 +195,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
   __shared__ unsigned long long s_peak[K];
   const int r0 = blockIdx.x * RB;
   const int rows = min(RB, nrows - r0);
-  if (EPI == EPI_JACOBI && ea.peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
+  if ((EPI == EPI_JACOBI || EPI == EPI_JACOBI_M) && ea.peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
   int nz0 = 0;
   bool staged = false;
   if constexpr (STAGE) {
@@ -171,7 +209,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       }
     }
     __syncthreads();
-  } else if (EPI == EPI_JACOBI && ea.peak) {
+  } else if ((EPI == EPI_JACOBI || EPI == EPI_JACOBI_M) && ea.peak) {
     __syncthreads();
   }
   const int lr = threadIdx.x / G;
@@ -228,7 +266,11 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       for (int q = 0; q < V; ++q) out[q] = __dadd_rn(xo[q], acc[q]);
     } else {
       double bv[V];
-      if (ea.b) {
+      if (EPI == EPI_JACOBI_M) {
+        row_apply<K, V, U>(ea.mrp, ea.mcol, ea.mval, ea.mx, row, voff, bv);
+#pragma unroll
+        for (int q = 0; q < V; ++q) bv[q] = __dmul_rn(ea.b_scale[voff + q], bv[q]);
+      } else if (ea.b) {
         VecIO<V>::load(ea.b + base, bv);
         if (ea.b_scale) {
 #pragma unroll
@@ -253,7 +295,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
     }
     VecIO<V>::store(Y + base, out);
   }
-  if (EPI == EPI_JACOBI && ea.peak) {
+  if ((EPI == EPI_JACOBI || EPI == EPI_JACOBI_M) && ea.peak) {
     // max over the lanes that own the same vectors (lane % G), then one
     // shared atomic per (warp, vector) and one global atomic per (CTA, vector)
     constexpr bool POW2 = (G & (G - 1)) == 0;  // lane % G groups survive xor shuffles
@@ -330,36 +372,6 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A);
 // per-CTA partials -- and the last CTA's fixed-order final sum and sigma
 // finish -- are bit-reproducible.  Saves the A V write + re-read and two
 // launches per quotient.
-// slice [voff, voff + VV) of (Op X)[row], sequential ascending-column sums
-template <int K, int VV, int U>
-__device__ __forceinline__ void row_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                          const double* __restrict__ val, const double* __restrict__ X, int row,
-                                          int voff, double* acc) {
-#pragma unroll
-  for (int q = 0; q < VV; ++q) acc[q] = 0.0;
-  const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
-  for (int j = jb; j < je; j += U) {
-    int cc[U];
-    double aa[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int jj = j + u < je ? j + u : je - 1;
-      cc[u] = __ldg(col + jj);
-      aa[u] = __ldg(val + jj);
-    }
-    double xv[U][VV];
-#pragma unroll
-    for (int u = 0; u < U; ++u) VecIO<VV>::load(X + (int64_t)cc[u] * K + voff, xv[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (j + u < je) {
-#pragma unroll
-        for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
-      }
-    }
-  }
-}
-
 // Masses M, N (nullable = identity): u.(M u) and v.(N v) from their rows in
 // the same pass (the coarse levels' inhomogeneous sweeps), without writing
 // M U, N V, A V.
@@ -559,6 +571,7 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   if (epi == EPI_RESID) bytes += 8.0 * n;                         // b
   if (epi == EPI_ADD) bytes += 8.0 * kk * n;                      // x_old
   if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * kk * n : 0.0) + 9.0 * n;  // b, d, skip (x_old == X)
+  if (epi == EPI_JACOBI_M) bytes += 4.0 * (n + 1) + 12.0 * (double)ea.mnnz + 8.0 * kk * n + 9.0 * n;
   // 16-byte vector loads need aligned blocks when K is even (K = 1 has none)
   bool aligned = (k & 1) || ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
                               reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold)) & 15) == 0;
@@ -568,10 +581,12 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
       case EPI_PLAIN: rc = launch_rows<EPI_PLAIN>(ctx, k, grid, bytes, A, X, Y, ea); break;
       case EPI_RESID: rc = launch_rows<EPI_RESID>(ctx, k, grid, bytes, A, X, Y, ea); break;
       case EPI_ADD: rc = launch_rows<EPI_ADD>(ctx, k, grid, bytes, A, X, Y, ea); break;
+      case EPI_JACOBI_M: rc = launch_rows<EPI_JACOBI_M>(ctx, k, grid, bytes, A, X, Y, ea); break;
       default: rc = launch_rows<EPI_JACOBI>(ctx, k, grid, bytes, A, X, Y, ea);
     }
     if (rc <= 0) return rc;
   }
+  if (epi == EPI_JACOBI_M) return 1;  // rows kernel only: the caller forms the mass product separately
   switch (epi) {
     case EPI_PLAIN:
       BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_PLAIN>, grid, TILE_THREADS, 0, A->nrows,
@@ -624,6 +639,30 @@ int jacobi_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t*
   ea.omega = omega;
   ea.peak = peak;
   return launch_tile(ctx, EPI_JACOBI, A, x, k, x_out, ea);
+}
+
+// Jacobi sweep with right-hand side sigma * (M mx), the mass product formed
+// row by row inside the sweep (bit-identical to spmm_dev(M, mx) followed by
+// jacobi_dev with b_scale = sigma).  Returns 1 when k has no rows-kernel
+// specialisation or the blocks are misaligned (caller takes the two-launch path).
+int jacobi_mass_dev(bamg_ctx* ctx, const bamg_csr* A, const double* d, const uint8_t* skip, const bamg_csr* M,
+                    const double* mx, const double* sigma, const double* x, double* x_out, int k, double omega,
+                    double* peak, const double* rd) {
+  EpiArgs ea{};
+  ea.d = d;
+  ea.rd = rd;
+  ea.skip = skip;
+  ea.b_scale = sigma;
+  ea.xold = x;
+  ea.omega = omega;
+  ea.peak = peak;
+  ea.mrp = M->rowptr;
+  ea.mcol = M->col;
+  ea.mval = M->val;
+  ea.mx = mx;
+  ea.mnnz = M->nnz;
+  if (!(k & 1) && (reinterpret_cast<uintptr_t>(mx) & 15) != 0) return 1;
+  return launch_tile(ctx, EPI_JACOBI_M, A, x, k, x_out, ea);
 }
 
 // rd[i] = RN(1 / d[i]) (the reciprocal the Jacobi epilogue's exact division uses)
