@@ -1735,6 +1735,307 @@ static int derived_pinv(bamg_ctx* ctx, const double* Bd, const double* LM, const
   return ok ? 0 : 1;
 }
 
+// ------------------------------------------ implicit coarsest operator
+// For large n the explicit K = L_M^-1 B L_N^-T (two n x n TRSMs) and K^+ (LU
+// + two more n x n TRSMs) cost ~5 n^3 flops.  The subspace iteration only
+// applies K^+ and K^+T to p ~ 20-30 vectors, so this path factors B once and
+// applies
+//   K^+ = (I - b0 b0^T) G (I - a0 a0^T),  G = L_N^T B^g L_M,
+// where B^g is the leading n x n block of the bordered inverse
+// [[B, 1/sqrt(n)], [1/sqrt(n)^T, 0]]^-1 (a {1}-inverse of the rank n-1 B, so
+// K G K = K) and a0, b0 are K's unit null vectors (the identity used for the
+// V-cycle's derived B^+).  Each application: two GEMMs with the Cholesky
+// factors and two triangular solves with p right-hand sides against the
+// bordered LU, whose LEAF x LEAF diagonal blocks are inverted once so every
+// leaf of the recursive solve is a single GEMM.
+constexpr int CLU_LEAF = 1024;
+
+__global__ void eye_block_kernel(double* X, int ld, int nb) {
+  BAMG_PDL_PROLOGUE();
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nb * nb) return;
+  int r = (int)(t % nb), c = (int)(t / nb);
+  X[(int64_t)c * ld + r] = r == c ? 1.0 : 0.0;
+}
+
+// Y[r][c] = X[perm[r]][c] (gather, m x p, ld m) or X[r] -> Y[perm[r]] (scatter)
+__global__ void perm_rows_kernel(const double* __restrict__ X, int m, int p, const int* __restrict__ perm,
+                                 double* __restrict__ Y, int scatter) {
+  BAMG_PDL_PROLOGUE();
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * p) return;
+  int r = (int)(t % m), c = (int)(t / m);
+  if (scatter) Y[(int64_t)c * m + perm[r]] = X[t];
+  else Y[t] = X[(int64_t)c * m + perm[r]];
+}
+
+// columns: dots[c] = v . Y[:, c]
+__global__ void vec_coldot_kernel(const double* __restrict__ Y, int ld, int n, const double* __restrict__ v,
+                                  double* __restrict__ dots) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  const double* y = Y + (int64_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i] * y[i];
+  s = bsum(s, sh);
+  if (threadIdx.x == 0) dots[blockIdx.x] = s;
+}
+
+// Y[:, c] = X[:, c] - v dots[c]   (n rows; X, Y ld)
+__global__ void rank1_sub_kernel(const double* __restrict__ X, int ldx, int n, int p, const double* __restrict__ v,
+                                 const double* __restrict__ dots, double* __restrict__ Y, int ldy) {
+  BAMG_PDL_PROLOGUE();
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * p) return;
+  int r = (int)(t % n), c = (int)(t / n);
+  Y[(int64_t)c * ldy + r] = X[(int64_t)c * ldx + r] - v[r] * dots[c];
+}
+
+__global__ void zero_row_kernel(double* X, int ld, int row, int p) {
+  BAMG_PDL_PROLOGUE();
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < p) X[(int64_t)c * ld + row] = 0.0;
+}
+
+struct CoarseLU {
+  int n = 0, m = 0, nblk = 0, leaf = CLU_LEAF;
+  double* LU = nullptr;    // m x m bordered LU (arena)
+  int* perm = nullptr;     // m
+  double* Linv = nullptr;  // nblk blocks of CLU_LEAF^2: inverses of L's diagonal blocks
+  double* Uinv = nullptr;  // same for U
+};
+
+// Triangular solve with the cached inverse diagonal blocks: recursion on
+// CLU_LEAF-aligned halves, each leaf one GEMM (X_i = op(T_ii^-1) B_i).
+static int trsm_cached(bamg_ctx* ctx, const CoarseLU& C, const double* T, const double* Tinv, int b0, int nb,
+                       bool lower_stored, bool trans, double* B, int ldb, int p, double* tmp) {
+  const int lt = C.m;
+  const int i0 = b0 * C.leaf;
+  const int n = std::min(nb * C.leaf, C.m - i0);
+  if (nb == 1) {
+    BAMG_TRY(gemm(ctx, trans, false, n, p, n, 1.0, Tinv + (size_t)b0 * C.leaf * C.leaf, C.leaf, B + i0, ldb,
+                  0.0, tmp, n));
+    return copy_block(ctx, tmp, n, B + i0, ldb, n, p);
+  }
+  const int hb = (nb + 1) / 2;
+  const int h = hb * C.leaf;  // rows of the first half (absolute: i0 .. i0 + h)
+  const bool eff_lower = lower_stored != trans;
+  const double* Tb0 = T + (int64_t)i0 * lt + i0;  // the sub-triangle's corner
+  if (eff_lower) {
+    BAMG_TRY(trsm_cached(ctx, C, T, Tinv, b0, hb, lower_stored, trans, B, ldb, p, tmp));
+    const double* Tb = trans ? Tb0 + (int64_t)h * lt : Tb0 + h;
+    BAMG_TRY(gemm(ctx, trans, false, n - h, p, h, -1.0, Tb, lt, B + i0, ldb, 1.0, B + i0 + h, ldb));
+    return trsm_cached(ctx, C, T, Tinv, b0 + hb, nb - hb, lower_stored, trans, B, ldb, p, tmp);
+  }
+  BAMG_TRY(trsm_cached(ctx, C, T, Tinv, b0 + hb, nb - hb, lower_stored, trans, B, ldb, p, tmp));
+  const double* Tb = trans ? Tb0 + h : Tb0 + (int64_t)h * lt;
+  BAMG_TRY(gemm(ctx, trans, false, h, p, n - h, -1.0, Tb, lt, B + i0 + h, ldb, 1.0, B + i0, ldb));
+  return trsm_cached(ctx, C, T, Tinv, b0, hb, lower_stored, trans, B, ldb, p, tmp);
+}
+
+// X (m x p, ld m) <- Bb^-1 X (trans: Bb^-T X); tmp (m x p) scratch, tmp2 (m x p) leaf scratch
+static int lu_solve_cached(bamg_ctx* ctx, const CoarseLU& C, double* X, int p, bool trans, double* tmp,
+                           double* tmp2) {
+  const int m = C.m;
+  const int g = grid_for((int64_t)m * p, 256);
+  if (!trans) {
+    BAMG_LAUNCH(ctx, perm_rows_kernel, g, 256, 0, X, m, p, C.perm, tmp, 0);
+    BAMG_TRY(trsm_cached(ctx, C, C.LU, C.Linv, 0, C.nblk, true, false, tmp, m, p, tmp2));   // L (unit lower)
+    BAMG_TRY(trsm_cached(ctx, C, C.LU, C.Uinv, 0, C.nblk, false, false, tmp, m, p, tmp2));  // U
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(X, tmp, sizeof(double) * (size_t)m * p, cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+    return 0;
+  }
+  BAMG_TRY(trsm_cached(ctx, C, C.LU, C.Uinv, 0, C.nblk, false, true, X, m, p, tmp2));  // U^T
+  BAMG_TRY(trsm_cached(ctx, C, C.LU, C.Linv, 0, C.nblk, true, true, X, m, p, tmp2));   // L^T
+  BAMG_LAUNCH(ctx, perm_rows_kernel, g, 256, 0, X, m, p, C.perm, tmp, 1);
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(X, tmp, sizeof(double) * (size_t)m * p, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+  return 0;
+}
+
+// Bordered LU of B + cached block inverses.  Returns 1 when the LU hit a
+// zero pivot.
+static int coarse_lu_build(bamg_ctx* ctx, const double* Bd, int n, CoarseLU& C, double* work) {
+  C.n = n;
+  C.m = n + 1;
+  C.nblk = (C.m + C.leaf - 1) / C.leaf;
+  int *piv, *bad;
+  BAMG_TRY(arena_get(ctx, (size_t)C.m * C.m, &C.LU));
+  BAMG_TRY(arena_get(ctx, (size_t)C.m, &piv));
+  BAMG_TRY(arena_get(ctx, (size_t)C.m, &C.perm));
+  BAMG_TRY(arena_get(ctx, 1, &bad));
+  BAMG_TRY(arena_get(ctx, (size_t)C.nblk * C.leaf * C.leaf, &C.Linv));
+  BAMG_TRY(arena_get(ctx, (size_t)C.nblk * C.leaf * C.leaf, &C.Uinv));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  BAMG_LAUNCH(ctx, border_fill_kernel, grid_for((int64_t)C.m * C.m, 256), 256, 0, Bd, n, C.LU);
+  BAMG_TRY(lu_blocked(ctx, C.LU, C.m, piv, bad, work));
+  BAMG_LAUNCH(ctx, perm_vector_kernel, 1, 32, 0, C.m, piv, C.perm);
+  for (int b = 0; b < C.nblk; ++b) {
+    const int i0 = b * C.leaf, ib = std::min(C.leaf, C.m - i0);
+    const double* Tkk = C.LU + (int64_t)i0 * C.m + i0;
+    double* Li = C.Linv + (size_t)b * C.leaf * C.leaf;
+    double* Ui = C.Uinv + (size_t)b * C.leaf * C.leaf;
+    BAMG_LAUNCH(ctx, eye_block_kernel, grid_for((int64_t)ib * ib, 256), 256, 0, Li, C.leaf, ib);
+    BAMG_LAUNCH(ctx, eye_block_kernel, grid_for((int64_t)ib * ib, 256), 256, 0, Ui, C.leaf, ib);
+    BAMG_TRY(tri_solve_blk(ctx, Tkk, C.m, ib, true, true, false, Li, C.leaf, ib, work));
+    BAMG_TRY(tri_solve_blk(ctx, Tkk, C.m, ib, false, false, false, Ui, C.leaf, ib, work));
+  }
+  int hb = 0;
+  BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
+  return hb ? 1 : 0;
+}
+
+struct KpOperator {
+  const CoarseLU* C;
+  const double *LM, *LN, *a0, *b0;
+  int n;
+  double *t1, *t2, *t3, *t4, *dots;  // scratch: n x p, m x p, m x p, m x p, p
+};
+
+// Yout = K^+ Yin (trans: K^+T Yin), n x p column-major
+static int kp_apply(bamg_ctx* ctx, const KpOperator& K, const double* Yin, double* Yout, int p, bool trans) {
+  const int n = K.n, m = K.C->m;
+  const double* pre = trans ? K.b0 : K.a0;   // projector applied first
+  const double* post = trans ? K.a0 : K.b0;  // projector applied last
+  const double* Lin = trans ? K.LN : K.LM;   // factor multiplied before the solve
+  const double* Lout = trans ? K.LM : K.LN;  // transposed factor after it
+  const int g = grid_for((int64_t)n * p, 256);
+  BAMG_LAUNCH(ctx, vec_coldot_kernel, p, 256, 0, Yin, n, n, pre, K.dots);
+  BAMG_LAUNCH(ctx, rank1_sub_kernel, g, 256, 0, Yin, n, n, p, pre, K.dots, K.t1, n);
+  BAMG_TRY(gemm(ctx, false, false, n, p, n, 1.0, Lin, n, K.t1, n, 0.0, K.t2, m));  // rows 0..n-1 of t2
+  BAMG_LAUNCH(ctx, zero_row_kernel, grid_for(p, 64), 64, 0, K.t2, m, n, p);
+  BAMG_TRY(lu_solve_cached(ctx, *K.C, K.t2, p, trans, K.t3, K.t4));
+  BAMG_TRY(gemm(ctx, true, false, n, p, n, 1.0, Lout, n, K.t2, m, 0.0, K.t1, n));
+  BAMG_LAUNCH(ctx, vec_coldot_kernel, p, 256, 0, K.t1, n, n, post, K.dots);
+  BAMG_LAUNCH(ctx, rank1_sub_kernel, g, 256, 0, K.t1, n, n, p, post, K.dots, Yout, n);
+  return 0;
+}
+
+static bool implicit_coarsest_enabled(int n) {
+  const char* e = getenv("BAMG_IMPLICIT_N");  // smallest n taking the implicit path (tests: small)
+  const int lim = e ? atoi(e) : 4096;
+  return lim > 0 && n >= lim;
+}
+
+template <typename Stage>
+static int coarsest_implicit(bamg_ctx* ctx, const double* Bd, const double* LM, const double* LN, int n, int r, int p,
+                             double* U, double* V, double* sigma, double* Y, double* Z, double* tmp, double* Gs,
+                             double* Ri, double* Vs, double* sv, double* work, double* a0, double* b0, double* A,
+                             double* Bv, double* KB, double* dots, Stage& stage) {
+  CoarseLU C;
+  const int lrc = coarse_lu_build(ctx, Bd, n, C, work);
+  if (lrc != 0) return lrc;  // zero pivot: explicit path
+  const int m = C.m;
+  double *e, *t1, *t2, *t3, *t4, *pd, *out;
+  BAMG_TRY(arena_get(ctx, (size_t)m * 2, &e));
+  BAMG_TRY(arena_get(ctx, (size_t)n * p, &t1));
+  BAMG_TRY(arena_get(ctx, (size_t)m * p, &t2));
+  BAMG_TRY(arena_get(ctx, (size_t)m * p, &t3));
+  BAMG_TRY(arena_get(ctx, (size_t)m * p, &t4));
+  BAMG_TRY(arena_get(ctx, (size_t)p, &pd));
+  BAMG_TRY(arena_get(ctx, 8, &out));
+  // null vectors of B from the bordered inverse's last column / row
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(e, 0, sizeof(double) * 2 * m, ctx->stream));
+  const double one = 1.0;
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e + (m - 1), &one, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e + m + (m - 1), &one, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  BAMG_TRY(lu_solve_cached(ctx, C, e, 1, false, t3, t4));      // e[0:n] ~ z, e[n] = omega
+  BAMG_TRY(lu_solve_cached(ctx, C, e + m, 1, true, t3, t4));   // (e+m)[0:n] ~ y
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, e, n);      // z (unit)
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, e + m, n);  // y (unit)
+  const double* z = e;
+  const double* y = e + m;
+  // certificate: |B z|, |B^T y| at round-off (B has rank n - 1 with these null vectors)
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * 8, ctx->stream));
+  BAMG_TRY(gemm(ctx, false, false, n, 1, n, 1.0, Bd, n, z, n, 0.0, t1, n));
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, Bd, n, y, n, 0.0, t1 + n, n));
+  BAMG_LAUNCH(ctx, frob2_kernel, 1, 256, 0, t1, (int64_t)n, out + 0);
+  BAMG_LAUNCH(ctx, frob2_kernel, 1, 256, 0, t1 + n, (int64_t)n, out + 1);
+  BAMG_LAUNCH(ctx, frob2_kernel, 2 * ctx->num_sms, 256, 0, Bd, (int64_t)n * n, out + 2);
+  double h[3];
+  BAMG_TRY(ctx_read_doubles(ctx, out, 3, h));
+  const double tol = 1e-13 * std::sqrt(h[2]) / std::sqrt((double)n);
+  const bool cert = std::sqrt(h[0]) <= tol && std::sqrt(h[1]) <= tol;
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] implicit coarsest n=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e -> %s\n", n, std::sqrt(h[0]),
+            std::sqrt(h[1]), std::sqrt(h[2]), cert ? "certified" : "explicit path");
+  if (!cert) return 1;
+  // K's unit null vectors: a0 ~ L_M^T y, b0 ~ L_N^T z
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, LM, n, y, n, 0.0, a0, n));
+  BAMG_TRY(gemm(ctx, true, false, n, 1, n, 1.0, LN, n, z, n, 0.0, b0, n));
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, a0, n);
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, 1, 256, 0, b0, n);
+  stage("@pinv");
+  KpOperator K{&C, LM, LN, a0, b0, n, t1, t2, t3, t4, pd};
+  // block subspace iteration on K^+ (as the explicit path), products applied
+  BAMG_LAUNCH(ctx, pseudo_random_kernel, grid_for((int64_t)n * p, 256), 256, 0, Y, (int64_t)n * p, 12345u);
+  BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+  std::vector<double> prev(p, 0.0), cur(p, 0.0);
+  int iters = 0;
+  for (int blk = 0; blk < 100; ++blk) {
+    for (int it = 0; it < 5; ++it) {
+      BAMG_TRY(kp_apply(ctx, K, Y, Z, p, true));
+      BAMG_TRY(orthonormalize(ctx, Z, n, p, Gs, Ri, tmp));
+      BAMG_TRY(kp_apply(ctx, K, Z, Y, p, false));
+      BAMG_TRY(orthonormalize(ctx, Y, n, p, Gs, Ri, tmp));
+    }
+    BAMG_TRY(kp_apply(ctx, K, Y, Z, p, true));
+    BAMG_TRY(jacobi_svd_public(ctx, Z, n, p, Vs, sv));
+    iters += 5;
+    BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
+    std::vector<double> c2 = cur;
+    std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
+    double change = 0.0;
+    for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
+    prev = c2;
+    if (change < 1e-14) break;
+  }
+  stage("@subspace");
+  // Rayleigh-Ritz: Z = K^+T Y, Jacobi: Z Vs = W diag(s); left vectors W, right Y Vs
+  BAMG_TRY(kp_apply(ctx, K, Y, Z, p, true));
+  BAMG_TRY(jacobi_svd_public(ctx, Z, n, p, Vs, sv));
+  std::vector<double> sh(p);
+  BAMG_TRY(ctx_read_doubles(ctx, sv, p, sh.data()));
+  std::vector<int> order(p);
+  for (int q = 0; q < p; ++q) order[q] = q;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return sh[a] > sh[b] || (sh[a] == sh[b] && a < b); });
+  BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Vs, p, 0.0, tmp, n));
+  std::vector<double> sig_host(r);
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(A, a0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Bv, b0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  sig_host[0] = 0.0;
+  for (int j = 1; j < r; ++j) {
+    int q = order[j - 1];
+    sig_host[j] = sh[q] > 0.0 ? 1.0 / sh[q] : INFINITY;
+    BAMG_TRY(copy_block(ctx, Z + (int64_t)q * n, n, A + (int64_t)j * n, n, n, 1));
+    BAMG_TRY(copy_block(ctx, tmp + (int64_t)q * n, n, Bv + (int64_t)j * n, n, n, 1));
+  }
+  double smax = 0.0;
+  int ntiny = 0;
+  for (int j = 0; j < r; ++j) smax = fmax(smax, sig_host[j]);
+  for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
+  BAMG_REQUIRE(ctx, ntiny <= 1, "large coarsest operator has more than one numerically-null triplet");
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+  stage("@ritz");
+  // unit a, b -> u = L_M^-T a, v = L_N^-T b (M- / N-normalised); sign rule
+  // u^T B v = a^T K b >= 0 evaluated with B after the solves
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, A, n);
+  BAMG_LAUNCH(ctx, cm_colnorm_scale_kernel, r, 256, 0, Bv, n);
+  BAMG_TRY(tri_solve(ctx, LM, n, true, false, true, A, n, r, work));
+  BAMG_TRY(tri_solve(ctx, LN, n, true, false, true, Bv, n, r, work));
+  BAMG_TRY(gemm(ctx, false, false, n, r, n, 1.0, Bd, n, Bv, n, 0.0, KB, n));
+  BAMG_LAUNCH(ctx, cm_coldot_kernel, r, 256, 0, A, KB, n, dots);
+  BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
+  stage("@finish");
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] implicit triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p,
+            iters, r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);
+  return 0;
+}
+
 // Large-n coarsest triplets.  Md and Nd are overwritten by their Cholesky
 // factors (they are the caller's dense temporaries).  With Zpinv non-null,
 // the V-cycle's pseudo-inverse of B is derived from the same factors
@@ -1746,8 +2047,6 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   const int p = r + 12 < n ? r + 12 : n;
   double *K, *Kp, *Y, *Z, *Gs, *Ri, *tmp, *Vs, *sv, *work, *a0, *b0, *A, *Bv, *KB, *dots;
   int* bad;
-  BAMG_TRY(arena_get(ctx, nn, &K));
-  BAMG_TRY(arena_get(ctx, nn, &Kp));
   BAMG_TRY(arena_get(ctx, (size_t)n * p, &Y));
   BAMG_TRY(arena_get(ctx, (size_t)n * p, &Z));
   BAMG_TRY(arena_get(ctx, (size_t)n * p, &tmp));
@@ -1792,6 +2091,13 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     return 2;
   }
   stage("@cholesky");
+  if (implicit_coarsest_enabled(n)) {
+    const int irc = coarsest_implicit(ctx, Bd, Md, Nd, n, r, p, U, V, sigma, Y, Z, tmp, Gs, Ri, Vs, sv, work, a0, b0,
+                                      A, Bv, KB, dots, stage);
+    if (irc <= 0) return irc;  // done (or an error); 1: not certified, take the explicit path
+  }
+  BAMG_TRY(arena_get(ctx, nn, &K));
+  BAMG_TRY(arena_get(ctx, nn, &Kp));
   // K = L_M^-1 B L_N^-T :  T = L_M^-1 B ; K^T = L_N^-1 T^T
   BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(K, Bd, sizeof(double) * nn, cudaMemcpyDeviceToDevice, ctx->stream));
   BAMG_TRY(tri_solve(ctx, Md, n, true, false, false, K, n, n, work));
