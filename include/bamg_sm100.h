@@ -284,6 +284,17 @@ int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const double* Md,
  * (dense.py:118-131, built solver.py:93-94) for the coarsest level. */
 int bamg_coarsest_triplets_pinv(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n, int r,
                                 double* U, double* V, double* sigma, double* Z, int* z_valid);
+/* As bamg_coarsest_triplets_pinv (Z may be null); when the large coarsest
+ * level took the implicit path (the bordered LU of B, no explicit K^+),
+ * *lu_out receives that LU for the V-cycle (bamg_hier_set_coarsest_lu) and Z
+ * is not formed.  Free with bamg_coarse_lu_destroy. */
+typedef struct bamg_coarse_lu bamg_coarse_lu;
+int bamg_coarsest_triplets_ex(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n, int r,
+                              double* U, double* V, double* sigma, double* Z, int* z_valid,
+                              bamg_coarse_lu** lu_out);
+/* x = B^+ b through the kept LU: (I - z z^T) B^g (I - y y^T) b. */
+int bamg_coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* lu, const double* b, double* x);
+int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* lu);
 
 /* ----------------------------------------------------------- solver (solver.py) */
 /* Hierarchy for the V-cycle (VCycleOperator, solver.py:79-124).  Level
@@ -295,6 +306,8 @@ int bamg_hier_destroy(bamg_hier* h);
 int bamg_hier_set_level(bamg_hier* h, int level, const bamg_csr* B, const double* d,
                         const uint8_t* skip, const bamg_csr* P, const bamg_csr* Q);
 int bamg_hier_set_coarsest(bamg_hier* h, const double* Z, int n);
+/* The coarsest solve through a kept coarse LU instead of an explicit Z. */
+int bamg_hier_set_coarsest_lu(bamg_hier* h, const bamg_coarse_lu* lu, int n);
 int bamg_hier_set_smoother(bamg_hier* h, double omega, int nu_pre, int nu_post);
 /* x = C b, one V-cycle from a zero guess. */
 int bamg_vcycle(bamg_ctx* ctx, bamg_hier* h, const double* b, double* x);

@@ -103,6 +103,10 @@ _SIGS = {
     "bamg_hier_destroy": [P],
     "bamg_hier_set_level": [P, C.c_int, PCSR, P, P, PCSR, PCSR],
     "bamg_hier_set_coarsest": [P, P, C.c_int],
+    "bamg_hier_set_coarsest_lu": [P, P, C.c_int],
+    "bamg_coarsest_triplets_ex": [P, P, P, P, C.c_int, C.c_int, P, P, P, P, P, P],
+    "bamg_coarse_lu_apply": [P, P, P, P],
+    "bamg_coarse_lu_destroy": [P, P],
     "bamg_hier_set_smoother": [P, F64, C.c_int, C.c_int],
     "bamg_vcycle": [P, P, P, P],
     "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, C.c_int, PINT, PF64, PINT],

@@ -303,6 +303,8 @@ def coarsest_triplets(B, M, N, r: int) -> TripletSet:
     # K^+ (5 x 18 GB at cfg3's n = 47,824): above 4 GB the V-cycle factorises
     # B itself after the setup's dense temporaries are gone
     U, V, s, Z = engine.coarsest_triplets(Bd, Mdd, Ndd, n, r, with_pinv=8 * n * n <= (4 << 30))
+    # Z: B's explicit pseudo-inverse derived from the triplet factors, or the
+    # kept bordered LU of B (engine.CoarseLU) when the implicit path ran
     trips = TripletSet(s, U, V)
     # B's pseudo-inverse from the same factors (large path): the V-cycle takes
     # it instead of factorising B again (solver.VCycleOperator)

@@ -347,7 +347,7 @@ int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
 int large_bordered_pinv(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out, double* zout,
                         double* yout);
 int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double* Nd, int n, int r, double* U,
-                            double* V, double* sigma, double* Zpinv, int* zvalid);
+                            double* V, double* sigma, double* Zpinv, int* zvalid, bamg_coarse_lu** lu_out);
 int large_full_rank_inverse(bamg_ctx* ctx, const double* A, int n, double* P, int rowmajor_out);
 
 // Size above which the blocked / subspace-iteration path replaces the
@@ -1051,7 +1051,8 @@ __global__ void triplet_finish_kernel(const double* __restrict__ Bd, const doubl
 }
 
 static int coarsest_triplets_impl(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n,
-                                  int r, double* U, double* V, double* sigma, double* Z, int* zvalid);
+                                  int r, double* U, double* V, double* sigma, double* Z, int* zvalid,
+                                  bamg_coarse_lu** lu_out = nullptr);
 
 extern "C" int bamg_coarsest_triplets(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n,
                                       int r, double* U, double* V, double* sigma) {
@@ -1066,14 +1067,23 @@ extern "C" int bamg_coarsest_triplets_pinv(bamg_ctx* ctx, const double* Bd, cons
   return coarsest_triplets_impl(ctx, Bd, Md, Nd, n, r, U, V, sigma, Z, z_valid);
 }
 
+extern "C" int bamg_coarsest_triplets_ex(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n,
+                                         int r, double* U, double* V, double* sigma, double* Z, int* z_valid,
+                                         bamg_coarse_lu** lu_out) {
+  if (z_valid) *z_valid = 0;
+  if (lu_out) *lu_out = nullptr;
+  return coarsest_triplets_impl(ctx, Bd, Md, Nd, n, r, U, V, sigma, Z, Z ? z_valid : nullptr, lu_out);
+}
+
 static int coarsest_triplets_impl(bamg_ctx* ctx, const double* Bd, const double* Md, const double* Nd, int n,
-                                  int r, double* U, double* V, double* sigma, double* Z, int* zvalid) {
+                                  int r, double* U, double* V, double* sigma, double* Z, int* zvalid,
+                                  bamg_coarse_lu** lu_out) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, n >= 1 && r >= 1 && r <= 64, "need 1 <= r <= 64");
   if (r > n) r = n;  // take = min(r, n)
   if (n > large_threshold(false)) {
     int rc = large_coarsest_triplets(ctx, Bd, const_cast<double*>(Md), const_cast<double*>(Nd), n, r, U, V, sigma,
-                                     Z, zvalid);
+                                     Z, zvalid, lu_out);
     arena_trim(ctx);
     return rc;
   }

@@ -1886,6 +1886,80 @@ static int coarse_lu_build(bamg_ctx* ctx, const double* Bd, int n, CoarseLU& C, 
   return hb ? 1 : 0;
 }
 
+// The coarsest LU kept for the V-cycle (opaque bamg_coarse_lu of the ABI):
+// persistent copies of the bordered LU, its permutation, the cached block
+// inverses and B's unit null vectors, plus the apply's scratch.
+struct bamg_coarse_lu {
+  CoarseLU C;
+  double *z = nullptr, *y = nullptr;
+  double *t = nullptr, *s1 = nullptr, *s2 = nullptr, *dots = nullptr;
+  std::vector<void*> mem;
+};
+
+static int clu_alloc(bamg_ctx* ctx, bamg_coarse_lu* h, size_t bytes, void** out) {
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(out, bytes));
+  h->mem.push_back(*out);
+  return 0;
+}
+
+static int coarse_lu_keep(bamg_ctx* ctx, const CoarseLU& C, const double* z, const double* y, bamg_coarse_lu** out) {
+  bamg_coarse_lu* h = new bamg_coarse_lu();
+  h->C = C;
+  const size_t m = C.m, blk = (size_t)C.nblk * C.leaf * C.leaf;
+  auto cp = [&](const void* src, size_t bytes, void** dst) -> int {
+    BAMG_TRY(clu_alloc(ctx, h, bytes, dst));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    return 0;
+  };
+  int rc = 0;
+  void* p = nullptr;
+  if ((rc = cp(C.LU, sizeof(double) * m * m, &p)) == 0) h->C.LU = (double*)p;
+  if (!rc && (rc = cp(C.perm, sizeof(int) * m, &p)) == 0) h->C.perm = (int*)p;
+  if (!rc && (rc = cp(C.Linv, sizeof(double) * blk, &p)) == 0) h->C.Linv = (double*)p;
+  if (!rc && (rc = cp(C.Uinv, sizeof(double) * blk, &p)) == 0) h->C.Uinv = (double*)p;
+  if (!rc && (rc = cp(z, sizeof(double) * C.n, &p)) == 0) h->z = (double*)p;
+  if (!rc && (rc = cp(y, sizeof(double) * C.n, &p)) == 0) h->y = (double*)p;
+  if (!rc && (rc = clu_alloc(ctx, h, sizeof(double) * m, &p)) == 0) h->t = (double*)p;
+  if (!rc && (rc = clu_alloc(ctx, h, sizeof(double) * m, &p)) == 0) h->s1 = (double*)p;
+  if (!rc && (rc = clu_alloc(ctx, h, sizeof(double) * m, &p)) == 0) h->s2 = (double*)p;
+  if (!rc && (rc = clu_alloc(ctx, h, sizeof(double) * 2, &p)) == 0) h->dots = (double*)p;
+  if (rc) {
+    for (void* q : h->mem) cudaFree(q);
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return 0;
+}
+
+// x = B^+ b = (I - z z^T) B^g (I - y y^T) b: the V-cycle's coarsest solve
+// through the kept LU (two triangular solves, leaves one GEMV each)
+int coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, double* x) {
+  const int n = h->C.n, m = h->C.m;
+  const int g = grid_for(n, 256);
+  BAMG_LAUNCH(ctx, vec_coldot_kernel, 1, 256, 0, b, n, n, (const double*)h->y, h->dots);
+  BAMG_LAUNCH(ctx, rank1_sub_kernel, g, 256, 0, b, n, n, 1, (const double*)h->y, (const double*)h->dots, h->t, m);
+  BAMG_LAUNCH(ctx, zero_row_kernel, 1, 32, 0, h->t, m, n, 1);
+  BAMG_TRY(lu_solve_cached(ctx, h->C, h->t, 1, false, h->s1, h->s2));
+  BAMG_LAUNCH(ctx, vec_coldot_kernel, 1, 256, 0, (const double*)h->t, m, n, (const double*)h->z, h->dots + 1);
+  BAMG_LAUNCH(ctx, rank1_sub_kernel, g, 256, 0, (const double*)h->t, m, n, 1, (const double*)h->z,
+              (const double*)(h->dots + 1), x, n);
+  return 0;
+}
+
+extern "C" int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* h) {
+  if (!h) return 0;
+  cudaStreamSynchronize(ctx->stream);  // in-flight V-cycles may still read it
+  for (void* q : h->mem) cudaFree(q);
+  delete h;
+  return 0;
+}
+
+extern "C" int bamg_coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, double* x) {
+  BAMG_REQUIRE(ctx, h != nullptr, "null coarse LU");
+  return coarse_lu_apply(ctx, h, b, x);
+}
+
 struct KpOperator {
   const CoarseLU* C;
   const double *LM, *LN, *a0, *b0;
@@ -1922,7 +1996,7 @@ template <typename Stage>
 static int coarsest_implicit(bamg_ctx* ctx, const double* Bd, const double* LM, const double* LN, int n, int r, int p,
                              double* U, double* V, double* sigma, double* Y, double* Z, double* tmp, double* Gs,
                              double* Ri, double* Vs, double* sv, double* work, double* a0, double* b0, double* A,
-                             double* Bv, double* KB, double* dots, Stage& stage) {
+                             double* Bv, double* KB, double* dots, Stage& stage, bamg_coarse_lu** lu_out) {
   CoarseLU C;
   const int lrc = coarse_lu_build(ctx, Bd, n, C, work);
   if (lrc != 0) return lrc;  // zero pivot: explicit path
@@ -2030,6 +2104,7 @@ static int coarsest_implicit(bamg_ctx* ctx, const double* Bd, const double* LM, 
   BAMG_LAUNCH(ctx, cm_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, A, Bv, dots, n, r, U, V);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
   stage("@finish");
+  if (lu_out) BAMG_TRY(coarse_lu_keep(ctx, C, z, y, lu_out));  // the V-cycle's coarsest solve
   if (getenv("BAMG_DEBUG"))
     fprintf(stderr, "[bamg] implicit triplets n=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n, p,
             iters, r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);
@@ -2041,8 +2116,9 @@ static int coarsest_implicit(bamg_ctx* ctx, const double* Bd, const double* LM, 
 // the V-cycle's pseudo-inverse of B is derived from the same factors
 // (derived_pinv) and *zvalid says whether it was certified.
 int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double* Nd, int n, int r, double* U,
-                            double* V, double* sigma, double* Zpinv, int* zvalid) {
+                            double* V, double* sigma, double* Zpinv, int* zvalid, bamg_coarse_lu** lu_out) {
   if (zvalid) *zvalid = 0;
+  if (lu_out) *lu_out = nullptr;
   const size_t nn = (size_t)n * n;
   const int p = r + 12 < n ? r + 12 : n;
   double *K, *Kp, *Y, *Z, *Gs, *Ri, *tmp, *Vs, *sv, *work, *a0, *b0, *A, *Bv, *KB, *dots;
@@ -2093,7 +2169,7 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
   stage("@cholesky");
   if (implicit_coarsest_enabled(n)) {
     const int irc = coarsest_implicit(ctx, Bd, Md, Nd, n, r, p, U, V, sigma, Y, Z, tmp, Gs, Ri, Vs, sv, work, a0, b0,
-                                      A, Bv, KB, dots, stage);
+                                      A, Bv, KB, dots, stage, lu_out);
     if (irc <= 0) return irc;  // done (or an error); 1: not certified, take the explicit path
   }
   BAMG_TRY(arena_get(ctx, nn, &K));

@@ -27,3 +27,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
 int normalize_cols_dev(bamg_ctx* ctx, double* X, int64_t n, int k);
 int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s);
 int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);
+
+struct bamg_coarse_lu;
+// x = B^+ b through the kept coarsest LU (dense_large.cu)
+int coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, double* x);

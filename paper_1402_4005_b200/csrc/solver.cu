@@ -48,6 +48,7 @@ struct bamg_hier {
   std::vector<HLevel> lv;
   const double* Z = nullptr;
   int nz = 0;
+  const bamg_coarse_lu* clu = nullptr;  // coarsest solve through the kept LU (large n)
   double omega = 0.7;
   int nu1 = 3, nu2 = 3;
   std::vector<std::pair<char*, size_t>> owned;  // level buffers (from / back to ctx->buf_pool)
@@ -133,6 +134,15 @@ extern "C" int bamg_hier_set_level(bamg_hier* h, int level, const bamg_csr* B, c
 extern "C" int bamg_hier_set_coarsest(bamg_hier* h, const double* Z, int n) {
   h->Z = Z;
   h->nz = n;
+  h->clu = nullptr;
+  hier_drop_graphs(h);
+  return 0;
+}
+
+extern "C" int bamg_hier_set_coarsest_lu(bamg_hier* h, const bamg_coarse_lu* lu, int n) {
+  h->clu = lu;
+  h->Z = nullptr;
+  h->nz = n;
   hier_drop_graphs(h);
   return 0;
 }
@@ -149,7 +159,7 @@ static int hier_prepare(bamg_hier* h) {
   if (h->ready) return 0;
   bamg_ctx* ctx = h->ctx;
   int L = (int)h->lv.size();
-  BAMG_REQUIRE(ctx, h->Z && h->nz == h->lv[L - 1].n, "coarsest pseudo-inverse missing or wrong size");
+  BAMG_REQUIRE(ctx, (h->Z || h->clu) && h->nz == h->lv[L - 1].n, "coarsest pseudo-inverse missing or wrong size");
   size_t total = 0;
   for (int l = 0; l < L; ++l) {
     HLevel& v = h->lv[l];
@@ -238,7 +248,11 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
   // coarsest: x_L = Z b_L
   HLevel& cl = h->lv[L - 1];
   double* xc = (L == 1) ? x_out : cl.x;
-  BAMG_LAUNCH(ctx, gemv_rowmajor_kernel, grid_for((int64_t)h->nz * 32, 256), 256, 0, h->nz, h->Z, bl, xc);
+  if (h->clu) {
+    BAMG_TRY(coarse_lu_apply(ctx, h->clu, bl, xc));
+  } else {
+    BAMG_LAUNCH(ctx, gemv_rowmajor_kernel, grid_for((int64_t)h->nz * 32, 256), 256, 0, h->nz, h->Z, bl, xc);
+  }
   // upward
   for (int l = L - 2; l >= 0; --l) {
     HLevel& v = h->lv[l];

@@ -362,6 +362,30 @@ def dense_pinv(Dcm, n, rank_tol=1e-12):
     return Z  # row-major pseudo-inverse
 
 
+class CoarseLU:
+    """The coarsest level's bordered LU kept on device by the implicit large
+    path (bamg_coarse_lu): the V-cycle's coarsest solve goes through it."""
+
+    def __init__(self, handle, n):
+        self.handle = handle
+        self.n = n
+        self.shape = (n, n)
+
+    def apply(self, b):
+        x = _empty(self.n)
+        bv = to_device_vec(b)
+        _lib.call("bamg_coarse_lu_apply", self.handle, _p(bv), _p(x))
+        return x
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().bamg_coarse_lu_destroy(_lib.ctx(), self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
     """(U, V, sigma, Z): with `with_pinv`, Z is B's row-major pseudo-inverse
     derived from the triplet solve's factors; None when not requested, when
@@ -371,18 +395,16 @@ def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
     U = _empty((n, take))
     V = _empty((n, take))
     s = _empty(take)
-    if with_pinv:
-        Z = _empty((n, n))
-        ok = C.c_int(0)
-        rc = _lib.call("bamg_coarsest_triplets_pinv", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s),
-                       _p(Z), C.byref(ok))
-    else:
-        rc = _lib.call("bamg_coarsest_triplets", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s))
+    ok = C.c_int(0)
+    lu = C.c_void_p()
+    Z = _empty((n, n)) if with_pinv else None
+    rc = _lib.call("bamg_coarsest_triplets_ex", _p(Bd), _p(Md), _p(Nd), n, take, _p(U), _p(V), _p(s),
+                   _p(Z) if Z is not None else None, C.byref(ok), C.byref(lu))
     if rc == 2:
         raise ValueError("matrix is not positive definite (coarsest mass matrix)")
-    if with_pinv:
-        return U, V, s, (Z if ok.value else None)
-    return U, V, s, None
+    if lu.value:
+        return U, V, s, CoarseLU(lu, n)  # implicit large path: the kept LU serves the V-cycle
+    return U, V, s, (Z if (Z is not None and ok.value) else None)
 
 
 def sign_fix_l1(x, stride=1, uniform_fallback=False):

@@ -125,13 +125,18 @@ class VCycleOperator:
                                              lev.dQ.ref() if lev.dQ is not None else None),
                        "bamg_hier_set_level")
         Zc = getattr(hierarchy.coarsest, "coarse_pinv", None)
-        if Zc is not None and coarsest_rank_tol == 1e-12:
-            # certified B_L^+ derived from the setup's triplet factors (same operator)
-            self._coarse = _DerivedPinv(Zc)
+        if isinstance(Zc, engine.CoarseLU) and coarsest_rank_tol == 1e-12:
+            # the setup's bordered LU of B_L (implicit large path): B_L^+ applied through it
+            self._coarse = Zc
+            _lib.check(L.bamg_hier_set_coarsest_lu(h, Zc.handle, Zc.n), "bamg_hier_set_coarsest_lu")
         else:
-            self._coarse = PinvOperator(hierarchy.coarsest.dB, rank_tol=coarsest_rank_tol)
-        _lib.check(L.bamg_hier_set_coarsest(h, _lib.ptr(self._coarse.Z), self._coarse.n),
-                   "bamg_hier_set_coarsest")
+            if Zc is not None and not isinstance(Zc, engine.CoarseLU) and coarsest_rank_tol == 1e-12:
+                # certified B_L^+ derived from the setup's triplet factors (same operator)
+                self._coarse = _DerivedPinv(Zc)
+            else:
+                self._coarse = PinvOperator(hierarchy.coarsest.dB, rank_tol=coarsest_rank_tol)
+            _lib.check(L.bamg_hier_set_coarsest(h, _lib.ptr(self._coarse.Z), self._coarse.n),
+                       "bamg_hier_set_coarsest")
         sm = self.smoother
         _lib.check(L.bamg_hier_set_smoother(h, float(sm.omega), int(sm.sweeps_pre), int(sm.sweeps_post)),
                    "bamg_hier_set_smoother")
