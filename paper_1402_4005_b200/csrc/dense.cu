@@ -210,7 +210,7 @@ jacobi_svd_coop_kernel(double* G, int nrows, double* V, int ncols, int m, double
         if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) continue;
         double zeta = (b - a) / (2.0 * c);
         double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        double cs = rsqrt(1.0 + t * t), sn = cs * t;
         for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
           double x = __ldcg(gp + r), y = __ldcg(gq + r);
           gp[r] = cs * x - sn * y;
@@ -274,7 +274,7 @@ jacobi_svd_smem_kernel(double* G, int nrows, double* V, int ncols, int m, double
         if (c == 0.0 || !(fabs(c) > tol * sqrt(a * b))) continue;
         double zeta = (b - a) / (2.0 * c);
         double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        double cs = rsqrt(1.0 + t * t), sn = cs * t;
         for (int r = lane; r < nrows; r += 32) {
           double x = gp[r], y = gq[r];
           gp[r] = cs * x - sn * y;
