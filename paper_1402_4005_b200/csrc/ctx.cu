@@ -202,35 +202,63 @@ constexpr int KMAX = 32;
 // (arrival counter, self-resetting) reduces them in a fixed order -- per
 // column, lanes stride over the CTAs, then a warp tree -- so the result is
 // bit-reproducible run to run.
+// KK > 0: k == KK at compile time, each thread loading UR rows before it
+// accumulates them (in the same row order, so the sums are bit-identical to
+// the generic form -- only more loads are in flight); KK == 0: any k <= KMAX.
+template <int KK, int UR>
 __global__ void __launch_bounds__(RED_THREADS)
-colreduce_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t n, int k, int kind,
+colreduce_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t n, int k_rt, int kind,
                  double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ out,
                  int take_sqrt) {
   BAMG_PDL_PROLOGUE();
+  constexpr int KA = KK > 0 ? KK : KMAX;  // accumulators
+  const int k = KK > 0 ? KK : k_rt;
   __shared__ double sh[RED_THREADS / 32][KMAX];
   __shared__ bool last;
   int64_t per = (n + gridDim.x - 1) / gridDim.x;
   int64_t r0 = (int64_t)blockIdx.x * per;
   int64_t r1 = r0 + per < n ? r0 + per : n;
-  double acc[KMAX];
+  double acc[KA];
 #pragma unroll
-  for (int c = 0; c < KMAX; ++c) acc[c] = 0.0;
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+  for (int c = 0; c < KA; ++c) acc[c] = 0.0;
+  int64_t r = r0 + threadIdx.x;
+  if constexpr (KK > 0) {
+    const int64_t step = blockDim.x;
+    for (; r + (UR - 1) * step < r1; r += UR * step) {
+      double xv[UR][KK], yv[UR][KK];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const double* xr = X + (r + u * step) * KK;
+#pragma unroll
+        for (int c = 0; c < KK; ++c) xv[u][c] = xr[c];
+        if (kind != 0) {
+          const double* yr = Y + (r + u * step) * KK;
+#pragma unroll
+          for (int c = 0; c < KK; ++c) yv[u][c] = yr[c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UR; ++u)
+#pragma unroll
+        for (int c = 0; c < KK; ++c) acc[c] += xv[u][c] * (kind == 0 ? xv[u][c] : yv[u][c]);
+    }
+  }
+  for (; r < r1; r += blockDim.x) {
     const double* xr = X + r * k;
     if (kind == 0) {
 #pragma unroll
-      for (int c = 0; c < KMAX; ++c)
+      for (int c = 0; c < KA; ++c)
         if (c < k) acc[c] += xr[c] * xr[c];
     } else {
       const double* yr = Y + r * k;
 #pragma unroll
-      for (int c = 0; c < KMAX; ++c)
+      for (int c = 0; c < KA; ++c)
         if (c < k) acc[c] += xr[c] * yr[c];
     }
   }
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int c = 0; c < KMAX; ++c) {
+  for (int c = 0; c < KA; ++c) {
     if (c < k) {
       double v = warp_sum(acc[c]);
       if (lane == 0) sh[wid][c] = v;
@@ -263,8 +291,19 @@ int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
   BAMG_REQUIRE(ctx, k >= 1 && k <= KMAX, "k must lie in [1, 32]");
   double* partial = nullptr;
   BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * k, &partial));
-  BAMG_LAUNCH(ctx, colreduce_kernel, red_blocks_for(n), RED_THREADS, 0, X, Y, n, k, kind, partial,
-              ctx->counters + 0, out_dev, take_sqrt);
+  const int g = red_blocks_for(n);
+  if (k == 8)
+    BAMG_LAUNCH(ctx, (colreduce_kernel<8, 4>), g, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else if (k == 16)
+    BAMG_LAUNCH(ctx, (colreduce_kernel<16, 2>), g, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else if (k == 1)
+    BAMG_LAUNCH(ctx, (colreduce_kernel<1, 8>), g, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else
+    BAMG_LAUNCH(ctx, (colreduce_kernel<0, 1>), g, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
   return 0;
 }
 
@@ -281,25 +320,81 @@ extern "C" int bamg_col_dots(bamg_ctx* ctx, const double* X, const double* Y, in
 
 // n x k block kernels: one thread per row walking its k entries (no 64-bit
 // div/mod per element; a row is one contiguous 8k-byte segment)
-__global__ void col_scale_div_kernel(double* X, int64_t n, int k, const double* s) {
+// x / d through the CTA's reciprocals of the k divisors (div_rn_recip:
+// bit-identical to the IEEE quotient; a full fp64 division per element held
+// this streaming kernel near 45 % of HBM bandwidth).  KK > 0: the row's k
+// values are loaded before any is stored (X is read and written in place, so
+// a rolled loop would serialise load -> divide -> store per element).
+template <int KK>
+__global__ void col_scale_div_kernel(double* X, int64_t n, int k_rt, const double* s, int fill_c, double fill_v) {
   BAMG_PDL_PROLOGUE();
+  const int k = KK > 0 ? KK : k_rt;
+  __shared__ double sd[KMAX], srd[KMAX];
+  if (threadIdx.x < k) {
+    double d = s[threadIdx.x];
+    if (d == 0.0) d = 1.0;
+    sd[threadIdx.x] = d;
+    srd[threadIdx.x] = 1.0 / d;
+  }
+  __syncthreads();
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   double* x = X + r * k;
-  for (int c = 0; c < k; ++c) {
-    double d = s[c];
-    if (d == 0.0) d = 1.0;
-    x[c] = x[c] / d;
+  if constexpr (KK > 0) {
+    double v[KK];
+#pragma unroll
+    for (int c = 0; c < KK; ++c) v[c] = x[c];
+#pragma unroll
+    for (int c = 0; c < KK; ++c) x[c] = c == fill_c ? fill_v : div_rn_recip(v[c], sd[c], srd[c]);
+  } else {
+    for (int c = 0; c < k; ++c) x[c] = c == fill_c ? fill_v : div_rn_recip(x[c], sd[c], srd[c]);
   }
 }
 
-int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
-  BAMG_LAUNCH(ctx, col_scale_div_kernel, grid_for(n, 256), 256, 0, X, n, k, s);
+// Flat form for k in {8, 16}: one double2 per thread, consecutive threads on
+// consecutive 16-byte words (the row-per-thread form's loads and stores were
+// 8 bytes at a 64-byte stride per lane).
+template <int KK>
+__global__ void col_scale_div_flat_kernel(double* X, int64_t total2, const double* s, int fill_c, double fill_v) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(KK % 2 == 0 && (KK & (KK - 1)) == 0, "power-of-two k");
+  __shared__ double sd[KK], srd[KK];
+  if (threadIdx.x < KK) {
+    double d = s[threadIdx.x];
+    if (d == 0.0) d = 1.0;
+    sd[threadIdx.x] = d;
+    srd[threadIdx.x] = 1.0 / d;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total2) return;
+  double2* x2 = reinterpret_cast<double2*>(X);
+  double2 v = x2[i];
+  const int c = (int)((2 * i) & (KK - 1));
+  v.x = c == fill_c ? fill_v : div_rn_recip(v.x, sd[c], srd[c]);
+  v.y = c + 1 == fill_c ? fill_v : div_rn_recip(v.y, sd[c + 1], srd[c + 1]);
+  x2[i] = v;
+}
+
+// X[:, c] /= s[c]; fill_c >= 0: column fill_c is set to fill_v instead (the
+// refresh's normalise-then-overwrite of the first test vector in one pass)
+int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s, int fill_c, double fill_v) {
+  const bool al16 = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  if (k == 8 && al16)
+    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<8>, grid_for(n * 4, 256), 256, 0, X, n * 4, s, fill_c, fill_v);
+  else if (k == 16 && al16)
+    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<16>, grid_for(n * 8, 256), 256, 0, X, n * 8, s, fill_c, fill_v);
+  else if (k == 8)
+    BAMG_LAUNCH(ctx, col_scale_div_kernel<8>, grid_for(n, 256), 256, 0, X, n, k, s, fill_c, fill_v);
+  else if (k == 16)
+    BAMG_LAUNCH(ctx, col_scale_div_kernel<16>, grid_for(n, 256), 256, 0, X, n, k, s, fill_c, fill_v);
+  else
+    BAMG_LAUNCH(ctx, col_scale_div_kernel<0>, grid_for(n, 256), 256, 0, X, n, k, s, fill_c, fill_v);
   return 0;
 }
 
 extern "C" int bamg_col_scale_div(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
-  return col_scale_div_dev(ctx, X, n, k, s);
+  return col_scale_div_dev(ctx, X, n, k, s, -1, 0.0);
 }
 
 __global__ void col_fill_kernel(double* X, int64_t n, int k, int c, double value) {
@@ -327,9 +422,28 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, const int32_t* 
   for (int c = 0; c < k; ++c) y[c] = x[c];
 }
 
+// k in {8, 16}: one double2 per thread (coalesced stores, 16-byte loads)
+template <int KK>
+__global__ void gather_rows_flat_kernel(const double* __restrict__ X, const int32_t* __restrict__ idx,
+                                        int64_t total2, double* __restrict__ Y) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total2) return;
+  constexpr int H = KK / 2;
+  const int64_t r = i / H;
+  const int c2 = (int)(i & (H - 1));
+  reinterpret_cast<double2*>(Y)[i] = reinterpret_cast<const double2*>(X + (int64_t)idx[r] * KK)[c2];
+}
+
 extern "C" int bamg_gather_rows(bamg_ctx* ctx, const double* X, const int32_t* idx, int64_t m,
                                 int k, double* Y) {
-  BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m, 256), 256, 0, X, idx, m, k, Y);
+  const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0;
+  if (al16 && k == 8)
+    BAMG_LAUNCH(ctx, gather_rows_flat_kernel<8>, grid_for(m * 4, 256), 256, 0, X, idx, m * 4, Y);
+  else if (al16 && k == 16)
+    BAMG_LAUNCH(ctx, gather_rows_flat_kernel<16>, grid_for(m * 8, 256), 256, 0, X, idx, m * 8, Y);
+  else
+    BAMG_LAUNCH(ctx, gather_rows_kernel, grid_for(m, 256), 256, 0, X, idx, m, k, Y);
   return 0;
 }
 
@@ -349,12 +463,35 @@ __global__ void permute_cols_kernel(const double* __restrict__ X, int64_t n, int
   for (int c = 0; c < k; ++c) y[c] = x[sp[c]];
 }
 
+// k in {8, 16}: one output double2 per thread (coalesced stores; the two
+// sources lie in the same 8k-byte row)
+template <int KK>
+__global__ void permute_cols_flat_kernel(const double* __restrict__ X, int64_t total2, Perm32 perm,
+                                         double* __restrict__ Y) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ int sp[32];
+  if (threadIdx.x < 32) sp[threadIdx.x] = perm.p[threadIdx.x];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total2) return;
+  const int64_t e = 2 * i;
+  const int c = (int)(e & (KK - 1));
+  const double* x = X + (e - c);
+  reinterpret_cast<double2*>(Y)[i] = make_double2(x[sp[c]], x[sp[c + 1]]);
+}
+
 extern "C" int bamg_permute_cols(bamg_ctx* ctx, const double* X, int64_t n, int k, const int32_t* perm_host,
                                  double* Y) {
   BAMG_REQUIRE(ctx, k >= 1 && k <= 32 && X != Y, "k in [1, 32] and distinct buffers");
   Perm32 p{};
   for (int c = 0; c < k; ++c) p.p[c] = perm_host[c];
-  BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n, 256), 256, 0, X, n, k, p, Y);
+  const bool al16 = (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  if (al16 && k == 8)
+    BAMG_LAUNCH(ctx, permute_cols_flat_kernel<8>, grid_for(n * 4, 256), 256, 0, X, n * 4, p, Y);
+  else if (al16 && k == 16)
+    BAMG_LAUNCH(ctx, permute_cols_flat_kernel<16>, grid_for(n * 8, 256), 256, 0, X, n * 8, p, Y);
+  else
+    BAMG_LAUNCH(ctx, permute_cols_kernel, grid_for(n, 256), 256, 0, X, n, k, p, Y);
   return 0;
 }
 

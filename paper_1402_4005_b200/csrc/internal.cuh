@@ -25,7 +25,8 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
                  const double* U, const double* V, int64_t n, int k, double* sigma,
                  double* U_flip_or_null, int mode, double* work3);
 int normalize_cols_dev(bamg_ctx* ctx, double* X, int64_t n, int k);
-int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s);
+int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s, int fill_c = -1,
+                      double fill_v = 0.0);
 int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);
 
 struct bamg_coarse_lu;

@@ -43,13 +43,56 @@ __global__ void rescale_kernel(double* __restrict__ X0, double* __restrict__ X1,
 }
 
 // u_c <- -u_c for flagged columns
+// k in {8, 16}: flat double2 form (consecutive threads on consecutive 16-byte
+// words), a word written only when one of its columns flips
+template <int KK>
+__global__ void flip_flat_kernel(double* __restrict__ X, int64_t total2, const double* __restrict__ flip) {
+  BAMG_PDL_PROLOGUE();
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < KK; ++c) any |= flip[c] != 0.0;
+  if (!any) return;
+  double2* x2 = reinterpret_cast<double2*>(X);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total2; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)((2 * i) & (KK - 1));
+    const bool f0 = flip[c] != 0.0, f1 = flip[c + 1] != 0.0;
+    if (f0 || f1) {
+      double2 v = x2[i];
+      if (f0) v.x = -v.x;
+      if (f1) v.y = -v.y;
+      x2[i] = v;
+    }
+  }
+}
+
+__global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ flip);
+
+static int flip_dev(bamg_ctx* ctx, double* X, int64_t total, int k, const double* flip) {
+  const bool al16 = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  const int cap = ctx->num_sms * 8;
+  if (al16 && (k == 8 || k == 16)) {
+    const int g = std::min(grid_for(total / 2, 256), cap);
+    if (k == 8) BAMG_LAUNCH(ctx, flip_flat_kernel<8>, g, 256, 0, X, total / 2, flip);
+    else BAMG_LAUNCH(ctx, flip_flat_kernel<16>, g, 256, 0, X, total / 2, flip);
+    return 0;
+  }
+  BAMG_LAUNCH(ctx, flip_kernel, std::min(grid_for(total / k, 256), cap), 256, 0, X, total, k, flip);
+  return 0;
+}
+
+// grid-stride, thread per row; a CTA leaves at once when no column flips
+// (the common case: the launch is then a few microseconds, not a 1M-thread pass)
 __global__ void flip_kernel(double* __restrict__ X, int64_t total, int k, const double* __restrict__ flip) {
   BAMG_PDL_PROLOGUE();
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // thread per row
-  if (r >= total / k) return;
-  double* x = X + r * k;
-  for (int c = 0; c < k; ++c)
-    if (flip[c] != 0.0) x[c] = -x[c];
+  bool any = false;
+  for (int c = 0; c < k; ++c) any |= flip[c] != 0.0;
+  if (!any) return;
+  const int64_t rows = total / k;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    double* x = X + r * k;
+    for (int c = 0; c < k; ++c)
+      if (flip[c] != 0.0) x[c] = -x[c];
+  }
 }
 
 // three column-dot sums in one pass (a.b, c.d, e.f per column), then -- in
@@ -149,7 +192,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
     if (rc == 0) {
       if (mode == 1 && U_flip_or_null) {
         int64_t total = n * k;
-        BAMG_LAUNCH(ctx, flip_kernel, grid_for(total / k, 256), 256, 0, U_flip_or_null, total, k, flip);
+        BAMG_TRY(flip_dev(ctx, U_flip_or_null, total, k, flip));
       }
       return 0;
     }
@@ -176,7 +219,7 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
               ctx->counters + 1, dots, sigma, flip, mode);
   if (mode == 1 && U_flip_or_null) {
     int64_t total = n * k;
-    BAMG_LAUNCH(ctx, flip_kernel, grid_for(total / k, 256), 256, 0, U_flip_or_null, total, k, flip);
+    BAMG_TRY(flip_dev(ctx, U_flip_or_null, total, k, flip));
   }
   return 0;
 }
@@ -261,9 +304,14 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
     if (v != V) BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(V, v, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (refresh) {
-    BAMG_TRY(normalize_cols_dev(ctx, U, n, k));
-    BAMG_TRY(normalize_cols_dev(ctx, V, n, k));
-    BAMG_TRY(col_fill_dev(ctx, U, n, k, 0, 1.0 / std::sqrt((double)n)));
+    // normalise U and V, then U[:, 0] = 1/sqrt(n): the fill rides on U's division pass
+    double *nu, *nv;
+    BAMG_TRY(arena_get(ctx, (size_t)k, &nu));
+    BAMG_TRY(arena_get(ctx, (size_t)k, &nv));
+    BAMG_TRY(colreduce(ctx, U, nullptr, n, k, 0, nu, 1));
+    BAMG_TRY(colreduce(ctx, V, nullptr, n, k, 0, nv, 1));
+    BAMG_TRY(col_scale_div_dev(ctx, U, n, k, nu, 0, 1.0 / std::sqrt((double)n)));
+    BAMG_TRY(col_scale_div_dev(ctx, V, n, k, nv));
     BAMG_TRY(rayleigh_dev(ctx, A, M, N, U, V, n, k, sigma, U, 1, nullptr));
   }
   return 0;

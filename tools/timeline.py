@@ -30,6 +30,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg1")
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--top", type=int, default=30)
+ap.add_argument("--dump", default=None, help="write the ordered launch list (name, start us, duration us) here")
 a = ap.parse_args()
 
 name = a.config
@@ -93,6 +94,12 @@ L.bamg_trace_enable(c, 0)
 rows = [r.split("\t") for r in buf.value.decode().splitlines()]
 ev = [(r[0], float(r[1]), float(r[2])) for r in rows]
 evpos = [int(r[3]) for r in rows]  # trace event index of each entry
+
+
+if a.dump:
+    with open(a.dump, "w") as f:
+        for n_, s_, e_ in ev:
+            f.write(f"{s_:10.1f}\t{e_ - s_:8.1f}\t{n_}\n")
 
 
 def marker(name):
