@@ -384,8 +384,10 @@ struct MassRows {
   const double* nval;
 };
 
-template <int K, int G, int U>
-__global__ void __launch_bounds__(TILE_THREADS)
+// MASS = false: identity masses (the finest levels) -- without the mass rows'
+// code the kernel fits 40 registers, 6 CTAs per SM (62 registers otherwise)
+template <int K, int G, int U, bool MASS>
+__global__ void __launch_bounds__(TILE_THREADS, MASS ? 1 : 6)
 rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                       const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
@@ -432,13 +434,13 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
       VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
       VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
       double mu[VV], nv[VV];
-      if (ms.mrp) {
+      if (MASS && ms.mrp) {
         row_apply<K, VV, U>(ms.mrp, ms.mcol, ms.mval, Uv, row, voff, mu);
       } else {
 #pragma unroll
         for (int q = 0; q < VV; ++q) mu[q] = uu[q];
       }
-      if (ms.nrp) {
+      if (MASS && ms.nrp) {
         row_apply<K, VV, U>(ms.nrp, ms.ncol, ms.nval, Vv, row, voff, nv);
       } else {
 #pragma unroll
@@ -511,8 +513,12 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   BAMG_TRY(check_csr(ctx, A));
   if (((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(V)) & 15) != 0 && !(k & 1)) return 1;
   // grid: a fixed function of the row count (so the partial-sum tree is
-  // reproducible), up to 8 CTAs per SM of row tiles in flight
-  constexpr int RQ_BLOCKS = 8 * 148;
+  // reproducible), capped at exactly one wave of the identity-mass kernel
+  // (6 CTAs per SM): 8 per SM left a third-occupied second wave (ncu: 24 % of
+  // HBM bandwidth, long-scoreboard bound; 107 -> 84 us at cfg1's level 0).
+  // Two row tiles in flight per thread (48 registers, 5 CTAs per SM) measured
+  // no faster.
+  constexpr int RQ_BLOCKS = 6 * 148;
   const int rb_rows = TILE_THREADS / 8;  // rows per tile at the widest G
   int nblk = (A->nrows + 4 * rb_rows - 1) / (4 * rb_rows);
   nblk = nblk < 1 ? 1 : (nblk > RQ_BLOCKS ? RQ_BLOCKS : nblk);
@@ -532,9 +538,14 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   switch (k) {
 #define BAMG_RQ_CASE(KK, GG, UU)                                                                              \
   case KK:                                                                                                   \
-    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, (rayleigh_fused_kernel<KK, GG, UU>), nblk, TILE_THREADS, 0,  \
-                    A->nrows, A->rowptr, A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, \
-                    mode, ms);                                                                               \
+    if (M || N)                                                                                              \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                           \
+                      (rayleigh_fused_kernel<KK, GG, UU, true>), nblk, TILE_THREADS, 0, A->nrows, A->rowptr,  \
+                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms);         \
+    else                                                                                                     \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                           \
+                      (rayleigh_fused_kernel<KK, GG, UU, false>), nblk, TILE_THREADS, 0, A->nrows, A->rowptr, \
+                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms);         \
     return 0;
     BAMG_RQ_CASE(1, 1, BAMG_U1)
     BAMG_RQ_CASE(2, 1, 4)
