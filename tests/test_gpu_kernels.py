@@ -218,12 +218,15 @@ def test_dense_pinv_bordered_lu_matches_svd(eng, golden, name, monkeypatch):
 
 
 @pytest.mark.parametrize("pool", [None, "64"])
-@pytest.mark.parametrize("shape", [(300, 400, 500, 0.05, 0.03), (500, 500, 500, 0.004, 0.004)])
+@pytest.mark.parametrize("shape", [(300, 400, 500, 0.05, 0.03), (500, 500, 500, 0.004, 0.004),
+                                   (400, 400, 600, 0.015, 0.013)])
 def test_spgemm_matches_scipy_storage_order_and_canonical(eng, shape, pool, monkeypatch):
     """C = A B with scipy csr_matmat semantics: order 1 reproduces scipy's raw
     product arrays (reverse-first-touch rows) bit for bit, order 0 the
     canonical make_csr form.  The first shape has rows with > 64 distinct
-    columns (global-scratch slow path), the second only fast-path rows.
+    columns (global-scratch slow path), the second only shared-memory-tier
+    rows (<= 32), the third all three tiers in one product (98 rows <= 32,
+    237 with 33-64 through the local-memory tier, 65 > 64).
     pool = 64 starts the slow-path scratch pool at 64 entries, so the count
     overflows it, grows it and recounts."""
     from scipy import sparse as sp
@@ -316,3 +319,30 @@ def test_device_lattice_chain_matches_host(eng, family, side):
     assert np.array_equal(D.indptr, H.indptr) and np.array_equal(D.indices, H.indices)
     assert np.array_equal(D.data, H.data)
     assert np.array_equal(dev.geometry.cpu().numpy().T, host.geometry)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 3, 8, 16])
+def test_block_kernels_match_numpy(eng, k):
+    """n x k block kernels (flat double2 forms for k = 8, 16; row forms
+    otherwise): column division is the IEEE quotient bit for bit (exact
+    reciprocal path), row gathers and column permutations are copies, column
+    norms agree with numpy to rounding (fixed-tree sums, not numpy's pairwise
+    order)."""
+    import torch
+    from paper_1402_4005_b200 import engine
+    rng = np.random.default_rng(11 + k)
+    n = 40_003
+    X = rng.standard_normal((n, k)) * np.exp(rng.uniform(-30, 30, (1, k)))
+    dX = torch.from_numpy(X.copy()).cuda()
+    nrm = engine.col_norms(dX).cpu().numpy()
+    ref = np.sqrt((X * X).sum(axis=0))
+    assert np.allclose(nrm, ref, rtol=1e-13, atol=0)
+    engine.normalize_cols(dX)
+    assert np.array_equal(dX.cpu().numpy(), X / nrm[None, :])
+    idx = rng.integers(0, n, 9_001).astype(np.int32)
+    G = engine.gather_rows(torch.from_numpy(X).cuda(), torch.from_numpy(idx).cuda()).cpu().numpy()
+    assert np.array_equal(G, X[idx])
+    perm = rng.permutation(k).astype(np.int32)
+    Pm = engine.permute_cols(torch.from_numpy(X).cuda(), perm).cpu().numpy()
+    assert np.array_equal(Pm, X[:, perm])
