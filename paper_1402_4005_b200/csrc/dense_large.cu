@@ -357,10 +357,13 @@ static bool trsm_recursive_enabled() {
 // triangle; `trans` solves with T^T (a lower T^T is upper).
 static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, bool unit, bool trans, double* B,
                      int ldb, int m, double* work /* NB*NB + NB*m */) {
-  // one launch wins when there are enough right-hand sides to fill the GPU
-  // and the 32-row sweep is short (measured: n = 256, m = 256; the blocked
-  // GEMM path wins at n = 1024 or for a handful of columns)
-  if (n <= 512 && m >= 32 && trsm_small_enabled()) {
+  // one launch: with reciprocal pivots its 32-row diagonal chain is short
+  // enough that it beats the blocked path's tri_inv + GEMM launches per
+  // 64-row block up to n = 512, also for a handful of right-hand sides
+  // (measured: cfg1 24.9 -> 24.2 ms; at n = 1024 the blocked path still wins,
+  // cfg2 61.9 vs 65.7 ms).  BAMG_TRSM_SMALL_N overrides the limit (development).
+  static const int small_n = getenv("BAMG_TRSM_SMALL_N") ? atoi(getenv("BAMG_TRSM_SMALL_N")) : 512;
+  if (n <= small_n && trsm_small_enabled()) {
     static bool attr = false;
     if (!attr) {
       BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(trsm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
