@@ -126,9 +126,13 @@ static int transpose_sq(bamg_ctx* ctx, const double* A, int n, double* T) {
 // row, and 44.8 us for 256 threads with the 64 steps unrolled (straight-line
 // code run once is instruction-fetch bound) -- keep the loop rolled.
 template <int NBT>
-__global__ void __launch_bounds__(16 * NBT) tri_inv_kernel(const double* __restrict__ T, int ld, int nb, int kind,
-                                                           double* __restrict__ Ti) {
+__global__ void __launch_bounds__(16 * NBT) tri_inv_kernel(const double* __restrict__ T0, const double* __restrict__ T1,
+                                                           int ld, int nb, int kind, double* __restrict__ Ti0,
+                                                           double* __restrict__ Ti1) {
   BAMG_PDL_PROLOGUE();
+  // CTA b inverts block b of a pair (two independent factorisations share the launch)
+  const double* __restrict__ T = blockIdx.x ? T1 : T0;
+  double* __restrict__ Ti = blockIdx.x ? Ti1 : Ti0;
   static_assert(NBT % 16 == 0, "16 column groups");
   constexpr int NQ = NBT / 16;
   __shared__ double sT[NBT * NBT];
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(16 * NBT) tri_inv_kernel(const double* __restr
 }
 
 static int tri_inv(bamg_ctx* ctx, const double* T, int ld, int nb, int kind, double* Ti) {
-  BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 1, 16 * NB, 0, T, ld, nb, kind, Ti);
+  BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 1, 16 * NB, 0, T, T, ld, nb, kind, Ti, Ti);
   return 0;
 }
 
@@ -391,8 +395,9 @@ static int tri_solve(bamg_ctx* ctx, const double* T, int n, bool lower_stored, b
 // against 74 us for the shared-memory form with three barriers and a jb^2
 // trailing sweep per column, 73 us for one warp left-looking, and 29 us for
 // 256 threads with the steps unrolled.
-__global__ void __launch_bounds__(1024) chol_block_kernel(double* A, int ld, int jb, int* bad) {
+__global__ void __launch_bounds__(1024) chol_block_kernel(double* A0, double* A1, int ld, int jb, int* bad) {
   BAMG_PDL_PROLOGUE();
+  double* A = blockIdx.x ? A1 : A0;  // CTA b factors block b of a pair
   __shared__ double colb[2][64];
   const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
   double a[4];
@@ -444,7 +449,7 @@ static int chol_blk(bamg_ctx* ctx, double* A, int lt, int n, int* bad, double* w
   for (int j0 = 0; j0 < n; j0 += NB) {
     int jb = (j0 + NB <= n) ? NB : n - j0;
     double* Ajj = A + (int64_t)j0 * lt + j0;
-    BAMG_LAUNCH(ctx, chol_block_kernel, 1, 1024, 0, Ajj, lt, jb, bad);
+    BAMG_LAUNCH(ctx, chol_block_kernel, 1, 1024, 0, Ajj, Ajj, lt, jb, bad);
     int r0 = j0 + jb, rn = n - r0;
     if (rn <= 0) break;
     BAMG_TRY(tri_inv(ctx, Ajj, lt, jb, 1, Li));
@@ -454,6 +459,38 @@ static int chol_blk(bamg_ctx* ctx, double* A, int lt, int n, int* bad, double* w
     BAMG_TRY(copy_block(ctx, tmp, rn, A21, lt, rn, jb));
     // A22 -= L21 L21^T
     BAMG_TRY(gemm(ctx, false, true, rn, rn, jb, -1.0, A21, lt, A21, lt, 1.0, A + (int64_t)r0 * lt + r0, lt));
+  }
+  return 0;
+}
+
+// Two independent blocked Cholesky factorisations (the coarsest masses M and
+// N) in lockstep: each panel's diagonal-block factorisation and inverse is
+// one two-CTA launch for both, so the latency-bound small kernels are paid
+// once per panel instead of twice.
+static int chol_blk_pair(bamg_ctx* ctx, double* A0, double* A1, int lt, int n, int* bad, double* work0,
+                         double* work1) {
+  double* Li0 = work0;
+  double* Li1 = work1;
+  double* tmp0 = work0 + NB * NB;
+  double* tmp1 = work1 + NB * NB;
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    const int jb = (j0 + NB <= n) ? NB : n - j0;
+    double* B0 = A0 + (int64_t)j0 * lt + j0;
+    double* B1 = A1 + (int64_t)j0 * lt + j0;
+    BAMG_LAUNCH(ctx, chol_block_kernel, 2, 1024, 0, B0, B1, lt, jb, bad);
+    const int r0 = j0 + jb, rn = n - r0;
+    if (rn <= 0) break;
+    BAMG_LAUNCH(ctx, tri_inv_kernel<NB>, 2, 16 * NB, 0, (const double*)B0, (const double*)B1, lt, jb, 1, Li0, Li1);
+    double* A21[2] = {A0 + (int64_t)j0 * lt + r0, A1 + (int64_t)j0 * lt + r0};
+    double* Li[2] = {Li0, Li1};
+    double* tmp[2] = {tmp0, tmp1};
+    double* base[2] = {A0, A1};
+    for (int m = 0; m < 2; ++m) {
+      BAMG_TRY(gemm(ctx, false, true, rn, jb, jb, 1.0, A21[m], lt, Li[m], jb, 0.0, tmp[m], rn));
+      BAMG_TRY(copy_block(ctx, tmp[m], rn, A21[m], lt, rn, jb));
+      BAMG_TRY(gemm(ctx, false, true, rn, rn, jb, -1.0, A21[m], lt, A21[m], lt, 1.0, base[m] + (int64_t)r0 * lt + r0,
+                    lt));
+    }
   }
   return 0;
 }
@@ -2183,8 +2220,16 @@ int large_coarsest_triplets(bamg_ctx* ctx, const double* Bd, double* Md, double*
     t_last = t;
   };
   stage("@start");
-  BAMG_TRY(cholesky_blocked(ctx, Md, n, bad, work));
-  BAMG_TRY(cholesky_blocked(ctx, Nd, n, bad, work));
+  if (n <= trsm_leaf()) {  // both factorisations in lockstep (shared small launches)
+    double* work_n;
+    BAMG_TRY(arena_get(ctx, (size_t)NB * NB + (size_t)NB * (n + 1) + 64, &work_n));
+    BAMG_TRY(chol_blk_pair(ctx, Md, Nd, n, n, bad, work, work_n));
+    BAMG_LAUNCH(ctx, zero_upper_kernel, grid_for((int64_t)n * n, 256), 256, 0, Md, n);
+    BAMG_LAUNCH(ctx, zero_upper_kernel, grid_for((int64_t)n * n, 256), 256, 0, Nd, n);
+  } else {
+    BAMG_TRY(cholesky_blocked(ctx, Md, n, bad, work));
+    BAMG_TRY(cholesky_blocked(ctx, Nd, n, bad, work));
+  }
   int hb = 0;
   BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb));
   if (hb) {
