@@ -172,38 +172,69 @@ spgemm_smem_count_kernel(int n, const int32_t* __restrict__ arp, const int32_t* 
   bool overflow = false;
   const bool rev_a = (order & SPG_REV_A) != 0, rev_b = (order & SPG_REV_B) != 0;
   const int a0 = arp[i], a1 = arp[i + 1];
-  for (int ja = 0; ja < a1 - a0 && !overflow; ++ja) {
-    const int jj = rev_a ? a1 - 1 - ja : a0 + ja;
-    const int j = acol[jj];
-    const double v = aval[jj];
-    const int b0 = brp[j], b1 = brp[j + 1];
-    for (int kb = 0; kb < b1 - b0; ++kb) {
-      const int kk = rev_b ? b1 - 1 - kb : b0 + kb;
-      const int c = bcol[kk];
-      const double pr = __dmul_rn(v, bval[kk]);
-      unsigned h = ((unsigned)c * 2654435761u) >> 26;  // 6 bits
-      while (true) {
-        unsigned int* wp = sslot + (h >> 2) * SPG_ST;
-        const unsigned int sh = (h & 3) * 8;
-        const unsigned int sl = (*wp >> sh) & 0xffu;
-        if (sl == 0xffu) {
-          if (len >= SCAP) {
-            overflow = true;
-            break;
-          }
-          *wp = (*wp & ~(0xffu << sh)) | ((unsigned int)len << sh);
-          skey[len * SPG_ST] = c;
-          sval[len * SPG_ST] = __dadd_rn(0.0, pr);
-          ++len;
-          break;
+  // the insert of one product into the row's list (first-touch order)
+  auto insert = [&](int c, double pr) {
+    unsigned h = ((unsigned)c * 2654435761u) >> 26;  // 6 bits
+    while (true) {
+      unsigned int* wp = sslot + (h >> 2) * SPG_ST;
+      const unsigned int sh = (h & 3) * 8;
+      const unsigned int sl = (*wp >> sh) & 0xffu;
+      if (sl == 0xffu) {
+        if (len >= SCAP) {
+          overflow = true;
+          return;
         }
-        if (skey[sl * SPG_ST] == c) {
-          sval[sl * SPG_ST] = __dadd_rn(sval[sl * SPG_ST], pr);
-          break;
-        }
-        h = (h + 1) & (SHS - 1);
+        *wp = (*wp & ~(0xffu << sh)) | ((unsigned int)len << sh);
+        skey[len * SPG_ST] = c;
+        sval[len * SPG_ST] = __dadd_rn(0.0, pr);
+        ++len;
+        return;
       }
-      if (overflow) break;
+      if (skey[sl * SPG_ST] == c) {
+        sval[sl * SPG_ST] = __dadd_rn(sval[sl * SPG_ST], pr);
+        return;
+      }
+      h = (h + 1) & (SHS - 1);
+    }
+  };
+  // loads batched ahead of the (serial) inserts: four A entries' columns,
+  // values and B row bounds, then each B row four entries at a time -- the
+  // products are still inserted one by one in scipy's order
+  constexpr int CA = 4, CB = 4;
+  const int na = a1 - a0;
+  for (int ja0 = 0; ja0 < na && !overflow; ja0 += CA) {
+    int jb0[CA], jb1[CA];
+    double av[CA];
+#pragma unroll
+    for (int u = 0; u < CA; ++u) {
+      const int ja = ja0 + u < na ? ja0 + u : na - 1;
+      const int jj = rev_a ? a1 - 1 - ja : a0 + ja;
+      const int j = acol[jj];
+      av[u] = aval[jj];
+      jb0[u] = brp[j];
+      jb1[u] = brp[j + 1];
+    }
+#pragma unroll
+    for (int u = 0; u < CA; ++u) {
+      if (ja0 + u >= na || overflow) break;
+      const int b0 = jb0[u], b1 = jb1[u], nb = b1 - b0;
+      const double v = av[u];
+      for (int kb0 = 0; kb0 < nb && !overflow; kb0 += CB) {
+        int cc[CB];
+        double bv[CB];
+#pragma unroll
+        for (int w = 0; w < CB; ++w) {
+          const int kb = kb0 + w < nb ? kb0 + w : nb - 1;
+          const int kk = rev_b ? b1 - 1 - kb : b0 + kb;
+          cc[w] = bcol[kk];
+          bv[w] = bval[kk];
+        }
+#pragma unroll
+        for (int w = 0; w < CB; ++w) {
+          if (kb0 + w >= nb || overflow) break;
+          insert(cc[w], __dmul_rn(v, bv[w]));
+        }
+      }
     }
   }
   if (overflow) {
