@@ -280,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
         raw[fid] = (ms.value, cnt.value, by.value)
     # the CSR family = its launches on every level (engine families 0 + 6)
     fam_stats["csr_stream_spmv_spmm_jacobi"] = tuple(a + b for a, b in zip(raw[0], raw[6]))
-    fam_stats["ls_fit_warp_per_point"] = raw[1]
+    fam_stats["ls_fit"] = raw[1]
     fine = raw[6]
     L.bamg_prof_enable(c, 0)
     dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
@@ -359,6 +359,9 @@ def run_ours(args, rank, world, local_rank):
             "families": {f: {"ms_total": round(v[0], 3), "launches": v[1],
                              "alg_GBps": round((v[2] / max(v[1], 1)) / (v[0] / 1e3 / max(v[1], 1)) / 1e9, 1) if v[1] else 0}
                          for f, v in fam_stats.items()}}
+    fit = fp64_fit_roofline(L, c, fam_stats.get("ls_fit"), args.steps, name)
+    if fit:
+        roof["ls_fit_fp64"] = fit
     if dom == "csr_stream_spmv_spmm_jacobi" and fine[1]:
         # the same family restricted to the finest levels (operators >= 2^18 rows):
         # bandwidth-sized launches, without the latency-bound coarse-level ones
@@ -394,6 +397,31 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.destroy_process_group()
     return line
+
+
+def fp64_fit_roofline(L, c, fam, steps, name):
+    """The LS fit against the fp64 CUDA-core peak.
+
+    flops per step: ncu's thread-level DFMA/DADD/DMUL counts over every fit
+    launch of one cfg1 step (profiles/rNN_ls_fit_flops.json, tools/fit_flops.py;
+    the fit is deterministic, so the count is the same every step).  time: the
+    fit family's live CUDA-event total over the profiled window.  peak: the DFMA
+    throughput probe (bamg_fp64_peak) run here, on this GPU."""
+    files = sorted(ROOT.glob("profiles/r*_ls_fit_flops.json"))
+    if not fam or not fam[1] or name != "cfg1" or not files:
+        return None
+    import ctypes as C
+    pk = C.c_double()
+    if L.bamg_fp64_peak(c, 5, C.byref(pk)) != 0:
+        return None
+    d = json.load(open(files[-1]))
+    fl = d["fp64_flops_per_step"]
+    ach = fl * steps / (fam[0] / 1e3) / 1e12
+    return {"bound": "fp64 latency", "achieved": round(ach, 3), "peak": round(pk.value, 2), "unit": "TFLOP/s",
+            "frac": round(ach / pk.value, 4), "flops_per_step": fl, "ms_per_step": round(fam[0] / steps, 3),
+            "alg_GBps": round(fam[2] / (fam[0] / 1e3) / 1e9, 1),
+            "peak_kind": "measured live (bamg_fp64_peak: DFMA chains, full occupancy)",
+            "flops_source": f"{files[-1].name}: ncu thread-level fp64 instruction counts, one step"}
 
 
 def family_traffic(family, alg_per_launch):

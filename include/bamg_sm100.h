@@ -63,6 +63,10 @@ int bamg_sync(bamg_ctx* ctx);
 int bamg_prof_enable(bamg_ctx* ctx, unsigned family_mask);
 int bamg_prof_read(bamg_ctx* ctx, int family, double* ms_host, int64_t* launches_host,
                    double* bytes_host);
+/* Measured fp64 FMA throughput of this device in TFLOP/s (best of `reps`
+ * ~1 ms launches).  No reference counterpart: SURVEY.md §8(d) asks for the LS
+ * fit to be reported against a measured fp64 CUDA-core peak. */
+int bamg_fp64_peak(bamg_ctx* ctx, int reps, double* tflops_host);
 /* Development trace: event pair around every launch, aggregated by kernel
  * name into "name total_ms count" lines. */
 int bamg_trace_enable(bamg_ctx* ctx, int on);
