@@ -567,6 +567,9 @@ struct TModel {
 template <int KM>
 struct TPoint {
   static constexpr bool EXACT = KM <= 16;
+  // exact mode with whole 32-byte row segments: the columns are read four
+  // tests at a time with 256-bit loads (the launcher checks X's alignment)
+  static constexpr bool VEC = EXACT && KM % 4 == 0;
   const double* X;
   int k;
   int nf;                        // finite tests (generic mode)
@@ -599,6 +602,39 @@ __device__ __forceinline__ double ttarget(const TPoint<KM>& P, int t, int base) 
   return P.swv(t) * yv;
 }
 
+__device__ __forceinline__ void ldg_v4(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+// tests t0..t0+3 of every trial column and of the target, the same values
+// tcol / ttarget give one scalar load at a time (VEC mode): av[q][u] =
+// sw * (C[col_q] - C[base]), bv[u] = sw * (y - C[base]) at test t0 + u.
+// One 256-bit load per row and chunk instead of four (or eight, with the
+// base row re-read per column): the fit was bound by load-issue throttling.
+template <int KM, int NC>
+__device__ __forceinline__ void tchunk(const TPoint<KM>& P, const int* cols, int base, int t0, double (&av)[NC][4],
+                                       double (&bv)[4]) {
+  double xb[4] = {0.0, 0.0, 0.0, 0.0};
+  if (base >= 0) ldg_v4(P.X + (int64_t)base * KM + t0, xb);
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double xc[4];
+    ldg_v4(P.X + (int64_t)cols[q] * KM + t0, xc);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double c = xc[u];
+      if (base >= 0) c -= xb[u];
+      av[q][u] = P.swv(t0 + u) * c;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    double yv = P.yv(t0 + u);
+    if (base >= 0) yv -= xb[u];
+    bv[u] = P.swv(t0 + u) * yv;
+  }
+}
+
 // ridge LS on NC columns (point indices cols[]); returns false when the
 // Cholesky factor fails the rank test (caller defers the point).  NC is a
 // compile-time constant so no guarded (issued but idle) lanes of the 4x4
@@ -614,16 +650,33 @@ __device__ __forceinline__ bool tls_solve_n(const TPoint<KM>& P, const int* cols
 #pragma unroll
     for (int q = 0; q < NC; ++q) G[p][q] = 0.0;
   }
-  _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-    double a[NC];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
-    double b = ttarget(P, t, base);
+  auto gram_add = [&](const double* a, double b) {
 #pragma unroll
     for (int p = 0; p < NC; ++p) {
       h[p] += a[p] * b;
 #pragma unroll
       for (int q = 0; q <= p; ++q) G[p][q] += a[p] * a[q];
+    }
+  };
+  if constexpr (TPoint<KM>::VEC) {
+#pragma unroll
+    for (int t0 = 0; t0 < KM; t0 += 4) {
+      double av[NC][4], bv[4];
+      tchunk<KM, NC>(P, cols, base, t0, av, bv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double a[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) a[q] = av[q][u];
+        gram_add(a, bv[u]);
+      }
+    }
+  } else {
+    _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
+      double a[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
+      gram_add(a, ttarget(P, t, base));
     }
   }
   const double l2 = P.lam * P.lam;
@@ -695,16 +748,33 @@ __device__ __forceinline__ bool tls_solve_n(const TPoint<KM>& P, const int* cols
     double g[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) g[q] = q < nc ? -l2 * c[q] : 0.0;  // ridge rows: -lam * (lam c)
-    _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-      double a[NC];
-      double r = ttarget(P, t, base);
+    auto resid_add = [&](const double* a, double r) {
 #pragma unroll
-      for (int q = 0; q < NC; ++q) {
-        a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
-        r -= a[q] * c[q];
-      }
+      for (int q = 0; q < NC; ++q) r -= a[q] * c[q];
 #pragma unroll
       for (int q = 0; q < NC; ++q) g[q] += a[q] * r;
+    };
+    if constexpr (TPoint<KM>::VEC) {
+#pragma unroll
+      for (int t0 = 0; t0 < KM; t0 += 4) {
+        double av[NC][4], bv[4];
+        tchunk<KM, NC>(P, cols, base, t0, av, bv);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double a[NC];
+#pragma unroll
+          for (int q = 0; q < NC; ++q) a[q] = av[q][u];
+          resid_add(a, bv[u]);
+        }
+      }
+    } else {
+      _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
+        double a[NC];
+        double r = ttarget(P, t, base);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) a[q] = q < nc ? tcol(P, t, cols[q], base) : 0.0;
+        resid_add(a, r);
+      }
     }
     double dlt[NC];
     chol_solve(g, dlt);
@@ -713,13 +783,29 @@ __device__ __forceinline__ bool tls_solve_n(const TPoint<KM>& P, const int* cols
       if (q < nc) c[q] += dlt[q];
   }
   double mis = 0.0;
-  _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-    double r = 0.0;
+  if constexpr (TPoint<KM>::VEC) {
 #pragma unroll
-    for (int q = 0; q < NC; ++q)
-      if (q < nc) r += tcol(P, t, cols[q], base) * c[q];
-    r -= ttarget(P, t, base);
-    mis += r * r;
+    for (int t0 = 0; t0 < KM; t0 += 4) {
+      double av[NC][4], bv[4];
+      tchunk<KM, NC>(P, cols, base, t0, av, bv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double r = 0.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) r += av[q][u] * c[q];
+        r -= bv[u];
+        mis += r * r;
+      }
+    }
+  } else {
+    _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
+      double r = 0.0;
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        if (q < nc) r += tcol(P, t, cols[q], base) * c[q];
+      r -= ttarget(P, t, base);
+      mis += r * r;
+    }
   }
   double cc = 0.0;
 #pragma unroll
@@ -1202,8 +1288,10 @@ static int fit_rows_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* co
                 radius, mcnt, cbuf, hist, out_cnt, defer, ndefer);
     BAMG_LAUNCH(ctx, fit_bucket_scan_kernel, 1, 32, 0, hist, nsorted);
     BAMG_LAUNCH(ctx, fit_bucket_scatter_kernel, grid_for(n, 256), 256, 0, mcnt, nfl, hist, order);
+    // the VEC specialisations read X in 32-byte segments
+    const bool x_aligned = (reinterpret_cast<uintptr_t>(X) & 31) == 0;
 #define BAMG_FIT_EXACT(KK)                                                                                       \
-  if (k == KK) {                                                                                                   \
+  if (k == KK && (x_aligned || !TPoint<KK>::VEC)) {                                                                                                 \
     BAMG_LAUNCH_FAM(ctx, FAM_FIT, fbytes, fit_rows_thread_kernel<KK>, grid_for(n, TFIT_THREADS), TFIT_THREADS, 0,  \
                     order, nsorted, flist, mcnt, cbuf, coarse_rank, X, k, w, lam, caliber, improvement_tol,        \
                     constrain, nonnegative, out_cnt, out_col, out_val, defer, ndefer);                             \
