@@ -1345,17 +1345,38 @@ extern "C" int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* 
 __global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double* __restrict__ val, int64_t n,
                                   int stride, int32_t* __restrict__ out);
 
-// Per-context status words of asynchronous fits (bamg_fit_rows_csr_slot):
-// 4 slots x 4 words, read back together by bamg_fit_rows_wait.
+// Per-context state of asynchronous fits (bamg_fit_rows_csr_slot): status
+// words (4 slots x 4 words, read back together by bamg_fit_rows_wait) and one
+// side stream per slot > 0.  Slot 0 records a fork event before its launches;
+// slots 1..3 wait on it and run on their side streams, so the fits of a batch
+// (P and W of a level) overlap -- the coarse levels' fits are one serial
+// greedy chain per thread (35-60 us whatever the size), and run side by side
+// at the cost of one.  Each joins back into the main stream right after its
+// launches, so every later main-stream operation is ordered after it.
 constexpr int FIT_SLOTS = 4;
-static unsigned long long* fit_slot_status(bamg_ctx* ctx) {
-  static thread_local std::vector<std::pair<bamg_ctx*, unsigned long long*>> table;
+struct FitSlots {
+  unsigned long long* status = nullptr;
+  cudaStream_t side[FIT_SLOTS] = {};
+  cudaEvent_t fork = nullptr, join[FIT_SLOTS] = {};
+  bool forked = false;
+};
+static FitSlots* fit_slots(bamg_ctx* ctx) {
+  static thread_local std::vector<std::pair<bamg_ctx*, FitSlots*>> table;
   for (auto& e : table)
     if (e.first == ctx) return e.second;
-  unsigned long long* p = nullptr;
-  if (cudaMalloc(&p, sizeof(unsigned long long) * 4 * FIT_SLOTS) != cudaSuccess) return nullptr;
-  table.push_back({ctx, p});
-  return p;
+  FitSlots* fs = new FitSlots();
+  bool ok = cudaMalloc(&fs->status, sizeof(unsigned long long) * 4 * FIT_SLOTS) == cudaSuccess &&
+            cudaEventCreateWithFlags(&fs->fork, cudaEventDisableTiming) == cudaSuccess;
+  for (int s = 1; s < FIT_SLOTS && ok; ++s)
+    ok = cudaStreamCreateWithFlags(&fs->side[s], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fs->join[s], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) return nullptr;
+  table.push_back({ctx, fs});
+  return fs;
+}
+static unsigned long long* fit_slot_status(bamg_ctx* ctx) {
+  FitSlots* fs = fit_slots(ctx);
+  return fs ? fs->status : nullptr;
 }
 
 static int fit_rows_csr_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank, const double* X,
@@ -1379,18 +1400,43 @@ extern "C" int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const 
                                       int32_t* out_cnt, int32_t* out_col, double* out_val, int32_t* rowptr,
                                       int slot) {
   BAMG_REQUIRE(ctx, slot >= 0 && slot < FIT_SLOTS, "slot must lie in [0, 4)");
-  ctx->arena.reset();
-  unsigned long long* st = fit_slot_status(ctx);
-  BAMG_REQUIRE(ctx, st != nullptr, "status allocation failed");
-  return fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
-                             nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st + 4 * slot);
+  FitSlots* fs = fit_slots(ctx);
+  BAMG_REQUIRE(ctx, fs != nullptr, "fit slot state allocation failed");
+  unsigned long long* st = fs->status + 4 * slot;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  BAMG_CHECK_CUDA(ctx, cudaStreamIsCapturing(ctx->stream, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  const bool side = slot > 0 && fs->forked && !capturing;
+  if (!side) {
+    // slot 0 (or a batch without one): scratch from a fresh arena, main stream
+    ctx->arena.reset();
+    if (slot == 0 && !capturing) {
+      BAMG_CHECK_CUDA(ctx, cudaEventRecord(fs->fork, ctx->stream));
+      fs->forked = true;
+    }
+    return fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                               nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st);
+  }
+  // later slot of the batch: the arena is NOT reset (its scratch follows the
+  // earlier slots'), inputs are ordered by the fork event
+  cudaStream_t main = ctx->stream;
+  BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(fs->side[slot], fs->fork, 0));
+  ctx->stream = fs->side[slot];
+  int rc = fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
+                               nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st);
+  ctx->stream = main;
+  BAMG_CHECK_CUDA(ctx, cudaEventRecord(fs->join[slot], fs->side[slot]));
+  BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(main, fs->join[slot], 0));
+  return rc;
 }
 
 extern "C" int bamg_fit_rows_wait(bamg_ctx* ctx, int nslots, const int32_t* slots, int64_t* status_host,
                                   int64_t* nnz_host) {
   BAMG_REQUIRE(ctx, nslots >= 1 && nslots <= FIT_SLOTS, "1..4 slots");
-  unsigned long long* st = fit_slot_status(ctx);
-  BAMG_REQUIRE(ctx, st != nullptr, "status allocation failed");
+  FitSlots* fs = fit_slots(ctx);
+  BAMG_REQUIRE(ctx, fs != nullptr, "fit slot state allocation failed");
+  fs->forked = false;
+  unsigned long long* st = fs->status;
   int64_t h[4 * FIT_SLOTS];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(st), 4 * FIT_SLOTS, h));
   for (int i = 0; i < nslots; ++i) {
