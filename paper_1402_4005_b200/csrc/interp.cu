@@ -860,9 +860,22 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
         for (int q = 1; q < TCAL; ++q) coef[q] = (q < wl) ? ct[q - 1] : 0.0;
       } else {
         double mis = 0.0;
-        _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
-          double r = ttarget(P, t, base);
-          mis += r * r;
+        if constexpr (TPoint<KM>::VEC) {
+#pragma unroll
+          for (int t0 = 0; t0 < KM; t0 += 4) {
+            double xb[4];
+            ldg_v4(P.X + (int64_t)base * KM + t0, xb);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              double r = P.swv(t0 + u) * (P.yv(t0 + u) - xb[u]);
+              mis += r * r;
+            }
+          }
+        } else {
+          _Pragma("unroll") for (int t = 0; t < P.ntest(); ++t) {
+            double r = ttarget(P, t, base);
+            mis += r * r;
+          }
         }
         data = total = mis;
         coef[0] = 1.0;
