@@ -67,6 +67,12 @@ int bamg_prof_read(bamg_ctx* ctx, int family, double* ms_host, int64_t* launches
  * ~1 ms launches).  No reference counterpart: SURVEY.md §8(d) asks for the LS
  * fit to be reported against a measured fp64 CUDA-core peak. */
 int bamg_fp64_peak(bamg_ctx* ctx, int reps, double* tflops_host);
+/* C = alpha op(A) op(B) + beta C, column-major fp64, BLAS argument order
+ * (device pointers, stream-ordered).  The dense kernels behind the coarsest
+ * level (gemm.cu: DMMA m8n8k4 tiles, GEMV); replaces the LAPACK/BLAS the
+ * reference reaches through numpy (dense.py:53-131). */
+int bamg_dgemm(bamg_ctx* ctx, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
+               const double* B, int ldb, double beta, double* C, int ldc);
 /* Development trace: event pair around every launch, aggregated by kernel
  * name into "name total_ms count" lines. */
 int bamg_trace_enable(bamg_ctx* ctx, int on);

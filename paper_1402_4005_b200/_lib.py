@@ -50,6 +50,7 @@ _SIGS = {
     "bamg_prof_enable": [P, C.c_uint],
     "bamg_prof_read": [P, C.c_int, PF64, PI64, PF64],
     "bamg_fp64_peak": [P, C.c_int, PF64],
+    "bamg_dgemm": [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64, P, C.c_int, P, C.c_int, F64, P, C.c_int],
     "bamg_trace_enable": [P, C.c_int],
     "bamg_trace_dump": [P, C.c_char_p, I64],
     "bamg_trace_timeline": [P, C.c_char_p, I64],

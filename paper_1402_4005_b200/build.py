@@ -72,7 +72,7 @@ def build(verbose: bool = False, force: bool = False, variant: str = "", defines
         return lib
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
-        "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+        "-lcudart_static", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

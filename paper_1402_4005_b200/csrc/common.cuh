@@ -241,6 +241,11 @@ static inline int arena_get(bamg_ctx* ctx, size_t count, T** out) {
   return 0;
 }
 
+// Opt a kernel in to `bytes` of dynamic shared memory on the context's device.
+// The attribute is per (function, device): recorded in a process-wide table so
+// a second device in the same process gets its own cudaFuncSetAttribute.
+int smem_optin(bamg_ctx* ctx, const void* fn, size_t bytes);
+
 // Pinned staging for small device->host reads (synchronises the stream).
 int ctx_read_doubles(bamg_ctx* ctx, const double* dev, size_t n, double* host);
 int ctx_read_i64(bamg_ctx* ctx, const int64_t* dev, size_t n, int64_t* host);

@@ -1,5 +1,7 @@
 // ctx.cu -- context lifetime, pinned staging, device scans and deterministic
 // column reductions shared by every other translation unit.
+#include <mutex>
+
 #include "common.cuh"
 
 extern "C" int bamg_version(void) { return BAMG_VERSION; }
@@ -39,6 +41,27 @@ extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
   for (auto e : ctx->exec_pool) cudaGraphExecDestroy(e);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
+  return 0;
+}
+
+int smem_optin(bamg_ctx* ctx, const void* fn, size_t bytes) {
+  struct Rec {
+    const void* fn;
+    int device;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Rec> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& r : done)
+    if (r.fn == fn && r.device == ctx->device && r.bytes >= bytes) return 0;
+  BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  for (auto& r : done)
+    if (r.fn == fn && r.device == ctx->device) {
+      r.bytes = bytes;
+      return 0;
+    }
+  done.push_back({fn, ctx->device, bytes});
   return 0;
 }
 

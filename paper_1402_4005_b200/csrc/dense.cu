@@ -309,12 +309,7 @@ static int jacobi_svd(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
   int m = ncols + (ncols & 1);
   const size_t smem = sizeof(double) * ((size_t)nrows * ncols + (size_t)ncols * ncols);
   if (ncols >= 2 && smem <= (size_t)JAC_SMEM_MAX && !getenv("BAMG_JACOBI_COOP")) {
-    static bool attr = false;
-    if (!attr) {
-      BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(jacobi_svd_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                JAC_SMEM_MAX));
-      attr = true;
-    }
+    BAMG_TRY(smem_optin(ctx, (const void*)jacobi_svd_smem_kernel, JAC_SMEM_MAX));
     double tol = 1e-15;
     if (const char* e = getenv("BAMG_JACOBI_TOL")) tol = atof(e);
     BAMG_LAUNCH(ctx, jacobi_svd_smem_kernel, 1, 1024, smem, G, nrows, V, ncols, m, tol, MAXSW);

@@ -29,6 +29,10 @@ int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* 
                       double fill_v = 0.0);
 int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);
 
+// C = alpha op(A) op(B) + beta C, column-major fp64 (gemm.cu)
+int dgemm_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+              const double* B, int ldb, double beta, double* C, int ldc);
+
 struct bamg_coarse_lu;
 // x = B^+ b through the kept coarsest LU (dense_large.cu)
 int coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, double* x);

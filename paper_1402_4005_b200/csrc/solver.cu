@@ -444,11 +444,15 @@ __global__ void mreduce_kernel(const double* __restrict__ partial, int nb, int m
 //   h[j+1] = sqrt(nrm2); happy test; previous rotations; new rotation;
 //   R[:, j]; g; y = R^-1 g (back substitution).  state[0] = happy flag,
 //   state[1] = h[j+1].
+// flag / when: with a CGS fast-path flag (see cgs_pythag_kernel) the kernel
+// runs only when (flag[0] != 0) == when, so the unsafe step's explicit norm
+// reaches the rotation exactly once.
 __global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const double* __restrict__ nrm2,
                               double beta, double* __restrict__ R, double* __restrict__ g,
                               double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ y,
-                              double* __restrict__ state) {
+                              double* __restrict__ state, const double* __restrict__ flag, int when) {
   BAMG_PDL_PROLOGUE();
+  if (flag && ((flag[0] != 0.0) != (when != 0))) return;
   extern __shared__ double sg[];  // j+1 working entries of g during the back substitution
   if (threadIdx.x == 0) {
     double hj1 = sqrt(nrm2[0]);
@@ -528,6 +532,291 @@ __global__ void scale_div_kernel(int64_t n, const double* __restrict__ a, const 
   if (i < n) out[i] = a[i] / s[0];
 }
 
+// ---- register-resident CGS2 passes (basis of <= CGS_MAXM vectors)
+// One Arnoldi step in three passes over the basis instead of five:
+//   A: h  = V^T w                                   (dots)
+//   B: w' = w - V h ; h2 = V^T w' ; |w'|^2          (update + dots, one read of V)
+//   C: v_{j+1} = (w' - V h2) / h_{j+1} ; x = x0 + e + V y ; |x|^2
+// with h_{j+1}^2 = |w'|^2 - |h2|^2 (Pythagoras: w'' = w' - V h2 is w' minus
+// its projection on the orthonormal basis), so the Givens update and the
+// least-squares y of column j are known before pass C and the iterate x the
+// stopping test needs is formed in the same read of V.  Where the difference
+// loses more than two digits (|w''|^2 < 1e-2 |w'|^2: w' nearly inside span V)
+// the step falls back on device to the explicit norm (cgs_fix_*).  Each CTA
+// owns a fixed contiguous row chunk and reduces its partial sums in a fixed
+// order (deterministic).  Values V_g[i] of a row stay in registers between
+// the update and the dots of pass B.
+constexpr int CGS_MAXM = 64;
+constexpr int CGS_THREADS = 128;
+constexpr int CGS_WARPS = CGS_THREADS / 32;
+constexpr int CGS_MAX_BLOCKS = 32 * 148;  // partial-sum slots per CTA: CGS_MAXM + 1
+
+template <int MAXM>
+__device__ __forceinline__ void cgs_load_ptrs(const double* const* __restrict__ Vp, int m, const double** sp) {
+  // slots past m alias V_0 (their coefficients are zero): the loads stay
+  // unconditional, so all of a row's loads issue back to back
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) sp[g] = Vp[g < m ? g : 0];
+  __syncthreads();
+}
+
+// per-warp partial sums acc[warp][slot] -> part[block * stride + slot], fixed order
+__device__ __forceinline__ void cgs_flush(double (*acc)[CGS_MAXM + 2], int nslots, double* __restrict__ part,
+                                          int stride) {
+  __syncthreads();
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < CGS_WARPS; ++w) v += acc[w][q];
+    part[(int64_t)blockIdx.x * stride + q] = v;
+  }
+}
+
+// Transpose reduction of 32 per-lane values: afterwards lane l holds
+// sum over the warp's lanes of a[l] (in a[0]); 31 shuffles instead of the
+// 160 of 32 separate butterfly sums.
+__device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane) {
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = hi ? a[i] : a[i + half];
+      const double keep = hi ? a[i + half] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return a[0];
+}
+
+// MODE 0 (pass A): part[b][g] = chunk sum of V_g . w
+// MODE 1 (pass B): w <- w - sum_g c_g V_g (in place); part[b][g] = V_g . w_new,
+//                  part[b][m] = |w_new|^2
+// A warp takes 32 consecutive rows (one per lane) at a time; the row's MAXM
+// basis values stay in registers, the 32 x MAXM products are folded across
+// the warp by transpose reductions, and lane l accumulates the dots of
+// vectors l, l + 32 over all of the warp's rows.
+template <int MAXM, int MODE>
+__global__ void __launch_bounds__(CGS_THREADS)
+cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c, double* __restrict__ w,
+                int64_t n, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
+  constexpr int NB = MAXM / 32;
+  __shared__ const double* sp[MAXM];
+  __shared__ double sc[MAXM];
+  __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (MODE == 1)
+    for (int g = threadIdx.x; g < MAXM; g += blockDim.x) sc[g] = g < m ? c[g] : 0.0;
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double dot[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) dot[q] = 0.0;
+  double wn2 = 0.0;
+  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
+    const int64_t i = base + lane;
+    const bool ok = i < r1;
+    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
+    double v[MAXM];
+#pragma unroll
+    for (int g = 0; g < MAXM; ++g) v[g] = __ldcs(sp[g] + ic);
+    double wi = w[ic];
+    if (MODE == 1) {
+      double t = 0.0;
+#pragma unroll
+      for (int g = 0; g < MAXM; ++g) t = fma(sc[g], v[g], t);
+      wi -= t;
+      if (ok) w[i] = wi;
+    }
+    if (!ok) wi = 0.0;
+    if (MODE == 1) wn2 = fma(wi, wi, wn2);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      if (q * 32 >= m) break;
+      double pr[32];
+#pragma unroll
+      for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * wi;
+      dot[q] += warp_transpose_sum32(pr, lane);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
+  if (MODE == 1) {
+    wn2 = warp_sum(wn2);
+    if (lane == 0) acc[wid][MAXM] = wn2;
+  }
+  __syncthreads();
+  const int nslots = MODE == 1 ? m + 1 : m;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
+    const int slot = (MODE == 1 && q == m) ? MAXM : q;
+    double t = 0.0;
+    for (int ww = 0; ww < CGS_WARPS; ++ww) t += acc[ww][slot];
+    part[(int64_t)blockIdx.x * (m + 1) + q] = t;
+  }
+}
+
+// out[i] = sum_b part[b * stride + i], i < cnt (fixed order)
+__global__ void cgs_reduce_kernel(const double* __restrict__ part, int nb, int stride, int cnt,
+                                  double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= cnt) return;
+  double v = 0.0;
+  for (int b = lane; b < nb; b += 32) v += part[(int64_t)b * stride + i];
+  v = warp_sum(v);
+  if (lane == 0) out[i] = v;
+}
+
+// hv[0..m) += h2[0..m);  nrm2 = |w'|^2 - |h2|^2 (h2 = sums[0..m), |w'|^2 = sums[m]);
+// flag[0] = 1 when the difference lost more than two digits
+__global__ void cgs_pythag_kernel(int m, const double* __restrict__ sums, double* __restrict__ hv,
+                                  double* __restrict__ nrm2, double* __restrict__ flag) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double red[32];
+  double q = 0.0;
+  for (int g = threadIdx.x; g < m; g += blockDim.x) {
+    const double h2 = sums[g];
+    hv[g] += h2;
+    q += h2 * h2;
+  }
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    const double wn = sums[m];
+    const double d = wn - t;
+    const bool unsafe = !(d >= 1e-2 * wn);
+    nrm2[0] = unsafe ? 0.0 : d;
+    flag[0] = unsafe ? 1.0 : 0.0;
+  }
+}
+
+// pass C: v_new = (w' - V h2) / state[1] (skipped on happy breakdown) and
+// x = x0 + e + V y with part[b] = chunk |x|^2; when flag[0] is set (unsafe
+// Pythagoras) the unscaled w'' goes to v_new and part[b] = chunk |w''|^2
+// instead, and x is left to cgs_fix_x_kernel.
+template <int MAXM>
+__global__ void __launch_bounds__(CGS_THREADS, 4)
+cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ h2,
+                 const double* __restrict__ y, const double* __restrict__ wp, const double* __restrict__ x0,
+                 const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
+                 int64_t n, double* __restrict__ vnew, double* __restrict__ x, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ const double* sp[MAXM];
+  __shared__ double sh[MAXM], sy[MAXM];
+  __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
+    sh[g] = g < m ? h2[g] : 0.0;
+    sy[g] = g < m ? y[g] : 0.0;
+  }
+  if (threadIdx.x < CGS_WARPS) acc[threadIdx.x][0] = 0.0;
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const bool unsafe = flag[0] != 0.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += CGS_THREADS) {
+    double v[MAXM];  // every load of the row issued before the first FMA
+#pragma unroll
+    for (int g = 0; g < MAXM; ++g) v[g] = __ldcs(sp[g] + i);
+    const double wpi = wp[i], x0i = x0[i], ei = e[i];
+    double t = 0.0, u = 0.0;
+#pragma unroll
+    for (int g = 0; g < MAXM; ++g) {
+      t = fma(sh[g], v[g], t);
+      u = fma(sy[g], v[g], u);
+    }
+    const double ww = wpi - t;
+    if (unsafe) {
+      vnew[i] = ww;
+      nrm = fma(ww, ww, nrm);
+    } else {
+      if (!happy) vnew[i] = ww * inv;
+      const double xi = x0i + (ei + u);
+      x[i] = xi;
+      nrm = fma(xi, xi, nrm);
+    }
+  }
+  nrm = warp_sum(nrm);
+  if (lane == 0) acc[wid][0] = nrm;
+  cgs_flush(acc, 1, part, 1);
+}
+
+// unsafe step, part 1 (one CTA): |w''|^2 from pass C's partials -> the
+// normal Givens path (givens_kernel is launched after this by the host loop
+// with nrm2 = this value).  No-op when the Pythagorean norm was safe.
+__global__ void cgs_fix_norm_kernel(const double* __restrict__ flag, const double* __restrict__ part, int nb,
+                                    double* __restrict__ nrm2) {
+  BAMG_PDL_PROLOGUE();
+  if (flag[0] == 0.0) return;
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    nrm2[0] = t;
+  }
+}
+
+// out[0] = sqrt(sum_b part[b]) (fixed order, one CTA)
+__global__ void sum_sqrt_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[0] = sqrt(t);
+  }
+}
+
+// unsafe step, part 2: scale v_new by the explicit norm and form x (+ |x|^2
+// partials).  No-op when safe.
+__global__ void __launch_bounds__(256)
+cgs_fix_x_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ y,
+                 const double* __restrict__ x0, const double* __restrict__ e, const double* __restrict__ state,
+                 const double* __restrict__ flag, int64_t n, double* __restrict__ vnew, double* __restrict__ x,
+                 double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  if (flag[0] == 0.0) return;
+  __shared__ double red[8];
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    double u = 0.0;
+    for (int g = 0; g < m; ++g) u = fma(y[g], Vp[g][i], u);
+    const double xi = x0[i] + (e[i] + u);
+    x[i] = xi;
+    nrm = fma(xi, xi, nrm);
+    if (!happy) vnew[i] *= inv;
+  }
+  nrm = warp_sum(nrm);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
 struct GmresWork {
   std::vector<double*> basis;     // device vectors (owned)
   double** dVp = nullptr;         // device pointer table
@@ -565,6 +854,26 @@ static int basis_reserve(bamg_ctx* ctx, GmresWork& W, int64_t n, int count) {
                                   cudaMemcpyHostToDevice));
   W.uploaded = W.basis.size();
   return 0;
+}
+
+static int cgs_grid(bamg_ctx* ctx, const void* fn, int64_t n) {
+  static std::vector<std::pair<const void*, int>> occ;  // per kernel (one device per process in practice)
+  int per_sm = 0;
+  for (auto& e : occ)
+    if (e.first == fn) per_sm = e.second;
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CGS_THREADS, 0) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    occ.push_back({fn, per_sm});
+  }
+  const int64_t by_rows = (n + 4 * CGS_THREADS - 1) / (4 * CGS_THREADS);
+  const int64_t g = std::min<int64_t>((int64_t)per_sm * ctx->num_sms, std::max<int64_t>(by_rows, 1));
+  return (int)std::min<int64_t>(g, CGS_MAX_BLOCKS);
+}
+
+static bool cgs_fast_enabled() {
+  static const bool on = !(getenv("BAMG_CGS_SLOW") && getenv("BAMG_CGS_SLOW")[0] == '1');
+  return on;
 }
 
 static GmresWork& gmres_work(bamg_ctx* ctx) {
@@ -614,9 +923,11 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   BAMG_TRY(arena_get(ctx, m_cap, &y));
   BAMG_TRY(arena_get(ctx, m_cap + 2, &hv));
   BAMG_TRY(arena_get(ctx, m_cap + 2, &h2));
-  BAMG_TRY(arena_get(ctx, (size_t)nb * (m_cap + 2), &part));
+  BAMG_TRY(arena_get(ctx, std::max((size_t)nb * (m_cap + 2), (size_t)CGS_MAX_BLOCKS * (CGS_MAXM + 2)), &part));
   BAMG_TRY(arena_get(ctx, 8, &scal));
   BAMG_TRY(arena_get(ctx, 4, &state));
+  double* flag;
+  BAMG_TRY(arena_get(ctx, 2, &flag));
   GmresWork& W = gmres_work(ctx);
   const int blk = 256;
   const int grd = grid_for(n, blk);
@@ -644,14 +955,15 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
     return 0;
   };
   // the iteration's metric and Givens state (happy flag) in ONE read
-  auto metric_state = [&](const double* xv, double* out_host, bool* happy) -> int {
+  // x_norm_ready: |x| already in scal[1] (the CGS fast path forms it with x)
+  auto metric_state = [&](const double* xv, double* out_host, bool* happy, bool x_norm_ready) -> int {
     if (stopping == 1) {
       BAMG_TRY(resid_dev(ctx, B, b, xv, tmp));
       BAMG_TRY(norm_into(tmp, scal));
     } else {
       BAMG_TRY(spmm_dev(ctx, B, xv, tmp, 1));
       BAMG_TRY(norm_into(tmp, scal));
-      BAMG_TRY(norm_into(xv, scal + 1));
+      if (!x_norm_ready) BAMG_TRY(norm_into(xv, scal + 1));
     }
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(scal + 4, state, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     double hv3[5];
@@ -718,6 +1030,52 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       BAMG_TRY(basis_reserve(ctx, W, n, j + 2));
       // w = op(V_j)
       BAMG_TRY(apply_op(ctx, B, h, W.basis[j], tmp, w));
+      if (j + 1 <= CGS_MAXM && cgs_fast_enabled()) {
+        // three passes over V (see cgs_dots_kernel); x and |x| formed in pass C
+        const int mj = j + 1;
+        auto dots = mj <= 32 ? cgs_dots_kernel<32, 0> : cgs_dots_kernel<64, 0>;
+        auto upd = mj <= 32 ? cgs_dots_kernel<32, 1> : cgs_dots_kernel<64, 1>;
+        auto fin = mj <= 16 ? cgs_final_kernel<16> : mj <= 32 ? cgs_final_kernel<32> : cgs_final_kernel<64>;  // NOLINT
+        // one full wave: resident CTAs per SM x SMs (register-bound kernels),
+        // capped so every CTA keeps >= 4 row batches; a fixed function of
+        // (n, kernel, device), so the partial-sum tree is reproducible
+        const int cb = std::min(cgs_grid(ctx, (const void*)upd, n), cgs_grid(ctx, (const void*)fin, n));
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 1) * n, dots, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)nullptr, w, n, part);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)mj * 32, 256), 256, 0, (const double*)part, cb, mj + 1,
+                    mj, hv);
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 2) * n, upd, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)hv, w, n, part);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
+                    mj + 1, mj + 1, h2);
+        BAMG_LAUNCH(ctx, cgs_pythag_kernel, 1, 256, 0, mj, (const double*)h2, hv, scal + 3, flag);
+        BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
+                    y, state, (const double*)flag, 0);
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 5) * n, fin, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)h2, (const double*)y, (const double*)w, x0, (const double*)e,
+                        (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
+        BAMG_LAUNCH(ctx, cgs_fix_norm_kernel, 1, 256, 0, (const double*)flag, (const double*)part, cb, scal + 3);
+        BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
+                    y, state, (const double*)flag, 1);
+        BAMG_LAUNCH(ctx, cgs_fix_x_kernel, cb, 256, 0, (const double* const*)W.dVp, mj, (const double*)y, x0,
+                    (const double*)e, (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
+        BAMG_LAUNCH(ctx, sum_sqrt_kernel, 1, 256, 0, (const double*)part, cb, scal + 1);
+        ++iters;
+        used = j + 1;
+        double mval;
+        bool happy = false;
+        BAMG_TRY(metric_state(x, &mval, &happy, true));
+        history_host[nhist++] = mval;
+        if (mval <= rtol) converged = true;
+        if (converged || happy || iters >= max_iters) {
+          if (happy) converged = true;
+          BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, nullptr, e, nullptr, n, tmp);
+          BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+          broke = true;
+          break;
+        }
+        continue;
+      }
       // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; |w|^2
       BAMG_LAUNCH(ctx, mdot_kernel, nb, GM_THREADS, 0, W.dVp, j + 1, w, n, part);
       BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, part, nb, j + 1, hv, 0);
@@ -729,7 +1087,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       // h += h2 (length j+1) via the reduce kernel's accumulate path
       BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, h2, 1, j + 1, hv, 1);
       BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn, y,
-                  state);
+                  state, (const double*)nullptr, 0);
       BAMG_LAUNCH(ctx, scale_new_basis_kernel, grd, blk, 0, w, state, n, W.basis[j + 1]);
       ++iters;
       used = j + 1;
@@ -737,7 +1095,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, x0, e, nullptr, n, x);
       double mval;
       bool happy = false;
-      BAMG_TRY(metric_state(x, &mval, &happy));
+      BAMG_TRY(metric_state(x, &mval, &happy, false));
       history_host[nhist++] = mval;
       if (mval <= rtol) converged = true;
       if (converged || happy || iters >= max_iters) {

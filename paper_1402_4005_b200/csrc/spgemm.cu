@@ -507,12 +507,7 @@ static int spgemm_count_launch(bamg_ctx* ctx, SpgemmMemo& m, const bamg_csr* A, 
     // shared-memory tier over every row; its overflow (> SCAP distinct
     // columns) through the local-memory tier (grid-stride over the device
     // count in stat[3]), whose overflow goes to the slow path
-    static bool attr = false;
-    if (!attr) {
-      BAMG_CHECK_CUDA(ctx, cudaFuncSetAttribute(spgemm_smem_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)SPG_SMEM_BYTES));
-      attr = true;
-    }
+    BAMG_TRY(smem_optin(ctx, (const void*)spgemm_smem_count_kernel, SPG_SMEM_BYTES));
     unsigned int* nmid = reinterpret_cast<unsigned int*>(m.stat + 3);
     BAMG_LAUNCH_FAM(ctx, FAM_SPGEMM, 0.0, spgemm_smem_count_kernel, grid_for(n, SPG_ST), SPG_ST, SPG_SMEM_BYTES, n,
                     A->rowptr, A->col, A->val, B->rowptr, B->col, B->val, order, cnt, m.redo, nmid, m.tcol, m.tval,
