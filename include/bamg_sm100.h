@@ -305,6 +305,15 @@ int bamg_coarsest_triplets_ex(bamg_ctx* ctx, const double* Bd, const double* Md,
 /* x = B^+ b through the kept LU: (I - z z^T) B^g (I - y y^T) b. */
 int bamg_coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* lu, const double* b, double* x);
 int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* lu);
+/* Banded coarsest level: the same triplets as bamg_coarsest_triplets
+ * (coarsest_triplets, bootstrap.py:205-281) and the V-cycle's B^+
+ * (PinvOperator, dense.py:118-131) from block-tridiagonal factorisations of
+ * the CSR operators (B, its explicit transpose Bt, M, N; no dense n x n
+ * matrix is formed).  Returns 1 -- nothing written -- when the half-bandwidth
+ * exceeds 160 or n / 4, or the factorisation is not certified; the caller
+ * then takes the dense path.  *lu_out: free with bamg_coarse_lu_destroy. */
+int bamg_coarsest_band(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M, const bamg_csr* N,
+                       int r, double* U, double* V, double* sigma, bamg_coarse_lu** lu_out);
 
 /* ----------------------------------------------------------- solver (solver.py) */
 /* Hierarchy for the V-cycle (VCycleOperator, solver.py:79-124).  Level

@@ -292,10 +292,27 @@ def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps 
     return TripletSet(sig, U, V)
 
 
-def coarsest_triplets(B, M, N, r: int) -> TripletSet:
-    """Exact generalized singular triplets of the coarsest operator (bootstrap.py:205-281)."""
+def _band_min_n() -> int:
+    import os
+    return int(os.environ.get("BAMG_BAND_N", "2048"))
+
+
+def coarsest_triplets(B, M, N, r: int, Bt: DeviceCSR | None = None) -> TripletSet:
+    """Exact generalized singular triplets of the coarsest operator (bootstrap.py:205-281).
+
+    Large banded levels (the lattice chains keep the fine ordering, so the
+    coarsest operators have half-bandwidth ~ side + 1) take the block-
+    tridiagonal path (csrc/band.cu: no dense n x n matrix); everything else,
+    or a band factorisation that is not certified, the dense path."""
     A, Md, Nd = as_device(B), as_device(M), as_device(N)
     n = A.shape[0]
+    if n >= _band_min_n():
+        out = engine.coarsest_triplets_band(A, Bt if Bt is not None else engine.transpose(A), Md, Nd, r)
+        if out is not None:
+            U, V, s, lu = out
+            trips = TripletSet(s, U, V)
+            trips.coarse_pinv = lu
+            return trips
     Bd = engine.csr_to_dense(A)
     Mdd = engine.csr_to_dense(Md)
     Ndd = engine.csr_to_dense(Nd)
@@ -368,7 +385,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         if _DEBUG:
             print(f"[bamg] coarsest level {depth} n={n}", file=sys.stderr, flush=True)
         with _phase("coarsest"):
-            trips = coarsest_triplets(A, Md, Nd, trips.r)
+            trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt)
         return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
 
     with _phase("smooth"):
@@ -412,7 +429,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             if _DEBUG:
                 print(f"[bamg] truncated at level {depth} n={n} (sick Galerkin product)", file=sys.stderr, flush=True)
             with _phase("coarsest"):
-                trips = coarsest_triplets(A, Md, Nd, trips.r)
+                trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt)
             return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
         with _phase("inject"):
             cranks = ranks.restrict(split) if ranks is not None else None

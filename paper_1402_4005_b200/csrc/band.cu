@@ -1,0 +1,1070 @@
+// band.cu -- the coarsest level when its operators are banded.
+//
+// The reference densifies the coarsest operator (bootstrap.py:205-281:
+// coarsest_triplets' doubled 2n x 2n generalized eigenproblem through
+// dense.py:74-92, and dense.py:118-131's SVD pseudo-inverse for the V-cycle).
+// On the lattice chains (tandem, uniform) the coarse points keep the fine
+// ordering, so B_L, M_L and N_L are banded with half-bandwidth ~ side + 1
+// (129 at cfg4's 16,384-point coarsest level): a dense LU would spend ~n^3
+// flops on zeros.  Here the three operators are factorised as BLOCK-
+// TRIDIAGONAL matrices with dense S x S blocks (S >= bandwidth, S <= 160),
+// padded at the FRONT with identity rows to N = nb S:
+//
+//   B = Lb Ub:  Lb = unit block lower bidiagonal (sub-blocks X_k),
+//               Ub = block upper bidiagonal (diagonal Schur complements S_k,
+//                    super-blocks the original Up_k)
+//     S_0 = D_0,  X_k = Lo_{k-1} S_{k-1}^-1,  S_k = D_k - X_k Up_{k-1}
+//   (block Thomas recurrence; each S_k is inverted explicitly by an in-place
+//   Gauss-Jordan with partial pivoting in one CTA's shared memory).  B has
+//   rank n - 1, which surfaces in the LAST Schur complement: it is inverted
+//   through the bordered matrix [[S, u], [v^T, 0]] (u = v = 1/sqrt(S)), whose
+//   inverse gives a {1}-inverse of S and its right / left null vectors (the
+//   bordered-system idea of the dense path).  G = Ub^g Lb^-1 is then a
+//   {1}-inverse of B (B G B = B), the null vectors of B follow from the last
+//   block's by one block sweep each, and B^+ = (I - z z^T) G (I - y y^T).
+//
+//   M = F F^T with F = Lm blockdiag(C_k) (the same recurrence on the
+//   symmetrised SPD mass matrix, C_k = chol(S_k)); any such factor serves
+//   K = F_M^-1 B F_N^-T (the triplets u = F_M^-T a, v = F_N^-T b do not
+//   depend on which one).
+//
+// K^+ = (I - b0 b0^T) F_N^T G F_M (I - a0 a0^T) (as the dense implicit path)
+// is applied by block sweeps; the r smallest singular triplets of K come from
+// block subspace iteration on K^+ with Rayleigh-Ritz (same iteration and
+// stopping rule as dense_large.cu).  Everything is certified before use:
+// |B z|, |B^T y| at round-off and |B G B x - B x| <= 1e-10 |B x|; an
+// uncertified factorisation (e.g. a Schur complement with a tiny pivot,
+// since there is no pivoting ACROSS blocks) returns 1 and the caller takes
+// the dense path.
+//
+// Sequential block sweeps (forward / backward substitution with p right-hand
+// sides) run as one thread-block-cluster kernel per sweep: the 8 CTAs of a
+// cluster own row slices of every block, and the new block of the solution
+// is exchanged through distributed shared memory behind one cluster barrier
+// per block step.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int BT_MAX_S = 160;
+constexpr int BT_CL = 8;         // CTAs per sweep cluster
+constexpr int BT_THREADS = 256;  // threads per sweep CTA
+constexpr int BT_MAXCOLS = 8;    // right-hand sides per sweep cluster
+constexpr int BT_NST = 4;        // W-slice stages in flight per sweep CTA
+
+// ------------------------------------------------------------- assembly
+__global__ void bt_bandwidth_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, int n,
+                                    int* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  int lo = 0, hi = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int d = i - col[e];
+      lo = max(lo, d);
+      hi = max(hi, -d);
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = max(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
+__device__ __forceinline__ double* bt_slot(int I, int J, int S, double* D, double* Lo, double* Up, int* bad) {
+  const int bi = I / S, bj = J / S, li = I - bi * S, lj = J - bj * S;
+  const size_t S2 = (size_t)S * S;
+  if (bi == bj) return D + bi * S2 + (size_t)lj * S + li;
+  if (bj == bi + 1) return Up + bi * S2 + (size_t)lj * S + li;
+  if (bj + 1 == bi) return Lo + bj * S2 + (size_t)lj * S + li;
+  *bad = 1;
+  return nullptr;
+}
+
+// CSR (n x n) -> padded block-tridiagonal blocks (zeroed beforehand).  sym:
+// the symmetric part 0.5 (A + A^T) (bootstrap.py:217-218): every slot gets at
+// most two halves, added in either order to zero -- the same double.
+__global__ void bt_scatter_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                  const double* __restrict__ val, int n, int off, int S, double* D, double* Lo,
+                                  double* Up, int sym, int* bad) {
+  BAMG_PDL_PROLOGUE();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int I = i + off, J = col[e] + off;
+      const double v = val[e];
+      if (!sym) {
+        double* s = bt_slot(I, J, S, D, Lo, Up, bad);
+        if (s) *s = v;
+      } else {
+        double* s1 = bt_slot(I, J, S, D, Lo, Up, bad);
+        double* s2 = bt_slot(J, I, S, D, Lo, Up, bad);
+        if (s1) atomicAdd(s1, 0.5 * v);
+        if (s2) atomicAdd(s2, 0.5 * v);
+      }
+    }
+}
+
+__global__ void bt_pad_kernel(double* D, int off, int S) {
+  BAMG_PDL_PROLOGUE();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < off) D[(size_t)t * S + t] = 1.0;
+}
+
+// --------------------------------------------- per-block dense kernels (1 CTA)
+struct GJJob {
+  const double* A;  // S x S input (column-major, ld S)
+  double* out;      // S x S: inverse, or the {1}-inverse block when bordered
+  double* nullr;    // bordered: right null vector of A (S), scaled
+  double* nulll;    // bordered: left null vector of A (S), scaled
+  int S;
+  int border;
+};
+struct GJJobs {
+  GJJob j[3];
+};
+
+// In-place Gauss-Jordan inverse with partial pivoting, one CTA per job (the
+// matrix lives in shared memory: m <= BT_MAX_S + 1).  Each step folds the row
+// interchange into the rank-1 update (a read-only pass collects the scaled
+// pivot row, the pivot column and the old row k), so a step costs three
+// barriers; every thread updates a fixed (row, column-stride) set of entries.
+// A pivot below 1e-14 of the matrix's largest entry flags `bad` (the block
+// recurrence is not trustworthy there; the caller falls back to the dense
+// path).  (A register-resident variant spilled and ran 2.7x slower.)
+__global__ void __launch_bounds__(1024) bt_gj_kernel(GJJobs jobs, int* bad) {
+  BAMG_PDL_PROLOGUE();
+  const GJJob J = blockIdx.x == 0 ? jobs.j[0] : (blockIdx.x == 1 ? jobs.j[1] : jobs.j[2]);
+  const int S = J.S, m = S + (J.border ? 1 : 0);
+  extern __shared__ double sm[];
+  double* A = sm;                 // m x m, column-major
+  double* colk = A + m * m;       // m
+  double* rowk = colk + m;        // m
+  double* krow = rowk + m;        // m
+  int* perm = reinterpret_cast<int*>(krow + m);  // m
+  __shared__ int s_p;
+  __shared__ double s_piv, red_v[32];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const double bv = J.border ? 1.0 / sqrt((double)S) : 0.0;
+  double amax = 0.0;
+  for (int t = tid; t < m * m; t += nt) {
+    const int r = t % m, c = t / m;
+    double v;
+    if (r < S && c < S) v = J.A[(size_t)c * S + r];
+    else v = (r == S && c == S) ? 0.0 : bv;
+    A[t] = v;
+    amax = fmax(amax, fabs(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) red_v[wid] = amax;
+  __syncthreads();
+  if (wid == 0) {
+    double v = lane < (nt >> 5) ? red_v[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red_v[0] = v;
+  }
+  __syncthreads();
+  const double tiny = 1e-14 * red_v[0];
+  const int ngrp = nt / m;
+  const int my_r = tid < ngrp * m ? tid % m : -1, my_c0 = tid < ngrp * m ? tid / m : 0;
+  for (int k = 0; k < m; ++k) {
+    if (wid == 0) {  // pivot: largest |A[i][k]|, i >= k, lowest row on ties
+      double best = -1.0;
+      int bi = m;
+      for (int i = k + lane; i < m; i += 32) {
+        const double v = fabs(A[k * m + i]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        s_piv = A[k * m + bi];
+        perm[k] = bi;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double piv = s_piv;
+    if (!(fabs(piv) > tiny)) {
+      if (tid == 0) atomicExch(bad, 1);
+      return;
+    }
+    const double inv = 1.0 / piv;
+    for (int t = tid; t < m; t += nt) {
+      rowk[t] = t == k ? inv : A[t * m + p] * inv;                      // new row k = old row p / piv
+      colk[t] = t == k ? 0.0 : (t == p ? A[k * m + k] : A[k * m + t]);  // column k after the swap
+      krow[t] = A[t * m + k];                                           // old row k -> row p
+    }
+    __syncthreads();
+    if (my_r >= 0) {
+      const double cr = colk[my_r];
+      for (int c = my_c0; c < m; c += ngrp) {
+        double* a = A + c * m + my_r;
+        if (my_r == k) {
+          *a = rowk[c];
+        } else {
+          const double base = c == k ? 0.0 : (my_r == p ? krow[c] : *a);
+          *a = base - cr * rowk[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, in reverse
+  for (int k = m - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k)
+      for (int r = tid; r < m; r += nt) {
+        const double a = A[k * m + r];
+        A[k * m + r] = A[p * m + r];
+        A[p * m + r] = a;
+      }
+    __syncthreads();
+  }
+  for (int t = tid; t < S * S; t += nt) {
+    const int r = t % S, c = t / S;
+    J.out[t] = A[c * m + r];
+  }
+  if (J.border)
+    for (int t = tid; t < S; t += nt) {
+      J.nullr[t] = A[S * m + t];  // last column, rows < S
+      J.nulll[t] = A[t * m + S];  // last row, columns < S
+    }
+}
+
+static inline size_t bt_gj_smem(int S) {
+  const size_t m = S + 1;
+  return sizeof(double) * (m * m + 3 * m) + sizeof(int) * (m + 1);
+}
+
+struct CholJob {
+  const double* A;  // S x S SPD
+  double* C;        // lower factor (upper zeroed)
+  int S;
+};
+struct CholJobs {
+  CholJob j[2];
+};
+
+__global__ void __launch_bounds__(1024) bt_chol_kernel(CholJobs jobs, int* bad) {
+  BAMG_PDL_PROLOGUE();
+  const CholJob J = jobs.j[blockIdx.x];
+  const int m = J.S;
+  extern __shared__ double sm[];
+  double* A = sm;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int t = tid; t < m * m; t += nt) A[t] = J.A[t];
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    const double d = A[k * m + k];
+    if (!(d > 0.0)) {
+      if (tid == 0) atomicExch(bad, 1);
+      return;
+    }
+    const double s = sqrt(d);
+    __syncthreads();
+    for (int r = k + tid; r < m; r += nt) A[k * m + r] = r == k ? s : A[k * m + r] / s;
+    __syncthreads();
+    const int w = m - k - 1;
+    for (int t = tid; t < w * w; t += nt) {
+      const int r = k + 1 + t % w, c = k + 1 + t / w;
+      if (r >= c) A[c * m + r] -= A[k * m + r] * A[k * m + c];
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < m * m; t += nt) {
+    const int r = t % m, c = t / m;
+    J.C[t] = r >= c ? A[t] : 0.0;
+  }
+}
+
+// x_k = C_k^-T b_k for every block k (C_k lower triangular, S x S), r
+// columns of the padded N x r block in place: one CTA per (block, column),
+// back substitution with a warp dot per row (row i of C^T = column i of C).
+__global__ void __launch_bounds__(256) bt_trsv_lt_kernel(const double* __restrict__ C, int S, int N, double* X,
+                                                         int ldx) {
+  BAMG_PDL_PROLOGUE();
+  const int k = blockIdx.x, col = blockIdx.y;
+  const double* Ck = C + (size_t)k * S * S;
+  double* x = X + (size_t)col * ldx + (size_t)k * S;
+  __shared__ double xs[BT_MAX_S];
+  for (int i = threadIdx.x; i < S; i += blockDim.x) xs[i] = x[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    for (int i = S - 1; i >= 0; --i) {
+      const double* ci = Ck + (size_t)i * S;  // column i of C = row i of C^T
+      double acc = 0.0;
+      for (int j = i + 1 + lane; j < S; j += 32) acc = fma(ci[j], xs[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) xs[i] = (xs[i] - acc) / ci[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S; i += blockDim.x) x[i] = xs[i];
+}
+
+// ----------------------------------------------------------- block sweeps
+// out_k = u_k - W_{k+coff} out_{k-dir} for k along `dir` (the W term skipped
+// at the first step and where W_{k+coff} does not exist); `init` (optional,
+// S values shared by every column) replaces out of the first step.  W is
+// given ROW-contiguous: Wr[k][i][j] = W_k(i, j) at Wr + k S^2 + i S + j (the
+// transpose of the column-major block).  Every forward / backward block
+// substitution of the band path has this form once the block-diagonal
+// factors are folded into W (W_k = S_k^-1 Up_k, ...) and into u (a batched
+// GEMM beforehand), so a step is ONE block GEMV and ONE exchange.
+// Columns [c0, c0 + BT_MAXCOLS) per cluster; CTA q of the cluster owns block
+// rows [q R, q R + R), R = ceil(S / BT_CL), stages its R x S slice of W and
+// its rows of u BT_NST - 1 steps ahead (16-byte cp.async), computes its rows
+// with G threads per output (interleaved columns, shuffle tree), and
+// publishes them through DSMEM behind one cluster barrier per step.
+struct SweepOp {
+  const double* W;
+  const double* init;
+  int coff, dir;
+  int dev = 0;  // development timing switches (bamg_band_sweep_probe): 1 no global store, 2 no gather,
+                // 4 no cluster barrier, 8 no prefetch
+};
+
+__device__ __forceinline__ void bt_cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void bt_cp8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+__global__ void __cluster_dims__(BT_CL, 1, 1) __launch_bounds__(BT_THREADS)
+    bt_sweep_kernel(int S, int nb, SweepOp op, const double* __restrict__ u, int ldu, double* __restrict__ out,
+                    int ldo, int p) {
+  BAMG_PDL_PROLOGUE();
+  constexpr int SL = BT_MAX_S / BT_CL + 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int c0 = (blockIdx.x / BT_CL) * BT_MAXCOLS;
+  const int nc = min(BT_MAXCOLS, p - c0);
+  const int R = (S + BT_CL - 1) / BT_CL;
+  const int r0 = min(S, q * R), r1 = min(S, r0 + R);
+  const int rows = r1 - r0;
+  const int SP = S + 2;  // slice row pitch (even: 16-byte rows; +2 spreads banks)
+  extern __shared__ double smem[];
+  double* sW = smem;                         // [BT_NST][SL][SP]
+  double* prev = sW + BT_NST * SL * SP;      // [BT_MAXCOLS][S]
+  double* os = prev + BT_MAXCOLS * S;        // [2][BT_MAXCOLS][SL]
+  double* su = os + 2 * BT_MAXCOLS * SL;     // [BT_NST][BT_MAXCOLS][SL]: u rows of the step
+  const int tid = threadIdx.x;
+  const size_t S2 = (size_t)S * S;
+  auto wvalid = [&](int k) { return op.W && k + op.coff >= 0 && k + op.coff < nb; };
+  auto kof = [&](int s) { return op.dir > 0 ? s : nb - 1 - s; };
+  // G threads per output (power of two <= 8), outputs = rows x nc
+  const int nout = rows * nc;
+  int G = 1;
+  while (G < 8 && nout * G * 2 <= BT_THREADS) G <<= 1;
+  const int my_o = tid / G, my_g = tid % G;
+  auto prefetch = [&](int s) {
+    const int k = kof(s), stage = s % BT_NST;
+    if (s > 0 && wvalid(k)) {
+      const double* W = op.W + (size_t)(k + op.coff) * S2 + (size_t)r0 * S;
+      double* dst = sW + stage * SL * SP;
+      const int h = S / 2;
+      for (int t = tid; t < rows * h; t += blockDim.x) {
+        const int i = t / h, j2 = t - i * h;
+        bt_cp16(dst + i * SP + 2 * j2, W + (size_t)i * S + 2 * j2);
+      }
+    }
+    double* du = su + stage * BT_MAXCOLS * SL;
+    for (int t = tid; t < nout; t += blockDim.x) {
+      const int i = t % rows, c = t / rows;
+      bt_cp8(du + c * SL + i, u + (size_t)(c0 + c) * ldu + (size_t)k * S + r0 + i);
+    }
+  };
+  for (int s = 0; s < BT_NST - 1; ++s) {
+    if (s < nb) prefetch(s);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int s = 0; s < nb; ++s) {
+    const int k = kof(s);
+    const int par = s & 1;
+    // one commit group per step: at most BT_NST - 2 younger groups in flight
+    // means step s's group has landed
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(BT_NST - 2));
+    __syncthreads();  // step s's stage visible; every thread is done with step s - 1's stage
+    if (s + BT_NST - 1 < nb && !(op.dev & 8)) prefetch(s + BT_NST - 1);  // reuses the stage of step s - 1
+    asm volatile("cp.async.commit_group;\n" ::);
+    const bool useW = s > 0 && wvalid(k);
+    const double* wsl = sW + (s % BT_NST) * SL * SP;
+    const double* usl = su + (s % BT_NST) * BT_MAXCOLS * SL;
+    {
+      const bool act = my_o < nout;
+      const int i = act ? my_o % rows : 0, c = act ? my_o / rows : 0;
+      double a0 = 0.0, a1 = 0.0;
+      if (useW && act) {
+        const double* wr = wsl + i * SP;
+        const double* pv = prev + c * S;
+        int j = my_g;
+        for (; j + G < S; j += 2 * G) {
+          a0 = fma(wr[j], pv[j], a0);
+          a1 = fma(wr[j + G], pv[j + G], a1);
+        }
+        if (j < S) a0 = fma(wr[j], pv[j], a0);
+      }
+      double acc = a0 + a1;
+      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);  // all lanes
+      if (act && my_g == 0) {
+        const double v = (s == 0 && op.init) ? op.init[r0 + i] : usl[c * SL + i] - acc;
+        if (!(op.dev & 1)) out[(size_t)(c0 + c) * ldo + (size_t)k * S + r0 + i] = v;
+        os[(par * BT_MAXCOLS + c) * SL + i] = v;
+      }
+    }
+    if (!(op.dev & 4)) cluster.sync();
+    else __syncthreads();
+    if (!(op.dev & 2))
+      for (int t = tid; t < S * nc; t += blockDim.x) {
+        const int i = t % S, c = t / S;
+        const int owner = i / R;
+        const double* rem = cluster.map_shared_rank(os, owner);
+        prev[c * S + i] = rem[(par * BT_MAXCOLS + c) * SL + (i - owner * R)];
+      }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  cluster.sync();  // no CTA leaves while a peer may still read its slices
+}
+
+static inline size_t bt_sweep_smem(int S) {
+  constexpr int SL = BT_MAX_S / BT_CL + 1;
+  return sizeof(double) * ((size_t)BT_NST * SL * (S + 2) + (size_t)BT_MAXCOLS * S + (size_t)2 * BT_MAXCOLS * SL +
+                           (size_t)BT_NST * BT_MAXCOLS * SL);
+}
+
+// Batched transpose of S x S blocks: out_k = in_k^T (column-major both)
+__global__ void bt_transpose_blocks_kernel(const double* __restrict__ in, int S, int nb, double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double tile[32][33];
+  const int k = blockIdx.z;
+  const double* A = in + (size_t)k * S * S;
+  double* T = out + (size_t)k * S * S;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + threadIdx.x, j = by + r;
+    if (i < S && j < S) tile[r][threadIdx.x] = A[(size_t)j * S + i];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + threadIdx.x, j = bx + r;
+    if (i < S && j < S) T[(size_t)j * S + i] = tile[threadIdx.x][r];
+  }
+}
+
+// ------------------------------------------------------- small vector ops
+__global__ void bt_embed_kernel(const double* __restrict__ X, int ldx, int n, int off, int N, int p,
+                                double* __restrict__ Y) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)N * p) return;
+  const int r = (int)(t % N), c = (int)(t / N);
+  Y[t] = r < off ? 0.0 : X[(size_t)c * ldx + (r - off)];
+}
+
+__global__ void bt_extract_kernel(const double* __restrict__ Y, int N, int off, int n, int p, double* __restrict__ X,
+                                  int ldx) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * p) return;
+  const int r = (int)(t % n), c = (int)(t / n);
+  X[(size_t)c * ldx + r] = Y[(size_t)c * N + off + r];
+}
+
+__device__ __forceinline__ double bt_bsum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
+// dots[c] = v . Y[:, c]
+__global__ void bt_coldot_kernel(const double* __restrict__ Y, int ld, int n, const double* __restrict__ v,
+                                 double* __restrict__ dots) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  const double* y = Y + (size_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(v[i], y[i], s);
+  s = bt_bsum(s, sh);
+  if (threadIdx.x == 0) dots[blockIdx.x] = s;
+}
+
+// out[c] = X[:, c] . Y[:, c]
+__global__ void bt_pairdot_kernel(const double* __restrict__ X, const double* __restrict__ Y, int ld, int n,
+                                  double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  const double* a = X + (size_t)blockIdx.x * ld;
+  const double* b = Y + (size_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+  s = bt_bsum(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// Y[:, c] = X[:, c] - v dots[c]
+__global__ void bt_rank1_kernel(const double* __restrict__ X, int ldx, int n, int p, const double* __restrict__ v,
+                                const double* __restrict__ dots, double* __restrict__ Y, int ldy) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * p) return;
+  const int r = (int)(t % n), c = (int)(t / n);
+  Y[(size_t)c * ldy + r] = X[(size_t)c * ldx + r] - v[r] * dots[c];
+}
+
+// column c of X (ld) scaled to unit 2-norm; norm to nrm[c] if non-null
+__global__ void bt_colnorm_kernel(double* X, int ld, int n, double* nrm) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  double* x = X + (size_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], x[i], s);
+  s = sqrt(bt_bsum(s, sh));
+  const double d = fmax(s, 1e-300);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] /= d;
+  if (nrm && threadIdx.x == 0) nrm[blockIdx.x] = s;
+}
+
+__global__ void bt_fill_random_kernel(double* X, int N, int off, int p, unsigned seed) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)N * p) return;
+  const int r = (int)(t % N);
+  unsigned h = (unsigned)(t * 2654435761ull) ^ (seed * 0x9e3779b9u);
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  X[t] = r < off ? 0.0 : (double)(h & 0xffffff) / 16777216.0 - 0.5;
+}
+
+// sums of squares: out[0] = |a|^2, out[1] = |b|^2 (one CTA)
+__global__ void bt_norms2_kernel(const double* __restrict__ a, int na, const double* __restrict__ b, int nbv,
+                                 double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) s = fma(a[i], a[i], s);
+  s = bt_bsum(s, sh);
+  if (threadIdx.x == 0) out[0] = s;
+  double w = 0.0;
+  for (int i = threadIdx.x; i < nbv; i += blockDim.x) w = fma(b[i], b[i], w);
+  w = bt_bsum(w, sh);
+  if (threadIdx.x == 0) out[1] = w;
+}
+
+__global__ void bt_diff2_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
+                                double* __restrict__ out) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double sh[32];
+  double s = 0.0, w = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = a[i] - b[i];
+    s = fma(d, d, s);
+    w = fma(b[i], b[i], w);
+  }
+  s = bt_bsum(s, sh);
+  w = bt_bsum(w, sh);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = w;
+  }
+}
+
+__global__ void bt_interleave_kernel(const double* __restrict__ U, const double* __restrict__ V,
+                                     const double* __restrict__ sgn, int n, int ld, int r, double* __restrict__ Uo,
+                                     double* __restrict__ Vo) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * r) return;
+  const int i = (int)(t / r), j = (int)(t % r);
+  Uo[t] = U[(size_t)j * ld + i];
+  const double v = V[(size_t)j * ld + i];
+  Vo[t] = sgn[j] < 0.0 ? -v : v;
+}
+
+}  // namespace
+
+// ================================================================== host
+// B's factor as the sweeps use it: X_k (k >= 1) and its row-contiguous copy
+// XT_k = X_k^T, Sinv_k = S_k^-1 (the last a {1}-inverse), WT_k = (Sinv_k
+// Up_k)^T (k < nb - 1), V_k = Up_{k-1} Sinv_k (k >= 1; V_k^T row-contiguous
+// is V_k itself)
+struct BtB {
+  const double *X, *XT, *Sinv, *WT, *V;
+};
+
+struct BandPinv {  // kept for the V-cycle: B^+ b = (I - z z^T) G (I - y y^T) b
+  int n = 0, N = 0, S = 0, nb = 0, off = 0;
+  double *XT = nullptr, *Sinv = nullptr, *WT = nullptr;  // B's factor for G (device, owned)
+  double *z = nullptr, *y = nullptr;                                  // unit null vectors, padded N
+  double *t1 = nullptr, *t2 = nullptr, *dots = nullptr;               // scratch
+  std::vector<void*> mem;
+};
+
+namespace {
+
+int bt_sweep(bamg_ctx* ctx, int S, int nb, const SweepOp& op, const double* u, int ldu, double* out, int ldo, int p) {
+  const size_t smem = bt_sweep_smem(S);
+  BAMG_TRY(smem_optin(ctx, (const void*)bt_sweep_kernel, smem));
+  const int clusters = (p + BT_MAXCOLS - 1) / BT_MAXCOLS;
+  BAMG_LAUNCH(ctx, bt_sweep_kernel, clusters * BT_CL, BT_THREADS, smem, S, nb, op, u, ldu, out, ldo, p);
+  return 0;
+}
+
+// out_k = alpha op(A_k) Y_k (+ beta out_k) for every block k in [k0, k0 + cnt)
+// (A_k: S x S blocks, Y / out: padded N x p, ld N) -- one batched DMMA GEMM
+int bt_blockdiag(bamg_ctx* ctx, int S, int N, const double* A, bool ta, const double* Y, double* out, int p, int k0,
+                 int cnt, int ydelta, double alpha = 1.0, double beta = 0.0) {
+  if (cnt <= 0) return 0;
+  const size_t S2 = (size_t)S * S;
+  return dgemm_batched_dev(ctx, ta, false, S, p, S, alpha, A + k0 * S2, S, (int64_t)S2, Y + (int64_t)(k0 + ydelta) * S,
+                           N, S, beta, out + (int64_t)k0 * S, N, S, cnt);
+}
+
+// G in (p columns, padded N): forward with Lb, block-diagonal S^-1, backward
+// with W; G^T: block-diagonal S^-T, forward with V^T, backward with X^T
+int bt_apply_G(bamg_ctx* ctx, int S, int nb, int N, const BtB& F, const double* in, double* tmp, double* out, int p,
+               bool trans) {
+  if (!trans) {
+    SweepOp f{F.XT, nullptr, 0, +1};
+    BAMG_TRY(bt_sweep(ctx, S, nb, f, in, N, tmp, N, p));
+    BAMG_TRY(bt_blockdiag(ctx, S, N, F.Sinv, false, tmp, out, p, 0, nb, 0));
+    SweepOp b{F.WT, nullptr, 0, -1};
+    return bt_sweep(ctx, S, nb, b, out, N, out, N, p);  // in place: step k reads u_k before writing out_k
+  }
+  BAMG_TRY(bt_blockdiag(ctx, S, N, F.Sinv, true, in, tmp, p, 0, nb, 0));
+  SweepOp f{F.V, nullptr, 0, +1};
+  BAMG_TRY(bt_sweep(ctx, S, nb, f, tmp, N, tmp, N, p));
+  SweepOp b{F.X, nullptr, +1, -1};
+  return bt_sweep(ctx, S, nb, b, tmp, N, out, N, p);
+}
+
+struct BtDims {
+  int n, N, S, nb, off;
+};
+
+int bt_assemble(bamg_ctx* ctx, const bamg_csr* A, const BtDims& d, int sym, double* D, double* Lo, double* Up,
+                int* bad) {
+  const size_t S2 = (size_t)d.S * d.S;
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(D, 0, sizeof(double) * S2 * d.nb, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(Lo, 0, sizeof(double) * S2 * d.nb, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(Up, 0, sizeof(double) * S2 * d.nb, ctx->stream));
+  BAMG_LAUNCH(ctx, bt_scatter_kernel, std::min(grid_for(d.n, 256), 4 * ctx->num_sms), 256, 0, A->rowptr, A->col,
+              A->val, d.n, d.off, d.S, D, Lo, Up, sym, bad);
+  if (d.off > 0) BAMG_LAUNCH(ctx, bt_pad_kernel, grid_for(d.off, 256), 256, 0, D, d.off, d.S);
+  return 0;
+}
+
+}  // namespace
+
+int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x) {
+  const int n = h->n, N = h->N;
+  BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for(N, 256), 256, 0, b, n, n, h->off, N, 1, h->t1);
+  BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->y, h->dots);
+  BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->y,
+              (const double*)h->dots, h->t1, N);
+  const BtB F{nullptr, h->XT, h->Sinv, h->WT, nullptr};
+  BAMG_TRY(bt_apply_G(ctx, h->S, h->nb, N, F, h->t1, h->t2, h->t1, 1, false));
+  BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->z, h->dots + 1);
+  BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->z,
+              (const double*)(h->dots + 1), h->t2, N);
+  BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for(n, 256), 256, 0, (const double*)h->t2, N, h->off, n, 1, x, n);
+  return 0;
+}
+
+void band_pinv_free(BandPinv* h) {
+  if (!h) return;
+  for (void* q : h->mem) cudaFree(q);
+  delete h;
+}
+
+// The band path.  Returns 0 (triplets in U, V, sigma; *keep = the V-cycle's
+// pseudo-inverse), 1 (not applicable or not certified: take the dense path),
+// < 0 on errors.  U, V: n x r interleaved (row-major n x r), sigma: r.
+int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
+                           const bamg_csr* N_, int r, double* U, double* V, double* sigma, BandPinv** keep) {
+  *keep = nullptr;
+  const int n = B->nrows;
+  // half-bandwidths of the three operators -> block size
+  int* bw;
+  BAMG_TRY(arena_get(ctx, 8, &bw));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bw, 0, sizeof(int) * 8, ctx->stream));
+  const int g = std::min(grid_for(n, 256), 2 * ctx->num_sms);
+  BAMG_LAUNCH(ctx, bt_bandwidth_kernel, g, 256, 0, B->rowptr, B->col, n, bw);
+  BAMG_LAUNCH(ctx, bt_bandwidth_kernel, g, 256, 0, M->rowptr, M->col, n, bw + 2);
+  BAMG_LAUNCH(ctx, bt_bandwidth_kernel, g, 256, 0, N_->rowptr, N_->col, n, bw + 4);
+  int hb[6];
+  BAMG_TRY(ctx_read_i32(ctx, bw, 6, hb));
+  const int band = std::max({hb[0], hb[1], hb[2], hb[3], hb[4], hb[5], 1});
+  const int S = std::max(32, (band + 7) / 8 * 8);
+  if (S > BT_MAX_S || S * 4 > n) return 1;
+  BtDims d;
+  d.n = n;
+  d.S = S;
+  d.nb = (n + S - 1) / S;
+  d.N = d.nb * S;
+  d.off = d.N - n;
+  const int nb = d.nb, Np = d.N;
+  const size_t S2 = (size_t)S * S, blk = S2 * nb;
+  const int p = std::min(r + 12, n);
+  BAMG_REQUIRE(ctx, p <= 48, "band path: subspace block too wide");
+
+  // ---- block storage (arena; the kept B factor is copied out at the end)
+  double *Db, *Lob, *Upb, *Xb, *XTb, *Sib, *Wb, *Vb_, *Dm, *Lom, *Upm, *Xm, *Sim, *Cm, *XCm, *Dn, *Lon, *Upn, *Xn, *Sin,
+      *Cn, *XCn;
+  double *qz, *ry;
+  int* bad;
+  for (double** pp : {&Db, &Lob, &Upb, &Xb, &XTb, &Sib, &Wb, &Vb_, &Dm, &Lom, &Upm, &Xm, &Sim, &Cm, &XCm, &Dn, &Lon,
+                      &Upn, &Xn, &Sin, &Cn, &XCn})
+    BAMG_TRY(arena_get(ctx, blk, pp));
+  BAMG_TRY(arena_get(ctx, S, &qz));
+  BAMG_TRY(arena_get(ctx, S, &ry));
+  BAMG_TRY(arena_get(ctx, 4, &bad));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int) * 4, ctx->stream));
+  BAMG_TRY(bt_assemble(ctx, B, d, 0, Db, Lob, Upb, bad));
+  BAMG_TRY(bt_assemble(ctx, M, d, 1, Dm, Lom, Upm, bad));
+  BAMG_TRY(bt_assemble(ctx, N_, d, 1, Dn, Lon, Upn, bad));
+
+  // ---- block Thomas recurrences of B, M, N in lockstep
+
+  const size_t ch_smem = sizeof(double) * S2;
+  BAMG_TRY(smem_optin(ctx, (const void*)bt_chol_kernel, ch_smem));
+  BAMG_TRY(smem_optin(ctx, (const void*)bt_gj_kernel, bt_gj_smem(S)));
+  struct Mat {
+    double *D, *Lo, *Up, *X, *Si;
+  } mats[3] = {{Db, Lob, Upb, Xb, Sib}, {Dm, Lom, Upm, Xm, Sim}, {Dn, Lon, Upn, Xn, Sin}};
+  for (int k = 0; k < nb; ++k) {
+    for (auto& mt : mats) {
+      if (k > 0) {
+        // X_k = Lo_{k-1} S_{k-1}^-1 ;  S_k = D_k - X_k Up_{k-1}  (in place in D_k)
+        BAMG_TRY(dgemm_dev(ctx, false, false, S, S, S, 1.0, mt.Lo + (k - 1) * S2, S, mt.Si + (k - 1) * S2, S, 0.0,
+                           mt.X + k * S2, S));
+        BAMG_TRY(dgemm_dev(ctx, false, false, S, S, S, -1.0, mt.X + k * S2, S, mt.Up + (k - 1) * S2, S, 1.0,
+                           mt.D + k * S2, S));
+      }
+    }
+    GJJobs jobs{};
+    const bool last = k == nb - 1;
+    for (int t = 0; t < 3; ++t)
+      jobs.j[t] = GJJob{mats[t].D + k * S2, mats[t].Si + k * S2, t == 0 ? qz : nullptr, t == 0 ? ry : nullptr, S,
+                        (t == 0 && last) ? 1 : 0};
+    BAMG_LAUNCH(ctx, bt_gj_kernel, 3, 1024, bt_gj_smem(S), jobs, bad);
+    CholJobs cj{};
+    cj.j[0] = CholJob{Dm + k * S2, Cm + k * S2, S};
+    cj.j[1] = CholJob{Dn + k * S2, Cn + k * S2, S};
+    BAMG_LAUNCH(ctx, bt_chol_kernel, 2, 1024, ch_smem, cj, bad + 1);
+  }
+  int hbad[2];
+  BAMG_TRY(ctx_read_i32(ctx, bad, 2, hbad));
+  if (hbad[0] || hbad[1]) {
+    if (getenv("BAMG_DEBUG"))
+      fprintf(stderr, "[bamg] band coarsest n=%d S=%d: %s -> dense path\n", n, S,
+              hbad[1] ? "mass Cholesky failed" : "tiny pivot in a Schur complement");
+    return 1;
+  }
+  // the folded sweep blocks: XC_k = X_k C_{k-1} (F, F^T products),
+  // W_k = Sinv_k Up_k, V_k = Up_{k-1} Sinv_k (B's sweeps)
+  if (nb > 1) {
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Xm + S2, S, S2, Cm, S, S2, 0.0, XCm + S2, S, S2, nb - 1));
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Xn + S2, S, S2, Cn, S, S2, 0.0, XCn + S2, S, S2, nb - 1));
+    // WT_k = (Sinv_k Up_k)^T = Up_k^T Sinv_k^T (row-contiguous W for the backward sweep)
+    BAMG_TRY(dgemm_batched_dev(ctx, true, true, S, S, S, 1.0, Upb, S, S2, Sib, S, S2, 0.0, Wb, S, S2, nb - 1));
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Upb, S, S2, Sib + S2, S, S2, 0.0, Vb_ + S2, S, S2,
+                               nb - 1));
+  }
+  BAMG_LAUNCH_GRID3(ctx, bt_transpose_blocks_kernel, dim3((S + 31) / 32, (S + 31) / 32, nb), dim3(32, 8), 0,
+                    (const double*)Xb, S, nb, XTb);
+  const BtB FB{Xb, XTb, Sib, Wb, Vb_};
+
+  // ---- null vectors of B (padded): z = backward W-sweep from the last
+  // block's right null vector, y = Lb^-T (0, ..., 0, left null of S_last)
+  double *z, *y, *t1, *t2, *t3, *scal;
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &z));
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &y));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t1));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t2));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t3));
+  BAMG_TRY(arena_get(ctx, 16, &scal));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(t1, 0, sizeof(double) * Np, ctx->stream));
+  {
+    SweepOp b{Wb, qz, 0, -1};
+    BAMG_TRY(bt_sweep(ctx, S, nb, b, t1, Np, z, Np, 1));
+  }
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(t1 + (size_t)(nb - 1) * S, ry, sizeof(double) * S, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+  {
+    SweepOp b{Xb, nullptr, +1, -1};
+    BAMG_TRY(bt_sweep(ctx, S, nb, b, t1, Np, y, Np, 1));
+  }
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, z, Np, Np, (double*)nullptr);
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, y, Np, Np, (double*)nullptr);
+
+  // ---- certificate: |B z|, |B^T y| at round-off; B G B x = B x
+  {
+    double *bz, *bty, *xr, *bx, *gbx, *bgbx;
+    BAMG_TRY(arena_get(ctx, (size_t)n, &bz));
+    BAMG_TRY(arena_get(ctx, (size_t)n, &bty));
+    BAMG_TRY(arena_get(ctx, (size_t)n, &xr));
+    BAMG_TRY(arena_get(ctx, (size_t)n, &bx));
+    BAMG_TRY(arena_get(ctx, (size_t)n, &gbx));
+    BAMG_TRY(arena_get(ctx, (size_t)n, &bgbx));
+    BAMG_TRY(spmm_dev(ctx, B, z + d.off, bz, 1));
+    BAMG_TRY(spmm_dev(ctx, Bt, y + d.off, bty, 1));
+    BAMG_LAUNCH(ctx, bt_norms2_kernel, 1, 256, 0, (const double*)bz, n, (const double*)B->val, (int)B->nnz, scal);
+    BAMG_LAUNCH(ctx, bt_norms2_kernel, 1, 256, 0, (const double*)bty, n, (const double*)bty, 0, scal + 4);
+    BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for(n, 256), 256, 0, xr, n, 0, 1, 4242u);
+    BAMG_TRY(spmm_dev(ctx, B, xr, bx, 1));
+    BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for(Np, 256), 256, 0, (const double*)bx, n, n, d.off, Np, 1, t1);
+    BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t1, t2, t3, 1, false));
+    BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for(n, 256), 256, 0, (const double*)t3, Np, d.off, n, 1, gbx, n);
+    BAMG_TRY(spmm_dev(ctx, B, gbx, bgbx, 1));
+    BAMG_LAUNCH(ctx, bt_diff2_kernel, 1, 256, 0, (const double*)bgbx, (const double*)bx, n, scal + 2);
+    double h[5];
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 5, h));
+    const double bf = std::sqrt(h[1]), tol = 1e-13 * bf / std::sqrt((double)n);
+    const bool cert = std::sqrt(h[0]) <= tol && std::sqrt(h[4]) <= tol && std::sqrt(h[2]) <= 1e-10 * std::sqrt(h[3]);
+    if (getenv("BAMG_DEBUG"))
+      fprintf(stderr, "[bamg] band coarsest n=%d S=%d nb=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e |BGBx-Bx|/|Bx|=%.3e -> %s\n",
+              n, S, nb, std::sqrt(h[0]), std::sqrt(h[4]), bf, std::sqrt(h[2]) / std::sqrt(h[3]),
+              cert ? "certified" : "dense path");
+    if (!cert) return 1;
+  }
+
+  // F Y: out_k = C_k Y_k + XC_k Y_{k-1};  F^T Y: out_k = C_k^T Y_k + XC_{k+1}^T Y_{k+1}
+  auto mul_F = [&](const double* Cc, const double* XC, const double* Yin, double* out, int pc) -> int {
+    BAMG_TRY(bt_blockdiag(ctx, S, Np, Cc, false, Yin, out, pc, 0, nb, 0));
+    return bt_blockdiag(ctx, S, Np, XC, false, Yin, out, pc, 1, nb - 1, -1, 1.0, 1.0);
+  };
+  auto mul_FT = [&](const double* Cc, const double* XC, const double* Yin, double* out, int pc) -> int {
+    BAMG_TRY(bt_blockdiag(ctx, S, Np, Cc, true, Yin, out, pc, 0, nb, 0));
+    // out_k += XC_{k+1}^T Y_{k+1}, k = 0 .. nb-2
+    if (nb < 2) return 0;
+    return dgemm_batched_dev(ctx, true, false, S, pc, S, 1.0, XC + S2, S, (int64_t)S2, Yin + S, Np, S, 1.0, out, Np,
+                             S, nb - 1);
+  };
+
+  // ---- K's unit null vectors: a0 ~ F_M^T y, b0 ~ F_N^T z (padded)
+  double *a0, *b0;
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &a0));
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &b0));
+  BAMG_TRY(mul_FT(Cm, XCm, y, a0, 1));
+  BAMG_TRY(mul_FT(Cn, XCn, z, b0, 1));
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, a0, Np, Np, (double*)nullptr);
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, b0, Np, Np, (double*)nullptr);
+
+  // ---- K^+ Y (trans: K^+T Y), padded N x p
+  double* pd;
+  BAMG_TRY(arena_get(ctx, (size_t)p, &pd));
+  auto kp_apply = [&](const double* Yin, double* Yout, bool trans) -> int {
+    const double* pre = trans ? b0 : a0;
+    const double* post = trans ? a0 : b0;
+    const int gg = grid_for((int64_t)Np * p, 256);
+    BAMG_LAUNCH(ctx, bt_coldot_kernel, p, 256, 0, Yin, Np, Np, pre, pd);
+    BAMG_LAUNCH(ctx, bt_rank1_kernel, gg, 256, 0, Yin, Np, Np, p, pre, (const double*)pd, t1, Np);
+    if (!trans) {
+      BAMG_TRY(mul_F(Cm, XCm, t1, t2, p));                               // F_M
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, false));     // G
+      BAMG_TRY(mul_FT(Cn, XCn, t1, t2, p));                              // F_N^T
+    } else {
+      BAMG_TRY(mul_F(Cn, XCn, t1, t2, p));                               // F_N
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, true));      // G^T
+      BAMG_TRY(mul_FT(Cm, XCm, t1, t2, p));                              // F_M^T
+    }
+    BAMG_LAUNCH(ctx, bt_coldot_kernel, p, 256, 0, (const double*)t2, Np, Np, post, pd);
+    BAMG_LAUNCH(ctx, bt_rank1_kernel, gg, 256, 0, (const double*)t2, Np, Np, p, post, (const double*)pd, Yout, Np);
+    return 0;
+  };
+
+  // ---- block subspace iteration on K^+ (dense_large.cu's iteration and stop rule)
+  double *Y, *Z, *Gs, *Ri, *tmp, *Vs, *sv;
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &Y));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &Z));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &tmp));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Gs));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Ri));
+  BAMG_TRY(arena_get(ctx, (size_t)p * p, &Vs));
+  BAMG_TRY(arena_get(ctx, (size_t)p, &sv));
+  BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for((int64_t)Np * p, 256), 256, 0, Y, Np, d.off, p, 12345u);
+  BAMG_TRY(dl_orthonormalize(ctx, Y, Np, p, Gs, Ri, tmp));
+  std::vector<double> prev(p, 0.0), cur(p, 0.0);
+  int iters = 0;
+  for (int blkit = 0; blkit < 100; ++blkit) {
+    for (int it = 0; it < 5; ++it) {
+      BAMG_TRY(kp_apply(Y, Z, true));
+      BAMG_TRY(dl_orthonormalize(ctx, Z, Np, p, Gs, Ri, tmp));
+      BAMG_TRY(kp_apply(Z, Y, false));
+      BAMG_TRY(dl_orthonormalize(ctx, Y, Np, p, Gs, Ri, tmp));
+    }
+    BAMG_TRY(kp_apply(Y, Z, true));
+    BAMG_TRY(jacobi_svd_public(ctx, Z, Np, p, Vs, sv));
+    iters += 5;
+    BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
+    std::vector<double> c2 = cur;
+    std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
+    double change = 0.0;
+    for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
+    prev = c2;
+    if (change < 1e-12) break;  // Ritz values settle into ~1e-15 rounding noise
+  }
+  // Rayleigh-Ritz: Z = K^+T Y, Jacobi: Z Vs = W diag(s); left vectors W, right Y Vs
+  BAMG_TRY(kp_apply(Y, Z, true));
+  BAMG_TRY(jacobi_svd_public(ctx, Z, Np, p, Vs, sv));
+  std::vector<double> sh(p);
+  BAMG_TRY(ctx_read_doubles(ctx, sv, p, sh.data()));
+  std::vector<int> order(p);
+  for (int q = 0; q < p; ++q) order[q] = q;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return sh[a] > sh[b] || (sh[a] == sh[b] && a < b); });
+  BAMG_TRY(dgemm_dev(ctx, false, false, Np, p, p, 1.0, Y, Np, Vs, p, 0.0, tmp, Np));
+  double *A, *Bv, *KB, *dots;
+  BAMG_TRY(arena_get(ctx, (size_t)Np * r, &A));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * r, &Bv));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &KB));
+  BAMG_TRY(arena_get(ctx, (size_t)r, &dots));
+  std::vector<double> sig_host(r);
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(A, a0, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Bv, b0, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  sig_host[0] = 0.0;
+  for (int j = 1; j < r; ++j) {
+    const int q = order[j - 1];
+    sig_host[j] = sh[q] > 0.0 ? 1.0 / sh[q] : INFINITY;
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(A + (size_t)j * Np, Z + (size_t)q * Np, sizeof(double) * Np,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Bv + (size_t)j * Np, tmp + (size_t)q * Np, sizeof(double) * Np,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  double smax = 0.0;
+  int ntiny = 0;
+  for (int j = 0; j < r; ++j) smax = fmax(smax, sig_host[j]);
+  for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
+  BAMG_REQUIRE(ctx, ntiny <= 1, "coarsest operator has more than one numerically-null triplet");
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+  // unit a, b -> u = F_M^-T a, v = F_N^-T b (M- / N-normalised); sign rule
+  // u^T B v >= 0 (bootstrap.py:262-263)
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, r, 256, 0, A, Np, Np, (double*)nullptr);
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, r, 256, 0, Bv, Np, Np, (double*)nullptr);
+  auto apply_FinvT = [&](const double* Cc, const double* Xf, double* Xio) -> int {
+    // F^-T = Lf^-T blockdiag(C^-T): block triangular solves, then the backward X^T sweep
+    BAMG_LAUNCH_GRID3(ctx, bt_trsv_lt_kernel, dim3(nb, r, 1), dim3(256), 0, Cc, S, Np, Xio, Np);
+    SweepOp b{Xf, nullptr, +1, -1};
+    return bt_sweep(ctx, S, nb, b, Xio, Np, Xio, Np, r);
+  };
+  BAMG_TRY(apply_FinvT(Cm, Xm, A));
+  BAMG_TRY(apply_FinvT(Cn, Xn, Bv));
+  double *Ua, *Vb;
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Ua));
+  BAMG_TRY(arena_get(ctx, (size_t)n * r, &Vb));
+  BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for((int64_t)n * r, 256), 256, 0, (const double*)A, Np, d.off, n, r, Ua, n);
+  BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for((int64_t)n * r, 256), 256, 0, (const double*)Bv, Np, d.off, n, r, Vb,
+              n);
+  for (int j = 0; j < r; ++j) BAMG_TRY(spmm_dev(ctx, B, Vb + (size_t)j * n, KB + (size_t)j * n, 1));
+  BAMG_LAUNCH(ctx, bt_pairdot_kernel, r, 256, 0, (const double*)Ua, (const double*)KB, n, n, dots);
+  BAMG_LAUNCH(ctx, bt_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, (const double*)Ua,
+              (const double*)Vb, (const double*)dots, n, n, r, U, V);
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
+
+  // ---- keep B's factor + null vectors for the V-cycle's coarsest solve
+  BandPinv* h = new BandPinv();
+  h->n = n;
+  h->N = Np;
+  h->S = S;
+  h->nb = nb;
+  h->off = d.off;
+  auto alloc = [&](size_t bytes, double** out) -> int {
+    void* q = nullptr;
+    if (cudaMalloc(&q, bytes) != cudaSuccess) return -1;
+    h->mem.push_back(q);
+    *out = static_cast<double*>(q);
+    return 0;
+  };
+  int rc = 0;
+  rc |= alloc(sizeof(double) * blk, &h->XT);
+  rc |= alloc(sizeof(double) * blk, &h->Sinv);
+  rc |= alloc(sizeof(double) * blk, &h->WT);
+  rc |= alloc(sizeof(double) * Np, &h->z);
+  rc |= alloc(sizeof(double) * Np, &h->y);
+  rc |= alloc(sizeof(double) * Np, &h->t1);
+  rc |= alloc(sizeof(double) * Np, &h->t2);
+  rc |= alloc(sizeof(double) * 4, &h->dots);
+  if (rc) {
+    band_pinv_free(h);
+    ctx->err = "band coarsest: allocation of the kept factor failed";
+    return -1;
+  }
+  for (auto pr : {std::make_pair(h->XT, (const double*)XTb), std::make_pair(h->Sinv, (const double*)Sib),
+                  std::make_pair(h->WT, (const double*)Wb)})
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(pr.first, pr.second, sizeof(double) * blk, cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(h->z, z, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(h->y, y, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  *keep = h;
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] band triplets n=%d S=%d nb=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n", n,
+            S, nb, p, iters, r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);
+  return 0;
+}
+
+// Development probe: time bt_sweep_kernel on random blocks (S, nb, p) with
+// the switches of SweepOp::dev; ms per sweep to *ms.
+extern "C" int bamg_band_sweep_probe(bamg_ctx* ctx, int S, int nb, int p, int reps, int dev, double* ms) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, S >= 32 && S <= BT_MAX_S && nb >= 1 && p >= 1 && p <= 48, "bad probe shape");
+  const size_t S2 = (size_t)S * S;
+  const int N = S * nb;
+  double *W, *u, *out;
+  BAMG_TRY(arena_get(ctx, S2 * nb, &W));
+  BAMG_TRY(arena_get(ctx, (size_t)N * p, &u));
+  BAMG_TRY(arena_get(ctx, (size_t)N * p, &out));
+  BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for((int64_t)S2 * nb, 256), 256, 0, W, (int)(S2 * nb), 0, 1, 7u);
+  BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for((int64_t)N * p, 256), 256, 0, u, N, 0, p, 9u);
+  SweepOp op{W, nullptr, 0, -1, dev};
+  BAMG_TRY(bt_sweep(ctx, S, nb, op, u, N, out, N, p));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, ctx->stream);
+  for (int i = 0; i < reps; ++i) BAMG_TRY(bt_sweep(ctx, S, nb, op, u, N, out, N, p));
+  cudaEventRecord(e1, ctx->stream);
+  BAMG_CHECK_CUDA(ctx, cudaEventSynchronize(e1));
+  float t = 0.f;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = t / reps;
+  return 0;
+}

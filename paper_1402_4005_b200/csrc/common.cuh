@@ -223,6 +223,16 @@ static inline cudaError_t bamg_launch_pdl(void (*kernel)(KArgs...), dim3 grid, d
     }                                                                           \
   } while (0)
 
+// Launch with a 3-D grid / 2-D block (no PDL attribute; accounting + error check).
+#define BAMG_LAUNCH_GRID3(ctx, kernel, grid3, block3, smem, ...)                \
+  do {                                                                          \
+    if ((ctx)->trace.on) trace_mark(ctx, #kernel);                              \
+    kernel<<<(grid3), (block3), (smem), (ctx)->stream>>>(__VA_ARGS__);          \
+    (ctx)->launches++;                                                          \
+    BAMG_CHECK_CUDA(ctx, cudaGetLastError());                                   \
+    if ((ctx)->trace.on) trace_mark(ctx, nullptr);                              \
+  } while (0)
+
 #define BAMG_TRY(expr)                                                          \
   do {                                                                          \
     int _rc = (expr);                                                           \

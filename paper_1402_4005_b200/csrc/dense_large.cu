@@ -1352,6 +1352,10 @@ static int orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, dou
 
 int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig);
 
+int dl_orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp) {
+  return orthonormalize(ctx, Y, n, p, G, Rinv, tmp);
+}
+
 // ---------------------------------------------- fused subspace iteration
 // `iters` steps of the block subspace iteration  Z = orth(K^+T Y),
 // Y = orth(K^+ Z)  in ONE cooperative launch (n <= SUB_MAX_N, p <= 32):
@@ -1912,6 +1916,7 @@ static int coarse_lu_build(bamg_ctx* ctx, const double* Bd, int n, CoarseLU& C, 
 // inverses and B's unit null vectors, plus the apply's scratch.
 struct bamg_coarse_lu {
   CoarseLU C;
+  BandPinv* band = nullptr;  // banded coarsest (band.cu): used instead of C when set
   double *z = nullptr, *y = nullptr;
   double *t = nullptr, *s1 = nullptr, *s2 = nullptr, *dots = nullptr;
   std::vector<void*> mem;
@@ -1956,6 +1961,7 @@ static int coarse_lu_keep(bamg_ctx* ctx, const CoarseLU& C, const double* z, con
 // x = B^+ b = (I - z z^T) B^g (I - y y^T) b: the V-cycle's coarsest solve
 // through the kept LU (two triangular solves, leaves one GEMV each)
 int coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, double* x) {
+  if (h->band) return band_pinv_apply(ctx, h->band, b, x);
   const int n = h->C.n, m = h->C.m;
   const int g = grid_for(n, 256);
   BAMG_LAUNCH(ctx, vec_coldot_kernel, 1, 256, 0, b, n, n, (const double*)h->y, h->dots);
@@ -1972,7 +1978,31 @@ extern "C" int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* h) {
   if (!h) return 0;
   cudaStreamSynchronize(ctx->stream);  // in-flight V-cycles may still read it
   for (void* q : h->mem) cudaFree(q);
+  band_pinv_free(h->band);
   delete h;
+  return 0;
+}
+
+// Banded coarsest level (band.cu): the r smallest generalized singular
+// triplets of (B, M, N) in U, V (n x r interleaved) and sigma, and the
+// V-cycle's pseudo-inverse of B in *lu_out.  Returns 1 when the operators are
+// not banded enough or the block factorisation is not certified (the caller
+// then takes the dense path).
+extern "C" int bamg_coarsest_band(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
+                                  const bamg_csr* N, int r, double* U, double* V, double* sigma,
+                                  bamg_coarse_lu** lu_out) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, B && Bt && M && N && lu_out, "null argument");
+  BAMG_REQUIRE(ctx, B->nrows == B->ncols && M->nrows == B->nrows && N->nrows == B->nrows, "shape mismatch");
+  BAMG_REQUIRE(ctx, r >= 1 && r <= B->nrows, "r out of range");
+  *lu_out = nullptr;
+  BandPinv* keep = nullptr;
+  const int rc = band_coarsest_triplets(ctx, B, Bt, M, N, r, U, V, sigma, &keep);
+  if (rc != 0) return rc;
+  bamg_coarse_lu* h = new bamg_coarse_lu();
+  h->C.n = B->nrows;
+  h->band = keep;
+  *lu_out = h;
   return 0;
 }
 

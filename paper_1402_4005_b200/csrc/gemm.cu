@@ -89,8 +89,13 @@ template <int BM, int BN, int WM, int WN, bool TA, bool TB>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     dgemm_tile_kernel(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
                       const double* __restrict__ B, int ldb, double beta, double* __restrict__ C, int ldc,
-                      int kchunk, double* __restrict__ part) {
+                      int kchunk, double* __restrict__ part, int64_t strA, int64_t strB, int64_t strC, int batched) {
   BAMG_PDL_PROLOGUE();
+  if (batched) {  // blockIdx.z selects the problem of a strided batch (split-k off)
+    A += strA * blockIdx.z;
+    B += strB * blockIdx.z;
+    C += strC * blockIdx.z;
+  }
   constexpr int NW_M = BM / WM, NW_N = BN / WN, NT = NW_M * NW_N * 32;
   constexpr int MT = WM / 8, NTL = WN / 8;
   constexpr int LA = BM + 4, LB = BN + 4;
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   double* sA = smem;                          // STAGES x BK x LA
   double* sB = smem + STAGES * BK * LA;       // STAGES x BK x LB
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int kb = blockIdx.z * kchunk;
+  const int kb = batched ? 0 : blockIdx.z * kchunk;
   const int ke = min(k, kb + kchunk);
   const int KT = ke > kb ? (ke - kb + BK - 1) / BK : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -258,7 +263,8 @@ constexpr size_t tile_smem() {
 
 template <int BM, int BN, int WM, int WN, bool TA, bool TB>
 int launch_tiles(bamg_ctx* ctx, int m, int n, int k, double alpha, const double* A, int lda, const double* B,
-                 int ldb, double beta, double* C, int ldc) {
+                 int ldb, double beta, double* C, int ldc, int batch = 1, int64_t sA = 0, int64_t sB = 0,
+                 int64_t sC = 0) {
   auto kern = dgemm_tile_kernel<BM, BN, WM, WN, TA, TB>;
   constexpr size_t smem = tile_smem<BM, BN>();
   BAMG_TRY(smem_optin(ctx, (const void*)kern, smem));
@@ -269,19 +275,25 @@ int launch_tiles(bamg_ctx* ctx, int m, int n, int k, double alpha, const double*
   // keeps >= 512 of k; the partials are reduced in fixed order
   int splits = 1;
   const int want = 2 * ctx->num_sms;
-  if (tiles < want && k >= 1024) {
+  if (batch == 1 && tiles < want && k >= 1024) {
     splits = (int)std::min<int64_t>((want + tiles - 1) / tiles, k / 512);
     splits = std::max(1, std::min(splits, 64));
   }
   int kchunk = (k + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   splits = k > 0 ? (k + kchunk - 1) / kchunk : 1;
+  if (batch > 1) {
+    splits = 1;
+    kchunk = k;
+  }
   double* part = nullptr;
   if (splits > 1) BAMG_TRY(arena_get(ctx, (size_t)splits * m * n, &part));
-  ctx->prof.flops[FAM_DENSE] += 2.0 * m * n * (double)k;
+  ctx->prof.flops[FAM_DENSE] += 2.0 * m * n * (double)k * batch;
+  const int gz = batch > 1 ? batch : splits;
+  const int bflag = batch > 1 ? 1 : 0;
   if (bamg_pdl_enabled()) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(gm, gn, splits);
+    cfg.gridDim = dim3(gm, gn, gz);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
@@ -291,11 +303,12 @@ int launch_tiles(bamg_ctx* ctx, int m, int n, int k, double alpha, const double*
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (ctx->trace.on) trace_mark(ctx, "dgemm_tile_kernel");
-    BAMG_CHECK_CUDA(ctx, cudaLaunchKernelEx(&cfg, kern, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part));
+    BAMG_CHECK_CUDA(ctx, cudaLaunchKernelEx(&cfg, kern, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part,
+                                            sA, sB, sC, bflag));
   } else {
     if (ctx->trace.on) trace_mark(ctx, "dgemm_tile_kernel");
-    kern<<<dim3(gm, gn, splits), NT, smem, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk,
-                                                          part);
+    kern<<<dim3(gm, gn, gz), NT, smem, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part,
+                                                      sA, sB, sC, bflag);
   }
   ctx->launches++;
   BAMG_CHECK_CUDA(ctx, cudaGetLastError());
@@ -310,11 +323,19 @@ int launch_tiles(bamg_ctx* ctx, int m, int n, int k, double alpha, const double*
 
 template <int BM, int BN, int WM, int WN>
 int dispatch_tiles(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
-                   const double* B, int ldb, double beta, double* C, int ldc) {
-  if (!ta && !tb) return launch_tiles<BM, BN, WM, WN, false, false>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  if (ta && !tb) return launch_tiles<BM, BN, WM, WN, true, false>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  if (!ta && tb) return launch_tiles<BM, BN, WM, WN, false, true>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  return launch_tiles<BM, BN, WM, WN, true, true>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+                   const double* B, int ldb, double beta, double* C, int ldc, int batch = 1, int64_t sA = 0,
+                   int64_t sB = 0, int64_t sC = 0) {
+  if (!ta && !tb)
+    return launch_tiles<BM, BN, WM, WN, false, false>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, batch, sA, sB,
+                                                      sC);
+  if (ta && !tb)
+    return launch_tiles<BM, BN, WM, WN, true, false>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, batch, sA, sB,
+                                                     sC);
+  if (!ta && tb)
+    return launch_tiles<BM, BN, WM, WN, false, true>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, batch, sA, sB,
+                                                     sC);
+  return launch_tiles<BM, BN, WM, WN, true, true>(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, batch, sA, sB,
+                                                  sC);
 }
 
 // y (len rows, stride incy) = alpha op(M) x + beta y, op(M) rows x cols
@@ -356,9 +377,23 @@ int dgemm_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha
     return gemv(ctx, ta, m, k, alpha, A, lda, B, tb ? ldb : 1, beta, C, 1);
   if (m == 1)  // C(0, j) = sum_p op(A)(0, p) op(B)(p, j): op(B)^T a
     return gemv(ctx, !tb, n, k, alpha, B, ldb, A, ta ? 1 : lda, beta, C, ldc);
-  if (m <= 64 || n <= 64)
+  // 128 x 128 tiles only when they fill the GPU; small products on 64 x 32
+  // tiles (more CTAs, shorter serial k loops per SM)
+  const int64_t big_tiles = (int64_t)((m + 127) / 128) * ((n + 127) / 128);
+  if (m <= 64 || n <= 64 || big_tiles < ctx->num_sms)
     return dispatch_tiles<64, 32, 32, 16>(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
   return dispatch_tiles<128, 128, 32, 64>(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+// Strided batch of `batch` independent products C_i = alpha op(A_i) op(B_i) +
+// beta C_i (X_i = X + i * sX): one launch, blockIdx.z = i.
+int dgemm_batched_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+                      int64_t sA, const double* B, int ldb, int64_t sB, double beta, double* C, int ldc, int64_t sC,
+                      int batch) {
+  if (m <= 0 || n <= 0 || batch <= 0) return 0;
+  if (batch == 1) return dgemm_dev(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  BAMG_REQUIRE(ctx, k > 0, "batched GEMM needs k > 0");
+  return dispatch_tiles<64, 32, 32, 16>(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, batch, sA, sB, sC);
 }
 
 // C ABI (tests / tools): device pointers, stream-ordered on the context.

@@ -32,6 +32,22 @@ int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value
 // C = alpha op(A) op(B) + beta C, column-major fp64 (gemm.cu)
 int dgemm_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
               const double* B, int ldb, double beta, double* C, int ldc);
+// strided batch: C_i = alpha op(A_i) op(B_i) + beta C_i, X_i = X + i * sX
+int dgemm_batched_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+                      int64_t sA, const double* B, int ldb, int64_t sB, double beta, double* C, int ldc, int64_t sC,
+                      int batch);
+
+// CholQR2 orthonormalisation of an n x p column-major block (dense_large.cu)
+int dl_orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp);
+// one-sided Jacobi SVD of an nrows x ncols block (dense.cu)
+int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig);
+
+// banded coarsest level (band.cu)
+struct BandPinv;
+int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
+                           const bamg_csr* N, int r, double* U, double* V, double* sigma, BandPinv** keep);
+int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x);
+void band_pinv_free(BandPinv* h);
 
 struct bamg_coarse_lu;
 // x = B^+ b through the kept coarsest LU (dense_large.cu)

@@ -407,6 +407,22 @@ def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
     return U, V, s, (Z if (Z is not None and ok.value) else None)
 
 
+def coarsest_triplets_band(B: DeviceCSR, Bt: DeviceCSR, M: DeviceCSR, N: DeviceCSR, r):
+    """(U, V, sigma, CoarseLU) from the block-tridiagonal factorisations of the
+    CSR operators (bamg_coarsest_band), or None when the level is not banded
+    enough or the factorisation was not certified (dense path then)."""
+    n = B.shape[0]
+    take = min(r, n)
+    U = _empty((n, take))
+    V = _empty((n, take))
+    s = _empty(take)
+    lu = C.c_void_p()
+    rc = _lib.call("bamg_coarsest_band", B.ref(), Bt.ref(), M.ref(), N.ref(), take, _p(U), _p(V), _p(s), C.byref(lu))
+    if rc != 0 or not lu.value:
+        return None
+    return U, V, s, CoarseLU(lu, n)
+
+
 def sign_fix_l1(x, stride=1, uniform_fallback=False):
     n = x.shape[0]
     out = _empty(n)

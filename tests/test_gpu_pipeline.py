@@ -177,3 +177,33 @@ def test_large_coarsest_path_matches(golden, name, panel_smem, monkeypatch):
     s_large = setup.triplets.sigmas
     s_small = ref.triplets.sigmas
     assert np.allclose(s_large, s_small, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["pipe_uniform63", "pipe_tandem32_k16_r30", "pipe2_tandem33_bamg2",
+                                  "pipe2_uniform33_bamg2"])
+def test_band_coarsest_path_matches(golden, name, monkeypatch):
+    """The block-tridiagonal coarsest path (csrc/band.cu; cfg4's 16,384-point
+    banded coarsest level) forced on small banded coarsest levels: same x0,
+    V-cycle, x and iteration count as the reference, and the same smallest
+    singular values as the small dense path."""
+    from paper_1402_4005_b200 import GmresConfig, VCycleOperator, engine, gmres, run_setup
+    from paper_1402_4005_b200.solver import _sign_fix_l1
+    monkeypatch.setenv("BAMG_BAND_N", "16")
+    g = golden(name)
+    prob = _problem(g)
+    cfg = _setup_cfg(g)
+    injected = int(g["cfg_ints"][13]) >= 0
+    draws = (g["init_right_draw"], g["init_left_draw"]) if injected else None
+    setup = run_setup(prob, cfg, draws=draws)
+    assert isinstance(getattr(setup.hierarchy.coarsest, "coarse_pinv", None), engine.CoarseLU)
+    assert np.abs(setup.x0 - g["x0"]).sum() <= 1e-9
+    vop = VCycleOperator(setup.hierarchy, cfg.smoother)
+    assert _close(vop.apply(g["vcycle_in"]), g["vcycle_out"], 1e-9)
+    restart, max_iters, rtol = gmres_args(g)
+    rep = gmres(prob.B, np.zeros(prob.n), setup.x0, GmresConfig(restart=restart, max_iters=max_iters, rtol=rtol),
+                precond=vop)
+    assert abs(rep.iterations - int(g["iterations"])) <= max(1, int(0.1 * int(g["iterations"])))
+    assert np.abs(_sign_fix_l1(rep.x) - g["x"]).sum() <= 1e-8
+    monkeypatch.setenv("BAMG_BAND_N", "100000000")
+    ref = run_setup(prob, cfg, draws=draws)
+    assert np.allclose(setup.triplets.sigmas, ref.triplets.sigmas, rtol=1e-6, atol=1e-12)
