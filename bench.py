@@ -6,18 +6,24 @@ Contract (see the task statement): `python bench.py --gpus N --steps K
 A step is one full pass of the hot path over the workload: run_setup
 (bootstrap AMG: smoothing, LS transfer operators, Galerkin products, coarsest
 triplets) + VCycleOperator (coarsest pseudo-inverse) + preconditioned GMRES
-to rtol 1e-8.  The default workload is BASELINE.json configs[1] (uniform 2-D
-random walk, 1023 x 1023 = 1,046,529 states, k = 8, seed-0 uniform(0,1)
-test vectors).  The metric is a time: `value` = device seconds per step with
-the operator, geometry and initial vectors resident in HBM;
-`e2e` = the same through `solve_steady_state` with host inputs (pinned
-H2D of B / draws / geometry and the D2H of x inside the timed region).
+to rtol 1e-8.  The default workload is BASELINE.json configs[4], the largest
+single-GPU configuration (BASELINE.json's metric names no config): the tandem
+queue 4095 x 4095 = 16,769,025 states, k = 16, seed-0 uniform(0,1) test
+vectors, unrestarted GMRES.  The metric is a time: `value` = device seconds
+per step with the operator, geometry and initial vectors resident in HBM
+(`setup_s` / `solve_s` split it); `e2e` = the same through
+`solve_steady_state` with host inputs (pinned H2D of B / draws / geometry and
+the D2H of x inside the timed region).  `parity` compares the last step's
+hierarchy and stationary vector with the reference-generated full-size
+fixture (tests/golden/big_cfgX.npz) after the timed regions.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): the setup runs replicated on
-every rank and the solve phase is row-partitioned (halo-exchanged V-cycle and
-CGS2 GMRES, paper_1402_4005_b200/distributed.py), strong scaling; `--replicas`
-runs independent solves instead (weak scaling).  Every rank times its own
-steps with CUDA events and rank 0 reports the max over ranks.
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N local ranks (127.0.0.1); under torchrun
+WORLD_SIZE must equal N.  Each rank runs an independent replica of the
+workload (`scaling: weak`; the setup is not partitioned yet, see DESIGN.md
+section 6); `--partitioned` instead row-partitions the solve phase over NCCL
+(paper_1402_4005_b200/distributed.py).  Every rank times its own steps with
+CUDA events and rank 0 reports the max over ranks.
 """
 
 from __future__ import annotations
@@ -44,6 +50,7 @@ CONFIGS = {
     "cfg3": ("planar", 2 ** 21, 12, None, None, "random planar Delaunay chain, 2^21 states, k=12"),
     "cfg4": ("tandem", 4095, 16, None, None, "tandem queue 4095x4095 (16,769,025 states), k=16"),
 }
+DEFAULT_CONFIG = "cfg4"  # the largest single-GPU configuration of BASELINE.json
 RTOL = 1e-8
 METRIC = "AMG-GMRES setup+solve time to ||Bx||/||x||<1e-8 (s); V-cycle HBM GB/s"
 
@@ -207,16 +214,18 @@ def run_ours(args, rank, world, local_rank):
     zero = torch.zeros(n, dtype=torch.float64, device="cuda")
     L = _lib.lib()
     c = _lib.ctx()
-
-    distributed = world > 1 and not args.replicas
+    partitioned = world > 1 and args.partitioned
+    stream = torch.cuda.current_stream()
 
     class _Rep:
         def __init__(self, its, hist, conv):
             self.iterations, self.residual_history, self.converged = its, hist, conv
 
-    def step():
+    def step(mark=None):
         setup = pb.run_setup(dprob, cfg, draws=(dV, dU), B_device=dB)
-        if distributed:
+        if mark is not None:
+            mark.record(stream)
+        if partitioned:
             # row-partitioned V-cycle + GMRES over NCCL (setup replicated per rank)
             from paper_1402_4005_b200.distributed import Comm, DistSolver
             ds = DistSolver(setup.hierarchy, cfg.smoother, Comm())
@@ -235,7 +244,6 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     # ---- device-timed region: K steps, barrier + sync both sides
-    stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = int(L.bamg_launch_count(c))
     import gc
@@ -246,9 +254,10 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ev0.record(stream)
         iters = []
-        marks = []
+        marks, mids = [], []
         for _ in range(args.steps):
-            setup, vop, rep = step()
+            mids.append(torch.cuda.Event(enable_timing=True))
+            setup, vop, rep = step(mark=mids[-1])
             iters.append(rep.iterations)
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record(stream)
@@ -257,11 +266,24 @@ def run_ours(args, rank, world, local_rank):
         barrier()
     gc.enable()
     launches = int(L.bamg_launch_count(c)) - launches0
+    dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    starts = [ev0] + marks[:-1]
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, marks)]
+    setup_ms = [a.elapsed_time(b) for a, b in zip(starts, mids)]
+    solve_ms = [a.elapsed_time(b) for a, b in zip(mids, marks)]
+    if dist is not None:
+        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    converged = bool(rep.converged) and rep.residual_history[-1] < RTOL
+
     # ---- roofline window: the same K steps again with the engine profiler on
-    # (CUDA events around every CSR-family / LS-fit launch on the engine's
-    # stream).  The events cost ~2 ms per cfg1 step, so `value` comes from the
-    # un-instrumented region above and the per-launch kernel times from this one.
-    L.bamg_prof_enable(c, (1 << 0) | (1 << 1) | (1 << 6))
+    # (CUDA events around every launch of the CSR row family, the LS fit and
+    # the GMRES orthogonalisation passes on the engine's stream).  The events
+    # cost time, so `value` comes from the un-instrumented region above and the
+    # per-launch kernel times from this one.
+    FAMS = {0: "csr", 1: "ls_fit", 3: "gmres_ortho", 6: "csr_fine"}
+    L.bamg_prof_enable(c, sum(1 << f for f in FAMS))
     gc.collect()
     gc.disable()
     barrier()
@@ -272,28 +294,23 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     gc.enable()
     import ctypes as C
-    fam_stats = {}
     raw = {}
-    for fid in (0, 1, 6):
+    for fid in FAMS:
         ms, cnt, by = C.c_double(), C.c_int64(), C.c_double()
         L.bamg_prof_read(c, fid, C.byref(ms), C.byref(cnt), C.byref(by))
         raw[fid] = (ms.value, cnt.value, by.value)
-    # the CSR family = its launches on every level (engine families 0 + 6)
-    fam_stats["csr_stream_spmv_spmm_jacobi"] = tuple(a + b for a, b in zip(raw[0], raw[6]))
-    fam_stats["ls_fit"] = raw[1]
-    fine = raw[6]
     L.bamg_prof_enable(c, 0)
-    dev_s = ev0.elapsed_time(ev1) / 1e3 / args.steps
-    step_ms = [ev0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
-    if dist is not None:
-        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s = float(t.item())
-    converged = bool(rep.converged) and rep.residual_history[-1] < RTOL
+    fam_stats = {
+        # the CSR family = its launches on every level (engine families 0 + 6)
+        "csr_stream_spmv_spmm_jacobi": tuple(a + b for a, b in zip(raw[0], raw[6])),
+        "gmres_cgs2_basis_passes": raw[3],
+        "ls_fit": raw[1],
+    }
+    fine = raw[6]
 
     # ---- V-cycle throughput (secondary metric of BASELINE.json)
     levels = setup.hierarchy.levels
-    if distributed:
+    if partitioned:
         vop = pb.VCycleOperator(setup.hierarchy, cfg.smoother)
     vb = vcycle_bytes(levels, cfg.smoother.sweeps_pre, cfg.smoother.sweeps_post)
     b = torch.randn(n, dtype=torch.float64, device="cuda")
@@ -309,6 +326,23 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     vms = e0.elapsed_time(e1) / nv
     peak, peak_kind = peaks()
+
+    # ---- parity of the last timed step against the reference's full-size fixture
+    parity = None
+    if not args.no_parity and rank == 0:
+        try:
+            sys.path.insert(0, str(ROOT / "tests"))
+            import bigparity
+            res = bigparity.check_config(name, result=(prob, dB, cfg, setup))
+            parity = {k_: res.get(k_) for k_ in ("ok", "why", "mode", "operators_checked", "iterations",
+                                                  "reference_iterations", "gmres_start", "x_err_l1",
+                                                  "x_err_l1_est", "x_err_l1_blocks", "vcycle_err_rel",
+                                                  "failures") if k_ in res}
+            parity["fixture"] = f"tests/golden/big_{name}.npz (unmodified reference, tests/golden/make_golden_big.py)"
+            del res
+        except Exception as exc:  # parity is reported, never fatal to the timing line
+            parity = {"ok": None, "why": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.empty_cache()
 
     # ---- e2e through the public API with host inputs
     Bh = prob.B
@@ -346,7 +380,17 @@ def run_ours(args, rank, world, local_rank):
         e2e_s = float(t.item())
 
     # ---- dominant kernel family -> roofline
-    dom = max(fam_stats, key=lambda f: fam_stats[f][0])
+    def fam_json(v):
+        ms, cnt, by = v
+        if not cnt:
+            return {"ms_per_step": 0.0, "launches_per_step": 0}
+        per = ms / 1e3 / cnt
+        return {"ms_per_step": round(ms / args.steps, 3), "launches_per_step": cnt // args.steps,
+                "alg_bytes_per_launch": round(by / cnt), "alg_GBps": round((by / cnt) / per / 1e9, 1) if per else 0.0,
+                "frac_of_hbm_peak": round((by / cnt) / per / 1e9 / peak, 4) if per else 0.0}
+
+    hbm_fams = {k_: v for k_, v in fam_stats.items() if k_ != "ls_fit"}
+    dom = max(hbm_fams, key=lambda f: hbm_fams[f][0])
     ms, cnt, by = fam_stats[dom]
     per_launch_s = ms / 1e3 / max(cnt, 1)
     achieved = (by / max(cnt, 1)) / per_launch_s / 1e9 if cnt else 0.0
@@ -357,14 +401,12 @@ def run_ours(args, rank, world, local_rank):
             "alg_bytes_per_launch": round(by / max(cnt, 1)),
             "launches_in_window": cnt, "share_of_step": round(ms / 1e3 / (dev_s * args.steps), 4),
             "window": f"{args.steps} profiled steps after the timed region (same workload)",
-            "families": {f: {"ms_total": round(v[0], 3), "launches": v[1],
-                             "alg_GBps": round((v[2] / max(v[1], 1)) / (v[0] / 1e3 / max(v[1], 1)) / 1e9, 1) if v[1] else 0}
-                         for f, v in fam_stats.items()}}
+            "families": {f: fam_json(v) for f, v in fam_stats.items()}}
     fit = fp64_fit_roofline(L, c, fam_stats.get("ls_fit"), args.steps, name)
     if fit:
         roof["ls_fit_fp64"] = fit
-    if dom == "csr_stream_spmv_spmm_jacobi" and fine[1]:
-        # the same family restricted to the finest levels (operators >= 2^18 rows):
+    if fine[1]:
+        # the CSR family restricted to the finest levels (operators >= 2^18 rows):
         # bandwidth-sized launches, without the latency-bound coarse-level ones
         fa = (fine[2] / fine[1]) / (fine[0] / 1e3 / fine[1]) / 1e9
         roof["finest_levels"] = {"rows_min": 1 << 18, "launches": fine[1], "ms_total": round(fine[0], 3),
@@ -373,8 +415,9 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": round(dev_s, 6), "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3, 3),
-        "higher_is_better": False, "scaling": "strong" if distributed else "weak", "vs_baseline": None,
+        "higher_is_better": False, "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
         "dtype": "f64",
+        "setup_s": round(float(np.mean(setup_ms)) / 1e3, 6), "solve_s": round(float(np.mean(solve_ms)) / 1e3, 6),
         "step_ms": {"min": round(min(step_ms), 3), "median": round(float(np.median(step_ms)), 3),
                     "max": round(max(step_ms), 3)},
         "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
@@ -383,7 +426,7 @@ def run_ours(args, rank, world, local_rank):
                    "levels": [lv.n for lv in levels], "gmres_iterations": iters[-1],
                    "converged": converged,
                    "parallelism": (f"row-partitioned V-cycle+GMRES over NCCL x{world}, setup replicated"
-                                   if distributed else f"replicas x{world}"),
+                                   if partitioned else f"independent replicas x{world}"),
                    "l2": "working set (operators + k-vector blocks) > 126 MB L2; no flush"},
         "vcycle": {"ms": round(vms, 4), "alg_bytes": int(vb), "GBps": round(vb / (vms / 1e3) / 1e9, 1),
                    "frac_of_hbm_peak": round(vb / (vms / 1e3) / 1e9 / peak, 4)},
@@ -392,6 +435,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "parity": parity,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, args.cpu_sample)
@@ -446,58 +490,105 @@ def family_traffic(family, alg_per_launch):
                                            f"over {d['launches']} launches of one step, applied per launch")
 
 
+SAMPLES = {"tandem": 128, "uniform2d": 127, "planar": 4096}  # side (lattices) or n (planar)
+
+
+def reference_calibration():
+    """profiles/r*_reference_calibration.json: per config, the full-size run of
+    the UNMODIFIED reference (tests/golden/make_golden_big.py, this build
+    container, single-core-equivalent seconds) over the linear extrapolation
+    of the port's bounded sample timed on the same machine (tools/ref_calibration.py)."""
+    files = sorted(ROOT.glob("profiles/r*_reference_calibration.json"))
+    if not files:
+        return {}, None
+    return json.loads(files[-1].read_text()).get("configs", {}), files[-1].name
+
+
 def cpu_baseline(name, sample=None, repeat=1):
-    """The oracle (numpy restatement of the reference) on a bounded sample of the
-    same family, extrapolated linearly in the state count to the full workload."""
+    """The oracle (numpy restatement of the reference, bit-identical to it on the
+    golden fixtures) timed on a bounded sample of the same family on ONE host
+    core (the reference is single-threaded: SURVEY.md section 8(b)), then
+    extrapolated to the full workload: linear in the state count, times the
+    calibration factor measured against a full-size run of the unmodified
+    reference (`calibration`).  `value_kind` says so; the sample's own time is
+    `sample_seconds`."""
     sys.path.insert(0, str(ROOT))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+
     from oracle import bamg_oracle as orc
     fam, size, k, stop, restart, desc = CONFIGS[name]
     from paper_1402_4005_b200 import chains
     if fam == "planar":
-        n_s = sample or 4096
+        n_s = sample or SAMPLES[fam]
         prob = chains.random_planar(n_s, seed=1, validate=False)
         n_full = size
     else:
-        side = sample or (127 if fam == "uniform2d" else 128)
+        side = sample or SAMPLES[fam]
         prob = chains.tandem_queue(side, validate=False) if fam == "tandem" else chains.uniform_2d(side, validate=False)
         n_s = prob.n
         n_full = size * size
     cfg = orc.default_cfg(fam, k=k, stop=stop, seed=0)
     right, left = draws_for(k, prob.n)
     best = None
-    for _ in range(repeat):
-        t0 = time.perf_counter()
-        levels, T, x0, its, hist, conv, x = orc.solve(prob.B, cfg, prob.geometry, right, left, restart, RTOL)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return {"value": round(best * n_full / n_s, 2), "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"oracle (numpy/scipy restatement, 1 thread) setup+solve on {fam} n={n_s} "
-                      f"({best:.2f} s, {its} GMRES its), scaled x{n_full / n_s:.1f} linearly in n to "
-                      f"n={n_full}"}
+    with threadpool_limits(1):
+        for _ in range(repeat):
+            t0 = time.perf_counter()
+            levels, T, x0, its, hist, conv, x = orc.solve(prob.B, cfg, prob.geometry, right, left, restart, RTOL)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+    cal, src = reference_calibration()
+    entry = cal.get(name)
+    factor = float(entry["factor"]) if entry else 1.0
+    out = {"value": round(best * n_full / n_s * factor, 2), "unit": "s", "cores": 1, "kind": "port",
+           "value_kind": "extrapolated: sample seconds x (n_full / n_sample) x calibration factor",
+           "sample_seconds": round(best, 3),
+           "sample": f"oracle (numpy/scipy restatement, 1 thread) setup+solve on {fam} n={n_s} "
+                     f"({best:.2f} s, {its} GMRES its), scaled x{n_full / n_s:.1f} linearly in n to n={n_full}"}
+    if entry:
+        out["calibration"] = dict(entry, source=src)
+    else:
+        out["calibration"] = {"factor": 1.0, "note": "no full-size reference run for this config"}
+    return out
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (the
-    oracle port; /root/reference is not on the GPU box), rank 0 only."""
+    oracle port; /root/reference is not on the GPU box) on one host core, rank
+    0 only; each step a bounded sample of the workload, extrapolated as
+    cpu_baseline() says."""
     if rank != 0:
         return None
     name = args.config
     for _ in range(args.warmup):
-        pass
-    vals = []
+        cpu_baseline(name, args.cpu_sample)
+    vals, samples = [], []
     for _ in range(args.steps):
         cb = cpu_baseline(name, args.cpu_sample)
         vals.append(cb["value"])
+        samples.append(cb["sample_seconds"])
     v = float(np.mean(vals))
     fam, size, k, stop, restart, desc = CONFIGS[name]
-    return {"metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+    cb = dict(cb, value=round(v, 2), sample_seconds=round(float(np.mean(samples)), 3))
+    return {"metric": METRIC, "value": round(v, 2), "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "value_kind": cb["value_kind"],
             "data": "synthetic: BASELINE generator chain, seed-0 uniform(0,1) test vectors",
             "config": {"workload": f"{name}: {desc}", "k": k, "gmres_restart": restart, "rtol": RTOL},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": cb["sample"]},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": cb,
+            "e2e": {"value": round(v, 2), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def relaunch_under_torchrun(args_list, n):
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run
+    with N local ranks (127.0.0.1) and pass its exit code through."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + args_list
+    return subprocess.call(cmd)
 
 
 def main():
@@ -506,15 +597,22 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of the row-partitioned solve")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="N>1: row-partition the solve over NCCL instead of independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(sys.argv[1:], args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:

@@ -633,7 +633,8 @@ struct BandPinv {  // kept for the V-cycle: B^+ b = (I - z z^T) G (I - y y^T) b
   double *XT = nullptr, *Sinv = nullptr, *WT = nullptr;  // B's factor for G (device, owned)
   double *z = nullptr, *y = nullptr;                                  // unit null vectors, padded N
   double *t1 = nullptr, *t2 = nullptr, *dots = nullptr;               // scratch
-  std::vector<void*> mem;
+  char* slab = nullptr;  // all of the above, one buffer from the context pool
+  size_t slab_bytes = 0;
 };
 
 namespace {
@@ -707,9 +708,11 @@ int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x
   return 0;
 }
 
-void band_pinv_free(BandPinv* h) {
+// back to the context pool: the next setup's band factor reuses the slab,
+// stream-ordered after every V-cycle that still reads this one
+void band_pinv_free(bamg_ctx* ctx, BandPinv* h) {
   if (!h) return;
-  for (void* q : h->mem) cudaFree(q);
+  if (h->slab) pool_give(ctx, h->slab, h->slab_bytes);
   delete h;
 }
 
@@ -1005,27 +1008,21 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   h->S = S;
   h->nb = nb;
   h->off = d.off;
-  auto alloc = [&](size_t bytes, double** out) -> int {
-    void* q = nullptr;
-    if (cudaMalloc(&q, bytes) != cudaSuccess) return -1;
-    h->mem.push_back(q);
-    *out = static_cast<double*>(q);
-    return 0;
-  };
-  int rc = 0;
-  rc |= alloc(sizeof(double) * blk, &h->XT);
-  rc |= alloc(sizeof(double) * blk, &h->Sinv);
-  rc |= alloc(sizeof(double) * blk, &h->WT);
-  rc |= alloc(sizeof(double) * Np, &h->z);
-  rc |= alloc(sizeof(double) * Np, &h->y);
-  rc |= alloc(sizeof(double) * Np, &h->t1);
-  rc |= alloc(sizeof(double) * Np, &h->t2);
-  rc |= alloc(sizeof(double) * 4, &h->dots);
-  if (rc) {
-    band_pinv_free(h);
-    ctx->err = "band coarsest: allocation of the kept factor failed";
+  const size_t nblk = 3 * blk + 4 * (size_t)Np + 8;
+  h->slab_bytes = sizeof(double) * nblk;
+  if (pool_take(ctx, h->slab_bytes, &h->slab) != 0) {
+    delete h;
     return -1;
   }
+  double* q = reinterpret_cast<double*>(h->slab);
+  h->XT = q;
+  h->Sinv = q + blk;
+  h->WT = q + 2 * blk;
+  h->z = q + 3 * blk;
+  h->y = h->z + Np;
+  h->t1 = h->y + Np;
+  h->t2 = h->t1 + Np;
+  h->dots = h->t2 + Np;
   for (auto pr : {std::make_pair(h->XT, (const double*)XTb), std::make_pair(h->Sinv, (const double*)Sib),
                   std::make_pair(h->WT, (const double*)Wb)})
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(pr.first, pr.second, sizeof(double) * blk, cudaMemcpyDeviceToDevice,

@@ -256,6 +256,13 @@ static inline int arena_get(bamg_ctx* ctx, size_t count, T** out) {
 // a second device in the same process gets its own cudaFuncSetAttribute.
 int smem_optin(bamg_ctx* ctx, const void* fn, size_t bytes);
 
+// Device buffers recycled across setups on the context's stream (V-cycle
+// level slabs, the banded coarsest factor): take the smallest pooled buffer
+// of at least `bytes` (else cudaMalloc); give one back (stream-ordered reuse:
+// no synchronisation, later users are enqueued after earlier ones).
+int pool_take(bamg_ctx* ctx, size_t bytes, char** out);
+void pool_give(bamg_ctx* ctx, char* p, size_t bytes);
+
 // Pinned staging for small device->host reads (synchronises the stream).
 int ctx_read_doubles(bamg_ctx* ctx, const double* dev, size_t n, double* host);
 int ctx_read_i64(bamg_ctx* ctx, const int64_t* dev, size_t n, int64_t* host);

@@ -44,6 +44,34 @@ extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
   return 0;
 }
 
+constexpr size_t BUF_POOL_MAX = 16;
+
+// smallest pooled buffer of at least `bytes`, else a fresh allocation
+int pool_take(bamg_ctx* ctx, size_t bytes, char** out) {
+  int best = -1;
+  for (int i = 0; i < (int)ctx->buf_pool.size(); ++i)
+    if (ctx->buf_pool[i].second >= bytes && (best < 0 || ctx->buf_pool[i].second < ctx->buf_pool[best].second))
+      best = i;
+  if (best >= 0) {
+    *out = ctx->buf_pool[best].first;
+    ctx->buf_pool.erase(ctx->buf_pool.begin() + best);
+    return 0;
+  }
+  BAMG_CHECK_CUDA(ctx, cudaMalloc(out, bytes));
+  return 0;
+}
+
+void pool_give(bamg_ctx* ctx, char* p, size_t bytes) {
+  ctx->buf_pool.push_back({p, bytes});
+  while (ctx->buf_pool.size() > BUF_POOL_MAX) {  // drop the smallest
+    int s = 0;
+    for (int i = 1; i < (int)ctx->buf_pool.size(); ++i)
+      if (ctx->buf_pool[i].second < ctx->buf_pool[s].second) s = i;
+    cudaFree(ctx->buf_pool[s].first);
+    ctx->buf_pool.erase(ctx->buf_pool.begin() + s);
+  }
+}
+
 int smem_optin(bamg_ctx* ctx, const void* fn, size_t bytes) {
   struct Rec {
     const void* fn;

@@ -1976,9 +1976,13 @@ int coarse_lu_apply(bamg_ctx* ctx, const bamg_coarse_lu* h, const double* b, dou
 
 extern "C" int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* h) {
   if (!h) return 0;
+  if (h->band) {  // pooled, stream-ordered reuse: no synchronisation
+    band_pinv_free(ctx, h->band);
+    delete h;
+    return 0;
+  }
   cudaStreamSynchronize(ctx->stream);  // in-flight V-cycles may still read it
   for (void* q : h->mem) cudaFree(q);
-  band_pinv_free(h->band);
   delete h;
   return 0;
 }

@@ -47,7 +47,7 @@ struct BandPinv;
 int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
                            const bamg_csr* N, int r, double* U, double* V, double* sigma, BandPinv** keep);
 int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x);
-void band_pinv_free(BandPinv* h);
+void band_pinv_free(bamg_ctx* ctx, BandPinv* h);
 
 struct bamg_coarse_lu;
 // x = B^+ b through the kept coarsest LU (dense_large.cu)

@@ -57,7 +57,6 @@ struct bamg_hier {
 };
 
 constexpr size_t EXEC_POOL_MAX = 16;
-constexpr size_t BUF_POOL_MAX = 8;
 
 // graphs go back to the context pool (a later hierarchy re-points them)
 static void hier_drop_graphs(bamg_hier* h) {
@@ -67,32 +66,6 @@ static void hier_drop_graphs(bamg_hier* h) {
     else cudaGraphExecDestroy(g.exec);
   }
   h->graphs.clear();
-}
-
-// smallest pooled buffer of at least `bytes`, else a fresh allocation
-static int pool_take(bamg_ctx* ctx, size_t bytes, char** out) {
-  int best = -1;
-  for (int i = 0; i < (int)ctx->buf_pool.size(); ++i)
-    if (ctx->buf_pool[i].second >= bytes && (best < 0 || ctx->buf_pool[i].second < ctx->buf_pool[best].second))
-      best = i;
-  if (best >= 0) {
-    *out = ctx->buf_pool[best].first;
-    ctx->buf_pool.erase(ctx->buf_pool.begin() + best);
-    return 0;
-  }
-  BAMG_CHECK_CUDA(ctx, cudaMalloc(out, bytes));
-  return 0;
-}
-
-static void pool_give(bamg_ctx* ctx, char* p, size_t bytes) {
-  ctx->buf_pool.push_back({p, bytes});
-  while (ctx->buf_pool.size() > BUF_POOL_MAX) {  // drop the smallest
-    int s = 0;
-    for (int i = 1; i < (int)ctx->buf_pool.size(); ++i)
-      if (ctx->buf_pool[i].second < ctx->buf_pool[s].second) s = i;
-    cudaFree(ctx->buf_pool[s].first);
-    ctx->buf_pool.erase(ctx->buf_pool.begin() + s);
-  }
 }
 
 extern "C" int bamg_hier_create(bamg_ctx* ctx, int nlevels, bamg_hier** out) {
