@@ -226,7 +226,13 @@ int bamg_fit_rows_csr(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_
                       int32_t* rowptr, int64_t* status_host, int64_t* nnz_host);
 /* Asynchronous bamg_fit_rows_csr into one of 4 slots (no host read), and the
  * ONE synchronisation that returns status (2 per slot) and nnz of the listed
- * slots: the P and W fits of a level share it. */
+ * slots: the P and W fits of a level share it.  Each slot call forks from the
+ * context stream at the call (everything enqueued before it, its inputs
+ * included, is ordered before the fit) onto the slot's own side stream with
+ * its own scratch; bamg_fit_rows_wait joins every pending slot back into the
+ * context stream.  Until then the caller must not enqueue work that reads a
+ * pending slot's outputs (out_cnt / out_col / out_val / rowptr) nor free
+ * them; other work, including other entry points, may run in between. */
 int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
                            const double* X, const double* w, int64_t n, int k, int caliber,
                            int radius, double improvement_tol, int constrain, int nonnegative,

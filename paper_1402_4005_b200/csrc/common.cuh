@@ -114,7 +114,16 @@ struct bamg_ctx {
   unsigned int* counters = nullptr;
   std::vector<std::pair<char*, size_t>> buf_pool;
   std::vector<cudaGraphExec_t> exec_pool;
+  // per-context state of the translation units, created on first use and
+  // released by bamg_ctx_destroy (no process-wide tables keyed by address)
+  struct FitSlots* fit_slots = nullptr;          // interp.cu
+  struct GmresWork* gmres_work = nullptr;        // solver.cu
+  struct SpgemmMemo* spgemm_memo = nullptr;      // spgemm.cu (SPG_SLOTS entries)
 };
+
+void fit_slots_release(bamg_ctx* ctx);
+void gmres_work_release(bamg_ctx* ctx);
+void spgemm_memo_release(bamg_ctx* ctx);
 
 static inline void trace_mark(bamg_ctx* ctx, const char* name) {
   KTrace& T = ctx->trace;

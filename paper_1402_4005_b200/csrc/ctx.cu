@@ -34,6 +34,9 @@ extern "C" int bamg_ctx_create(int device, void* cuda_stream, bamg_ctx** out) {
 extern "C" int bamg_ctx_destroy(bamg_ctx* ctx) {
   if (!ctx) return 0;
   cudaStreamSynchronize(ctx->stream);
+  fit_slots_release(ctx);
+  gmres_work_release(ctx);
+  spgemm_memo_release(ctx);
   ctx->arena.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->counters) cudaFree(ctx->counters);

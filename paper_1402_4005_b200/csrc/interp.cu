@@ -24,6 +24,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <utility>
+
 #include "internal.cuh"
 
 constexpr int FIT_WARPS = 4;     // warps per CTA
@@ -1359,34 +1361,56 @@ __global__ void rows_count_kernel(const int32_t* __restrict__ cnt, const double*
                                   int stride, int32_t* __restrict__ out);
 
 // Per-context state of asynchronous fits (bamg_fit_rows_csr_slot): status
-// words (4 slots x 4 words, read back together by bamg_fit_rows_wait) and one
-// side stream per slot > 0.  Slot 0 records a fork event before its launches;
-// slots 1..3 wait on it and run on their side streams, so the fits of a batch
-// (P and W of a level) overlap -- the coarse levels' fits are one serial
-// greedy chain per thread (35-60 us whatever the size), and run side by side
-// at the cost of one.  Each joins back into the main stream right after its
-// launches, so every later main-stream operation is ordered after it.
+// words (4 slots x 4 words, read back together by bamg_fit_rows_wait), one
+// side stream, fork / join event and scratch arena per slot.  Every slot call
+// records its OWN fork event on the main stream, so everything enqueued on
+// the main stream before the call (its inputs included) is ordered before the
+// slot's launches on its side stream; the fits of a batch (P and W of a
+// level) then overlap -- the coarse levels' fits are one serial greedy chain
+// per thread (35-60 us whatever the size) and run side by side at the cost
+// of one.  The joins are deferred to bamg_fit_rows_wait, which orders the
+// main stream after every pending slot before reading the status words.
+// Slots never touch the context arena (each has its own), so main-stream work
+// between slot calls -- including entry points that reset the arena -- is
+// safe; what must not happen before bamg_fit_rows_wait is main-stream work
+// that READS a pending slot's outputs.  While the stream is being captured
+// into a graph the slots run on the main stream.
 constexpr int FIT_SLOTS = 4;
 struct FitSlots {
   unsigned long long* status = nullptr;
   cudaStream_t side[FIT_SLOTS] = {};
-  cudaEvent_t fork = nullptr, join[FIT_SLOTS] = {};
-  bool forked = false;
+  cudaEvent_t fork[FIT_SLOTS] = {}, join[FIT_SLOTS] = {};
+  Arena arena[FIT_SLOTS];
+  bool pending[FIT_SLOTS] = {};
 };
+
 static FitSlots* fit_slots(bamg_ctx* ctx) {
-  static thread_local std::vector<std::pair<bamg_ctx*, FitSlots*>> table;
-  for (auto& e : table)
-    if (e.first == ctx) return e.second;
+  if (ctx->fit_slots) return ctx->fit_slots;
   FitSlots* fs = new FitSlots();
-  bool ok = cudaMalloc(&fs->status, sizeof(unsigned long long) * 4 * FIT_SLOTS) == cudaSuccess &&
-            cudaEventCreateWithFlags(&fs->fork, cudaEventDisableTiming) == cudaSuccess;
-  for (int s = 1; s < FIT_SLOTS && ok; ++s)
+  bool ok = cudaMalloc(&fs->status, sizeof(unsigned long long) * 4 * FIT_SLOTS) == cudaSuccess;
+  for (int s = 0; s < FIT_SLOTS && ok; ++s)
     ok = cudaStreamCreateWithFlags(&fs->side[s], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fs->fork[s], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&fs->join[s], cudaEventDisableTiming) == cudaSuccess;
-  if (!ok) return nullptr;
-  table.push_back({ctx, fs});
-  return fs;
+  ctx->fit_slots = fs;  // released (also when partially built) by fit_slots_release
+  return ok ? fs : nullptr;
 }
+
+void fit_slots_release(bamg_ctx* ctx) {
+  FitSlots* fs = ctx->fit_slots;
+  if (!fs) return;
+  for (int s = 0; s < FIT_SLOTS; ++s) {
+    if (fs->side[s]) cudaStreamSynchronize(fs->side[s]);
+    fs->arena[s].release();
+    if (fs->side[s]) cudaStreamDestroy(fs->side[s]);
+    if (fs->fork[s]) cudaEventDestroy(fs->fork[s]);
+    if (fs->join[s]) cudaEventDestroy(fs->join[s]);
+  }
+  if (fs->status) cudaFree(fs->status);
+  delete fs;
+  ctx->fit_slots = nullptr;
+}
+
 static unsigned long long* fit_slot_status(bamg_ctx* ctx) {
   FitSlots* fs = fit_slots(ctx);
   return fs ? fs->status : nullptr;
@@ -1419,27 +1443,35 @@ extern "C" int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const 
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   BAMG_CHECK_CUDA(ctx, cudaStreamIsCapturing(ctx->stream, &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
-  const bool side = slot > 0 && fs->forked && !capturing;
-  if (!side) {
-    // slot 0 (or a batch without one): scratch from a fresh arena, main stream
-    ctx->arena.reset();
-    if (slot == 0 && !capturing) {
-      BAMG_CHECK_CUDA(ctx, cudaEventRecord(fs->fork, ctx->stream));
-      fs->forked = true;
-    }
-    return fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
-                               nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st);
-  }
-  // later slot of the batch: the arena is NOT reset (its scratch follows the
-  // earlier slots'), inputs are ordered by the fork event
   cudaStream_t main = ctx->stream;
-  BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(fs->side[slot], fs->fork, 0));
-  ctx->stream = fs->side[slot];
+  Arena saved;
+  std::swap(saved, ctx->arena);  // the slot's scratch comes from its own arena
+  std::swap(ctx->arena, fs->arena[slot]);
+  if (!capturing) {
+    // the slot's previous use of its arena ran on its side stream: stream-ordered
+    ctx->arena.reset();
+    if (cudaEventRecord(fs->fork[slot], main) != cudaSuccess ||
+        cudaStreamWaitEvent(fs->side[slot], fs->fork[slot], 0) != cudaSuccess) {
+      std::swap(ctx->arena, fs->arena[slot]);
+      std::swap(saved, ctx->arena);
+      ctx->err = "fit slot fork failed";
+      return -1;
+    }
+    ctx->stream = fs->side[slot];
+  } else {
+    cudaStreamSynchronize(fs->side[slot]);  // no capture-time reset may overlap a side-stream user
+    ctx->arena.reset();
+  }
   int rc = fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
                                nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st);
   ctx->stream = main;
-  BAMG_CHECK_CUDA(ctx, cudaEventRecord(fs->join[slot], fs->side[slot]));
-  BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(main, fs->join[slot], 0));
+  std::swap(ctx->arena, fs->arena[slot]);
+  std::swap(saved, ctx->arena);
+  if (!capturing) {
+    // even after an error: the join keeps the main stream ordered after whatever was enqueued
+    cudaEventRecord(fs->join[slot], fs->side[slot]);
+    fs->pending[slot] = true;
+  }
   return rc;
 }
 
@@ -1448,7 +1480,11 @@ extern "C" int bamg_fit_rows_wait(bamg_ctx* ctx, int nslots, const int32_t* slot
   BAMG_REQUIRE(ctx, nslots >= 1 && nslots <= FIT_SLOTS, "1..4 slots");
   FitSlots* fs = fit_slots(ctx);
   BAMG_REQUIRE(ctx, fs != nullptr, "fit slot state allocation failed");
-  fs->forked = false;
+  for (int s = 0; s < FIT_SLOTS; ++s)  // join every pending slot back into the main stream
+    if (fs->pending[s]) {
+      BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, fs->join[s], 0));
+      fs->pending[s] = false;
+    }
   unsigned long long* st = fs->status;
   int64_t h[4 * FIT_SLOTS];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(st), 4 * FIT_SLOTS, h));

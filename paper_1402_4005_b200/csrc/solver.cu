@@ -850,11 +850,17 @@ static bool cgs_fast_enabled() {
 }
 
 static GmresWork& gmres_work(bamg_ctx* ctx) {
-  static thread_local std::vector<std::pair<bamg_ctx*, GmresWork*>> table;
-  for (auto& e : table)
-    if (e.first == ctx) return *e.second;
-  table.push_back({ctx, new GmresWork()});
-  return *table.back().second;
+  if (!ctx->gmres_work) ctx->gmres_work = new GmresWork();
+  return *ctx->gmres_work;
+}
+
+void gmres_work_release(bamg_ctx* ctx) {
+  GmresWork* W = ctx->gmres_work;
+  if (!W) return;
+  for (double* p : W->basis) cudaFree(p);
+  if (W->dVp) cudaFree(W->dVp);
+  delete W;
+  ctx->gmres_work = nullptr;
 }
 
 static int apply_op(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const double* v, double* tmp,

@@ -427,11 +427,20 @@ struct SpgemmMemo {
 constexpr int SPG_SLOTS = 4;
 
 static SpgemmMemo& memo(bamg_ctx* ctx, int slot = 0) {
-  static thread_local std::vector<std::pair<bamg_ctx*, SpgemmMemo*>> table;
-  for (auto& e : table)
-    if (e.first == ctx) return e.second[slot];
-  table.push_back({ctx, new SpgemmMemo[SPG_SLOTS]()});
-  return table.back().second[slot];
+  if (!ctx->spgemm_memo) ctx->spgemm_memo = new SpgemmMemo[SPG_SLOTS]();
+  return ctx->spgemm_memo[slot];
+}
+
+void spgemm_memo_release(bamg_ctx* ctx) {
+  if (!ctx->spgemm_memo) return;
+  for (int s = 0; s < SPG_SLOTS; ++s) {
+    SpgemmMemo& m = ctx->spgemm_memo[s];
+    for (void* p : {(void*)m.nbig_dev, (void*)m.list, (void*)m.off, (void*)m.pkey, (void*)m.pval, (void*)m.stat,
+                    (void*)m.tcol, (void*)m.tval, (void*)m.parked, (void*)m.redo, (void*)m.nredo})
+      if (p) cudaFree(p);
+  }
+  delete[] ctx->spgemm_memo;
+  ctx->spgemm_memo = nullptr;
 }
 
 static int memo_reserve(bamg_ctx* ctx, SpgemmMemo& m, int64_t n) {
