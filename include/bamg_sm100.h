@@ -141,6 +141,14 @@ int bamg_chain_lattice_count(bamg_ctx* ctx, int family, int side, double lam, do
                              int32_t* rowptr, double* geometry, int64_t* nnz_host);
 int bamg_chain_lattice_fill(bamg_ctx* ctx, int family, int side, double lam, double mu1, double mu2,
                             const int32_t* rowptr, int32_t* col, double* val);
+/* B = I - A of the random planar walk (chains.py:270-302) from its Delaunay
+ * triangles (ntri x 3 int32 vertex ids; Qhull on the host): count writes
+ * rowptr (n + 1) and nnz, fill writes col / val.  Bit-identical to the
+ * reference's make_csr(I - A) on the same edge set. */
+int bamg_chain_planar_count(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, int32_t* rowptr,
+                            int64_t* nnz_host);
+int bamg_chain_planar_fill(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, const int32_t* rowptr,
+                           int32_t* col, double* val);
 
 /* ------------------------------------------------------ relax (relax.py) */
 /* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit

@@ -64,6 +64,8 @@ _SIGS = {
     "bamg_count_nonpositive": [P, P, I64, PI64],
     "bamg_chain_lattice_count": [P, C.c_int, C.c_int, F64, F64, F64, P, P, PI64],
     "bamg_chain_lattice_fill": [P, C.c_int, C.c_int, F64, F64, F64, P, P, P],
+    "bamg_chain_planar_count": [P, P, I64, C.c_int, P, PI64],
+    "bamg_chain_planar_fill": [P, P, I64, C.c_int, P, P, P],
     "bamg_spgemm_count": [P, PCSR, PCSR, C.c_int, P, PI64],
     "bamg_spgemm_fill": [P, PCSR, PCSR, C.c_int, P, P, P],
     "bamg_spgemm_count_slot": [P, PCSR, PCSR, C.c_int, P, C.c_int],

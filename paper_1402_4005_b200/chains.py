@@ -171,6 +171,37 @@ def lattice_chain_device(family: str, side: int, lam: float = 11.0 / 31.0, mu1: 
     return ChainProblem(A=None, B=B, n=n, family=family, params=params, geometry=geo)
 
 
+def planar_chain_device(n: int, seed: int = 1) -> ChainProblem:
+    """The random planar chain's B assembled in HBM from the Delaunay triangles
+    (csrc/chains.cu): the same point draw as random_planar / the reference
+    (chains.py:279-280), Qhull on the host, then degrees, de-duplicated
+    neighbour lists and the canonical CSR of I - A on the device -- bit for bit
+    random_planar's B without the host matrix or its upload.  A is not formed."""
+    import ctypes as C
+
+    import torch
+    from scipy.spatial import Delaunay
+
+    from . import _lib
+    from .device import DeviceCSR, device
+    if n < 4:
+        raise ValueError("need at least four points")
+    rng = np.random.default_rng(np.random.SeedSequence(seed))
+    pts = rng.random((n, 2))
+    tri = np.ascontiguousarray(Delaunay(pts).simplices, dtype=np.int32)
+    dev = device()
+    dtri = torch.from_numpy(tri).to(dev)
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    nnz = C.c_int64(0)
+    _lib.call("bamg_chain_planar_count", _lib.ptr(dtri), tri.shape[0], n, _lib.ptr(rp), C.byref(nnz))
+    ci = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+    va = torch.empty(nnz.value, dtype=torch.float64, device=dev)
+    _lib.call("bamg_chain_planar_fill", _lib.ptr(dtri), tri.shape[0], n, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(va))
+    B = DeviceCSR(rp, ci, va, (n, n))
+    geo = torch.from_numpy(np.ascontiguousarray(pts.T)).to(dev)
+    return ChainProblem(A=None, B=B, n=n, family="planar", params={"n": n}, geometry=geo, seed=seed)
+
+
 def birth_death(n: int, mu: float = 0.96) -> ChainProblem:
     """Biased walk on a path (chains.py:64-92)."""
     if n < 2:
@@ -270,6 +301,36 @@ def petri_reachability(spec, state_cap: int = 10 ** 6) -> ChainProblem:
                               shape=(n, n)))
     return _finish(A, "petri", {"places": places, "n_transitions": len(transitions),
                                 "initial_marking": list(marking), "n": n})
+
+
+def petri_spec_from_json(text: str):
+    """Petri net from JSON {places, transitions: [{inputs, outputs, weight}], initial_marking}
+    (chains.py:370-378), as the (places, transitions, marking) tuple petri_reachability takes."""
+    import json
+    doc = json.loads(text)
+    transitions = tuple(({int(k): int(v) for k, v in t["inputs"].items()},
+                         {int(k): int(v) for k, v in t["outputs"].items()},
+                         float(t.get("weight", 1.0))) for t in doc["transitions"])
+    return (int(doc["places"]), transitions, tuple(int(x) for x in doc["initial_marking"]))
+
+
+def import_chain(path) -> ChainProblem:
+    """Chain from a Matrix Market file holding A or B = I - A, told apart by the
+    column sums (near one: stochastic A; near zero: B) (chains.py:426-447)."""
+    from .sparse import load_matrix_market
+    M = load_matrix_market(path)
+    if M.shape[0] != M.shape[1]:
+        raise ValueError("imported matrix must be square")
+    colsums = np.asarray(M.sum(axis=0)).ravel()
+    if np.abs(colsums - 1.0).max(initial=0.0) <= 1e-8:
+        A = M
+    elif np.abs(colsums).max(initial=0.0) <= 1e-8:
+        A = make_csr(sp.eye_array(M.shape[0], format="csr", dtype=np.float64) - M)
+    else:
+        worst = int(np.argmax(np.minimum(np.abs(colsums - 1.0), np.abs(colsums))))
+        raise ValueError(f"file is neither column-stochastic nor zero-column-sum: column {worst} "
+                         f"sums to {colsums[worst]:.16g}")
+    return _finish(A, "imported", {"path": str(path)})
 
 
 def make_chain(family: str, **kw) -> ChainProblem:

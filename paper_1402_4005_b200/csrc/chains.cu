@@ -10,6 +10,8 @@
 // Two passes over the rows: count (entries per row) -> exclusive scan ->
 // fill.  Node numbering node = q2 * side + q1 (tandem), iy * side + ix
 // (uniform), as the reference.
+#include <algorithm>
+
 #include "internal.cuh"
 
 struct TandemRow {
@@ -148,5 +150,134 @@ extern "C" int bamg_chain_lattice_fill(bamg_ctx* ctx, int family, int side, doub
   const int64_t n = (int64_t)side * side;
   BAMG_LAUNCH(ctx, lattice_chain_kernel<1>, grid_for(n, 256), 256, 0, family, side, lam, mu1, mu2, (int32_t*)nullptr,
               rowptr, col, val, (double*)nullptr);
+  return 0;
+}
+
+// ------------------------------------------------------------ planar chain
+// B = I - A of the random planar walk (chains.py:270-302) from the Delaunay
+// triangles (the triangulation itself is Qhull on the host; the reference's
+// Bowyer-Watson is O(n^2)): every triangle lists its two other corners at
+// each corner, each row's list is sorted and de-duplicated (an interior edge
+// comes from two triangles), deg = unique neighbour count, and row i of B
+// holds 1.0 on the diagonal and -(1.0 / deg[j]) at every neighbour j -- the
+// reference's A has 1/deg[j] in column j (chains.py:296-299), so the values
+// and the canonical column order are bit-identical to make_csr(I - A).
+__global__ void planar_tri_count_kernel(const int32_t* __restrict__ tri, int64_t ntri, int32_t* __restrict__ cnt) {
+  BAMG_PDL_PROLOGUE();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += (int64_t)gridDim.x * blockDim.x)
+    for (int q = 0; q < 3; ++q) atomicAdd(&cnt[tri[3 * t + q]], 2);
+}
+
+__global__ void planar_tri_fill_kernel(const int32_t* __restrict__ tri, int64_t ntri, int32_t* __restrict__ cur,
+                                       int32_t* __restrict__ nbr) {
+  BAMG_PDL_PROLOGUE();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v[3] = {tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+    for (int q = 0; q < 3; ++q) {
+      const int32_t p = atomicAdd(&cur[v[q]], 2);
+      nbr[p] = v[(q + 1) % 3];
+      nbr[p + 1] = v[(q + 2) % 3];
+    }
+  }
+}
+
+// sort + de-duplicate each row's list in place; deg[i] = unique count,
+// cnt1[i] = deg[i] + 1 (row length of B: neighbours and the diagonal)
+__global__ void planar_row_unique_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ nbr, int n,
+                                         int32_t* __restrict__ deg, int32_t* __restrict__ cnt1,
+                                         int* __restrict__ isolated) {
+  BAMG_PDL_PROLOGUE();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t* a = nbr + off[i];
+  const int len = off[i + 1] - off[i];
+  for (int x = 1; x < len; ++x) {  // insertion sort (mean degree ~6)
+    const int32_t v = a[x];
+    int y = x - 1;
+    while (y >= 0 && a[y] > v) {
+      a[y + 1] = a[y];
+      --y;
+    }
+    a[y + 1] = v;
+  }
+  int u = 0;
+  for (int x = 0; x < len; ++x)
+    if (u == 0 || a[x] != a[u - 1]) a[u++] = a[x];
+  deg[i] = u;
+  cnt1[i] = u + 1;
+  if (u == 0) atomicExch(isolated, 1);
+}
+
+__global__ void planar_fill_b_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                     const int32_t* __restrict__ deg, int n, const int32_t* __restrict__ rowptr,
+                                     int32_t* __restrict__ col, double* __restrict__ val) {
+  BAMG_PDL_PROLOGUE();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t* a = nbr + off[i];
+  const int u = deg[i];
+  int w = rowptr[i];
+  bool diag = false;
+  for (int x = 0; x < u; ++x) {
+    const int32_t j = a[x];
+    if (!diag && j > i) {
+      col[w] = i;
+      val[w++] = 1.0;
+      diag = true;
+    }
+    col[w] = j;
+    val[w++] = -(1.0 / (double)deg[j]);
+  }
+  if (!diag) {
+    col[w] = i;
+    val[w] = 1.0;
+  }
+}
+
+// both calls rebuild the (cheap) sorted neighbour lists in the arena
+static int planar_lists(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, int32_t** off, int32_t** nbr,
+                        int32_t** deg, int32_t** cnt1, int* isolated_host) {
+  int32_t *cnt, *cur;
+  int* iso;
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cnt));
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, off));
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, &cur));
+  BAMG_TRY(arena_get(ctx, (size_t)6 * ntri + 1, nbr));
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, deg));
+  BAMG_TRY(arena_get(ctx, (size_t)n + 1, cnt1));
+  BAMG_TRY(arena_get(ctx, 1, &iso));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(iso, 0, sizeof(int), ctx->stream));
+  const int g = std::min(grid_for(ntri, 256), 8 * ctx->num_sms);
+  BAMG_LAUNCH(ctx, planar_tri_count_kernel, g, 256, 0, tri, ntri, cnt);
+  int64_t total = 0;
+  BAMG_TRY(scan_i32(ctx, cnt, *off, n, &total));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(cur, *off, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_LAUNCH(ctx, planar_tri_fill_kernel, g, 256, 0, tri, ntri, cur, *nbr);
+  BAMG_LAUNCH(ctx, planar_row_unique_kernel, grid_for(n, 256), 256, 0, (const int32_t*)*off, *nbr, n, *deg, *cnt1,
+              iso);
+  BAMG_TRY(ctx_read_i32(ctx, iso, 1, isolated_host));
+  return 0;
+}
+
+extern "C" int bamg_chain_planar_count(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, int32_t* rowptr,
+                                       int64_t* nnz_host) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, n >= 4 && ntri >= 1 && 6 * ntri < ((int64_t)1 << 31), "planar chain: bad sizes");
+  int32_t *off, *nbr, *deg, *cnt1;
+  int iso = 0;
+  BAMG_TRY(planar_lists(ctx, tri, ntri, n, &off, &nbr, &deg, &cnt1, &iso));
+  BAMG_REQUIRE(ctx, iso == 0, "triangulation left an isolated point");
+  return scan_i32(ctx, cnt1, rowptr, n, nnz_host);
+}
+
+extern "C" int bamg_chain_planar_fill(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, const int32_t* rowptr,
+                                      int32_t* col, double* val) {
+  ctx->arena.reset();
+  int32_t *off, *nbr, *deg, *cnt1;
+  int iso = 0;
+  BAMG_TRY(planar_lists(ctx, tri, ntri, n, &off, &nbr, &deg, &cnt1, &iso));
+  BAMG_LAUNCH(ctx, planar_fill_b_kernel, grid_for(n, 256), 256, 0, (const int32_t*)off, (const int32_t*)nbr,
+              (const int32_t*)deg, n, rowptr, col, val);
   return 0;
 }

@@ -81,6 +81,11 @@ struct KProf {
   size_t used[NFAM] = {};
   double bytes[NFAM] = {};
   double flops[NFAM] = {};
+  // batched[f]: launches of family f add their bytes but no event pair; the
+  // caller times the whole batch with one pair on the context stream (the
+  // LS-fit slots overlap on side streams: per-launch pairs would count the
+  // overlapped time twice)
+  bool batched[NFAM] = {};
 };
 
 // Whole-engine launch trace (development): every BAMG_LAUNCH brackets its
@@ -151,12 +156,11 @@ static inline cudaEvent_t prof_event(bamg_ctx* ctx, int fam) {
 #define BAMG_LAUNCH_FAM(ctx, fam, nbytes, kernel, grid, block, smem, ...)       \
   do {                                                                          \
     bool _prof = ((ctx)->prof.mask >> (fam)) & 1u;                              \
-    if (_prof && (grid) > 0) {                                                  \
-      cudaEventRecord(prof_event(ctx, fam), (ctx)->stream);                     \
-      (ctx)->prof.bytes[fam] += (double)(nbytes);                               \
-    }                                                                           \
+    bool _ev = _prof && !(ctx)->prof.batched[fam];                              \
+    if (_prof && (grid) > 0) (ctx)->prof.bytes[fam] += (double)(nbytes);        \
+    if (_ev && (grid) > 0) cudaEventRecord(prof_event(ctx, fam), (ctx)->stream); \
     BAMG_LAUNCH(ctx, kernel, grid, block, smem, __VA_ARGS__);                   \
-    if (_prof && (grid) > 0) cudaEventRecord(prof_event(ctx, fam), (ctx)->stream); \
+    if (_ev && (grid) > 0) cudaEventRecord(prof_event(ctx, fam), (ctx)->stream); \
   } while (0)
 
 // ---------------------------------------------------------------- error glue

@@ -1444,6 +1444,11 @@ extern "C" int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const 
   BAMG_CHECK_CUDA(ctx, cudaStreamIsCapturing(ctx->stream, &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
   cudaStream_t main = ctx->stream;
+  const bool prof = (ctx->prof.mask >> FAM_FIT) & 1u;
+  bool first_of_batch = true;
+  for (int s = 0; s < FIT_SLOTS; ++s) first_of_batch = first_of_batch && !fs->pending[s];
+  if (prof && !capturing && first_of_batch)  // one event pair per batch (closed in bamg_fit_rows_wait)
+    cudaEventRecord(prof_event(ctx, FAM_FIT), main);
   Arena saved;
   std::swap(saved, ctx->arena);  // the slot's scratch comes from its own arena
   std::swap(ctx->arena, fs->arena[slot]);
@@ -1462,8 +1467,10 @@ extern "C" int bamg_fit_rows_csr_slot(bamg_ctx* ctx, const bamg_csr* adj, const 
     cudaStreamSynchronize(fs->side[slot]);  // no capture-time reset may overlap a side-stream user
     ctx->arena.reset();
   }
+  ctx->prof.batched[FAM_FIT] = !capturing;
   int rc = fit_rows_csr_launch(ctx, adj, coarse_rank, X, w, n, k, caliber, radius, improvement_tol, constrain,
                                nonnegative, ridge_override, out_cnt, out_col, out_val, rowptr, st);
+  ctx->prof.batched[FAM_FIT] = false;
   ctx->stream = main;
   std::swap(ctx->arena, fs->arena[slot]);
   std::swap(saved, ctx->arena);
@@ -1480,11 +1487,15 @@ extern "C" int bamg_fit_rows_wait(bamg_ctx* ctx, int nslots, const int32_t* slot
   BAMG_REQUIRE(ctx, nslots >= 1 && nslots <= FIT_SLOTS, "1..4 slots");
   FitSlots* fs = fit_slots(ctx);
   BAMG_REQUIRE(ctx, fs != nullptr, "fit slot state allocation failed");
+  bool any = false;
   for (int s = 0; s < FIT_SLOTS; ++s)  // join every pending slot back into the main stream
     if (fs->pending[s]) {
       BAMG_CHECK_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, fs->join[s], 0));
       fs->pending[s] = false;
+      any = true;
     }
+  if (any && ((ctx->prof.mask >> FAM_FIT) & 1u))  // close the batch's event pair
+    cudaEventRecord(prof_event(ctx, FAM_FIT), ctx->stream);
   unsigned long long* st = fs->status;
   int64_t h[4 * FIT_SLOTS];
   BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<const int64_t*>(st), 4 * FIT_SLOTS, h));

@@ -94,3 +94,38 @@ def adjacency_structure(M, Mt: DeviceCSR | None = None) -> DeviceCSR:
     A = as_device(M)
     T = Mt if Mt is not None else engine.transpose(A)
     return engine.sym_pattern(A, T)
+
+
+def save_matrix_market(path, M, comment: str = "") -> None:
+    """Matrix Market coordinate file, 1-based, 17 significant digits (sparse.py:152-155).
+
+    Host I/O of a result: device operators are copied down once."""
+    from scipy.io import mmwrite
+    from scipy import sparse as _sp
+    if hasattr(M, "to_host"):
+        M = M.to_host()
+    mmwrite(str(path), _sp.coo_matrix(M), comment=comment, field="real", precision=17, symmetry="general")
+
+
+def load_matrix_market(path):
+    """Matrix Market file -> canonical CSR (sparse.py:158-160)."""
+    from scipy.io import mmread
+    return make_csr(mmread(str(path)))
+
+
+def save_vector(path, x, comment: str = "") -> None:
+    """Dense vector as an n x 1 Matrix Market array (sparse.py:163-166)."""
+    from scipy.io import mmwrite
+    if hasattr(x, "cpu"):
+        x = x.cpu().numpy()
+    mmwrite(str(path), np.asarray(x, dtype=np.float64).reshape(-1, 1), comment=comment, field="real", precision=17)
+
+
+def load_vector(path) -> np.ndarray:
+    """sparse.py:169-173."""
+    from scipy.io import mmread
+    from scipy import sparse as _sp
+    arr = mmread(str(path))
+    if _sp.issparse(arr):
+        arr = arr.toarray()
+    return np.asarray(arr, dtype=np.float64).ravel()

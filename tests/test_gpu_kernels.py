@@ -321,6 +321,21 @@ def test_device_lattice_chain_matches_host(eng, family, side):
     assert np.array_equal(dev.geometry.cpu().numpy().T, host.geometry)
 
 
+@pytest.mark.parametrize("n", [4, 5, 100, 1024, 30_000])
+def test_device_planar_chain_matches_host(eng, n):
+    """On-device assembly of the planar chain from its Delaunay triangles
+    (remainder): the host generator's canonical CSR of
+    B = I - A and the point geometry, bit for bit."""
+    from paper_1402_4005_b200 import chains
+    host = chains.random_planar(n, seed=1)
+    dev = chains.planar_chain_device(n, seed=1)
+    H = host.B
+    D = dev.B.to_host()
+    assert np.array_equal(D.indptr, H.indptr) and np.array_equal(D.indices, H.indices)
+    assert np.array_equal(D.data, H.data)
+    assert np.array_equal(dev.geometry.cpu().numpy().T, host.geometry)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [1, 3, 8, 16])
 def test_block_kernels_match_numpy(eng, k):
