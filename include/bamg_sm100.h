@@ -325,9 +325,11 @@ int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* lu);
  * the CSR operators (B, its explicit transpose Bt, M, N; no dense n x n
  * matrix is formed).  Returns 1 -- nothing written -- when the half-bandwidth
  * exceeds 160 or n / 4, or the factorisation is not certified; the caller
- * then takes the dense path.  *lu_out: free with bamg_coarse_lu_destroy. */
+ * then takes the dense path.  Vin (n x r interleaved, may be NULL): the
+ * level's incoming right test vectors, a warm start for the subspace
+ * iteration.  *lu_out: free with bamg_coarse_lu_destroy. */
 int bamg_coarsest_band(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M, const bamg_csr* N,
-                       int r, double* U, double* V, double* sigma, bamg_coarse_lu** lu_out);
+                       int r, const double* Vin, double* U, double* V, double* sigma, bamg_coarse_lu** lu_out);
 
 /* ----------------------------------------------------------- solver (solver.py) */
 /* Hierarchy for the V-cycle (VCycleOperator, solver.py:79-124).  Level

@@ -112,7 +112,7 @@ _SIGS = {
     "bamg_coarse_lu_apply": [P, P, P, P],
     "bamg_coarse_lu_destroy": [P, P],
     "bamg_band_sweep_probe": [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, PF64],
-    "bamg_coarsest_band": [P, PCSR, PCSR, PCSR, PCSR, C.c_int, P, P, P, P],
+    "bamg_coarsest_band": [P, PCSR, PCSR, PCSR, PCSR, C.c_int, P, P, P, P, P],
     "bamg_hier_set_smoother": [P, F64, C.c_int, C.c_int],
     "bamg_vcycle": [P, P, P, P],
     "bamg_gmres": [P, PCSR, P, P, P, P, C.c_int, C.c_int, F64, C.c_int, PINT, PF64, PINT],

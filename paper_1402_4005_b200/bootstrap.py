@@ -297,7 +297,7 @@ def _band_min_n() -> int:
     return int(os.environ.get("BAMG_BAND_N", "2048"))
 
 
-def coarsest_triplets(B, M, N, r: int, Bt: DeviceCSR | None = None) -> TripletSet:
+def coarsest_triplets(B, M, N, r: int, Bt: DeviceCSR | None = None, warm: "TripletSet | None" = None) -> TripletSet:
     """Exact generalized singular triplets of the coarsest operator (bootstrap.py:205-281).
 
     Large banded levels (the lattice chains keep the fine ordering, so the
@@ -307,7 +307,8 @@ def coarsest_triplets(B, M, N, r: int, Bt: DeviceCSR | None = None) -> TripletSe
     A, Md, Nd = as_device(B), as_device(M), as_device(N)
     n = A.shape[0]
     if n >= _band_min_n():
-        out = engine.coarsest_triplets_band(A, Bt if Bt is not None else engine.transpose(A), Md, Nd, r)
+        out = engine.coarsest_triplets_band(A, Bt if Bt is not None else engine.transpose(A), Md, Nd, r,
+                                            warm_right=warm.dright if warm is not None else None)
         if out is not None:
             U, V, s, lu = out
             trips = TripletSet(s, U, V)
@@ -385,7 +386,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         if _DEBUG:
             print(f"[bamg] coarsest level {depth} n={n}", file=sys.stderr, flush=True)
         with _phase("coarsest"):
-            trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt)
+            trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt, warm=trips)
         return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
 
     with _phase("smooth"):
@@ -429,7 +430,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             if _DEBUG:
                 print(f"[bamg] truncated at level {depth} n={n} (sick Galerkin product)", file=sys.stderr, flush=True)
             with _phase("coarsest"):
-                trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt)
+                trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt, warm=trips)
             return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
         with _phase("inject"):
             cranks = ranks.restrict(split) if ranks is not None else None

@@ -1993,7 +1993,7 @@ extern "C" int bamg_coarse_lu_destroy(bamg_ctx* ctx, bamg_coarse_lu* h) {
 // not banded enough or the block factorisation is not certified (the caller
 // then takes the dense path).
 extern "C" int bamg_coarsest_band(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
-                                  const bamg_csr* N, int r, double* U, double* V, double* sigma,
+                                  const bamg_csr* N, int r, const double* Vin, double* U, double* V, double* sigma,
                                   bamg_coarse_lu** lu_out) {
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, B && Bt && M && N && lu_out, "null argument");
@@ -2001,7 +2001,7 @@ extern "C" int bamg_coarsest_band(bamg_ctx* ctx, const bamg_csr* B, const bamg_c
   BAMG_REQUIRE(ctx, r >= 1 && r <= B->nrows, "r out of range");
   *lu_out = nullptr;
   BandPinv* keep = nullptr;
-  const int rc = band_coarsest_triplets(ctx, B, Bt, M, N, r, U, V, sigma, &keep);
+  const int rc = band_coarsest_triplets(ctx, B, Bt, M, N, r, Vin, U, V, sigma, &keep);
   if (rc != 0) return rc;
   bamg_coarse_lu* h = new bamg_coarse_lu();
   h->C.n = B->nrows;

@@ -45,7 +45,8 @@ int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V,
 // banded coarsest level (band.cu)
 struct BandPinv;
 int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M,
-                           const bamg_csr* N, int r, double* U, double* V, double* sigma, BandPinv** keep);
+                           const bamg_csr* N, int r, const double* Vin, double* U, double* V, double* sigma,
+                           BandPinv** keep);
 int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x);
 void band_pinv_free(bamg_ctx* ctx, BandPinv* h);
 

@@ -407,7 +407,7 @@ def coarsest_triplets(Bd, Md, Nd, n, r, with_pinv=False):
     return U, V, s, (Z if (Z is not None and ok.value) else None)
 
 
-def coarsest_triplets_band(B: DeviceCSR, Bt: DeviceCSR, M: DeviceCSR, N: DeviceCSR, r):
+def coarsest_triplets_band(B: DeviceCSR, Bt: DeviceCSR, M: DeviceCSR, N: DeviceCSR, r, warm_right=None):
     """(U, V, sigma, CoarseLU) from the block-tridiagonal factorisations of the
     CSR operators (bamg_coarsest_band), or None when the level is not banded
     enough or the factorisation was not certified (dense path then)."""
@@ -417,7 +417,11 @@ def coarsest_triplets_band(B: DeviceCSR, Bt: DeviceCSR, M: DeviceCSR, N: DeviceC
     V = _empty((n, take))
     s = _empty(take)
     lu = C.c_void_p()
-    rc = _lib.call("bamg_coarsest_band", B.ref(), Bt.ref(), M.ref(), N.ref(), take, _p(U), _p(V), _p(s), C.byref(lu))
+    warm = None
+    if warm_right is not None and tuple(warm_right.shape) == (n, take):
+        warm = warm_right.contiguous()
+    rc = _lib.call("bamg_coarsest_band", B.ref(), Bt.ref(), M.ref(), N.ref(), take, _p(warm), _p(U), _p(V), _p(s),
+                   C.byref(lu))
     if rc != 0 or not lu.value:
         return None
     return U, V, s, CoarseLU(lu, n)
