@@ -472,22 +472,21 @@ def fp64_fit_roofline(L, c, fam, steps, name):
 def family_traffic(family, alg_per_launch):
     """roofline.traffic: DRAM bytes per launch of the roofline's kernel family.
 
-    From the committed ncu capture (profiles/rNN_csr_family_traffic.json, made by
+    From the committed ncu capture (profiles/rNN_family_traffic.json, made by
     tools/family_traffic.py): ncu's dram__bytes_read.sum + dram__bytes_write.sum
-    over every CSR row-kernel launch of one cfg1 step, divided by the engine's
-    algorithmic bytes for the same launches (graph-free run, so every launch is
-    profiled).  The timed region's launches (V-cycle graph nodes are not event-
-    timed) get that measured traffic/algorithmic ratio applied to their own
+    over every launch of the family in one graph-free step, divided by the
+    engine's algorithmic bytes for the same launches.  The timed region's
+    launches get that measured traffic/algorithmic ratio applied to their own
     algorithmic bytes per launch."""
-    files = sorted(ROOT.glob("profiles/r*_csr_family_traffic.json"))
-    if family != "csr_stream_spmv_spmm_jacobi" or not files:
-        return None, None
-    d = json.load(open(files[-1]))
-    ratio = d.get("traffic_over_alg")
-    if not ratio:
-        return None, None
-    return round(alg_per_launch * ratio), (f"{files[-1].name}: ncu DRAM bytes / algorithmic bytes = {ratio:.3f} "
-                                           f"over {d['launches']} launches of one step, applied per launch")
+    for f in sorted(ROOT.glob("profiles/r*_family_traffic.json"), reverse=True):
+        d = json.load(open(f))
+        e = d.get("families", {}).get(family)
+        if e and e.get("traffic_over_alg"):
+            ratio = e["traffic_over_alg"]
+            return round(alg_per_launch * ratio), (f"{f.name}: ncu DRAM bytes / algorithmic bytes = {ratio:.3f} "
+                                                   f"over {e['launches']} launches of one {d.get('config')} step, "
+                                                   f"applied per launch")
+    return None, None
 
 
 SAMPLES = {"tandem": 128, "uniform2d": 127, "planar": 4096}  # side (lattices) or n (planar)

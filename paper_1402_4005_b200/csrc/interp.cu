@@ -1,5 +1,8 @@
-// interp.cu -- least-squares interpolation / restriction rows, one warp per
-// fine point (interp.py:105-289).
+// interp.cu -- least-squares interpolation / restriction rows
+// (interp.py:105-289): one thread per fine point on the production path
+// (fit_rows_thread_kernel: corrected semi-normal equations with compile-time
+// trial sizes), one warp per point for the rest (fit_rows_kernel below,
+// Householder QR with the reference's pseudo-inverse branch).
 //
 // Per fine point i the warp
 //   1. builds the candidate list: coarse points among the radius-1

@@ -1,9 +1,10 @@
 """Least-squares interpolation and restriction (mirrors markovmg/interp.py).
 
-The per-fine-point greedy ridge least squares runs one warp per point in
-csrc/interp.cu; this module keeps the reference's configuration objects and
-entry points and assembles the fixed-stride row output into canonical CSR on
-device.
+The per-fine-point greedy ridge least squares runs one THREAD per point in
+csrc/interp.cu (compile-time trial sizes, points bucketed by candidate count);
+points outside that path go to the warp-per-point Householder-QR kernel.  This
+module keeps the reference's configuration objects and entry points and
+assembles the fixed-stride row output into canonical CSR on device.
 """
 
 from __future__ import annotations

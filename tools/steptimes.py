@@ -46,7 +46,7 @@ zero = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
 from paper_1402_4005_b200 import _lib
 import ctypes as C
 if a.prof:
-    _lib.lib().bamg_prof_enable(_lib.ctx(), (1 << 0) | (1 << 1) | (1 << 6))
+    _lib.lib().bamg_prof_enable(_lib.ctx(), (1 << 0) | (1 << 1) | (1 << 3) | (1 << 6))
 for i in range(a.steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -67,6 +67,7 @@ if a.prof:
         _lib.lib().bamg_prof_read(_lib.ctx(), fid, C.byref(ms), C.byref(cnt), C.byref(by))
         return ms.value, cnt.value, by.value
     # the CSR family = engine families 0 (coarse levels) + 6 (operators >= 2^18 rows)
-    for fname, fids in (("csr_stream_spmv_spmm_jacobi", (0, 6)), ("ls_fit", (1,))):
+    for fname, fids in (("csr_stream_spmv_spmm_jacobi", (0, 6)), ("ls_fit", (1,)),
+                        ("gmres_cgs2_basis_passes", (3,))):
         ms, cnt, by = (sum(v) for v in zip(*(rd(f) for f in fids)))
         print(json.dumps({"family": fname, "ms": ms, "launches": cnt, "alg_bytes": by}), flush=True)
