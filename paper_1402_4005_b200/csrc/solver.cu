@@ -330,6 +330,14 @@ constexpr int GM_BLOCKS = RED_BLOCKS;
 constexpr int GM_THREADS = 256;
 constexpr int GM_GROUP = 16;  // basis vectors per register group
 
+// state code of an Arnoldi step (code[0]): 1 = one projection suffices (DGKS),
+// 0 = second projection, safe Pythagorean norm, 2 = second projection with the
+// explicit norm.  A kernel gated on `mask` runs iff bit code[0] is set.
+__device__ __forceinline__ bool cgs_gate(const double* code, unsigned mask) {
+  return !code || ((mask >> (int)code[0]) & 1u);
+}
+
+
 // partial[b * m + i] = sum over block b's chunk of V_i . w   (i < m)
 __global__ void __launch_bounds__(GM_THREADS)
 mdot_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ w, int64_t n,
@@ -417,15 +425,15 @@ __global__ void mreduce_kernel(const double* __restrict__ partial, int nb, int m
 //   h[j+1] = sqrt(nrm2); happy test; previous rotations; new rotation;
 //   R[:, j]; g; y = R^-1 g (back substitution).  state[0] = happy flag,
 //   state[1] = h[j+1].
-// flag / when: with a CGS fast-path flag (see cgs_pythag_kernel) the kernel
-// runs only when (flag[0] != 0) == when, so the unsafe step's explicit norm
-// reaches the rotation exactly once.
+// flag / mask: with a CGS step code (see cgs_gate) the kernel runs only when
+// bit flag[0] of mask is set, so each branch's norm reaches the rotation
+// exactly once.
 __global__ void givens_kernel(int j, int ldr, double* __restrict__ h, const double* __restrict__ nrm2,
                               double beta, double* __restrict__ R, double* __restrict__ g,
                               double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ y,
-                              double* __restrict__ state, const double* __restrict__ flag, int when) {
+                              double* __restrict__ state, const double* __restrict__ flag, unsigned mask) {
   BAMG_PDL_PROLOGUE();
-  if (flag && ((flag[0] != 0.0) != (when != 0))) return;
+  if (!cgs_gate(flag, mask)) return;
   extern __shared__ double sg[];  // j+1 working entries of g during the back substitution
   if (threadIdx.x == 0) {
     double hj1 = sqrt(nrm2[0]);
@@ -506,6 +514,13 @@ __global__ void scale_div_kernel(int64_t n, const double* __restrict__ a, const 
 }
 
 // ---- register-resident CGS2 passes (basis of <= CGS_MAXM vectors)
+// Reorthogonalisation is applied only where it is needed (the DGKS criterion,
+// eta = 1/sqrt(2)): pass A also forms |w|^2, and when the first projection
+// keeps |w - V h|^2 = |w|^2 - |h|^2 >= |w|^2 / 2 the step is ONE more pass
+// (pass C with h, straight from w) -- two passes over V instead of three.
+// Otherwise the classical second pass runs (below).  Which branch a step
+// takes is decided on the device (a state code, every kernel gated on it),
+// so the host never waits for it.
 // One Arnoldi step in three passes over the basis instead of five:
 //   A: h  = V^T w                                   (dots)
 //   B: w' = w - V h ; h2 = V^T w' ; |w'|^2          (update + dots, one read of V)
@@ -520,6 +535,7 @@ __global__ void scale_div_kernel(int64_t n, const double* __restrict__ a, const 
 // order (deterministic).  Values V_g[i] of a row stay in registers between
 // the update and the dots of pass B.
 constexpr int CGS_MAXM = 64;
+__constant__ bool cgs_force_two_pass = false;  // BAMG_CGS_ALWAYS_REORTH=1 (development)
 constexpr int CGS_THREADS = 128;
 constexpr int CGS_WARPS = CGS_THREADS / 32;
 constexpr int CGS_MAX_BLOCKS = 32 * 148;  // partial-sum slots per CTA: CGS_MAXM + 1
@@ -560,9 +576,9 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane
   return a[0];
 }
 
-// MODE 0 (pass A): part[b][g] = chunk sum of V_g . w
+// MODE 0 (pass A): part[b][g] = chunk sum of V_g . w, part[b][m] = |w|^2
 // MODE 1 (pass B): w <- w - sum_g c_g V_g (in place); part[b][g] = V_g . w_new,
-//                  part[b][m] = |w_new|^2
+//                  part[b][m] = |w_new|^2  (runs only for code 0)
 // A warp takes 32 consecutive rows (one per lane) at a time; the row's MAXM
 // basis values stay in registers, the 32 x MAXM products are folded across
 // the warp by transpose reductions, and lane l accumulates the dots of
@@ -570,8 +586,9 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane
 template <int MAXM, int MODE>
 __global__ void __launch_bounds__(CGS_THREADS)
 cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c, double* __restrict__ w,
-                int64_t n, double* __restrict__ part) {
+                int64_t n, double* __restrict__ part, const double* __restrict__ code) {
   BAMG_PDL_PROLOGUE();
+  if (MODE == 1 && !cgs_gate(code, 1u << 0)) return;
   static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
   constexpr int NB = MAXM / 32;
   __shared__ const double* sp[MAXM];
@@ -603,7 +620,7 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __res
       if (ok) w[i] = wi;
     }
     if (!ok) wi = 0.0;
-    if (MODE == 1) wn2 = fma(wi, wi, wn2);
+    wn2 = fma(wi, wi, wn2);
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
       if (q * 32 >= m) break;
@@ -615,14 +632,12 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __res
   }
 #pragma unroll
   for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
-  if (MODE == 1) {
-    wn2 = warp_sum(wn2);
-    if (lane == 0) acc[wid][MAXM] = wn2;
-  }
+  wn2 = warp_sum(wn2);
+  if (lane == 0) acc[wid][MAXM] = wn2;
   __syncthreads();
-  const int nslots = MODE == 1 ? m + 1 : m;
+  const int nslots = m + 1;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
-    const int slot = (MODE == 1 && q == m) ? MAXM : q;
+    const int slot = q == m ? MAXM : q;
     double t = 0.0;
     for (int ww = 0; ww < CGS_WARPS; ++ww) t += acc[ww][slot];
     part[(int64_t)blockIdx.x * (m + 1) + q] = t;
@@ -631,8 +646,9 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __res
 
 // out[i] = sum_b part[b * stride + i], i < cnt (fixed order)
 __global__ void cgs_reduce_kernel(const double* __restrict__ part, int nb, int stride, int cnt,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, const double* __restrict__ code, unsigned mask) {
   BAMG_PDL_PROLOGUE();
+  if (!cgs_gate(code, mask)) return;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= cnt) return;
   double v = 0.0;
@@ -641,11 +657,40 @@ __global__ void cgs_reduce_kernel(const double* __restrict__ part, int nb, int s
   if (lane == 0) out[i] = v;
 }
 
-// hv[0..m) += h2[0..m);  nrm2 = |w'|^2 - |h2|^2 (h2 = sums[0..m), |w'|^2 = sums[m]);
-// flag[0] = 1 when the difference lost more than two digits
+// DGKS decision after pass A: h = hv[0..m), |w|^2 = hv[m].  One projection
+// suffices when |w|^2 - |h|^2 >= |w|^2 / 2 (code 1, nrm2 = that difference);
+// else code 0 (the second pass runs).
+// (code 1 also copies h to h2: pass C projects with h2, and the Givens update
+// rotates hv in place)
+__global__ void cgs_dgks_kernel(int m, const double* __restrict__ hv, double* __restrict__ nrm2,
+                                double* __restrict__ code, double* __restrict__ h2) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double red[32];
+  double q = 0.0;
+  for (int g = threadIdx.x; g < m; g += blockDim.x) q = fma(hv[g], hv[g], q);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    const double wn = hv[m], d = wn - t;
+    const bool one = d >= 0.5 * wn && wn > 0.0 && !cgs_force_two_pass;
+    code[0] = one ? 1.0 : 0.0;
+    if (one) nrm2[0] = d;
+    red[0] = one ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (red[0] == 1.0)
+    for (int g = threadIdx.x; g < m; g += blockDim.x) h2[g] = hv[g];
+}
+
+// (code 0 only) hv[0..m) += h2[0..m);  nrm2 = |w'|^2 - |h2|^2 (h2 = sums[0..m),
+// |w'|^2 = sums[m]); code 2 when the difference lost more than two digits
 __global__ void cgs_pythag_kernel(int m, const double* __restrict__ sums, double* __restrict__ hv,
                                   double* __restrict__ nrm2, double* __restrict__ flag) {
   BAMG_PDL_PROLOGUE();
+  if (!cgs_gate(flag, 1u << 0)) return;
   __shared__ double red[32];
   double q = 0.0;
   for (int g = threadIdx.x; g < m; g += blockDim.x) {
@@ -663,7 +708,7 @@ __global__ void cgs_pythag_kernel(int m, const double* __restrict__ sums, double
     const double d = wn - t;
     const bool unsafe = !(d >= 1e-2 * wn);
     nrm2[0] = unsafe ? 0.0 : d;
-    flag[0] = unsafe ? 1.0 : 0.0;
+    flag[0] = unsafe ? 2.0 : 0.0;
   }
 }
 
@@ -674,7 +719,8 @@ __global__ void cgs_pythag_kernel(int m, const double* __restrict__ sums, double
 template <int MAXM>
 __global__ void __launch_bounds__(CGS_THREADS, 4)
 cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ h2,
-                 const double* __restrict__ y, const double* __restrict__ wp, const double* __restrict__ x0,
+                 const double* __restrict__ h1, const double* __restrict__ y, const double* __restrict__ wp,
+                 const double* __restrict__ x0,
                  const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
                  int64_t n, double* __restrict__ vnew, double* __restrict__ x, double* __restrict__ part) {
   BAMG_PDL_PROLOGUE();
@@ -682,13 +728,14 @@ cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __re
   __shared__ double sh[MAXM], sy[MAXM];
   __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  (void)h1;  // h2 holds the projection coefficients of either branch
   for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
     sh[g] = g < m ? h2[g] : 0.0;
     sy[g] = g < m ? y[g] : 0.0;
   }
   if (threadIdx.x < CGS_WARPS) acc[threadIdx.x][0] = 0.0;
   cgs_load_ptrs<MAXM>(Vp, m, sp);
-  const bool unsafe = flag[0] != 0.0;
+  const bool unsafe = flag[0] == 2.0;
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -727,7 +774,7 @@ cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __re
 __global__ void cgs_fix_norm_kernel(const double* __restrict__ flag, const double* __restrict__ part, int nb,
                                     double* __restrict__ nrm2) {
   BAMG_PDL_PROLOGUE();
-  if (flag[0] == 0.0) return;
+  if (flag[0] != 2.0) return;
   __shared__ double red[32];
   double v = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
@@ -765,7 +812,7 @@ cgs_fix_x_kernel(const double* const* __restrict__ Vp, int m, const double* __re
                  const double* __restrict__ flag, int64_t n, double* __restrict__ vnew, double* __restrict__ x,
                  double* __restrict__ part) {
   BAMG_PDL_PROLOGUE();
-  if (flag[0] == 0.0) return;
+  if (flag[0] != 2.0) return;
   __shared__ double red[8];
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
@@ -844,6 +891,15 @@ static int cgs_grid(bamg_ctx* ctx, const void* fn, int64_t n) {
   return (int)std::min<int64_t>(g, CGS_MAX_BLOCKS);
 }
 
+static void cgs_apply_env() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* e = getenv("BAMG_CGS_ALWAYS_REORTH");
+  const bool v = e && e[0] == '1';
+  cudaMemcpyToSymbol(cgs_force_two_pass, &v, sizeof(bool));
+}
+
 static bool cgs_fast_enabled() {
   static const bool on = !(getenv("BAMG_CGS_SLOW") && getenv("BAMG_CGS_SLOW")[0] == '1');
   return on;
@@ -883,6 +939,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, B && B->nrows == B->ncols, "square operator expected");
   BAMG_REQUIRE(ctx, max_iters >= 0, "max_iters must be nonnegative");
+  cgs_apply_env();
   const int64_t n = B->nrows;
   const int nb = GM_BLOCKS;
   // workspace
@@ -934,6 +991,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
     return 0;
   };
   // the iteration's metric and Givens state (happy flag) in ONE read
+  double last_code = -1.0;  // the step's CGS code, read with the metric
   // x_norm_ready: |x| already in scal[1] (the CGS fast path forms it with x)
   auto metric_state = [&](const double* xv, double* out_host, bool* happy, bool x_norm_ready) -> int {
     if (stopping == 1) {
@@ -945,8 +1003,10 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       if (!x_norm_ready) BAMG_TRY(norm_into(xv, scal + 1));
     }
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(scal + 4, state, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-    double hv3[5];
-    BAMG_TRY(ctx_read_doubles(ctx, scal, 5, hv3));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(scal + 5, flag, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    double hv3[6];
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 6, hv3));
+    last_code = hv3[5];
     if (stopping == 1) *out_host = hv3[0] / denom0;
     else *out_host = hv3[1] == 0.0 ? INFINITY : hv3[0] / hv3[1];
     *happy = hv3[4] != 0.0;
@@ -981,6 +1041,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(e, 0, sizeof(double) * n, ctx->stream));
 
   int iters = 0;
+  int one_pass_steps = 0;  // Arnoldi steps that took the single projection (DGKS)
   bool converged = false;
   bool first_cycle = true;
   while (iters < max_iters && !converged) {
@@ -1020,22 +1081,24 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
         // (n, kernel, device), so the partial-sum tree is reproducible
         const int cb = std::min(cgs_grid(ctx, (const void*)upd, n), cgs_grid(ctx, (const void*)fin, n));
         BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 1) * n, dots, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)nullptr, w, n, part);
-        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)mj * 32, 256), 256, 0, (const double*)part, cb, mj + 1,
-                    mj, hv);
-        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 2) * n, upd, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)hv, w, n, part);
+                        (const double*)nullptr, w, n, part, (const double*)nullptr);
         BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
-                    mj + 1, mj + 1, h2);
+                    mj + 1, mj + 1, hv, (const double*)nullptr, 0u);  // h and |w|^2
+        BAMG_LAUNCH(ctx, cgs_dgks_kernel, 1, 256, 0, mj, (const double*)hv, scal + 3, flag, h2);
+        // second projection (code 0 only; its bytes are booked after the step's read-back)
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 0.0, upd, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)hv, w, n, part, (const double*)flag);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
+                    mj + 1, mj + 1, h2, (const double*)flag, 1u);
         BAMG_LAUNCH(ctx, cgs_pythag_kernel, 1, 256, 0, mj, (const double*)h2, hv, scal + 3, flag);
         BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
-                    y, state, (const double*)flag, 0);
+                    y, state, (const double*)flag, 0b011u);
         BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 5) * n, fin, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)h2, (const double*)y, (const double*)w, x0, (const double*)e,
+                        (const double*)h2, (const double*)hv, (const double*)y, (const double*)w, x0, (const double*)e,
                         (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
         BAMG_LAUNCH(ctx, cgs_fix_norm_kernel, 1, 256, 0, (const double*)flag, (const double*)part, cb, scal + 3);
         BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
-                    y, state, (const double*)flag, 1);
+                    y, state, (const double*)flag, 0b100u);
         BAMG_LAUNCH(ctx, cgs_fix_x_kernel, cb, 256, 0, (const double* const*)W.dVp, mj, (const double*)y, x0,
                     (const double*)e, (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
         BAMG_LAUNCH(ctx, sum_sqrt_kernel, 1, 256, 0, (const double*)part, cb, scal + 1);
@@ -1044,6 +1107,9 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
         double mval;
         bool happy = false;
         BAMG_TRY(metric_state(x, &mval, &happy, true));
+        if (last_code != 1.0 && ((ctx->prof.mask >> FAM_ORTHO) & 1u))  // the second projection ran
+          ctx->prof.bytes[FAM_ORTHO] += 8.0 * (mj + 2) * n;
+        if (last_code == 1.0) ++one_pass_steps;
         history_host[nhist++] = mval;
         if (mval <= rtol) converged = true;
         if (converged || happy || iters >= max_iters) {
@@ -1066,7 +1132,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       // h += h2 (length j+1) via the reduce kernel's accumulate path
       BAMG_LAUNCH(ctx, mreduce_kernel, grid_for((int64_t)(j + 1) * 32, 256), 256, 0, h2, 1, j + 1, hv, 1);
       BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn, y,
-                  state, (const double*)nullptr, 0);
+                  state, (const double*)nullptr, 0u);
       BAMG_LAUNCH(ctx, scale_new_basis_kernel, grd, blk, 0, w, state, n, W.basis[j + 1]);
       ++iters;
       used = j + 1;
@@ -1094,6 +1160,8 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   }
   *iters_host = iters;
   *nhistory_host = nhist;
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] gmres: %d iterations, %d with one projection (DGKS)\n", iters, one_pass_steps);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return converged ? 0 : 1;
 }

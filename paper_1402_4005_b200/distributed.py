@@ -21,7 +21,9 @@ halo ordered by owner rank.  Per application:
 
 Row-local kernels make the result independent of the rank count up to the
 order of the all-reduced sums.  The plan construction (which rows each rank
-needs from which peer) is host bookkeeping on the levels' index arrays.
+needs from which peer) renumbers the rank's slice of each DEVICE operator on
+the device; only the halo id lists cross to the host (for the all-gather of
+requests).
 """
 
 from __future__ import annotations
@@ -196,8 +198,55 @@ def localize_host(A: sp.csr_array, row_part: RowPartition, col_part: RowPartitio
     return loc.indptr.astype(np.int32), new.astype(np.int32), np.ascontiguousarray(loc.data), n_ext, plan
 
 
-def localize(A: sp.csr_array, row_part: RowPartition, col_part: RowPartition, rank: int, comm: Comm):
-    """Device version of localize_host."""
+def _plan_from_halo(halo_ids: np.ndarray, col_part: RowPartition, rank: int, comm: Comm) -> HaloPlan:
+    """Exchange plan for an owner-ordered halo (ids ascending within each owner)."""
+    c0, c1 = col_part.range(rank)
+    owners = col_part.owner(halo_ids)
+    recv_counts, recv_offset, requests = {}, {}, {}
+    off = 0
+    for peer in np.unique(owners):
+        ids = halo_ids[owners == peer]
+        recv_counts[int(peer)] = int(ids.size)
+        recv_offset[int(peer)] = off
+        requests[int(peer)] = ids
+        off += ids.size
+    everyone = comm.all_gather_object(requests)
+    send_local = {}
+    for peer, req in enumerate(everyone):
+        if peer == rank or rank not in req:
+            continue
+        send_local[peer] = (np.asarray(req[rank]) - c0).astype(np.int32)
+    return HaloPlan(c1 - c0, halo_ids, recv_counts, recv_offset, send_local)
+
+
+def localize_device(A: DeviceCSR, row_part: RowPartition, col_part: RowPartition, rank: int, comm: Comm):
+    """localize_host on the device operator: the rank's row slice stays in HBM,
+    its columns are renumbered on the device (owned first, then the halo in
+    owner order -- a contiguous partition makes ascending ids owner-ordered),
+    and only the halo ids (a few grid rows for the lattice strips) come to the
+    host for the plan.  No copy of the operator leaves the device."""
+    r0, r1 = row_part.range(rank)
+    c0, c1 = col_part.range(rank)
+    rp = A.rowptr[r0:r1 + 1]
+    e0, e1 = (int(v) for v in rp[[0, -1]].tolist())
+    cols = A.col[e0:e1].long()
+    vals = A.val[e0:e1]
+    own = (cols >= c0) & (cols < c1)
+    halo = torch.unique(cols[~own])
+    new = torch.empty_like(cols)
+    new[own] = cols[own] - c0
+    new[~own] = (c1 - c0) + torch.searchsorted(halo, cols[~own])
+    plan = _plan_from_halo(halo.cpu().numpy().astype(np.int64), col_part, rank, comm)
+    n_ext = plan.n_own + int(halo.numel())
+    M = DeviceCSR((rp - e0).to(torch.int32).contiguous(), new.to(torch.int32).contiguous(), vals.contiguous(),
+                  (r1 - r0, n_ext))
+    return M, plan
+
+
+def localize(A, row_part: RowPartition, col_part: RowPartition, rank: int, comm: Comm):
+    """Rank-local operator + plan: device path for a DeviceCSR, host path for scipy."""
+    if isinstance(A, DeviceCSR):
+        return localize_device(A, row_part, col_part, rank, comm)
     indptr, cols, vals, n_ext, plan = localize_host(A, row_part, col_part, rank, comm)
     M = DeviceCSR(torch.from_numpy(indptr).to(device()), torch.from_numpy(cols).to(device()),
                   torch.from_numpy(vals).to(device()), (indptr.size - 1, n_ext))
@@ -225,15 +274,15 @@ class DistLevel:
         self.part, self.cpart = part, cpart
         self.r0, self.r1 = part.range(rank)
         self.n_own = self.r1 - self.r0
-        self.B = _DistOp(lev.B, part, part, rank, comm)
+        self.B = _DistOp(lev.dB, part, part, rank, comm)
         d = lev.ddiag[self.r0:self.r1].contiguous()
         self.d = d
         self.skip = engine.degenerate_rows(lev.dB, lev.ddiag)[self.r0:self.r1].contiguous()
         self.omega = omega
         if cpart is not None:
             c0, c1 = cpart.range(rank)
-            self.Q = _DistOp(lev.Q, cpart, part, rank, comm)   # coarse rows, fine columns
-            self.P = _DistOp(lev.P, part, cpart, rank, comm)   # fine rows, coarse columns
+            self.Q = _DistOp(lev.dQ, cpart, part, rank, comm)   # coarse rows, fine columns
+            self.P = _DistOp(lev.dP, part, cpart, rank, comm)   # fine rows, coarse columns
             self.r_ext = torch.empty(self.Q.n_ext, dtype=torch.float64, device=device())
             self.xc_ext = torch.empty(self.P.n_ext, dtype=torch.float64, device=device())
         ne = self.B.n_ext
@@ -333,7 +382,7 @@ class DistSolver:
         lev0 = hierarchy.levels[0]
         self.part = RowPartition(lev0.n, self.comm.world)
         self.r0, self.r1 = self.part.range(self.comm.rank)
-        self.B = _DistOp(lev0.B, self.part, self.part, self.comm.rank, self.comm)
+        self.B = _DistOp(lev0.dB, self.part, self.part, self.comm.rank, self.comm)
         self.x_ext = torch.empty(self.B.n_ext, dtype=torch.float64, device=device())
         self.n_own = self.r1 - self.r0
 

@@ -13,11 +13,16 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
-def _init(rank, world, port):
+def _init(rank, world, port, backend="gloo"):
+    import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     return dist
 
 
@@ -62,16 +67,17 @@ def plan_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def solve_worker(rank, world, port, out_dir, name, agg):
-    """GPU: distributed V-cycle + GMRES on one shared device (host-staged gloo halos)."""
+def solve_worker(rank, world, port, out_dir, name, agg, backend="gloo"):
+    """GPU: distributed V-cycle + GMRES -- gloo: ranks share one device (host-staged
+    halos); nccl: one device per rank (device-buffer p2p and all-reduce)."""
     import torch
     from conftest import csr_from, gmres_args, load_golden
     import paper_1402_4005_b200 as pb
     from paper_1402_4005_b200.chains import ChainProblem
     from paper_1402_4005_b200.distributed import Comm, DistSolver
     from test_gpu_pipeline import _setup_cfg
-    _init(rank, world, port)
-    torch.cuda.set_device(0)
+    _init(rank, world, port, backend)
+    torch.cuda.set_device(rank if backend == "nccl" else 0)
     g = load_golden(name)
     B = csr_from(g, "B")
     prob = ChainProblem(A=None, B=B, n=B.shape[0], family=str(g["family"]), params={},

@@ -40,3 +40,23 @@ def test_two_rank_solve_matches_reference(tmp_path, golden, name, agg):
         assert np.abs(z["x"] - g["x"]).sum() <= 1e-8
         if agg < 1000:
             assert int(z["levels_partitioned"]) >= 2
+
+
+@pytest.mark.parametrize("name,agg", [("pipe_uniform63", 100), ("pipe_tandem32_k16_r30", 100)])
+def test_two_rank_nccl_solve_matches_reference(tmp_path, golden, name, agg):
+    """The NCCL branch (device-buffer halos, all-reduce on the GPU): one rank per
+    device, so it needs two GPUs (the single-GPU pool of this build skips it)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL: one rank per device)")
+    import torch.multiprocessing as mp
+    import dist_workers
+    mp.spawn(dist_workers.solve_worker, args=(2, _port(), str(tmp_path), name, agg, "nccl"), nprocs=2, join=True)
+    g = golden(name)
+    for r in range(2):
+        z = np.load(tmp_path / f"solve_{r}.npz")
+        ref = g["vcycle_out"]
+        assert np.abs(z["vout"] - ref).max() <= 1e-9 * np.abs(ref).max()
+        assert abs(int(z["its"]) - int(g["iterations"])) <= max(1, int(0.1 * int(g["iterations"])))
+        assert np.abs(z["x"] - g["x"]).sum() <= 1e-8
+        assert int(z["levels_partitioned"]) >= 2
