@@ -476,6 +476,24 @@ static inline size_t bt_sweep_smem(int S) {
                            (size_t)BT_NST * BT_MAXCOLS * SL);
 }
 
+// Level 0 of a recursive-doubling plan: A_k = -(Wst_{k+coff})^T (the map from
+// out_{k-dir} to out_k; Wst row-contiguous as the sweep reads it), zero where
+// the recurrence has no term (first step, or W_{k+coff} absent).
+__global__ void bt_dbl_level0_kernel(const double* __restrict__ Wst, int S, int nb, int coff, int dir,
+                                     double* __restrict__ A) {
+  BAMG_PDL_PROLOGUE();
+  const int k = blockIdx.z;
+  const size_t S2 = (size_t)S * S;
+  const int kc = k + coff, kp = k - dir;
+  const bool live = kp >= 0 && kp < nb && kc >= 0 && kc < nb;
+  const double* W = Wst + (size_t)kc * S2;
+  double* Ak = A + (size_t)k * S2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < S * S; t += gridDim.x * blockDim.x) {
+    const int i = t % S, j = t / S;  // A(i, j) column-major = -W_op(i, j) = -Wst[i * S + j]
+    Ak[t] = live ? -W[(size_t)i * S + j] : 0.0;
+  }
+}
+
 // Batched transpose of S x S blocks: out_k = in_k^T (column-major both)
 __global__ void bt_transpose_blocks_kernel(const double* __restrict__ in, int S, int nb, double* __restrict__ out) {
   BAMG_PDL_PROLOGUE();
@@ -649,19 +667,31 @@ __global__ void bt_interleave_kernel(const double* __restrict__ U, const double*
 }  // namespace
 
 // ================================================================== host
+// Recursive-doubling plan of one block recurrence out_k = u_k - W out_{k-dir}:
+// A[l][k] maps out_{k - dir 2^l} to out_k after l doublings (column-major
+// S x S, zero where the chain has already ended).  Applying it is L =
+// ceil(log2 nb) batched GEMMs  u_k += A[l][k] u_{k - dir 2^l}  (ping-pong
+// buffers) instead of nb sequential block steps.
+struct BtDbl {
+  int L = 0, dir = 1;
+  const double* A = nullptr;
+};
+
 // B's factor as the sweeps use it: X_k (k >= 1) and its row-contiguous copy
 // XT_k = X_k^T, Sinv_k = S_k^-1 (the last a {1}-inverse), WT_k = (Sinv_k
 // Up_k)^T (k < nb - 1), V_k = Up_{k-1} Sinv_k (k >= 1; V_k^T row-contiguous
 // is V_k itself)
 struct BtB {
   const double *X, *XT, *Sinv, *WT, *V;
+  BtDbl fL, bU, fUT, bLT;  // doubling plans of the four sweeps of G / G^T (A null: sequential)
 };
 
 struct BandPinv {  // kept for the V-cycle: B^+ b = (I - z z^T) G (I - y y^T) b
   int n = 0, N = 0, S = 0, nb = 0, off = 0;
   double *XT = nullptr, *Sinv = nullptr, *WT = nullptr;  // B's factor for G (device, owned)
+  BtDbl fL, bU;                                          // doubling plans of G's two sweeps (or A null)
   double *z = nullptr, *y = nullptr;                                  // unit null vectors, padded N
-  double *t1 = nullptr, *t2 = nullptr, *dots = nullptr;               // scratch
+  double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *dots = nullptr;  // scratch
   char* slab = nullptr;  // all of the above, one buffer from the context pool
   size_t slab_bytes = 0;
 };
@@ -686,20 +716,89 @@ int bt_blockdiag(bamg_ctx* ctx, int S, int N, const double* A, bool ta, const do
                            N, S, beta, out + (int64_t)k0 * S, N, S, cnt);
 }
 
+int bt_dbl_levels(int nb) {
+  int L = 0;
+  while ((1 << L) < nb) ++L;
+  return L;
+}
+
+// A (L x nb x S^2, caller-owned) <- the doubling plan of the sweep (Wst, coff, dir)
+int bt_dbl_build(bamg_ctx* ctx, int S, int nb, const double* Wst, int coff, int dir, double* A, BtDbl* plan) {
+  const size_t S2 = (size_t)S * S, lvl = S2 * nb;
+  const int L = bt_dbl_levels(nb);
+  plan->L = L;
+  plan->dir = dir;
+  plan->A = A;
+  if (L == 0) return 0;
+  BAMG_LAUNCH_GRID3(ctx, bt_dbl_level0_kernel, dim3((S * S + 255) / 256, 1, nb), dim3(256), 0, Wst, S, nb, coff, dir,
+                    A);
+  for (int l = 0; l + 1 < L; ++l) {
+    const int h = 1 << l;
+    const double* Al = A + l * lvl;
+    double* An = A + (l + 1) * lvl;
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(An, 0, sizeof(double) * lvl, ctx->stream));
+    const int cnt = nb - h;
+    if (cnt <= 0) continue;
+    // A[l+1][k] = A[l][k] A[l][k - dir h] over the k whose partner exists
+    const int k0 = dir > 0 ? h : 0;
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Al + (size_t)k0 * S2, S, (int64_t)S2,
+                               Al + (size_t)(k0 - dir * h) * S2, S, (int64_t)S2, 0.0, An + (size_t)k0 * S2, S,
+                               (int64_t)S2, cnt));
+  }
+  return 0;
+}
+
+// out = the sweep's solution for right-hand sides u (N x p, ld N); buf: N x p
+// scratch; u and out may alias
+int bt_dbl_apply(bamg_ctx* ctx, int S, int nb, int N, const BtDbl& plan, const double* u, double* out, double* buf,
+                 int p) {
+  const size_t S2 = (size_t)S * S, lvl = S2 * nb;
+  // levels alternate between out and buf so that the result lands in out
+  double* bufs[2] = {out, buf};
+  int cur = (plan.L % 2 == 0) ? 0 : 1;  // start so that after L swaps we end in out
+  if (u != bufs[cur])
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(bufs[cur], u, sizeof(double) * N * p, cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int l = 0; l < plan.L; ++l) {
+    const int h = 1 << l;
+    double* src = bufs[cur];
+    double* dst = bufs[cur ^ 1];
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(dst, src, sizeof(double) * N * p, cudaMemcpyDeviceToDevice, ctx->stream));
+    const int cnt = nb - h;
+    if (cnt > 0) {
+      const int k0 = plan.dir > 0 ? h : 0;
+      BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, p, S, 1.0, plan.A + l * lvl + (size_t)k0 * S2, S, (int64_t)S2,
+                                 src + (int64_t)(k0 - plan.dir * h) * S, N, S, 1.0, dst + (int64_t)k0 * S, N, S, cnt));
+    }
+    cur ^= 1;
+  }
+  return 0;
+}
+
 // G in (p columns, padded N): forward with Lb, block-diagonal S^-1, backward
 // with W; G^T: block-diagonal S^-T, forward with V^T, backward with X^T
 int bt_apply_G(bamg_ctx* ctx, int S, int nb, int N, const BtB& F, const double* in, double* tmp, double* out, int p,
-               bool trans) {
+               bool trans, double* dbl) {
+  // dbl: N x p scratch for the doubling plans (needed when they are set)
   if (!trans) {
-    SweepOp f{F.XT, nullptr, 0, +1};
-    BAMG_TRY(bt_sweep(ctx, S, nb, f, in, N, tmp, N, p));
+    if (F.fL.A) {
+      BAMG_TRY(bt_dbl_apply(ctx, S, nb, N, F.fL, in, tmp, dbl, p));
+    } else {
+      SweepOp f{F.XT, nullptr, 0, +1};
+      BAMG_TRY(bt_sweep(ctx, S, nb, f, in, N, tmp, N, p));
+    }
     BAMG_TRY(bt_blockdiag(ctx, S, N, F.Sinv, false, tmp, out, p, 0, nb, 0));
+    if (F.bU.A) return bt_dbl_apply(ctx, S, nb, N, F.bU, out, out, dbl, p);
     SweepOp b{F.WT, nullptr, 0, -1};
     return bt_sweep(ctx, S, nb, b, out, N, out, N, p);  // in place: step k reads u_k before writing out_k
   }
   BAMG_TRY(bt_blockdiag(ctx, S, N, F.Sinv, true, in, tmp, p, 0, nb, 0));
-  SweepOp f{F.V, nullptr, 0, +1};
-  BAMG_TRY(bt_sweep(ctx, S, nb, f, tmp, N, tmp, N, p));
+  if (F.fUT.A) {
+    BAMG_TRY(bt_dbl_apply(ctx, S, nb, N, F.fUT, tmp, tmp, dbl, p));
+  } else {
+    SweepOp f{F.V, nullptr, 0, +1};
+    BAMG_TRY(bt_sweep(ctx, S, nb, f, tmp, N, tmp, N, p));
+  }
+  if (F.bLT.A) return bt_dbl_apply(ctx, S, nb, N, F.bLT, tmp, out, dbl, p);
   SweepOp b{F.X, nullptr, +1, -1};
   return bt_sweep(ctx, S, nb, b, tmp, N, out, N, p);
 }
@@ -728,8 +827,8 @@ int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x
   BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->y, h->dots);
   BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->y,
               (const double*)h->dots, h->t1, N);
-  const BtB F{nullptr, h->XT, h->Sinv, h->WT, nullptr};
-  BAMG_TRY(bt_apply_G(ctx, h->S, h->nb, N, F, h->t1, h->t2, h->t1, 1, false));
+  BtB F{nullptr, h->XT, h->Sinv, h->WT, nullptr, h->fL, h->bU, BtDbl{}, BtDbl{}};
+  BAMG_TRY(bt_apply_G(ctx, h->S, h->nb, N, F, h->t1, h->t2, h->t1, 1, false, h->t3));
   BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->z, h->dots + 1);
   BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->z,
               (const double*)(h->dots + 1), h->t2, N);
@@ -839,7 +938,21 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   }
   BAMG_LAUNCH_GRID3(ctx, bt_transpose_blocks_kernel, dim3((S + 31) / 32, (S + 31) / 32, nb), dim3(32, 8), 0,
                     (const double*)Xb, S, nb, XTb);
-  const BtB FB{Xb, XTb, Sib, Wb, Vb_};
+  BtB FB{Xb, XTb, Sib, Wb, Vb_, BtDbl{}, BtDbl{}, BtDbl{}, BtDbl{}};
+  // recursive-doubling plans of the four sweeps of G / G^T: log2(nb) batched
+  // GEMMs per sweep instead of nb cluster steps; kept only when they reproduce
+  // the sequential sweeps (checked below with the certificate)
+  const int Ld = bt_dbl_levels(nb);
+  double *dfL = nullptr, *dbU = nullptr, *dfUT = nullptr, *dbLT = nullptr;
+  BtDbl pfL, pbU, pfUT, pbLT;
+  const bool use_dbl = Ld > 0 && !(getenv("BAMG_BAND_SEQUENTIAL") && getenv("BAMG_BAND_SEQUENTIAL")[0] == '1');
+  if (use_dbl) {
+    for (double** pp : {&dfL, &dbU, &dfUT, &dbLT}) BAMG_TRY(arena_get(ctx, (size_t)Ld * blk, pp));
+    BAMG_TRY(bt_dbl_build(ctx, S, nb, XTb, 0, +1, dfL, &pfL));
+    BAMG_TRY(bt_dbl_build(ctx, S, nb, Wb, 0, -1, dbU, &pbU));
+    BAMG_TRY(bt_dbl_build(ctx, S, nb, Vb_, 0, +1, dfUT, &pfUT));
+    BAMG_TRY(bt_dbl_build(ctx, S, nb, Xb, +1, -1, dbLT, &pbLT));
+  }
 
   // ---- null vectors of B (padded): z = backward W-sweep from the last
   // block's right null vector, y = Lb^-T (0, ..., 0, left null of S_last)
@@ -849,6 +962,8 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t1));
   BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t2));
   BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t3));
+  double* t4;
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &t4));
   BAMG_TRY(arena_get(ctx, 16, &scal));
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(t1, 0, sizeof(double) * Np, ctx->stream));
   {
@@ -880,12 +995,38 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
     BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for(n, 256), 256, 0, xr, n, 0, 1, 4242u);
     BAMG_TRY(spmm_dev(ctx, B, xr, bx, 1));
     BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for(Np, 256), 256, 0, (const double*)bx, n, n, d.off, Np, 1, t1);
-    BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t1, t2, t3, 1, false));
+    BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t1, t2, t3, 1, false, t4));
+    if (use_dbl) {  // the doubling plans must reproduce the sequential sweeps (G and G^T)
+      BtB FD = FB;
+      FD.fL = pfL;
+      FD.bU = pbU;
+      FD.fUT = pfUT;
+      FD.bLT = pbLT;
+      double *gq = t2 + Np, *gs = t2 + 2 * Np, *gd = t2 + 3 * Np;  // p >= 4 columns of scratch
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FD, t1, gq, gd, 1, false, t4));
+      BAMG_LAUNCH(ctx, bt_diff2_kernel, 1, 256, 0, (const double*)gd, (const double*)t3, Np, scal + 6);
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t1, gq, gs, 1, true, t4));
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FD, t1, gq, gd, 1, true, t4));
+      BAMG_LAUNCH(ctx, bt_diff2_kernel, 1, 256, 0, (const double*)gd, (const double*)gs, Np, scal + 8);
+    }
     BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for(n, 256), 256, 0, (const double*)t3, Np, d.off, n, 1, gbx, n);
     BAMG_TRY(spmm_dev(ctx, B, gbx, bgbx, 1));
     BAMG_LAUNCH(ctx, bt_diff2_kernel, 1, 256, 0, (const double*)bgbx, (const double*)bx, n, scal + 2);
-    double h[5];
-    BAMG_TRY(ctx_read_doubles(ctx, scal, 5, h));
+    double h[10] = {};
+    BAMG_TRY(ctx_read_doubles(ctx, scal, use_dbl ? 10 : 5, h));
+    if (use_dbl) {
+      const double eg = std::sqrt(h[6] / std::max(h[7], 1e-300)), egt = std::sqrt(h[8] / std::max(h[9], 1e-300));
+      const bool dbl_ok = eg <= 1e-11 && egt <= 1e-11;
+      if (getenv("BAMG_DEBUG"))
+        fprintf(stderr, "[bamg] band doubling: |G_dbl b - G b| = %.2e, transposed %.2e -> %s\n", eg, egt,
+                dbl_ok ? "doubling" : "sequential sweeps");
+      if (dbl_ok) {
+        FB.fL = pfL;
+        FB.bU = pbU;
+        FB.fUT = pfUT;
+        FB.bLT = pbLT;
+      }
+    }
     const double bf = std::sqrt(h[1]), tol = 1e-13 * bf / std::sqrt((double)n);
     const bool cert = std::sqrt(h[0]) <= tol && std::sqrt(h[4]) <= tol && std::sqrt(h[2]) <= 1e-10 * std::sqrt(h[3]);
     if (getenv("BAMG_DEBUG"))
@@ -928,11 +1069,11 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
     BAMG_LAUNCH(ctx, bt_rank1_kernel, gg, 256, 0, Yin, Np, Np, p, pre, (const double*)pd, t1, Np);
     if (!trans) {
       BAMG_TRY(mul_F(Cm, XCm, t1, t2, p));                               // F_M
-      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, false));     // G
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, false, t4));     // G
       BAMG_TRY(mul_FT(Cn, XCn, t1, t2, p));                              // F_N^T
     } else {
       BAMG_TRY(mul_F(Cn, XCn, t1, t2, p));                               // F_N
-      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, true));      // G^T
+      BAMG_TRY(bt_apply_G(ctx, S, nb, Np, FB, t2, t3, t1, p, true, t4));      // G^T
       BAMG_TRY(mul_FT(Cm, XCm, t1, t2, p));                              // F_M^T
     }
     BAMG_LAUNCH(ctx, bt_coldot_kernel, p, 256, 0, (const double*)t2, Np, Np, post, pd);
@@ -1051,7 +1192,8 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   h->S = S;
   h->nb = nb;
   h->off = d.off;
-  const size_t nblk = 3 * blk + 4 * (size_t)Np + 8;
+  const bool keep_dbl = FB.fL.A != nullptr;
+  const size_t nblk = 3 * blk + (keep_dbl ? 2 * (size_t)Ld * blk : 0) + 5 * (size_t)Np + 8;
   h->slab_bytes = sizeof(double) * nblk;
   if (pool_take(ctx, h->slab_bytes, &h->slab) != 0) {
     delete h;
@@ -1065,7 +1207,16 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   h->y = h->z + Np;
   h->t1 = h->y + Np;
   h->t2 = h->t1 + Np;
-  h->dots = h->t2 + Np;
+  h->t3 = h->t2 + Np;
+  h->dots = h->t3 + Np;
+  if (keep_dbl) {
+    double* a = h->dots + 8;
+    h->fL = BtDbl{Ld, +1, a};
+    h->bU = BtDbl{Ld, -1, a + (size_t)Ld * blk};
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(a, dfL, sizeof(double) * Ld * blk, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(a + (size_t)Ld * blk, dbU, sizeof(double) * Ld * blk,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   for (auto pr : {std::make_pair(h->XT, (const double*)XTb), std::make_pair(h->Sinv, (const double*)Sib),
                   std::make_pair(h->WT, (const double*)Wb)})
     BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(pr.first, pr.second, sizeof(double) * blk, cudaMemcpyDeviceToDevice,
