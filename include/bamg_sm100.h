@@ -149,6 +149,11 @@ int bamg_chain_planar_count(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int
                             int64_t* nnz_host);
 int bamg_chain_planar_fill(bamg_ctx* ctx, const int32_t* tri, int64_t ntri, int n, const int32_t* rowptr,
                            int32_t* col, double* val);
+/* BASELINE's test vectors without the host: numpy default_rng(seed).random((k, n))
+ * twice (right, then left) from the PCG64 state (st, inc) numpy derives from the
+ * seed, bit-identical, written n x k interleaved (the layout run_setup takes). */
+int bamg_uniform_draws(bamg_ctx* ctx, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int k,
+                       int64_t n, double* right, double* left);
 
 /* ------------------------------------------------------ relax (relax.py) */
 /* skip_i = d_i <= 0 || (sum_j |A_ij| - |d_i|) > 4 d_i.  Pass the explicit

@@ -65,6 +65,7 @@ _SIGS = {
     "bamg_chain_lattice_count": [P, C.c_int, C.c_int, F64, F64, F64, P, P, PI64],
     "bamg_chain_lattice_fill": [P, C.c_int, C.c_int, F64, F64, F64, P, P, P],
     "bamg_chain_planar_count": [P, P, I64, C.c_int, P, PI64],
+    "bamg_uniform_draws": [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, I64, P, P],
     "bamg_chain_planar_fill": [P, P, I64, C.c_int, P, P, P],
     "bamg_spgemm_count": [P, PCSR, PCSR, C.c_int, P, PI64],
     "bamg_spgemm_fill": [P, PCSR, PCSR, C.c_int, P, P, P],

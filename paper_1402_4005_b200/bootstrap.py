@@ -260,7 +260,13 @@ def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps 
     ops = ops or _LevelOps(A)
     n = A.shape[0]
     r = cfg.n_tests
-    if draws is None:
+    if isinstance(draws, str):
+        if draws != "uniform":
+            raise ValueError(f"unknown draws {draws!r} (expected 'uniform' or a (right, left) pair)")
+        # BASELINE's uniform(0,1) vectors, default_rng(cfg.seed).random((r, n)) twice,
+        # generated on the device (engine.uniform_draws: numpy's PCG64, bit-identical)
+        right_h, left_h = engine.uniform_draws(cfg.seed, r, n)
+    elif draws is None:
         if rng is None:
             rng = np.random.default_rng(np.random.SeedSequence(cfg.seed))
         right_h = rng.standard_normal((r, n))
@@ -458,8 +464,10 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     """Full setup: initial vectors, the configured cycles, x0 (bootstrap.py:395-429).
 
     `draws=(right, left)` injects the raw (k, n) initial vectors (BASELINE's
-    uniform(0,1) seed-0 vectors); otherwise the reference's own
-    SeedSequence(seed).spawn(2)[0] standard-normal stream is used.
+    uniform(0,1) seed-0 vectors); `draws="uniform"` draws those vectors
+    (default_rng(cfg.seed).random, right then left) on the device; otherwise
+    the reference's own SeedSequence(seed).spawn(2)[0] standard-normal stream
+    is used.
     """
     t0 = time.perf_counter()
     A = B_device if B_device is not None else as_device(problem.B)

@@ -281,3 +281,66 @@ extern "C" int bamg_chain_planar_fill(bamg_ctx* ctx, const int32_t* tri, int64_t
               (const int32_t*)deg, n, rowptr, col, val);
   return 0;
 }
+
+// ------------------------------------------- seeded test vectors on device
+// BASELINE.json's test vectors are numpy's default_rng(seed).random((k, n))
+// twice (right, then left).  numpy's PCG64 is a 128-bit LCG (multiplier
+// 0x2360ed051fc65da44385df649fccf645) with the XSL-RR 128/64 output, and
+// random() maps a draw u to (u >> 11) * 2^-53.  Each thread jumps its LCG
+// ahead to the start of its chunk (binary powers of the affine step) and
+// produces the chunk: the same doubles as numpy, bit for bit, written in the
+// engine's n x k interleaved layout -- no 2 k n x 8-byte host upload.
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)2549297995355413924ull << 64) | (u128)4865540595714422341ull;
+}
+
+__device__ __forceinline__ uint64_t pcg_xsl_rr(u128 s) {
+  const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+  const unsigned rot = (unsigned)(s >> 122);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+__global__ void pcg64_uniform_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                     int64_t total, int64_t chunk, int k, int64_t n, double* __restrict__ right,
+                                     double* __restrict__ left) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = t * chunk;
+  if (i0 >= total) return;
+  const u128 inc = ((u128)inc_hi << 64) | inc_lo;
+  u128 s = ((u128)st_hi << 64) | st_lo;
+  // s <- state after i0 steps: (A, C) = step^i0 by binary powers
+  u128 A = 1, C = 0, a = pcg_mult(), c = inc;
+  for (int64_t e = i0; e; e >>= 1) {
+    if (e & 1) {
+      A = a * A;
+      C = a * C + c;
+    }
+    c = a * c + c;
+    a = a * a;
+  }
+  s = A * s + C;
+  const int64_t kn = (int64_t)k * n;
+  const int64_t i1 = min(total, i0 + chunk);
+  const u128 m = pcg_mult();
+  for (int64_t i = i0; i < i1; ++i) {
+    s = s * m + inc;
+    const double v = (double)(pcg_xsl_rr(s) >> 11) * (1.0 / 9007199254740992.0);
+    const int64_t j = i < kn ? i : i - kn;  // position in the (k, n) C-order draw
+    const int64_t c = j / n, row = j - c * n;
+    (i < kn ? right : left)[row * k + c] = v;
+  }
+}
+
+extern "C" int bamg_uniform_draws(bamg_ctx* ctx, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                  int k, int64_t n, double* right, double* left) {
+  BAMG_REQUIRE(ctx, k >= 1 && n >= 1 && right && left, "bad draw shape");
+  const int64_t total = 2 * (int64_t)k * n;
+  const int64_t chunk = 256;
+  const int64_t threads = (total + chunk - 1) / chunk;
+  BAMG_LAUNCH(ctx, pcg64_uniform_kernel, grid_for(threads, 128), 128, 0, st_hi, st_lo, inc_hi, inc_lo, total, chunk, k,
+              n, right, left);
+  return 0;
+}

@@ -427,6 +427,19 @@ def coarsest_triplets_band(B: DeviceCSR, Bt: DeviceCSR, M: DeviceCSR, N: DeviceC
     return U, V, s, CoarseLU(lu, n)
 
 
+def uniform_draws(seed: int, k: int, n: int):
+    """numpy default_rng(seed).random((k, n)) twice (right, then left) generated on
+    the device (PCG64 jump-ahead, bit-identical), as n x k interleaved blocks."""
+    import numpy as np
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    right = _empty((n, k))
+    left = _empty((n, k))
+    _lib.call("bamg_uniform_draws", s >> 64, s & m64, inc >> 64, inc & m64, int(k), int(n), _p(right), _p(left))
+    return right, left
+
+
 def sign_fix_l1(x, stride=1, uniform_fallback=False):
     n = x.shape[0]
     out = _empty(n)

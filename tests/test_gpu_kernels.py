@@ -321,6 +321,17 @@ def test_device_lattice_chain_matches_host(eng, family, side):
     assert np.array_equal(dev.geometry.cpu().numpy().T, host.geometry)
 
 
+@pytest.mark.parametrize("seed,k,n", [(0, 8, 1), (0, 16, 1000), (0, 8, 100_003), (7, 12, 4097)])
+def test_device_uniform_draws_match_numpy(eng, seed, k, n):
+    """BASELINE's test vectors drawn on the device (numpy PCG64 jump-ahead):
+    default_rng(seed).random((k, n)) twice, bit for bit, n x k interleaved."""
+    from paper_1402_4005_b200 import engine
+    g = np.random.default_rng(seed)
+    right, left = g.random((k, n)), g.random((k, n))
+    dr, dl = engine.uniform_draws(seed, k, n)
+    assert np.array_equal(dr.cpu().numpy(), right.T) and np.array_equal(dl.cpu().numpy(), left.T)
+
+
 @pytest.mark.parametrize("n", [4, 5, 100, 1024, 30_000])
 def test_device_planar_chain_matches_host(eng, n):
     """On-device assembly of the planar chain from its Delaunay triangles
