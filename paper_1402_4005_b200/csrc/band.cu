@@ -55,6 +55,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int BT_MAX_S = 160;
+__device__ bool bt_debug = false;
 constexpr int BT_CL = 8;         // CTAs per sweep cluster
 constexpr int BT_THREADS = 256;  // threads per sweep CTA
 constexpr int BT_MAXCOLS = 8;    // right-hand sides per sweep cluster
@@ -203,7 +204,11 @@ __device__ __forceinline__ void bt_gj_body(const GJJob& J, int* bad) {
     const int p = s_p;
     const double piv = s_piv;
     if (!(fabs(piv) > tiny)) {
-      if (tid == 0) atomicExch(bad, 1);
+      if (tid == 0) {
+        atomicExch(bad, 1);
+        if (bt_debug) printf("[bamg gj] block %d: pivot %.3e at column %d of %d (max %.3e)\n", (int)blockIdx.x, piv, k, m,
+                             tiny * 1e14);
+      }
       return;
     }
     const double inv = 1.0 / piv;
@@ -513,6 +518,54 @@ __global__ void bt_transpose_blocks_kernel(const double* __restrict__ in, int S,
   }
 }
 
+// ---------------------------------------------------- cyclic reduction
+// GJ inverses of `count` blocks at stride sA (one CTA each): the eliminated
+// blocks of one cyclic-reduction level, all at once.
+__global__ void __launch_bounds__(1024) bt_gj_batched_kernel(const double* __restrict__ A, int64_t sA,
+                                                             double* __restrict__ out, int64_t sO, int S, int* bad) {
+  BAMG_PDL_PROLOGUE();
+  const GJJob J{A + sA * blockIdx.x, out + sO * blockIdx.x, nullptr, nullptr, S, 0};
+  bt_gj_body(J, bad);
+}
+
+// dst (count compact S x p blocks, ld S) <- blocks of the N x p matrix X (ld N)
+// starting at row r0, one every rstride rows
+__global__ void bt_blocks_gather_kernel(const double* __restrict__ X, int ldx, int64_t r0, int64_t rstride, int S,
+                                        int p, int count, double* __restrict__ dst) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t total = (int64_t)count * S * p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % S);
+    const int64_t rest = t / S;
+    const int c = (int)(rest % p), b = (int)(rest / p);
+    dst[t] = X[(size_t)c * ldx + r0 + (int64_t)b * rstride + i];
+  }
+}
+
+// Y = A X for a CSR A (n x n) and column-major n x p blocks (ld ldx / ldy)
+__global__ void bt_csr_cm_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, int n, const double* __restrict__ X, int ldx,
+                                 double* __restrict__ Y, int ldy, int p) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t total = (int64_t)n * p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % n), c = (int)(t / n);
+    const double* x = X + (size_t)c * ldx;
+    double s = 0.0;
+    for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) s = fma(val[e], x[col[e]], s);
+    Y[(size_t)c * ldy + i] = s;
+  }
+}
+
+// X[:, c] *= w[c]
+__global__ void bt_scale_cols_kernel(double* X, int ld, int n, int p, const double* __restrict__ w) {
+  BAMG_PDL_PROLOGUE();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * p) return;
+  const int r = (int)(t % n), c = (int)(t / n);
+  X[(size_t)c * ld + r] *= w[c];
+}
+
 // ------------------------------------------------------- small vector ops
 __global__ void bt_embed_kernel(const double* __restrict__ X, int ldx, int n, int off, int N, int p,
                                 double* __restrict__ Y) {
@@ -694,6 +747,7 @@ struct BandPinv {  // kept for the V-cycle: B^+ b = (I - z z^T) G (I - y y^T) b
   double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *dots = nullptr;  // scratch
   char* slab = nullptr;  // all of the above, one buffer from the context pool
   size_t slab_bytes = 0;
+  struct CRF* cr = nullptr;  // cyclic-reduction factor (band_cr_triplets), else the Thomas blocks above
 };
 
 namespace {
@@ -821,12 +875,22 @@ int bt_assemble(bamg_ctx* ctx, const bamg_csr* A, const BtDims& d, int sym, doub
 
 }  // namespace
 
+int cr_solve_public(bamg_ctx* ctx, const CRF& F, double* X, int N, int p, bool trans, double* T);
+
 int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x) {
   const int n = h->n, N = h->N;
   BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for(N, 256), 256, 0, b, n, n, h->off, N, 1, h->t1);
   BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->y, h->dots);
   BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->y,
               (const double*)h->dots, h->t1, N);
+  if (h->cr) {
+    BAMG_TRY(cr_solve_public(ctx, *h->cr, h->t1, N, 1, false, h->t3));
+    BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->z, h->dots + 1);
+    BAMG_LAUNCH(ctx, bt_rank1_kernel, grid_for(N, 256), 256, 0, (const double*)h->t1, N, N, 1, (const double*)h->z,
+                (const double*)(h->dots + 1), h->t2, N);
+    BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for(n, 256), 256, 0, (const double*)h->t2, N, h->off, n, 1, x, n);
+    return 0;
+  }
   BtB F{nullptr, h->XT, h->Sinv, h->WT, nullptr, h->fL, h->bU, BtDbl{}, BtDbl{}};
   BAMG_TRY(bt_apply_G(ctx, h->S, h->nb, N, F, h->t1, h->t2, h->t1, 1, false, h->t3));
   BAMG_LAUNCH(ctx, bt_coldot_kernel, 1, 256, 0, (const double*)h->t1, N, N, (const double*)h->z, h->dots + 1);
@@ -841,7 +905,504 @@ int band_pinv_apply(bamg_ctx* ctx, const BandPinv* h, const double* b, double* x
 void band_pinv_free(bamg_ctx* ctx, BandPinv* h) {
   if (!h) return;
   if (h->slab) pool_give(ctx, h->slab, h->slab_bytes);
+  delete h->cr;
   delete h;
+}
+
+
+// ================================================= cyclic-reduction path
+// Block cyclic reduction of the block-tridiagonal B (nb = 2^L blocks): level
+// l eliminates the even blocks of the current system (their inverses in ONE
+// batched Gauss-Jordan launch) and leaves the odd ones with
+//   D'_k = D_k - a_k U_{k-1} - b_k L_{k+1},  L'_k = -a_k L_{k-1},
+//   U'_k = -b_k U_{k+1},   a_k = L_k D_{k-1}^-1,  b_k = U_k D_{k+1}^-1,
+// (batched DMMA GEMMs); the last block of B survives every level and carries
+// the rank deficiency: its bordered Gauss-Jordan gives the {1}-inverse and
+// its null vectors.  L levels of independent work replace the nb sequential
+// steps of the block-Thomas recurrence.  The solve G x (G a {1}-inverse of B)
+// is the reduction (odd blocks -= a x_even_left + b x_even_right), the final
+// block, and the back substitution (even blocks = D^-1 (x - Le x_odd_left -
+// Ue x_odd_right)); G^T applies the transposed steps in reverse order with
+// the same blocks, so B^T needs no factorisation of its own.
+struct CRF {
+  int S = 0, nb = 0, L = 0;
+  double* base = nullptr;  // per level l (e = nb >> (l+1) blocks each): Dinv, Le, Ue, al, be; then Gf, qf, rf
+  size_t S2() const { return (size_t)S * S; }
+  size_t lvl_off(int l) const {
+    size_t o = 0;
+    for (int i = 0; i < l; ++i) o += 5 * (size_t)(nb >> (i + 1)) * S2();
+    return o;
+  }
+  double* Dinv(int l) const { return base + lvl_off(l); }
+  double* Le(int l) const { return Dinv(l) + (size_t)(nb >> (l + 1)) * S2(); }
+  double* Ue(int l) const { return Le(l) + (size_t)(nb >> (l + 1)) * S2(); }
+  double* al(int l) const { return Ue(l) + (size_t)(nb >> (l + 1)) * S2(); }
+  double* be(int l) const { return al(l) + (size_t)(nb >> (l + 1)) * S2(); }
+  double* Gf() const { return base + lvl_off(L); }
+  double* qf() const { return Gf() + S2(); }
+  double* rf() const { return qf() + S; }
+  static size_t doubles(int S, int nb, int L) {
+    size_t o = 0;
+    for (int i = 0; i < L; ++i) o += 5 * (size_t)(nb >> (i + 1)) * S * S;
+    return o + (size_t)S * S + 2 * (size_t)S;
+  }
+};
+
+namespace {
+
+int bt_gemm_b(bamg_ctx* ctx, bool ta, int S, int p, double alpha, const double* A, int64_t sA, const double* B,
+              int ldb, int64_t sB, double beta, double* C, int ldc, int64_t sC, int cnt) {
+  if (cnt <= 0) return 0;
+  return dgemm_batched_dev(ctx, ta, false, S, p, S, alpha, A, S, sA, B, ldb, sB, beta, C, ldc, sC, cnt);
+}
+
+// factor the block-tridiagonal (D, Lr, U) (nb blocks each, Lr[k] = A(k, k-1),
+// Lr[0] = 0, U[nb-1] = 0; all overwritten) into F; returns 1 on a tiny pivot
+int cr_factor(bamg_ctx* ctx, int S, int nb, double* D, double* Lr, double* U, double* D2, double* L2, double* U2,
+              CRF& F, int* bad) {
+  const size_t S2 = (size_t)S * S;
+  const int64_t s1 = (int64_t)S2, s2 = 2 * (int64_t)S2;
+  const size_t gj = bt_step_smem(S);
+  BAMG_TRY(smem_optin(ctx, (const void*)bt_gj_batched_kernel, gj));
+  BAMG_TRY(smem_optin(ctx, (const void*)bt_step_kernel, gj));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int) * 2, ctx->stream));
+  double *Dw = D, *Lw = Lr, *Uw = U, *Dn = D2, *Ln = L2, *Un = U2;
+  for (int l = 0; l < F.L; ++l) {
+    const int m = nb >> l, e = m / 2;
+    // even blocks' inverses, all at once
+    BAMG_LAUNCH(ctx, bt_gj_batched_kernel, e, 1024, gj, (const double*)Dw, s2, F.Dinv(l), s1, S, bad);
+    if (getenv("BAMG_DEBUG")) {
+      int hb0 = 0;
+      BAMG_TRY(ctx_read_i32(ctx, bad, 1, &hb0));
+      if (hb0) fprintf(stderr, "[bamg] band CR: tiny pivot at level %d (m=%d)\n", l, m);
+    }
+    double *al = F.al(l), *be = F.be(l);
+    // a_i = L_{2i+1} Dinv_i ;  b_i = U_{2i+1} Dinv_{i+1}
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Lw + S2, S, s2, F.Dinv(l), S, s1, 0.0, al, S, s1, e));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(be + (size_t)(e - 1) * S2, 0, sizeof(double) * S2, ctx->stream));
+    if (e > 1)
+      BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, 1.0, Uw + S2, S, s2, F.Dinv(l) + S2, S, s1, 0.0, be, S,
+                                 s1, e - 1));
+    // D'_i = D_{2i+1} - a_i U_{2i} - b_i L_{2i+2}
+    BAMG_CHECK_CUDA(ctx, cudaMemcpy2DAsync(Dn, S2 * sizeof(double), Dw + S2, 2 * S2 * sizeof(double),
+                                           S2 * sizeof(double), e, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, -1.0, al, S, s1, Uw, S, s2, 1.0, Dn, S, s1, e));
+    if (e > 1)
+      BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, -1.0, be, S, s1, Lw + 2 * S2, S, s2, 1.0, Dn, S, s1,
+                                 e - 1));
+    // L'_i = -a_i L_{2i} (i >= 1), U'_i = -b_i U_{2i+2} (i <= e-2)
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(Ln, 0, sizeof(double) * S2 * e, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(Un, 0, sizeof(double) * S2 * e, ctx->stream));
+    if (e > 1) {
+      BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, -1.0, al + S2, S, s1, Lw + 2 * S2, S, s2, 0.0, Ln + S2,
+                                 S, s1, e - 1));
+      BAMG_TRY(dgemm_batched_dev(ctx, false, false, S, S, S, -1.0, be, S, s1, Uw + 2 * S2, S, s2, 0.0, Un, S, s1,
+                                 e - 1));
+    }
+    // the eliminated blocks' couplings, for the back substitution
+    BAMG_CHECK_CUDA(ctx, cudaMemcpy2DAsync(F.Le(l), S2 * sizeof(double), Lw, 2 * S2 * sizeof(double),
+                                           S2 * sizeof(double), e, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpy2DAsync(F.Ue(l), S2 * sizeof(double), Uw, 2 * S2 * sizeof(double),
+                                           S2 * sizeof(double), e, cudaMemcpyDeviceToDevice, ctx->stream));
+    std::swap(Dw, Dn);
+    std::swap(Lw, Ln);
+    std::swap(Uw, Un);
+  }
+  // the surviving (last) block: bordered Gauss-Jordan -> {1}-inverse, null vectors
+  GJJobs jobs{};
+  jobs.j[0] = GJJob{Dw, F.Gf(), F.qf(), F.rf(), S, 1};
+  CholJobs cj{};
+  BAMG_LAUNCH(ctx, bt_step_kernel, 1, 1024, gj, jobs, 1, cj, 0, bad, bad + 1);
+  int hb[2];
+  BAMG_TRY(ctx_read_i32(ctx, bad, 2, hb));
+  return hb[0] ? 1 : 0;
+}
+
+// X (N x p, ld N) <- G X (trans: G^T X), in place; T: scratch of nb/2 * S * p doubles
+int cr_solve(bamg_ctx* ctx, const CRF& F, double* X, int N, int p, bool trans, double* T) {
+  const int S = F.S, nb = F.nb, L = F.L;
+  const size_t S2 = (size_t)S * S;
+  const int64_t s1 = (int64_t)S2;
+  // Dinv application to the even blocks of level l: X_even <- op(Dinv) X_even (via T)
+  auto dinv = [&](int l, bool ta) -> int {
+    const int64_t h = (int64_t)1 << l;
+    const int e = nb >> (l + 1);
+    const int64_t tot = (int64_t)e * S * p;
+    BAMG_LAUNCH(ctx, bt_blocks_gather_kernel, std::min(grid_for(tot, 256), 8 * ctx->num_sms), 256, 0,
+                (const double*)X, N, (h - 1) * S, 2 * h * S, S, p, e, T);
+    return bt_gemm_b(ctx, ta, S, p, 1.0, F.Dinv(l), s1, T, S, (int64_t)S * p, 0.0, X + (h - 1) * S, N, 2 * h * S, e);
+  };
+  auto fin = [&](bool ta) -> int {
+    const int64_t tot = (int64_t)S * p;
+    BAMG_LAUNCH(ctx, bt_blocks_gather_kernel, grid_for(tot, 256), 256, 0, (const double*)X, N, (int64_t)(nb - 1) * S,
+                (int64_t)S, S, p, 1, T);
+    return bt_gemm_b(ctx, ta, S, p, 1.0, F.Gf(), s1, T, S, (int64_t)S * p, 0.0, X + (int64_t)(nb - 1) * S, N, 0, 1);
+  };
+  if (!trans) {
+    for (int l = 0; l < L; ++l) {  // reduction: odd_i -= a_i even_i + b_i even_{i+1}
+      const int64_t h = (int64_t)1 << l;
+      const int e = nb >> (l + 1);
+      BAMG_TRY(bt_gemm_b(ctx, false, S, p, -1.0, F.al(l), s1, X + (h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (2 * h - 1) * S, N, 2 * h * S, e));
+      BAMG_TRY(bt_gemm_b(ctx, false, S, p, -1.0, F.be(l), s1, X + (3 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (2 * h - 1) * S, N, 2 * h * S, e - 1));
+    }
+    BAMG_TRY(fin(false));
+    for (int l = L - 1; l >= 0; --l) {  // back substitution: even_i = Dinv (even_i - Ue odd_i - Le odd_{i-1})
+      const int64_t h = (int64_t)1 << l;
+      const int e = nb >> (l + 1);
+      BAMG_TRY(bt_gemm_b(ctx, false, S, p, -1.0, F.Ue(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (h - 1) * S, N, 2 * h * S, e));
+      BAMG_TRY(bt_gemm_b(ctx, false, S, p, -1.0, F.Le(l) + S2, s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (3 * h - 1) * S, N, 2 * h * S, e - 1));
+      BAMG_TRY(dinv(l, false));
+    }
+    return 0;
+  }
+  for (int l = 0; l < L; ++l) {  // K_l^T: even = Dinv^T even; odd_i -= Ue_i^T even_i + Le_{i+1}^T even_{i+1}
+    const int64_t h = (int64_t)1 << l;
+    const int e = nb >> (l + 1);
+    BAMG_TRY(dinv(l, true));
+    BAMG_TRY(bt_gemm_b(ctx, true, S, p, -1.0, F.Ue(l), s1, X + (h - 1) * S, N, 2 * h * S, 1.0, X + (2 * h - 1) * S,
+                       N, 2 * h * S, e));
+    BAMG_TRY(bt_gemm_b(ctx, true, S, p, -1.0, F.Le(l) + S2, s1, X + (3 * h - 1) * S, N, 2 * h * S, 1.0,
+                       X + (2 * h - 1) * S, N, 2 * h * S, e - 1));
+  }
+  BAMG_TRY(fin(true));
+  for (int l = L - 1; l >= 0; --l) {  // R_l^T: even_i -= a_i^T odd_i ; even_{i+1} -= b_i^T odd_i
+    const int64_t h = (int64_t)1 << l;
+    const int e = nb >> (l + 1);
+    BAMG_TRY(bt_gemm_b(ctx, true, S, p, -1.0, F.al(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0, X + (h - 1) * S,
+                       N, 2 * h * S, e));
+    BAMG_TRY(bt_gemm_b(ctx, true, S, p, -1.0, F.be(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                       X + (3 * h - 1) * S, N, 2 * h * S, e - 1));
+  }
+  return 0;
+}
+
+// right null vector (B z = 0): back substitution from (0, ..., 0, qf);
+// left null vector (B^T y = 0): transposed reduction from (0, ..., 0, rf)
+int cr_null(bamg_ctx* ctx, const CRF& F, double* X, int N, bool left, double* T) {
+  const int S = F.S, nb = F.nb, L = F.L;
+  const size_t S2 = (size_t)S * S;
+  const int64_t s1 = (int64_t)S2;
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(X, 0, sizeof(double) * N, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(X + (size_t)(nb - 1) * S, left ? F.rf() : F.qf(), sizeof(double) * S,
+                                       cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int l = L - 1; l >= 0; --l) {
+    const int64_t h = (int64_t)1 << l;
+    const int e = nb >> (l + 1);
+    if (left) {
+      BAMG_TRY(bt_gemm_b(ctx, true, S, 1, -1.0, F.al(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (h - 1) * S, N, 2 * h * S, e));
+      BAMG_TRY(bt_gemm_b(ctx, true, S, 1, -1.0, F.be(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (3 * h - 1) * S, N, 2 * h * S, e - 1));
+    } else {
+      BAMG_TRY(bt_gemm_b(ctx, false, S, 1, -1.0, F.Ue(l), s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (h - 1) * S, N, 2 * h * S, e));
+      BAMG_TRY(bt_gemm_b(ctx, false, S, 1, -1.0, F.Le(l) + S2, s1, X + (2 * h - 1) * S, N, 2 * h * S, 1.0,
+                         X + (3 * h - 1) * S, N, 2 * h * S, e - 1));
+      const int64_t tot = (int64_t)e * S;
+      BAMG_LAUNCH(ctx, bt_blocks_gather_kernel, grid_for(tot, 256), 256, 0, (const double*)X, N, (h - 1) * S,
+                  2 * h * S, S, 1, e, T);
+      BAMG_TRY(bt_gemm_b(ctx, false, S, 1, 1.0, F.Dinv(l), s1, T, S, (int64_t)S, 0.0, X + (h - 1) * S, N, 2 * h * S,
+                         e));
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+
+int cr_solve_public(bamg_ctx* ctx, const CRF& F, double* X, int N, int p, bool trans, double* T) {
+  return cr_solve(ctx, F, X, N, p, trans, T);
+}
+
+// ---- the CR path's triplets: subspace iteration in the original variables
+// (no factor of M or N): with G a {1}-inverse of B, y / z the left / right
+// null vectors of B, P_y u = u - y (y^T M u) / (y^T M y) and P_z v = v - z
+// (z^T N v) / (z^T N z), the iteration of dense_large.cu on K^+ is
+//   u <- P_y G^T N P_z v   (M-orthonormalised),   v <- P_z G M P_y u   (N-orthonormalised)
+// (K = F_M^-1 B F_N^-T for any factors M = F_M F_M^T, N = F_N F_N^T; the
+// vectors a = F_M^T u, b = F_N^T v are never formed), Ritz values from the
+// p x p M-Gram of u, and the final vectors come out M- / N-normalised as
+// bootstrap.py:256-260 wants.
+int band_cr_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const bamg_csr* M, const bamg_csr* Nm,
+                     int r, const double* Vin, double* U, double* V, double* sigma, BandPinv** keep) {
+  *keep = nullptr;
+  const int n = B->nrows;
+  if (getenv("BAMG_DEBUG")) {
+    const bool on = true;
+    cudaMemcpyToSymbol(bt_debug, &on, sizeof(bool));
+  }
+  int* bw;
+  BAMG_TRY(arena_get(ctx, 8, &bw));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bw, 0, sizeof(int) * 8, ctx->stream));
+  BAMG_LAUNCH(ctx, bt_bandwidth_kernel, std::min(grid_for(n, 256), 2 * ctx->num_sms), 256, 0, B->rowptr, B->col, n,
+              bw);
+  int hb[2];
+  BAMG_TRY(ctx_read_i32(ctx, bw, 2, hb));
+  const int band = std::max({hb[0], hb[1], 1});
+  const int S = std::max(32, (band + 7) / 8 * 8);
+  int nb = 2;
+  while ((int64_t)nb * S < n) nb *= 2;
+  if (S > BT_MAX_S || S * 4 > n) return 1;
+  int L = 0;
+  while ((1 << L) < nb) ++L;
+  const int Np = nb * S, off = Np - n;
+  const size_t S2 = (size_t)S * S, blk = S2 * nb;
+  const int p = std::min(r + 12, n);
+  BAMG_REQUIRE(ctx, p <= 48, "band path: subspace block too wide");
+  BtDims d{n, Np, S, nb, off};
+  // ---- factor
+  double *D, *Lo, *Up, *Lr, *D2, *L2, *U2;
+  for (double** pp : {&D, &Lo, &Up, &Lr, &D2, &L2, &U2}) BAMG_TRY(arena_get(ctx, blk, pp));
+  int* bad;
+  BAMG_TRY(arena_get(ctx, 4, &bad));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int) * 4, ctx->stream));
+  BAMG_TRY(bt_assemble(ctx, B, d, 0, D, Lo, Up, bad));
+  // Lr[k] = A(k, k-1) = Lo[k-1], Lr[0] = 0
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(Lr, 0, sizeof(double) * S2, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Lr + S2, Lo, sizeof(double) * S2 * (nb - 1), cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+  CRF F;
+  F.S = S;
+  F.nb = nb;
+  F.L = L;
+  BAMG_TRY(arena_get(ctx, CRF::doubles(S, nb, L), &F.base));
+  const int frc = cr_factor(ctx, S, nb, D, Lr, Up, D2, L2, U2, F, bad + 2);
+  if (frc < 0) return frc;
+  if (frc > 0) {
+    if (getenv("BAMG_DEBUG")) fprintf(stderr, "[bamg] band CR n=%d S=%d: tiny pivot -> dense path\n", n, S);
+    return 1;
+  }
+  // ---- null vectors (padded, then unit)
+  double *zN, *yN, *T, *xa, *xb, *scal;
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &zN));
+  BAMG_TRY(arena_get(ctx, (size_t)Np, &yN));
+  BAMG_TRY(arena_get(ctx, (size_t)(nb / 2 + 1) * S * p, &T));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &xa));
+  BAMG_TRY(arena_get(ctx, (size_t)Np * p, &xb));
+  BAMG_TRY(arena_get(ctx, 16, &scal));
+  BAMG_TRY(cr_null(ctx, F, zN, Np, false, T));
+  BAMG_TRY(cr_null(ctx, F, yN, Np, true, T));
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, zN, Np, Np, (double*)nullptr);
+  BAMG_LAUNCH(ctx, bt_colnorm_kernel, 1, 256, 0, yN, Np, Np, (double*)nullptr);
+  const double* z = zN + off;  // unpadded views (the padding entries are zero)
+  const double* y = yN + off;
+  // ---- certificate: |B z|, |B^T y| at round-off; B G B x = B x
+  {
+    double *bz, *bty, *xr, *bx, *gbx, *bgbx;
+    for (double** pp : {&bz, &bty, &xr, &bx, &gbx, &bgbx}) BAMG_TRY(arena_get(ctx, (size_t)n, pp));
+    BAMG_TRY(spmm_dev(ctx, B, z, bz, 1));
+    BAMG_TRY(spmm_dev(ctx, Bt, y, bty, 1));
+    BAMG_LAUNCH(ctx, bt_norms2_kernel, 1, 256, 0, (const double*)bz, n, (const double*)B->val, (int)B->nnz, scal);
+    BAMG_LAUNCH(ctx, bt_norms2_kernel, 1, 256, 0, (const double*)bty, n, (const double*)bty, 0, scal + 4);
+    BAMG_LAUNCH(ctx, bt_fill_random_kernel, grid_for(n, 256), 256, 0, xr, n, 0, 1, 4242u);
+    BAMG_TRY(spmm_dev(ctx, B, xr, bx, 1));
+    BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for(Np, 256), 256, 0, (const double*)bx, n, n, off, Np, 1, xa);
+    BAMG_TRY(cr_solve(ctx, F, xa, Np, 1, false, T));
+    BAMG_LAUNCH(ctx, bt_extract_kernel, grid_for(n, 256), 256, 0, (const double*)xa, Np, off, n, 1, gbx, n);
+    BAMG_TRY(spmm_dev(ctx, B, gbx, bgbx, 1));
+    BAMG_LAUNCH(ctx, bt_diff2_kernel, 1, 256, 0, (const double*)bgbx, (const double*)bx, n, scal + 2);
+    double h[5];
+    BAMG_TRY(ctx_read_doubles(ctx, scal, 5, h));
+    const double bf = std::sqrt(h[1]), tol = 1e-13 * bf / std::sqrt((double)n);
+    const bool cert = std::sqrt(h[0]) <= tol && std::sqrt(h[4]) <= tol && std::sqrt(h[2]) <= 1e-10 * std::sqrt(h[3]);
+    if (getenv("BAMG_DEBUG"))
+      fprintf(stderr, "[bamg] band CR n=%d S=%d nb=%d |Bz|=%.3e |B^Ty|=%.3e |B|F=%.3e |BGBx-Bx|/|Bx|=%.3e -> %s\n", n,
+              S, nb, std::sqrt(h[0]), std::sqrt(h[4]), bf, std::sqrt(h[2]) / std::sqrt(h[3]),
+              cert ? "certified" : "dense path");
+    if (!cert) return 1;
+  }
+  // ---- projections in the M / N inner products: cy = M y / (y^T M y), cz = N z / (z^T N z)
+  double *cy, *cz, *yMy;
+  BAMG_TRY(arena_get(ctx, (size_t)n, &cy));
+  BAMG_TRY(arena_get(ctx, (size_t)n, &cz));
+  BAMG_TRY(arena_get(ctx, 4, &yMy));
+  BAMG_TRY(spmm_dev(ctx, M, y, cy, 1));
+  BAMG_TRY(spmm_dev(ctx, Nm, z, cz, 1));
+  BAMG_LAUNCH(ctx, bt_pairdot_kernel, 1, 256, 0, (const double*)y, (const double*)cy, n, n, yMy);
+  BAMG_LAUNCH(ctx, bt_pairdot_kernel, 1, 256, 0, (const double*)z, (const double*)cz, n, n, yMy + 1);
+  double hm[2];
+  BAMG_TRY(ctx_read_doubles(ctx, yMy, 2, hm));
+  BAMG_REQUIRE(ctx, hm[0] > 0.0 && hm[1] > 0.0, "mass matrix is not positive on the null vectors");
+  {
+    const double a = 1.0 / hm[0], b = 1.0 / hm[1];
+    double* ab;
+    BAMG_TRY(arena_get(ctx, 2, &ab));
+    const double hab[2] = {a, b};
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(ab, hab, sizeof(hab), cudaMemcpyHostToDevice, ctx->stream));
+    BAMG_LAUNCH(ctx, bt_scale_cols_kernel, grid_for(n, 256), 256, 0, cy, n, n, 1, (const double*)ab);
+    BAMG_LAUNCH(ctx, bt_scale_cols_kernel, grid_for(n, 256), 256, 0, cz, n, n, 1, (const double*)(ab + 1));
+    BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // hab lifetime
+  }
+  double *pd, *Yv, *Zu, *W, *MX, *Gs, *Ri, *Vs, *sv, *tmpn;
+  BAMG_TRY(arena_get(ctx, (size_t)p, &pd));
+  for (double** pp : {&Yv, &Zu, &W, &MX, &tmpn}) BAMG_TRY(arena_get(ctx, (size_t)n * p, pp));
+  for (double** pp : {&Gs, &Ri, &Vs}) BAMG_TRY(arena_get(ctx, (size_t)p * p, pp));
+  BAMG_TRY(arena_get(ctx, (size_t)p, &sv));
+  const int gnp = grid_for((int64_t)n * p, 256);
+  auto proj = [&](double* X, const double* c, const double* v) -> int {  // X -= v (c^T X)
+    BAMG_LAUNCH(ctx, bt_coldot_kernel, p, 256, 0, (const double*)X, n, n, c, pd);
+    BAMG_LAUNCH(ctx, bt_rank1_kernel, gnp, 256, 0, (const double*)X, n, n, p, v, (const double*)pd, X, n);
+    return 0;
+  };
+  auto csr_cm = [&](const bamg_csr* A, const double* X, double* Y) -> int {
+    BAMG_LAUNCH(ctx, bt_csr_cm_kernel, std::min(gnp, 16 * ctx->num_sms), 256, 0, A->rowptr, A->col, A->val, n, X, n,
+                Y, n, p);
+    return 0;
+  };
+  // G-type solve of the n x p block X (in place) through the padded layout
+  auto gsolve = [&](double* X, bool trans) -> int {
+    BAMG_LAUNCH(ctx, bt_embed_kernel, grid_for((int64_t)Np * p, 256), 256, 0, (const double*)X, n, n, off, Np, p, xa);
+    BAMG_TRY(cr_solve(ctx, F, xa, Np, p, trans, T));
+    BAMG_LAUNCH(ctx, bt_extract_kernel, gnp, 256, 0, (const double*)xa, Np, off, n, p, X, n);
+    return 0;
+  };
+  // u-block Zu = P_y G^T N P_z Yv ;  v-block Yv = P_z G M P_y Zu
+  auto kp_t = [&](const double* Yin, double* Zout) -> int {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(W, Yin, sizeof(double) * n * p, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_TRY(proj(W, cz, z));
+    BAMG_TRY(csr_cm(Nm, W, Zout));
+    BAMG_TRY(gsolve(Zout, true));
+    return proj(Zout, cy, y);
+  };
+  auto kp = [&](const double* Zin, double* Yout) -> int {
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(W, Zin, sizeof(double) * n * p, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_TRY(proj(W, cy, y));
+    BAMG_TRY(csr_cm(M, W, Yout));
+    BAMG_TRY(gsolve(Yout, false));
+    return proj(Yout, cz, z);
+  };
+  auto gram = [&](const bamg_csr* A, const double* X) -> int {  // Gs = X^T A X
+    BAMG_TRY(csr_cm(A, X, MX));
+    return dgemm_dev(ctx, true, false, p, p, n, 1.0, X, n, MX, n, 0.0, Gs, p);
+  };
+  auto ortho = [&](const bamg_csr* A, double* X) -> int {  // CholQR2 in the A inner product
+    for (int pass = 0; pass < 2; ++pass) {
+      BAMG_TRY(gram(A, X));
+      BAMG_TRY(dl_cholqr_apply(ctx, Gs, X, n, p, Ri, tmpn));
+    }
+    return 0;
+  };
+  // ---- start: random block, the first r columns warm-started from the level's incoming right vectors
+  BAMG_LAUNCH(ctx, bt_fill_random_kernel, gnp, 256, 0, Yv, n, 0, p, 12345u);
+  if (Vin) {
+    BAMG_LAUNCH(ctx, bt_embed_rows_kernel, grid_for((int64_t)n * r, 256), 256, 0, Vin, r, n, 0, n, Zu);
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Yv, Zu, sizeof(double) * (size_t)n * r, cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+  }
+  BAMG_TRY(proj(Yv, cz, z));
+  BAMG_TRY(ortho(Nm, Yv));
+  std::vector<double> prev(p, 0.0), cur(p, 0.0);
+  int iters = 0;
+  for (int blkit = 0; blkit < 100; ++blkit) {
+    for (int it = 0; it < 5; ++it) {
+      BAMG_TRY(kp_t(Yv, Zu));
+      BAMG_TRY(ortho(M, Zu));
+      BAMG_TRY(kp(Zu, Yv));
+      BAMG_TRY(ortho(Nm, Yv));
+    }
+    // Ritz values: singular values of K^+T on the block = sqrt of the M-Gram of Zu
+    BAMG_TRY(kp_t(Yv, Zu));
+    BAMG_TRY(gram(M, Zu));
+    BAMG_TRY(jacobi_svd_public(ctx, Gs, p, p, Vs, sv));
+    iters += 5;
+    BAMG_TRY(ctx_read_doubles(ctx, sv, p, cur.data()));
+    for (double& v : cur) v = std::sqrt(std::max(v, 0.0));
+    std::vector<double> c2 = cur;
+    std::sort(c2.begin(), c2.end(), [](double a, double b) { return a > b; });
+    double change = 0.0;
+    for (int q = 0; q < r; ++q) change = fmax(change, fabs(c2[q] - prev[q]) / fmax(c2[q], 1e-300));
+    prev = c2;
+    if (change < 1e-12) break;  // Ritz values settle into ~1e-15 rounding noise
+  }
+  // ---- Rayleigh-Ritz: Zu = K^+T Yv, M-Gram = W diag(s^2) W^T; u = Zu W / s, v = Yv W
+  BAMG_TRY(kp_t(Yv, Zu));
+  BAMG_TRY(gram(M, Zu));
+  BAMG_TRY(jacobi_svd_public(ctx, Gs, p, p, Vs, sv));
+  std::vector<double> lam(p);
+  BAMG_TRY(ctx_read_doubles(ctx, sv, p, lam.data()));
+  std::vector<int> order(p);
+  for (int q = 0; q < p; ++q) order[q] = q;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return lam[a] > lam[b] || (lam[a] == lam[b] && a < b); });
+  double *Ua, *Vb, *KB, *dots, *invs;
+  for (double** pp : {&Ua, &Vb, &KB}) BAMG_TRY(arena_get(ctx, (size_t)n * r, pp));
+  BAMG_TRY(arena_get(ctx, (size_t)r, &dots));
+  BAMG_TRY(arena_get(ctx, (size_t)p, &invs));
+  BAMG_TRY(dgemm_dev(ctx, false, false, n, p, p, 1.0, Zu, n, Vs, p, 0.0, W, n));   // Zu W
+  BAMG_TRY(dgemm_dev(ctx, false, false, n, p, p, 1.0, Yv, n, Vs, p, 0.0, MX, n));  // Yv W
+  std::vector<double> sig_host(r), hinv(p, 0.0);
+  for (int q = 0; q < p; ++q) hinv[q] = lam[q] > 0.0 ? 1.0 / std::sqrt(lam[q]) : 0.0;
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(invs, hinv.data(), sizeof(double) * p, cudaMemcpyHostToDevice, ctx->stream));
+  BAMG_LAUNCH(ctx, bt_scale_cols_kernel, gnp, 256, 0, W, n, n, p, (const double*)invs);
+  // slot 0: the null triplet (y, z) M- / N-normalised; slots 1.. the largest Ritz values of K^+
+  {
+    double hn[2] = {1.0 / std::sqrt(hm[0]), 1.0 / std::sqrt(hm[1])};
+    double* nn;
+    BAMG_TRY(arena_get(ctx, 2, &nn));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(nn, hn, sizeof(hn), cudaMemcpyHostToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Ua, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Vb, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    BAMG_LAUNCH(ctx, bt_scale_cols_kernel, grid_for(n, 256), 256, 0, Ua, n, n, 1, (const double*)nn);
+    BAMG_LAUNCH(ctx, bt_scale_cols_kernel, grid_for(n, 256), 256, 0, Vb, n, n, 1, (const double*)(nn + 1));
+    sig_host[0] = 0.0;
+    for (int j = 1; j < r; ++j) {
+      const int q = order[j - 1];
+      sig_host[j] = lam[q] > 0.0 ? 1.0 / std::sqrt(lam[q]) : INFINITY;
+      BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Ua + (size_t)j * n, W + (size_t)q * n, sizeof(double) * n,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+      BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Vb + (size_t)j * n, MX + (size_t)q * n, sizeof(double) * n,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // hn lifetime
+  }
+  double smax = 0.0;
+  int ntiny = 0;
+  for (int j = 0; j < r; ++j) smax = fmax(smax, sig_host[j]);
+  for (int j = 0; j < r; ++j) ntiny += sig_host[j] <= fmax(1e-10, 1e-8 * smax) ? 1 : 0;
+  BAMG_REQUIRE(ctx, ntiny <= 1, "coarsest operator has more than one numerically-null triplet");
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(sigma, sig_host.data(), sizeof(double) * r, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+  // sign rule u^T B v >= 0 (bootstrap.py:262-263)
+  for (int j = 0; j < r; ++j) BAMG_TRY(spmm_dev(ctx, B, Vb + (size_t)j * n, KB + (size_t)j * n, 1));
+  BAMG_LAUNCH(ctx, bt_pairdot_kernel, r, 256, 0, (const double*)Ua, (const double*)KB, n, n, dots);
+  BAMG_LAUNCH(ctx, bt_interleave_kernel, grid_for((int64_t)n * r, 256), 256, 0, (const double*)Ua,
+              (const double*)Vb, (const double*)dots, n, n, r, U, V);
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // sig_host lifetime
+  // ---- keep the CR factor + unit null vectors for the V-cycle's coarsest solve
+  BandPinv* h = new BandPinv();
+  h->n = n;
+  h->N = Np;
+  h->S = S;
+  h->nb = nb;
+  h->off = off;
+  const size_t fd = CRF::doubles(S, nb, L);
+  const size_t nbuf = fd + 5 * (size_t)Np + (size_t)(nb / 2 + 1) * S + 8;
+  h->slab_bytes = sizeof(double) * nbuf;
+  if (pool_take(ctx, h->slab_bytes, &h->slab) != 0) {
+    delete h;
+    return -1;
+  }
+  double* q = reinterpret_cast<double*>(h->slab);
+  h->cr = new CRF(F);
+  h->cr->base = q;
+  h->z = q + fd;
+  h->y = h->z + Np;
+  h->t1 = h->y + Np;
+  h->t2 = h->t1 + Np;
+  h->t3 = h->t2 + Np;
+  h->dots = h->t3 + (size_t)(nb / 2 + 1) * S;
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(q, F.base, sizeof(double) * fd, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(h->z, zN, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(h->y, yN, sizeof(double) * Np, cudaMemcpyDeviceToDevice, ctx->stream));
+  *keep = h;
+  if (getenv("BAMG_DEBUG"))
+    fprintf(stderr, "[bamg] band CR triplets n=%d S=%d nb=%d p=%d subspace iterations=%d sigma1=%.6e sigma_r=%.6e\n",
+            n, S, nb, p, iters, r > 1 ? sig_host[1] : 0.0, sig_host[r - 1]);
+  return 0;
 }
 
 // The band path.  Returns 0 (triplets in U, V, sigma; *keep = the V-cycle's
@@ -851,6 +1412,15 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
                            const bamg_csr* N_, int r, const double* Vin, double* U, double* V, double* sigma,
                            BandPinv** keep) {
   *keep = nullptr;
+  // Cyclic reduction first; it pivots only inside its S x S blocks, so a
+  // structurally singular diagonal block (seen on small BAMG^2 coarse
+  // operators) sends it here, to block Thomas, whose Schur complements
+  // carry the coupling, before the dense path.
+  if (!(getenv("BAMG_BAND_THOMAS") && getenv("BAMG_BAND_THOMAS")[0] == '1')) {
+    const int rc = band_cr_triplets(ctx, B, Bt, M, N_, r, Vin, U, V, sigma, keep);
+    if (rc != 1) return rc;
+    if (getenv("BAMG_DEBUG")) fprintf(stderr, "[bamg] band CR not applicable -> block Thomas\n");
+  }
   const int n = B->nrows;
   // half-bandwidths of the three operators -> block size
   int* bw;

@@ -1356,6 +1356,25 @@ int dl_orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double*
   return orthonormalize(ctx, Y, n, p, G, Rinv, tmp);
 }
 
+// Y <- Y R^-1 for a given SPD Gram matrix G = R^T R (p x p): one CholQR
+// application with a caller-computed Gram (e.g. Y^T M Y for M-orthonormal
+// columns).  Rinv, tmp: p x p and n x p scratch (the p not in {16..32} path).
+int dl_cholqr_apply(bamg_ctx* ctx, const double* G, double* Y, int n, int p, double* Rinv, double* tmp) {
+  BAMG_REQUIRE(ctx, p <= SMALLP, "subspace block wider than the small Cholesky kernel");
+  switch (p) {
+    case 16: BAMG_LAUNCH(ctx, cholqr_apply_kernel<16>, grid_for(n, 256), 256, 0, G, Y, n); return 0;
+    case 20: BAMG_LAUNCH(ctx, cholqr_apply_kernel<20>, grid_for(n, 256), 256, 0, G, Y, n); return 0;
+    case 24: BAMG_LAUNCH(ctx, cholqr_apply_kernel<24>, grid_for(n, 256), 256, 0, G, Y, n); return 0;
+    case 28: BAMG_LAUNCH(ctx, cholqr_apply_kernel<28>, grid_for(n, 256), 256, 0, G, Y, n); return 0;
+    case 32: BAMG_LAUNCH(ctx, cholqr_apply_kernel<32>, grid_for(n, 256), 256, 0, G, Y, n); return 0;
+    default: break;
+  }
+  BAMG_LAUNCH(ctx, small_chol_inv_kernel, 1, 256, 0, G, p, Rinv, (double*)nullptr);
+  BAMG_TRY(gemm(ctx, false, false, n, p, p, 1.0, Y, n, Rinv, p, 0.0, tmp, n));
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Y, tmp, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToDevice, ctx->stream));
+  return 0;
+}
+
 // ---------------------------------------------- fused subspace iteration
 // `iters` steps of the block subspace iteration  Z = orth(K^+T Y),
 // Y = orth(K^+ Z)  in ONE cooperative launch (n <= SUB_MAX_N, p <= 32):

@@ -39,6 +39,8 @@ int dgemm_batched_dev(bamg_ctx* ctx, bool ta, bool tb, int m, int n, int k, doub
 
 // CholQR2 orthonormalisation of an n x p column-major block (dense_large.cu)
 int dl_orthonormalize(bamg_ctx* ctx, double* Y, int n, int p, double* G, double* Rinv, double* tmp);
+// Y <- Y R^-1 for a caller-computed Gram G = R^T R (dense_large.cu)
+int dl_cholqr_apply(bamg_ctx* ctx, const double* G, double* Y, int n, int p, double* Rinv, double* tmp);
 // one-sided Jacobi SVD of an nrows x ncols block (dense.cu)
 int jacobi_svd_public(bamg_ctx* ctx, double* G, int nrows, int ncols, double* V, double* sig);
 
