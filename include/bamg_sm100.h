@@ -383,6 +383,28 @@ int bamg_combine(bamg_ctx* ctx, const double* const* Vp, int m, const double* y,
 int bamg_sign_fix_l1(bamg_ctx* ctx, const double* x, int64_t n, int stride, double* out,
                      int uniform_fallback);
 
+/* ---- field-of-values diagnostics (fov.cu; reference markovmg/fov.py) ----
+ * Dense column-major fp64 n x n on device, n <= 1200 in the Python mirror
+ * (fov.py:22 DENSE_CAP).
+ * bamg_fov_points replaces the angle sweep of fov_boundary (fov.py:85-115):
+ *   points[2t], points[2t+1] = re, im of the supporting point v^H A v of angle
+ *   theta_t = 2 pi t / n_angles (v the unit top eigenvector of the Hermitian
+ *   part of e^{i theta} A).  tol: Lanczos residual bound relative to |A|_F
+ *   (0 -> 1e-13).  *iterations: Lanczos steps taken (host, may be NULL).
+ * bamg_eigvals replaces eigenvalue_dots' np.linalg.eigvals (fov.py:60-67):
+ *   unsorted wr, wi (device, n each); returns 2 if the QR iteration stalls.
+ * bamg_range_basis replaces project_range / projected_preconditioned's
+ *   SVD range basis (fov.py:194-223): *rank (host) = #{sigma > rank_tol
+ *   sigma_max}; basis (n x rank, descending sigma, column-major) and
+ *   projected = basis^T A basis (rank x rank); basis == NULL queries the rank
+ *   only.  A zero matrix is an argument error (-2), like the reference's
+ *   ValueError. */
+int bamg_fov_points(bamg_ctx* ctx, const double* A, int n, int n_angles, double tol, double* points,
+                    int* iterations);
+int bamg_eigvals(bamg_ctx* ctx, const double* A, int n, double* wr, double* wi);
+int bamg_range_basis(bamg_ctx* ctx, const double* A, int n, double rank_tol, double* basis,
+                     double* projected, int* rank);
+
 #ifdef __cplusplus
 }
 #endif

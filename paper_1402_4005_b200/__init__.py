@@ -17,6 +17,8 @@ from .coarsen import (CfSplitting, CoarseningConfig, cr_coarsen, geometric_coars
                       splitting_from_mask)
 from .dense import PinvOperator
 from .device import DeviceCSR
+from .fov import (FovResult, ProjectedSystem, eigenvalue_dots, elman_bound, fov_boundary, project_range,
+                  projected_preconditioned, theorem2_bound)
 from .interp import (InterpConfig, WeightedTestSet, build_interpolation, build_restriction,
                      singular_test_weights)
 from .presets import PRESETS, build_problem, default_setup_config

@@ -102,6 +102,9 @@ _SIGS = {
     "bamg_permute_cols": [P, P, I64, C.c_int, C.POINTER(C.c_int32), P],
     "bamg_csr_to_dense": [P, PCSR, P, C.c_int, C.c_int],
     "bamg_dense_pinv": [P, P, C.c_int, F64, P],
+    "bamg_fov_points": [P, P, C.c_int, C.c_int, F64, P, C.POINTER(C.c_int)],
+    "bamg_eigvals": [P, P, C.c_int, P, P],
+    "bamg_range_basis": [P, P, C.c_int, F64, P, P, C.POINTER(C.c_int)],
     "bamg_coarsest_triplets": [P, P, P, P, C.c_int, C.c_int, P, P, P],
     "bamg_coarsest_triplets_pinv": [P, P, P, P, C.c_int, C.c_int, P, P, P, P, P],
     "bamg_hier_create": [P, C.c_int, C.POINTER(P)],

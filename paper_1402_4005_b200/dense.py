@@ -2,9 +2,10 @@
 
 `PinvOperator` builds the explicit pseudo-inverse of the (singular) coarsest
 operator on device by a one-sided Jacobi SVD with the reference's rank rule
-(dense.py:118-131) and applies it as one GEMV.  `gen_sym_eig` / `svd` /
-`sym_eig` / `herm_eig_max` of the reference serve the FOV analysis (out of
-scope) and are not mirrored.
+(dense.py:118-131) and applies it as one GEMV.  The reference's `gen_sym_eig`
+/ `svd` / `sym_eig` / `herm_eig_max` are LAPACK calls behind its coarsest level
+and FOV tooling; here the coarsest level has its own kernels (dense.cu,
+dense_large.cu, band.cu) and the FOV analysis its own (fov.py / fov.cu).
 """
 
 from __future__ import annotations

@@ -362,6 +362,34 @@ def dense_pinv(Dcm, n, rank_tol=1e-12):
     return Z  # row-major pseudo-inverse
 
 
+# ------------------------------------------------------ FOV diagnostics
+def fov_points(Dcm, n, n_angles, tol=0.0):
+    """Supporting points (re, im interleaved) of the angle sweep; Dcm column-major."""
+    pts = _empty(2 * n_angles)
+    it = C.c_int(0)
+    _lib.call("bamg_fov_points", _p(Dcm), int(n), int(n_angles), float(tol), _p(pts), C.byref(it))
+    return pts, it.value
+
+
+def eigvals(Dcm, n):
+    """(wr, wi) of a dense column-major matrix (unsorted)."""
+    wr, wi = _empty(n), _empty(n)
+    if _lib.call("bamg_eigvals", _p(Dcm), int(n), _p(wr), _p(wi)) == 2:
+        raise np.linalg.LinAlgError("Eigenvalues did not converge")
+    return wr, wi
+
+
+def range_basis(Dcm, n, rank_tol):
+    """(basis n x r, projected r x r) of a dense column-major matrix, as
+    row-major torch views of the column-major results."""
+    B = _empty(n * n)
+    P = _empty(n * n)
+    r = C.c_int(0)
+    _lib.call("bamg_range_basis", _p(Dcm), int(n), float(rank_tol), _p(B), _p(P), C.byref(r))
+    r = r.value
+    return B[: n * r].view(r, n).T, P[: r * r].view(r, r).T
+
+
 class CoarseLU:
     """The coarsest level's bordered LU kept on device by the implicit large
     path (bamg_coarse_lu): the V-cycle's coarsest solve goes through it."""
