@@ -28,7 +28,8 @@ class BamgError(RuntimeError):
 
 class CSR(C.Structure):
     _fields_ = [("nrows", C.c_int32), ("ncols", C.c_int32), ("nnz", C.c_int64),
-                ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+                ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
+                ("packed", C.c_void_p), ("dict", C.c_void_p)]
 
 
 P = C.c_void_p
@@ -57,6 +58,7 @@ _SIGS = {
     "bamg_trace_position": [P],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
+    "bamg_csr_pack": [P, PCSR, P, P, PINT],
     "bamg_csr_transpose": [P, PCSR, P, P, P],
     "bamg_sym_pattern_count": [P, PCSR, PCSR, P, PI64],
     "bamg_sym_pattern_fill": [P, PCSR, PCSR, P, P],
@@ -212,8 +214,30 @@ def check(rc: int, what: str, c=None):
 _SLOW_MS = float(_os.environ.get("BAMG_SLOWCALL_MS", "0") or 0)
 
 
+# BAMG_NVTX=1: one NVTX range per engine call (named after the C ABI entry),
+# nested inside the per-level phase ranges bootstrap.py / solver.py push
+# (tracing).  Off by default: the push/pop pair costs ~1 us per call.
+NVTX = bool(int(_os.environ.get("BAMG_NVTX", "0") or 0))
+
+
+def nvtx_push(name: str) -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_push(name)
+
+
+def nvtx_pop() -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_pop()
+
+
 def call(name: str, *args):
     c = ctx()
+    if NVTX:
+        torch.cuda.nvtx.range_push(name)
+        try:
+            return check(getattr(lib(), name)(c, *args), name, c)
+        finally:
+            torch.cuda.nvtx.range_pop()
     if _SLOW_MS > 0:
         import time
         t0 = time.perf_counter()

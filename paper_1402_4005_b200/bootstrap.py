@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import engine
+from . import _lib, engine
 from .coarsen import AxisRanks, CfSplitting, CoarseningConfig, make_splitting
 from .device import DeviceCSR, device
 from .interp import InterpConfig, build_transfer_pair, singular_test_weights
@@ -43,10 +43,12 @@ RECORDER = None
 
 
 class _phase:
-    def __init__(self, name):
+    def __init__(self, name, level=None):
         self.name = name
+        self.level = level
 
     def __enter__(self):
+        _lib.nvtx_push(f"bamg.setup.{self.name}" if self.level is None else f"bamg.setup.L{self.level}.{self.name}")
         if RECORDER is not None:
             RECORDER(self.name, True)
         if PHASES is not None:
@@ -59,6 +61,7 @@ class _phase:
         if PHASES is not None:
             torch.cuda.synchronize()
             PHASES[self.name] = PHASES.get(self.name, 0.0) + time.perf_counter() - self.t
+        _lib.nvtx_pop()
 
 
 class TripletSet:
@@ -366,7 +369,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
     """One recursive setup pass (bootstrap.py:337-392); returns (levels, triplets)."""
     A = as_device(B)
     if ops is None:
-        with _phase("level_ops"):
+        with _phase("level_ops", depth):
             ops = _LevelOps(A)
     Md, Nd = as_device(M), as_device(N)
     n = A.shape[0]
@@ -379,7 +382,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
     split = None
     if n >= cfg.coarsening.stop_size and depth + 1 < cfg.coarsening.max_levels:
         seed = seed_stream.next()
-        with _phase("split"):
+        with _phase("split", depth):
             if cfg.coarsening.mode == "cr":
                 split = make_splitting(A, ranks, cfg.coarsening, seed, adj=ops.adj, diag=ops.d)
             else:
@@ -391,25 +394,25 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
     if split is None:
         if _DEBUG:
             print(f"[bamg] coarsest level {depth} n={n}", file=sys.stderr, flush=True)
-        with _phase("coarsest"):
+        with _phase("coarsest", depth):
             trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt, warm=trips)
         return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
 
-    with _phase("smooth"):
+    with _phase("smooth", depth):
         _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
 
     levels = None
     for _ in range(cfg.inner_passes):
-        with _phase("weights"):
+        with _phase("weights", depth):
             v_tests = singular_test_weights(A, trips.dright)
             u_tests = singular_test_weights(A, trips.dleft, transpose_side=True,
                                             infinite_slot=0 if cfg.interp.constrain_constant_in_q else None,
                                             Bt=ops.Bt)
-        with _phase("adjacency"):
+        with _phase("adjacency", depth):
             adj = ops.adj
-        with _phase("ls_fit"):
+        with _phase("ls_fit", depth):
             P, W = build_transfer_pair(A, split, v_tests, u_tests, cfg.interp, adj=adj)
-        with _phase("galerkin"):
+        with _phase("galerkin", depth):
             # B_c = (Q B) P (sparse.py:102-117), M_c = Q M Q^T, N_c = P^T N P
             # (bootstrap.py:372-373): the independent products of each stage
             # are counted together (one host read per stage).  Identity masses
@@ -435,10 +438,10 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         if sick:
             if _DEBUG:
                 print(f"[bamg] truncated at level {depth} n={n} (sick Galerkin product)", file=sys.stderr, flush=True)
-            with _phase("coarsest"):
+            with _phase("coarsest", depth):
                 trips = coarsest_triplets(A, Md, Nd, trips.r, Bt=ops.Bt, warm=trips)
             return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
-        with _phase("inject"):
+        with _phase("inject", depth):
             cranks = ranks.restrict(split) if ranks is not None else None
             cl = engine.gather_rows(trips.dleft, split.dcoarse)
             cr = engine.gather_rows(trips.dright, split.dcoarse)
@@ -448,13 +451,13 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         sub_levels, coarse = bootstrap_cycle(Bc, Mc, Nc, coarse, cfg, cranks, depth + 1,
                                              first_cycle, seed_stream)
         # prolong: u <- Q^T u_c (= W u_c), v <- P v_c; normalise; pin; refresh; smooth
-        with _phase("prolong"):
+        with _phase("prolong", depth):
             U = engine.spmm(W, coarse.dleft)
             V = engine.spmm(P, coarse.dright)
             trips = TripletSet(coarse.dsigmas.clone(), U, V)
             engine.smooth_block(ops.B, ops.Bt, _mass(Md), _mass(Nd), ops.d, ops.skip, ops.skip_t,
                                 U, V, trips.dsigmas, 0, cfg.smoother.omega, 0, smooth=0, refresh=1)
-        with _phase("smooth"):
+        with _phase("smooth", depth):
             _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True)
         levels = [Level(depth, A, ops.d, Md, Nd, split, P, Q, ranks, Bt=ops.Bt, W=W)] + sub_levels
     return levels, trips
@@ -475,6 +478,10 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     root = np.random.SeedSequence(cfg.seed)
     ss_init, ss_levels = root.spawn(2)
     with _phase("level_ops"):
+        # the generators' B = I - A has a handful of distinct values: the k = 1
+        # sweeps / residuals / SpMVs of the solve stream its packed copy
+        # (4 instead of 12 bytes per entry, same bits); redone every setup
+        engine.pack_operator(A)
         ops = _LevelOps(A)
     rng = np.random.default_rng(ss_init) if draws is None else None
     with _phase("init"):

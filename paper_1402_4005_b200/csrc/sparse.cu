@@ -10,7 +10,9 @@
 // (sparse.py:81-86 -> scipy _sparsetools csr_matvec: sum = 0; sum += a*x).
 // The Jacobi epilogue reproduces relax.py:78-83 bit for bit:
 //   r = b - Ax;  upd = (omega * r) / d;  upd = 0 on skipped rows;  x + upd.
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -317,6 +319,227 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
   }
 }
 
+// Software-pipelined row kernel (persistent CTAs, same arithmetic).
+// csr_rows_kernel's per-thread chain is rowptr -> col/val -> X gathers (one
+// round per U entries) -> epilogue operands: four to five dependent memory
+// latencies per row, with the wide gathers in flight only a fraction of the
+// time (ncu at cfg4 level 0, k = 16: long-scoreboard bound, 40 % of HBM).
+// Here every G-thread group walks its rows (tile blockIdx.x + i * gridDim.x)
+// as a stream of chunks of <= U entries, and one step issues, before it
+// consumes anything: the gathers and values of the current chunk, the column
+// indices of the NEXT chunk (of this row or of the group's next row), the
+// extents of the row after next, and the epilogue operands of a row that
+// finishes.  A step therefore costs one memory latency and keeps
+// U * 8V + 12U bytes per thread in flight.  Sums stay sequential in ascending
+// column order per (row, vector): bit-identical to csr_rows_kernel.
+template <int EPI, int K, int G, int U, int MINB>
+__global__ void __launch_bounds__(TILE_THREADS, MINB)
+csr_rows_pipe_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                     const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y,
+                     EpiArgs ea) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(EPI != EPI_JACOBI_M, "the mass-fused sweep stays on csr_rows_kernel");
+  constexpr int V = K / G;
+  constexpr int RB = TILE_THREADS / G;
+  __shared__ unsigned long long s_peak[K];
+  const bool want_peak = EPI == EPI_JACOBI && ea.peak != nullptr;
+  if (want_peak) {
+    if (threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
+    __syncthreads();
+  }
+  const int lr = threadIdx.x / G;
+  const int sub = threadIdx.x - lr * G;
+  const int voff = sub * V;
+  const int stride = gridDim.x * RB;
+  const int limit = lr < RB ? ntiles * RB : 0;  // threads past the last whole group idle (K = 12: 252 of 256)
+  double pk[V], acc[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) pk[q] = 0.0, acc[q] = 0.0;
+
+  int row = blockIdx.x * RB + lr;
+  int j = 0, je = 0;
+  if (row < limit && row < nrows) j = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  int row_n = row + stride, jb_n = 0, je_n = 0;
+  if (row_n < limit && row_n < nrows) jb_n = __ldg(rowptr + row_n), je_n = __ldg(rowptr + row_n + 1);
+  int cc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cc[u] = j + u < je ? __ldg(col + j + u) : 0;
+
+  while (row < limit) {
+    const bool fin = j + U >= je;  // this chunk completes the row
+    // (1) gathers and (2) values of the current chunk
+    double xv[U][V], aa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < je) {
+        VecIO<V>::load(X + (int64_t)cc[u] * K + voff, xv[u]);
+        aa[u] = __ldg(val + j + u);
+      } else {
+        aa[u] = 0.0;
+#pragma unroll
+        for (int q = 0; q < V; ++q) xv[u][q] = 0.0;
+      }
+    }
+    // (3) the next chunk's columns: the rest of this row, or the head of the group's next row
+    const int rown = fin ? row_n : row;
+    const int jn = fin ? jb_n : j + U;
+    const int jen = fin ? je_n : je;
+    int ccn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ccn[u] = jn + u < jen ? __ldg(col + jn + u) : 0;
+    // (4) on a row change, the extents of the row after next
+    int row_nn = row_n, jb_nn = jb_n, je_nn = je_n;
+    if (fin) {
+      row_nn = row_n + stride;
+      jb_nn = je_nn = 0;
+      if (row_nn < limit && row_nn < nrows) jb_nn = __ldg(rowptr + row_nn), je_nn = __ldg(rowptr + row_nn + 1);
+    }
+    // (5) epilogue operands of a finishing row
+    const bool emit = fin && row < nrows;
+    const int64_t base = (int64_t)row * K + voff;
+    double e0[V], e1[V], dd = 1.0, rdd = 0.0;
+    bool sk = false;
+    if (emit) {
+      if (EPI == EPI_RESID) VecIO<V>::load(ea.b + base, e0);
+      if (EPI == EPI_ADD) VecIO<V>::load(ea.xold + base, e0);
+      if (EPI == EPI_JACOBI) {
+        VecIO<V>::load(ea.xold + base, e0);
+        if (ea.b) VecIO<V>::load(ea.b + base, e1);
+        sk = ea.skip[row] != 0;
+        dd = ea.d[row];
+        if (ea.rd) rdd = ea.rd[row];
+      }
+    }
+    // (6) accumulate in column order
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < je) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+      }
+    }
+    // (7) finish the row
+    if (emit) {
+      double out[V];
+      if (EPI == EPI_PLAIN) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) out[q] = acc[q];
+      } else if (EPI == EPI_RESID) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) out[q] = __dsub_rn(e0[q], acc[q]);
+      } else if (EPI == EPI_ADD) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) out[q] = __dadd_rn(e0[q], acc[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          double bv = 0.0;
+          if (ea.b) bv = ea.b_scale ? __dmul_rn(ea.b_scale[voff + q], e1[q]) : e1[q];
+          const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc[q]));
+          const double upd = sk ? 0.0 : (ea.rd ? div_rn_recip(num, dd, rdd) : __ddiv_rn(num, dd));
+          out[q] = __dadd_rn(e0[q], upd);
+          pk[q] = fmax(pk[q], fabs(out[q]));
+        }
+      }
+      VecIO<V>::store(Y + base, out);
+    }
+    if (fin) {
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = 0.0;
+      row_n = row_nn, jb_n = jb_nn, je_n = je_nn;
+    }
+    row = rown, j = jn, je = jen;
+#pragma unroll
+    for (int u = 0; u < U; ++u) cc[u] = ccn[u];
+  }
+  if (want_peak) {
+    constexpr bool POW2 = (G & (G - 1)) == 0;
+    if constexpr (POW2) {
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        double m = pk[q];
+        for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        pk[q] = m;
+      }
+    }
+    if (lr < RB && (!POW2 || (threadIdx.x & 31) < G)) {
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        atomicMax(&s_peak[sub * V + q], (unsigned long long)__double_as_longlong(pk[q]));
+    }
+    __syncthreads();
+    if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
+  }
+}
+
+// BAMG_ROWS_PIPE: "0" disables the pipelined kernel; "K:U:MINB[,K:U:MINB...]"
+// overrides the per-K tuning (development: tools/csr_bench.py sweeps)
+struct PipeCfg {
+  int u, minb;
+};
+static PipeCfg pipe_cfg(int k) {
+  static int init = 0;
+  static PipeCfg tab[33];
+  if (!init) {
+    for (int i = 0; i <= 32; ++i) tab[i] = PipeCfg{0, 0};
+    // measured at cfg4's level 0 (tools/pipe_sweep.sh): k = 16 sweeps with a right-hand side or the
+    // per-column peak gain 7-13 % (one atomic per CTA and column instead of one per 32 rows)
+    tab[16] = PipeCfg{4, 4};
+    const char* e = getenv("BAMG_ROWS_PIPE");
+    if (e && e[0] == '0' && e[1] == 0) {
+      for (int i = 0; i <= 32; ++i) tab[i] = PipeCfg{0, 0};
+    } else if (e) {
+      int kk, uu, mm;
+      const char* p = e;
+      while (sscanf(p, "%d:%d:%d", &kk, &uu, &mm) == 3) {
+        if (kk >= 1 && kk <= 32) tab[kk] = PipeCfg{uu, mm};
+        p = strchr(p, ',');
+        if (!p) break;
+        ++p;
+      }
+    }
+    init = 1;
+  }
+  return tab[k];
+}
+
+// returns 1 when (k, the configured U / MINB) has no pipelined instance
+template <int EPI>
+static int launch_rows_pipe(bamg_ctx* ctx, int k, double bytes, const bamg_csr* A, const double* X, double* Y,
+                            const EpiArgs& ea) {
+  const PipeCfg pc = pipe_cfg(k);
+  if (pc.u == 0) return 1;
+#define BAMG_PIPE_CASE(KK, GG, UU, MB)                                                                      \
+  if (k == KK && pc.u == UU && pc.minb == MB) {                                                             \
+    const int rb = TILE_THREADS / GG;                                                                       \
+    const int ntiles = (A->nrows + rb - 1) / rb;                                                            \
+    const int g = ntiles < ctx->num_sms * MB ? ntiles : ctx->num_sms * MB;                                \
+    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                            \
+                    (csr_rows_pipe_kernel<EPI, KK, GG, UU, MB>), g, TILE_THREADS, 0, A->nrows, ntiles,      \
+                    A->rowptr, A->col, A->val, X, Y, ea);                                                   \
+    return 0;                                                                                               \
+  }
+  BAMG_PIPE_CASE(16, 8, 4, 5)
+  BAMG_PIPE_CASE(16, 8, 4, 4)
+  BAMG_PIPE_CASE(16, 8, 5, 4)
+  BAMG_PIPE_CASE(16, 8, 6, 4)
+  BAMG_PIPE_CASE(16, 8, 6, 3)
+  BAMG_PIPE_CASE(16, 8, 8, 3)
+  BAMG_PIPE_CASE(12, 6, 6, 4)
+  BAMG_PIPE_CASE(12, 6, 6, 3)
+  BAMG_PIPE_CASE(8, 4, 6, 4)
+  BAMG_PIPE_CASE(8, 4, 6, 3)
+  BAMG_PIPE_CASE(8, 4, 8, 3)
+  BAMG_PIPE_CASE(1, 1, 4, 8)
+  BAMG_PIPE_CASE(1, 1, 4, 6)
+  BAMG_PIPE_CASE(1, 1, 6, 5)
+  BAMG_PIPE_CASE(1, 1, 6, 6)
+  BAMG_PIPE_CASE(1, 1, 8, 6)
+  BAMG_PIPE_CASE(1, 1, 8, 4)
+#undef BAMG_PIPE_CASE
+  return 1;
+}
+
 #ifndef BAMG_U1
 #define BAMG_U1 4
 #endif
@@ -570,6 +793,8 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
   return 0;
 }
 
+static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea);
+
 static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, int k,
                        double* Y, const EpiArgs& ea) {
   BAMG_TRY(check_csr(ctx, A));
@@ -586,6 +811,22 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   // 16-byte vector loads need aligned blocks when K is even (K = 1 has none)
   bool aligned = (k & 1) || ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
                               reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold)) & 15) == 0;
+  if (k == 1 && A->packed) {
+    const int rc = launch_packed(ctx, epi, A, X, Y, ea);
+    if (rc <= 0) return rc;
+  }
+  static const bool pipe_forced = getenv("BAMG_ROWS_PIPE") != nullptr;
+  if (rows_kernel_enabled() && aligned && epi != EPI_JACOBI_M &&
+      (pipe_forced || (epi == EPI_JACOBI && (ea.peak || ea.b)))) {
+    int rc = 1;
+    switch (epi) {
+      case EPI_PLAIN: rc = launch_rows_pipe<EPI_PLAIN>(ctx, k, bytes, A, X, Y, ea); break;
+      case EPI_RESID: rc = launch_rows_pipe<EPI_RESID>(ctx, k, bytes, A, X, Y, ea); break;
+      case EPI_ADD: rc = launch_rows_pipe<EPI_ADD>(ctx, k, bytes, A, X, Y, ea); break;
+      default: rc = launch_rows_pipe<EPI_JACOBI>(ctx, k, bytes, A, X, Y, ea);
+    }
+    if (rc <= 0) return rc;
+  }
   if (rows_kernel_enabled() && aligned) {
     int rc = 1;
     switch (epi) {
@@ -614,6 +855,253 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
     default:
       BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, csr_tile_kernel<EPI_JACOBI>, grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->col, A->val, X, k, Y, ea);
+  }
+  return 0;
+}
+
+// ------------------------------------------------ packed operator (CSR-VI)
+// The chain generators' B = I - A carries a handful of distinct values (the
+// transition rates / 1/deg), and the lattice and mesh orderings keep
+// |col - row| < 2^23.  Such an operator is stored a second time as one 32-bit
+// word per entry -- (col - row) << 8 | value code -- plus a 256-entry value
+// dictionary (with the correctly rounded reciprocals beside it): 4 instead of
+// 12 bytes per entry on the k = 1 V-cycle sweeps, residuals and the GMRES
+// SpMV, which are HBM-bound.  Decoding returns the original fp64 value, the
+// sums keep the CSR order: bit-identical to csr_rows_kernel.  The Jacobi
+// diagonal and its reciprocal come from the row's own delta = 0 entry (no d /
+// rd streams).  Operators with more than 256 distinct values (every Galerkin
+// level) or wider rows are simply not packed.
+constexpr int PACK_DICT = 256;
+constexpr int PACK_HASH = 1024;  // open addressing, power of two
+constexpr unsigned long long PACK_EMPTY = 0xFFFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ unsigned int pack_hash(unsigned long long b) {
+  b ^= b >> 33;
+  b *= 0xff51afd7ed558ccdull;
+  b ^= b >> 33;
+  return (unsigned int)b & (PACK_HASH - 1);
+}
+
+// distinct value bit patterns -> global table (count[0] = distinct values, count[1] = failures)
+__global__ void __launch_bounds__(256)
+pack_collect_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                    const double* __restrict__ val, unsigned long long* __restrict__ table,
+                    unsigned int* __restrict__ count) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ unsigned long long s_tab[PACK_HASH];
+  __shared__ unsigned int s_n, s_bad;
+  for (int i = threadIdx.x; i < PACK_HASH; i += blockDim.x) s_tab[i] = PACK_EMPTY;
+  if (threadIdx.x == 0) s_n = 0u, s_bad = 0u;
+  __syncthreads();
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows; row += gridDim.x * blockDim.x) {
+    const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+    for (int j = jb; j < je; ++j) {
+      const int delta = __ldg(col + j) - row;
+      if (delta >= (1 << 23) || delta < -(1 << 23)) s_bad = 1u;
+      const unsigned long long b = (unsigned long long)__double_as_longlong(__ldg(val + j));
+      if (b == PACK_EMPTY) {
+        s_bad = 1u;
+        continue;
+      }
+      unsigned int h = pack_hash(b);
+      for (int probe = 0; probe < PACK_HASH; ++probe) {
+        const unsigned long long cur = s_tab[h];
+        if (cur == b) break;
+        if (cur == PACK_EMPTY) {
+          if (s_n > 2 * PACK_DICT) {  // hopeless: stop filling the table
+            s_bad = 1u;
+            break;
+          }
+          const unsigned long long old = atomicCAS(&s_tab[h], PACK_EMPTY, b);
+          if (old == PACK_EMPTY) {
+            atomicAdd(&s_n, 1u);
+            break;
+          }
+          if (old == b) break;
+        }
+        h = (h + 1) & (PACK_HASH - 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) atomicAdd(count + 1, 1u);
+    return;
+  }
+  for (int i = threadIdx.x; i < PACK_HASH; i += blockDim.x) {
+    const unsigned long long b = s_tab[i];
+    if (b == PACK_EMPTY) continue;
+    unsigned int h = pack_hash(b);
+    for (int probe = 0; probe < PACK_HASH; ++probe) {
+      const unsigned long long old = atomicCAS(table + h, PACK_EMPTY, b);
+      if (old == PACK_EMPTY) {
+        atomicAdd(count, 1u);
+        break;
+      }
+      if (old == b) break;
+      h = (h + 1) & (PACK_HASH - 1);
+      if (probe == PACK_HASH - 1) atomicAdd(count + 1, 1u);
+    }
+  }
+}
+
+// one CTA: the table's values sorted by bit pattern (a fixed order whatever
+// the insertion races were) -> dict[0..255], RN(1 / v) -> dict[256..511]
+__global__ void __launch_bounds__(PACK_HASH)
+pack_dict_kernel(const unsigned long long* __restrict__ table, unsigned int* __restrict__ count,
+                 double* __restrict__ dict) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ unsigned long long s[PACK_HASH];
+  const int t = threadIdx.x;
+  s[t] = table[t];
+  if (t < 2 * PACK_DICT) dict[t] = 0.0;
+  __syncthreads();
+  if (count[1] != 0u || count[0] > PACK_DICT) {
+    if (t == 0) count[1] = 1u;
+    return;
+  }
+  const unsigned long long mine = s[t];
+  if (mine == PACK_EMPTY) return;
+  int rank = 0;
+  for (int i = 0; i < PACK_HASH; ++i) rank += (s[i] != PACK_EMPTY && s[i] < mine) ? 1 : 0;
+  const double v = __longlong_as_double((long long)mine);
+  dict[rank] = v;
+  dict[PACK_DICT + rank] = __drcp_rn(v);
+}
+
+__global__ void __launch_bounds__(256)
+pack_encode_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                   const double* __restrict__ val, const double* __restrict__ dict,
+                   const unsigned int* __restrict__ count, uint32_t* __restrict__ packed) {
+  BAMG_PDL_PROLOGUE();
+  if (count[1] != 0u) return;
+  __shared__ unsigned long long s_key[PACK_DICT];
+  const int nd = (int)count[0];
+  for (int i = threadIdx.x; i < PACK_DICT; i += blockDim.x)
+    s_key[i] = i < nd ? (unsigned long long)__double_as_longlong(dict[i]) : PACK_EMPTY;
+  __syncthreads();
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows; row += gridDim.x * blockDim.x) {
+    const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+    for (int j = jb; j < je; ++j) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(__ldg(val + j));
+      int lo = 0, hi = nd - 1;  // the value is in the dictionary by construction
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_key[mid] < b) lo = mid + 1;
+        else hi = mid;
+      }
+      const int delta = __ldg(col + j) - row;
+      packed[j] = ((uint32_t)delta << 8) | (uint32_t)lo;
+    }
+  }
+}
+
+extern "C" int bamg_csr_pack(bamg_ctx* ctx, const bamg_csr* A, uint32_t* packed, double* dict, int* ok_host) {
+  ctx->arena.reset();
+  BAMG_TRY(check_csr(ctx, A));
+  BAMG_REQUIRE(ctx, packed && dict && ok_host, "null output");
+  *ok_host = 0;
+  if (A->nrows != A->ncols || A->nnz == 0) return 0;
+  unsigned long long* table;
+  BAMG_TRY(arena_get(ctx, (size_t)PACK_HASH + 1, &table));
+  unsigned int* count = reinterpret_cast<unsigned int*>(table + PACK_HASH);
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(table, 0xFF, sizeof(unsigned long long) * PACK_HASH, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(count, 0, sizeof(unsigned long long), ctx->stream));
+  const int g = grid_for(A->nrows, 256);
+  const int grid = g < ctx->num_sms * 8 ? g : ctx->num_sms * 8;
+  BAMG_LAUNCH(ctx, pack_collect_kernel, grid, 256, 0, A->nrows, A->rowptr, A->col, A->val, table, count);
+  BAMG_LAUNCH(ctx, pack_dict_kernel, 1, PACK_HASH, 0, table, count, dict);
+  BAMG_LAUNCH(ctx, pack_encode_kernel, grid, 256, 0, A->nrows, A->rowptr, A->col, A->val, dict, count, packed);
+  int64_t res = 0;
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(count), 1, &res));
+  *ok_host = ((uint64_t)res >> 32) == 0 ? 1 : 0;  // count[1] == 0
+  return 0;
+}
+
+// thread per row, k = 1; same sums as csr_rows_kernel<EPI, 1, 1, U>
+template <int EPI, int U>
+__global__ void __launch_bounds__(TILE_THREADS, 8)
+csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint32_t* __restrict__ pk,
+                       const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
+                       EpiArgs ea) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double s_dict[2 * PACK_DICT];
+  for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
+  __syncthreads();
+  const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
+  if (row >= nrows) return;
+  const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  double acc = 0.0, dd = 0.0, rdd = __longlong_as_double(0x7FF0000000000000ll);  // no diagonal entry: d = 0, 1/d = inf
+  const double* xr = X + row;
+  for (int j = jb; j < je; j += U) {
+    uint32_t w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = __ldg(pk + (j + u < je ? j + u : je - 1));
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(xr + ((int32_t)w[u] >> 8));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < je) {
+        const double a = s_dict[w[u] & 255u];
+        acc = __dadd_rn(acc, __dmul_rn(a, xv[u]));
+        if (EPI == EPI_JACOBI && (w[u] >> 8) == 0u) dd = a, rdd = s_dict[PACK_DICT + (w[u] & 255u)];
+      }
+    }
+  }
+  double out;
+  if (EPI == EPI_PLAIN) {
+    out = acc;
+  } else if (EPI == EPI_RESID) {
+    out = __dsub_rn(ea.b[row], acc);
+  } else {
+    const double bv = ea.b ? ea.b[row] : 0.0;
+    const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc));
+    const double upd = ea.skip[row] != 0 ? 0.0 : div_rn_recip(num, dd, rdd);
+    out = __dadd_rn(ea.xold[row], upd);
+  }
+  Y[row] = out;
+}
+
+// the bytes the packed kernels move (what the profiler's family figures use)
+static double packed_bytes(int epi, const bamg_csr* A, const EpiArgs& ea) {
+  const double n = A->nrows;
+  double bytes = 4.0 * (n + 1) + 4.0 * (double)A->nnz + 8.0 * A->ncols + 8.0 * n;
+  if (epi == EPI_RESID) bytes += 8.0 * n;
+  if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * n : 0.0) + n;  // b, skip (d and 1/d come from the dictionary)
+  return bytes;
+}
+
+static bool packed_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BAMG_NO_PACKED");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// returns 1 when the call is not covered (caller takes the CSR kernels)
+static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea) {
+  if (!A->packed || !A->dict || !packed_enabled()) return 1;
+  if (epi == EPI_JACOBI && (ea.peak || ea.b_scale || ea.xold != X)) return 1;
+  if (epi != EPI_PLAIN && epi != EPI_RESID && epi != EPI_JACOBI) return 1;
+  const int grid = (A->nrows + TILE_THREADS - 1) / TILE_THREADS;
+  if (grid == 0) return 0;
+  const double bytes = packed_bytes(epi, A, ea);
+  const int fam = A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE;
+  switch (epi) {
+    case EPI_PLAIN:
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, 4>), grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->packed, A->dict, X, Y, ea);
+      break;
+    case EPI_RESID:
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, 4>), grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->packed, A->dict, X, Y, ea);
+      break;
+    default:
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, 4>), grid, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->packed, A->dict, X, Y, ea);
   }
   return 0;
 }

@@ -24,7 +24,7 @@ def device():
 
 
 class DeviceCSR:
-    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity")
+    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity", "packed", "dict")
 
     def __init__(self, rowptr, col, val, shape, is_identity=False):
         self.rowptr = rowptr
@@ -33,6 +33,9 @@ class DeviceCSR:
         self.shape = (int(shape[0]), int(shape[1]))
         self.is_identity = is_identity
         self._desc = None
+        # packed copy for the k = 1 kernels (engine.pack_operator), else None
+        self.packed = None
+        self.dict = None
 
     @property
     def nnz(self) -> int:
@@ -47,7 +50,9 @@ class DeviceCSR:
             self._desc = _lib.CSR(self.shape[0], self.shape[1], self.nnz,
                                   self.rowptr.data_ptr(),
                                   self.col.data_ptr() if self.nnz else None,
-                                  self.val.data_ptr() if self.nnz else None)
+                                  self.val.data_ptr() if self.nnz else None,
+                                  self.packed.data_ptr() if self.packed is not None else None,
+                                  self.dict.data_ptr() if self.dict is not None else None)
         return self._desc
 
     def ref(self):

@@ -56,6 +56,24 @@ def spmm(A: DeviceCSR, X):
     return Y
 
 
+def pack_operator(A: DeviceCSR) -> bool:
+    """Attach the packed (value-indexed, 32-bit) copy the k = 1 kernels stream
+    instead of col / val (bamg_csr_pack).  True when A qualifies (<= 256
+    distinct values, |col - row| < 2^23); otherwise A is left as it is."""
+    A.packed = A.dict = None
+    A._desc = None
+    if A.shape[0] != A.shape[1] or A.nnz == 0:
+        return False
+    packed = _empty(A.nnz, I32)
+    dic = _empty(512, F64)
+    ok = C.c_int(0)
+    _lib.call("bamg_csr_pack", A.ref(), _p(packed), _p(dic), C.byref(ok))
+    if ok.value:
+        A.packed, A.dict = packed, dic
+        A._desc = None
+    return bool(ok.value)
+
+
 def transpose(A: DeviceCSR) -> DeviceCSR:
     rp = _empty(A.shape[1] + 1, I32)
     ci = _empty(A.nnz, I32)

@@ -372,3 +372,59 @@ def test_block_kernels_match_numpy(eng, k):
     perm = rng.permutation(k).astype(np.int32)
     Pm = engine.permute_cols(torch.from_numpy(X).cuda(), perm).cpu().numpy()
     assert np.array_equal(Pm, X[:, perm])
+
+
+@pytest.mark.parametrize("family,side", [("tandem", 63), ("uniform2d", 40), ("planar", 1500)])
+def test_packed_operator_kernels_bitexact(eng, family, side):
+    """bamg_csr_pack: the k = 1 SpMV / residual / Jacobi kernels on the packed
+    (value-indexed, 32-bit) copy of a generator chain's B reproduce the CSR
+    kernels -- and scipy's csr_matvec -- bit for bit (sparse.py:81-86, relax.py:66-83)."""
+    from paper_1402_4005_b200 import chains, engine
+    if family == "planar":
+        prob = chains.random_planar(side, seed=1)
+    elif family == "tandem":
+        prob = chains.tandem_queue(side)
+    else:
+        prob = chains.uniform_2d(side)
+    B = orc.canon(prob.B)
+    n = B.shape[0]
+    dB = up(eng, B)
+    plain = up(eng, B)
+    assert engine.pack_operator(dB)
+    assert dB.packed is not None and dB.desc().packed
+    rng = np.random.default_rng(7)
+    x, b = rng.standard_normal(n), rng.standard_normal(n)
+    dx, db = dvec(x), dvec(b)
+    # SpMV
+    y = engine.spmm(dB, dx)
+    assert np.array_equal(y.cpu().numpy(), B @ x)
+    assert torch.equal(y, engine.spmm(plain, dx))
+    # residual
+    r = torch.empty_like(dx)
+    r0 = torch.empty_like(dx)
+    eng[0].call("bamg_residual", dB.ref(), eng[0].ptr(db), eng[0].ptr(dx), eng[0].ptr(r))
+    eng[0].call("bamg_residual", plain.ref(), eng[0].ptr(db), eng[0].ptr(dx), eng[0].ptr(r0))
+    assert torch.equal(r, r0)
+    assert np.array_equal(r.cpu().numpy(), b - B @ x)
+    # Jacobi (homogeneous and with a right-hand side), against the CSR kernel and the oracle
+    d = engine.diag(plain)
+    skip = engine.degenerate_rows(plain, d)
+    for rhs in (None, db):
+        got = engine.jacobi(dB, d, skip, dx, b=rhs)
+        assert torch.equal(got, engine.jacobi(plain, d, skip, dx, b=rhs))
+        dg = B.diagonal()
+        want = orc.sweep(B, x, np.zeros(n) if rhs is None else b, 0.7, dg, orc.skip_rows(B, dg))
+        assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_pack_operator_declines_general_values(eng):
+    """More than 256 distinct values (any Galerkin operator): not packed, CSR kernels run."""
+    from scipy import sparse as sp
+    from paper_1402_4005_b200 import engine
+    rng = np.random.default_rng(3)
+    A = orc.canon(sp.random_array((2000, 2000), density=0.004, random_state=rng) + sp.eye_array(2000))
+    dA = up(eng, A)
+    assert not engine.pack_operator(dA)
+    assert dA.packed is None and not dA.desc().packed
+    x = rng.standard_normal(2000)
+    assert np.array_equal(engine.spmm(dA, dvec(x)).cpu().numpy(), A @ x)
