@@ -768,6 +768,189 @@ cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __re
   cgs_flush(acc, 1, part, 1);
 }
 
+// ---- two-pass CGS2 through the Gram matrix (the default)
+// CGS2's second projection h2 = V^T (w - V h1) equals h1 - G h1 with
+// G = V^T V, so when G is carried along the step needs no second sweep over V
+// for it: pass A (dots, above) gives h1 and |w|^2, a one-CTA kernel forms the
+// total coefficients c = h1 + h2 = 2 h1 - G h1 and the new vector's norm
+// |w - V c|^2 = |w|^2 - 2 c.h1 + c^T G c, and ONE more pass writes
+// v_new = (w - V c) / h_{j+1}, the iterate x = x0 + e + V y with |x|^2, and --
+// from the same registers -- V^T v_new and |v_new|^2, the new row of G.  G holds
+// the stored basis' true inner products (round-off defects and the new
+// vector's actual norm included), so later projections compensate them to first
+// order; the defects themselves are what CGS2 leaves, O(eps |w| / h_{j+1}).
+// Two reads of the basis per Arnoldi step instead of three.  When the norm
+// formula cancels more than six digits (w all but inside span V) the step
+// writes w - V c unscaled and takes the explicit norm (cgs_fix_*).
+constexpr int CGS_LDG = CGS_MAXM + 1;
+
+__global__ void cgs_gram_init_kernel(double* __restrict__ G) {
+  BAMG_PDL_PROLOGUE();
+  for (int i = threadIdx.x; i < CGS_LDG * CGS_LDG; i += blockDim.x) G[i] = i == 0 ? 1.0 : 0.0;
+}
+
+// hv[0..m) = h1, hv[m] = |w|^2  ->  hv[0..m) = c2[0..m) = 2 h1 - G h1,
+// nrm2 = |w - V c|^2; flag 0 (safe) or 2 (explicit norm)
+__global__ void cgs_gram_coef_kernel(int m, const double* __restrict__ G, double* __restrict__ hv,
+                                     double* __restrict__ c2, double* __restrict__ nrm2,
+                                     double* __restrict__ flag) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double h1[CGS_MAXM], c[CGS_MAXM], gc[CGS_MAXM];
+  const int g = threadIdx.x;
+  if (g < m) h1[g] = hv[g];
+  __syncthreads();
+  if (g < m) {
+    double t = 0.0;
+    for (int a = 0; a < m; ++a) t = fma(G[g * CGS_LDG + a], h1[a], t);
+    c[g] = h1[g] + (h1[g] - t);
+  }
+  __syncthreads();
+  if (g < m) {
+    double t = 0.0;
+    for (int a = 0; a < m; ++a) t = fma(G[g * CGS_LDG + a], c[a], t);
+    gc[g] = t;
+    hv[g] = c[g];
+    c2[g] = c[g];
+  }
+  __syncthreads();
+  if (g == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int a = 0; a < m; ++a) {
+      s1 = fma(c[a], h1[a], s1);
+      s2 = fma(c[a], gc[a], s2);
+    }
+    const double wn = hv[m];
+    const double d = (wn - s1) - (s1 - s2);
+    const bool unsafe = !(d >= 1e-6 * wn) || !(wn > 0.0);
+    nrm2[0] = unsafe ? 0.0 : d;
+    flag[0] = unsafe ? 2.0 : 0.0;
+  }
+}
+
+// the update pass: ww = w - V c; v_new = ww / state[1] (unscaled when flag = 2,
+// skipped on happy breakdown); x = x0 + e + V y (flag 0 only);
+// part[b][0..m) = V^T ww, part[b][m] = |ww|^2, part[b][m + 1] = |x|^2
+template <int MAXM>
+__global__ void __launch_bounds__(CGS_THREADS)
+cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
+                  const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
+                  const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
+                  int64_t n, double* __restrict__ vnew, double* __restrict__ x, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
+  constexpr int NB = MAXM / 32;
+  __shared__ const double* sp[MAXM];
+  __shared__ double sc[MAXM], sy[MAXM];
+  __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
+    sc[g] = g < m ? c[g] : 0.0;
+    sy[g] = g < m ? y[g] : 0.0;
+  }
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const bool unsafe = flag[0] == 2.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  double dot[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) dot[q] = 0.0;
+  double wn2 = 0.0, xn2 = 0.0;
+  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
+    const int64_t i = base + lane;
+    const bool ok = i < r1;
+    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
+    double v[MAXM];
+#pragma unroll
+    for (int g = 0; g < MAXM; ++g) v[g] = __ldcs(sp[g] + ic);
+    const double wi = w[ic], x0i = x0[ic], ei = e[ic];
+    double t = 0.0, u = 0.0;
+#pragma unroll
+    for (int g = 0; g < MAXM; ++g) {
+      t = fma(sc[g], v[g], t);
+      u = fma(sy[g], v[g], u);
+    }
+    double ww = wi - t;
+    if (ok) {
+      if (unsafe) {
+        vnew[i] = ww;
+      } else {
+        if (!happy) vnew[i] = ww * inv;
+        const double xi = x0i + (ei + u);
+        x[i] = xi;
+        xn2 = fma(xi, xi, xn2);
+      }
+    } else {
+      ww = 0.0;
+    }
+    wn2 = fma(ww, ww, wn2);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      if (q * 32 >= m) break;
+      double pr[32];
+#pragma unroll
+      for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * ww;
+      dot[q] += warp_transpose_sum32(pr, lane);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
+  wn2 = warp_sum(wn2);
+  xn2 = warp_sum(xn2);
+  if (lane == 0) acc[wid][MAXM] = wn2, acc[wid][MAXM + 1] = xn2;
+  __syncthreads();
+  const int nslots = m + 2;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
+    const int slot = q >= m ? MAXM + (q - m) : q;
+    double t = 0.0;
+    for (int ww2 = 0; ww2 < CGS_WARPS; ++ww2) t += acc[ww2][slot];
+    part[(int64_t)blockIdx.x * (m + 2) + q] = t;
+  }
+}
+
+// (flag 2 only) the explicit norm |w - V c|^2 = gs[m] for the Givens step
+__global__ void cgs_gram_fix_norm_kernel(const double* __restrict__ flag, const double* __restrict__ gs, int m,
+                                         double* __restrict__ nrm2) {
+  BAMG_PDL_PROLOGUE();
+  if (threadIdx.x == 0 && flag[0] == 2.0) nrm2[0] = gs[m];
+}
+
+// row / column m of G from gs = V^T ww, |ww|^2 (ww scaled by 1 / state[1] to
+// v_new), and |x|: sqrt(gs[m + 1]), or from cgs_fix_x_kernel's partials after
+// an explicit-norm step
+__global__ void cgs_gram_update_kernel(int m, const double* __restrict__ gs, const double* __restrict__ state,
+                                       const double* __restrict__ flag, const double* __restrict__ part_x, int nbx,
+                                       double* __restrict__ G, double* __restrict__ xnorm) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double red[32];
+  const bool unsafe = flag[0] == 2.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  if (!happy && m < CGS_MAXM) {
+    for (int g = threadIdx.x; g < m; g += blockDim.x) {
+      const double v = gs[g] * inv;
+      G[g * CGS_LDG + m] = v;
+      G[m * CGS_LDG + g] = v;
+    }
+    if (threadIdx.x == 0) G[m * CGS_LDG + m] = gs[m] * inv * inv;
+  }
+  if (!unsafe) {
+    if (threadIdx.x == 0) xnorm[0] = sqrt(gs[m + 1]);
+    return;
+  }
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nbx; b += blockDim.x) v += part_x[b];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    xnorm[0] = sqrt(t);
+  }
+}
+
 // unsafe step, part 1 (one CTA): |w''|^2 from pass C's partials -> the
 // normal Givens path (givens_kernel is launched after this by the host loop
 // with nrm2 = this value).  No-op when the Pythagorean norm was safe.
@@ -900,6 +1083,12 @@ static void cgs_apply_env() {
   cudaMemcpyToSymbol(cgs_force_two_pass, &v, sizeof(bool));
 }
 
+// BAMG_CGS_GRAM=0: the three-pass CGS2 (explicit second projection) instead of the Gram form
+static bool cgs_gram_enabled() {
+  const char* e = getenv("BAMG_CGS_GRAM");
+  return !(e && e[0] == '0');
+}
+
 static bool cgs_fast_enabled() {
   static const bool on = !(getenv("BAMG_CGS_SLOW") && getenv("BAMG_CGS_SLOW")[0] == '1');
   return on;
@@ -962,8 +1151,10 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   BAMG_TRY(arena_get(ctx, std::max((size_t)nb * (m_cap + 2), (size_t)CGS_MAX_BLOCKS * (CGS_MAXM + 2)), &part));
   BAMG_TRY(arena_get(ctx, 8, &scal));
   BAMG_TRY(arena_get(ctx, 4, &state));
-  double* flag;
+  double *flag, *gram, *gsum;
   BAMG_TRY(arena_get(ctx, 2, &flag));
+  BAMG_TRY(arena_get(ctx, (size_t)CGS_LDG * CGS_LDG, &gram));
+  BAMG_TRY(arena_get(ctx, CGS_MAXM + 2, &gsum));
   GmresWork& W = gmres_work(ctx);
   const int blk = 256;
   const int grd = grid_for(n, blk);
@@ -1042,6 +1233,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
 
   int iters = 0;
   int one_pass_steps = 0;  // Arnoldi steps that took the single projection (DGKS)
+  int explicit_norm_steps = 0;  // Gram-path steps that fell back to the explicit norm
   bool converged = false;
   bool first_cycle = true;
   while (iters < max_iters && !converged) {
@@ -1070,6 +1262,49 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
       BAMG_TRY(basis_reserve(ctx, W, n, j + 2));
       // w = op(V_j)
       BAMG_TRY(apply_op(ctx, B, h, W.basis[j], tmp, w));
+      if (j + 1 <= CGS_MAXM && cgs_fast_enabled() && cgs_gram_enabled()) {
+        // two passes over V (see cgs_gram_coef_kernel): dots, then the update with x, |x| and G's new row
+        const int mj = j + 1;
+        if (j == 0) BAMG_LAUNCH(ctx, cgs_gram_init_kernel, 1, 256, 0, gram);
+        auto dots = mj <= 32 ? cgs_dots_kernel<32, 0> : cgs_dots_kernel<64, 0>;
+        auto upd = mj <= 32 ? cgs_update_kernel<32> : cgs_update_kernel<64>;
+        const int cb = std::min(cgs_grid(ctx, (const void*)dots, n), cgs_grid(ctx, (const void*)upd, n));
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 1) * n, dots, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)nullptr, w, n, part, (const double*)nullptr);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
+                    mj + 1, mj + 1, hv, (const double*)nullptr, 0u);  // h1 and |w|^2
+        BAMG_LAUNCH(ctx, cgs_gram_coef_kernel, 1, CGS_MAXM, 0, mj, (const double*)gram, hv, h2, scal + 3, flag);
+        BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
+                    y, state, (const double*)flag, 0b011u);
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 5) * n, upd, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
+                        (const double*)h2, (const double*)y, (const double*)w, x0, (const double*)e,
+                        (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 2) * 32, 256), 256, 0, (const double*)part, cb,
+                    mj + 2, mj + 2, gsum, (const double*)nullptr, 0u);  // V^T ww, |ww|^2, |x|^2
+        BAMG_LAUNCH(ctx, cgs_gram_fix_norm_kernel, 1, 32, 0, (const double*)flag, (const double*)gsum, mj, scal + 3);
+        BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
+                    y, state, (const double*)flag, 0b100u);
+        BAMG_LAUNCH(ctx, cgs_fix_x_kernel, cb, 256, 0, (const double* const*)W.dVp, mj, (const double*)y, x0,
+                    (const double*)e, (const double*)state, (const double*)flag, n, W.basis[j + 1], x, part);
+        BAMG_LAUNCH(ctx, cgs_gram_update_kernel, 1, 256, 0, mj, (const double*)gsum, (const double*)state,
+                    (const double*)flag, (const double*)part, cb, gram, scal + 1);
+        ++iters;
+        used = j + 1;
+        double mval;
+        bool happy = false;
+        BAMG_TRY(metric_state(x, &mval, &happy, true));
+        if (last_code == 2.0) ++explicit_norm_steps;
+        history_host[nhist++] = mval;
+        if (mval <= rtol) converged = true;
+        if (converged || happy || iters >= max_iters) {
+          if (happy) converged = true;
+          BAMG_LAUNCH(ctx, combine_kernel, grd, blk, 0, W.dVp, used, y, nullptr, e, nullptr, n, tmp);
+          BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(e, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+          broke = true;
+          break;
+        }
+        continue;
+      }
       if (j + 1 <= CGS_MAXM && cgs_fast_enabled()) {
         // three passes over V (see cgs_dots_kernel); x and |x| formed in pass C
         const int mj = j + 1;
@@ -1161,7 +1396,8 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
   *iters_host = iters;
   *nhistory_host = nhist;
   if (getenv("BAMG_DEBUG"))
-    fprintf(stderr, "[bamg] gmres: %d iterations, %d with one projection (DGKS)\n", iters, one_pass_steps);
+    fprintf(stderr, "[bamg] gmres: %d iterations, %d with one projection (DGKS), %d with the explicit norm\n", iters,
+            one_pass_steps, explicit_norm_steps);
   BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return converged ? 0 : 1;
 }
