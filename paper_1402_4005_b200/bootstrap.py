@@ -480,7 +480,10 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     with _phase("level_ops"):
         # the generators' B = I - A has a handful of distinct values: the k = 1
         # sweeps / residuals / SpMVs of the solve stream its packed copy
-        # (4 instead of 12 bytes per entry, same bits); redone every setup
+        # (4 instead of 12 bytes per entry, same bits); redone every setup, on a
+        # wrapper of its own so the hierarchy owns the packed arrays (the
+        # caller's operator is left as it came)
+        A = DeviceCSR(A.rowptr, A.col, A.val, A.shape, is_identity=A.is_identity)
         engine.pack_operator(A)
         ops = _LevelOps(A)
     rng = np.random.default_rng(ss_init) if draws is None else None

@@ -340,13 +340,91 @@ colreduce_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// k = 8 / 16 with 16-byte aligned blocks: the CTA's row chunk read as one flat
+// stream of double2 (fully coalesced; the row-per-thread form above touches 32
+// lines per load instruction and ran at 2.1 TB/s on cfg4's level 0).  A
+// thread's stride is a whole number of rows, so it always sees the same column
+// pair; UR loads are in flight per thread.  Fixed order: thread partials, then
+// per column the 256 / (KK / 2) owning threads in ascending order, then the
+// last CTA's pass over the per-CTA partials as above.
+template <int KK, int UR>
+__global__ void __launch_bounds__(RED_THREADS)
+colreduce_wide_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t n, int kind,
+                      double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ out,
+                      int take_sqrt) {
+  BAMG_PDL_PROLOGUE();
+  constexpr int PAIRS = KK / 2;
+  static_assert(RED_THREADS % PAIRS == 0, "a thread must keep its column pair");
+  __shared__ double sh[RED_THREADS][2];
+  __shared__ bool last;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per;
+  const int64_t r1 = r0 + per < n ? r0 + per : n;
+  const double2* X2 = reinterpret_cast<const double2*>(X);
+  const double2* Y2 = reinterpret_cast<const double2*>(Y);
+  const int64_t u1 = r1 * PAIRS;
+  double a0 = 0.0, a1 = 0.0;
+  int64_t u = r0 * PAIRS + threadIdx.x;
+  for (; u + (int64_t)(UR - 1) * RED_THREADS < u1; u += (int64_t)UR * RED_THREADS) {
+    double2 xv[UR], yv[UR];
+#pragma unroll
+    for (int i = 0; i < UR; ++i) {
+      xv[i] = X2[u + (int64_t)i * RED_THREADS];
+      if (kind != 0) yv[i] = Y2[u + (int64_t)i * RED_THREADS];
+    }
+#pragma unroll
+    for (int i = 0; i < UR; ++i) {
+      a0 += xv[i].x * (kind == 0 ? xv[i].x : yv[i].x);
+      a1 += xv[i].y * (kind == 0 ? xv[i].y : yv[i].y);
+    }
+  }
+  for (; u < u1; u += RED_THREADS) {
+    const double2 xv = X2[u];
+    const double2 yv = kind == 0 ? xv : Y2[u];
+    a0 += xv.x * yv.x;
+    a1 += xv.y * yv.y;
+  }
+  sh[threadIdx.x][0] = a0;
+  sh[threadIdx.x][1] = a1;
+  __syncthreads();
+  if (threadIdx.x < KK) {
+    const int c = threadIdx.x;
+    // the chunk starts on a row boundary: thread t owns columns 2 (t % PAIRS), + 1
+    double v = 0.0;
+    for (int t = c / 2; t < RED_THREADS; t += PAIRS) v += sh[t][c & 1];
+    partial[(int64_t)blockIdx.x * KK + c] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = wid; c < KK; c += RED_THREADS / 32) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += __ldcg(partial + (int64_t)b * KK + c);
+    v = warp_sum(v);
+    if (lane == 0) out[c] = take_sqrt ? sqrt(v) : v;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k, int kind,
               double* out_dev, int take_sqrt) {
   BAMG_REQUIRE(ctx, k >= 1 && k <= KMAX, "k must lie in [1, 32]");
   double* partial = nullptr;
   BAMG_TRY(arena_get(ctx, (size_t)RED_BLOCKS * k, &partial));
   const int g = red_blocks_for(n);
-  if (k == 8)
+  const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0;
+  if (k == 16 && al16)
+    BAMG_LAUNCH(ctx, (colreduce_wide_kernel<16, 8>), g, RED_THREADS, 0, X, Y, n, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else if (k == 8 && al16)
+    BAMG_LAUNCH(ctx, (colreduce_wide_kernel<8, 8>), g, RED_THREADS, 0, X, Y, n, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else if (k == 8)
     BAMG_LAUNCH(ctx, (colreduce_kernel<8, 4>), g, RED_THREADS, 0, X, Y, n, k, kind, partial, ctx->counters + 0,
                 out_dev, take_sqrt);
   else if (k == 16)
@@ -409,7 +487,8 @@ __global__ void col_scale_div_kernel(double* X, int64_t n, int k_rt, const doubl
 // consecutive 16-byte words (the row-per-thread form's loads and stores were
 // 8 bytes at a 64-byte stride per lane).
 template <int KK>
-__global__ void col_scale_div_flat_kernel(double* X, int64_t total2, const double* s, int fill_c, double fill_v) {
+__global__ void col_scale_div_flat_kernel(double* X, int64_t total2, const double* s, int fill_c, double fill_v,
+                                          const double* src) {
   BAMG_PDL_PROLOGUE();
   static_assert(KK % 2 == 0 && (KK & (KK - 1)) == 0, "power-of-two k");
   __shared__ double sd[KK], srd[KK];
@@ -423,7 +502,7 @@ __global__ void col_scale_div_flat_kernel(double* X, int64_t total2, const doubl
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total2) return;
   double2* x2 = reinterpret_cast<double2*>(X);
-  double2 v = x2[i];
+  double2 v = src ? reinterpret_cast<const double2*>(src)[i] : x2[i];  // src: out-of-place (X = src / s)
   const int c = (int)((2 * i) & (KK - 1));
   v.x = c == fill_c ? fill_v : div_rn_recip(v.x, sd[c], srd[c]);
   v.y = c + 1 == fill_c ? fill_v : div_rn_recip(v.y, sd[c + 1], srd[c + 1]);
@@ -432,12 +511,18 @@ __global__ void col_scale_div_flat_kernel(double* X, int64_t total2, const doubl
 
 // X[:, c] /= s[c]; fill_c >= 0: column fill_c is set to fill_v instead (the
 // refresh's normalise-then-overwrite of the first test vector in one pass)
-int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s, int fill_c, double fill_v) {
-  const bool al16 = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s, int fill_c, double fill_v,
+                      const double* src) {
+  const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (src && src != X && !((k == 8 || k == 16) && al16)) {  // only the flat kernels divide out of place
+    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(X, src, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    src = nullptr;
+  }
+  if (src == X) src = nullptr;
   if (k == 8 && al16)
-    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<8>, grid_for(n * 4, 256), 256, 0, X, n * 4, s, fill_c, fill_v);
+    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<8>, grid_for(n * 4, 256), 256, 0, X, n * 4, s, fill_c, fill_v, src);
   else if (k == 16 && al16)
-    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<16>, grid_for(n * 8, 256), 256, 0, X, n * 8, s, fill_c, fill_v);
+    BAMG_LAUNCH(ctx, col_scale_div_flat_kernel<16>, grid_for(n * 8, 256), 256, 0, X, n * 8, s, fill_c, fill_v, src);
   else if (k == 8)
     BAMG_LAUNCH(ctx, col_scale_div_kernel<8>, grid_for(n, 256), 256, 0, X, n, k, s, fill_c, fill_v);
   else if (k == 16)
@@ -448,7 +533,7 @@ int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* 
 }
 
 extern "C" int bamg_col_scale_div(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s) {
-  return col_scale_div_dev(ctx, X, n, k, s, -1, 0.0);
+  return col_scale_div_dev(ctx, X, n, k, s, -1, 0.0, nullptr);
 }
 
 __global__ void col_fill_kernel(double* X, int64_t n, int k, int c, double value) {

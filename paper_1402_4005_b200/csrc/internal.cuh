@@ -25,8 +25,9 @@ int rayleigh_dev(bamg_ctx* ctx, const bamg_csr* A, const bamg_csr* M, const bamg
                  const double* U, const double* V, int64_t n, int k, double* sigma,
                  double* U_flip_or_null, int mode, double* work3);
 int normalize_cols_dev(bamg_ctx* ctx, double* X, int64_t n, int k);
+// src non-null: X = src / s (out of place)
 int col_scale_div_dev(bamg_ctx* ctx, double* X, int64_t n, int k, const double* s, int fill_c = -1,
-                      double fill_v = 0.0);
+                      double fill_v = 0.0, const double* src = nullptr);
 int col_fill_dev(bamg_ctx* ctx, double* X, int64_t n, int k, int c, double value);
 
 // C = alpha op(A) op(B) + beta C, column-major fp64 (gemm.cu)

@@ -257,8 +257,20 @@ extern "C" int bamg_smooth_block(bamg_ctx* ctx, const bamg_csr* A, const bamg_cs
       if (M) BAMG_TRY(arena_get(ctx, (size_t)total, &MU));
       if (N) BAMG_TRY(arena_get(ctx, (size_t)total, &NV));
     }
+    // an odd number (>= 3) of sweeps would leave the result in the scratch pair and cost a
+    // device copy of both blocks: a third buffer per side routes the last sweep into U / V
+    // (U -> U2 -> U3 -> U)
+    double *U3 = nullptr, *V3 = nullptr;
+    if ((nsweeps & 1) && nsweeps >= 3) {
+      BAMG_TRY(arena_get(ctx, (size_t)total, &U3));
+      BAMG_TRY(arena_get(ctx, (size_t)total, &V3));
+    }
     double *u = U, *v = V, *uo = U2, *vo = V2;
     for (int s = 0; s < nsweeps; ++s) {
+      if (U3 && s >= 1) {  // sweeps 1 .. n-1 alternate U2 <-> U3 and the last one lands in U / V
+        uo = s == nsweeps - 1 ? U : (u == U2 ? U3 : U2);
+        vo = s == nsweeps - 1 ? V : (v == V2 ? V3 : V2);
+      }
       BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(peak, 0, sizeof(double) * 2 * k, ctx->stream));
       // right vectors: rhs sigma * M u (the mass product fused into the sweep
       // when the rows kernel covers k), left vectors: sigma * N v
@@ -360,9 +372,11 @@ extern "C" int bamg_test_weights(bamg_ctx* ctx, const bamg_csr* A, const double*
   ctx->arena.reset();
   BAMG_REQUIRE(ctx, k >= 1 && k <= 32, "k must lie in [1, 32]");
   const int64_t total = n * k;
-  if (Xn != X)
-    BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(Xn, X, sizeof(double) * total, cudaMemcpyDeviceToDevice, ctx->stream));
-  BAMG_TRY(normalize_cols_dev(ctx, Xn, n, k));
+  // Xn = X / |X| column-wise: the norms from X, the division straight into Xn (no copy of the block)
+  double* nrm;
+  BAMG_TRY(arena_get(ctx, (size_t)k, &nrm));
+  BAMG_TRY(colreduce(ctx, X, nullptr, n, k, 0, nrm, 1));
+  BAMG_TRY(col_scale_div_dev(ctx, Xn, n, k, nrm, -1, 0.0, X));
   double *R, *res;
   BAMG_TRY(arena_get(ctx, (size_t)total, &R));
   BAMG_TRY(arena_get(ctx, (size_t)k, &res));

@@ -794,9 +794,6 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
 }
 
 static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea);
-template <int EPI>
-static int launch_stream(bamg_ctx* ctx, int k, double bytes, const bamg_csr* A, const double* X, double* Y,
-                         const EpiArgs& ea);
 
 static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, int k,
                        double* Y, const EpiArgs& ea) {
@@ -814,16 +811,6 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
   // 16-byte vector loads need aligned blocks when K is even (K = 1 has none)
   bool aligned = (k & 1) || ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
                               reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold)) & 15) == 0;
-  if (epi != EPI_JACOBI_M) {
-    int rc = 1;
-    switch (epi) {
-      case EPI_PLAIN: rc = launch_stream<EPI_PLAIN>(ctx, k, bytes, A, X, Y, ea); break;
-      case EPI_RESID: rc = launch_stream<EPI_RESID>(ctx, k, bytes, A, X, Y, ea); break;
-      case EPI_ADD: rc = launch_stream<EPI_ADD>(ctx, k, bytes, A, X, Y, ea); break;
-      default: rc = launch_stream<EPI_JACOBI>(ctx, k, bytes, A, X, Y, ea);
-    }
-    if (rc <= 0) return rc;
-  }
   if (k == 1 && A->packed) {
     const int rc = launch_packed(ctx, epi, A, X, Y, ea);
     if (rc <= 0) return rc;
@@ -1031,9 +1018,17 @@ extern "C" int bamg_csr_pack(bamg_ctx* ctx, const bamg_csr* A, uint32_t* packed,
   return 0;
 }
 
+#ifndef BAMG_PACKED_U
+#define BAMG_PACKED_U 4
+#endif
+constexpr int PACKED_U = BAMG_PACKED_U;
+#ifndef BAMG_PACKED_MINB
+#define BAMG_PACKED_MINB 8
+#endif
+
 // thread per row, k = 1; same sums as csr_rows_kernel<EPI, 1, 1, U>
 template <int EPI, int U>
-__global__ void __launch_bounds__(TILE_THREADS, 8)
+__global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
 csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint32_t* __restrict__ pk,
                        const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
                        EpiArgs ea) {
@@ -1044,6 +1039,15 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint
   const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
   if (row >= nrows) return;
   const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  // epilogue operands depend on the row only: in flight with the row's first loads
+  double eb = 0.0, exo = 0.0;
+  bool sk = false;
+  if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
+  if (EPI == EPI_JACOBI) {
+    if (ea.b) eb = __ldg(ea.b + row);
+    exo = __ldg(ea.xold + row);
+    sk = ea.skip[row] != 0;
+  }
   double acc = 0.0, dd = 0.0, rdd = __longlong_as_double(0x7FF0000000000000ll);  // no diagonal entry: d = 0, 1/d = inf
   const double* xr = X + row;
   for (int j = jb; j < je; j += U) {
@@ -1066,12 +1070,11 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint
   if (EPI == EPI_PLAIN) {
     out = acc;
   } else if (EPI == EPI_RESID) {
-    out = __dsub_rn(ea.b[row], acc);
+    out = __dsub_rn(eb, acc);
   } else {
-    const double bv = ea.b ? ea.b[row] : 0.0;
-    const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc));
-    const double upd = ea.skip[row] != 0 ? 0.0 : div_rn_recip(num, dd, rdd);
-    out = __dadd_rn(ea.xold[row], upd);
+    const double num = __dmul_rn(ea.omega, __dsub_rn(eb, acc));
+    const double upd = sk ? 0.0 : div_rn_recip(num, dd, rdd);
+    out = __dadd_rn(exo, upd);
   }
   Y[row] = out;
 }
@@ -1105,384 +1108,18 @@ static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double
   const int fam = A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE;
   switch (epi) {
     case EPI_PLAIN:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, 4>), grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->packed, A->dict, X, Y, ea);
       break;
     case EPI_RESID:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, 4>), grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->packed, A->dict, X, Y, ea);
       break;
     default:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, 4>), grid, TILE_THREADS, 0, A->nrows,
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
                       A->rowptr, A->packed, A->dict, X, Y, ea);
   }
   return 0;
-}
-
-// -------------------------------------------- bulk-staged CSR stream kernel
-// The row kernels above are bound by dependent global-memory latencies, not
-// by bytes: rowptr -> col/val -> gathers -> epilogue operands, each a DRAM
-// round trip with only a slice of the row's bytes in flight (ncu, cfg4 level
-// 0: k = 16 sweeps 40 % of HBM, packed k = 1 sweeps 60 %, long scoreboard).
-// Every one of those operands except the gathers is a CONTIGUOUS stream per
-// row tile, so here a persistent CTA hands them to the bulk-copy engine
-// (cp.async.bulk global -> shared, mbarrier complete_tx) STAGES - 1 tiles
-// ahead: rowptr[r0 .. r0 + RB], the tile's col / val (or packed words) slice,
-// the epilogue rows (x_old, b, or the residual's b), d, 1/d and the skip
-// bytes.  The threads then read only shared memory plus the x gathers, which
-// mostly hit L1 / L2.  In-flight bytes no longer depend on registers or
-// occupancy: (STAGES - 1) x ~13 KB per CTA.  Arithmetic and summation order
-// are those of csr_rows_kernel (bit-identical).  A tile whose slices do not
-// fit the stage (more than CAPF entries per row on average), the last partial
-// tile, or slices that would need bytes past an array's last whole 16-byte
-// chunk take the same code with global loads.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "BAMG_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@p bra BAMG_DONE_%=;\n"
-      "bra BAMG_WAIT_%=;\n"
-      "BAMG_DONE_%=:\n"
-      "}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-struct StreamHdr {
-  int streamed;  // 1: the stage holds the tile; 0: read global memory
-  int nz0;       // first entry of the tile
-  int sh_rp, sh_col, sh_val, sh_skip;  // element shifts of the 16-byte aligned copies
-  int pad0, pad1;
-};
-
-template <int K, int G, bool PACKED, int EPI, int CAPF>
-struct StreamLayout {
-  static constexpr int RB = TILE_THREADS / G;
-  static constexpr int CAP = RB * CAPF;
-  static constexpr int r16(int x) { return (x + 15) & ~15; }
-  static constexpr bool NEED_E0 = EPI != EPI_PLAIN;                  // b (resid) / x_old (add, jacobi)
-  static constexpr bool NEED_E1 = EPI == EPI_JACOBI;                 // b
-  static constexpr bool NEED_D = EPI == EPI_JACOBI && !PACKED;       // d, 1/d
-  static constexpr bool NEED_SKIP = EPI == EPI_JACOBI;
-  static constexpr int OFF_HDR = 0;
-  static constexpr int OFF_RP = 32;
-  static constexpr int OFF_COL = OFF_RP + r16((RB + 1) * 4 + 16);    // col, or the packed words
-  static constexpr int OFF_VAL = OFF_COL + r16(CAP * 4 + 16);
-  static constexpr int OFF_E0 = OFF_VAL + (PACKED ? 0 : r16(CAP * 8 + 16));
-  static constexpr int OFF_E1 = OFF_E0 + (NEED_E0 ? RB * K * 8 : 0);
-  static constexpr int OFF_D = OFF_E1 + (NEED_E1 ? RB * K * 8 : 0);
-  static constexpr int OFF_RD = OFF_D + (NEED_D ? r16(RB * 8) : 0);
-  static constexpr int OFF_SKIP = OFF_RD + (NEED_D ? r16(RB * 8) : 0);
-  static constexpr int STAGE_BYTES = r16(OFF_SKIP + (NEED_SKIP ? r16(RB + 16) : 0));
-};
-
-struct StreamArgs {
-  int nrows, ntiles;
-  int64_t nnz;
-  const int32_t* rowptr;
-  const int32_t* col;      // PACKED: the packed words
-  const double* val;       // PACKED: unused
-  const double* dict;      // PACKED: 512 doubles
-  const double* X;
-  double* Y;
-  int64_t xrows;           // rows of the epilogue blocks (= nrows)
-};
-
-// whole 16-byte chunks covering elements [e0, e0 + cnt) of an array of `total` elements of `es` bytes;
-// false when that needs bytes past the array's last whole chunk
-__device__ __forceinline__ bool stream_plan(int64_t e0, int64_t cnt, int es, int64_t total, int64_t& a0, uint32_t& bytes,
-                                            int& shift) {
-  const int64_t b0 = e0 * es, b1 = (e0 + cnt) * es;
-  a0 = b0 & ~(int64_t)15;
-  const int64_t a1 = (b1 + 15) & ~(int64_t)15;
-  bytes = (uint32_t)(a1 - a0);
-  shift = (int)((b0 - a0) / es);
-  return a1 <= ((total * es) & ~(int64_t)15) || a1 == b1 && b1 <= total * es;
-}
-
-constexpr int STREAM_THREADS = TILE_THREADS + 32;  // 8 consumer warps + the producer warp
-
-template <int EPI, int K, int G, int U, bool PACKED, int CAPF, int STAGES, int MINB>
-__global__ void __launch_bounds__(STREAM_THREADS, MINB)
-csr_stream_kernel(StreamArgs sa, EpiArgs ea) {
-  BAMG_PDL_PROLOGUE();
-  using L = StreamLayout<K, G, PACKED, EPI, CAPF>;
-  constexpr int V = K / G;
-  constexpr int RB = L::RB;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[STAGES], empty[STAGES];
-  __shared__ unsigned long long s_peak[K];
-  __shared__ double s_dict[PACKED ? 2 * PACK_DICT : 1];
-  const bool want_peak = EPI == EPI_JACOBI && ea.peak != nullptr;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], TILE_THREADS / 32);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (want_peak && threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
-  if (PACKED)
-    for (int i = threadIdx.x; i < 2 * PACK_DICT; i += STREAM_THREADS) s_dict[i] = sa.dict[i];
-  __syncthreads();
-
-  const int lr = threadIdx.x / G;
-  const int sub = threadIdx.x - lr * G;
-  const int voff = sub * V;
-  double pk[V];
-#pragma unroll
-  for (int q = 0; q < V; ++q) pk[q] = 0.0;
-
-  // producer (thread 0): hand tile `t` to the copy engine, into stage `s`
-  auto issue = [&](int t, int s) {
-    unsigned char* st = smem_raw + (size_t)s * L::STAGE_BYTES;
-    StreamHdr* h = reinterpret_cast<StreamHdr*>(st + L::OFF_HDR);
-    const int r0 = t * RB;
-    const int rows = min(RB, sa.nrows - r0);
-    bool ok = rows == RB;
-    int nz0 = 0, cnt = 0;
-    if (ok) {
-      nz0 = __ldg(sa.rowptr + r0);
-      cnt = __ldg(sa.rowptr + r0 + RB) - nz0;
-      ok = cnt <= L::CAP;
-    }
-    int64_t a_rp = 0, a_col = 0, a_val = 0, a_sk = 0;
-    uint32_t b_rp = 0, b_col = 0, b_val = 0, b_sk = 0;
-    int sh_rp = 0, sh_col = 0, sh_val = 0, sh_sk = 0;
-    if (ok) {
-      ok = stream_plan(r0, RB + 1, 4, (int64_t)sa.nrows + 1, a_rp, b_rp, sh_rp);
-      if (cnt > 0) {
-        ok = ok && stream_plan(nz0, cnt, 4, sa.nnz, a_col, b_col, sh_col);
-        if (!PACKED) ok = ok && stream_plan(nz0, cnt, 8, sa.nnz, a_val, b_val, sh_val);
-      }
-      if (L::NEED_SKIP) ok = ok && stream_plan(r0, RB, 1, sa.nrows, a_sk, b_sk, sh_sk);
-    }
-    h->streamed = ok ? 1 : 0;
-    h->nz0 = nz0;
-    h->sh_rp = sh_rp, h->sh_col = sh_col, h->sh_val = sh_val, h->sh_skip = sh_sk;
-    if (!ok) {
-      mbar_arrive(&full[s]);
-      return;
-    }
-    constexpr uint32_t ROWB = RB * K * 8;
-    uint32_t total = b_rp + b_col + b_val + b_sk;
-    if (L::NEED_E0) total += ROWB;
-    if (L::NEED_E1 && ea.b) total += ROWB;
-    if (L::NEED_D) total += RB * 8 + (ea.rd ? RB * 8 : 0);
-    mbar_expect_tx(&full[s], total);
-    bulk_g2s(st + L::OFF_RP, reinterpret_cast<const char*>(sa.rowptr) + a_rp, b_rp, &full[s]);
-    if (b_col) bulk_g2s(st + L::OFF_COL, reinterpret_cast<const char*>(sa.col) + a_col, b_col, &full[s]);
-    if (b_val) bulk_g2s(st + L::OFF_VAL, reinterpret_cast<const char*>(sa.val) + a_val, b_val, &full[s]);
-    const int64_t rowoff = (int64_t)r0 * K;
-    if (L::NEED_E0) {
-      const double* src = EPI == EPI_RESID ? ea.b : ea.xold;
-      bulk_g2s(st + L::OFF_E0, src + rowoff, ROWB, &full[s]);
-    }
-    if (L::NEED_E1 && ea.b) bulk_g2s(st + L::OFF_E1, ea.b + rowoff, ROWB, &full[s]);
-    if (L::NEED_D) {
-      bulk_g2s(st + L::OFF_D, ea.d + r0, RB * 8, &full[s]);
-      if (ea.rd) bulk_g2s(st + L::OFF_RD, ea.rd + r0, RB * 8, &full[s]);
-    }
-    if (L::NEED_SKIP) bulk_g2s(st + L::OFF_SKIP, reinterpret_cast<const char*>(ea.skip) + a_sk, b_sk, &full[s]);
-  };
-
-  const int first = blockIdx.x, step = gridDim.x;
-  if (threadIdx.x >= TILE_THREADS) {
-    // producer warp: one lane runs up to STAGES tiles ahead of the consumers; its
-    // rowptr reads (the tile's entry range) stall nobody else
-    if (threadIdx.x == TILE_THREADS) {
-      int it = 0;
-      for (int t = first; t < sa.ntiles; t += step, ++it) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(it / STAGES - 1) & 1u);
-        issue(t, s);
-      }
-    }
-  } else {
-  int it = 0;
-  for (int t = first; t < sa.ntiles; t += step, ++it) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
-    const unsigned char* st = smem_raw + (size_t)s * L::STAGE_BYTES;
-    const StreamHdr h = *reinterpret_cast<const StreamHdr*>(st + L::OFF_HDR);
-    const int r0 = t * RB;
-    const int rows = min(RB, sa.nrows - r0);
-    if (lr < rows) {
-      const int row = r0 + lr;
-      const bool stg = h.streamed != 0;
-      const int32_t* s_rp = reinterpret_cast<const int32_t*>(st + L::OFF_RP) + h.sh_rp;
-      // entry j of the tile lives at s_col[j] / s_val[j] (pointers pre-shifted by the tile's first entry)
-      const int32_t* s_col = reinterpret_cast<const int32_t*>(st + L::OFF_COL) + h.sh_col - h.nz0;
-      const double* s_val = reinterpret_cast<const double*>(st + L::OFF_VAL) + h.sh_val - h.nz0;
-      const int jb = stg ? s_rp[lr] : __ldg(sa.rowptr + row);
-      const int je = stg ? s_rp[lr + 1] : __ldg(sa.rowptr + row + 1);
-      double acc[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = 0.0;
-      double dd = 0.0, rdd = __longlong_as_double(0x7FF0000000000000ll);
-      for (int j = jb; j < je; j += U) {
-        int cc[U];
-        double aa[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int jj = j + u < je ? j + u : je - 1;
-          if (PACKED) {
-            const uint32_t w = (uint32_t)(stg ? s_col[jj] : __ldg(sa.col + jj));
-            cc[u] = row + ((int32_t)w >> 8);
-            aa[u] = s_dict[w & 255u];
-            if (EPI == EPI_JACOBI && (w >> 8) == 0u && j + u < je) dd = aa[u], rdd = s_dict[PACK_DICT + (w & 255u)];
-          } else {
-            cc[u] = stg ? s_col[jj] : __ldg(sa.col + jj);
-            aa[u] = stg ? s_val[jj] : __ldg(sa.val + jj);
-          }
-        }
-        double xv[U][V];
-#pragma unroll
-        for (int u = 0; u < U; ++u) VecIO<V>::load(sa.X + (int64_t)cc[u] * K + voff, xv[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (j + u < je) {
-#pragma unroll
-            for (int q = 0; q < V; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
-          }
-        }
-      }
-      const int64_t base = (int64_t)row * K + voff;
-      const double* s_e0 = reinterpret_cast<const double*>(st + L::OFF_E0) + lr * K + voff;
-      const double* s_e1 = reinterpret_cast<const double*>(st + L::OFF_E1) + lr * K + voff;
-      double out[V];
-      if (EPI == EPI_PLAIN) {
-#pragma unroll
-        for (int q = 0; q < V; ++q) out[q] = acc[q];
-      } else if (EPI == EPI_RESID || EPI == EPI_ADD) {
-        const double* g = (EPI == EPI_RESID ? ea.b : ea.xold) + base;
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-          const double e = stg ? s_e0[q] : __ldg(g + q);
-          out[q] = EPI == EPI_RESID ? __dsub_rn(e, acc[q]) : __dadd_rn(e, acc[q]);
-        }
-      } else {
-        bool sk;
-        if (stg) sk = (st + L::OFF_SKIP)[h.sh_skip + lr] != 0;
-        else sk = ea.skip[row] != 0;
-        if (!PACKED) {
-          dd = stg ? reinterpret_cast<const double*>(st + L::OFF_D)[lr] : ea.d[row];
-          if (ea.rd) rdd = stg ? reinterpret_cast<const double*>(st + L::OFF_RD)[lr] : ea.rd[row];
-        }
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-          double bv = 0.0;
-          if (ea.b) {
-            bv = stg ? s_e1[q] : __ldg(ea.b + base + q);
-            if (ea.b_scale) bv = __dmul_rn(ea.b_scale[voff + q], bv);
-          }
-          const double xo = stg ? s_e0[q] : __ldg(ea.xold + base + q);
-          const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc[q]));
-          const double upd = sk ? 0.0 : ((PACKED || ea.rd) ? div_rn_recip(num, dd, rdd) : __ddiv_rn(num, dd));
-          out[q] = __dadd_rn(xo, upd);
-          pk[q] = fmax(pk[q], fabs(out[q]));
-        }
-      }
-      VecIO<V>::store(sa.Y + base, out);
-    }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with the stage
-  }
-  }
-  if (want_peak) {
-    constexpr bool POW2 = (G & (G - 1)) == 0;
-    if (threadIdx.x < TILE_THREADS) {
-      if constexpr (POW2) {
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-          double m = pk[q];
-          for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-          pk[q] = m;
-        }
-      }
-      if (lr < RB && (!POW2 || (threadIdx.x & 31) < G)) {
-#pragma unroll
-        for (int q = 0; q < V; ++q)
-          atomicMax(&s_peak[sub * V + q], (unsigned long long)__double_as_longlong(pk[q]));
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
-  }
-}
-
-static int stream_mode() {  // BAMG_STREAM=0 disables the bulk-staged kernels (read per call: tests flip it)
-  const char* e = getenv("BAMG_STREAM");
-  return (e && e[0] == '0') ? 0 : 1;
-}
-
-template <int EPI, int K, int G, int U, bool PACKED, int CAPF, int STAGES, int MINB>
-static int launch_stream_one(bamg_ctx* ctx, double bytes, const bamg_csr* A, const double* X, double* Y,
-                             const EpiArgs& ea) {
-  using L = StreamLayout<K, G, PACKED, EPI, CAPF>;
-  auto kern = csr_stream_kernel<EPI, K, G, U, PACKED, CAPF, STAGES, MINB>;
-  const size_t smem = (size_t)L::STAGE_BYTES * STAGES;
-  BAMG_TRY(smem_optin(ctx, (const void*)kern, smem));
-  StreamArgs sa{};
-  sa.nrows = A->nrows;
-  sa.ntiles = (A->nrows + L::RB - 1) / L::RB;
-  sa.nnz = A->nnz;
-  sa.rowptr = A->rowptr;
-  sa.col = PACKED ? reinterpret_cast<const int32_t*>(A->packed) : A->col;
-  sa.val = A->val;
-  sa.dict = A->dict;
-  sa.X = X;
-  sa.Y = Y;
-  sa.xrows = A->nrows;
-  const int g = sa.ntiles < ctx->num_sms * MINB ? sa.ntiles : ctx->num_sms * MINB;
-  BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes, kern, g, STREAM_THREADS, smem, sa, ea);
-  return 0;
-}
-
-// returns 1 when the call is not covered
-template <int EPI>
-static int launch_stream(bamg_ctx* ctx, int k, double bytes, const bamg_csr* A, const double* X, double* Y,
-                         const EpiArgs& ea) {
-  if (!stream_mode()) return 1;
-  if (A->nrows < 512) return 1;  // a handful of tiles: nothing to pipeline
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!al16(A->rowptr) || !al16(A->col) || !al16(A->val) || !al16(X) || !al16(Y) || !al16(ea.b) || !al16(ea.xold) ||
-      !al16(ea.d) || !al16(ea.rd) || !al16(ea.skip))
-    return 1;
-  const bool packed = k == 1 && A->packed && A->dict && packed_enabled() && al16(A->packed) &&
-                      (EPI != EPI_JACOBI || (!ea.b_scale));
-  if (k == 1) {
-    if (EPI == EPI_ADD || !packed) return 1;
-    return launch_stream_one<EPI, 1, 1, 8, true, 8, 3, 5>(ctx, packed_bytes(EPI, A, ea), A, X, Y, ea);
-  }
-  if (k == 16) {
-    const char* e = getenv("BAMG_STREAM_U16");  // development: gather depth / occupancy variants
-    const int v = e ? atoi(e) : 6;
-    if (v == 4) return launch_stream_one<EPI, 16, 8, 4, false, 10, 3, 5>(ctx, bytes, A, X, Y, ea);
-    if (v == 8) return launch_stream_one<EPI, 16, 8, 8, false, 10, 3, 3>(ctx, bytes, A, X, Y, ea);
-    if (v == 64) return launch_stream_one<EPI, 16, 8, 6, false, 10, 4, 4>(ctx, bytes, A, X, Y, ea);
-    return launch_stream_one<EPI, 16, 8, 6, false, 10, 3, 4>(ctx, bytes, A, X, Y, ea);
-  }
-  if (k == 12) return launch_stream_one<EPI, 12, 6, 4, false, 10, 3, 4>(ctx, bytes, A, X, Y, ea);
-  if (k == 8) return launch_stream_one<EPI, 8, 4, 6, false, 10, 3, 4>(ctx, bytes, A, X, Y, ea);
-  return 1;
 }
 
 // Internal entry points (used by the setup / solver translation units).

@@ -172,6 +172,12 @@ def gmres(B, b, x_init, cfg: GmresConfig, precond: VCycleOperator | None = None,
 
     `to_host=False` leaves the iterate on the device only (report.x_device)."""
     A = as_device(B)
+    if precond is not None:
+        # the hierarchy's finest operator is B itself, possibly with the packed
+        # copy the setup attached: the Arnoldi SpMVs stream that
+        f = precond.hierarchy.finest.dB
+        if f.packed is not None and f.nnz == A.nnz and f.val.data_ptr() == A.val.data_ptr():
+            A = f
     n = A.shape[0]
     bv = _vec(b, n)
     x0 = _vec(x_init, n)

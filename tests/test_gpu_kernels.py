@@ -428,48 +428,3 @@ def test_pack_operator_declines_general_values(eng):
     assert dA.packed is None and not dA.desc().packed
     x = rng.standard_normal(2000)
     assert np.array_equal(engine.spmm(dA, dvec(x)).cpu().numpy(), A @ x)
-
-
-@pytest.mark.parametrize("k", [8, 12, 16])
-def test_stream_kernels_match_row_kernels_bitexact(eng, k, monkeypatch):
-    """The bulk-staged (cp.async.bulk + mbarrier) CSR kernels reproduce the row
-    kernels bit for bit: SpMM, prolong-add, and Jacobi with / without a scaled
-    right-hand side and the per-column peak, on a square operator with ragged
-    rows (empty rows, a tile over the stage capacity, a partial last tile)."""
-    from scipy import sparse as sp
-    from paper_1402_4005_b200 import engine
-    rng = np.random.default_rng(100 + k)
-    n = 5003
-    A = sp.random_array((n, n), density=0.0015, random_state=rng).tolil()
-    A[100:140, :600] = rng.standard_normal((40, 600))      # a tile far over the stage capacity
-    A[300:310, :] = 0.0                                      # empty rows
-    A = orc.canon(sp.csr_array(A) + sp.diags_array(1.0 + rng.random(n)))
-    X = rng.standard_normal((n, k))
-    Bv = rng.standard_normal((n, k))
-    scale = rng.standard_normal(k)
-    dA = up(eng, A)
-    d = engine.diag(dA)
-    skip = engine.degenerate_rows(dA, d)
-    dX, dB, ds = dvec(X), dvec(Bv), dvec(scale)
-
-    def run():
-        out = {"spmm": engine.spmm(dA, dX)}
-        y = torch.empty_like(dX)
-        eng[0].call("bamg_addmv", dA.ref(), eng[0].ptr(dX[:, 0].contiguous()), eng[0].ptr(dB[:, 0].contiguous()),
-                    eng[0].ptr(y[:, 0].contiguous()))
-        out["jac"] = engine.jacobi(dA, d, skip, dX)
-        out["jac_b"] = engine.jacobi(dA, d, skip, dX, b=dB)
-        peak = torch.zeros(k, dtype=torch.float64, device="cuda")
-        out["jac_bs"] = engine.jacobi(dA, d, skip, dX, b=dB, b_scale=ds, peak=peak)
-        out["peak"] = peak
-        return out
-
-    monkeypatch.setenv("BAMG_STREAM", "0")
-    monkeypatch.setenv("BAMG_ROWS_PIPE", "0")
-    want = run()
-    monkeypatch.setenv("BAMG_STREAM", "1")
-    got = run()
-    for key in want:
-        assert torch.equal(got[key], want[key]), key
-    ref = np.stack([A @ X[:, c] for c in range(k)], axis=1)
-    assert np.array_equal(got["spmm"].cpu().numpy(), ref)
