@@ -585,10 +585,17 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane
 // vectors l, l + 32 over all of the warp's rows.
 template <int MAXM, int MODE>
 __global__ void __launch_bounds__(CGS_THREADS)
-cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c, double* __restrict__ w,
-                int64_t n, double* __restrict__ part, const double* __restrict__ code) {
+cgs_dots_kernel(const double* const* __restrict__ Vp, int m_all, const double* __restrict__ c, double* __restrict__ w,
+                int64_t n, double* __restrict__ part, const double* __restrict__ code, int nblk) {
   BAMG_PDL_PROLOGUE();
   if (MODE == 1 && !cgs_gate(code, 1u << 0)) return;
+  // more than nblk CTAs (pass A only): CTAs [y nblk, (y + 1) nblk) take the basis vectors
+  // [y MAXM, (y + 1) MAXM) -- two <32> groups keep 116 registers (4 CTAs per SM) where one <64>
+  // pass needs 168 (2-3 per SM)
+  const int by = blockIdx.x / nblk, bx = blockIdx.x - by * nblk;
+  const int stride = m_all + 1, slot0 = by * MAXM;
+  Vp += slot0;
+  const int m = min(MAXM, m_all - slot0);
   static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
   constexpr int NB = MAXM / 32;
   __shared__ const double* sp[MAXM];
@@ -598,8 +605,8 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __res
   if (MODE == 1)
     for (int g = threadIdx.x; g < MAXM; g += blockDim.x) sc[g] = g < m ? c[g] : 0.0;
   cgs_load_ptrs<MAXM>(Vp, m, sp);
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  const int64_t per = (n + nblk - 1) / nblk;
+  const int64_t r0 = (int64_t)bx * per, r1 = min(r0 + per, n);
   double dot[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) dot[q] = 0.0;
@@ -635,12 +642,12 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m, const double* __res
   wn2 = warp_sum(wn2);
   if (lane == 0) acc[wid][MAXM] = wn2;
   __syncthreads();
-  const int nslots = m + 1;
+  const int nslots = m + (by == 0 ? 1 : 0);  // |w|^2 (slot m_all) from the first group only
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
     const int slot = q == m ? MAXM : q;
     double t = 0.0;
     for (int ww = 0; ww < CGS_WARPS; ++ww) t += acc[ww][slot];
-    part[(int64_t)blockIdx.x * (m + 1) + q] = t;
+    part[(int64_t)bx * stride + (q == m ? m_all : slot0 + q)] = t;
   }
 }
 
@@ -909,6 +916,100 @@ cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __r
   }
 }
 
+// The update pass for 32 < m <= 64 with the row's vectors split over a warp
+// pair: warp half h of a pair keeps vectors [32 h, 32 h + 32) of 32 rows in
+// registers (118 registers, 4 CTAs per SM, against 190 and 2 for whole rows in
+// one thread); the halves exchange their partial projections through shared
+// memory (two 64-thread named barriers per 32 rows), half 0 forms ww, v_new and
+// x, and both take their vectors' dots with ww from the registers they hold.
+__global__ void __launch_bounds__(CGS_THREADS)
+cgs_update_pair_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
+                       const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
+                       const double* __restrict__ e, const double* __restrict__ state,
+                       const double* __restrict__ flag, int64_t n, double* __restrict__ vnew,
+                       double* __restrict__ x, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  constexpr int MAXM = 64, PAIRS = CGS_WARPS / 2;
+  __shared__ const double* sp[MAXM];
+  __shared__ double sc[MAXM], sy[MAXM];
+  __shared__ double acc[PAIRS][MAXM + 2];
+  __shared__ double xt[PAIRS][32], xu[PAIRS][32], xw[PAIRS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pair = wid >> 1, half = wid & 1;
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
+    sc[g] = g < m ? c[g] : 0.0;
+    sy[g] = g < m ? y[g] : 0.0;
+  }
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const bool unsafe = flag[0] == 2.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  const int g0 = half * 32;
+  double dot = 0.0, wn2 = 0.0, xn2 = 0.0;
+  for (int64_t base = r0 + pair * 32; base < r1; base += 32 * PAIRS) {
+    const int64_t i = base + lane;
+    const bool ok = i < r1;
+    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
+    double v[32];
+#pragma unroll
+    for (int g = 0; g < 32; ++g) v[g] = __ldcs(sp[g0 + g] + ic);
+    double wi = 0.0, x0i = 0.0, ei = 0.0;
+    if (half == 0) wi = w[ic], x0i = x0[ic], ei = e[ic];
+    double t = 0.0, u = 0.0;
+#pragma unroll
+    for (int g = 0; g < 32; ++g) {
+      t = fma(sc[g0 + g], v[g], t);
+      u = fma(sy[g0 + g], v[g], u);
+    }
+    if (half == 1) xt[pair][lane] = t, xu[pair][lane] = u;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    double ww = 0.0;
+    if (half == 0) {
+      t += xt[pair][lane];
+      u += xu[pair][lane];
+      ww = wi - t;
+      if (ok) {
+        if (unsafe) {
+          vnew[i] = ww;
+        } else {
+          if (!happy) vnew[i] = ww * inv;
+          const double xi = x0i + (ei + u);
+          x[i] = xi;
+          xn2 = fma(xi, xi, xn2);
+        }
+      } else {
+        ww = 0.0;
+      }
+      wn2 = fma(ww, ww, wn2);
+      xw[pair][lane] = ww;
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    if (half == 1) ww = xw[pair][lane];
+    if (g0 < m) {
+      double pr[32];
+#pragma unroll
+      for (int g = 0; g < 32; ++g) pr[g] = v[g] * ww;
+      dot += warp_transpose_sum32(pr, lane);
+    }
+  }
+  acc[pair][g0 + lane] = dot;
+  if (half == 0) {
+    wn2 = warp_sum(wn2);
+    xn2 = warp_sum(xn2);
+    if (lane == 0) acc[pair][MAXM] = wn2, acc[pair][MAXM + 1] = xn2;
+  }
+  __syncthreads();
+  const int nslots = m + 2;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
+    const int slot = q >= m ? MAXM + (q - m) : q;
+    double t = 0.0;
+    for (int p = 0; p < PAIRS; ++p) t += acc[p][slot];
+    part[(int64_t)blockIdx.x * (m + 2) + q] = t;
+  }
+}
+
 // (flag 2 only) the explicit norm |w - V c|^2 = gs[m] for the Givens step
 __global__ void cgs_gram_fix_norm_kernel(const double* __restrict__ flag, const double* __restrict__ gs, int m,
                                          double* __restrict__ nrm2) {
@@ -1089,6 +1190,11 @@ static bool cgs_gram_enabled() {
   return !(e && e[0] == '0');
 }
 
+static bool cgs_pair_enabled() {  // BAMG_CGS_PAIR=0: whole rows per thread for m > 32 (development)
+  static const bool on = !(getenv("BAMG_CGS_PAIR") && getenv("BAMG_CGS_PAIR")[0] == '0');
+  return on;
+}
+
 static bool cgs_fast_enabled() {
   static const bool on = !(getenv("BAMG_CGS_SLOW") && getenv("BAMG_CGS_SLOW")[0] == '1');
   return on;
@@ -1266,12 +1372,15 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
         // two passes over V (see cgs_gram_coef_kernel): dots, then the update with x, |x| and G's new row
         const int mj = j + 1;
         if (j == 0) BAMG_LAUNCH(ctx, cgs_gram_init_kernel, 1, 256, 0, gram);
-        auto dots = mj <= 32 ? cgs_dots_kernel<32, 0> : cgs_dots_kernel<64, 0>;
-        auto upd = mj <= 32 ? cgs_update_kernel<32> : cgs_update_kernel<64>;
-        const int cb = std::min(cgs_grid(ctx, (const void*)dots, n), cgs_grid(ctx, (const void*)upd, n));
-        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 1) * n, dots, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)nullptr, w, n, part, (const double*)nullptr);
-        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
+        auto dots = cgs_dots_kernel<32, 0>;
+        auto upd = mj <= 32 ? cgs_update_kernel<32> : (cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64>);
+        // pass A in vector groups of 32 (one wave in total); the update pass keeps whole rows
+        const int groups = (mj + 31) / 32;
+        const int cbd = std::max(1, cgs_grid(ctx, (const void*)dots, n) / groups);
+        const int cb = cgs_grid(ctx, (const void*)upd, n);
+        BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + groups) * n, dots, cbd * groups, CGS_THREADS, 0,
+                        (const double* const*)W.dVp, mj, (const double*)nullptr, w, n, part, (const double*)nullptr, cbd);
+        BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cbd,
                     mj + 1, mj + 1, hv, (const double*)nullptr, 0u);  // h1 and |w|^2
         BAMG_LAUNCH(ctx, cgs_gram_coef_kernel, 1, CGS_MAXM, 0, mj, (const double*)gram, hv, h2, scal + 3, flag);
         BAMG_LAUNCH(ctx, givens_kernel, 1, 256, sizeof(double) * (j + 2), j, m_cap, hv, scal + 3, beta, R, g, cs, sn,
@@ -1316,13 +1425,13 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
         // (n, kernel, device), so the partial-sum tree is reproducible
         const int cb = std::min(cgs_grid(ctx, (const void*)upd, n), cgs_grid(ctx, (const void*)fin, n));
         BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (mj + 1) * n, dots, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)nullptr, w, n, part, (const double*)nullptr);
+                        (const double*)nullptr, w, n, part, (const double*)nullptr, cb);
         BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
                     mj + 1, mj + 1, hv, (const double*)nullptr, 0u);  // h and |w|^2
         BAMG_LAUNCH(ctx, cgs_dgks_kernel, 1, 256, 0, mj, (const double*)hv, scal + 3, flag, h2);
         // second projection (code 0 only; its bytes are booked after the step's read-back)
         BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 0.0, upd, cb, CGS_THREADS, 0, (const double* const*)W.dVp, mj,
-                        (const double*)hv, w, n, part, (const double*)flag);
+                        (const double*)hv, w, n, part, (const double*)flag, cb);
         BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(mj + 1) * 32, 256), 256, 0, (const double*)part, cb,
                     mj + 1, mj + 1, h2, (const double*)flag, 1u);
         BAMG_LAUNCH(ctx, cgs_pythag_kernel, 1, 256, 0, mj, (const double*)h2, hv, scal + 3, flag);
