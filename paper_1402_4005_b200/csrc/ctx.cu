@@ -353,18 +353,25 @@ colreduce_wide_kernel(const double* __restrict__ X, const double* __restrict__ Y
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ out,
                       int take_sqrt) {
   BAMG_PDL_PROLOGUE();
-  constexpr int PAIRS = KK / 2;
+  // KK == 1: one vector read as double2 (both halves belong to the column; an odd tail element
+  // is added by the CTA that owns it)
+  constexpr int PAIRS = KK == 1 ? 1 : KK / 2;
   static_assert(RED_THREADS % PAIRS == 0, "a thread must keep its column pair");
   __shared__ double sh[RED_THREADS][2];
   __shared__ bool last;
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  if (KK == 1) per = (per + 1) & ~(int64_t)1;  // even chunks keep the double2 loads aligned
+  const int64_t r0 = min((int64_t)blockIdx.x * per, n);
   const int64_t r1 = r0 + per < n ? r0 + per : n;
   const double2* X2 = reinterpret_cast<const double2*>(X);
   const double2* Y2 = reinterpret_cast<const double2*>(Y);
-  const int64_t u1 = r1 * PAIRS;
+  const int64_t u1 = KK == 1 ? r1 / 2 : r1 * PAIRS;
   double a0 = 0.0, a1 = 0.0;
-  int64_t u = r0 * PAIRS + threadIdx.x;
+  int64_t u = (KK == 1 ? r0 / 2 : r0 * PAIRS) + threadIdx.x;
+  if (KK == 1 && (r1 & 1) && r1 == n && r0 < r1 && threadIdx.x == 0) {
+    const double xl = X[n - 1];
+    a0 = xl * (kind == 0 ? xl : Y[n - 1]);
+  }
   for (; u + (int64_t)(UR - 1) * RED_THREADS < u1; u += (int64_t)UR * RED_THREADS) {
     double2 xv[UR], yv[UR];
 #pragma unroll
@@ -387,7 +394,13 @@ colreduce_wide_kernel(const double* __restrict__ X, const double* __restrict__ Y
   sh[threadIdx.x][0] = a0;
   sh[threadIdx.x][1] = a1;
   __syncthreads();
-  if (threadIdx.x < KK) {
+  if (KK == 1) {
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int t = 0; t < RED_THREADS; ++t) v += sh[t][0] + sh[t][1];
+      partial[blockIdx.x] = v;
+    }
+  } else if (threadIdx.x < KK) {
     const int c = threadIdx.x;
     // the chunk starts on a row boundary: thread t owns columns 2 (t % PAIRS), + 1
     double v = 0.0;
@@ -420,6 +433,9 @@ int colreduce(bamg_ctx* ctx, const double* X, const double* Y, int64_t n, int k,
   const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0;
   if (k == 16 && al16)
     BAMG_LAUNCH(ctx, (colreduce_wide_kernel<16, 8>), g, RED_THREADS, 0, X, Y, n, kind, partial, ctx->counters + 0,
+                out_dev, take_sqrt);
+  else if (k == 1 && al16)
+    BAMG_LAUNCH(ctx, (colreduce_wide_kernel<1, 8>), g, RED_THREADS, 0, X, Y, n, kind, partial, ctx->counters + 0,
                 out_dev, take_sqrt);
   else if (k == 8 && al16)
     BAMG_LAUNCH(ctx, (colreduce_wide_kernel<8, 8>), g, RED_THREADS, 0, X, Y, n, kind, partial, ctx->counters + 0,

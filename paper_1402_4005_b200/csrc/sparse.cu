@@ -609,8 +609,11 @@ struct MassRows {
 
 // MASS = false: identity masses (the finest levels) -- without the mass rows'
 // code the kernel fits 40 registers, 6 CTAs per SM (62 registers otherwise)
+#ifndef BAMG_RQ_MASS_MINB
+#define BAMG_RQ_MASS_MINB 4
+#endif
 template <int K, int G, int U, bool MASS>
-__global__ void __launch_bounds__(TILE_THREADS, MASS ? 1 : 6)
+__global__ void __launch_bounds__(TILE_THREADS, MASS ? BAMG_RQ_MASS_MINB : 6)
 rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                       const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
@@ -744,7 +747,9 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   constexpr int RQ_BLOCKS = 6 * 148;
   const int rb_rows = TILE_THREADS / 8;  // rows per tile at the widest G
   int nblk = (A->nrows + 4 * rb_rows - 1) / (4 * rb_rows);
-  nblk = nblk < 1 ? 1 : (nblk > RQ_BLOCKS ? RQ_BLOCKS : nblk);
+  // the mass variant holds BAMG_RQ_MASS_MINB CTAs per SM (76 registers): its own one-wave cap
+  const int cap = (M || N) ? BAMG_RQ_MASS_MINB * 148 : RQ_BLOCKS;
+  nblk = nblk < 1 ? 1 : (nblk > cap ? cap : nblk);
   double* partial;
   BAMG_TRY(arena_get(ctx, (size_t)RQ_BLOCKS * 3 * k, &partial));
   const double n = A->nrows;
@@ -1222,6 +1227,8 @@ __device__ double selftest_operand(unsigned long long h, unsigned long long h2, 
     }
   }
   const unsigned long long sign = (h >> 63) << 63;
+  // signed zeros as numerators (every sixteenth x of modes 2 and 3): the zero fast path of div_rn_recip
+  if (!is_d && mode >= 2 && ((h2 >> 50) % 16ull) == 0ull) return __longlong_as_double((long long)sign);
   if (e < -1022) {  // subnormal / zero
     int sh = -1022 - e;
     unsigned long long m = sh >= 53 ? 0ull : ((mant | (1ull << 52)) >> sh);
