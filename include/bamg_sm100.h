@@ -388,6 +388,16 @@ int bamg_dense_gemv_rows(bamg_ctx* ctx, const double* Z, int n, const double* b,
 int bamg_mdot(bamg_ctx* ctx, const double* const* Vp, int m, const double* w, int64_t n, double* out);
 int bamg_mupdate(bamg_ctx* ctx, const double* const* Vp, int m, const double* c, double* w, int64_t n,
                  double* nrm2);
+/* The two fused basis passes of bamg_gmres' Arnoldi step (two-pass CGS2 through the
+ * Gram matrix G = V^T V, solver.py:183-196 replaced) on the caller's row block, m <= 64:
+ *   bamg_cgs_dots:   out[0..m) = V^T w, out[m] = |w|^2
+ *   bamg_cgs_update: ww = w - V c (c = 2 h1 - G h1), vnew = ww * inv_norm unless happy,
+ *                    x = x0 + e + V y, out = [V^T ww (m), |ww|^2, |x|^2]
+ * The caller all-reduces `out` over its ranks between the passes (one all-reduce each). */
+int bamg_cgs_dots(bamg_ctx* ctx, const double* const* Vp, int m, const double* w, int64_t n, double* out);
+int bamg_cgs_update(bamg_ctx* ctx, const double* const* Vp, int m, const double* c, const double* y,
+                    const double* w, const double* x0, const double* e, double inv_norm, int happy,
+                    int64_t n, double* vnew, double* x, double* out);
 int bamg_combine(bamg_ctx* ctx, const double* const* Vp, int m, const double* y, const double* base,
                  const double* add, int64_t n, double* out);
 

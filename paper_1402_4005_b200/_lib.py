@@ -131,6 +131,8 @@ _SIGS = {
     "bamg_mdot": [P, P, C.c_int, P, I64, P],
     "bamg_mupdate": [P, P, C.c_int, P, P, I64, P],
     "bamg_combine": [P, P, C.c_int, P, P, P, I64, P],
+    "bamg_cgs_dots": [P, P, C.c_int, P, I64, P],
+    "bamg_cgs_update": [P, P, C.c_int, P, P, P, P, P, F64, C.c_int, I64, P, P, P],
 }
 _RESTYPES = {"bamg_last_error": C.c_char_p, "bamg_launch_count": C.c_int64, "bamg_sync_count": C.c_int64,
              "bamg_trace_position": C.c_int64}

@@ -165,15 +165,40 @@ static int hier_prepare(bamg_hier* h) {
 
 // x = 0 + (omega * (b - 0)) / d  on unskipped rows (the first sweep from the
 // zero guess, bit-identical to relax.py:78-83 with x = 0).
+template <bool VEC>
 __global__ void jacobi_from_zero_kernel(int n, const double* __restrict__ b, const double* __restrict__ d,
                                         const uint8_t* __restrict__ skip, double omega,
                                         double* __restrict__ x, const double* __restrict__ rd) {
   BAMG_PDL_PROLOGUE();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double num = __dmul_rn(omega, b[i]);
-  double upd = skip[i] ? 0.0 : (rd ? div_rn_recip(num, d[i], rd[i]) : __ddiv_rn(num, d[i]));
-  x[i] = __dadd_rn(0.0, upd);
+  // two rows per thread (16-byte loads); the plain IEEE division needs no 1/d stream here --
+  // a pure streaming kernel has the issue slots for it (25 instead of 33 bytes per row)
+  (void)rd;
+  const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (!VEC) {  // misaligned caller buffers: scalar loads, same arithmetic
+    for (int r = i; r < min(i + 2, n); ++r) x[r] = __dadd_rn(0.0, skip[r] ? 0.0 : __ddiv_rn(__dmul_rn(omega, b[r]), d[r]));
+    return;
+  }
+  if (i + 1 < n) {
+    const double2 bv = *reinterpret_cast<const double2*>(b + i);
+    const double2 dv = *reinterpret_cast<const double2*>(d + i);
+    const uchar2 sk = *reinterpret_cast<const uchar2*>(skip + i);
+    double2 out;
+    out.x = __dadd_rn(0.0, sk.x ? 0.0 : __ddiv_rn(__dmul_rn(omega, bv.x), dv.x));
+    out.y = __dadd_rn(0.0, sk.y ? 0.0 : __ddiv_rn(__dmul_rn(omega, bv.y), dv.y));
+    *reinterpret_cast<double2*>(x + i) = out;
+  } else if (i < n) {
+    x[i] = __dadd_rn(0.0, skip[i] ? 0.0 : __ddiv_rn(__dmul_rn(omega, b[i]), d[i]));
+  }
+}
+
+static int jacobi_from_zero(bamg_ctx* ctx, int64_t n, const double* b, const double* d, const uint8_t* skip,
+                            double omega, double* x) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(x)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(skip) & 1) == 0;
+  const int g = grid_for((n + 1) / 2, 256);
+  if (vec) BAMG_LAUNCH(ctx, jacobi_from_zero_kernel<true>, g, 256, 0, (int)n, b, d, skip, omega, x, (const double*)nullptr);
+  else BAMG_LAUNCH(ctx, jacobi_from_zero_kernel<false>, g, 256, 0, (int)n, b, d, skip, omega, x, (const double*)nullptr);
+  return 0;
 }
 
 // y = Z b, Z row-major n x n (warp per row, coalesced).
@@ -202,7 +227,7 @@ static int vcycle_impl(bamg_ctx* ctx, bamg_hier* h, const double* b_in, double* 
     double* cur = v.x;
     double* oth = v.x2;
     if (h->nu1 > 0) {
-      BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(v.n, 256), 256, 0, v.n, bl, v.d, v.skip, om, cur, v.rd);
+      BAMG_TRY(jacobi_from_zero(ctx, v.n, bl, v.d, v.skip, om, cur));
       for (int s = 1; s < h->nu1; ++s) {
         BAMG_TRY(jacobi_dev(ctx, &v.B, v.d, v.skip, bl, nullptr, cur, oth, 1, om, nullptr, v.rd));
         std::swap(cur, oth);
@@ -1654,8 +1679,7 @@ extern "C" int bamg_addmv(bamg_ctx* ctx, const bamg_csr* A, const double* xc, co
 
 extern "C" int bamg_jacobi_zero(bamg_ctx* ctx, int64_t n, const double* b, const double* d, const uint8_t* skip,
                                 double omega, double* x) {
-  BAMG_LAUNCH(ctx, jacobi_from_zero_kernel, grid_for(n, 256), 256, 0, (int)n, b, d, skip, omega, x, (const double*)nullptr);
-  return 0;
+  return jacobi_from_zero(ctx, n, b, d, skip, omega, x);
 }
 
 extern "C" int bamg_dense_gemv_rows(bamg_ctx* ctx, const double* Z, int n, const double* b, double* y) {
@@ -1685,6 +1709,54 @@ extern "C" int bamg_mupdate(bamg_ctx* ctx, const double* const* Vp, int m, const
   } else {
     BAMG_LAUNCH(ctx, mupdate_kernel<0>, GM_BLOCKS, GM_THREADS, 0, Vp, m, c, w, n, part);
   }
+  return 0;
+}
+
+// ---- rank-local passes of the two-pass (Gram) CGS2 step for the row-partitioned solve
+// (distributed.py): the same fused kernels bamg_gmres runs, on the caller's row block, with
+// the partial sums left for the caller's all-reduce between them.
+__global__ void cgs_set_state_kernel(double* __restrict__ state, double* __restrict__ flag, double happy,
+                                     double norm, double code) {
+  BAMG_PDL_PROLOGUE();
+  state[0] = happy;
+  state[1] = norm;
+  flag[0] = code;
+}
+
+// out[0..m) = V^T w, out[m] = |w|^2 over the n local rows (m <= 64)
+extern "C" int bamg_cgs_dots(bamg_ctx* ctx, const double* const* Vp, int m, const double* w, int64_t n,
+                             double* out) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, m >= 1 && m <= CGS_MAXM, "1..64 basis vectors per fused pass");
+  double* part;
+  BAMG_TRY(arena_get(ctx, (size_t)CGS_MAX_BLOCKS * (CGS_MAXM + 2), &part));
+  auto dots = cgs_dots_kernel<32, 0>;
+  const int groups = (m + 31) / 32;
+  const int cbd = std::max(1, cgs_grid(ctx, (const void*)dots, n) / groups);
+  BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (m + groups) * n, dots, cbd * groups, CGS_THREADS, 0, Vp, m,
+                  (const double*)nullptr, const_cast<double*>(w), n, part, (const double*)nullptr, cbd);
+  BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(m + 1) * 32, 256), 256, 0, (const double*)part, cbd, m + 1,
+              m + 1, out, (const double*)nullptr, 0u);
+  return 0;
+}
+
+// ww = w - V c; vnew = ww * inv_norm (skipped when happy != 0); x = x0 + e + V y;
+// out[0..m) = V^T ww, out[m] = |ww|^2, out[m + 1] = |x|^2 over the n local rows
+extern "C" int bamg_cgs_update(bamg_ctx* ctx, const double* const* Vp, int m, const double* c, const double* y,
+                               const double* w, const double* x0, const double* e, double inv_norm, int happy,
+                               int64_t n, double* vnew, double* x, double* out) {
+  ctx->arena.reset();
+  BAMG_REQUIRE(ctx, m >= 1 && m <= CGS_MAXM, "1..64 basis vectors per fused pass");
+  double *part, *st;
+  BAMG_TRY(arena_get(ctx, (size_t)CGS_MAX_BLOCKS * (CGS_MAXM + 2), &part));
+  BAMG_TRY(arena_get(ctx, 4, &st));
+  BAMG_LAUNCH(ctx, cgs_set_state_kernel, 1, 1, 0, st, st + 2, happy ? 1.0 : 0.0, 1.0 / inv_norm, 0.0);
+  auto upd = m <= 32 ? cgs_update_kernel<32> : (cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64>);
+  const int cb = cgs_grid(ctx, (const void*)upd, n);
+  BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (m + 5) * n, upd, cb, CGS_THREADS, 0, Vp, m, c, y, w, x0, e,
+                  (const double*)st, (const double*)(st + 2), n, vnew, x, part);
+  BAMG_LAUNCH(ctx, cgs_reduce_kernel, grid_for((int64_t)(m + 2) * 32, 256), 256, 0, (const double*)part, cb, m + 2,
+              m + 2, out, (const double*)nullptr, 0u);
   return 0;
 }
 

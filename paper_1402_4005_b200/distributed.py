@@ -416,12 +416,34 @@ class DistSolver:
             return np.inf
         return np.sqrt(self._norm2(self.spmv(x))) / nx
 
+    #: basis vectors the fused passes keep in registers (csrc/solver.cu CGS_MAXM)
+    MAX_FUSED = 64
+
+    def _table(self, vecs):
+        return torch.tensor([v.data_ptr() for v in vecs], dtype=torch.int64, device=device())
+
+    def _bx_norm2_local(self, x):
+        y = self.spmv(x)
+        out = torch.empty(1, dtype=torch.float64, device=device())
+        _lib.call("bamg_col_dots", _lib.ptr(y), _lib.ptr(y), self.n_own, 1, _lib.ptr(out))
+        return out
+
     def solve(self, x0_own, restart=None, max_iters=1000, rtol=1e-8):
+        """The engine's Arnoldi step (csrc/solver.cu, two-pass CGS2 through the Gram
+        matrix) on this rank's rows: pass A (V^T w, |w|^2) -> ONE all-reduce -> the
+        coefficients c = 2 h1 - G h1, the new vector's norm and the Givens update on the
+        host (the scalars the stopping test reads anyway) -> pass B (v_new, x, V^T v_new,
+        |x|^2) and |Bx|^2 -> ONE all-reduce.  Two reads of the local basis block, two
+        all-reduces and two host reads per iteration (the first version took five
+        all-reduces and four basis sweeps).  Cycles longer than 64 vectors are restarted
+        at 64 (the fused passes hold the row's basis values in registers)."""
+        from scipy.linalg import solve_triangular
         x0 = x0_own.clone()
         rhs = self.vc.apply(_lincomb([self.spmv(x0)], [-1.0]))  # C(b - B x0), b = 0
         hist = [self.metric(x0)]
         if hist[0] <= rtol:
             return 0, hist, True, x0
+        dev = device()
         e = torch.zeros_like(x0)
         x = x0.clone()
         its, done = 0, False
@@ -430,28 +452,47 @@ class DistSolver:
             beta = np.sqrt(self._norm2(r))
             if beta == 0.0:
                 break
-            m = min(restart or max_iters, max_iters - its)
+            m = min(restart or max_iters, max_iters - its, self.MAX_FUSED)
             V = [_lincomb([r], [1.0 / beta])]
+            G = np.zeros((m + 1, m + 1))
+            G[0, 0] = 1.0
             R = np.zeros((m, m))
             g = np.zeros(m + 1)
             g[0] = beta
             cs, sn = np.zeros(m), np.zeros(m)
             used, happy = 0, False
+            e_try = e
             for j in range(m):
+                mj = j + 1
                 w = self.op(V[j])
-                table, h1 = self._dots(V, w)
-                nrm = torch.empty(1, dtype=torch.float64, device=device())
-                _lib.call("bamg_mupdate", _lib.ptr(table), len(V), _lib.ptr(h1), _lib.ptr(w), self.n_own, None)
-                _, h2 = self._dots(V, w)
-                _lib.call("bamg_mupdate", _lib.ptr(table), len(V), _lib.ptr(h2), _lib.ptr(w), self.n_own,
-                          _lib.ptr(nrm))
-                self.comm.allreduce_(nrm)
+                table = self._table(V)
+                out1 = torch.empty(mj + 1, dtype=torch.float64, device=dev)
+                _lib.call("bamg_cgs_dots", _lib.ptr(table), mj, _lib.ptr(w), self.n_own, _lib.ptr(out1))
+                self.comm.allreduce_(out1)
+                o1 = out1.cpu().numpy()
+                h1, wn = o1[:mj], float(o1[mj])
+                Gm = G[:mj, :mj]
+                c = h1 + (h1 - Gm @ h1)
+                s1, s2 = float(c @ h1), float(c @ (Gm @ c))
+                eta2 = (wn - s1) - (s1 - s2)
+                explicit = not (eta2 >= 1e-6 * wn) or not (wn > 0.0)
+                cd = torch.from_numpy(np.ascontiguousarray(c)).to(dev)
+                vnew = torch.empty_like(w)
+                xnew = torch.empty_like(w)
+                out2 = torch.empty(mj + 3, dtype=torch.float64, device=dev)
+                yd = torch.zeros(mj, dtype=torch.float64, device=dev)
+                if explicit:
+                    # the norm formula cancelled: w - V c unscaled, its norm from the pass itself
+                    _lib.call("bamg_cgs_update", _lib.ptr(table), mj, _lib.ptr(cd), _lib.ptr(yd), _lib.ptr(w),
+                              _lib.ptr(x0), _lib.ptr(e), 1.0, 0, self.n_own, _lib.ptr(vnew), _lib.ptr(xnew),
+                              _lib.ptr(out2))
+                    part = out2[: mj + 2].clone()
+                    self.comm.allreduce_(part)
+                    eta2 = float(part[mj].item())
                 h = np.empty(j + 2)
-                h[: j + 1] = (h1 + h2).cpu().numpy()
-                h[j + 1] = np.sqrt(float(nrm.item()))
-                happy = h[j + 1] <= 1e-14 * beta
-                if not happy:
-                    V.append(_lincomb([w], [1.0 / h[j + 1]]))
+                h[:mj] = c
+                h[mj] = np.sqrt(max(eta2, 0.0))
+                happy = h[mj] <= 1e-14 * beta
                 for i in range(j):
                     t = cs[i] * h[i] + sn[i] * h[i + 1]
                     h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1]
@@ -463,25 +504,49 @@ class DistSolver:
                 g[j + 1] = -sn[j] * g[j]
                 g[j] = cs[j] * g[j]
                 its += 1
-                used = j + 1
-                from scipy.linalg import solve_triangular
+                used = mj
                 y = solve_triangular(R[:used, :used], g[:used], lower=False)
-                yd = torch.from_numpy(y).to(device())
-                tab = torch.tensor([v.data_ptr() for v in V[:used]], dtype=torch.int64, device=device())
-                e_try = torch.empty_like(e)
-                _lib.call("bamg_combine", _lib.ptr(tab), used, _lib.ptr(yd), None, _lib.ptr(e), self.n_own,
-                          _lib.ptr(e_try))
-                x = _lincomb([e_try], [1.0], base=x0)
-                hist.append(self.metric(x))
+                yd = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
+                eta = float(np.sqrt(max(eta2, 0.0)))
+                inv = 1.0 / eta if eta > 0.0 else 1.0
+                if explicit:
+                    # scale the unscaled w - V c kept above; x through the same pass with c = 0
+                    if not happy:
+                        vnew = _lincomb([vnew], [inv])
+                    zero_c = torch.zeros(mj, dtype=torch.float64, device=dev)
+                    scratch = torch.empty_like(w)
+                    outx = torch.empty(mj + 3, dtype=torch.float64, device=dev)
+                    _lib.call("bamg_cgs_update", _lib.ptr(table), mj, _lib.ptr(zero_c), _lib.ptr(yd), _lib.ptr(w),
+                              _lib.ptr(x0), _lib.ptr(e), 1.0, 1, self.n_own, _lib.ptr(scratch), _lib.ptr(xnew),
+                              _lib.ptr(outx))
+                    out2[mj + 1] = outx[mj + 1]
+                else:
+                    _lib.call("bamg_cgs_update", _lib.ptr(table), mj, _lib.ptr(cd), _lib.ptr(yd), _lib.ptr(w),
+                              _lib.ptr(x0), _lib.ptr(e), inv, int(happy), self.n_own, _lib.ptr(vnew),
+                              _lib.ptr(xnew), _lib.ptr(out2))
+                x = xnew
+                out2[mj + 2 : mj + 3] = self._bx_norm2_local(x)
+                self.comm.allreduce_(out2)
+                o2 = out2.cpu().numpy()
+                if not happy:
+                    V.append(vnew)
+                    G[:mj, mj] = G[mj, :mj] = o2[:mj] * inv
+                    G[mj, mj] = o2[mj] * inv * inv
+                nx = np.sqrt(o2[mj + 1])
+                hist.append(np.inf if nx == 0.0 else float(np.sqrt(o2[mj + 2]) / nx))
+                e_try = None  # formed on demand: e + V y
                 if hist[-1] <= rtol:
                     done = True
                 if done or happy or its >= max_iters:
                     done = done or happy
-                    e = e_try
                     break
-            else:
-                e = e_try
-                x = _lincomb([e], [1.0], base=x0)
+            # e <- e + V y (end of the cycle: converged, happy breakdown, restart or the cap)
+            tab = self._table(V[:used])
+            e_new = torch.empty_like(e)
+            _lib.call("bamg_combine", _lib.ptr(tab), used, _lib.ptr(yd), None, _lib.ptr(e), self.n_own,
+                      _lib.ptr(e_new))
+            e = e_new
+            x = _lincomb([e], [1.0], base=x0)
         return its, hist, done, x
 
     def gather(self, x_own):

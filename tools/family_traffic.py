@@ -1,7 +1,7 @@
 """DRAM traffic per launch of the roofline's kernel families over one bench step.
 
   BAMG_NO_GRAPHS=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      -k regex:"csr_rows_kernel|rayleigh_fused_kernel|cgs_dots_kernel|cgs_final_kernel" --csv --log-file t.csv \
+      -k regex:"csr_rows|rayleigh_fused_kernel|cgs_dots_kernel|cgs_final_kernel|cgs_update" --csv --log-file t.csv \
       python tools/steptimes.py --config cfg4 --steps 1 --prof > alg.txt
   python tools/family_traffic.py t.csv alg.txt profiles/r02_family_traffic.json cfg4
 
@@ -16,8 +16,8 @@ import re
 import sys
 from collections import defaultdict
 
-FAMILIES = {"csr_stream_spmv_spmm_jacobi": r"csr_rows_kernel|rayleigh_fused_kernel",
-            "gmres_cgs2_basis_passes": r"cgs_dots_kernel|cgs_final_kernel"}
+FAMILIES = {"csr_stream_spmv_spmm_jacobi": r"csr_rows_kernel|csr_rows_pipe_kernel|csr_rows_packed_kernel|rayleigh_fused_kernel",
+            "gmres_cgs2_basis_passes": r"cgs_dots_kernel|cgs_final_kernel|cgs_update_kernel|cgs_update_pair_kernel"}
 
 path, algp, out = sys.argv[1], sys.argv[2], sys.argv[3]
 cfgname = sys.argv[4] if len(sys.argv) > 4 else "cfg4"
