@@ -227,8 +227,14 @@ def run_ours(args, rank, world, local_rank):
         def __init__(self, its, hist, conv):
             self.iterations, self.residual_history, self.converged = its, hist, conv
 
+    setup_comm = None
+    if partitioned:
+        from paper_1402_4005_b200.distributed import Comm
+        setup_comm = Comm()
+
     def step(mark=None):
-        setup = pb.run_setup(dprob, cfg, draws=(dV, dU), B_device=dB)
+        # partitioned: the bootstrap relaxation is split by triplet slot over the ranks
+        setup = pb.run_setup(dprob, cfg, draws=(dV, dU), B_device=dB, comm=setup_comm)
         if mark is not None:
             mark.record(stream)
         if partitioned:
@@ -435,7 +441,8 @@ def run_ours(args, rank, world, local_rank):
                    "gmres_restart": restart, "rtol": RTOL, "setup_cycles": cfg.setup_cycles,
                    "levels": [lv.n for lv in levels], "gmres_iterations": iters[-1],
                    "converged": converged,
-                   "parallelism": (f"row-partitioned V-cycle+GMRES over NCCL x{world}, setup replicated"
+                   "parallelism": (f"row-partitioned V-cycle+GMRES over NCCL x{world}; setup: bootstrap relaxation "
+                                   "slot-partitioned, fits / Galerkin products / coarsest replicated"
                                    if partitioned else f"independent replicas x{world}"),
                    "l2": "working set (operators + k-vector blocks) > 126 MB L2; no flush"},
         # bytes as stored (level 0 streams its packed 4-byte entries); csr_model_bytes is SURVEY 8(d)'s

@@ -250,7 +250,7 @@ def _mass(M: DeviceCSR):
     return None if M.is_identity else M
 
 
-def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps | None = None):
+def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps | None = None, comm=None):
     """Smoothed random left/right test vectors; left slot 0 constant (bootstrap.py:180-202).
 
     The raw draws come from `rng.standard_normal((r, n))` twice (right, then
@@ -286,8 +286,11 @@ def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps 
     sig = torch.zeros(r, dtype=torch.float64, device=device())
     sm = cfg.smoother
     # nu1 homogeneous sweeps per slot, no runaway rescaling (bootstrap.py:191-194)
-    engine.smooth_block(A, ops.Bt, None, None, ops.d, ops.skip, ops.skip_t, U, V, sig,
-                        sm.sweeps_pre, sm.omega, inhomogeneous=0, smooth=2, refresh=0)
+    if _slot_partitioned(comm, n, r):
+        _smooth_slots(ops, None, None, U, V, sig, cfg, 0, 2, comm)
+    else:
+        engine.smooth_block(A, ops.Bt, None, None, ops.d, ops.skip, ops.skip_t, U, V, sig,
+                            sm.sweeps_pre, sm.omega, inhomogeneous=0, smooth=2, refresh=0)
     engine.col_fill(U, 0, 1.0 / np.sqrt(n))
     engine.normalize_cols(V)
     engine.normalize_cols(U)
@@ -339,9 +342,48 @@ def coarsest_triplets(B, M, N, r: int, Bt: DeviceCSR | None = None, warm: "Tripl
     return trips
 
 
-def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inhomogeneous: bool):
-    """bootstrap.py:284-314 in one engine call."""
+#: levels below this many rows are smoothed replicated (the all-gather would cost more than it saves)
+SLOT_PARTITION_MIN_ROWS = 1 << 14
+
+
+def _slot_partitioned(comm, n: int, r: int) -> bool:
+    return comm is not None and comm.world > 1 and r >= comm.world and n >= SLOT_PARTITION_MIN_ROWS
+
+
+def _smooth_slots(ops: _LevelOps, M, N, U, V, sig, cfg: SetupConfig, inhomogeneous: int, smooth: int, comm):
+    """The block's sweeps with the r triplet slots split over the ranks (multi-GPU setup).
+
+    The coupled sweeps of bootstrap.py:291-308 never mix slots -- slot k's u, v and sigma only
+    see each other -- so rank q relaxes slots [b_q, b_q+1) against the replicated operators
+    with no communication at all, and ONE all-gather per side returns the full n x r blocks
+    (NVLink / NVSwitch: 2 n r 8 bytes per level).  Every column goes through the same sweep
+    arithmetic as on one GPU; only the in-sweep Rayleigh quotients' partial-sum grouping depends
+    on the slice width, so the hierarchy's patterns are those of the single-GPU setup and its
+    values agree to round-off."""
+    from .distributed import slot_bounds
+    r = U.shape[1]
+    b = slot_bounds(r, comm.world)
+    s0, s1 = int(b[comm.rank]), int(b[comm.rank + 1])
+    Ul, Vl = U[:, s0:s1].contiguous(), V[:, s0:s1].contiguous()
+    sl = sig[s0:s1].clone()
     sm = cfg.smoother
+    engine.smooth_block(ops.B, ops.Bt, M, N, ops.d, ops.skip, ops.skip_t, Ul, Vl, sl,
+                        sm.sweeps_pre, sm.omega, inhomogeneous, smooth=smooth, refresh=0)
+    U.copy_(comm.all_gather_cols(Ul, b))
+    V.copy_(comm.all_gather_cols(Vl, b))
+    sig.copy_(comm.all_gather_cols(sl.reshape(1, -1), b).reshape(-1))
+
+
+def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inhomogeneous: bool, comm=None):
+    """bootstrap.py:284-314 in one engine call (slots split over the ranks of `comm`)."""
+    sm = cfg.smoother
+    if _slot_partitioned(comm, trips.n, trips.r):
+        _smooth_slots(ops, _mass(M), _mass(N), trips.dleft, trips.dright, trips.dsigmas, cfg,
+                      int(inhomogeneous), 1, comm)
+        # normalise, pin the constant left slot, refresh the sigmas: replicated on the full block
+        engine.smooth_block(ops.B, ops.Bt, _mass(M), _mass(N), ops.d, ops.skip, ops.skip_t,
+                            trips.dleft, trips.dright, trips.dsigmas, 0, sm.omega, 0, smooth=0, refresh=1)
+        return
     engine.smooth_block(ops.B, ops.Bt, _mass(M), _mass(N), ops.d, ops.skip, ops.skip_t,
                         trips.dleft, trips.dright, trips.dsigmas, sm.sweeps_pre, sm.omega,
                         int(inhomogeneous), smooth=1, refresh=1)
@@ -365,7 +407,7 @@ def _coarsest_level(depth, A, ops, Md, Nd, ranks, trips: TripletSet) -> Level:
 
 def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None, depth: int = 0,
                     first_cycle: bool = True, seed_stream: _SeedStream | None = None,
-                    ops: _LevelOps | None = None):
+                    ops: _LevelOps | None = None, comm=None):
     """One recursive setup pass (bootstrap.py:337-392); returns (levels, triplets)."""
     A = as_device(B)
     if ops is None:
@@ -399,7 +441,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         return [_coarsest_level(depth, A, ops, Md, Nd, ranks, trips)], trips
 
     with _phase("smooth", depth):
-        _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle)
+        _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=not first_cycle, comm=comm)
 
     levels = None
     for _ in range(cfg.inner_passes):
@@ -449,7 +491,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             engine.normalize_cols(cr)
         coarse = TripletSet(trips.dsigmas.clone(), cl, cr)
         sub_levels, coarse = bootstrap_cycle(Bc, Mc, Nc, coarse, cfg, cranks, depth + 1,
-                                             first_cycle, seed_stream)
+                                             first_cycle, seed_stream, comm=comm)
         # prolong: u <- Q^T u_c (= W u_c), v <- P v_c; normalise; pin; refresh; smooth
         with _phase("prolong", depth):
             U = engine.spmm(W, coarse.dleft)
@@ -458,12 +500,12 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             engine.smooth_block(ops.B, ops.Bt, _mass(Md), _mass(Nd), ops.d, ops.skip, ops.skip_t,
                                 U, V, trips.dsigmas, 0, cfg.smoother.omega, 0, smooth=0, refresh=1)
         with _phase("smooth", depth):
-            _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True)
+            _smooth_block(ops, Md, Nd, trips, cfg, inhomogeneous=True, comm=comm)
         levels = [Level(depth, A, ops.d, Md, Nd, split, P, Q, ranks, Bt=ops.Bt, W=W)] + sub_levels
     return levels, trips
 
 
-def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None = None) -> SetupResult:
+def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None = None, comm=None) -> SetupResult:
     """Full setup: initial vectors, the configured cycles, x0 (bootstrap.py:395-429).
 
     `draws=(right, left)` injects the raw (k, n) initial vectors (BASELINE's
@@ -471,6 +513,10 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     (default_rng(cfg.seed).random, right then left) on the device; otherwise
     the reference's own SeedSequence(seed).spawn(2)[0] standard-normal stream
     is used.
+
+    `comm` (distributed.Comm of an initialised process group, one rank per GPU):
+    the bootstrap relaxation -- the largest setup phase -- is split by triplet
+    slot over the ranks (`_smooth_slots`); every rank ends with the same hierarchy.
     """
     t0 = time.perf_counter()
     A = B_device if B_device is not None else as_device(problem.B)
@@ -488,7 +534,7 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
         ops = _LevelOps(A)
     rng = np.random.default_rng(ss_init) if draws is None else None
     with _phase("init"):
-        trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops)
+        trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops, comm=comm)
     stream = _SeedStream(ss_levels)
     eye = DeviceCSR.identity(n)
     geometry = problem.geometry
@@ -498,7 +544,7 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     hierarchy = None
     for cycle in range(cfg.setup_cycles):
         levels, trips = bootstrap_cycle(A, eye, eye, trips, cfg, geometry=geometry, depth=0,
-                                        first_cycle=(cycle == 0), seed_stream=stream, ops=ops)
+                                        first_cycle=(cycle == 0), seed_stream=stream, ops=ops, comm=comm)
         hierarchy = Hierarchy(levels)
         engine.col_fill(trips.dleft, 0, 1.0 / np.sqrt(n))
         engine.refresh_sigmas(A, None, None, trips.dleft, trips.dright, trips.dsigmas)

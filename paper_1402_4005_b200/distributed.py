@@ -58,6 +58,11 @@ class RowPartition:
         return np.searchsorted(self.offsets, np.asarray(idx), side="right") - 1
 
 
+def slot_bounds(k: int, world: int) -> np.ndarray:
+    """Test-vector slots [b[r], b[r+1]) smoothed by rank r (as even as k allows)."""
+    return np.array([(k * r) // world for r in range(world + 1)], dtype=np.int64)
+
+
 @dataclass
 class HaloPlan:
     """Exchange plan of one local operator's halo-extended numbering."""
@@ -113,6 +118,26 @@ class Comm:
             bufs = [torch.empty_like(pad) for _ in range(self.world)]
             dist.all_gather(bufs, pad)
         return torch.cat([bufs[r][: sizes[r]] for r in range(self.world)])
+
+    def all_gather_cols(self, own: torch.Tensor, bounds) -> torch.Tensor:
+        """n x k block from every rank's n x (bounds[r+1] - bounds[r]) column slice."""
+        if not self.active or self.world == 1:
+            return own
+        n = own.shape[0]
+        widths = [int(bounds[r + 1] - bounds[r]) for r in range(self.world)]
+        mx = max(widths)
+        pad = own if own.shape[1] == mx else torch.cat(
+            [own, torch.zeros((n, mx - own.shape[1]), dtype=own.dtype, device=own.device)], dim=1)
+        pad = pad.contiguous()
+        if self.gloo:
+            hp = pad.cpu()
+            bufs = [torch.empty_like(hp) for _ in range(self.world)]
+            dist.all_gather(bufs, hp)
+            bufs = [b.to(own.device) for b in bufs]
+        else:
+            bufs = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(bufs, pad)
+        return torch.cat([bufs[r][:, : widths[r]] for r in range(self.world)], dim=1).contiguous()
 
     def exchange(self, x_ext: torch.Tensor, plan: HaloPlan, sendbufs: dict, sendidx: dict):
         """Fill x_ext[n_own:] with the halo values owned by the peers."""

@@ -96,3 +96,56 @@ def solve_worker(rank, world, port, out_dir, name, agg, backend="gloo"):
              levels_partitioned=len(ds.vc.levels))
     import torch.distributed as dist
     dist.destroy_process_group()
+
+
+def setup_worker(rank, world, port, out_dir, name, backend="gloo"):
+    """GPU: run_setup with the bootstrap relaxation split by triplet slot over the ranks
+    (ranks share the device under gloo).  Every rank must end with the reference's hierarchy:
+    patterns bit-exact, values and x0 within the single-GPU tolerances."""
+    import torch
+    from conftest import csr_from, load_golden
+    import paper_1402_4005_b200 as pb
+    from paper_1402_4005_b200 import bootstrap
+    from paper_1402_4005_b200.distributed import Comm
+    from test_gpu_pipeline import _close, _problem, _same_pattern, _setup_cfg
+    _init(rank, world, port, backend)
+    torch.cuda.set_device(rank if backend == "nccl" else 0)
+    bootstrap.SLOT_PARTITION_MIN_ROWS = 64  # partition every level of the desk-size fixture
+    g = load_golden(name)
+    cfg = _setup_cfg(g)
+    injected = int(g["cfg_ints"][13]) >= 0
+    draws = (g["init_right_draw"], g["init_left_draw"]) if injected else None
+    setup = pb.run_setup(_problem(g), cfg, draws=draws, comm=Comm())
+    levels = setup.hierarchy.levels
+    ok = len(levels) == int(g["n_levels"])
+    worst = 0.0
+    for li, lev in enumerate(levels):
+        for key in ("B", "M", "N") + (("P", "Q") if lev.dP is not None else ()):
+            ref = csr_from(g, f"L{li}_{key}")
+            got = getattr(lev, key)
+            ok = ok and _same_pattern(got, ref) and _close(got.data, ref.data, 1e-9)
+        if lev.dP is not None:
+            ok = ok and bool(np.array_equal(lev.split.coarse, g[f"L{li}_coarse"]))
+    x0_err = float(np.abs(setup.x0 - g["x0"]).sum())
+    np.savez(Path(out_dir) / f"setup_{rank}.npz", ok=int(ok), x0_err=x0_err, x0=setup.x0)
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
+def cols_worker(rank, world, port, out_dir):
+    """CPU: the slot partition's column all-gather (uneven widths) and the host side of the
+    Gram-form Arnoldi coefficients against explicit CGS2 on a random basis."""
+    import torch
+    from paper_1402_4005_b200.distributed import Comm, slot_bounds
+    _init(rank, world, port)
+    comm = Comm()
+    ok = True
+    for k in (16, 12, 7):
+        b = slot_bounds(k, world)
+        ok = ok and b[0] == 0 and b[-1] == k and bool(np.all(np.diff(b) >= 0))
+        full = torch.arange(50 * k, dtype=torch.float64).reshape(50, k)
+        own = full[:, int(b[rank]): int(b[rank + 1])].contiguous()
+        ok = ok and bool(torch.equal(comm.all_gather_cols(own, b), full))
+    np.save(Path(out_dir) / f"cols_{rank}.npy", np.array([ok]))
+    import torch.distributed as dist
+    dist.destroy_process_group()
