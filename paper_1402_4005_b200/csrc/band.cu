@@ -857,6 +857,18 @@ int bt_apply_G(bamg_ctx* ctx, int S, int nb, int N, const BtB& F, const double* 
   return bt_sweep(ctx, S, nb, b, tmp, N, out, N, p);
 }
 
+// subspace block width of the banded triplet iteration: r wanted triplets plus guard columns.
+// An application of K^+ here is a chain of ~40 small launches whose cost barely depends on the
+// width, while the iteration count falls with the guard (convergence ~ (s_{p+1} / s_r)^2 per
+// iteration): measured at cfg4 (r = 16, tools/band_p_sweep.sh) 47.8 ms at p = 28, 42.0 at 32,
+// 33.4 at 40, 36.3 at 48 -- so r + 24 instead of the dense path's r + 12
+// (BAMG_BAND_P overrides, development)
+static int band_block_width(int r, int n) {
+  int p = r + 24;
+  if (const char* e = getenv("BAMG_BAND_P")) p = std::max(r + 1, atoi(e));
+  return std::min(std::min(p, 48), n);
+}
+
 struct BtDims {
   int n, N, S, nb, off;
 };
@@ -1152,7 +1164,7 @@ int band_cr_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt, const
   while ((1 << L) < nb) ++L;
   const int Np = nb * S, off = Np - n;
   const size_t S2 = (size_t)S * S, blk = S2 * nb;
-  const int p = std::min(r + 12, n);
+  const int p = band_block_width(r, n);
   BAMG_REQUIRE(ctx, p <= 48, "band path: subspace block too wide");
   BtDims d{n, Np, S, nb, off};
   // ---- factor
@@ -1443,7 +1455,7 @@ int band_coarsest_triplets(bamg_ctx* ctx, const bamg_csr* B, const bamg_csr* Bt,
   d.off = d.N - n;
   const int nb = d.nb, Np = d.N;
   const size_t S2 = (size_t)S * S, blk = S2 * nb;
-  const int p = std::min(r + 12, n);
+  const int p = band_block_width(r, n);
   BAMG_REQUIRE(ctx, p <= 48, "band path: subspace block too wide");
 
   // ---- block storage (arena; the kept B factor is copied out at the end)
