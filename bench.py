@@ -174,8 +174,9 @@ def vcycle_bytes(levels, nu1, nu2, as_stored=False):
     for li, lv in enumerate(levels[:-1]):
         n, nnz = lv.n, lv.nnz
         if as_stored and lv.dB.packed is not None:
-            sweep = 4 * nnz + 4 * (n + 1) + 25 * n
-            resid = 4 * nnz + 4 * (n + 1) + 24 * n
+            words = int(lv.dB.packed.numel())  # slice-major words incl. padding; offsets per 32 rows
+            sweep = 4 * words + 4 * (n // 32 + 1) + 25 * n
+            resid = 4 * words + 4 * (n // 32 + 1) + 24 * n
         else:
             sweep = 12 * nnz + 4 * (n + 1) + 32 * n
             resid = 12 * nnz + 4 * (n + 1) + 24 * n

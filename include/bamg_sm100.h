@@ -45,12 +45,16 @@ typedef struct bamg_csr {
   const int32_t* rowptr; /* nrows + 1 */
   const int32_t* col;    /* nnz */
   const double* val;     /* nnz */
-  /* optional packed copy made by bamg_csr_pack (NULL: none): one word per entry,
-   * (col - row) << 8 | value code, and the 512-double dictionary (values, then
-   * their correctly rounded reciprocals).  The k = 1 kernels read it instead of
-   * col / val; results are bit-identical. */
-  const uint32_t* packed; /* nnz */
+  /* optional packed copy made by bamg_csr_pack_plan / _fill (NULL: none): one 32-bit word
+   * per entry, (col - row) << 8 | value code, stored slice-major over 32-row slices (word u of
+   * row 32 s + l at pslice[s] + 32 u + l; rows shorter than the slice's longest are padded with
+   * code 255), the slice offsets pslice[nrows / 32 + 1] (in words), and the 512-double
+   * dictionary (values, then their correctly rounded reciprocals).  The k = 1 kernels read it
+   * instead of rowptr / col / val; results are bit-identical. */
+  const uint32_t* packed; /* pwords */
   const double* dict;     /* 512 */
+  const int32_t* pslice;  /* ceil(nrows / 32) + 1 */
+  int64_t pwords;
 } bamg_csr;
 
 /* ---------------------------------------------------------------- context */
@@ -92,13 +96,18 @@ int64_t bamg_trace_position(bamg_ctx* ctx);
 /* y = A x.  BIT-EXACT vs scipy csr_matvec.  Replaces spmv, sparse.py:81-86;
  * with A = explicit transpose it replaces spmv_transpose, sparse.py:89-94. */
 int bamg_spmv(bamg_ctx* ctx, const bamg_csr* A, const double* x, double* y);
-/* Packed (value-indexed, 32-bit) copy of a square operator for the HBM-bound
- * k = 1 kernels (SpMV, V-cycle Jacobi sweeps and residuals): fills packed[nnz]
- * and dict[512] and sets *ok_host = 1 when A has at most 256 distinct values
- * and |col - row| < 2^23 (the generators' B = I - A, chains.py:95-302), else
- * *ok_host = 0 and the caller keeps the plain CSR.  Storage only -- no
- * reference counterpart; replaces nothing in sparse.py:21-46 (the CSR stays). */
-int bamg_csr_pack(bamg_ctx* ctx, const bamg_csr* A, uint32_t* packed, double* dict, int* ok_host);
+/* Packed (value-indexed, 32-bit, slice-major) copy of a square operator for the HBM-bound
+ * k = 1 kernels (SpMV, V-cycle Jacobi sweeps and residuals).  _plan fills dict[512] and
+ * pslice[ceil(nrows / 32) + 1] and sets *ok_host = the number of dictionary entries and
+ * *words_host = the packed length when A
+ * has at most 254 distinct values and |col - row| < 2^23 (the generators' B = I - A,
+ * chains.py:95-302), else *ok_host = 0 and the caller keeps the plain CSR; _fill writes the
+ * words (ndict = the plan's *ok_host).  Storage
+ * only -- no reference counterpart; replaces nothing in sparse.py:21-46 (the CSR stays). */
+int bamg_csr_pack_plan(bamg_ctx* ctx, const bamg_csr* A, int32_t* pslice, double* dict, int* ok_host,
+                       int64_t* words_host);
+int bamg_csr_pack_fill(bamg_ctx* ctx, const bamg_csr* A, const int32_t* pslice, const double* dict, int ndict,
+                       uint32_t* packed);
 /* Y = A X for k interleaved vectors (n x k).  BIT-EXACT per column vs
  * csr_matvecs (interp.py:95, bootstrap.py:384-385). */
 int bamg_spmm(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k);

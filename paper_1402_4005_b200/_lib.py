@@ -29,7 +29,7 @@ class BamgError(RuntimeError):
 class CSR(C.Structure):
     _fields_ = [("nrows", C.c_int32), ("ncols", C.c_int32), ("nnz", C.c_int64),
                 ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
-                ("packed", C.c_void_p), ("dict", C.c_void_p)]
+                ("packed", C.c_void_p), ("dict", C.c_void_p), ("pslice", C.c_void_p), ("pwords", C.c_int64)]
 
 
 P = C.c_void_p
@@ -58,7 +58,8 @@ _SIGS = {
     "bamg_trace_position": [P],
     "bamg_spmv": [P, PCSR, P, P],
     "bamg_spmm": [P, PCSR, P, P, C.c_int],
-    "bamg_csr_pack": [P, PCSR, P, P, PINT],
+    "bamg_csr_pack_plan": [P, PCSR, P, P, PINT, PI64],
+    "bamg_csr_pack_fill": [P, PCSR, P, P, C.c_int, P],
     "bamg_csr_transpose": [P, PCSR, P, P, P],
     "bamg_sym_pattern_count": [P, PCSR, PCSR, P, PI64],
     "bamg_sym_pattern_fill": [P, PCSR, PCSR, P, P],

@@ -868,7 +868,9 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
 // The chain generators' B = I - A carries a handful of distinct values (the
 // transition rates / 1/deg), and the lattice and mesh orderings keep
 // |col - row| < 2^23.  Such an operator is stored a second time as one 32-bit
-// word per entry -- (col - row) << 8 | value code -- plus a 256-entry value
+// word per entry -- (col - row) << 8 | value code, slice-major over 32-row
+// slices (SELL-32: word u of the slice's 32 rows contiguous, short rows padded
+// with code 255) -- plus a 256-entry value
 // dictionary (with the correctly rounded reciprocals beside it): 4 instead of
 // 12 bytes per entry on the k = 1 V-cycle sweeps, residuals and the GMRES
 // SpMV, which are HBM-bound.  Decoding returns the original fp64 value, the
@@ -974,52 +976,98 @@ pack_dict_kernel(const unsigned long long* __restrict__ table, unsigned int* __r
   dict[PACK_DICT + rank] = __drcp_rn(v);
 }
 
+// words per 32-row slice: 32 x (longest row of the slice)
 __global__ void __launch_bounds__(256)
-pack_encode_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                   const double* __restrict__ val, const double* __restrict__ dict,
-                   const unsigned int* __restrict__ count, uint32_t* __restrict__ packed) {
+pack_slice_width_kernel(int nrows, const int32_t* __restrict__ rowptr, int nslices, int32_t* __restrict__ w32) {
   BAMG_PDL_PROLOGUE();
-  if (count[1] != 0u) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  int len = row < nrows ? __ldg(rowptr + row + 1) - __ldg(rowptr + row) : 0;
+  for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+  if ((threadIdx.x & 31) == 0 && (row >> 5) < nslices) w32[row >> 5] = 32 * len;
+}
+
+constexpr uint32_t PACK_PAD = 255u;  // value code of a padding word (delta 0): loaded, never accumulated
+
+// slice-major (SELL-32) fill: word u of row 32 s + l at pslice[s] + 32 u + l
+__global__ void __launch_bounds__(256)
+pack_fill_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                 const double* __restrict__ val, const double* __restrict__ dict, int nd,
+                 const int32_t* __restrict__ pslice, uint32_t* __restrict__ packed) {
+  BAMG_PDL_PROLOGUE();
   __shared__ unsigned long long s_key[PACK_DICT];
-  const int nd = (int)count[0];
   for (int i = threadIdx.x; i < PACK_DICT; i += blockDim.x)
     s_key[i] = i < nd ? (unsigned long long)__double_as_longlong(dict[i]) : PACK_EMPTY;
   __syncthreads();
-  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows; row += gridDim.x * blockDim.x) {
-    const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
-    for (int j = jb; j < je; ++j) {
-      const unsigned long long b = (unsigned long long)__double_as_longlong(__ldg(val + j));
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slice = row >> 5, lane = threadIdx.x & 31;
+  if (slice * 32 >= nrows) return;
+  const int base = __ldg(pslice + slice);
+  const int width = (__ldg(pslice + slice + 1) - base) >> 5;
+  int jb = 0, je = 0;
+  if (row < nrows) jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  for (int u = 0; u < width; ++u) {
+    uint32_t word = PACK_PAD;
+    if (jb + u < je) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(__ldg(val + jb + u));
       int lo = 0, hi = nd - 1;  // the value is in the dictionary by construction
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (s_key[mid] < b) lo = mid + 1;
         else hi = mid;
       }
-      const int delta = __ldg(col + j) - row;
-      packed[j] = ((uint32_t)delta << 8) | (uint32_t)lo;
+      const int delta = __ldg(col + jb + u) - row;
+      word = ((uint32_t)delta << 8) | (uint32_t)lo;
     }
+    packed[base + 32 * u + lane] = word;
   }
 }
 
-extern "C" int bamg_csr_pack(bamg_ctx* ctx, const bamg_csr* A, uint32_t* packed, double* dict, int* ok_host) {
+// Step 1: dictionary (dict[512]), slice offsets (pslice[nslices + 1], in words) and the
+// verdict: *ok_host = number of dictionary entries (0: A does not qualify),
+// *words_host = length of the packed array.
+extern "C" int bamg_csr_pack_plan(bamg_ctx* ctx, const bamg_csr* A, int32_t* pslice, double* dict, int* ok_host,
+                                  int64_t* words_host) {
   ctx->arena.reset();
   BAMG_TRY(check_csr(ctx, A));
-  BAMG_REQUIRE(ctx, packed && dict && ok_host, "null output");
+  BAMG_REQUIRE(ctx, pslice && dict && ok_host && words_host, "null output");
   *ok_host = 0;
+  *words_host = 0;
   if (A->nrows != A->ncols || A->nnz == 0) return 0;
+  const int nslices = (A->nrows + 31) / 32;
   unsigned long long* table;
-  BAMG_TRY(arena_get(ctx, (size_t)PACK_HASH + 1, &table));
+  int32_t* w32;
+  BAMG_TRY(arena_get(ctx, (size_t)PACK_HASH + 2, &table));
+  BAMG_TRY(arena_get(ctx, (size_t)nslices, &w32));
   unsigned int* count = reinterpret_cast<unsigned int*>(table + PACK_HASH);
+  int64_t* total = reinterpret_cast<int64_t*>(table + PACK_HASH + 1);
   BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(table, 0xFF, sizeof(unsigned long long) * PACK_HASH, ctx->stream));
-  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(count, 0, sizeof(unsigned long long), ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), ctx->stream));
   const int g = grid_for(A->nrows, 256);
   const int grid = g < ctx->num_sms * 8 ? g : ctx->num_sms * 8;
   BAMG_LAUNCH(ctx, pack_collect_kernel, grid, 256, 0, A->nrows, A->rowptr, A->col, A->val, table, count);
   BAMG_LAUNCH(ctx, pack_dict_kernel, 1, PACK_HASH, 0, table, count, dict);
-  BAMG_LAUNCH(ctx, pack_encode_kernel, grid, 256, 0, A->nrows, A->rowptr, A->col, A->val, dict, count, packed);
-  int64_t res = 0;
-  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(count), 1, &res));
-  *ok_host = ((uint64_t)res >> 32) == 0 ? 1 : 0;  // count[1] == 0
+  BAMG_LAUNCH(ctx, pack_slice_width_kernel, grid_for((int64_t)nslices * 32, 256), 256, 0, A->nrows, A->rowptr, nslices,
+              w32);
+  BAMG_TRY(scan_i32_dev(ctx, w32, pslice, nslices, total));
+  int64_t res[2] = {0, 0};
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(count), 2, res));
+  const uint64_t flags = (uint64_t)res[0];
+  // count[1] == 0 (no failure), at most 255 values (code 255 pads), offsets fit int32
+  if ((flags >> 32) == 0 && (flags & 0xffffffffu) < PACK_PAD && res[1] < (int64_t)1 << 31) {
+    *ok_host = (int)(flags & 0xffffffffu);
+    *words_host = res[1];
+  }
+  return 0;
+}
+
+// Step 2: the packed words (words_host of them) for a plan that said ok.
+extern "C" int bamg_csr_pack_fill(bamg_ctx* ctx, const bamg_csr* A, const int32_t* pslice, const double* dict,
+                                  int ndict, uint32_t* packed) {
+  BAMG_TRY(check_csr(ctx, A));
+  BAMG_REQUIRE(ctx, pslice && dict && packed && ndict >= 1 && ndict < (int)PACK_PAD, "bad packed plan");
+  const int nslices = (A->nrows + 31) / 32;
+  BAMG_LAUNCH(ctx, pack_fill_kernel, grid_for((int64_t)nslices * 32, 256), 256, 0, A->nrows, A->rowptr, A->col, A->val,
+              dict, ndict, pslice, packed);
   return 0;
 }
 
@@ -1031,10 +1079,12 @@ constexpr int PACKED_U = BAMG_PACKED_U;
 #define BAMG_PACKED_MINB 8
 #endif
 
-// thread per row, k = 1; same sums as csr_rows_kernel<EPI, 1, 1, U>
+// thread per row, k = 1, slice-major words: a warp's load of "entry u of my row" is one
+// contiguous 128-byte line (row-major words cost 5-6 lines per load: the kernel sat at 69 % of
+// the L1 pipe and 49 % of DRAM).  Same sums, in the same order, as csr_rows_kernel<EPI, 1, 1, U>.
 template <int EPI, int U>
 __global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
-csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint32_t* __restrict__ pk,
+csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
                        const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
                        EpiArgs ea) {
   BAMG_PDL_PROLOGUE();
@@ -1042,41 +1092,52 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint
   for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
   __syncthreads();
   const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
-  if (row >= nrows) return;
-  const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+  const int slice = row >> 5, lane = threadIdx.x & 31;
+  if (slice * 32 >= nrows) return;
+  const bool valid = row < nrows;
+  const int base = __ldg(pslice + slice);
+  const int width = (__ldg(pslice + slice + 1) - base) >> 5;
   // epilogue operands depend on the row only: in flight with the row's first loads
   double eb = 0.0, exo = 0.0;
   bool sk = false;
-  if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
-  if (EPI == EPI_JACOBI) {
-    if (ea.b) eb = __ldg(ea.b + row);
-    exo = __ldg(ea.xold + row);
-    sk = ea.skip[row] != 0;
+  if (valid) {
+    if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
+    if (EPI == EPI_JACOBI) {
+      if (ea.b) eb = __ldg(ea.b + row);
+      exo = __ldg(ea.xold + row);
+      sk = ea.skip[row] != 0;
+    }
   }
-  double acc = 0.0, dd = 0.0, rdd = __longlong_as_double(0x7FF0000000000000ll);  // no diagonal entry: d = 0, 1/d = inf
-  const double* xr = X + row;
-  for (int j = jb; j < je; j += U) {
+  double acc = 0.0;
+  uint32_t dcode = PACK_PAD;  // value code of the row's diagonal entry (delta 0), if it has one
+  const double* xr = X + (valid ? row : nrows - 1);  // rows past the end hold padding only (delta 0)
+  const uint32_t* p = pk + base + lane;
+  for (int u = 0; u < width; u += U) {
     uint32_t w[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) w[u] = __ldg(pk + (j + u < je ? j + u : je - 1));
+    for (int i = 0; i < U; ++i) w[i] = u + i < width ? __ldg(p + 32 * (u + i)) : PACK_PAD;
     double xv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = __ldg(xr + ((int32_t)w[u] >> 8));
+    for (int i = 0; i < U; ++i) xv[i] = __ldg(xr + ((int32_t)w[i] >> 8));
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (j + u < je) {
-        const double a = s_dict[w[u] & 255u];
-        acc = __dadd_rn(acc, __dmul_rn(a, xv[u]));
-        if (EPI == EPI_JACOBI && (w[u] >> 8) == 0u) dd = a, rdd = s_dict[PACK_DICT + (w[u] & 255u)];
+    for (int i = 0; i < U; ++i) {
+      const uint32_t code = w[i] & 255u;
+      if (code != PACK_PAD) {
+        acc = __dadd_rn(acc, __dmul_rn(s_dict[code], xv[i]));
+        if (EPI == EPI_JACOBI && w[i] < 256u) dcode = code;
       }
     }
   }
+  if (!valid) return;
   double out;
   if (EPI == EPI_PLAIN) {
     out = acc;
   } else if (EPI == EPI_RESID) {
     out = __dsub_rn(eb, acc);
   } else {
+    // no diagonal entry: d = 0, 1/d = inf (such rows are skip rows)
+    const double dd = dcode != PACK_PAD ? s_dict[dcode] : 0.0;
+    const double rdd = dcode != PACK_PAD ? s_dict[PACK_DICT + dcode] : __longlong_as_double(0x7FF0000000000000ll);
     const double num = __dmul_rn(ea.omega, __dsub_rn(eb, acc));
     const double upd = sk ? 0.0 : div_rn_recip(num, dd, rdd);
     out = __dadd_rn(exo, upd);
@@ -1087,7 +1148,7 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ rowptr, const uint
 // the bytes the packed kernels move (what the profiler's family figures use)
 static double packed_bytes(int epi, const bamg_csr* A, const EpiArgs& ea) {
   const double n = A->nrows;
-  double bytes = 4.0 * (n + 1) + 4.0 * (double)A->nnz + 8.0 * A->ncols + 8.0 * n;
+  double bytes = 4.0 * (n / 32 + 1) + 4.0 * (double)A->pwords + 8.0 * A->ncols + 8.0 * n;
   if (epi == EPI_RESID) bytes += 8.0 * n;
   if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * n : 0.0) + n;  // b, skip (d and 1/d come from the dictionary)
   return bytes;
@@ -1104,7 +1165,7 @@ static bool packed_enabled() {
 
 // returns 1 when the call is not covered (caller takes the CSR kernels)
 static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea) {
-  if (!A->packed || !A->dict || !packed_enabled()) return 1;
+  if (!A->packed || !A->dict || !A->pslice || !packed_enabled()) return 1;
   if (epi == EPI_JACOBI && (ea.peak || ea.b_scale || ea.xold != X)) return 1;
   if (epi != EPI_PLAIN && epi != EPI_RESID && epi != EPI_JACOBI) return 1;
   const int grid = (A->nrows + TILE_THREADS - 1) / TILE_THREADS;
@@ -1114,15 +1175,15 @@ static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double
   switch (epi) {
     case EPI_PLAIN:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->rowptr, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea);
       break;
     case EPI_RESID:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->rowptr, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea);
       break;
     default:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->rowptr, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea);
   }
   return 0;
 }

@@ -24,7 +24,7 @@ def device():
 
 
 class DeviceCSR:
-    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity", "packed", "dict")
+    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity", "packed", "dict", "pslice")
 
     def __init__(self, rowptr, col, val, shape, is_identity=False):
         self.rowptr = rowptr
@@ -36,6 +36,7 @@ class DeviceCSR:
         # packed copy for the k = 1 kernels (engine.pack_operator), else None
         self.packed = None
         self.dict = None
+        self.pslice = None
 
     @property
     def nnz(self) -> int:
@@ -52,7 +53,9 @@ class DeviceCSR:
                                   self.col.data_ptr() if self.nnz else None,
                                   self.val.data_ptr() if self.nnz else None,
                                   self.packed.data_ptr() if self.packed is not None else None,
-                                  self.dict.data_ptr() if self.dict is not None else None)
+                                  self.dict.data_ptr() if self.dict is not None else None,
+                                  self.pslice.data_ptr() if self.pslice is not None else None,
+                                  int(self.packed.numel()) if self.packed is not None else 0)
         return self._desc
 
     def ref(self):

@@ -57,21 +57,24 @@ def spmm(A: DeviceCSR, X):
 
 
 def pack_operator(A: DeviceCSR) -> bool:
-    """Attach the packed (value-indexed, 32-bit) copy the k = 1 kernels stream
-    instead of col / val (bamg_csr_pack).  True when A qualifies (<= 256
-    distinct values, |col - row| < 2^23); otherwise A is left as it is."""
-    A.packed = A.dict = None
+    """Attach the packed (value-indexed, 32-bit, slice-major) copy the k = 1 kernels
+    stream instead of rowptr / col / val (bamg_csr_pack_plan / _fill).  True when A
+    qualifies (<= 254 distinct values, |col - row| < 2^23); otherwise A is left as it is."""
+    A.packed = A.dict = A.pslice = None
     A._desc = None
     if A.shape[0] != A.shape[1] or A.nnz == 0:
         return False
-    packed = _empty(A.nnz, I32)
+    pslice = _empty((A.shape[0] + 31) // 32 + 1, I32)
     dic = _empty(512, F64)
-    ok = C.c_int(0)
-    _lib.call("bamg_csr_pack", A.ref(), _p(packed), _p(dic), C.byref(ok))
-    if ok.value:
-        A.packed, A.dict = packed, dic
-        A._desc = None
-    return bool(ok.value)
+    nd, words = C.c_int(0), C.c_int64(0)
+    _lib.call("bamg_csr_pack_plan", A.ref(), _p(pslice), _p(dic), C.byref(nd), C.byref(words))
+    if not nd.value:
+        return False
+    packed = _empty(max(words.value, 1), I32)
+    _lib.call("bamg_csr_pack_fill", A.ref(), _p(pslice), _p(dic), nd.value, _p(packed))
+    A.packed, A.dict, A.pslice = packed, dic, pslice
+    A._desc = None
+    return True
 
 
 def transpose(A: DeviceCSR) -> DeviceCSR:
