@@ -115,10 +115,22 @@ csr_tile_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 // partial sums live in registers and each neighbour's K-value segment is read
 // with 16-byte vector loads.  Per-vector sums stay sequential in ascending
 // column order (bit-identical to the pair kernel and to scipy).
+__device__ __forceinline__ void ldg_v4f64(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void stg_v4f64(double* p, const double* v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
 template <int K>
 struct VecIO {
   static __device__ __forceinline__ void load(const double* __restrict__ p, double* v) {
-    if constexpr (K % 2 == 0) {
+    if constexpr (K % 4 == 0) {
+      // 256-bit loads (sm_100): a thread owns 32-byte segments of a row of the block
+#pragma unroll
+      for (int i = 0; i < K / 4; ++i) ldg_v4f64(p + 4 * i, v + 4 * i);
+    } else if constexpr (K % 2 == 0) {
       const double2* q = reinterpret_cast<const double2*>(p);
 #pragma unroll
       for (int i = 0; i < K / 2; ++i) {
@@ -132,7 +144,10 @@ struct VecIO {
     }
   }
   static __device__ __forceinline__ void store(double* __restrict__ p, const double* v) {
-    if constexpr (K % 2 == 0) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < K / 4; ++i) stg_v4f64(p + 4 * i, v + 4 * i);
+    } else if constexpr (K % 2 == 0) {
       double2* q = reinterpret_cast<double2*>(p);
 #pragma unroll
       for (int i = 0; i < K / 2; ++i) q[i] = make_double2(v[2 * i], v[2 * i + 1]);
@@ -178,14 +193,14 @@ __device__ __forceinline__ void row_apply(const int32_t* __restrict__ rowptr, co
 // U at a time: all U neighbour segments are loaded before any is accumulated,
 // so each thread keeps U independent loads in flight.  256 threads per CTA,
 // 256 / G rows per CTA; col/val of the CTA's rows staged in shared memory.
-template <int EPI, int K, int G, int U, bool STAGE>
+template <int EPI, int K, int G, int U, bool STAGE, int MB = 0, bool EARLY = false>
 // 8 resident CTAs per SM caps the row kernels at 32 registers (full
 // occupancy): measured ~25% faster for k = 8 / 16 than the 40-72 registers
 // ptxas picks otherwise (tools/csr_bench.py)
 #ifndef BAMG_ROWS_MINB
 #define BAMG_ROWS_MINB 8
 #endif
-__global__ void __launch_bounds__(TILE_THREADS, BAMG_ROWS_MINB)
+__global__ void __launch_bounds__(TILE_THREADS, (MB > 0 ? MB : BAMG_ROWS_MINB))
 csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y, EpiArgs ea) {
   BAMG_PDL_PROLOGUE();
@@ -226,6 +241,17 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 #pragma unroll
     for (int q = 0; q < V; ++q) acc[q] = 0.0;
     const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+    // EARLY: the Jacobi epilogue's operands depend on the row only -- issued with the row extents
+    // instead of after the gathers (one memory latency less per row: the sweep is latency-bound)
+    [[maybe_unused]] bool e_sk = false;
+    [[maybe_unused]] double e_dd = 1.0, e_rdd = 0.0, e_xo[V], e_b[V];
+    if constexpr (EARLY && EPI == EPI_JACOBI) {
+      e_sk = ea.skip[row] != 0;
+      e_dd = ea.d[row];
+      e_rdd = ea.rd ? ea.rd[row] : 0.0;
+      VecIO<V>::load(ea.xold + (int64_t)row * K + voff, e_xo);
+      if (ea.b) VecIO<V>::load(ea.b + (int64_t)row * K + voff, e_b);
+    }
     for (int j = jb; j < je; j += U) {
       int cc[U];
       double aa[U];
@@ -273,7 +299,12 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 #pragma unroll
         for (int q = 0; q < V; ++q) bv[q] = __dmul_rn(ea.b_scale[voff + q], bv[q]);
       } else if (ea.b) {
-        VecIO<V>::load(ea.b + base, bv);
+        if constexpr (EARLY && EPI == EPI_JACOBI) {
+#pragma unroll
+          for (int q = 0; q < V; ++q) bv[q] = e_b[q];
+        } else {
+          VecIO<V>::load(ea.b + base, bv);
+        }
         if (ea.b_scale) {
 #pragma unroll
           for (int q = 0; q < V; ++q) bv[q] = __dmul_rn(ea.b_scale[voff + q], bv[q]);
@@ -283,10 +314,18 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
         for (int q = 0; q < V; ++q) bv[q] = 0.0;
       }
       double xo[V];
-      VecIO<V>::load(ea.xold + base, xo);
-      const bool sk = ea.skip[row] != 0;
-      const double dd = ea.d[row];
-      const double rdd = ea.rd ? ea.rd[row] : 0.0;
+      bool sk;
+      double dd, rdd;
+      if constexpr (EARLY && EPI == EPI_JACOBI) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) xo[q] = e_xo[q];
+        sk = e_sk, dd = e_dd, rdd = e_rdd;
+      } else {
+        VecIO<V>::load(ea.xold + base, xo);
+        sk = ea.skip[row] != 0;
+        dd = ea.d[row];
+        rdd = ea.rd ? ea.rd[row] : 0.0;
+      }
 #pragma unroll
       for (int q = 0; q < V; ++q) {
         const double num = __dmul_rn(ea.omega, __dsub_rn(bv[q], acc[q]));
@@ -332,7 +371,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
 // finishes.  A step therefore costs one memory latency and keeps
 // U * 8V + 12U bytes per thread in flight.  Sums stay sequential in ascending
 // column order per (row, vector): bit-identical to csr_rows_kernel.
-template <int EPI, int K, int G, int U, int MINB>
+template <int EPI, int K, int G, int U, int MINB, bool HASB = true>
 __global__ void __launch_bounds__(TILE_THREADS, MINB)
 csr_rows_pipe_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                      const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y,
@@ -404,7 +443,9 @@ csr_rows_pipe_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, 
       if (EPI == EPI_ADD) VecIO<V>::load(ea.xold + base, e0);
       if (EPI == EPI_JACOBI) {
         VecIO<V>::load(ea.xold + base, e0);
-        if (ea.b) VecIO<V>::load(ea.b + base, e1);
+        if constexpr (HASB) {
+          if (ea.b) VecIO<V>::load(ea.b + base, e1);
+        }
         sk = ea.skip[row] != 0;
         dd = ea.d[row];
         if (ea.rd) rdd = ea.rd[row];
@@ -434,7 +475,9 @@ csr_rows_pipe_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, 
 #pragma unroll
         for (int q = 0; q < V; ++q) {
           double bv = 0.0;
-          if (ea.b) bv = ea.b_scale ? __dmul_rn(ea.b_scale[voff + q], e1[q]) : e1[q];
+          if constexpr (HASB) {
+            if (ea.b) bv = ea.b_scale ? __dmul_rn(ea.b_scale[voff + q], e1[q]) : e1[q];
+          }
           const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc[q]));
           const double upd = sk ? 0.0 : (ea.rd ? div_rn_recip(num, dd, rdd) : __ddiv_rn(num, dd));
           out[q] = __dadd_rn(e0[q], upd);
@@ -470,6 +513,22 @@ csr_rows_pipe_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, 
     __syncthreads();
     if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
   }
+}
+
+// BAMG_G16 = "G:U": threads per row / unroll of the k = 16 kernels (G = 4: 256-bit segments)
+static void g16_cfg(int* g, int* u, int* mb = nullptr, int* pg = nullptr) {
+  static int gg = 0, uu = 0, mm = 0, pp = 0;
+  if (!gg) {
+    int a = 8, b = 4, c = 8;
+    const char* e = getenv("BAMG_G16");
+    if (!(e && sscanf(e, "%d:%d:%d", &a, &b, &c) == 3)) a = 8, b = 4, c = 8;
+    const char* e2 = getenv("BAMG_PIPE_G16");
+    pp = e2 ? atoi(e2) : 8;
+    uu = b, mm = c, gg = a;
+  }
+  *g = gg, *u = uu;
+  if (mb) *mb = mm;
+  if (pg) *pg = pp;
 }
 
 // BAMG_ROWS_PIPE: "0" disables the pipelined kernel; "K:U:MINB[,K:U:MINB...]"
@@ -509,14 +568,25 @@ static int launch_rows_pipe(bamg_ctx* ctx, int k, double bytes, const bamg_csr* 
                             const EpiArgs& ea) {
   const PipeCfg pc = pipe_cfg(k);
   if (pc.u == 0) return 1;
+  int g16, u16;
+  g16_cfg(&u16, &u16, nullptr, &g16);
+  if (k == 16 && g16 != 8 &&
+      ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(ea.b) |
+        reinterpret_cast<uintptr_t>(ea.xold)) & 31) != 0)
+    g16 = 8;
 #define BAMG_PIPE_CASE(KK, GG, UU, MB)                                                                      \
-  if (k == KK && pc.u == UU && pc.minb == MB) {                                                             \
+  if (k == KK && pc.u == UU && pc.minb == MB && (KK != 16 || g16 == GG)) {                                  \
     const int rb = TILE_THREADS / GG;                                                                       \
     const int ntiles = (A->nrows + rb - 1) / rb;                                                            \
     const int g = ntiles < ctx->num_sms * MB ? ntiles : ctx->num_sms * MB;                                \
-    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                            \
-                    (csr_rows_pipe_kernel<EPI, KK, GG, UU, MB>), g, TILE_THREADS, 0, A->nrows, ntiles,      \
-                    A->rowptr, A->col, A->val, X, Y, ea);                                                   \
+    if (EPI == EPI_JACOBI && !ea.b)                                                                         \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                          \
+                      (csr_rows_pipe_kernel<EPI, KK, GG, UU, MB, false>), g, TILE_THREADS, 0, A->nrows,     \
+                      ntiles, A->rowptr, A->col, A->val, X, Y, ea);                                         \
+    else                                                                                                    \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                          \
+                      (csr_rows_pipe_kernel<EPI, KK, GG, UU, MB>), g, TILE_THREADS, 0, A->nrows, ntiles,    \
+                      A->rowptr, A->col, A->val, X, Y, ea);                                                 \
     return 0;                                                                                               \
   }
   BAMG_PIPE_CASE(16, 8, 4, 5)
@@ -525,6 +595,15 @@ static int launch_rows_pipe(bamg_ctx* ctx, int k, double bytes, const bamg_csr* 
   BAMG_PIPE_CASE(16, 8, 6, 4)
   BAMG_PIPE_CASE(16, 8, 6, 3)
   BAMG_PIPE_CASE(16, 8, 8, 3)
+  BAMG_PIPE_CASE(16, 4, 2, 4)
+  BAMG_PIPE_CASE(16, 4, 2, 3)
+  BAMG_PIPE_CASE(16, 4, 4, 3)
+  BAMG_PIPE_CASE(16, 4, 1, 4)
+  BAMG_PIPE_CASE(16, 4, 1, 5)
+  BAMG_PIPE_CASE(16, 2, 1, 4)
+  BAMG_PIPE_CASE(16, 2, 1, 3)
+  BAMG_PIPE_CASE(16, 2, 2, 3)
+  BAMG_PIPE_CASE(16, 2, 2, 2)
   BAMG_PIPE_CASE(12, 6, 6, 4)
   BAMG_PIPE_CASE(12, 6, 6, 3)
   BAMG_PIPE_CASE(8, 4, 6, 4)
@@ -562,6 +641,40 @@ static int rows_stage_mode() {
 template <int EPI>
 static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const bamg_csr* A, const double* X, double* Y,
                        const EpiArgs& ea) {
+  if (k == 16) {
+    int g16, u16, m16;
+    g16_cfg(&g16, &u16, &m16);
+    const bool al32 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
+                        reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold) |
+                        reinterpret_cast<uintptr_t>(ea.mx)) & 31) == 0;
+    static const bool early = getenv("BAMG_EARLY") && getenv("BAMG_EARLY")[0] == '1';
+#define BAMG_ROWS16(GG, UU, MM)                                                                            \
+  if (al32 && g16 == GG && u16 == UU && m16 == MM) {                                                       \
+    int g = (A->nrows + TILE_THREADS / GG - 1) / (TILE_THREADS / GG);                                      \
+    if (early && EPI == EPI_JACOBI) {                                                                      \
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                        \
+                      (csr_rows_kernel<EPI, 16, GG, UU, false, MM, true>), g, TILE_THREADS, 0, A->nrows,   \
+                      A->rowptr, A->col, A->val, X, Y, ea);                                                \
+      return 0;                                                                                            \
+    }                                                                                                      \
+    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                          \
+                    (csr_rows_kernel<EPI, 16, GG, UU, false, MM>), g, TILE_THREADS, 0, A->nrows, A->rowptr, \
+                    A->col, A->val, X, Y, ea);                                                             \
+    return 0;                                                                                              \
+  }
+    BAMG_ROWS16(8, 4, 8)
+    BAMG_ROWS16(8, 4, 6)
+    BAMG_ROWS16(8, 4, 5)
+    BAMG_ROWS16(8, 6, 5)
+    BAMG_ROWS16(4, 4, 4)
+    BAMG_ROWS16(4, 4, 3)
+    BAMG_ROWS16(4, 2, 4)
+    BAMG_ROWS16(4, 2, 5)
+    BAMG_ROWS16(4, 3, 4)
+    BAMG_ROWS16(2, 2, 4)
+    BAMG_ROWS16(2, 2, 3)
+#undef BAMG_ROWS16
+  }
   switch (k) {
 #define BAMG_ROWS_CASE(KK, GG, UU)                                                                         \
   case KK: {                                                                                               \
@@ -800,6 +913,59 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
 
 static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea);
 
+// k = 16 with 32-byte-aligned blocks: 256-bit row segments (G = 4 threads per row).  Measured at
+// cfg4's level 0 (tools/g16_sweep.sh, L2 flushed): plain SpMM 1143 -> 928 us through the pipelined
+// kernel at U = 2 (0.85 of the HBM peak); the Jacobi sweep without a peak 1540 -> 1282 us through
+// the row kernel with its epilogue operands issued beside the row extents (one memory latency less
+// per row); the sweep with a peak stays on the G = 8 pipelined kernel (one atomic per CTA and column;
+// the G = 4 pipelined sweep needs > 64 registers and loses more to occupancy or spills than it gains).
+template <int EPI, int G, int U, int MB, bool HASB>
+static int launch_pipe16(bamg_ctx* ctx, double bytes, const bamg_csr* A, const double* X, double* Y,
+                         const EpiArgs& ea) {
+  const int rb = TILE_THREADS / G;
+  const int ntiles = (A->nrows + rb - 1) / rb;
+  const int g = ntiles < ctx->num_sms * MB ? ntiles : ctx->num_sms * MB;
+  BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,
+                  (csr_rows_pipe_kernel<EPI, 16, G, U, MB, HASB>), g, TILE_THREADS, 0, A->nrows, ntiles, A->rowptr,
+                  A->col, A->val, X, Y, ea);
+  return 0;
+}
+
+static int k16_policy() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("BAMG_K16");
+    mode = e ? atoi(e) : 1;
+  }
+  return mode;
+}
+
+static int launch_k16(bamg_ctx* ctx, int epi, double bytes, const bamg_csr* A, const double* X, double* Y,
+                      const EpiArgs& ea) {
+  const int mode = k16_policy();
+  if (mode == 0) return 1;
+  if (((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(ea.b) |
+        reinterpret_cast<uintptr_t>(ea.xold)) & 31) != 0)
+    return 1;
+  switch (epi) {
+    case EPI_PLAIN: return launch_pipe16<EPI_PLAIN, 4, 2, 4, true>(ctx, bytes, A, X, Y, ea);
+    case EPI_RESID: return launch_pipe16<EPI_RESID, 4, 2, 4, true>(ctx, bytes, A, X, Y, ea);
+    case EPI_ADD: return launch_pipe16<EPI_ADD, 4, 2, 4, true>(ctx, bytes, A, X, Y, ea);
+    case EPI_JACOBI: {
+      if (ea.peak) {
+        if (mode == 2 && !ea.b) return launch_pipe16<EPI_JACOBI, 4, 2, 3, false>(ctx, bytes, A, X, Y, ea);
+        return 1;  // G = 8 pipelined kernel
+      }
+      const int g = (A->nrows + TILE_THREADS / 4 - 1) / (TILE_THREADS / 4);
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,
+                      (csr_rows_kernel<EPI_JACOBI, 16, 4, 2, false, 5, true>), g, TILE_THREADS, 0, A->nrows,
+                      A->rowptr, A->col, A->val, X, Y, ea);
+      return 0;
+    }
+    default: return 1;
+  }
+}
+
 static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, int k,
                        double* Y, const EpiArgs& ea) {
   BAMG_TRY(check_csr(ctx, A));
@@ -821,6 +987,10 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
     if (rc <= 0) return rc;
   }
   static const bool pipe_forced = getenv("BAMG_ROWS_PIPE") != nullptr;
+  if (k == 16 && rows_kernel_enabled() && !pipe_forced && !getenv("BAMG_G16")) {
+    const int rc = launch_k16(ctx, epi, bytes, A, X, Y, ea);
+    if (rc <= 0) return rc;
+  }
   if (rows_kernel_enabled() && aligned && epi != EPI_JACOBI_M &&
       (pipe_forced || (epi == EPI_JACOBI && (ea.peak || ea.b)))) {
     int rc = 1;

@@ -73,6 +73,12 @@ for name in a.configs.split(","):
             (f"spmm Bt k={kk}", lambda: engine.spmm(At, X), base),
             (f"jacobi B k={kk}", lambda: engine.jacobi(A, d, skip, X, b=Bv), base + 8.0 * kk * n + 9.0 * n),
         ]
+        if kk > 1:
+            pk = torch.zeros(kk, dtype=torch.float64, device="cuda")
+            rows += [
+                (f"jacobi B k={kk} hom", lambda: engine.jacobi(A, d, skip, X), base + 9.0 * n),
+                (f"jacobi B k={kk} hom+peak", lambda: engine.jacobi(A, d, skip, X, peak=pk), base + 9.0 * n),
+            ]
         # speed of light at this size: a device copy moving the same bytes (read + write)
         half = int(base // 16)
         src = torch.ones(half, dtype=torch.float64, device="cuda")
