@@ -245,6 +245,13 @@ int bamg_test_weights(bamg_ctx* ctx, const bamg_csr* A, const double* X, int64_t
  * into out_col/out_val (n x caliber) and out_cnt[i] (C points: identity entry;
  * no-candidate F points: 0).  status_host (2 int64): [0] fits that took the
  * rank-deficient pseudo-inverse branch, [1] points deferred to the warp path. */
+/* Multi-GPU setup: restrict every following LS fit of this context to the
+ * fine points in rows [row_lo, row_hi) -- the per-point loop of _build_rows
+ * (interp.py:258-289) is independent per point, so each rank fits its own row block and
+ * the fixed-stride outputs (out_cnt / out_col / out_val) are all-gathered by rows.  Rows
+ * outside the range get out_cnt = 0.  row_lo < 0 restores the full range.  (The warp-only
+ * fallback path, k > 16 or caliber > 4, ignores the range and fits every row.) */
+int bamg_fit_set_row_range(bamg_ctx* ctx, int64_t row_lo, int64_t row_hi);
 int bamg_fit_rows(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* coarse_rank,
                   const double* X, const double* w, int64_t n, int k, int caliber,
                   int radius, double improvement_tol, int constrain, int nonnegative,

@@ -87,6 +87,7 @@ _SIGS = {
                           C.c_int, C.c_int, C.c_int],
     "bamg_refresh_sigmas": [P, PCSR, PCSR, PCSR, P, P, P, P, C.c_int],
     "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
+    "bamg_fit_set_row_range": [P, I64, I64],
     "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
                       F64, P, P, P, PI64],
     "bamg_fit_rows_csr": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,

@@ -389,6 +389,22 @@ def _smooth_block(ops: _LevelOps, M, N, trips: TripletSet, cfg: SetupConfig, inh
                         int(inhomogeneous), smooth=1, refresh=1)
 
 
+def _spgemm_many(products, comm=None):
+    """engine.spgemm_many, the rows of every product split over the ranks of `comm`
+    (multi-GPU setup): row i of A B only needs row i of A, so rank q multiplies its
+    contiguous block of A's rows by the replicated B and the blocks are all-gathered --
+    the same rows, bit for bit (per-row accumulation order included), as the full product."""
+    from .interp import PARTITION_STATS, ROW_PARTITION_MIN_ROWS
+    if comm is None or comm.world == 1 or min(A.shape[0] for A, _, _ in products) < ROW_PARTITION_MIN_ROWS:
+        return engine.spgemm_many(products)
+    from .distributed import RowPartition, row_slice
+    parts = [RowPartition(A.shape[0], comm.world) for A, _, _ in products]
+    local = engine.spgemm_many([(row_slice(A, *pt.range(comm.rank)), Bm, order)
+                                for (A, Bm, order), pt in zip(products, parts)])
+    PARTITION_STATS["products"] += len(products)
+    return [comm.all_gather_csr_rows(Cl, pt) for Cl, pt in zip(local, parts)]
+
+
 def _operator_degenerate(Bc: DeviceCSR) -> bool:
     """bootstrap.py:332-334."""
     d = engine.diag(Bc)
@@ -453,7 +469,7 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
         with _phase("adjacency", depth):
             adj = ops.adj
         with _phase("ls_fit", depth):
-            P, W = build_transfer_pair(A, split, v_tests, u_tests, cfg.interp, adj=adj)
+            P, W = build_transfer_pair(A, split, v_tests, u_tests, cfg.interp, adj=adj, comm=comm)
         with _phase("galerkin", depth):
             # B_c = (Q B) P (sparse.py:102-117), M_c = Q M Q^T, N_c = P^T N P
             # (bootstrap.py:372-373): the independent products of each stage
@@ -466,13 +482,13 @@ def bootstrap_cycle(B, M, N, trips: TripletSet, cfg: SetupConfig, geometry=None,
             stage1 = [(Q, A, 1)]
             stage1.append((Q, W, engine.SPGEMM_REV_A) if Md.is_identity else (Q, Md, 1))
             stage1.append((Pt, P, engine.SPGEMM_REV_B) if Nd.is_identity else (Nd, P, 1))
-            QB, QM, NP = engine.spgemm_many(stage1)
+            QB, QM, NP = _spgemm_many(stage1, comm)
             stage2 = [(QB, P, 0)]
             if not Md.is_identity:
                 stage2.append((QM, W, 0))
             if not Nd.is_identity:
                 stage2.append((Pt, NP, 0))
-            out2 = engine.spgemm_many(stage2)
+            out2 = _spgemm_many(stage2, comm)
             Bc = out2[0]
             Mc = QM if Md.is_identity else out2[1]
             Nc = NP if Nd.is_identity else out2[-1]

@@ -122,6 +122,9 @@ struct bamg_ctx {
   // per-context state of the translation units, created on first use and
   // released by bamg_ctx_destroy (no process-wide tables keyed by address)
   struct FitSlots* fit_slots = nullptr;          // interp.cu
+  // bamg_fit_set_row_range: the LS fits only produce rows [fit_lo, fit_hi) (multi-GPU setup:
+  // every rank fits its row block, the blocks are all-gathered); fit_lo < 0 = every row
+  int64_t fit_lo = -1, fit_hi = -1;
   struct GmresWork* gmres_work = nullptr;        // solver.cu
   struct SpgemmMemo* spgemm_memo = nullptr;      // spgemm.cu (SPG_SLOTS entries)
 };

@@ -948,10 +948,14 @@ __device__ bool tsolve_model(const TPoint<KM>& P, const int* trial, int tlen, bo
 // coarse points: identity rows; fine points: appended to the work list
 __global__ void fit_prepare_kernel(int n, const int32_t* __restrict__ crank, int caliber, int32_t* __restrict__ out_cnt,
                                    int32_t* __restrict__ out_col, double* __restrict__ out_val,
-                                   int32_t* __restrict__ list, unsigned int* __restrict__ nlist) {
+                                   int32_t* __restrict__ list, unsigned int* __restrict__ nlist, int lo, int hi) {
   BAMG_PDL_PROLOGUE();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (i < lo || i >= hi) {  // another rank's row (bamg_fit_set_row_range)
+    out_cnt[i] = 0;
+    return;
+  }
   int ci = crank[i];
   if (ci >= 0) {
     int64_t o = (int64_t)i * caliber;
@@ -1292,8 +1296,10 @@ static int fit_rows_launch(bamg_ctx* ctx, const bamg_csr* adj, const int32_t* co
     BAMG_TRY(arena_get(ctx, (size_t)n + 1, &flist));
     BAMG_TRY(arena_get(ctx, 1, &nfl));
     BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(nfl, 0, sizeof(unsigned int), ctx->stream));
+    const int row_lo = ctx->fit_lo >= 0 ? (int)(ctx->fit_lo < n ? ctx->fit_lo : n) : 0;
+    const int row_hi = ctx->fit_lo >= 0 ? (int)(ctx->fit_hi < n ? ctx->fit_hi : n) : (int)n;
     BAMG_LAUNCH(ctx, fit_prepare_kernel, grid_for(n, 256), 256, 0, (int)n, coarse_rank, caliber, out_cnt, out_col,
-                out_val, flist, nfl);
+                out_val, flist, nfl, row_lo, row_hi);
     int32_t *mcnt, *cbuf, *order;
     unsigned int *hist, *nsorted;
     BAMG_TRY(arena_get(ctx, (size_t)n + 1, &mcnt));
@@ -1342,6 +1348,17 @@ static int fit_status_check(bamg_ctx* ctx, const int64_t* st, int64_t* status_ho
     status_host[1] = st[2] & 0xffffffffll;
   }
   BAMG_REQUIRE(ctx, st[1] == 0, "candidate list overflow (more than 256 coarse candidates for one point)");
+  return 0;
+}
+
+extern "C" int bamg_fit_set_row_range(bamg_ctx* ctx, int64_t row_lo, int64_t row_hi) {
+  if (row_lo < 0) {
+    ctx->fit_lo = ctx->fit_hi = -1;
+    return 0;
+  }
+  BAMG_REQUIRE(ctx, row_hi >= row_lo, "row range must be ordered");
+  ctx->fit_lo = row_lo;
+  ctx->fit_hi = row_hi;
   return 0;
 }
 

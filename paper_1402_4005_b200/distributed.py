@@ -63,6 +63,15 @@ def slot_bounds(k: int, world: int) -> np.ndarray:
     return np.array([(k * r) // world for r in range(world + 1)], dtype=np.int64)
 
 
+def row_slice(A, r0: int, r1: int):
+    """Rows [r0, r1) of a DeviceCSR as a DeviceCSR over views of its arrays (one host read)."""
+    from .device import DeviceCSR
+    ends = A.rowptr[[r0, r1]].cpu()
+    j0, j1 = int(ends[0]), int(ends[1])
+    rp = (A.rowptr[r0:r1 + 1] - j0).contiguous()
+    return DeviceCSR(rp, A.col[j0:j1], A.val[j0:j1], (r1 - r0, A.shape[1]))
+
+
 @dataclass
 class HaloPlan:
     """Exchange plan of one local operator's halo-extended numbering."""
@@ -138,6 +147,41 @@ class Comm:
             bufs = [torch.empty_like(pad) for _ in range(self.world)]
             dist.all_gather(bufs, pad)
         return torch.cat([bufs[r][:, : widths[r]] for r in range(self.world)], dim=1).contiguous()
+
+    def all_gather_flat(self, own: torch.Tensor, sizes=None) -> torch.Tensor:
+        """Concatenation (rank order) of every rank's 1-D tensor; `sizes` = their lengths when
+        every rank already knows them (saves the size all-gather)."""
+        if not self.active or self.world == 1:
+            return own
+        if sizes is None:
+            sizes = self.all_gather_object(int(own.numel()))
+        mx = max(max(sizes), 1)
+        pad = torch.zeros(mx, dtype=own.dtype, device=own.device)
+        pad[: own.numel()] = own
+        if self.gloo:
+            hp = pad.cpu()
+            bufs = [torch.empty_like(hp) for _ in range(self.world)]
+            dist.all_gather(bufs, hp)
+            bufs = [b.to(own.device) for b in bufs]
+        else:
+            bufs = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(bufs, pad)
+        return torch.cat([bufs[r][: sizes[r]] for r in range(self.world)])
+
+    def all_gather_csr_rows(self, C_own, part: "RowPartition"):
+        """Full CSR from every rank's block of rows (rank order): per-row counts, columns and
+        values are concatenated, the row pointer is their running sum (int32, as everywhere)."""
+        from .device import DeviceCSR
+        if not self.active or self.world == 1:
+            return C_own
+        rows = [int(part.offsets[r + 1] - part.offsets[r]) for r in range(self.world)]
+        counts = self.all_gather_flat((C_own.rowptr[1:] - C_own.rowptr[:-1]).contiguous(), rows)
+        nnzs = self.all_gather_object(int(C_own.nnz))
+        col = self.all_gather_flat(C_own.col[: C_own.nnz].contiguous(), nnzs)
+        val = self.all_gather_flat(C_own.val[: C_own.nnz].contiguous(), nnzs)
+        rp = torch.zeros(part.n + 1, dtype=torch.int32, device=counts.device)
+        rp[1:] = torch.cumsum(counts, 0, dtype=torch.int32)
+        return DeviceCSR(rp, col, val, (part.n, C_own.shape[1]))
 
     def exchange(self, x_ext: torch.Tensor, plan: HaloPlan, sendbufs: dict, sendidx: dict):
         """Fill x_ext[n_own:] with the halo values owned by the peers."""

@@ -276,10 +276,17 @@ def fit_rows_csr(adj, coarse_rank, X, w, caliber, radius, tol, constrain, nonneg
     return DeviceCSR(rp, ci[: nnz.value], va[: nnz.value], (n, ncols)), (int(status[0]), int(status[1]))
 
 
-def fit_rows_csr_many(fits):
+def fit_set_row_range(lo=None, hi=None):
+    """Restrict the following LS fits to the fine points in rows [lo, hi) (None: every row)."""
+    _lib.call("bamg_fit_set_row_range", -1 if lo is None else int(lo), -1 if hi is None else int(hi))
+
+
+def fit_rows_csr_many(fits, raw=False):
     """Independent fits [dict(adj, coarse_rank, X, w, caliber, radius, tol,
     constrain, nonneg, ncols[, ridge])] (at most 4) with ONE host read for all
-    of them: [(DeviceCSR, (pinv_branch_fits, deferred)), ...]."""
+    of them: [(DeviceCSR, (pinv_branch_fits, deferred)), ...].  raw=True returns the
+    fixed-stride rows [(cnt, col, val, caliber, ncols), ...] instead (the multi-GPU setup
+    all-gathers them by rows before the CSR assembly)."""
     if not 1 <= len(fits) <= 4:
         raise ValueError("1..4 fits per batch")
     bufs = []
@@ -300,6 +307,8 @@ def fit_rows_csr_many(fits):
     status = (C.c_int64 * (2 * len(fits)))()
     nnz = (C.c_int64 * len(fits))()
     _lib.call("bamg_fit_rows_wait", len(fits), slots, status, nnz)
+    if raw:
+        return [(cnt, col, val, cal, ncols) for (n, cal, cnt, col, val, rp, ncols) in bufs]
     out = []
     for i, (n, cal, cnt, col, val, rp, ncols) in enumerate(bufs):
         m = int(nnz[i])

@@ -23,6 +23,11 @@ WEIGHT_SPREAD = 1e4    # interp.py:27
 RIDGE_KAPPA = 0.1      # interp.py:30
 COEF_CAP = 10.0        # interp.py:33
 
+#: levels below this many rows are fitted replicated on every rank (multi-GPU setup)
+ROW_PARTITION_MIN_ROWS = 1 << 14
+#: how many fits / sparse products of this process ran row-partitioned (tests, diagnostics)
+PARTITION_STATS = {"fits": 0, "products": 0}
+
 
 @dataclass(frozen=True)
 class InterpConfig:
@@ -108,16 +113,42 @@ def build_restriction_rows(B, split: CfSplitting, tests: WeightedTestSet, cfg: I
 
 
 def build_transfer_pair(B, split: CfSplitting, v_tests: WeightedTestSet, u_tests: WeightedTestSet,
-                        cfg: InterpConfig, adj: DeviceCSR | None = None):
+                        cfg: InterpConfig, adj: DeviceCSR | None = None, comm=None):
     """(P, W): build_interpolation and build_restriction_rows of one level
-    with one host synchronisation for both fits (they are independent)."""
+    with one host synchronisation for both fits (they are independent).
+
+    `comm` with more than one rank (multi-GPU setup): the per-point loop of _build_rows
+    (interp.py:258-289) is independent per point, so every rank fits the fine points of its
+    own contiguous row block (against the replicated test vectors and adjacency) and the
+    fixed-stride rows are all-gathered before the CSR assembly: the same rows, bit for bit,
+    as the single-GPU fit."""
     from .sparse import adjacency_structure
     S = adj if adj is not None else adjacency_structure(B)
     common = dict(adj=S, coarse_rank=split.dcrank, caliber=cfg.caliber, radius=cfg.search_radius,
                   tol=cfg.improvement_tol, nonneg=cfg.nonnegative, ncols=split.n_coarse)
-    (P, _), (W, _) = engine.fit_rows_csr_many([
-        dict(common, X=v_tests.dvectors, w=v_tests.dweights, constrain=False),
-        dict(common, X=u_tests.dvectors, w=u_tests.dweights, constrain=cfg.constrain_constant_in_q)])
+    fits = [dict(common, X=v_tests.dvectors, w=v_tests.dweights, constrain=False),
+            dict(common, X=u_tests.dvectors, w=u_tests.dweights, constrain=cfg.constrain_constant_in_q)]
+    n = int(v_tests.dvectors.shape[0])
+    if comm is not None and comm.world > 1 and n >= ROW_PARTITION_MIN_ROWS:
+        from .distributed import RowPartition
+        part = RowPartition(n, comm.world)
+        r0, r1 = part.range(comm.rank)
+        engine.fit_set_row_range(r0, r1)
+        try:
+            raw = engine.fit_rows_csr_many(fits, raw=True)
+        finally:
+            engine.fit_set_row_range(None)
+        rows = [int(part.offsets[r + 1] - part.offsets[r]) for r in range(comm.world)]
+        out = []
+        for cnt, col, val, cal, ncols in raw:
+            cnt_f = comm.all_gather_flat(cnt[r0:r1].contiguous(), rows)
+            wide = [m * cal for m in rows]
+            col_f = comm.all_gather_flat(col[r0 * cal:r1 * cal].contiguous(), wide)
+            val_f = comm.all_gather_flat(val[r0 * cal:r1 * cal].contiguous(), wide)
+            out.append(engine.rows_to_csr(cnt_f, col_f, val_f, n, cal, ncols))
+            PARTITION_STATS["fits"] += 1
+        return out[0], out[1]
+    (P, _), (W, _) = engine.fit_rows_csr_many(fits)
     return P, W
 
 

@@ -111,6 +111,8 @@ def setup_worker(rank, world, port, out_dir, name, backend="gloo"):
     _init(rank, world, port, backend)
     torch.cuda.set_device(rank if backend == "nccl" else 0)
     bootstrap.SLOT_PARTITION_MIN_ROWS = 64  # partition every level of the desk-size fixture
+    from paper_1402_4005_b200 import interp
+    interp.ROW_PARTITION_MIN_ROWS = 64      # ... its LS fits (row blocks) and Galerkin products too
     g = load_golden(name)
     cfg = _setup_cfg(g)
     injected = int(g["cfg_ints"][13]) >= 0
@@ -127,7 +129,8 @@ def setup_worker(rank, world, port, out_dir, name, backend="gloo"):
         if lev.dP is not None:
             ok = ok and bool(np.array_equal(lev.split.coarse, g[f"L{li}_coarse"]))
     x0_err = float(np.abs(setup.x0 - g["x0"]).sum())
-    np.savez(Path(out_dir) / f"setup_{rank}.npz", ok=int(ok), x0_err=x0_err, x0=setup.x0)
+    np.savez(Path(out_dir) / f"setup_{rank}.npz", ok=int(ok), x0_err=x0_err, x0=setup.x0,
+             fits=interp.PARTITION_STATS["fits"], products=interp.PARTITION_STATS["products"])
     import torch.distributed as dist
     dist.destroy_process_group()
 
@@ -146,6 +149,24 @@ def cols_worker(rank, world, port, out_dir):
         full = torch.arange(50 * k, dtype=torch.float64).reshape(50, k)
         own = full[:, int(b[rank]): int(b[rank + 1])].contiguous()
         ok = ok and bool(torch.equal(comm.all_gather_cols(own, b), full))
+    # row-block pieces of a CSR product (multi-GPU Galerkin products / LS fits): slices of the
+    # rows, all-gathered, give back the matrix
+    from scipy import sparse as sp
+    from paper_1402_4005_b200.device import DeviceCSR
+    from paper_1402_4005_b200.distributed import RowPartition, row_slice
+    M = sp.random(37, 23, density=0.2, random_state=5, format="csr")
+    M.sort_indices()
+    D = DeviceCSR(torch.from_numpy(M.indptr.astype(np.int32)), torch.from_numpy(M.indices.astype(np.int32)),
+                  torch.from_numpy(M.data.copy()), M.shape)
+    part = RowPartition(37, world)
+    own = row_slice(D, *part.range(rank))
+    r0, r1 = part.range(rank)
+    ok = ok and own.shape == (r1 - r0, 23) and int(own.rowptr[-1]) == own.nnz
+    full = comm.all_gather_csr_rows(own, part)
+    ok = ok and bool(torch.equal(full.rowptr, D.rowptr)) and bool(torch.equal(full.col, D.col)) \
+        and bool(torch.equal(full.val, D.val))
+    flat = comm.all_gather_flat(torch.arange(rank + 2, dtype=torch.int32))
+    ok = ok and flat.tolist() == [v for r in range(world) for v in range(r + 2)]
     np.save(Path(out_dir) / f"cols_{rank}.npy", np.array([ok]))
     import torch.distributed as dist
     dist.destroy_process_group()

@@ -65,7 +65,8 @@ def test_two_rank_nccl_solve_matches_reference(tmp_path, golden, name, agg):
 @pytest.mark.parametrize("name", ["pipe_cfg0_tandem64", "pipe_tandem32_k16_r30", "pipe_planar1024_k12"])
 def test_two_rank_slot_partitioned_setup_matches_reference(tmp_path, name):
     """run_setup(comm=...): the bootstrap relaxation split by triplet slot over two ranks
-    (k = 8, 16 and 12: 4 / 8 / 6 slots per rank) gives the reference's hierarchy on every
+    (k = 8, 16 and 12: 4 / 8 / 6 slots per rank), the LS fits split by row block and the
+    Galerkin products by row block of the left factor give the reference's hierarchy on every
     rank -- patterns bit-exact, values within 1e-9, x0 within 1e-9 -- and both ranks agree."""
     import torch.multiprocessing as mp
     import dist_workers
@@ -74,4 +75,5 @@ def test_two_rank_slot_partitioned_setup_matches_reference(tmp_path, name):
     for r in range(2):
         assert int(z[r]["ok"]) == 1
         assert float(z[r]["x0_err"]) <= 1e-9
+        assert int(z[r]["fits"]) >= 2 and int(z[r]["products"]) >= 4  # the partitioned paths ran
     assert np.array_equal(z[0]["x0"], z[1]["x0"])
