@@ -29,7 +29,10 @@ class BamgError(RuntimeError):
 class CSR(C.Structure):
     _fields_ = [("nrows", C.c_int32), ("ncols", C.c_int32), ("nnz", C.c_int64),
                 ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
-                ("packed", C.c_void_p), ("dict", C.c_void_p), ("pslice", C.c_void_p), ("pwords", C.c_int64)]
+                ("packed", C.c_void_p), ("dict", C.c_void_p), ("pslice", C.c_void_p), ("pwords", C.c_int64),
+                ("ptiles", C.c_void_p), ("st_w", C.c_int32), ("st_diag", C.c_int32),
+                ("st_delta", C.c_int32 * 8), ("st_val", C.c_double * 8), ("st_d", C.c_double),
+                ("st_rd", C.c_double), ("st_tiles", C.c_int64)]
 
 
 P = C.c_void_p
@@ -88,6 +91,7 @@ _SIGS = {
     "bamg_refresh_sigmas": [P, PCSR, PCSR, PCSR, P, P, P, P, C.c_int],
     "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
     "bamg_fit_set_row_range": [P, I64, I64],
+    "bamg_csr_pack_stencil": [P, PCSR, P, PCSR],
     "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
                       F64, P, P, P, PI64],
     "bamg_fit_rows_csr": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,

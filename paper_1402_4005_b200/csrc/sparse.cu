@@ -1241,6 +1241,104 @@ extern "C" int bamg_csr_pack_fill(bamg_ctx* ctx, const bamg_csr* A, const int32_
   return 0;
 }
 
+// ---- stencil tiles of a packed operator
+// record written by pack_stencil_kernel (device, 16 x 8 bytes): [0] w, [1] diag index,
+// [2..9] word of entry u, [10] matching tiles
+__global__ void __launch_bounds__(256)
+pack_stencil_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
+                    uint8_t* __restrict__ tiles, unsigned long long* __restrict__ rec) {
+  BAMG_PDL_PROLOGUE();
+  // the candidate: an interior point of the middle lattice line when the rows are a square
+  // lattice (nrows / 2 itself starts a line for an even side, and is the centre for an odd one:
+  // a quarter line further is interior for both)
+  int ref = nrows / 2 + (int)sqrt((double)nrows) / 4;
+  if (ref >= nrows) ref = nrows / 2;
+  const int rbase = __ldg(pslice + (ref >> 5));
+  const int rwidth = (__ldg(pslice + (ref >> 5) + 1) - rbase) >> 5;
+  uint32_t rw[8];
+  int w = 0, diag = -1;
+  bool ok = true;
+  for (int u = 0; u < rwidth; ++u) {
+    const uint32_t word = __ldg(pk + rbase + 32 * u + (ref & 31));
+    if ((word & 255u) == PACK_PAD) continue;
+    if (w == 8) {
+      ok = false;
+      break;
+    }
+    if (word < 256u) diag = w;
+    rw[w++] = word;
+  }
+  ok = ok && w >= 1 && diag >= 0;
+  const int row = blockIdx.x * 256 + threadIdx.x;
+  bool match = ok && row < nrows;
+  if (match) {
+    const int base = __ldg(pslice + (row >> 5));
+    const int width = (__ldg(pslice + (row >> 5) + 1) - base) >> 5;
+    match = width >= w;
+    for (int u = 0; match && u < width; ++u) {
+      const uint32_t word = __ldg(pk + base + 32 * u + (row & 31));
+      match = u < w ? word == rw[u] : (word & 255u) == PACK_PAD;
+    }
+  }
+  const int all = __syncthreads_and(match ? 1 : 0);
+  if (threadIdx.x == 0) {
+    tiles[blockIdx.x] = all ? 1 : 0;
+    if (all) atomicAdd(rec + 10, 1ull);
+    if (blockIdx.x == 0) {
+      rec[0] = ok ? (unsigned long long)w : 0ull;
+      rec[1] = (unsigned long long)(diag < 0 ? 0 : diag);
+      for (int u = 0; u < 8; ++u) rec[2 + u] = u < w ? rw[u] : 0ull;
+    }
+  }
+}
+
+extern "C" int bamg_csr_pack_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* tiles, bamg_csr* out) {
+  ctx->arena.reset();
+  BAMG_TRY(check_csr(ctx, A));
+  BAMG_REQUIRE(ctx, out && tiles, "null output");
+  *out = *A;
+  out->ptiles = nullptr;
+  out->st_w = 0;
+  out->st_tiles = 0;
+  if (!A->packed || !A->dict || !A->pslice || A->nrows < 256) return 0;
+  const int ntiles = (A->nrows + 255) / 256;
+  unsigned long long* rec;
+  BAMG_TRY(arena_get(ctx, 16, &rec));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(rec, 0, 16 * sizeof(unsigned long long), ctx->stream));
+  BAMG_LAUNCH(ctx, pack_stencil_kernel, ntiles, 256, 0, A->nrows, A->pslice, A->packed, tiles, rec);
+  int64_t h[11];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(rec), 11, h));
+  const int w = (int)h[0];
+  if (w < 1 || w > 8 || 2 * h[10] < ntiles) return 0;
+  // the dictionary entries of the stencil's codes (values and reciprocals) in one small read
+  double dict[2 * PACK_DICT];
+  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(dict, A->dict, sizeof(dict), cudaMemcpyDeviceToHost, ctx->stream));
+  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->syncs++;
+  out->st_w = w;
+  out->st_diag = (int)h[1];
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t word = (uint32_t)h[2 + u];
+    out->st_delta[u] = u < w ? ((int32_t)word >> 8) : 0;
+    out->st_val[u] = u < w ? dict[word & 255u] : 0.0;
+  }
+  const uint32_t dw = (uint32_t)h[2 + out->st_diag];
+  out->st_d = dict[dw & 255u];
+  out->st_rd = dict[PACK_DICT + (dw & 255u)];
+  out->ptiles = tiles;
+  out->st_tiles = h[10];
+  return 0;
+}
+
+// the stencil row in the kernel's parameter space (constant bank operands)
+struct StencilArgs {
+  const uint8_t* tiles;
+  int w;
+  int delta[8];
+  double val[8];
+  double d, rd;
+};
+
 #ifndef BAMG_PACKED_U
 #define BAMG_PACKED_U 4
 #endif
@@ -1256,8 +1354,42 @@ template <int EPI, int U>
 __global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
 csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
                        const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
-                       EpiArgs ea) {
+                       EpiArgs ea, const __grid_constant__ StencilArgs st) {
   BAMG_PDL_PROLOGUE();
+  if (st.tiles && st.tiles[blockIdx.x]) {
+    // stencil tile (TILE_THREADS = 256 rows, all valid, all carrying the stencil row): no packed
+    // words, no dictionary -- offsets and values are constant-bank operands
+    const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
+    double eb = 0.0;
+    bool sk = false;
+    if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
+    if (EPI == EPI_JACOBI) {
+      if (ea.b) eb = __ldg(ea.b + row);
+      sk = ea.skip[row] != 0;
+    }
+    const double* xr = X + row;
+    double xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < st.w) xv[u] = __ldg(xr + st.delta[u]);
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < st.w) acc = __dadd_rn(acc, __dmul_rn(st.val[u], xv[u]));
+    double out;
+    if (EPI == EPI_PLAIN) {
+      out = acc;
+    } else if (EPI == EPI_RESID) {
+      out = __dsub_rn(eb, acc);
+    } else {
+      const double exo = __ldg(ea.xold + row);
+      const double num = __dmul_rn(ea.omega, __dsub_rn(eb, acc));
+      const double upd = sk ? 0.0 : div_rn_recip(num, st.d, st.rd);
+      out = __dadd_rn(exo, upd);
+    }
+    Y[row] = out;
+    return;
+  }
   __shared__ double s_dict[2 * PACK_DICT];
   for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
   __syncthreads();
@@ -1318,7 +1450,10 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint
 // the bytes the packed kernels move (what the profiler's family figures use)
 static double packed_bytes(int epi, const bamg_csr* A, const EpiArgs& ea) {
   const double n = A->nrows;
-  double bytes = 4.0 * (n / 32 + 1) + 4.0 * (double)A->pwords + 8.0 * A->ncols + 8.0 * n;
+  // stencil tiles read neither their words nor the slice offsets
+  const double generic = A->ptiles ? 1.0 - 256.0 * (double)A->st_tiles / n : 1.0;
+  double bytes = generic * (4.0 * (n / 32 + 1) + 4.0 * (double)A->pwords) + 8.0 * A->ncols + 8.0 * n;
+  if (A->ptiles) bytes += n / 256;
   if (epi == EPI_RESID) bytes += 8.0 * n;
   if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * n : 0.0) + n;  // b, skip (d and 1/d come from the dictionary)
   return bytes;
@@ -1342,18 +1477,28 @@ static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double
   if (grid == 0) return 0;
   const double bytes = packed_bytes(epi, A, ea);
   const int fam = A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE;
+  StencilArgs st{};
+  static const bool no_stencil = getenv("BAMG_NO_STENCIL") && getenv("BAMG_NO_STENCIL")[0] == '1';
+  if (A->ptiles && A->st_w >= 1 && A->st_w <= 8 && !no_stencil) {
+    static_assert(TILE_THREADS == 256, "stencil tiles are 256 rows");
+    st.tiles = A->ptiles;
+    st.w = A->st_w;
+    for (int u = 0; u < 8; ++u) st.delta[u] = A->st_delta[u], st.val[u] = A->st_val[u];
+    st.d = A->st_d;
+    st.rd = A->st_rd;
+  }
   switch (epi) {
     case EPI_PLAIN:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea, st);
       break;
     case EPI_RESID:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea, st);
       break;
     default:
       BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea);
+                      A->pslice, A->packed, A->dict, X, Y, ea, st);
   }
   return 0;
 }

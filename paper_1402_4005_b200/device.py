@@ -24,7 +24,8 @@ def device():
 
 
 class DeviceCSR:
-    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity", "packed", "dict", "pslice")
+    __slots__ = ("rowptr", "col", "val", "shape", "_desc", "is_identity", "packed", "dict", "pslice",
+                 "ptiles", "stencil")
 
     def __init__(self, rowptr, col, val, shape, is_identity=False):
         self.rowptr = rowptr
@@ -37,6 +38,10 @@ class DeviceCSR:
         self.packed = None
         self.dict = None
         self.pslice = None
+        # stencil of the packed copy (engine.pack_operator): the tile flags (device) and the
+        # filled descriptor bamg_csr_pack_stencil returned (the st_* fields are copied from it)
+        self.ptiles = None
+        self.stencil = None
 
     @property
     def nnz(self) -> int:
@@ -56,6 +61,14 @@ class DeviceCSR:
                                   self.dict.data_ptr() if self.dict is not None else None,
                                   self.pslice.data_ptr() if self.pslice is not None else None,
                                   int(self.packed.numel()) if self.packed is not None else 0)
+            st = self.stencil
+            if st is not None and self.ptiles is not None and self.packed is not None:
+                d = self._desc
+                d.ptiles = self.ptiles.data_ptr()
+                d.st_w, d.st_diag, d.st_d, d.st_rd, d.st_tiles = st.st_w, st.st_diag, st.st_d, st.st_rd, st.st_tiles
+                for u in range(8):
+                    d.st_delta[u] = st.st_delta[u]
+                    d.st_val[u] = st.st_val[u]
         return self._desc
 
     def ref(self):

@@ -9,6 +9,7 @@ exactly one engine entry point.  No arithmetic happens in Python.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -60,7 +61,7 @@ def pack_operator(A: DeviceCSR) -> bool:
     """Attach the packed (value-indexed, 32-bit, slice-major) copy the k = 1 kernels
     stream instead of rowptr / col / val (bamg_csr_pack_plan / _fill).  True when A
     qualifies (<= 254 distinct values, |col - row| < 2^23); otherwise A is left as it is."""
-    A.packed = A.dict = A.pslice = None
+    A.packed = A.dict = A.pslice = A.ptiles = A.stencil = None
     A._desc = None
     if A.shape[0] != A.shape[1] or A.nnz == 0:
         return False
@@ -74,6 +75,16 @@ def pack_operator(A: DeviceCSR) -> bool:
     _lib.call("bamg_csr_pack_fill", A.ref(), _p(pslice), _p(dic), nd.value, _p(packed))
     A.packed, A.dict, A.pslice = packed, dic, pslice
     A._desc = None
+    # stencil tiles: 256-row tiles whose rows all carry the interior row's entry list are swept
+    # from the kernel's parameter space (no packed words read); lattice generators only
+    if os.environ.get("BAMG_NO_STENCIL") == "1":
+        return True
+    tiles = _empty((A.shape[0] + 255) // 256, U8)
+    out = _lib.CSR()
+    _lib.call("bamg_csr_pack_stencil", A.ref(), _p(tiles), C.byref(out))
+    if out.ptiles:
+        A.ptiles, A.stencil = tiles, out
+        A._desc = None
     return True
 
 

@@ -374,7 +374,8 @@ def test_block_kernels_match_numpy(eng, k):
     assert np.array_equal(Pm, X[:, perm])
 
 
-@pytest.mark.parametrize("family,side", [("tandem", 63), ("uniform2d", 40), ("planar", 1500)])
+@pytest.mark.parametrize("family,side", [("tandem", 63), ("uniform2d", 40), ("planar", 1500),
+                                         ("tandem", 700), ("uniform2d", 611)])
 def test_packed_operator_kernels_bitexact(eng, family, side):
     """bamg_csr_pack: the k = 1 SpMV / residual / Jacobi kernels on the packed
     (value-indexed, 32-bit) copy of a generator chain's B reproduce the CSR
@@ -392,6 +393,14 @@ def test_packed_operator_kernels_bitexact(eng, family, side):
     plain = up(eng, B)
     assert engine.pack_operator(dB)
     assert dB.packed is not None and dB.desc().packed
+    # stencil tiles (bamg_csr_pack_stencil): the big lattices sweep most 256-row tiles from the
+    # interior row's entry list, the small ones (every tile crosses a lattice line) and the mesh do not
+    if family != "planar" and side >= 600:
+        assert dB.ptiles is not None and dB.desc().ptiles
+        assert 0.5 < float(dB.ptiles.sum()) / dB.ptiles.numel() < 1.0
+        assert dB.desc().st_w == int(np.diff(B.indptr)[n // 2 + side // 4])
+    else:
+        assert dB.ptiles is None and not dB.desc().ptiles
     rng = np.random.default_rng(7)
     x, b = rng.standard_normal(n), rng.standard_normal(n)
     dx, db = dvec(x), dvec(b)
