@@ -175,8 +175,12 @@ def vcycle_bytes(levels, nu1, nu2, as_stored=False):
         n, nnz = lv.n, lv.nnz
         if as_stored and lv.dB.packed is not None:
             words = int(lv.dB.packed.numel())  # slice-major words incl. padding; offsets per 32 rows
-            sweep = 4 * words + 4 * (n // 32 + 1) + 25 * n
-            resid = 4 * words + 4 * (n // 32 + 1) + 24 * n
+            opb = 4 * words + 4 * (n // 32 + 1)
+            if lv.dB.ptiles is not None:
+                # stencil tiles read a flag per 256 rows instead of their words and offsets
+                opb = opb * (1.0 - 256.0 * int(lv.dB.stencil.st_tiles) / n) + n / 256
+            sweep = opb + 25 * n
+            resid = opb + 24 * n
         else:
             sweep = 12 * nnz + 4 * (n + 1) + 32 * n
             resid = 12 * nnz + 4 * (n + 1) + 24 * n

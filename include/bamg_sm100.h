@@ -55,7 +55,7 @@ typedef struct bamg_csr {
   const double* dict;     /* 512 */
   const int32_t* pslice;  /* ceil(nrows / 32) + 1 */
   int64_t pwords;
-  /* optional stencil of the packed copy (bamg_csr_pack_stencil; ptiles NULL: none): the lattice
+  /* optional stencil (bamg_csr_stencil; ptiles NULL: none): the lattice
    * generators' interior rows all carry the same (col - row, value) list, so a 256-row tile whose
    * rows all equal that list is flagged in ptiles[ceil(nrows / 256)] and swept without reading its
    * packed words at all -- offsets and values come from the kernel's parameter space.  Same
@@ -120,12 +120,14 @@ int bamg_csr_pack_plan(bamg_ctx* ctx, const bamg_csr* A, int32_t* pslice, double
                        int64_t* words_host);
 int bamg_csr_pack_fill(bamg_ctx* ctx, const bamg_csr* A, const int32_t* pslice, const double* dict, int ndict,
                        uint32_t* packed);
-/* Stencil of a packed operator (A->packed / dict / pslice set): the word list of row
- * nrows / 2 + sqrt(nrows) / 4 (an interior point of a square lattice) is the candidate; tiles[ceil(nrows / 256)] gets 1 for every 256-row tile whose rows all carry exactly
- * that list.  *out receives a copy of A with ptiles = tiles and the st_* fields filled when the
- * candidate has 1..8 entries, a diagonal, and at least half of the tiles match (one host read);
- * otherwise *out = *A with ptiles = NULL.  Storage only, like bamg_csr_pack_plan. */
-int bamg_csr_pack_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* tiles, bamg_csr* out);
+/* Stencil of a lattice operator: the (col - row, value) list of row nrows / 2 + sqrt(nrows) / 4
+ * (an interior point of a square lattice) is the candidate; tiles[ceil(nrows / 256)] gets 1 for every
+ * 256-row tile whose rows all carry exactly that list.  *out receives a copy of A with ptiles = tiles
+ * and the st_* fields filled when the candidate has 1..8 entries, a diagonal, and at least half of the
+ * tiles match (one host read); otherwise *out = *A with ptiles = NULL.  The k = 1 packed kernels and
+ * the k-wide sweeps of such an operator take offsets and values of flagged tiles from their
+ * parameter space.  Storage only, like bamg_csr_pack_plan. */
+int bamg_csr_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* tiles, bamg_csr* out);
 /* Y = A X for k interleaved vectors (n x k).  BIT-EXACT per column vs
  * csr_matvecs (interp.py:95, bootstrap.py:384-385). */
 int bamg_spmm(bamg_ctx* ctx, const bamg_csr* A, const double* X, double* Y, int k);

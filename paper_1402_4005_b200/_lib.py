@@ -91,7 +91,7 @@ _SIGS = {
     "bamg_refresh_sigmas": [P, PCSR, PCSR, PCSR, P, P, P, P, C.c_int],
     "bamg_test_weights": [P, PCSR, P, I64, C.c_int, C.c_int, P, P],
     "bamg_fit_set_row_range": [P, I64, I64],
-    "bamg_csr_pack_stencil": [P, PCSR, P, PCSR],
+    "bamg_csr_stencil": [P, PCSR, P, PCSR],
     "bamg_fit_rows": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,
                       F64, P, P, P, PI64],
     "bamg_fit_rows_csr": [P, PCSR, P, P, P, I64, C.c_int, C.c_int, C.c_int, F64, C.c_int, C.c_int,

@@ -548,6 +548,9 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
         A = DeviceCSR(A.rowptr, A.col, A.val, A.shape, is_identity=A.is_identity)
         engine.pack_operator(A)
         ops = _LevelOps(A)
+        if A.ptiles is not None:
+            # a lattice chain: B^T has an interior stencil too (the k-wide sweeps of the left vectors)
+            engine.attach_stencil(ops.Bt)
     rng = np.random.default_rng(ss_init) if draws is None else None
     with _phase("init"):
         trips = init_test_vectors(A, cfg, rng=rng, draws=draws, ops=ops, comm=comm)

@@ -913,6 +913,253 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
 
 static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea);
 
+// the stencil row in the kernel's parameter space (constant bank operands)
+struct StencilArgs {
+  const uint8_t* tiles;
+  int w;
+  int delta[8];
+  double val[8];
+  double d, rd;
+};
+
+// k-wide sweeps of a lattice operator with stencil tiles (bamg_csr_stencil).  csr_rows_kernel's
+// per-row chain is rowptr -> col / val -> gathers -> epilogue operands; in a flagged 256-row tile
+// every row's offsets and values are the kernel's constant-bank operands, so a row is ONE round of
+// loads: its W gathers, its right-hand side and its skip flag, all issued together, and the tile
+// reads neither rowptr / col / val nor d / 1/d.  Persistent CTAs stride over the tiles (one
+// atomic per CTA and column for the peak); tiles that cross a lattice boundary take the CSR row
+// code.  Sums in ascending column order per (row, vector): bit-identical to csr_rows_kernel.
+template <int EPI, int V>
+__device__ __forceinline__ void wide_epilogue(const EpiArgs& ea, int K, int row, int voff, const double* acc,
+                                              const double* bv_in, bool hasb, bool sk, double dd, double rdd,
+                                              double* pk, double* __restrict__ Y) {
+  const int64_t base = (int64_t)row * K + voff;
+  double out[V];
+  if (EPI == EPI_PLAIN) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[q] = acc[q];
+  } else if (EPI == EPI_RESID) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[q] = __dsub_rn(bv_in[q], acc[q]);
+  } else {
+    double xo[V];
+    VecIO<V>::load(ea.xold + base, xo);
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      double bv = 0.0;
+      if (hasb) bv = ea.b_scale ? __dmul_rn(ea.b_scale[voff + q], bv_in[q]) : bv_in[q];
+      const double num = __dmul_rn(ea.omega, __dsub_rn(bv, acc[q]));
+      const double upd = sk ? 0.0 : div_rn_recip(num, dd, rdd);
+      out[q] = __dadd_rn(xo[q], upd);
+      pk[q] = fmax(pk[q], fabs(out[q]));
+    }
+  }
+  VecIO<V>::store(Y + base, out);
+}
+
+// a tile that crosses a lattice boundary: the CSR row code, out of line (its registers are not the
+// stencil path's)
+template <int V>
+struct PeakV {
+  double v[V];
+};
+
+template <int EPI, int K, int G>
+__device__ __noinline__ PeakV<K / G> stencil_generic_tile(int nrows, const int32_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val, const double* __restrict__ X,
+                                                          double* __restrict__ Y, const EpiArgs& ea, int r0, int voff,
+                                                          bool hasb) {
+  constexpr int V = K / G;
+  constexpr int RB = TILE_THREADS / G;
+  double pk[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) pk[q] = 0.0;
+  for (int p = 0; p < G; ++p) {
+    const int row = r0 + p * RB;
+    if (row >= nrows) break;
+    double acc[V], bv[V];
+    bool sk = false;
+    double dd = 1.0, rdd = 0.0;
+    if (hasb) VecIO<V>::load(ea.b + (int64_t)row * K + voff, bv);
+    if (EPI == EPI_JACOBI) {
+      sk = ea.skip[row] != 0;
+      dd = ea.d[row];
+      rdd = ea.rd ? ea.rd[row] : 0.0;
+    }
+    row_apply<K, V, 4>(rowptr, col, val, X, row, voff, acc);
+    // without a stored reciprocal the IEEE division (div_rn_recip needs RN(1 / d))
+    if (EPI == EPI_JACOBI && !ea.rd) {
+      const int64_t base = (int64_t)row * K + voff;
+      double xo[V], out[V];
+      VecIO<V>::load(ea.xold + base, xo);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        double b1 = 0.0;
+        if (hasb) b1 = ea.b_scale ? __dmul_rn(ea.b_scale[voff + q], bv[q]) : bv[q];
+        const double num = __dmul_rn(ea.omega, __dsub_rn(b1, acc[q]));
+        out[q] = __dadd_rn(xo[q], sk ? 0.0 : __ddiv_rn(num, dd));
+        pk[q] = fmax(pk[q], fabs(out[q]));
+      }
+      VecIO<V>::store(Y + base, out);
+    } else {
+      wide_epilogue<EPI, V>(ea, K, row, voff, acc, bv, hasb, sk, dd, rdd, pk, Y);
+    }
+  }
+  PeakV<V> r;
+#pragma unroll
+  for (int q = 0; q < V; ++q) r.v[q] = pk[q];
+  return r;
+}
+
+template <int EPI, int K, int G, int W, int MINB, int UNR>
+__global__ void __launch_bounds__(TILE_THREADS, MINB)
+csr_rows_stencil_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ val, const double* __restrict__ X, double* __restrict__ Y,
+                        EpiArgs ea, const __grid_constant__ StencilArgs st) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(EPI == EPI_PLAIN || EPI == EPI_RESID || EPI == EPI_JACOBI, "epilogues of the B / B^T sweeps");
+  constexpr int V = K / G;
+  constexpr int RB = TILE_THREADS / G;  // rows per pass; a 256-row tile is G passes
+  __shared__ unsigned long long s_peak[K];
+  const bool want_peak = EPI == EPI_JACOBI && ea.peak != nullptr;
+  if (want_peak) {
+    if (threadIdx.x < K) s_peak[threadIdx.x] = 0ull;
+    __syncthreads();
+  }
+  const int lr = threadIdx.x / G;
+  const int sub = threadIdx.x - lr * G;
+  const int voff = sub * V;
+  const bool hasb = EPI == EPI_RESID || (EPI == EPI_JACOBI && ea.b != nullptr);
+  double pk[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) pk[q] = 0.0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * 256 + lr;
+    if (st.tiles[tile]) {
+#pragma unroll UNR
+      for (int p = 0; p < G; ++p) {
+        const int row = r0 + p * RB;
+        const double* xr = X + (int64_t)row * K + voff;
+        double xv[W][V], bv[V];
+#pragma unroll
+        for (int u = 0; u < W; ++u)
+          if (u < st.w) VecIO<V>::load(xr + (int64_t)st.delta[u] * K, xv[u]);
+        bool sk = false;
+        if (hasb) VecIO<V>::load(ea.b + (int64_t)row * K + voff, bv);
+        if (EPI == EPI_JACOBI) sk = ea.skip[row] != 0;
+        double acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+          if (u < st.w) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(st.val[u], xv[u][q]));
+          }
+        }
+        wide_epilogue<EPI, V>(ea, K, row, voff, acc, bv, hasb, sk, st.d, st.rd, pk, Y);
+      }
+    } else {
+      const PeakV<V> g = stencil_generic_tile<EPI, K, G>(nrows, rowptr, col, val, X, Y, ea, r0, voff, hasb);
+#pragma unroll
+      for (int q = 0; q < V; ++q) pk[q] = fmax(pk[q], g.v[q]);
+    }
+  }
+  if (want_peak) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      double m = pk[q];
+      for (int o = G; o < 32; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      pk[q] = m;
+    }
+    if ((threadIdx.x & 31) < G) {
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        atomicMax(&s_peak[sub * V + q], (unsigned long long)__double_as_longlong(pk[q]));
+    }
+    __syncthreads();
+    if (threadIdx.x < K) atomic_max_nonneg(&ea.peak[threadIdx.x], __longlong_as_double((long long)s_peak[threadIdx.x]));
+  }
+}
+
+static bool stencil_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BAMG_NO_STENCIL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// the bytes a k-wide stencil sweep moves: flagged tiles read no operator, no d / 1/d
+static double stencil_bytes(int epi, const bamg_csr* A, int k, const EpiArgs& ea) {
+  const double n = A->nrows, kk = k;
+  const double generic = 1.0 - 256.0 * (double)A->st_tiles / n;
+  double bytes = generic * (4.0 * (n + 1) + 12.0 * (double)A->nnz) + n / 256 + 8.0 * kk * A->ncols + 8.0 * kk * n;
+  if (epi == EPI_RESID) bytes += 8.0 * kk * n;
+  if (epi == EPI_JACOBI) bytes += (ea.b ? 8.0 * kk * n : 0.0) + n + generic * 16.0 * n;
+  return bytes;
+}
+
+// returns 1 when the call is not covered (caller takes the CSR kernels)
+static int launch_stencil(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, int k, double* Y,
+                          const EpiArgs& ea) {
+  if (!A->ptiles || A->st_w < 1 || A->st_w > 8 || !stencil_enabled()) return 1;
+  if (epi != EPI_PLAIN && epi != EPI_RESID && epi != EPI_JACOBI) return 1;
+  if (epi == EPI_JACOBI && ea.xold != X) return 1;
+  if (((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(ea.b) |
+        reinterpret_cast<uintptr_t>(ea.xold)) & 31) != 0)
+    return 1;
+  StencilArgs st{};
+  st.tiles = A->ptiles;
+  st.w = A->st_w;
+  for (int u = 0; u < 8; ++u) st.delta[u] = A->st_delta[u], st.val[u] = A->st_val[u];
+  st.d = A->st_d;
+  st.rd = A->st_rd;
+  const int ntiles = (A->nrows + 255) / 256;
+  const double bytes = stencil_bytes(epi, A, k, ea);
+  const int fam = A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE;
+  // BAMG_STENCIL_CFG = "MB:UNR" (development: CTAs per SM and passes in flight)
+  static int cmb = 0, cun = 0;
+  if (!cmb) {
+    int a = 4, b = 2;
+    const char* e = getenv("BAMG_STENCIL_CFG");
+    if (!(e && sscanf(e, "%d:%d", &a, &b) == 2)) a = 4, b = 2;
+    cmb = a, cun = b;
+  }
+#define BAMG_STENCIL_CASE(EE, KK, GG, WW, MB, UN)                                                              \
+  if (epi == EE && k == KK && A->st_w <= WW && cmb == MB && cun == UN) {                                      \
+    const int g = ntiles < ctx->num_sms * MB ? ntiles : ctx->num_sms * MB;                                    \
+    BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_stencil_kernel<EE, KK, GG, WW, MB, UN>), g, TILE_THREADS, 0,    \
+                    A->nrows, ntiles, A->rowptr, A->col, A->val, X, Y, ea, st);                               \
+    return 0;                                                                                                 \
+  }
+#define BAMG_STENCIL_K(KK, GG, MB, UN)                \
+  BAMG_STENCIL_CASE(EPI_PLAIN, KK, GG, 4, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_RESID, KK, GG, 4, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_JACOBI, KK, GG, 4, MB, UN)    \
+  BAMG_STENCIL_CASE(EPI_PLAIN, KK, GG, 5, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_PLAIN, KK, GG, 8, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_RESID, KK, GG, 5, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_RESID, KK, GG, 8, MB, UN)     \
+  BAMG_STENCIL_CASE(EPI_JACOBI, KK, GG, 5, MB, UN)    \
+  BAMG_STENCIL_CASE(EPI_JACOBI, KK, GG, 8, MB, UN)
+  BAMG_STENCIL_K(16, 8, 4, 2)
+  BAMG_STENCIL_K(16, 8, 6, 1)
+  BAMG_STENCIL_K(16, 8, 5, 1)
+  BAMG_STENCIL_K(16, 8, 3, 2)
+  BAMG_STENCIL_K(16, 8, 4, 1)
+  BAMG_STENCIL_K(8, 4, 4, 2)
+  BAMG_STENCIL_K(8, 4, 6, 1)
+  BAMG_STENCIL_K(8, 4, 5, 1)
+  BAMG_STENCIL_K(8, 4, 3, 2)
+  BAMG_STENCIL_K(8, 4, 4, 1)
+#undef BAMG_STENCIL_K
+#undef BAMG_STENCIL_CASE
+  return 1;
+}
+
 // k = 16 with 32-byte-aligned blocks: 256-bit row segments (G = 4 threads per row).  Measured at
 // cfg4's level 0 (tools/g16_sweep.sh, L2 flushed): plain SpMM 1143 -> 928 us through the pipelined
 // kernel at U = 2 (0.85 of the HBM peak); the Jacobi sweep without a peak 1540 -> 1282 us through
@@ -984,6 +1231,10 @@ static int launch_tile(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* 
                               reinterpret_cast<uintptr_t>(ea.b) | reinterpret_cast<uintptr_t>(ea.xold)) & 15) == 0;
   if (k == 1 && A->packed) {
     const int rc = launch_packed(ctx, epi, A, X, Y, ea);
+    if (rc <= 0) return rc;
+  }
+  if (k > 1 && A->ptiles && rows_kernel_enabled()) {
+    const int rc = launch_stencil(ctx, epi, A, X, k, Y, ea);
     if (rc <= 0) return rc;
   }
   static const bool pipe_forced = getenv("BAMG_ROWS_PIPE") != nullptr;
@@ -1241,58 +1492,62 @@ extern "C" int bamg_csr_pack_fill(bamg_ctx* ctx, const bamg_csr* A, const int32_
   return 0;
 }
 
-// ---- stencil tiles of a packed operator
-// record written by pack_stencil_kernel (device, 16 x 8 bytes): [0] w, [1] diag index,
-// [2..9] word of entry u, [10] matching tiles
+// ---- stencil tiles of a lattice operator
+// record written by csr_stencil_kernel (device, 20 x 8 bytes): [0] w, [1] diag index,
+// [2..9] col - row of entry u, [10..17] value bits of entry u, [18] matching tiles
 __global__ void __launch_bounds__(256)
-pack_stencil_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
-                    uint8_t* __restrict__ tiles, unsigned long long* __restrict__ rec) {
+csr_stencil_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                   const double* __restrict__ val, uint8_t* __restrict__ tiles, unsigned long long* __restrict__ rec) {
   BAMG_PDL_PROLOGUE();
   // the candidate: an interior point of the middle lattice line when the rows are a square
   // lattice (nrows / 2 itself starts a line for an even side, and is the centre for an odd one:
   // a quarter line further is interior for both)
   int ref = nrows / 2 + (int)sqrt((double)nrows) / 4;
   if (ref >= nrows) ref = nrows / 2;
-  const int rbase = __ldg(pslice + (ref >> 5));
-  const int rwidth = (__ldg(pslice + (ref >> 5) + 1) - rbase) >> 5;
-  uint32_t rw[8];
-  int w = 0, diag = -1;
-  bool ok = true;
-  for (int u = 0; u < rwidth; ++u) {
-    const uint32_t word = __ldg(pk + rbase + 32 * u + (ref & 31));
-    if ((word & 255u) == PACK_PAD) continue;
-    if (w == 8) {
-      ok = false;
-      break;
+  const int rb = __ldg(rowptr + ref), w = __ldg(rowptr + ref + 1) - rb;
+  bool ok = w >= 1 && w <= 8;
+  int rdelta[8];
+  unsigned long long rbits[8];
+  int diag = -1;
+  if (ok) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      rdelta[u] = 0, rbits[u] = 0ull;
+      if (u < w) {
+        rdelta[u] = __ldg(col + rb + u) - ref;
+        rbits[u] = (unsigned long long)__double_as_longlong(__ldg(val + rb + u));
+        if (rdelta[u] == 0) diag = u;
+      }
     }
-    if (word < 256u) diag = w;
-    rw[w++] = word;
   }
-  ok = ok && w >= 1 && diag >= 0;
+  ok = ok && diag >= 0;
   const int row = blockIdx.x * 256 + threadIdx.x;
   bool match = ok && row < nrows;
   if (match) {
-    const int base = __ldg(pslice + (row >> 5));
-    const int width = (__ldg(pslice + (row >> 5) + 1) - base) >> 5;
-    match = width >= w;
-    for (int u = 0; match && u < width; ++u) {
-      const uint32_t word = __ldg(pk + base + 32 * u + (row & 31));
-      match = u < w ? word == rw[u] : (word & 255u) == PACK_PAD;
-    }
+    const int jb = __ldg(rowptr + row);
+    match = __ldg(rowptr + row + 1) - jb == w;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (match && u < w)
+        match = __ldg(col + jb + u) - row == rdelta[u] &&
+                (unsigned long long)__double_as_longlong(__ldg(val + jb + u)) == rbits[u];
   }
   const int all = __syncthreads_and(match ? 1 : 0);
   if (threadIdx.x == 0) {
     tiles[blockIdx.x] = all ? 1 : 0;
-    if (all) atomicAdd(rec + 10, 1ull);
+    if (all) atomicAdd(rec + 18, 1ull);
     if (blockIdx.x == 0) {
       rec[0] = ok ? (unsigned long long)w : 0ull;
       rec[1] = (unsigned long long)(diag < 0 ? 0 : diag);
-      for (int u = 0; u < 8; ++u) rec[2 + u] = u < w ? rw[u] : 0ull;
+      for (int u = 0; u < 8; ++u) {
+        rec[2 + u] = ok ? (unsigned long long)(long long)rdelta[u] : 0ull;
+        rec[10 + u] = ok ? rbits[u] : 0ull;
+      }
     }
   }
 }
 
-extern "C" int bamg_csr_pack_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* tiles, bamg_csr* out) {
+extern "C" int bamg_csr_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* tiles, bamg_csr* out) {
   ctx->arena.reset();
   BAMG_TRY(check_csr(ctx, A));
   BAMG_REQUIRE(ctx, out && tiles, "null output");
@@ -1300,44 +1555,30 @@ extern "C" int bamg_csr_pack_stencil(bamg_ctx* ctx, const bamg_csr* A, uint8_t* 
   out->ptiles = nullptr;
   out->st_w = 0;
   out->st_tiles = 0;
-  if (!A->packed || !A->dict || !A->pslice || A->nrows < 256) return 0;
+  if (A->nrows != A->ncols || A->nrows < 256 || A->nnz == 0) return 0;
   const int ntiles = (A->nrows + 255) / 256;
   unsigned long long* rec;
-  BAMG_TRY(arena_get(ctx, 16, &rec));
-  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(rec, 0, 16 * sizeof(unsigned long long), ctx->stream));
-  BAMG_LAUNCH(ctx, pack_stencil_kernel, ntiles, 256, 0, A->nrows, A->pslice, A->packed, tiles, rec);
-  int64_t h[11];
-  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(rec), 11, h));
+  BAMG_TRY(arena_get(ctx, 20, &rec));
+  BAMG_CHECK_CUDA(ctx, cudaMemsetAsync(rec, 0, 20 * sizeof(unsigned long long), ctx->stream));
+  BAMG_LAUNCH(ctx, csr_stencil_kernel, ntiles, 256, 0, A->nrows, A->rowptr, A->col, A->val, tiles, rec);
+  int64_t h[19];
+  BAMG_TRY(ctx_read_i64(ctx, reinterpret_cast<int64_t*>(rec), 19, h));
   const int w = (int)h[0];
-  if (w < 1 || w > 8 || 2 * h[10] < ntiles) return 0;
-  // the dictionary entries of the stencil's codes (values and reciprocals) in one small read
-  double dict[2 * PACK_DICT];
-  BAMG_CHECK_CUDA(ctx, cudaMemcpyAsync(dict, A->dict, sizeof(dict), cudaMemcpyDeviceToHost, ctx->stream));
-  BAMG_CHECK_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->syncs++;
+  if (w < 1 || w > 8 || 2 * h[18] < ntiles) return 0;
   out->st_w = w;
   out->st_diag = (int)h[1];
   for (int u = 0; u < 8; ++u) {
-    const uint32_t word = (uint32_t)h[2 + u];
-    out->st_delta[u] = u < w ? ((int32_t)word >> 8) : 0;
-    out->st_val[u] = u < w ? dict[word & 255u] : 0.0;
+    out->st_delta[u] = u < w ? (int32_t)h[2 + u] : 0;
+    double v = 0.0;
+    if (u < w) memcpy(&v, &h[10 + u], sizeof(double));
+    out->st_val[u] = v;
   }
-  const uint32_t dw = (uint32_t)h[2 + out->st_diag];
-  out->st_d = dict[dw & 255u];
-  out->st_rd = dict[PACK_DICT + (dw & 255u)];
+  out->st_d = out->st_val[out->st_diag];
+  out->st_rd = 1.0 / out->st_d;  // IEEE round-to-nearest: the value __drcp_rn gives the dictionary
   out->ptiles = tiles;
-  out->st_tiles = h[10];
+  out->st_tiles = h[18];
   return 0;
 }
-
-// the stencil row in the kernel's parameter space (constant bank operands)
-struct StencilArgs {
-  const uint8_t* tiles;
-  int w;
-  int delta[8];
-  double val[8];
-  double d, rd;
-};
 
 #ifndef BAMG_PACKED_U
 #define BAMG_PACKED_U 4

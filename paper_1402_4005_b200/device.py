@@ -38,8 +38,8 @@ class DeviceCSR:
         self.packed = None
         self.dict = None
         self.pslice = None
-        # stencil of the packed copy (engine.pack_operator): the tile flags (device) and the
-        # filled descriptor bamg_csr_pack_stencil returned (the st_* fields are copied from it)
+        # stencil (engine.attach_stencil): the tile flags (device) and the
+        # filled descriptor bamg_csr_stencil returned (the st_* fields are copied from it)
         self.ptiles = None
         self.stencil = None
 
@@ -62,7 +62,7 @@ class DeviceCSR:
                                   self.pslice.data_ptr() if self.pslice is not None else None,
                                   int(self.packed.numel()) if self.packed is not None else 0)
             st = self.stencil
-            if st is not None and self.ptiles is not None and self.packed is not None:
+            if st is not None and self.ptiles is not None:
                 d = self._desc
                 d.ptiles = self.ptiles.data_ptr()
                 d.st_w, d.st_diag, d.st_d, d.st_rd, d.st_tiles = st.st_w, st.st_diag, st.st_d, st.st_rd, st.st_tiles

@@ -75,10 +75,27 @@ def pack_operator(A: DeviceCSR) -> bool:
     _lib.call("bamg_csr_pack_fill", A.ref(), _p(pslice), _p(dic), nd.value, _p(packed))
     A.packed, A.dict, A.pslice = packed, dic, pslice
     A._desc = None
-    # stencil tiles: 256-row tiles whose rows all carry the interior row's entry list are swept
-    # from the kernel's parameter space (no packed words read); lattice generators only
-    if os.environ.get("BAMG_NO_STENCIL") == "1":
-        return True
+    attach_stencil(A)
+    return True
+
+
+def attach_stencil(A: DeviceCSR) -> bool:
+    """Flag the 256-row tiles of a lattice operator whose rows all carry the interior row's
+    (col - row, value) list (bamg_csr_stencil); the k = 1 packed kernels and the k-wide sweeps
+    take those tiles' offsets and values from their parameter space.  False (A unchanged) for
+    operators without a dominant row: meshes, Galerkin levels."""
+    A.ptiles = A.stencil = None
+    A._desc = None
+    if os.environ.get("BAMG_NO_STENCIL") == "1" or A.shape[0] != A.shape[1] or A.nnz == 0:
+        return False
+    tiles = _empty((A.shape[0] + 255) // 256, U8)
+    out = _lib.CSR()
+    _lib.call("bamg_csr_stencil", A.ref(), _p(tiles), C.byref(out))
+    if not out.ptiles:
+        return False
+    A.ptiles, A.stencil = tiles, out
+    A._desc = None
+    return True
     tiles = _empty((A.shape[0] + 255) // 256, U8)
     out = _lib.CSR()
     _lib.call("bamg_csr_pack_stencil", A.ref(), _p(tiles), C.byref(out))

@@ -59,6 +59,8 @@ for name in a.configs.split(","):
     k = bench.CONFIGS[name][2]
     A = DeviceCSR.from_host(prob.B)
     At = engine.transpose(A)
+    engine.attach_stencil(A)   # lattice operators: stencil tiles (BAMG_NO_STENCIL=1 disables)
+    engine.attach_stencil(At)
     n, nnz = A.shape[0], A.nnz
     d = engine.diag(A)
     skip = engine.degenerate_rows(A, d)
