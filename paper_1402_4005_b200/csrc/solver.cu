@@ -601,6 +601,37 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane
   return a[0];
 }
 
+// The same fold for NV = 8 or 16 values per lane: log2(NV) halving steps leave lane l with value
+// l mod NV summed over its group of NV lanes, and the 32 / NV groups are added by plain butterfly
+// steps (9 / 16 shuffles instead of 31); every lane ends with the total of value l mod NV.
+template <int NV>
+__device__ __forceinline__ double warp_transpose_sum_n(double (&a)[NV], int lane) {
+#pragma unroll
+  for (int half = NV / 2; half >= 1; half >>= 1) {
+    const bool hi = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = hi ? a[i] : a[i + half];
+      const double keep = hi ? a[i + half] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  double r = a[0];
+#pragma unroll
+  for (int o = NV; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+// products of the row's NS values with s, folded over the warp (NS <= 32 slots of one group)
+template <int NS>
+__device__ __forceinline__ double cgs_fold(const double* v, double s, int lane) {
+  constexpr int NV = NS <= 8 ? 8 : 32;  // (the 16-value fold compiles to more registers than the 32-value one)
+  double pr[NV];
+#pragma unroll
+  for (int g = 0; g < NV; ++g) pr[g] = g < NS ? v[g < NS ? g : 0] * s : 0.0;
+  return warp_transpose_sum_n<NV>(pr, lane);
+}
+
 // MODE 0 (pass A): part[b][g] = chunk sum of V_g . w, part[b][m] = |w|^2
 // MODE 1 (pass B): w <- w - sum_g c_g V_g (in place); part[b][g] = V_g . w_new,
 //                  part[b][m] = |w_new|^2  (runs only for code 0)
@@ -608,6 +639,54 @@ __device__ __forceinline__ double warp_transpose_sum32(double (&a)[32], int lane
 // basis values stay in registers, the 32 x MAXM products are folded across
 // the warp by transpose reductions, and lane l accumulates the dots of
 // vectors l, l + 32 over all of the warp's rows.
+// NS = the slots a thread really loads (a multiple of 8, >= the group's m): slots past m alias V_0
+// with zero coefficients, and every aliased load is an L1 hit that still costs an LSU slot -- a
+// group of 5 vectors read through 32 slots spent most of its load issue on them.
+template <int NS, int MODE>
+__device__ __forceinline__ void cgs_dots_body(const double* const* sp, const double* sc, double (*acc)[CGS_MAXM + 2],
+                                              int m, double* __restrict__ w, int64_t r0, int64_t r1, int lane,
+                                              int wid) {
+  constexpr int NB = (NS + 31) / 32;
+  double dot[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) dot[q] = 0.0;
+  double wn2 = 0.0;
+  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
+    const int64_t i = base + lane;
+    const bool ok = i < r1;
+    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
+    double v[NS];
+#pragma unroll
+    for (int g = 0; g < NS; ++g) v[g] = __ldcs(sp[g] + ic);
+    double wi = w[ic];
+    if (MODE == 1) {
+      double t = 0.0;
+#pragma unroll
+      for (int g = 0; g < NS; ++g) t = fma(sc[g], v[g], t);
+      wi -= t;
+      if (ok) w[i] = wi;
+    }
+    if (!ok) wi = 0.0;
+    wn2 = fma(wi, wi, wn2);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      if (q * 32 >= m) break;
+      if constexpr (NS <= 32) {
+        dot[q] += cgs_fold<NS>(v, wi, lane);
+      } else {
+        double pr[32];
+#pragma unroll
+        for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * wi;
+        dot[q] += warp_transpose_sum32(pr, lane);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
+  wn2 = warp_sum(wn2);
+  if (lane == 0) acc[wid][CGS_MAXM] = wn2;
+}
+
 template <int MAXM, int MODE>
 __global__ void __launch_bounds__(CGS_THREADS)
 cgs_dots_kernel(const double* const* __restrict__ Vp, int m_all, const double* __restrict__ c, double* __restrict__ w,
@@ -622,7 +701,6 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m_all, const double* _
   Vp += slot0;
   const int m = min(MAXM, m_all - slot0);
   static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
-  constexpr int NB = MAXM / 32;
   __shared__ const double* sp[MAXM];
   __shared__ double sc[MAXM];
   __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
@@ -632,44 +710,14 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m_all, const double* _
   cgs_load_ptrs<MAXM>(Vp, m, sp);
   const int64_t per = (n + nblk - 1) / nblk;
   const int64_t r0 = (int64_t)bx * per, r1 = min(r0 + per, n);
-  double dot[NB];
-#pragma unroll
-  for (int q = 0; q < NB; ++q) dot[q] = 0.0;
-  double wn2 = 0.0;
-  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
-    const int64_t i = base + lane;
-    const bool ok = i < r1;
-    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
-    double v[MAXM];
-#pragma unroll
-    for (int g = 0; g < MAXM; ++g) v[g] = __ldcs(sp[g] + ic);
-    double wi = w[ic];
-    if (MODE == 1) {
-      double t = 0.0;
-#pragma unroll
-      for (int g = 0; g < MAXM; ++g) t = fma(sc[g], v[g], t);
-      wi -= t;
-      if (ok) w[i] = wi;
-    }
-    if (!ok) wi = 0.0;
-    wn2 = fma(wi, wi, wn2);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (q * 32 >= m) break;
-      double pr[32];
-#pragma unroll
-      for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * wi;
-      dot[q] += warp_transpose_sum32(pr, lane);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
-  wn2 = warp_sum(wn2);
-  if (lane == 0) acc[wid][MAXM] = wn2;
+  if (MAXM == 32 && m <= 8) cgs_dots_body<8, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
+  else if (MAXM == 32 && m <= 16) cgs_dots_body<16, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
+  else if (MAXM == 32 && m <= 24) cgs_dots_body<24, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
+  else cgs_dots_body<MAXM, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
   __syncthreads();
   const int nslots = m + (by == 0 ? 1 : 0);  // |w|^2 (slot m_all) from the first group only
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
-    const int slot = q == m ? MAXM : q;
+    const int slot = q == m ? CGS_MAXM : q;
     double t = 0.0;
     for (int ww = 0; ww < CGS_WARPS; ++ww) t += acc[ww][slot];
     part[(int64_t)bx * stride + (q == m ? m_all : slot0 + q)] = t;
@@ -862,44 +910,29 @@ __global__ void cgs_gram_coef_kernel(int m, const double* __restrict__ G, double
 // the update pass: ww = w - V c; v_new = ww / state[1] (unscaled when flag = 2,
 // skipped on happy breakdown); x = x0 + e + V y (flag 0 only);
 // part[b][0..m) = V^T ww, part[b][m] = |ww|^2, part[b][m + 1] = |x|^2
-template <int MAXM>
-__global__ void __launch_bounds__(CGS_THREADS)
-cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
-                  const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
-                  const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
-                  int64_t n, double* __restrict__ vnew, double* __restrict__ x, double* __restrict__ part) {
-  BAMG_PDL_PROLOGUE();
-  static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
-  constexpr int NB = MAXM / 32;
-  __shared__ const double* sp[MAXM];
-  __shared__ double sc[MAXM], sy[MAXM];
-  __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
-    sc[g] = g < m ? c[g] : 0.0;
-    sy[g] = g < m ? y[g] : 0.0;
-  }
-  cgs_load_ptrs<MAXM>(Vp, m, sp);
-  const bool unsafe = flag[0] == 2.0;
-  const bool happy = state[0] != 0.0;
-  const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+template <int NS>
+__device__ __forceinline__ void cgs_update_body(const double* const* sp, const double* sc, const double* sy,
+                                                double (*acc)[CGS_MAXM + 2], int m, const double* __restrict__ w,
+                                                const double* __restrict__ x0, const double* __restrict__ e,
+                                                bool unsafe, bool happy, double inv, int64_t r0, int64_t r1,
+                                                double* __restrict__ vnew, double* __restrict__ x, int lane, int wid) {
+  constexpr int NB = (NS + 31) / 32;
   double dot[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) dot[q] = 0.0;
   double wn2 = 0.0, xn2 = 0.0;
+#pragma unroll 1
   for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
     const int64_t i = base + lane;
     const bool ok = i < r1;
     const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
-    double v[MAXM];
+    double v[NS];
 #pragma unroll
-    for (int g = 0; g < MAXM; ++g) v[g] = __ldcs(sp[g] + ic);
+    for (int g = 0; g < NS; ++g) v[g] = __ldcs(sp[g] + ic);
     const double wi = w[ic], x0i = x0[ic], ei = e[ic];
     double t = 0.0, u = 0.0;
 #pragma unroll
-    for (int g = 0; g < MAXM; ++g) {
+    for (int g = 0; g < NS; ++g) {
       t = fma(sc[g], v[g], t);
       u = fma(sy[g], v[g], u);
     }
@@ -920,21 +953,52 @@ cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __r
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
       if (q * 32 >= m) break;
-      double pr[32];
+      if constexpr (NS <= 32) {
+        dot[q] += cgs_fold<NS>(v, ww, lane);
+      } else {
+        double pr[32];
 #pragma unroll
-      for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * ww;
-      dot[q] += warp_transpose_sum32(pr, lane);
+        for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * ww;
+        dot[q] += warp_transpose_sum32(pr, lane);
+      }
     }
   }
 #pragma unroll
   for (int q = 0; q < NB; ++q) acc[wid][q * 32 + lane] = dot[q];
   wn2 = warp_sum(wn2);
   xn2 = warp_sum(xn2);
-  if (lane == 0) acc[wid][MAXM] = wn2, acc[wid][MAXM + 1] = xn2;
+  if (lane == 0) acc[wid][CGS_MAXM] = wn2, acc[wid][CGS_MAXM + 1] = xn2;
+}
+
+template <int MAXM, int NS = MAXM>
+__global__ void __launch_bounds__(CGS_THREADS, (NS <= 8 ? 5 : NS <= 32 ? 4 : 2))
+cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
+                  const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
+                  const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
+                  int64_t n, double* __restrict__ vnew, double* __restrict__ x, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  static_assert(MAXM % 32 == 0, "basis slots come in warps of 32");
+  __shared__ const double* sp[MAXM];
+  __shared__ double sc[MAXM], sy[MAXM];
+  __shared__ double acc[CGS_WARPS][CGS_MAXM + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
+    sc[g] = g < m ? c[g] : 0.0;
+    sy[g] = g < m ? y[g] : 0.0;
+  }
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const bool unsafe = flag[0] == 2.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  // NS = the slots a thread loads: the next multiple of 8 above m (see cgs_dots_body); one kernel
+  // per NS, so the short passes keep their own (small) register count and occupancy
+  cgs_update_body<NS>(sp, sc, sy, acc, m, w, x0, e, unsafe, happy, inv, r0, r1, vnew, x, lane, wid);
   __syncthreads();
   const int nslots = m + 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
-    const int slot = q >= m ? MAXM + (q - m) : q;
+    const int slot = q >= m ? CGS_MAXM + (q - m) : q;
     double t = 0.0;
     for (int ww2 = 0; ww2 < CGS_WARPS; ++ww2) t += acc[ww2][slot];
     part[(int64_t)blockIdx.x * (m + 2) + q] = t;
@@ -947,44 +1011,28 @@ cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __r
 // one thread); the halves exchange their partial projections through shared
 // memory (two 64-thread named barriers per 32 rows), half 0 forms ww, v_new and
 // x, and both take their vectors' dots with ww from the registers they hold.
-__global__ void __launch_bounds__(CGS_THREADS)
-cgs_update_pair_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
-                       const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
-                       const double* __restrict__ e, const double* __restrict__ state,
-                       const double* __restrict__ flag, int64_t n, double* __restrict__ vnew,
-                       double* __restrict__ x, double* __restrict__ part) {
-  BAMG_PDL_PROLOGUE();
-  constexpr int MAXM = 64, PAIRS = CGS_WARPS / 2;
-  __shared__ const double* sp[MAXM];
-  __shared__ double sc[MAXM], sy[MAXM];
-  __shared__ double acc[PAIRS][MAXM + 2];
-  __shared__ double xt[PAIRS][32], xu[PAIRS][32], xw[PAIRS][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int pair = wid >> 1, half = wid & 1;
-  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
-    sc[g] = g < m ? c[g] : 0.0;
-    sy[g] = g < m ? y[g] : 0.0;
-  }
-  cgs_load_ptrs<MAXM>(Vp, m, sp);
-  const bool unsafe = flag[0] == 2.0;
-  const bool happy = state[0] != 0.0;
-  const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+template <int NS>
+__device__ __forceinline__ void cgs_pair_body(const double* const* sp, const double* sc, const double* sy,
+                                              double (*acc)[CGS_MAXM + 2], double (*xt)[32], double (*xu)[32],
+                                              double (*xw)[32], int m, const double* __restrict__ w,
+                                              const double* __restrict__ x0, const double* __restrict__ e,
+                                              bool unsafe, bool happy, double inv, int64_t r0, int64_t r1,
+                                              double* __restrict__ vnew, double* __restrict__ x, int lane, int pair,
+                                              int half, int npairs) {
   const int g0 = half * 32;
   double dot = 0.0, wn2 = 0.0, xn2 = 0.0;
-  for (int64_t base = r0 + pair * 32; base < r1; base += 32 * PAIRS) {
+  for (int64_t base = r0 + pair * 32; base < r1; base += 32 * npairs) {
     const int64_t i = base + lane;
     const bool ok = i < r1;
     const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
-    double v[32];
+    double v[NS];
 #pragma unroll
-    for (int g = 0; g < 32; ++g) v[g] = __ldcs(sp[g0 + g] + ic);
+    for (int g = 0; g < NS; ++g) v[g] = __ldcs(sp[g0 + g] + ic);
     double wi = 0.0, x0i = 0.0, ei = 0.0;
     if (half == 0) wi = w[ic], x0i = x0[ic], ei = e[ic];
     double t = 0.0, u = 0.0;
 #pragma unroll
-    for (int g = 0; g < 32; ++g) {
+    for (int g = 0; g < NS; ++g) {
       t = fma(sc[g0 + g], v[g], t);
       u = fma(sy[g0 + g], v[g], u);
     }
@@ -1012,27 +1060,70 @@ cgs_update_pair_kernel(const double* const* __restrict__ Vp, int m, const double
     }
     asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
     if (half == 1) ww = xw[pair][lane];
-    if (g0 < m) {
-      double pr[32];
-#pragma unroll
-      for (int g = 0; g < 32; ++g) pr[g] = v[g] * ww;
-      dot += warp_transpose_sum32(pr, lane);
-    }
+    if (g0 < m) dot += cgs_fold<NS>(v, ww, lane);
   }
   acc[pair][g0 + lane] = dot;
   if (half == 0) {
     wn2 = warp_sum(wn2);
     xn2 = warp_sum(xn2);
-    if (lane == 0) acc[pair][MAXM] = wn2, acc[pair][MAXM + 1] = xn2;
+    if (lane == 0) acc[pair][CGS_MAXM] = wn2, acc[pair][CGS_MAXM + 1] = xn2;
   }
+}
+
+__global__ void __launch_bounds__(CGS_THREADS)
+cgs_update_pair_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
+                       const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
+                       const double* __restrict__ e, const double* __restrict__ state,
+                       const double* __restrict__ flag, int64_t n, double* __restrict__ vnew,
+                       double* __restrict__ x, double* __restrict__ part) {
+  BAMG_PDL_PROLOGUE();
+  constexpr int MAXM = 64, PAIRS = CGS_WARPS / 2;
+  __shared__ const double* sp[MAXM];
+  __shared__ double sc[MAXM], sy[MAXM];
+  __shared__ double acc[PAIRS][CGS_MAXM + 2];
+  __shared__ double xt[PAIRS][32], xu[PAIRS][32], xw[PAIRS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pair = wid >> 1, half = wid & 1;
+  for (int g = threadIdx.x; g < MAXM; g += blockDim.x) {
+    sc[g] = g < m ? c[g] : 0.0;
+    sy[g] = g < m ? y[g] : 0.0;
+  }
+  cgs_load_ptrs<MAXM>(Vp, m, sp);
+  const bool unsafe = flag[0] == 2.0;
+  const bool happy = state[0] != 0.0;
+  const double inv = 1.0 / state[1];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
+  // the upper half holds vectors [32, m): the slots it loads are the next multiple of 8 (the
+  // branch is uniform per warp; both halves run the same trips and barriers)
+  const int mh = half == 0 ? 32 : m - 32;
+  if (mh <= 8)
+    cgs_pair_body<8>(sp, sc, sy, acc, xt, xu, xw, m, w, x0, e, unsafe, happy, inv, r0, r1, vnew, x, lane, pair, half, PAIRS);
+  else if (mh <= 16)
+    cgs_pair_body<16>(sp, sc, sy, acc, xt, xu, xw, m, w, x0, e, unsafe, happy, inv, r0, r1, vnew, x, lane, pair, half, PAIRS);
+  else if (mh <= 24)
+    cgs_pair_body<24>(sp, sc, sy, acc, xt, xu, xw, m, w, x0, e, unsafe, happy, inv, r0, r1, vnew, x, lane, pair, half, PAIRS);
+  else
+    cgs_pair_body<32>(sp, sc, sy, acc, xt, xu, xw, m, w, x0, e, unsafe, happy, inv, r0, r1, vnew, x, lane, pair, half, PAIRS);
   __syncthreads();
   const int nslots = m + 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
-    const int slot = q >= m ? MAXM + (q - m) : q;
+    const int slot = q >= m ? CGS_MAXM + (q - m) : q;
     double t = 0.0;
     for (int p = 0; p < PAIRS; ++p) t += acc[p][slot];
     part[(int64_t)blockIdx.x * (m + 2) + q] = t;
   }
+}
+
+typedef void (*cgs_update_fn)(const double* const*, int, const double*, const double*, const double*, const double*,
+                              const double*, const double*, const double*, int64_t, double*, double*, double*);
+static bool cgs_pair_enabled();
+static cgs_update_fn cgs_update_select(int m) {
+  if (m <= 8) return cgs_update_kernel<32, 8>;
+  if (m <= 16) return cgs_update_kernel<32, 16>;
+  if (m <= 24) return cgs_update_kernel<32, 24>;
+  if (m <= 32) return cgs_update_kernel<32, 32>;
+  return cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64, 64>;
 }
 
 // (flag 2 only) the explicit norm |w - V c|^2 = gs[m] for the Givens step
@@ -1398,7 +1489,7 @@ extern "C" int bamg_gmres(bamg_ctx* ctx, const bamg_csr* B, bamg_hier* h, const 
         const int mj = j + 1;
         if (j == 0) BAMG_LAUNCH(ctx, cgs_gram_init_kernel, 1, 256, 0, gram);
         auto dots = cgs_dots_kernel<32, 0>;
-        auto upd = mj <= 32 ? cgs_update_kernel<32> : (cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64>);
+        auto upd = cgs_update_select(mj);
         // pass A in vector groups of 32 (one wave in total); the update pass keeps whole rows
         const int groups = (mj + 31) / 32;
         const int cbd = std::max(1, cgs_grid(ctx, (const void*)dots, n) / groups);
@@ -1751,7 +1842,7 @@ extern "C" int bamg_cgs_update(bamg_ctx* ctx, const double* const* Vp, int m, co
   BAMG_TRY(arena_get(ctx, (size_t)CGS_MAX_BLOCKS * (CGS_MAXM + 2), &part));
   BAMG_TRY(arena_get(ctx, 4, &st));
   BAMG_LAUNCH(ctx, cgs_set_state_kernel, 1, 1, 0, st, st + 2, happy ? 1.0 : 0.0, 1.0 / inv_norm, 0.0);
-  auto upd = m <= 32 ? cgs_update_kernel<32> : (cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64>);
+  auto upd = cgs_update_select(m);
   const int cb = cgs_grid(ctx, (const void*)upd, n);
   BAMG_LAUNCH_FAM(ctx, FAM_ORTHO, 8.0 * (m + 5) * n, upd, cb, CGS_THREADS, 0, Vp, m, c, y, w, x0, e,
                   (const double*)st, (const double*)(st + 2), n, vnew, x, part);
