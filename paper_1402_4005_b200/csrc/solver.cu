@@ -565,6 +565,16 @@ constexpr int CGS_THREADS = 128;
 constexpr int CGS_WARPS = CGS_THREADS / 32;
 constexpr int CGS_MAX_BLOCKS = 32 * 148;  // partial-sum slots per CTA: CGS_MAXM + 1
 
+// rows per CTA chunk, a multiple of 32: with the 256-byte aligned basis vectors every warp load
+// (32 consecutive doubles) then covers exactly two whole 128-byte lines.  Unaligned chunks made
+// each load straddle a line shared with the neighbouring warp's, and under the evict-first
+// streaming loads that line was fetched from DRAM twice: ncu showed the passes at the DRAM peak
+// (6.0-6.6 TB/s) while reading 1.15-1.22x their algorithmic bytes at m = 32 ... 60.
+__device__ __forceinline__ int64_t cgs_chunk_rows(int64_t n, int nblk) {
+  const int64_t per = (n + nblk - 1) / nblk;
+  return (per + 31) & ~(int64_t)31;
+}
+
 template <int MAXM>
 __device__ __forceinline__ void cgs_load_ptrs(const double* const* __restrict__ Vp, int m, const double** sp) {
   // slots past m alias V_0 (their coefficients are zero): the loads stay
@@ -708,7 +718,7 @@ cgs_dots_kernel(const double* const* __restrict__ Vp, int m_all, const double* _
   if (MODE == 1)
     for (int g = threadIdx.x; g < MAXM; g += blockDim.x) sc[g] = g < m ? c[g] : 0.0;
   cgs_load_ptrs<MAXM>(Vp, m, sp);
-  const int64_t per = (n + nblk - 1) / nblk;
+  const int64_t per = cgs_chunk_rows(n, nblk);
   const int64_t r0 = (int64_t)bx * per, r1 = min(r0 + per, n);
   if (MAXM == 32 && m <= 8) cgs_dots_body<8, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
   else if (MAXM == 32 && m <= 16) cgs_dots_body<16, MODE>(sp, sc, acc, m, w, r0, r1, lane, wid);
@@ -818,7 +828,7 @@ cgs_final_kernel(const double* const* __restrict__ Vp, int m, const double* __re
   const bool unsafe = flag[0] == 2.0;
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t per = cgs_chunk_rows(n, gridDim.x);
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
   double nrm = 0.0;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += CGS_THREADS) {
@@ -990,7 +1000,7 @@ cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __r
   const bool unsafe = flag[0] == 2.0;
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t per = cgs_chunk_rows(n, gridDim.x);
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
   // NS = the slots a thread loads: the next multiple of 8 above m (see cgs_dots_body); one kernel
   // per NS, so the short passes keep their own (small) register count and occupancy
@@ -1092,7 +1102,7 @@ cgs_update_pair_kernel(const double* const* __restrict__ Vp, int m, const double
   const bool unsafe = flag[0] == 2.0;
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t per = cgs_chunk_rows(n, gridDim.x);
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
   // the upper half holds vectors [32, m): the slots it loads are the next multiple of 8 (the
   // branch is uniform per warp; both halves run the same trips and barriers)
@@ -1216,7 +1226,7 @@ cgs_fix_x_kernel(const double* const* __restrict__ Vp, int m, const double* __re
   __shared__ double red[8];
   const bool happy = state[0] != 0.0;
   const double inv = 1.0 / state[1];
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t per = cgs_chunk_rows(n, gridDim.x);
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(r0 + per, n);
   double nrm = 0.0;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {

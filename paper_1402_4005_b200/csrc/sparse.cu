@@ -711,6 +711,15 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A);
 // Masses M, N (nullable = identity): u.(M u) and v.(N v) from their rows in
 // the same pass (the coarse levels' inhomogeneous sweeps), without writing
 // M U, N V, A V.
+// the stencil row in the kernel's parameter space (constant bank operands)
+struct StencilArgs {
+  const uint8_t* tiles;
+  int w;
+  int delta[8];
+  double val[8];
+  double d, rd;
+};
+
 struct MassRows {
   const int32_t* mrp;
   const int32_t* mcol;
@@ -725,15 +734,21 @@ struct MassRows {
 #ifndef BAMG_RQ_MASS_MINB
 #define BAMG_RQ_MASS_MINB 4
 #endif
+// identity masses: 5 CTAs per SM (48 registers) since the stencil path (6 spilled at 40)
+#ifndef BAMG_RQ_MINB
+#define BAMG_RQ_MINB 5
+#endif
 template <int K, int G, int U, bool MASS>
-__global__ void __launch_bounds__(TILE_THREADS, MASS ? BAMG_RQ_MASS_MINB : 6)
+__global__ void __launch_bounds__(TILE_THREADS, MASS ? BAMG_RQ_MASS_MINB : BAMG_RQ_MINB)
 rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                       const double* __restrict__ val, const double* __restrict__ Vv, const double* __restrict__ Uv,
                       double* __restrict__ partial, unsigned int* __restrict__ counter, double* __restrict__ dots,
-                      double* __restrict__ sigma, double* __restrict__ flip, int mode, MassRows ms) {
+                      double* __restrict__ sigma, double* __restrict__ flip, int mode, MassRows ms,
+                      const __grid_constant__ StencilArgs st) {
   BAMG_PDL_PROLOGUE();
   constexpr int VV = K / G;
   constexpr int RB = TILE_THREADS / G;
+  constexpr bool STENCIL_OK = 256 % RB == 0;  // a row tile lies inside one 256-row stencil tile
   __shared__ double sv[3][TILE_THREADS][VV];
   __shared__ bool last;
   const int lr = threadIdx.x / G;
@@ -748,24 +763,46 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
       double acc[VV];
 #pragma unroll
       for (int q = 0; q < VV; ++q) acc[q] = 0.0;
-      const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
-      for (int j = jb; j < je; j += U) {
-        int cc[U];
-        double aa[U];
+      if (STENCIL_OK && st.tiles && st.tiles[(tile * RB) >> 8]) {
+        // stencil tile (bamg_csr_stencil): offsets and values from the parameter space, the
+        // same products in the same order
+        const double* xr = Vv + (int64_t)row * K + voff;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int jj = j + u < je ? j + u : je - 1;
-          cc[u] = __ldg(col + jj);
-          aa[u] = __ldg(val + jj);
+        for (int u0 = 0; u0 < 8; u0 += 4) {
+          if (u0 < st.w) {
+            double xv[4][VV];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u0 + u < st.w) VecIO<VV>::load(xr + (int64_t)st.delta[u0 + u] * K, xv[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (u0 + u < st.w) {
+#pragma unroll
+                for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(st.val[u0 + u], xv[u][q]));
+              }
+            }
+          }
         }
-        double xv[U][VV];
+      } else {
+        const int jb = __ldg(rowptr + row), je = __ldg(rowptr + row + 1);
+        for (int j = jb; j < je; j += U) {
+          int cc[U];
+          double aa[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) VecIO<VV>::load(Vv + (int64_t)cc[u] * K + voff, xv[u]);
+          for (int u = 0; u < U; ++u) {
+            const int jj = j + u < je ? j + u : je - 1;
+            cc[u] = __ldg(col + jj);
+            aa[u] = __ldg(val + jj);
+          }
+          double xv[U][VV];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (j + u < je) {
+          for (int u = 0; u < U; ++u) VecIO<VV>::load(Vv + (int64_t)cc[u] * K + voff, xv[u]);
 #pragma unroll
-            for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+          for (int u = 0; u < U; ++u) {
+            if (j + u < je) {
+#pragma unroll
+              for (int q = 0; q < VV; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(aa[u], xv[u][q]));
+            }
           }
         }
       }
@@ -857,7 +894,7 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   // HBM bandwidth, long-scoreboard bound; 107 -> 84 us at cfg1's level 0).
   // Two row tiles in flight per thread (48 registers, 5 CTAs per SM) measured
   // no faster.
-  constexpr int RQ_BLOCKS = 6 * 148;
+  constexpr int RQ_BLOCKS = BAMG_RQ_MINB * 148;
   const int rb_rows = TILE_THREADS / 8;  // rows per tile at the widest G
   int nblk = (A->nrows + 4 * rb_rows - 1) / (4 * rb_rows);
   // the mass variant holds BAMG_RQ_MASS_MINB CTAs per SM (76 registers): its own one-wave cap
@@ -867,6 +904,19 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
   BAMG_TRY(arena_get(ctx, (size_t)RQ_BLOCKS * 3 * k, &partial));
   const double n = A->nrows;
   double bytes = 4.0 * (n + 1) + 12.0 * (double)A->nnz + 8.0 * k * A->ncols + 8.0 * k * n;
+  StencilArgs st{};
+  {
+    const char* e = getenv("BAMG_NO_STENCIL");
+    if (A->ptiles && A->st_w >= 1 && A->st_w <= 8 && !(e && e[0] == '1')) {
+      st.tiles = A->ptiles;
+      st.w = A->st_w;
+      for (int u = 0; u < 8; ++u) st.delta[u] = A->st_delta[u], st.val[u] = A->st_val[u];
+      st.d = A->st_d;
+      st.rd = A->st_rd;
+      // flagged tiles read no operator
+      bytes -= (256.0 * (double)A->st_tiles / n) * (4.0 * (n + 1) + 12.0 * (double)A->nnz);
+    }
+  }
   MassRows ms{};
   if (M) {
     ms.mrp = M->rowptr, ms.mcol = M->col, ms.mval = M->val;
@@ -882,11 +932,11 @@ int rayleigh_fused_dev(bamg_ctx* ctx, const bamg_csr* A, const double* U, const 
     if (M || N)                                                                                              \
       BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                           \
                       (rayleigh_fused_kernel<KK, GG, UU, true>), nblk, TILE_THREADS, 0, A->nrows, A->rowptr,  \
-                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms);         \
+                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms, st);     \
     else                                                                                                     \
       BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                           \
                       (rayleigh_fused_kernel<KK, GG, UU, false>), nblk, TILE_THREADS, 0, A->nrows, A->rowptr, \
-                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms);         \
+                      A->col, A->val, V, U, partial, ctx->counters + 2, dots, sigma, flip, mode, ms, st);     \
     return 0;
     BAMG_RQ_CASE(1, 1, BAMG_U1)
     BAMG_RQ_CASE(2, 1, 4)
@@ -912,15 +962,6 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A) {
 }
 
 static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double* X, double* Y, const EpiArgs& ea);
-
-// the stencil row in the kernel's parameter space (constant bank operands)
-struct StencilArgs {
-  const uint8_t* tiles;
-  int w;
-  int delta[8];
-  double val[8];
-  double d, rd;
-};
 
 // k-wide sweeps of a lattice operator with stencil tiles (bamg_csr_stencil).  csr_rows_kernel's
 // per-row chain is rowptr -> col / val -> gathers -> epilogue operands; in a flagged 256-row tile

@@ -21,6 +21,6 @@ echo "cgs full rc=$?"
 BAMG_NO_GRAPHS=1 ncu --set full --import-source on --clock-control none -k regex:"csr_rows_packed_kernel" -s 200 -c 3 \
     -o gpurun_out/csr_packed_full -f python tools/steptimes.py --config cfg4 --steps 1 > gpurun_out/csr_packed_full.log 2>&1
 echo "packed full rc=$?"
-ncu --set full --import-source on --clock-control none -k regex:"csr_rows_pipe_kernel|csr_rows_kernel<1, 16|csr_rows_kernel<\(int\)1, \(int\)16" -c 3 \
+ncu --set full --import-source on --clock-control none -k regex:"csr_rows_stencil_kernel" -c 3 \
     -o gpurun_out/csr_k16_full -f python tools/steptimes.py --config cfg4 --steps 1 > gpurun_out/csr_k16_full.log 2>&1
 echo "k16 full rc=$?"
