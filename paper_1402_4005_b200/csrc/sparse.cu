@@ -1633,50 +1633,10 @@ constexpr int PACKED_U = BAMG_PACKED_U;
 // contiguous 128-byte line (row-major words cost 5-6 lines per load: the kernel sat at 69 % of
 // the L1 pipe and 49 % of DRAM).  Same sums, in the same order, as csr_rows_kernel<EPI, 1, 1, U>.
 template <int EPI, int U>
-__global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
-csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
-                       const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
-                       EpiArgs ea, const __grid_constant__ StencilArgs st) {
-  BAMG_PDL_PROLOGUE();
-  if (st.tiles && st.tiles[blockIdx.x]) {
-    // stencil tile (TILE_THREADS = 256 rows, all valid, all carrying the stencil row): no packed
-    // words, no dictionary -- offsets and values are constant-bank operands
-    const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
-    double eb = 0.0;
-    bool sk = false;
-    if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
-    if (EPI == EPI_JACOBI) {
-      if (ea.b) eb = __ldg(ea.b + row);
-      sk = ea.skip[row] != 0;
-    }
-    const double* xr = X + row;
-    double xv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < st.w) xv[u] = __ldg(xr + st.delta[u]);
-    double acc = 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < st.w) acc = __dadd_rn(acc, __dmul_rn(st.val[u], xv[u]));
-    double out;
-    if (EPI == EPI_PLAIN) {
-      out = acc;
-    } else if (EPI == EPI_RESID) {
-      out = __dsub_rn(eb, acc);
-    } else {
-      const double exo = __ldg(ea.xold + row);
-      const double num = __dmul_rn(ea.omega, __dsub_rn(eb, acc));
-      const double upd = sk ? 0.0 : div_rn_recip(num, st.d, st.rd);
-      out = __dadd_rn(exo, upd);
-    }
-    Y[row] = out;
-    return;
-  }
-  __shared__ double s_dict[2 * PACK_DICT];
-  for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
-  __syncthreads();
-  const int row = blockIdx.x * TILE_THREADS + threadIdx.x;
-  const int slice = row >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void packed_row(int nrows, int row, int lane, const int32_t* __restrict__ pslice,
+                                           const uint32_t* __restrict__ pk, const double* s_dict,
+                                           const double* __restrict__ X, double* __restrict__ Y, const EpiArgs& ea) {
+  const int slice = row >> 5;
   if (slice * 32 >= nrows) return;
   const bool valid = row < nrows;
   const int base = __ldg(pslice + slice);
@@ -1729,6 +1689,78 @@ csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint
   Y[row] = out;
 }
 
+template <int EPI, int U>
+__global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
+csr_rows_packed_kernel(int nrows, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
+                       const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
+                       EpiArgs ea) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double s_dict[2 * PACK_DICT];
+  for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
+  __syncthreads();
+  packed_row<EPI, U>(nrows, blockIdx.x * TILE_THREADS + threadIdx.x, threadIdx.x & 31, pslice, pk, s_dict, X, Y, ea);
+}
+
+// The packed operator of a lattice chain with stencil tiles (bamg_csr_stencil): persistent CTAs
+// stride over the 256-row tiles.  A flagged tile reads no packed words and no dictionary: its
+// rows' offsets and values are constant-bank operands, so a row is one round of loads (gathers,
+// right-hand side, skip flag) and ~60 instructions; the next tile's flag is fetched one tile
+// ahead, so no load waits on it.  (With one CTA per tile every CTA paid flag -> gathers -> store
+// as a dependent chain, and the predicated 8-slot form issued 144 instructions per row: ncu had
+// the sweep issue-bound at 31 % of the DRAM peak.)  Tiles that cross a lattice boundary take the
+// packed words.  SW = the stencil's entry count at compile time (4, 5; 8 = any count up to 8).
+template <int EPI, int U, int SW>
+__global__ void __launch_bounds__(TILE_THREADS, BAMG_PACKED_MINB)
+csr_rows_stencil1_kernel(int nrows, int ntiles, const int32_t* __restrict__ pslice, const uint32_t* __restrict__ pk,
+                         const double* __restrict__ dict, const double* __restrict__ X, double* __restrict__ Y,
+                         EpiArgs ea, const __grid_constant__ StencilArgs st) {
+  BAMG_PDL_PROLOGUE();
+  __shared__ double s_dict[2 * PACK_DICT];
+  for (int i = threadIdx.x; i < 2 * PACK_DICT; i += TILE_THREADS) s_dict[i] = dict[i];
+  __syncthreads();
+  int tile = blockIdx.x;
+  unsigned char f = tile < ntiles ? st.tiles[tile] : 0;
+  while (tile < ntiles) {
+    const int tn = tile + gridDim.x;
+    const unsigned char fn = tn < ntiles ? st.tiles[tn] : 0;
+    const int row = tile * TILE_THREADS + threadIdx.x;
+    if (f) {
+      double eb = 0.0, exo = 0.0;
+      bool sk = false;
+      if (EPI == EPI_RESID) eb = __ldg(ea.b + row);
+      if (EPI == EPI_JACOBI) {
+        if (ea.b) eb = __ldg(ea.b + row);
+        exo = __ldg(ea.xold + row);
+        sk = ea.skip[row] != 0;
+      }
+      const double* xr = X + row;
+      double xv[SW];
+#pragma unroll
+      for (int u = 0; u < SW; ++u)
+        if (SW < 8 || u < st.w) xv[u] = __ldg(xr + st.delta[u]);
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < SW; ++u)
+        if (SW < 8 || u < st.w) acc = __dadd_rn(acc, __dmul_rn(st.val[u], xv[u]));
+      double out;
+      if (EPI == EPI_PLAIN) {
+        out = acc;
+      } else if (EPI == EPI_RESID) {
+        out = __dsub_rn(eb, acc);
+      } else {
+        const double num = __dmul_rn(ea.omega, __dsub_rn(eb, acc));
+        const double upd = sk ? 0.0 : div_rn_recip(num, st.d, st.rd);
+        out = __dadd_rn(exo, upd);
+      }
+      Y[row] = out;
+    } else {
+      packed_row<EPI, U>(nrows, row, threadIdx.x & 31, pslice, pk, s_dict, X, Y, ea);
+    }
+    tile = tn;
+    f = fn;
+  }
+}
+
 // the bytes the packed kernels move (what the profiler's family figures use)
 static double packed_bytes(int epi, const bamg_csr* A, const EpiArgs& ea) {
   const double n = A->nrows;
@@ -1769,19 +1801,27 @@ static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double
     st.d = A->st_d;
     st.rd = A->st_rd;
   }
+  const int ntiles = grid;
+  const int pgrid = ntiles < ctx->num_sms * BAMG_PACKED_MINB ? ntiles : ctx->num_sms * BAMG_PACKED_MINB;
+#define BAMG_STENCIL1_LAUNCH(EE, SWV)                                                                          \
+  BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_stencil1_kernel<EE, PACKED_U, SWV>), pgrid, TILE_THREADS, 0,       \
+                  A->nrows, ntiles, A->pslice, A->packed, A->dict, X, Y, ea, st)
+#define BAMG_PACKED_EPI(EE)                                                                                     \
+  do {                                                                                                          \
+    if (!st.tiles)                                                                                              \
+      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EE, PACKED_U>), grid, TILE_THREADS, 0, A->nrows, \
+                      A->pslice, A->packed, A->dict, X, Y, ea);                                                 \
+    else if (st.w == 4) BAMG_STENCIL1_LAUNCH(EE, 4);                                                            \
+    else if (st.w == 5) BAMG_STENCIL1_LAUNCH(EE, 5);                                                            \
+    else BAMG_STENCIL1_LAUNCH(EE, 8);                                                                           \
+  } while (0)
   switch (epi) {
-    case EPI_PLAIN:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_PLAIN, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea, st);
-      break;
-    case EPI_RESID:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_RESID, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea, st);
-      break;
-    default:
-      BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_packed_kernel<EPI_JACOBI, PACKED_U>), grid, TILE_THREADS, 0, A->nrows,
-                      A->pslice, A->packed, A->dict, X, Y, ea, st);
+    case EPI_PLAIN: BAMG_PACKED_EPI(EPI_PLAIN); break;
+    case EPI_RESID: BAMG_PACKED_EPI(EPI_RESID); break;
+    default: BAMG_PACKED_EPI(EPI_JACOBI);
   }
+#undef BAMG_PACKED_EPI
+#undef BAMG_STENCIL1_LAUNCH
   return 0;
 }
 
