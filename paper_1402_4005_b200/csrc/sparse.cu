@@ -714,7 +714,7 @@ static int check_csr(bamg_ctx* ctx, const bamg_csr* A);
 // the stencil row in the kernel's parameter space (constant bank operands)
 struct StencilArgs {
   const uint8_t* tiles;
-  int w;
+  int w, diag;
   int delta[8];
   double val[8];
   double d, rd;
@@ -757,13 +757,19 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
   double s0[VV], s1[VV], s2[VV];
 #pragma unroll
   for (int q = 0; q < VV; ++q) s0[q] = s1[q] = s2[q] = 0.0;
+  // stencil flag of a row tile, fetched one tile ahead (no load of the tile waits on it)
+  unsigned char fnext = 0;
+  if (STENCIL_OK && st.tiles && blockIdx.x * RB < nrows) fnext = st.tiles[(blockIdx.x * RB) >> 8];
   for (int tile = blockIdx.x; tile * RB < nrows; tile += gridDim.x) {
     const int row = tile * RB + lr;
+    const unsigned char sten = fnext;
+    if (STENCIL_OK && st.tiles && (tile + (int)gridDim.x) * RB < nrows)
+      fnext = st.tiles[((tile + (int)gridDim.x) * RB) >> 8];
     if (row < nrows) {
       double acc[VV];
 #pragma unroll
       for (int q = 0; q < VV; ++q) acc[q] = 0.0;
-      if (STENCIL_OK && st.tiles && st.tiles[(tile * RB) >> 8]) {
+      if (STENCIL_OK && sten) {
         // stencil tile (bamg_csr_stencil): offsets and values from the parameter space, the
         // same products in the same order
         const double* xr = Vv + (int64_t)row * K + voff;
@@ -967,13 +973,14 @@ static int launch_packed(bamg_ctx* ctx, int epi, const bamg_csr* A, const double
 // per-row chain is rowptr -> col / val -> gathers -> epilogue operands; in a flagged 256-row tile
 // every row's offsets and values are the kernel's constant-bank operands, so a row is ONE round of
 // loads: its W gathers, its right-hand side and its skip flag, all issued together, and the tile
-// reads neither rowptr / col / val nor d / 1/d.  Persistent CTAs stride over the tiles (one
+// reads neither rowptr / col / val nor d / 1/d (W = the stencil's entry count at compile time, 8 = any
+// count up to 8; the tile flag is fetched one tile ahead).  Persistent CTAs stride over the tiles (one
 // atomic per CTA and column for the peak); tiles that cross a lattice boundary take the CSR row
 // code.  Sums in ascending column order per (row, vector): bit-identical to csr_rows_kernel.
 template <int EPI, int V>
 __device__ __forceinline__ void wide_epilogue(const EpiArgs& ea, int K, int row, int voff, const double* acc,
                                               const double* bv_in, bool hasb, bool sk, double dd, double rdd,
-                                              double* pk, double* __restrict__ Y) {
+                                              double* pk, double* __restrict__ Y, const double* xo_in = nullptr) {
   const int64_t base = (int64_t)row * K + voff;
   double out[V];
   if (EPI == EPI_PLAIN) {
@@ -984,7 +991,12 @@ __device__ __forceinline__ void wide_epilogue(const EpiArgs& ea, int K, int row,
     for (int q = 0; q < V; ++q) out[q] = __dsub_rn(bv_in[q], acc[q]);
   } else {
     double xo[V];
-    VecIO<V>::load(ea.xold + base, xo);
+    if (xo_in) {  // the iterate's own row was one of the gathers (the stencil's diagonal entry)
+#pragma unroll
+      for (int q = 0; q < V; ++q) xo[q] = xo_in[q];
+    } else {
+      VecIO<V>::load(ea.xold + base, xo);
+    }
 #pragma unroll
     for (int q = 0; q < V; ++q) {
       double bv = 0.0;
@@ -1075,9 +1087,13 @@ csr_rows_stencil_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowpt
   double pk[V];
 #pragma unroll
   for (int q = 0; q < V; ++q) pk[q] = 0.0;
+  unsigned char fnext = blockIdx.x < ntiles ? st.tiles[blockIdx.x] : 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int r0 = tile * 256 + lr;
-    if (st.tiles[tile]) {
+    // the flag was fetched one tile ahead: no load of this tile waits on it
+    const unsigned char f = fnext;
+    fnext = tile + (int)gridDim.x < ntiles ? st.tiles[tile + gridDim.x] : 0;
+    if (f) {
 #pragma unroll UNR
       for (int p = 0; p < G; ++p) {
         const int row = r0 + p * RB;
@@ -1085,7 +1101,7 @@ csr_rows_stencil_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowpt
         double xv[W][V], bv[V];
 #pragma unroll
         for (int u = 0; u < W; ++u)
-          if (u < st.w) VecIO<V>::load(xr + (int64_t)st.delta[u] * K, xv[u]);
+          if (W < 8 || u < st.w) VecIO<V>::load(xr + (int64_t)st.delta[u] * K, xv[u]);
         bool sk = false;
         if (hasb) VecIO<V>::load(ea.b + (int64_t)row * K + voff, bv);
         if (EPI == EPI_JACOBI) sk = ea.skip[row] != 0;
@@ -1094,7 +1110,7 @@ csr_rows_stencil_kernel(int nrows, int ntiles, const int32_t* __restrict__ rowpt
         for (int q = 0; q < V; ++q) acc[q] = 0.0;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
-          if (u < st.w) {
+          if (W < 8 || u < st.w) {
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(st.val[u], xv[u][q]));
           }
@@ -1155,6 +1171,7 @@ static int launch_stencil(bamg_ctx* ctx, int epi, const bamg_csr* A, const doubl
   StencilArgs st{};
   st.tiles = A->ptiles;
   st.w = A->st_w;
+  st.diag = A->st_diag;
   for (int u = 0; u < 8; ++u) st.delta[u] = A->st_delta[u], st.val[u] = A->st_val[u];
   st.d = A->st_d;
   st.rd = A->st_rd;
@@ -1170,7 +1187,7 @@ static int launch_stencil(bamg_ctx* ctx, int epi, const bamg_csr* A, const doubl
     cmb = a, cun = b;
   }
 #define BAMG_STENCIL_CASE(EE, KK, GG, WW, MB, UN)                                                              \
-  if (epi == EE && k == KK && A->st_w <= WW && cmb == MB && cun == UN) {                                      \
+  if (epi == EE && k == KK && (WW == 8 ? A->st_w <= 8 : A->st_w == WW) && cmb == MB && cun == UN) {           \
     const int g = ntiles < ctx->num_sms * MB ? ntiles : ctx->num_sms * MB;                                    \
     BAMG_LAUNCH_FAM(ctx, fam, bytes, (csr_rows_stencil_kernel<EE, KK, GG, WW, MB, UN>), g, TILE_THREADS, 0,    \
                     A->nrows, ntiles, A->rowptr, A->col, A->val, X, Y, ea, st);                               \
