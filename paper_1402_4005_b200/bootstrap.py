@@ -558,6 +558,9 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     eye = DeviceCSR.identity(n)
     geometry = problem.geometry
     if geometry is not None and not isinstance(geometry, AxisRanks):
+        ready = getattr(problem, "geometry_ready", None)
+        if ready is not None:  # the coordinates were copied in on a side stream
+            torch.cuda.current_stream().wait_event(ready)
         with _phase("axis_ranks"):
             geometry = AxisRanks.from_geometry(geometry)
     hierarchy = None

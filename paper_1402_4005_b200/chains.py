@@ -35,6 +35,10 @@ class ChainProblem:
     params: dict
     geometry: np.ndarray | None = None
     seed: int | None = None
+    # optional torch.cuda.Event: a device `geometry` tensor still being copied in on another
+    # stream is ready once it has fired (run_setup waits on it right before the first split,
+    # so the upload overlaps the initial relaxation)
+    geometry_ready: object = None
 
 
 def _finish(A, family, params, geometry=None, seed=None, validate=True) -> ChainProblem:

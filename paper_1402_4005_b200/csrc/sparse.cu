@@ -675,6 +675,35 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
     BAMG_ROWS16(2, 2, 3)
 #undef BAMG_ROWS16
   }
+  if (k == 1 && (EPI == EPI_JACOBI || EPI == EPI_RESID || EPI == EPI_PLAIN) && A->nnz > 5 * (int64_t)A->nrows) {
+    // Galerkin levels of the V-cycle (7-9 entries per row): the whole row in one round of U = 8
+    // gathers and the Jacobi operands issued beside the row extents -- three dependent memory
+    // latencies per row (extents -> col / val -> gathers) instead of five.
+    // BAMG_K1W = "U:MB:EARLY" (development), "0" = off
+    static int wu = -1, wmb = 0, wearly = 0;
+    if (wu < 0) {
+      int a = 8, b = 5, c = 1;
+      const char* e = getenv("BAMG_K1W");
+      if (e && e[0] == '0' && e[1] == 0) a = 0;
+      else if (!(e && sscanf(e, "%d:%d:%d", &a, &b, &c) == 3)) a = 8, b = 5, c = 1;
+      wu = a, wmb = b, wearly = c;
+    }
+    const int g = (A->nrows + TILE_THREADS - 1) / TILE_THREADS;
+#define BAMG_K1W_CASE(UU, MM, EE)                                                                          \
+  if (wu == UU && wmb == MM && wearly == EE) {                                                             \
+    BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,                          \
+                    (csr_rows_kernel<EPI, 1, 1, UU, false, MM, EE != 0>), g, TILE_THREADS, 0, A->nrows,    \
+                    A->rowptr, A->col, A->val, X, Y, ea);                                                  \
+    return 0;                                                                                              \
+  }
+    BAMG_K1W_CASE(8, 6, 1)
+    BAMG_K1W_CASE(8, 5, 1)
+    BAMG_K1W_CASE(8, 8, 1)
+    BAMG_K1W_CASE(8, 6, 0)
+    BAMG_K1W_CASE(4, 8, 1)
+    BAMG_K1W_CASE(6, 6, 1)
+#undef BAMG_K1W_CASE
+  }
   switch (k) {
 #define BAMG_ROWS_CASE(KK, GG, UU)                                                                         \
   case KK: {                                                                                               \

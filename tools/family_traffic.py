@@ -16,7 +16,7 @@ import re
 import sys
 from collections import defaultdict
 
-FAMILIES = {"csr_stream_spmv_spmm_jacobi": r"csr_rows_kernel|csr_rows_pipe_kernel|csr_rows_packed_kernel|csr_rows_stencil_kernel|rayleigh_fused_kernel",
+FAMILIES = {"csr_stream_spmv_spmm_jacobi": r"csr_rows_kernel|csr_rows_pipe_kernel|csr_rows_packed_kernel|csr_rows_stencil_kernel|csr_rows_stencil1_kernel|rayleigh_fused_kernel",
             "gmres_cgs2_basis_passes": r"cgs_dots_kernel|cgs_final_kernel|cgs_update_kernel|cgs_update_pair_kernel"}
 
 path, algp, out = sys.argv[1], sys.argv[2], sys.argv[3]

@@ -18,7 +18,7 @@ ncu --set full --import-source on --clock-control none -k regex:"cgs_dots_kernel
     -o gpurun_out/cgs_gram_full -f python tools/steptimes.py --config cfg4 --steps 1 > gpurun_out/cgs_full.log 2>&1
 echo "cgs full rc=$?"
 # level-0 V-cycle sweeps on the packed operator and the k = 16 smoothing sweep
-BAMG_NO_GRAPHS=1 ncu --set full --import-source on --clock-control none -k regex:"csr_rows_packed_kernel" -s 200 -c 3 \
+BAMG_NO_GRAPHS=1 ncu --set full --import-source on --clock-control none -k regex:"csr_rows_stencil1_kernel|csr_rows_packed_kernel" -s 200 -c 3 \
     -o gpurun_out/csr_packed_full -f python tools/steptimes.py --config cfg4 --steps 1 > gpurun_out/csr_packed_full.log 2>&1
 echo "packed full rc=$?"
 ncu --set full --import-source on --clock-control none -k regex:"csr_rows_stencil_kernel" -c 3 \
