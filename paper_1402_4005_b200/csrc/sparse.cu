@@ -763,9 +763,9 @@ struct MassRows {
 #ifndef BAMG_RQ_MASS_MINB
 #define BAMG_RQ_MASS_MINB 4
 #endif
-// identity masses: 5 CTAs per SM (48 registers) since the stencil path (6 spilled at 40)
+// identity masses: 4 CTAs per SM (64 registers) since the stencil path and the early u / v loads
 #ifndef BAMG_RQ_MINB
-#define BAMG_RQ_MINB 5
+#define BAMG_RQ_MINB 4
 #endif
 template <int K, int G, int U, bool MASS>
 __global__ void __launch_bounds__(TILE_THREADS, MASS ? BAMG_RQ_MASS_MINB : BAMG_RQ_MINB)
@@ -795,6 +795,14 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
     if (STENCIL_OK && st.tiles && (tile + (int)gridDim.x) * RB < nrows)
       fnext = st.tiles[((tile + (int)gridDim.x) * RB) >> 8];
     if (row < nrows) {
+      // the row's own u and v segments depend on the row only: issued before the gathers, so the
+      // row costs one round of memory latency (they used to follow the sums: two rounds)
+      // (identity masses only: the mass variant is short of registers and loads them after the sums)
+      double uu[VV], vv[VV];
+      if (!MASS) {
+        VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
+        VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
+      }
       double acc[VV];
 #pragma unroll
       for (int q = 0; q < VV; ++q) acc[q] = 0.0;
@@ -841,9 +849,10 @@ rayleigh_fused_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32
           }
         }
       }
-      double uu[VV], vv[VV];
-      VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
-      VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
+      if (MASS) {
+        VecIO<VV>::load(Uv + (int64_t)row * K + voff, uu);
+        VecIO<VV>::load(Vv + (int64_t)row * K + voff, vv);
+      }
       double mu[VV], nv[VV];
       if (MASS && ms.mrp) {
         row_apply<K, VV, U>(ms.mrp, ms.mcol, ms.mval, Uv, row, voff, mu);
