@@ -652,42 +652,54 @@ __device__ __forceinline__ double cgs_fold(const double* v, double s, int lane) 
 // NS = the slots a thread really loads (a multiple of 8, >= the group's m): slots past m alias V_0
 // with zero coefficients, and every aliased load is an L1 hit that still costs an LSU slot -- a
 // group of 5 vectors read through 32 slots spent most of its load issue on them.
+// RU = row sets in flight per thread: a short basis (NS = 8, 16) has too few loads per row to cover the
+// memory latency at the kernel's occupancy (m = 1: 8 KB in flight per SM, 1.1 TB/s), so 32 / NS row
+// sets are loaded before any is folded; the folds follow in row order (the sums are unchanged).
 template <int NS, int MODE>
 __device__ __forceinline__ void cgs_dots_body(const double* const* sp, const double* sc, double (*acc)[CGS_MAXM + 2],
                                               int m, double* __restrict__ w, int64_t r0, int64_t r1, int lane,
                                               int wid) {
   constexpr int NB = (NS + 31) / 32;
+  constexpr int RU = NS <= 8 ? 4 : (NS <= 16 ? 2 : 1);
   double dot[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) dot[q] = 0.0;
   double wn2 = 0.0;
-  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
-    const int64_t i = base + lane;
-    const bool ok = i < r1;
-    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
-    double v[NS];
+  for (int64_t base = r0 + wid * 32; base < r1; base += (int64_t)RU * CGS_THREADS) {
+    double v[RU][NS], wi[RU];
+    bool ok[RU];
 #pragma unroll
-    for (int g = 0; g < NS; ++g) v[g] = __ldcs(sp[g] + ic);
-    double wi = w[ic];
-    if (MODE == 1) {
-      double t = 0.0;
+    for (int r = 0; r < RU; ++r) {
+      const int64_t i = base + (int64_t)r * CGS_THREADS + lane;
+      ok[r] = i < r1;
+      const int64_t ic = ok[r] ? i : r0;  // rows past the chunk read row r0 and contribute 0
 #pragma unroll
-      for (int g = 0; g < NS; ++g) t = fma(sc[g], v[g], t);
-      wi -= t;
-      if (ok) w[i] = wi;
+      for (int g = 0; g < NS; ++g) v[r][g] = __ldcs(sp[g] + ic);
+      wi[r] = w[ic];
     }
-    if (!ok) wi = 0.0;
-    wn2 = fma(wi, wi, wn2);
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (q * 32 >= m) break;
-      if constexpr (NS <= 32) {
-        dot[q] += cgs_fold<NS>(v, wi, lane);
-      } else {
-        double pr[32];
+    for (int r = 0; r < RU; ++r) {
+      if (r > 0 && base + (int64_t)r * CGS_THREADS >= r1) break;  // warp-uniform: no rows left
+      if (MODE == 1) {
+        double t = 0.0;
 #pragma unroll
-        for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * wi;
-        dot[q] += warp_transpose_sum32(pr, lane);
+        for (int g = 0; g < NS; ++g) t = fma(sc[g], v[r][g], t);
+        wi[r] -= t;
+        if (ok[r]) w[base + (int64_t)r * CGS_THREADS + lane] = wi[r];
+      }
+      if (!ok[r]) wi[r] = 0.0;
+      wn2 = fma(wi[r], wi[r], wn2);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        if (q * 32 >= m) break;
+        if constexpr (NS <= 32) {
+          dot[q] += cgs_fold<NS>(v[r], wi[r], lane);
+        } else {
+          double pr[32];
+#pragma unroll
+          for (int g = 0; g < 32; ++g) pr[g] = q * 32 + g < NS ? v[r][q * 32 + g < NS ? q * 32 + g : 0] * wi[r] : 0.0;
+          dot[q] += warp_transpose_sum32(pr, lane);
+        }
       }
     }
   }
@@ -927,49 +939,59 @@ __device__ __forceinline__ void cgs_update_body(const double* const* sp, const d
                                                 bool unsafe, bool happy, double inv, int64_t r0, int64_t r1,
                                                 double* __restrict__ vnew, double* __restrict__ x, int lane, int wid) {
   constexpr int NB = (NS + 31) / 32;
+  constexpr int RU = NS <= 8 ? 4 : (NS <= 16 ? 2 : 1);  // row sets in flight (see cgs_dots_body)
   double dot[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) dot[q] = 0.0;
   double wn2 = 0.0, xn2 = 0.0;
 #pragma unroll 1
-  for (int64_t base = r0 + wid * 32; base < r1; base += CGS_THREADS) {
-    const int64_t i = base + lane;
-    const bool ok = i < r1;
-    const int64_t ic = ok ? i : r0;  // rows past the chunk read row r0 and contribute 0
-    double v[NS];
+  for (int64_t base = r0 + wid * 32; base < r1; base += (int64_t)RU * CGS_THREADS) {
+    double v[RU][NS], wi[RU], x0i[RU], ei[RU];
+    bool ok[RU];
 #pragma unroll
-    for (int g = 0; g < NS; ++g) v[g] = __ldcs(sp[g] + ic);
-    const double wi = w[ic], x0i = x0[ic], ei = e[ic];
-    double t = 0.0, u = 0.0;
+    for (int r = 0; r < RU; ++r) {
+      const int64_t i = base + (int64_t)r * CGS_THREADS + lane;
+      ok[r] = i < r1;
+      const int64_t ic = ok[r] ? i : r0;  // rows past the chunk read row r0 and contribute 0
 #pragma unroll
-    for (int g = 0; g < NS; ++g) {
-      t = fma(sc[g], v[g], t);
-      u = fma(sy[g], v[g], u);
+      for (int g = 0; g < NS; ++g) v[r][g] = __ldcs(sp[g] + ic);
+      wi[r] = w[ic], x0i[r] = x0[ic], ei[r] = e[ic];
     }
-    double ww = wi - t;
-    if (ok) {
-      if (unsafe) {
-        vnew[i] = ww;
-      } else {
-        if (!happy) vnew[i] = ww * inv;
-        const double xi = x0i + (ei + u);
-        x[i] = xi;
-        xn2 = fma(xi, xi, xn2);
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      if (r > 0 && base + (int64_t)r * CGS_THREADS >= r1) break;  // warp-uniform: no rows left
+      const int64_t i = base + (int64_t)r * CGS_THREADS + lane;
+      double t = 0.0, u = 0.0;
+#pragma unroll
+      for (int g = 0; g < NS; ++g) {
+        t = fma(sc[g], v[r][g], t);
+        u = fma(sy[g], v[r][g], u);
       }
-    } else {
-      ww = 0.0;
-    }
-    wn2 = fma(ww, ww, wn2);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (q * 32 >= m) break;
-      if constexpr (NS <= 32) {
-        dot[q] += cgs_fold<NS>(v, ww, lane);
+      double ww = wi[r] - t;
+      if (ok[r]) {
+        if (unsafe) {
+          vnew[i] = ww;
+        } else {
+          if (!happy) vnew[i] = ww * inv;
+          const double xi = x0i[r] + (ei[r] + u);
+          x[i] = xi;
+          xn2 = fma(xi, xi, xn2);
+        }
       } else {
-        double pr[32];
+        ww = 0.0;
+      }
+      wn2 = fma(ww, ww, wn2);
 #pragma unroll
-        for (int g = 0; g < 32; ++g) pr[g] = v[q * 32 + g] * ww;
-        dot[q] += warp_transpose_sum32(pr, lane);
+      for (int q = 0; q < NB; ++q) {
+        if (q * 32 >= m) break;
+        if constexpr (NS <= 32) {
+          dot[q] += cgs_fold<NS>(v[r], ww, lane);
+        } else {
+          double pr[32];
+#pragma unroll
+          for (int g = 0; g < 32; ++g) pr[g] = q * 32 + g < NS ? v[r][q * 32 + g < NS ? q * 32 + g : 0] * ww : 0.0;
+          dot[q] += warp_transpose_sum32(pr, lane);
+        }
       }
     }
   }
@@ -981,7 +1003,7 @@ __device__ __forceinline__ void cgs_update_body(const double* const* sp, const d
 }
 
 template <int MAXM, int NS = MAXM>
-__global__ void __launch_bounds__(CGS_THREADS, (NS <= 8 ? 5 : NS <= 32 ? 4 : 2))
+__global__ void __launch_bounds__(CGS_THREADS, (NS <= 32 ? 4 : NS <= 48 ? 3 : 2))
 cgs_update_kernel(const double* const* __restrict__ Vp, int m, const double* __restrict__ c,
                   const double* __restrict__ y, const double* __restrict__ w, const double* __restrict__ x0,
                   const double* __restrict__ e, const double* __restrict__ state, const double* __restrict__ flag,
@@ -1133,6 +1155,11 @@ static cgs_update_fn cgs_update_select(int m) {
   if (m <= 16) return cgs_update_kernel<32, 16>;
   if (m <= 24) return cgs_update_kernel<32, 24>;
   if (m <= 32) return cgs_update_kernel<32, 32>;
+  // m = 33..48: whole rows per thread through 40 / 48 slots (139 / 154 registers, 3 CTAs per SM, no
+  // pair barriers) beat the warp-pair split, whose upper half idles there; BAMG_CGS_MID=0 disables
+  static const bool mid = !(getenv("BAMG_CGS_MID") && getenv("BAMG_CGS_MID")[0] == '0');
+  if (mid && m <= 40) return cgs_update_kernel<64, 40>;
+  if (mid && m <= 48) return cgs_update_kernel<64, 48>;
   return cgs_pair_enabled() ? cgs_update_pair_kernel : cgs_update_kernel<64, 64>;
 }
 
