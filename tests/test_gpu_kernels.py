@@ -425,6 +425,43 @@ def test_packed_operator_kernels_bitexact(eng, family, side):
         want = orc.sweep(B, x, np.zeros(n) if rhs is None else b, 0.7, dg, orc.skip_rows(B, dg))
         assert np.array_equal(got.cpu().numpy(), want)
 
+@pytest.mark.parametrize("family,side,k", [("tandem", 700, 16), ("uniform2d", 611, 8), ("tandem", 900, 8)])
+def test_stencil_tiles_wide_sweeps_bitexact(eng, family, side, k):
+    """bamg_csr_stencil: the k-wide SpMM / Jacobi sweeps (right-hand side, per-vector scale, peak)
+    and the fused Rayleigh quotients of a lattice operator and of its transpose, taken from the
+    stencil tiles, reproduce the CSR row kernels bit for bit (relax.py:66-83, bootstrap.py:144-153)."""
+    from paper_1402_4005_b200 import chains, engine
+    prob = chains.tandem_queue(side) if family == "tandem" else chains.uniform_2d(side)
+    B = orc.canon(prob.B)
+    n = B.shape[0]
+    for M in (B, orc.canon(B.T)):
+        dS, dP = up(eng, M), up(eng, M)
+        assert engine.attach_stencil(dS) and dS.desc().ptiles and dS.desc().st_w >= 3
+        rng = np.random.default_rng(11)
+        X = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+        Bv = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+        sc = torch.from_numpy(rng.uniform(0.5, 2.0, k)).cuda()
+        assert torch.equal(engine.spmm(dS, X), engine.spmm(dP, X))
+        assert np.array_equal(engine.spmm(dS, X).cpu().numpy(), M @ X.cpu().numpy())
+        d = engine.diag(dP)
+        skip = engine.degenerate_rows(dP, d)
+        for rhs, scale in ((None, None), (Bv, None), (Bv, sc)):
+            pk_s = torch.zeros(k, dtype=torch.float64, device="cuda")
+            pk_p = torch.zeros(k, dtype=torch.float64, device="cuda")
+            got = engine.jacobi(dS, d, skip, X, b=rhs, b_scale=scale, peak=pk_s)
+            want = engine.jacobi(dP, d, skip, X, b=rhs, b_scale=scale, peak=pk_p)
+            assert torch.equal(got, want)
+            assert torch.equal(pk_s, pk_p)
+            assert torch.equal(engine.jacobi(dS, d, skip, X, b=rhs, b_scale=scale),
+                               engine.jacobi(dP, d, skip, X, b=rhs, b_scale=scale))
+        # Rayleigh quotients u.(Av) / (|u| |v|) with identity masses: same partial-sum tree
+        U = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+        sig_s = torch.ones(k, dtype=torch.float64, device="cuda")
+        sig_p = torch.ones(k, dtype=torch.float64, device="cuda")
+        engine.refresh_sigmas(dS, None, None, U, X, sig_s, flip=False)
+        engine.refresh_sigmas(dP, None, None, U, X, sig_p, flip=False)
+        assert torch.equal(sig_s, sig_p)
+
 
 def test_pack_operator_declines_general_values(eng):
     """More than 256 distinct values (any Galerkin operator): not packed, CSR kernels run."""
