@@ -378,17 +378,21 @@ def run_ours(args, rank, world, local_rank):
     copy_stream = torch.cuda.Stream()
 
     def e2e_step():
-        # B first (the setup needs it at once); the coordinates follow on a copy stream and are
-        # first read at the first C/F split, after the initial relaxation (ChainProblem.geometry_ready)
-        rp, ci, va = [t.to("cuda", non_blocking=True) for t in pins[:3]]
-        ready = torch.cuda.Event()
+        # every input goes over a copy stream: B first (ChainProblem.B_ready: the setup draws its
+        # seeded test vectors while it lands), then the coordinates, which are first read at the
+        # first C/F split, after the initial relaxation (ChainProblem.geometry_ready)
+        b_ready, g_ready = torch.cuda.Event(), torch.cuda.Event()
         copy_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(copy_stream):
+            rp, ci, va = [t.to("cuda", non_blocking=True) for t in pins[:3]]
+            b_ready.record(copy_stream)
             ge = pins[3].to("cuda", non_blocking=True)
-            ready.record(copy_stream)
-        ge.record_stream(torch.cuda.current_stream())
+            g_ready.record(copy_stream)
+        for t in (rp, ci, va, ge):
+            t.record_stream(torch.cuda.current_stream())
         B = DeviceCSR(rp, ci, va, Bh.shape)
-        p = ChainProblem(A=None, B=B, n=n, family=fam, params={}, geometry=ge, geometry_ready=ready)
+        p = ChainProblem(A=None, B=B, n=n, family=fam, params={}, geometry=ge, geometry_ready=g_ready,
+                         B_ready=b_ready)
         rep2 = pb.solve_steady_state(p, cfg, gcfg, draws="uniform", to_host=False)
         xout.copy_(rep2.x_device, non_blocking=True)
         torch.cuda.synchronize()

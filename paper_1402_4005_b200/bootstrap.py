@@ -250,6 +250,10 @@ def _mass(M: DeviceCSR):
     return None if M.is_identity else M
 
 
+class _OwnedDraws(tuple):
+    """(right, left) device blocks drawn by run_setup itself: relaxed in place, no defensive copy."""
+
+
 def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps | None = None, comm=None):
     """Smoothed random left/right test vectors; left slot 0 constant (bootstrap.py:180-202).
 
@@ -277,9 +281,11 @@ def init_test_vectors(B, cfg: SetupConfig, rng=None, draws=None, ops: _LevelOps 
     else:
         right_h, left_h = draws
     if isinstance(right_h, torch.Tensor):
-        # device-resident draws, already n x k interleaved; the smoothing works in place
-        V = right_h.clone()
-        U = left_h.clone()
+        # device-resident draws, already n x k interleaved; the smoothing works in place, so a
+        # caller's blocks are copied and the ones drawn here are not
+        own = isinstance(draws, (str, _OwnedDraws))
+        V = right_h if own else right_h.clone()
+        U = left_h if own else left_h.clone()
     else:
         V = engine.to_device_vec(np.ascontiguousarray(np.asarray(right_h, dtype=np.float64).T))
         U = engine.to_device_vec(np.ascontiguousarray(np.asarray(left_h, dtype=np.float64).T))
@@ -539,6 +545,14 @@ def run_setup(problem, cfg: SetupConfig, draws=None, B_device: DeviceCSR | None 
     n = A.shape[0]
     root = np.random.SeedSequence(cfg.seed)
     ss_init, ss_levels = root.spawn(2)
+    if isinstance(draws, str) and draws == "uniform":
+        # the seeded draws need nothing of the operator: generated first, so they overlap an
+        # operator still being copied in (ChainProblem.B_ready)
+        with _phase("draws"):
+            draws = _OwnedDraws(engine.uniform_draws(cfg.seed, cfg.n_tests, n))
+    ready = getattr(problem, "B_ready", None)
+    if ready is not None:  # the operator's arrays were copied in on a side stream
+        torch.cuda.current_stream().wait_event(ready)
     with _phase("level_ops"):
         # the generators' B = I - A has a handful of distinct values: the k = 1
         # sweeps / residuals / SpMVs of the solve stream its packed copy

@@ -39,6 +39,9 @@ class ChainProblem:
     # stream is ready once it has fired (run_setup waits on it right before the first split,
     # so the upload overlaps the initial relaxation)
     geometry_ready: object = None
+    # the same for a device operator B whose arrays are still in flight: run_setup draws the seeded
+    # test vectors first and waits on this event before it first touches B
+    B_ready: object = None
 
 
 def _finish(A, family, params, geometry=None, seed=None, validate=True) -> ChainProblem:

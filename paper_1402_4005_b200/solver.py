@@ -214,6 +214,9 @@ def solve_steady_state(problem, setup_cfg: SetupConfig | None, gmres_cfg: GmresC
     A = as_device(problem.B)
     n = A.shape[0]
     if setup_cfg is None or setup_cfg.setup_cycles == 0:
+        ready = getattr(problem, "B_ready", None)
+        if ready is not None:  # operator arrays copied in on a side stream (run_setup waits itself)
+            torch.cuda.current_stream().wait_event(ready)
         x0 = np.full(n, 1.0 / n)
         t0 = time.perf_counter()
         report = gmres(A, np.zeros(n), x0, gmres_cfg, precond=None)

@@ -1,6 +1,8 @@
-for p in 28 32 36 40 44 48; do
-  echo "== p=$p"
-  BAMG_BAND_P=$p BAMG_DEBUG=1 python tools/breakdown.py --config cfg4 --reps 3 --top 1 > /tmp/bp.out 2> /tmp/bp.err
-  grep -o '"coarsest": [0-9.]*' /tmp/bp.out | tr '\n' ' '; echo
-  grep "band triplets" /tmp/bp.err | tail -1 | cut -c1-200
+#!/bin/bash
+# banded coarsest level: width of the subspace block (BAMG_BAND_P = r + guard), cfg4 setup time
+cd /root/repo
+for p in 32 40 48 56 64; do
+  echo "== BAMG_BAND_P=$p"
+  BAMG_BAND_P=$p python tools/steptimes.py --config cfg4 --steps 4 2>&1 | grep '"step": 3' | cut -c1-140
 done
+BAMG_DEBUG=1 python tools/steptimes.py --config cfg4 --steps 1 2>&1 | grep -i "band\|subspace\|ritz" | head -20
