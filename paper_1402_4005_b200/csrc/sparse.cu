@@ -245,6 +245,7 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
     // instead of after the gathers (one memory latency less per row: the sweep is latency-bound)
     [[maybe_unused]] bool e_sk = false;
     [[maybe_unused]] double e_dd = 1.0, e_rdd = 0.0, e_xo[V], e_b[V];
+    if constexpr (EARLY && EPI == EPI_ADD) VecIO<V>::load(ea.xold + (int64_t)row * K + voff, e_xo);
     if constexpr (EARLY && EPI == EPI_JACOBI) {
       e_sk = ea.skip[row] != 0;
       e_dd = ea.d[row];
@@ -289,7 +290,12 @@ csr_rows_kernel(int nrows, const int32_t* __restrict__ rowptr, const int32_t* __
       for (int q = 0; q < V; ++q) out[q] = __dsub_rn(bv[q], acc[q]);
     } else if (EPI == EPI_ADD) {
       double xo[V];
-      VecIO<V>::load(ea.xold + base, xo);
+      if constexpr (EARLY) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) xo[q] = e_xo[q];
+      } else {
+        VecIO<V>::load(ea.xold + base, xo);
+      }
 #pragma unroll
       for (int q = 0; q < V; ++q) out[q] = __dadd_rn(xo[q], acc[q]);
     } else {
@@ -703,6 +709,18 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
     BAMG_K1W_CASE(4, 8, 1)
     BAMG_K1W_CASE(6, 6, 1)
 #undef BAMG_K1W_CASE
+  }
+  if (k == 1 && EPI == EPI_ADD) {
+    // the V-cycle's prolongation + correction (rows of 1-2 entries): the old iterate issued beside
+    // the row extents (BAMG_K1W=0 disables)
+    static const bool off = getenv("BAMG_K1W") && getenv("BAMG_K1W")[0] == '0' && getenv("BAMG_K1W")[1] == 0;
+    if (!off) {
+      const int g = (A->nrows + TILE_THREADS - 1) / TILE_THREADS;
+      BAMG_LAUNCH_FAM(ctx, A->nrows >= FINE_ROWS ? FAM_TILE_FINE : FAM_TILE, bytes,
+                      (csr_rows_kernel<EPI, 1, 1, 2, false, 8, true>), g, TILE_THREADS, 0, A->nrows, A->rowptr,
+                      A->col, A->val, X, Y, ea);
+      return 0;
+    }
   }
   switch (k) {
 #define BAMG_ROWS_CASE(KK, GG, UU)                                                                         \

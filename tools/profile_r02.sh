@@ -14,7 +14,7 @@ BAMG_NO_GRAPHS=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__t
     > gpurun_out/traffic_cfg4_alg.txt 2>&1
 echo "traffic rc=$?"
 # the two GMRES passes at m ~ 44 (the <32>-group dots and the warp-pair update)
-ncu --set full --import-source on --clock-control none -k regex:"cgs_dots_kernel|cgs_update_pair_kernel" -s 86 -c 2 \
+ncu --set full --import-source on --clock-control none -k regex:"cgs_dots_kernel|cgs_update_pair_kernel" -s 62 -c 2 \
     -o gpurun_out/cgs_gram_full -f python tools/steptimes.py --config cfg4 --steps 1 > gpurun_out/cgs_full.log 2>&1
 echo "cgs full rc=$?"
 # level-0 V-cycle sweeps on the packed operator and the k = 16 smoothing sweep
