@@ -602,14 +602,7 @@ static int launch_rows_pipe(bamg_ctx* ctx, int k, double bytes, const bamg_csr* 
   BAMG_PIPE_CASE(16, 8, 6, 3)
   BAMG_PIPE_CASE(16, 8, 8, 3)
   BAMG_PIPE_CASE(16, 4, 2, 4)
-  BAMG_PIPE_CASE(16, 4, 2, 3)
   BAMG_PIPE_CASE(16, 4, 4, 3)
-  BAMG_PIPE_CASE(16, 4, 1, 4)
-  BAMG_PIPE_CASE(16, 4, 1, 5)
-  BAMG_PIPE_CASE(16, 2, 1, 4)
-  BAMG_PIPE_CASE(16, 2, 1, 3)
-  BAMG_PIPE_CASE(16, 2, 2, 3)
-  BAMG_PIPE_CASE(16, 2, 2, 2)
   BAMG_PIPE_CASE(12, 6, 6, 4)
   BAMG_PIPE_CASE(12, 6, 6, 3)
   BAMG_PIPE_CASE(8, 4, 6, 4)
@@ -669,16 +662,9 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
     return 0;                                                                                              \
   }
     BAMG_ROWS16(8, 4, 8)
-    BAMG_ROWS16(8, 4, 6)
-    BAMG_ROWS16(8, 4, 5)
-    BAMG_ROWS16(8, 6, 5)
     BAMG_ROWS16(4, 4, 4)
-    BAMG_ROWS16(4, 4, 3)
-    BAMG_ROWS16(4, 2, 4)
     BAMG_ROWS16(4, 2, 5)
-    BAMG_ROWS16(4, 3, 4)
     BAMG_ROWS16(2, 2, 4)
-    BAMG_ROWS16(2, 2, 3)
 #undef BAMG_ROWS16
   }
   if (k == 1 && (EPI == EPI_JACOBI || EPI == EPI_RESID || EPI == EPI_PLAIN) && A->nnz > 5 * (int64_t)A->nrows) {
@@ -702,12 +688,9 @@ static int launch_rows(bamg_ctx* ctx, int k, int /*grid*/, double bytes, const b
                     A->rowptr, A->col, A->val, X, Y, ea);                                                  \
     return 0;                                                                                              \
   }
-    BAMG_K1W_CASE(8, 6, 1)
     BAMG_K1W_CASE(8, 5, 1)
-    BAMG_K1W_CASE(8, 8, 1)
+    BAMG_K1W_CASE(8, 6, 1)
     BAMG_K1W_CASE(8, 6, 0)
-    BAMG_K1W_CASE(4, 8, 1)
-    BAMG_K1W_CASE(6, 6, 1)
 #undef BAMG_K1W_CASE
   }
   if (k == 1 && EPI == EPI_ADD) {
@@ -1260,14 +1243,8 @@ static int launch_stencil(bamg_ctx* ctx, int epi, const bamg_csr* A, const doubl
   BAMG_STENCIL_CASE(EPI_JACOBI, KK, GG, 5, MB, UN)    \
   BAMG_STENCIL_CASE(EPI_JACOBI, KK, GG, 8, MB, UN)
   BAMG_STENCIL_K(16, 8, 4, 2)
-  BAMG_STENCIL_K(16, 8, 6, 1)
-  BAMG_STENCIL_K(16, 8, 5, 1)
-  BAMG_STENCIL_K(16, 8, 3, 2)
   BAMG_STENCIL_K(16, 8, 4, 1)
   BAMG_STENCIL_K(8, 4, 4, 2)
-  BAMG_STENCIL_K(8, 4, 6, 1)
-  BAMG_STENCIL_K(8, 4, 5, 1)
-  BAMG_STENCIL_K(8, 4, 3, 2)
   BAMG_STENCIL_K(8, 4, 4, 1)
 #undef BAMG_STENCIL_K
 #undef BAMG_STENCIL_CASE

@@ -3,7 +3,7 @@
 cd /root/repo
 out=gpurun_out/g16_sweep3.txt; : > $out
 for e in 0 1; do
-for g in 8:4:8 8:4:6 8:4:5 8:6:5 4:4:4 4:4:3 4:2:4 4:2:5 4:3:4 2:2:4 2:2:3; do
+for g in 8:4:8 4:4:4 4:2:5 2:2:4; do
   echo "== BAMG_G16=$g EARLY=$e BAMG_ROWS_PIPE=0" >> $out
   BAMG_EARLY=$e BAMG_G16=$g BAMG_ROWS_PIPE=0 python tools/csr_bench.py --configs cfg4 --ks 16 --reps 6 2>&1 | grep jacobi >> $out
 done

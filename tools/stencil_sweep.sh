@@ -3,7 +3,7 @@
 cd /root/repo
 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_pipeline.py -x -q -m gpu 2>&1 | tail -2
 out=gpurun_out/stencil_sweep.txt; : > $out
-for c in 4:2 4:1 3:2; do
+for c in 4:2 4:1; do
   echo "== BAMG_STENCIL_CFG=$c" >> $out
   BAMG_STENCIL_CFG=$c python tools/csr_bench.py --configs cfg4 --ks 16 --reps 6 2>&1 | grep -v copy >> $out
 done
